@@ -678,6 +678,75 @@ int lor_apply_noise(int32_t n, const double* pos, const int32_t* Z, double sigma
 }
 
 /* ---------------------------------------------------------- train step --- */
+/* One simulated worker of the step body (S/trainer.cpp:262-292): denoise,
+ * normalize, forward, per-worker masked_loss_grad and backward accumulated
+ * into g; returns the worker's loss in *loss_out. */
+static int worker_body(const Params* pp, Params* gg, int gi, int B, int D, const int64_t* atom_ptr,
+                       const double* pos, const int32_t* Z, const int32_t* dsidx, const uint8_t* emask,
+                       const uint8_t* fmask, const double* energy, const double* forces,
+                       const uint8_t* denoise_flag, int ntab, const double* rho, const uint8_t* rho_has,
+                       const double* mean, const double* stdv, const double* fstd, const uint8_t* has,
+                       double noise_sigma, int noise_scheme, uint64_t seed, int64_t step, double lambda_e,
+                       double lambda_f, double* loss_out) {
+    const Params p = *pp;
+    const uint64_t kNoiseTag = 0x4e4f4953;
+    int st = 0;
+    *loss_out = 0.0;
+    const int64_t base = atom_ptr[(int64_t)gi * B];
+    const int64_t natoms = atom_ptr[(int64_t)(gi + 1) * B] - base;
+    int64_t* lptr = malloc(sizeof(int64_t) * (B + 1));
+    for (int b = 0; b <= B; ++b) lptr[b] = atom_ptr[(int64_t)gi * B + b] - base;
+    double* xs = malloc(sizeof(double) * 3 * natoms);
+    double* le = malloc(sizeof(double) * B);
+    double* lf = malloc(sizeof(double) * 3 * natoms);
+    int32_t* ld = malloc(sizeof(int32_t) * B);
+    uint8_t* lem = malloc(B);
+    uint8_t* lfm = malloc(B);
+    double* pe = malloc(sizeof(double) * B * D);
+    double* pf = malloc(sizeof(double) * 3 * D * natoms);
+    double* ge = malloc(sizeof(double) * B * D);
+    double* gf = malloc(sizeof(double) * 3 * D * natoms);
+    Cache* caches = calloc((size_t)B, sizeof(Cache));
+    for (int b = 0; b < B && !st; ++b) {
+        const int pos_ = gi * B + b;
+        const int64_t o = atom_ptr[pos_], lo = lptr[b];
+        const int32_t n = (int32_t)(atom_ptr[pos_ + 1] - o);
+        ld[b] = dsidx[pos_];
+        if (denoise_flag && denoise_flag[pos_]) { /* make_denoising_sample S/denoise.cpp:42-53 */
+            const uint64_t ns = lor_mix_seed(lor_mix_seed(seed, kNoiseTag + (uint64_t)step), (uint64_t)pos_);
+            double* lab = malloc(sizeof(double) * 3 * n);
+            st = lor_apply_noise(n, pos + 3 * o, Z + o, noise_sigma, noise_scheme, ns, xs + 3 * lo, lab);
+            lem[b] = 0, lfm[b] = 1;
+            if (!st)
+                st = normalize_one(n, Z + o, ld[b], 0, 1, 0.0, lab, ntab, rho, rho_has, mean, stdv, fstd, has,
+                                   le + b, lf + 3 * lo);
+            free(lab);
+        } else {
+            memcpy(xs + 3 * lo, pos + 3 * o, sizeof(double) * 3 * n);
+            lem[b] = emask[pos_], lfm[b] = fmask[pos_];
+            st = normalize_one(n, Z + o, ld[b], lem[b], lfm[b], energy[pos_], forces + 3 * o, ntab, rho, rho_has,
+                               mean, stdv, fstd, has, le + b, lf + 3 * lo);
+        }
+        if (!st) st = run_encoder(&p, n, xs + 3 * lo, Z + o, &caches[b]);
+        if (!st) heads_forward(&p, &caches[b], pe + (int64_t)b * D, pf + 3 * D * lo);
+    }
+    double bd[7];
+    if (!st)
+        st = lor_loss_grad(B, lptr, D, ld, lem, lfm, le, lf, pe, pf, lambda_e, lambda_f, bd, ge, gf);
+    if (!st) {
+        *loss_out = bd[0];
+        for (int b = 0; b < B; ++b)
+            backward_one(&p, &caches[b], ge + (int64_t)b * D, gf + 3 * D * lptr[b], gg);
+    }
+    for (int b = 0; b < B; ++b)
+        if (caches[b].h) cache_free(&caches[b]);
+    free(caches);
+    free(lptr), free(xs), free(le), free(lf), free(ld), free(lem), free(lfm);
+    free(pe), free(pf), free(ge), free(gf);
+    return st;
+}
+
+
 int lor_train_step(int H, int L, int K, double rc, int D, int G, int B, const int64_t* atom_ptr, const double* pos,
                    const int32_t* Z, const int32_t* dsidx, const uint8_t* emask, const uint8_t* fmask,
                    const double* energy, const double* forces, const uint8_t* denoise_flag, int ntab,
@@ -692,61 +761,14 @@ int lor_train_step(int H, int L, int K, double rc, int D, int G, int B, const in
     Params p, g;
     params_view(&p, H, L, K, rc, D, params);
     params_view(&g, H, L, K, rc, D, grads);
-    const uint64_t kNoiseTag = 0x4e4f4953;
     double loss_sum = 0.0;
     int st = 0;
     for (int gi = 0; gi < G && !st; ++gi) {
-        const int64_t base = atom_ptr[(int64_t)gi * B];
-        const int64_t natoms = atom_ptr[(int64_t)(gi + 1) * B] - base;
-        int64_t* lptr = malloc(sizeof(int64_t) * (B + 1));
-        for (int b = 0; b <= B; ++b) lptr[b] = atom_ptr[(int64_t)gi * B + b] - base;
-        double* xs = malloc(sizeof(double) * 3 * natoms);
-        double* le = malloc(sizeof(double) * B);
-        double* lf = malloc(sizeof(double) * 3 * natoms);
-        int32_t* ld = malloc(sizeof(int32_t) * B);
-        uint8_t* lem = malloc(B);
-        uint8_t* lfm = malloc(B);
-        double* pe = malloc(sizeof(double) * B * D);
-        double* pf = malloc(sizeof(double) * 3 * D * natoms);
-        double* ge = malloc(sizeof(double) * B * D);
-        double* gf = malloc(sizeof(double) * 3 * D * natoms);
-        Cache* caches = calloc((size_t)B, sizeof(Cache));
-        for (int b = 0; b < B && !st; ++b) {
-            const int pos_ = gi * B + b;
-            const int64_t o = atom_ptr[pos_], lo = lptr[b];
-            const int32_t n = (int32_t)(atom_ptr[pos_ + 1] - o);
-            ld[b] = dsidx[pos_];
-            if (denoise_flag && denoise_flag[pos_]) { /* make_denoising_sample S/denoise.cpp:42-53 */
-                const uint64_t ns = lor_mix_seed(lor_mix_seed(seed, kNoiseTag + (uint64_t)step), (uint64_t)pos_);
-                double* lab = malloc(sizeof(double) * 3 * n);
-                st = lor_apply_noise(n, pos + 3 * o, Z + o, noise_sigma, noise_scheme, ns, xs + 3 * lo, lab);
-                lem[b] = 0, lfm[b] = 1;
-                if (!st)
-                    st = normalize_one(n, Z + o, ld[b], 0, 1, 0.0, lab, ntab, rho, rho_has, mean, stdv, fstd, has,
-                                       le + b, lf + 3 * lo);
-                free(lab);
-            } else {
-                memcpy(xs + 3 * lo, pos + 3 * o, sizeof(double) * 3 * n);
-                lem[b] = emask[pos_], lfm[b] = fmask[pos_];
-                st = normalize_one(n, Z + o, ld[b], lem[b], lfm[b], energy[pos_], forces + 3 * o, ntab, rho, rho_has,
-                                   mean, stdv, fstd, has, le + b, lf + 3 * lo);
-            }
-            if (!st) st = run_encoder(&p, n, xs + 3 * lo, Z + o, &caches[b]);
-            if (!st) heads_forward(&p, &caches[b], pe + (int64_t)b * D, pf + 3 * D * lo);
-        }
-        double bd[7];
-        if (!st)
-            st = lor_loss_grad(B, lptr, D, ld, lem, lfm, le, lf, pe, pf, lambda_e, lambda_f, bd, ge, gf);
-        if (!st) {
-            loss_sum += bd[0];
-            for (int b = 0; b < B; ++b)
-                backward_one(&p, &caches[b], ge + (int64_t)b * D, gf + 3 * D * lptr[b], &g);
-        }
-        for (int b = 0; b < B; ++b)
-            if (caches[b].h) cache_free(&caches[b]);
-        free(caches);
-        free(lptr), free(xs), free(le), free(lf), free(ld), free(lem), free(lfm);
-        free(pe), free(pf), free(ge), free(gf);
+        double wl = 0.0;
+        st = worker_body(&p, &g, gi, B, D, atom_ptr, pos, Z, dsidx, emask, fmask, energy, forces, denoise_flag, ntab,
+                         rho, rho_has, mean, stdv, fstd, has, noise_sigma, noise_scheme, seed, step, lambda_e,
+                         lambda_f, &wl);
+        loss_sum += wl;
     }
     if (!st) {
         const double sG = 1.0 / (double)G; /* scale_params S/model.cpp:134-138 */
@@ -1159,4 +1181,28 @@ int lor_synth_fill(int task, int64_t count, double mode, double sigma, int min_a
         }
     }
     return 0;
+}
+
+/* Worker g's contribution alone (its loss and gradient SUM before the /G), for
+ * checking a data-parallel decomposition: sum over g of these == the step body. */
+int lor_worker_step(int H, int L, int K, double rc, int D, int G, int B, int g, const int64_t* atom_ptr,
+                    const double* pos, const int32_t* Z, const int32_t* dsidx, const uint8_t* emask,
+                    const uint8_t* fmask, const double* energy, const double* forces, const uint8_t* denoise_flag,
+                    int ntab, const double* rho, const uint8_t* rho_has, const double* mean, const double* stdv,
+                    const double* fstd, const uint8_t* has, double noise_sigma, int noise_scheme, uint64_t seed,
+                    int64_t step, double lambda_e, double lambda_f, const double* params, double* out_loss,
+                    double* out_grads) {
+    if (validate_config(H, L, K, rc, D)) return 1;
+    if (g < 0 || g >= G) return set_err("worker_step: bad worker"), 1;
+    const int64_t NP = lor_param_count(H, L, K, D);
+    memset(out_grads, 0, sizeof(double) * NP);
+    Params p, gg;
+    params_view(&p, H, L, K, rc, D, (double*)params);
+    params_view(&gg, H, L, K, rc, D, out_grads);
+    const int st = worker_body(&p, &gg, g, B, D, atom_ptr, pos, Z, dsidx, emask, fmask, energy, forces, denoise_flag,
+                               ntab, rho, rho_has, mean, stdv, fstd, has, noise_sigma, noise_scheme, seed, step,
+                               lambda_e, lambda_f, out_loss);
+    params_free(&p);
+    params_free(&gg);
+    return st;
 }

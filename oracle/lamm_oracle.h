@@ -59,6 +59,14 @@ int lor_train_step(int H, int L, int K, double rc, int D, int G, int B, const in
                    int64_t step, double lambda_e, double lambda_f, double lr, double clip, double decay, double eps,
                    double* params, double* rms_v, double* out_loss, double* out_grad_norm, double* out_grads);
 
+int lor_worker_step(int H, int L, int K, double rc, int D, int G, int B, int g, const int64_t* atom_ptr,
+                    const double* pos, const int32_t* Z, const int32_t* dsidx, const uint8_t* emask,
+                    const uint8_t* fmask, const double* energy, const double* forces, const uint8_t* denoise_flag,
+                    int ntab, const double* rho, const uint8_t* rho_has, const double* mean, const double* stdv,
+                    const double* fstd, const uint8_t* has, double noise_sigma, int noise_scheme, uint64_t seed,
+                    int64_t step, double lambda_e, double lambda_f, const double* params, double* out_loss,
+                    double* out_grads);
+
 int lor_greedy_assign(const int64_t* atoms, int64_t n, int G, int B, int32_t* out);
 /* Returns the number of mini-batches (or < 0 on error). All outputs have
  * capacity n (scheduled samples never exceed n). */

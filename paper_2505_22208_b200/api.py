@@ -1,0 +1,445 @@
+"""Host-side mirror of the reference's C++ API for the train-step path.
+
+Thin numpy wrappers over the C ABI (include/lamm_b200.h); every computation
+runs in liblamm_b200.so — host C++ for the scheduler/generators, sm_100a CUDA
+kernels for the model, loss and optimizer. Names and argument meaning follow
+the reference (H = /root/reference/proj/core/include/lamm):
+
+* ``init_params``                       H/model.hpp:72
+* ``Device.build_neighbor_list``        H/core.hpp:83
+* ``Device.forward`` / ``backward``     H/model.hpp:123-129
+* ``Device.masked_loss_grad``           H/loss.hpp:81-84
+* ``Device.train_step``                 S/trainer.cpp:258-327 (no public reference entry)
+* ``greedy_assign`` / ``plan`` / ``schedule_metrics``   H/scheduler.hpp:66-91
+* ``make_trace``                        H/trace.hpp:39
+* ``temperature_counts`` / ``build_epoch_index`` / ``synth_generate``  H/dataset.hpp:56-138
+
+Batches are dicts of numpy arrays (packed CSR over atoms)::
+
+    atom_ptr int64[B+1], pos f64[N,3], Z int32[N], dataset_index int32[B],
+    energy_mask u8[B], force_mask u8[B], energy f64[B], forces f64[N,3], denoise u8[B]
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import (BatchViewC, InputError, LossBreakdownC, LossConfigC, ModelConfigC, NonFiniteError,  # noqa: F401
+                   RefTableC, StepResultC, TrainConfigC, check, lib)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _c(a, dt):
+    return np.ascontiguousarray(a, dtype=dt)
+
+
+@dataclass(frozen=True)
+class ModelConfig:
+    """lamm::model::ModelConfig (H/model.hpp:34-40)."""
+    hidden: int = 64
+    layers: int = 2
+    rbf: int = 16
+    cutoff: float = 5.0
+    heads: int = 1
+
+    def c(self) -> ModelConfigC:
+        return ModelConfigC(self.hidden, self.layers, self.rbf, self.heads, self.cutoff)
+
+    def astuple(self):
+        return (self.hidden, self.layers, self.rbf, self.cutoff, self.heads)
+
+
+@dataclass
+class LossConfig:
+    """lamm::loss::LossConfig (H/loss.hpp:26-29)."""
+    lambda_energy: float = 1.0
+    lambda_force: float = 1.0
+
+
+@dataclass
+class TrainConfig:
+    """Step-body fields of lamm::trainer::TrainConfig (H/trainer.hpp:33-50)."""
+    learning_rate: float = 1e-3
+    clip_norm: float = 10.0
+    rms_decay: float = 0.99
+    rms_epsilon: float = 1e-8
+    noise_sigma: float = 0.3
+    noise_scheme: str = "centered"
+    seed: int = 0
+    lambda_energy: float = 1.0
+    lambda_force: float = 1.0
+
+    def c(self) -> TrainConfigC:
+        return TrainConfigC(self.learning_rate, self.clip_norm, self.rms_decay, self.rms_epsilon, self.noise_sigma,
+                            1 if self.noise_scheme == "centered" else 0, self.seed, self.lambda_energy,
+                            self.lambda_force)
+
+
+def param_count(cfg: ModelConfig) -> int:
+    mc = cfg.c()
+    return int(lib().lamm_param_count(C.byref(mc)))
+
+
+def init_params(cfg: ModelConfig, seed: int) -> np.ndarray:
+    """lamm::model::init_params — bit-exact with the reference."""
+    out = np.empty(param_count(cfg), np.float64)
+    mc = cfg.c()
+    check(lib().lamm_init_params(C.byref(mc), C.c_uint64(seed), _p(out)))
+    return out
+
+
+def _batch_view(b: dict):
+    keep = {
+        "atom_ptr": _c(b["atom_ptr"], np.int64), "pos": _c(b["pos"], np.float64), "Z": _c(b["Z"], np.int32),
+        "dataset_index": _c(b.get("dataset_index", np.zeros(len(b["atom_ptr"]) - 1)), np.int32),
+        "energy_mask": _c(b.get("energy_mask", np.zeros(len(b["atom_ptr"]) - 1)), np.uint8),
+        "force_mask": _c(b.get("force_mask", np.zeros(len(b["atom_ptr"]) - 1)), np.uint8),
+        "energy": _c(b.get("energy", np.zeros(len(b["atom_ptr"]) - 1)), np.float64),
+        "forces": _c(b.get("forces", np.zeros((len(b["Z"]), 3))), np.float64),
+        "denoise": _c(b.get("denoise", np.zeros(len(b["atom_ptr"]) - 1)), np.uint8),
+    }
+    B = len(keep["atom_ptr"]) - 1
+    v = BatchViewC(B, int(keep["atom_ptr"][-1]), _p(keep["atom_ptr"]), _p(keep["pos"]), _p(keep["Z"]),
+                   _p(keep["dataset_index"]), _p(keep["energy_mask"]), _p(keep["force_mask"]), _p(keep["energy"]),
+                   _p(keep["forces"]), _p(keep["denoise"]))
+    return v, keep
+
+
+def _table_view(t: dict):
+    keep = {k: _c(t[k], dt) for k, dt in (("rho", np.float64), ("rho_has", np.uint8), ("mean", np.float64),
+                                          ("std", np.float64), ("fstd", np.float64), ("has", np.uint8))}
+    v = RefTableC(len(keep["mean"]), _p(keep["rho"]), _p(keep["rho_has"]), _p(keep["mean"]), _p(keep["std"]),
+                  _p(keep["fstd"]), _p(keep["has"]))
+    return v, keep
+
+
+def empty_table(n: int) -> dict:
+    """A ReferenceTable with no reference energies, zero mean and unit scales."""
+    return dict(rho=np.zeros((n, 119)), rho_has=np.zeros((n, 119), np.uint8), mean=np.zeros(n), std=np.ones(n),
+                fstd=np.ones(n), has=np.ones(n, np.uint8))
+
+
+@dataclass
+class StepResult:
+    loss: float
+    grad_norm: float
+    local: dict
+    n_atoms: int
+    n_edges: int
+    status: int
+
+
+def _breakdown(b: LossBreakdownC) -> dict:
+    return dict(total=b.total, energy_term=b.energy_term, force_term=b.force_term, energy_labeled=b.energy_labeled,
+                force_labeled=b.force_labeled, energy_empty=bool(b.energy_empty), force_empty=bool(b.force_empty))
+
+
+class Device:
+    """One lamm_ctx: a model replica on one GPU (one CUDA stream)."""
+
+    def __init__(self, cfg: ModelConfig, device: int = 0, params: np.ndarray | None = None, seed: int = 0):
+        self.cfg = cfg
+        self._h = C.c_void_p()
+        mc = cfg.c()
+        check(lib().lamm_ctx_create(device, C.byref(mc), C.byref(self._h)))
+        self.n_params = param_count(cfg)
+        self.set_params(init_params(cfg, seed) if params is None else params)
+        self._batch = None
+        self._keep = None
+
+    def close(self):
+        if self._h:
+            lib().lamm_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_option(self, name: str, value: int):
+        check(lib().lamm_ctx_set_option(self._h, name.encode(), C.c_int64(int(value))))
+
+    # ---------------------------------------------------------- parameters
+    def set_params(self, flat):
+        flat = _c(flat, np.float64)
+        check(lib().lamm_params_set(self._h, _p(flat), C.c_size_t(len(flat))))
+
+    def params(self) -> np.ndarray:
+        out = np.empty(self.n_params)
+        check(lib().lamm_params_get(self._h, _p(out), C.c_size_t(self.n_params)))
+        return out
+
+    def set_rms_state(self, flat):
+        flat = _c(flat, np.float64)
+        check(lib().lamm_rms_state_set(self._h, _p(flat), C.c_size_t(len(flat))))
+
+    def rms_state(self) -> np.ndarray:
+        out = np.empty(self.n_params)
+        check(lib().lamm_rms_state_get(self._h, _p(out), C.c_size_t(self.n_params)))
+        return out
+
+    # --------------------------------------------------------------- batch
+    def set_reference_table(self, table: dict | None):
+        if table is None:
+            check(lib().lamm_ref_table_set(self._h, None))
+            return
+        v, self._tkeep = _table_view(table)
+        check(lib().lamm_ref_table_set(self._h, C.byref(v)))
+
+    def set_batch(self, batch: dict):
+        v, keep = _batch_view(batch)
+        check(lib().lamm_batch_set(self._h, C.byref(v)))
+        self._batch, self._keep = batch, keep
+        self.B = len(keep["atom_ptr"]) - 1
+        self.N = int(keep["atom_ptr"][-1])
+
+    def labels(self):
+        e, f = np.empty(self.B), np.empty((self.N, 3))
+        check(lib().lamm_labels_get(self._h, _p(e), _p(f)))
+        return e, f
+
+    def build_neighbor_list(self, fp64: bool = True):
+        """Per-sample pair lists: (sample_pair_ptr, i, j, dist, unit); i/j local."""
+        P = C.c_int64()
+        check(lib().lamm_neighbor_list(self._h, C.byref(P)))
+        P = P.value
+        ptr = np.empty(self.B + 1, np.int64)
+        oi, oj = np.empty(P, np.int32), np.empty(P, np.int32)
+        dist = np.empty(P) if fp64 else None
+        unit = np.empty((P, 3)) if fp64 else None
+        check(lib().lamm_neighbor_list_copy(self._h, _p(ptr), _p(oi), _p(oj), _p(dist), _p(unit)))
+        return ptr, oi, oj, dist, unit
+
+    # ---------------------------------------------------------------- model
+    def forward(self):
+        """Energies [B, D] and forces (reference Prediction layout, flat)."""
+        e = np.empty((self.B, self.cfg.heads))
+        f = np.empty(3 * self.cfg.heads * self.N)
+        check(lib().lamm_forward(self._h, _p(e), _p(f)))
+        return e, f
+
+    def forward_cache(self, which: str, layer: int) -> np.ndarray:
+        out = np.empty((self.N, self.cfg.hidden))
+        check(lib().lamm_forward_cache_get(self._h, 0 if which == "h" else 1, layer, _p(out)))
+        return out
+
+    def masked_loss_grad(self, lcfg: LossConfig | None = None):
+        lcfg = lcfg or LossConfig()
+        bd = LossBreakdownC()
+        ge = np.empty((self.B, self.cfg.heads))
+        gf = np.empty(3 * self.cfg.heads * self.N)
+        lc = LossConfigC(lcfg.lambda_energy, lcfg.lambda_force)
+        check(lib().lamm_loss_grad(self._h, C.byref(lc), C.byref(bd), _p(ge), _p(gf)))
+        return _breakdown(bd), ge, gf
+
+    def backward(self, up_energy=None, up_forces=None, grads=None) -> np.ndarray:
+        """Accumulates the batch parameter gradient into ``grads`` (fp64)."""
+        g = np.zeros(self.n_params) if grads is None else grads
+        ue = None if up_energy is None else _c(up_energy, np.float64)
+        uf = None if up_forces is None else _c(up_forces, np.float64)
+        if (ue is None) != (uf is None):
+            ue = np.zeros((self.B, self.cfg.heads)) if ue is None else ue
+            uf = np.zeros(3 * self.cfg.heads * self.N) if uf is None else uf
+        check(lib().lamm_backward(self._h, _p(ue), _p(uf), _p(g)))
+        return g
+
+    def grads(self) -> np.ndarray:
+        out = np.empty(self.n_params)
+        check(lib().lamm_grads_get(self._h, _p(out), C.c_size_t(self.n_params)))
+        return out
+
+    # ----------------------------------------------------------- training
+    def comm_init(self, nranks: int, rank: int, unique_id: bytes):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        check(lib().lamm_comm_init(self._h, nranks, rank, buf))
+
+    def train_step(self, batch: dict, tcfg: TrainConfig, step: int, workers: int = 1, rank: int = 0) -> StepResult:
+        v, keep = _batch_view(batch)
+        res = StepResultC()
+        tc = tcfg.c()
+        st = lib().lamm_train_step(self._h, C.byref(v), C.byref(tc), C.c_int64(step), workers, rank, C.byref(res))
+        self._keep = keep
+        self.B = len(keep["atom_ptr"]) - 1
+        self.N = int(keep["atom_ptr"][-1])
+        check(st)
+        return StepResult(res.loss, res.grad_norm, _breakdown(res.local), res.n_atoms, res.n_edges, res.status)
+
+    def optimizer_step(self, grad_sum, workers: int, tcfg: TrainConfig) -> float:
+        g = _c(grad_sum, np.float64)
+        gn = C.c_double()
+        tc = tcfg.c()
+        check(lib().lamm_optimizer_step(self._h, _p(g), workers, C.byref(tc), C.byref(gn)))
+        return gn.value
+
+    # --------------------------------------------------------------- timing
+    def sync(self):
+        check(lib().lamm_sync(self._h))
+
+    def event_record(self, slot: int):
+        check(lib().lamm_event_record(self._h, slot))
+
+    def event_elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_float()
+        check(lib().lamm_event_elapsed_ms(self._h, a, b, C.byref(ms)))
+        return ms.value
+
+    def kernel_times(self) -> dict:
+        n = C.c_int()
+        check(lib().lamm_kernel_times(self._h, 0, None, None, None, C.byref(n)))
+        k = n.value
+        names = (C.c_char_p * max(k, 1))()
+        ms = np.zeros(max(k, 1))
+        cnt = np.zeros(max(k, 1), np.int64)
+        check(lib().lamm_kernel_times(self._h, k, names, _p(ms), _p(cnt), C.byref(n)))
+        return {names[i].decode(): (float(ms[i]), int(cnt[i])) for i in range(k)}
+
+    def kernel_times_reset(self):
+        check(lib().lamm_kernel_times_reset(self._h))
+
+    def last_step_launches(self) -> int:
+        return int(lib().lamm_last_step_launches(self._h))
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().lamm_comm_unique_id(buf))
+    return buf.raw
+
+
+# ------------------------------------------------------------ host: schedule
+MODES = {"balanced": 0, "greedy_only": 1, "naive": 2}
+
+
+def greedy_assign(atoms, workers: int, batch_per_worker: int) -> np.ndarray:
+    a = _c(atoms, np.int64)
+    out = np.empty(len(a), np.int32)
+    check(lib().lamm_greedy_assign(_p(a), C.c_int64(len(a)), workers, batch_per_worker, _p(out)))
+    return out
+
+
+def plan(atoms, workers: int, batch_per_worker: int, num_splits: int = 100, seed: int = 0,
+         mode: str = "balanced") -> dict:
+    """lamm::scheduler::plan + schedule_metrics, as flat ScheduledSample arrays."""
+    a = _c(atoms, np.int64)
+    n = len(a)
+    cap = max(n, 1)
+    out = dict(sample=np.empty(cap, np.int64), worker=np.empty(cap, np.int32), atoms=np.empty(cap, np.int64),
+               split=np.empty(cap, np.int64), chunk_rank=np.empty(cap, np.int64),
+               worker_atoms=np.empty(cap, np.int64))
+    nb, dr = C.c_int64(), C.c_int64()
+    check(lib().lamm_plan(_p(a), C.c_int64(n), workers, batch_per_worker, num_splits, C.c_uint64(seed), MODES[mode],
+                          _p(out["sample"]), _p(out["worker"]), _p(out["atoms"]), _p(out["split"]),
+                          _p(out["chunk_rank"]), _p(out["worker_atoms"]), C.byref(nb), C.byref(dr)))
+    nb, dr = nb.value, dr.value
+    tot = nb * workers * batch_per_worker
+    for k in ("sample", "worker", "atoms", "split", "chunk_rank"):
+        out[k] = out[k][:tot]
+    out["worker_atoms"] = out["worker_atoms"][:nb * workers]
+    mx, mean, mono, grow = C.c_double(), C.c_double(), C.c_int64(), C.c_int64()
+    check(lib().lamm_schedule_metrics(C.c_int64(nb), workers, batch_per_worker, _p(out["worker"]), _p(out["atoms"]),
+                                      _p(out["split"]), _p(out["chunk_rank"]), C.byref(mx), C.byref(mean),
+                                      C.byref(mono), C.byref(grow)))
+    out.update(n_batches=nb, dropped=dr, max_imbalance=mx.value, mean_imbalance=mean.value,
+               monotonicity_violations=mono.value, growth_events=grow.value)
+    return out
+
+
+TRACE_KINDS = {"constant": 0, "uniform": 1, "lognormal": 2, "bimodal": 3}
+
+
+def make_trace(kind="lognormal", count=1000, min_atoms=1, max_atoms=300, constant_atoms=15.0, mode=15.0, sigma=0.45,
+               mode_a=15.0, sigma_a=0.30, mode_b=160.0, sigma_b=0.30, weight_a=0.5, seed=0) -> np.ndarray:
+    out = np.empty(count, np.int64)
+    D = C.c_double
+    check(lib().lamm_make_trace(TRACE_KINDS[kind], C.c_int64(count), C.c_int64(min_atoms), C.c_int64(max_atoms),
+                                D(constant_atoms), D(mode), D(sigma), D(mode_a), D(sigma_a), D(mode_b), D(sigma_b),
+                                D(weight_a), C.c_uint64(seed), _p(out)))
+    return out
+
+
+def temperature_counts(sizes, temperature: float) -> np.ndarray:
+    s = _c(sizes, np.float64)
+    out = np.empty(len(s))
+    check(lib().lamm_temperature_counts(_p(s), len(s), C.c_double(temperature), _p(out)))
+    return out
+
+
+def build_epoch_index(repeats, sizes, seed: int):
+    r, s = _c(repeats, np.float64), _c(sizes, np.int64)
+    cap = int(sum(int(np.rint(x)) for x in r)) + 8
+    osub, osam = np.empty(cap, np.int32), np.empty(cap, np.int64)
+    cnt = C.c_int64()
+    check(lib().lamm_build_epoch_index(_p(r), _p(s), len(s), C.c_uint64(seed), C.c_int64(cap), _p(osub), _p(osam),
+                                       C.byref(cnt)))
+    return osub[:cnt.value], osam[:cnt.value]
+
+
+TASKS = {"energy_and_forces": 0, "energy_only": 1, "denoising": 2}
+
+
+def synth_generate(count: int, seed: int, *, task="energy_and_forces", mode=15.0, sigma=0.45, min_atoms=2,
+                   max_atoms=300, elements=(6,), relax_steps=6, relax_step=0.02, energy_scale=1.0, offsets=None,
+                   threads: int = 8, dataset_index: int = 0) -> dict:
+    """lamm::dataset::synth_generate (Morse clusters) as a packed batch dict."""
+    el = _c(list(elements), np.int32)
+    offsets = offsets or {}
+    oz = _c(list(offsets.keys()) or [0], np.int32)
+    ov = _c(list(offsets.values()) or [0.0], np.float64)
+    ap = np.empty(count + 1, np.int64)
+    D = C.c_double
+    check(lib().lamm_synth_counts(C.c_int64(count), D(mode), D(sigma), min_atoms, max_atoms, C.c_uint64(seed),
+                                  _p(ap)))
+    N = int(ap[-1])
+    b = dict(atom_ptr=ap, pos=np.empty((N, 3)), Z=np.empty(N, np.int32), energy_mask=np.empty(count, np.uint8),
+             force_mask=np.empty(count, np.uint8), energy=np.empty(count), forces=np.empty((N, 3)))
+    check(lib().lamm_synth_fill(TASKS[task], C.c_int64(count), D(mode), D(sigma), min_atoms, max_atoms, _p(el),
+                                len(el), relax_steps, D(relax_step), D(energy_scale), _p(oz), _p(ov), len(offsets),
+                                C.c_uint64(seed), threads, _p(ap), _p(b["pos"]), _p(b["Z"]), _p(b["energy_mask"]),
+                                _p(b["force_mask"]), _p(b["energy"]), _p(b["forces"])))
+    b["dataset_index"] = np.full(count, dataset_index, np.int32)
+    b["denoise"] = np.full(count, 1 if task == "denoising" else 0, np.uint8)
+    return b
+
+
+def mix_seed(a: int, b: int) -> int:
+    return int(lib().lamm_mix_seed(a, b))
+
+
+def rng_normals(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n)
+    check(lib().lamm_rng_normals(C.c_uint64(seed), C.c_int64(n), _p(out)))
+    return out
+
+
+def select(batch: dict, ids) -> dict:
+    """Packs the samples ``ids`` (in order) of a batch dict into a new batch."""
+    ap = batch["atom_ptr"]
+    ids = np.asarray(ids, np.int64)
+    sizes = ap[ids + 1] - ap[ids]
+    nap = np.zeros(len(ids) + 1, np.int64)
+    np.cumsum(sizes, out=nap[1:])
+    rows = np.concatenate([np.arange(ap[i], ap[i + 1]) for i in ids]) if len(ids) else np.zeros(0, np.int64)
+    out = dict(atom_ptr=nap)
+    for k in ("pos", "Z", "forces"):
+        out[k] = np.ascontiguousarray(batch[k][rows])
+    for k in ("dataset_index", "energy_mask", "force_mask", "energy", "denoise"):
+        out[k] = np.ascontiguousarray(batch[k][ids])
+    return out
+
+
+def concat(batches) -> dict:
+    """Concatenates packed batch dicts sample-wise."""
+    batches = list(batches)
+    out = {}
+    for k in ("pos", "Z", "forces", "dataset_index", "energy_mask", "force_mask", "energy", "denoise"):
+        out[k] = np.concatenate([b[k] for b in batches])
+    sizes = np.concatenate([np.diff(b["atom_ptr"]) for b in batches])
+    out["atom_ptr"] = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    return out

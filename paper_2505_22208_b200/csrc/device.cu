@@ -1,0 +1,1209 @@
+// device.cu - host orchestration of the sm_100a LaMM step: lamm_ctx, device
+// buffers, batch staging, the captured CUDA graph of the step, NCCL, and the
+// device half of the C ABI declared in include/lamm_b200.h.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.cuh"
+#include "rng.hpp"
+
+namespace lamm_b200 {
+
+#define CK(x)                                                                                        \
+    do {                                                                                             \
+        const cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess) throw CudaErr(std::string(#x) + ": " + cudaGetErrorString(e_));       \
+    } while (0)
+
+// ---------------------------------------------------------------- NCCL ----
+// Loaded at first use so the library has no link-time NCCL dependency and
+// binds whichever libnccl.so.2 the process already has (torch's or the system's).
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        a.ok = a.get_unique_id && a.comm_init_rank && a.all_reduce && a.comm_destroy && a.error_string;
+        return a;
+    }();
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw NcclErr(std::string(what) + ": " + nccl().error_string(r));
+}
+
+// ------------------------------------------------------------- buffers ----
+struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct KernelSlot {
+    std::string name;
+    cudaEvent_t a = nullptr, b = nullptr;
+};
+
+struct Ops;
+
+}  // namespace lamm_b200
+
+struct lamm_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    lamm_model_config cfg{};
+    int H = 0, L = 0, K = 0, D = 0;
+    int64_t NP = 0;
+    int nsm = 148;
+    const lamm_b200::Ops* ops = nullptr;
+    // persistent parameter state
+    lamm_b200::Buf p64, v64, g64, p32, tanh_emb, grads, block_scratch;
+    // staging (pinned host -> device blob, header first)
+    char* h_stage = nullptr;
+    size_t h_stage_cap = 0;
+    lamm_b200::Buf d_stage;
+    lamm_b200::StepHeader* h_result = nullptr;  // pinned copy of the header after a step
+    // capacities
+    int64_t Ncap = 0, Bcap = 0, Pcap = 0;
+    std::map<std::string, lamm_b200::Buf> bufs;
+    // reference table
+    bool use_table = false;
+    int ntab = 0;
+    std::vector<uint8_t> h_thas;
+    // host mirror of the current batch
+    int32_t B = 0;
+    int64_t N = 0;
+    std::vector<int64_t> h_atom_ptr;
+    std::vector<int32_t> h_Z, h_dsidx;
+    std::vector<uint8_t> h_emask, h_fmask;
+    int me = 0, mf = 0;
+    bool batch_valid = false, nlist_valid = false, fwd_valid = false, loss_valid = false;
+    // launch geometry
+    int grid_warp = 0, grid_gemm = 0, grid_upd = 0, grid_small = 0, grid_opt = 0, ncta_red = 0, grid_reduce = 0;
+    // graphs
+    cudaGraphExec_t g_step = nullptr, g_opt = nullptr;
+    bool graph_dirty = true;
+    bool use_graph = true, profile = false, export64 = false;
+    int denoise_scheme = 1;
+    double opt_inv_g = 1.0, opt_lr = 0, opt_decay = 0, opt_eps = 0, opt_clip = 0;
+    int opt_G = 1;
+    // NCCL
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    // timing
+    cudaEvent_t ev[64] = {};
+    std::vector<lamm_b200::KernelSlot> slots;
+    size_t slot_cursor = 0;
+    std::map<std::string, std::pair<double, int64_t>> ktimes;
+    int64_t launches = 0, last_step_launches = 0, graph_launches = 0;
+};
+
+namespace lamm_b200 {
+
+using Ctx = lamm_ctx;
+
+Buf& buf(Ctx& c, const std::string& name) { return c.bufs[name]; }
+
+void ensure_buf(Ctx& c, const std::string& name, size_t bytes, bool& changed) {
+    Buf& b = c.bufs[name];
+    if (b.bytes >= bytes && b.p) return;
+    if (b.p) CK(cudaFree(b.p));
+    b.p = nullptr;
+    CK(cudaMalloc(&b.p, std::max<size_t>(bytes, 256)));
+    b.bytes = std::max<size_t>(bytes, 256);
+    changed = true;
+}
+
+void alloc_param_state(Ctx& c) {
+    auto mk = [&](Buf& b, size_t bytes) {
+        CK(cudaMalloc(&b.p, bytes));
+        CK(cudaMemset(b.p, 0, bytes));
+        b.bytes = bytes;
+    };
+    mk(c.p64, sizeof(double) * c.NP);
+    mk(c.v64, sizeof(double) * c.NP);
+    mk(c.g64, sizeof(double) * c.NP);
+    mk(c.p32, sizeof(float) * c.NP);
+    mk(c.tanh_emb, sizeof(float) * kMaxZ * c.H);
+    mk(c.grads, sizeof(float) * (c.NP + 4));
+    mk(c.block_scratch, sizeof(double) * 4096);
+}
+
+// Grows every batch-sized buffer to hold N atoms, B samples and P pairs.
+void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
+    bool changed = false;
+    if (N > c.Ncap) c.Ncap = std::max<int64_t>(N + N / 4, 1024);
+    if (B > c.Bcap) c.Bcap = std::max<int64_t>(B + B / 4, 64);
+    if (P > c.Pcap) c.Pcap = std::max<int64_t>(P + P / 4, 4096);
+    const int64_t Nc = c.Ncap, Bc = c.Bcap, Pc = c.Pcap;
+    const int H = c.H, K = c.K, D = c.D, L = c.L;
+    ensure_buf(c, "atom_ptr", 8 * (Bc + 1), changed);
+    ensure_buf(c, "Z", 4 * Nc, changed);
+    ensure_buf(c, "zslot", 4 * Nc, changed);
+    ensure_buf(c, "z2s", 4 * 128, changed);
+    ensure_buf(c, "dsidx", 4 * Bc, changed);
+    ensure_buf(c, "emask", Bc, changed);
+    ensure_buf(c, "fmask", Bc, changed);
+    ensure_buf(c, "denoise", Bc, changed);
+    ensure_buf(c, "sample_of", 4 * Nc, changed);
+    for (const char* n : {"x", "y", "z"}) ensure_buf(c, n, 8 * Nc, changed);
+    ensure_buf(c, "En", 8 * Bc, changed);
+    ensure_buf(c, "Fn", 24 * Nc, changed);
+    ensure_buf(c, "cnt", 4 * Nc, changed);
+    ensure_buf(c, "row_ptr", 4 * (Nc + 1), changed);
+    ensure_buf(c, "col", 4 * Pc, changed);
+    ensure_buf(c, "geo", 16 * Pc, changed);
+    ensure_buf(c, "rbf", 4 * static_cast<size_t>(Pc) * K, changed);
+    if (c.export64) {
+        ensure_buf(c, "dist64", 8 * Pc, changed);
+        ensure_buf(c, "unit64", 24 * Pc, changed);
+    }
+    for (int l = 1; l <= L; ++l) {
+        ensure_buf(c, "t" + std::to_string(l), 4 * static_cast<size_t>(Nc) * H, changed);
+        ensure_buf(c, "h" + std::to_string(l), 4 * static_cast<size_t>(Nc) * H, changed);
+    }
+    for (int l = 0; l < L; ++l) ensure_buf(c, "mu" + std::to_string(l), 4 * static_cast<size_t>(Nc) * H, changed);
+    ensure_buf(c, "e_atom", 4 * Nc * D, changed);
+    ensure_buf(c, "A", 4 * Nc * D, changed);
+    ensure_buf(c, "F", 12 * Nc * D, changed);
+    ensure_buf(c, "Epred", 8 * Bc * D, changed);
+    ensure_buf(c, "gE", 4 * Bc * D, changed);
+    ensure_buf(c, "gF", 12 * Nc * D, changed);
+    ensure_buf(c, "sample_terms", 16 * Bc, changed);
+    ensure_buf(c, "gh", 4 * static_cast<size_t>(Nc) * H, changed);
+    ensure_buf(c, "gm", 4 * static_cast<size_t>(Nc) * H, changed);
+    ensure_buf(c, "Q", 4 * static_cast<size_t>(Nc) * (H + K + 4), changed);
+    for (int l = 0; l < L; ++l) {
+        ensure_buf(c, "part_wf" + std::to_string(l), 4 * static_cast<size_t>(c.grid_warp) * H * K, changed);
+        ensure_buf(c, "part_wu" + std::to_string(l), 4 * static_cast<size_t>(c.grid_gemm) * H * H, changed);
+    }
+    ensure_buf(c, "part_head", 4 * static_cast<size_t>(c.ncta_red) * (3 * H + K) * D, changed);
+    ensure_buf(c, "part_emb", 4 * static_cast<size_t>(c.ncta_red) * kMaxZ * H, changed);
+    if (changed) c.graph_dirty = true;
+}
+
+Dev make_dev(Ctx& c) {
+    Dev d{};
+    d.H = c.H, d.L = c.L, d.K = c.K, d.D = c.D;
+    d.rc = c.cfg.cutoff;
+    d.Ncap = c.Ncap, d.Bcap = c.Bcap, d.Pcap = c.Pcap;
+    d.hdr = c.d_stage.as<StepHeader>();
+    d.atom_ptr = buf(c, "atom_ptr").as<int64_t>();
+    d.Z = buf(c, "Z").as<int32_t>();
+    d.zslot = buf(c, "zslot").as<int32_t>();
+    d.z_to_slot = buf(c, "z2s").as<int32_t>();
+    d.dsidx = buf(c, "dsidx").as<int32_t>();
+    d.emask = buf(c, "emask").as<uint8_t>();
+    d.fmask = buf(c, "fmask").as<uint8_t>();
+    d.denoise = buf(c, "denoise").as<uint8_t>();
+    d.sample_of = buf(c, "sample_of").as<int32_t>();
+    d.x = buf(c, "x").as<double>(), d.y = buf(c, "y").as<double>(), d.z = buf(c, "z").as<double>();
+    d.En = buf(c, "En").as<double>();
+    d.Fn = buf(c, "Fn").as<double>();
+    d.use_table = c.use_table ? 1 : 0;
+    d.denoise_scheme = c.denoise_scheme;
+    d.ntab = c.ntab;
+    d.rho = buf(c, "rho").as<double>();
+    d.rho_has = buf(c, "rho_has").as<uint8_t>();
+    d.tmean = buf(c, "tmean").as<double>();
+    d.tstd = buf(c, "tstd").as<double>();
+    d.tfstd = buf(c, "tfstd").as<double>();
+    d.thas = buf(c, "thas").as<uint8_t>();
+    d.cnt = buf(c, "cnt").as<int32_t>();
+    d.row_ptr = buf(c, "row_ptr").as<int32_t>();
+    d.col = buf(c, "col").as<int32_t>();
+    d.geo = buf(c, "geo").as<float4>();
+    d.rbf = buf(c, "rbf").as<float>();
+    d.export64 = c.export64 ? 1 : 0;
+    d.dist64 = c.export64 ? buf(c, "dist64").as<double>() : nullptr;
+    d.unit64 = c.export64 ? buf(c, "unit64").as<double>() : nullptr;
+    float* p = c.p32.as<float>();
+    const int H = c.H, K = c.K, D = c.D, L = c.L;
+    d.emb = p;
+    p += kMaxZ * H;
+    for (int l = 0; l < L; ++l) d.wf[l] = p, p += H * K;
+    for (int l = 0; l < L; ++l) d.wu[l] = p, p += H * H;
+    d.we = p, p += H * D;
+    d.wfh = p;
+    d.tanh_emb = c.tanh_emb.as<float>();
+    d.tanh_emb_w = c.tanh_emb.as<float>();
+    for (int l = 1; l <= L; ++l) {
+        d.t[l] = buf(c, "t" + std::to_string(l)).as<float>();
+        d.h[l] = buf(c, "h" + std::to_string(l)).as<float>();
+    }
+    for (int l = 0; l < L; ++l) d.mu[l] = buf(c, "mu" + std::to_string(l)).as<float>();
+    d.e_atom = buf(c, "e_atom").as<float>();
+    d.A = buf(c, "A").as<float>();
+    d.F = buf(c, "F").as<float>();
+    d.Epred = buf(c, "Epred").as<double>();
+    d.gE = buf(c, "gE").as<float>();
+    d.gF = buf(c, "gF").as<float>();
+    d.sample_terms = buf(c, "sample_terms").as<double>();
+    d.block_scratch = c.block_scratch.as<double>();
+    d.gh = buf(c, "gh").as<float>();
+    d.gm = buf(c, "gm").as<float>();
+    d.Q = buf(c, "Q").as<float>();
+    for (int l = 0; l < L; ++l) {
+        d.part_wf[l] = buf(c, "part_wf" + std::to_string(l)).as<float>();
+        d.part_wu[l] = buf(c, "part_wu" + std::to_string(l)).as<float>();
+    }
+    d.part_head = buf(c, "part_head").as<float>();
+    d.part_emb = buf(c, "part_emb").as<float>();
+    d.ncta_edge = c.grid_warp, d.ncta_gemm = c.grid_gemm, d.ncta_red = c.ncta_red;
+    d.grads = c.grads.as<float>();
+    d.p64 = c.p64.as<double>();
+    d.v64 = c.v64.as<double>();
+    d.g64_in = nullptr;
+    d.p32 = c.p32.as<float>();
+    d.NP = c.NP;
+    d.emb_rows = kMaxZ;
+    return d;
+}
+
+BatchArrays make_batch_arrays(Ctx& c) {
+    BatchArrays b{};
+    b.atom_ptr = buf(c, "atom_ptr").as<int64_t>();
+    b.Z = buf(c, "Z").as<int32_t>();
+    b.zslot = buf(c, "zslot").as<int32_t>();
+    b.z_to_slot = buf(c, "z2s").as<int32_t>();
+    b.dsidx = buf(c, "dsidx").as<int32_t>();
+    b.emask = buf(c, "emask").as<uint8_t>();
+    b.fmask = buf(c, "fmask").as<uint8_t>();
+    b.denoise = buf(c, "denoise").as<uint8_t>();
+    return b;
+}
+
+// ------------------------------------------------------------- launches ---
+template <class Kern, class... Args>
+void launch(Ctx& c, const char* name, Kern kernel, int grid, int block, size_t smem, Args... args) {
+    KernelSlot* slot = nullptr;
+    if (c.profile) {
+        if (c.slot_cursor >= c.slots.size()) {
+            KernelSlot s;
+            CK(cudaEventCreate(&s.a));
+            CK(cudaEventCreate(&s.b));
+            c.slots.push_back(s);
+        }
+        slot = &c.slots[c.slot_cursor++];
+        slot->name = name;
+        CK(cudaEventRecord(slot->a, c.stream));
+    }
+    kernel<<<grid, block, smem, c.stream>>>(args...);
+    CK(cudaGetLastError());
+    if (slot) CK(cudaEventRecord(slot->b, c.stream));
+    ++c.launches;
+}
+
+void collect_kernel_times(Ctx& c) {
+    if (!c.profile) return;
+    for (size_t k = 0; k < c.slot_cursor && k < c.slots.size(); ++k) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, c.slots[k].a, c.slots[k].b) == cudaSuccess) {
+            auto& e = c.ktimes[c.slots[k].name];
+            e.first += ms;
+            e.second += 1;
+        } else {
+            (void)cudaGetLastError();
+        }
+    }
+}
+
+struct Ops {
+    void (*setup)(Ctx&);
+    void (*prep)(Ctx&);
+    void (*nlist)(Ctx&);
+    void (*forward)(Ctx&);
+    void (*loss)(Ctx&);
+    void (*backward)(Ctx&, bool general);
+    void (*opt)(Ctx&);
+};
+
+template <int H, int K>
+struct Model {
+    static size_t smem_update() { return sizeof(float) * (H * H + 2 * 32 * H); }
+    static size_t smem_bwd_gemm() { return sizeof(float) * (H * H + 2 * 32 * H); }
+    static size_t smem_bwd_edge() { return sizeof(float) * 8 * H * K; }
+    static size_t smem_force(int D) { return sizeof(float) * (D * H + K * D); }
+    static size_t smem_head_reduce(int D) { return sizeof(float) * (3 * H + K) * D; }
+
+    static void setup(Ctx& c) {
+        CK(cudaFuncSetAttribute(k_update<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_update()));
+        CK(cudaFuncSetAttribute(k_bwd_gemm<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bwd_gemm()));
+        CK(cudaFuncSetAttribute(k_bwd_edge<H, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem_bwd_edge()));
+        CK(cudaFuncSetAttribute(k_embed_grad<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(sizeof(float) * kMaxZ * H)));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bwd_edge<H, K>, 256, smem_bwd_edge()));
+        c.grid_warp = c.nsm * std::max(1, occ);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bwd_gemm<H>, 256, smem_bwd_gemm()));
+        c.grid_gemm = c.nsm * std::max(1, occ);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update<H>, 256, smem_update()));
+        c.grid_upd = c.nsm * std::max(1, occ);
+        c.grid_small = c.nsm * 4;
+        c.ncta_red = c.nsm;
+        c.grid_opt = static_cast<int>(std::min<int64_t>((c.NP + 255) / 256, 4 * c.nsm));
+        c.grid_reduce = static_cast<int>(std::min<int64_t>((c.NP + 255) / 256, 8 * c.nsm));
+    }
+
+    static void prep(Ctx& c) {
+        launch(c, "prep", k_prep, c.grid_small, 128, 0, make_dev(c), make_batch_arrays(c));
+    }
+
+    static void nlist(Ctx& c) {
+        const Dev d = make_dev(c);
+        launch(c, "nbr_count", k_nbr_count, c.grid_warp, 256, 0, d);
+        launch(c, "nbr_scan", k_scan, 1, 1024, 0, d);
+        launch(c, "nbr_fill", k_nbr_fill<K>, c.grid_warp, 256, 0, d);
+    }
+
+    static void forward(Ctx& c) {
+        const Dev d = make_dev(c);
+        for (int l = 0; l < c.L; ++l) {
+            launch(c, "message", k_message<H, K>, c.grid_warp, 256, 0, d, l);
+            launch(c, "update", k_update<H>, c.grid_upd, 256, smem_update(), d, l, l == c.L - 1 ? 1 : 0);
+        }
+        if (c.L == 0) throw InputErr("model: layers == 0 is not supported by the device path");
+        launch(c, "force", k_force<H, K>, c.grid_warp, 256, smem_force(c.D), d);
+        launch(c, "energy", k_energy, c.grid_small, 128, sizeof(double) * 128 * c.D, d);
+    }
+
+    static void loss(Ctx& c) {
+        const Dev d = make_dev(c);
+        launch(c, "loss", k_loss, c.grid_small, 128, 0, d);
+        launch(c, "loss_final", k_loss_final, 1, 1024, 0, d);
+    }
+
+    static void backward(Ctx& c, bool general) {
+        const Dev d = make_dev(c);
+        const int passes = general ? c.D : 1;
+        for (int q = 0; q < passes; ++q) {
+            const int ch = general ? q : -1;
+            launch(c, "head_bwd", k_head_bwd<H, K>, c.grid_warp, 256, 0, d, ch, q == 0 ? 1 : 0);
+            launch(c, "head_reduce", k_head_reduce<H, K>, c.ncta_red, 128, smem_head_reduce(c.D), d, ch,
+                   q == 0 ? 1 : 0);
+        }
+        for (int l = c.L - 1; l >= 0; --l) {
+            launch(c, "bwd_gemm", k_bwd_gemm<H>, c.grid_gemm, 256, smem_bwd_gemm(), d, l);
+            launch(c, "bwd_edge", k_bwd_edge<H, K>, c.grid_warp, 256, smem_bwd_edge(), d, l);
+        }
+        launch(c, "embed_grad", k_embed_grad<H>, c.ncta_red, H, sizeof(float) * kMaxZ * H, d);
+        SegTable tab{};
+        int64_t off = 0;
+        auto add = [&](int64_t n, int kind, const float* src, int ncta, int stride) {
+            tab.s[tab.nseg++] = Seg{off, static_cast<int32_t>(n), kind, src, ncta, stride};
+            off += n;
+        };
+        add(static_cast<int64_t>(kMaxZ) * H, 1, d.part_emb, c.ncta_red, 0);
+        for (int l = 0; l < c.L; ++l) add(H * K, 0, d.part_wf[l], c.grid_warp, H * K);
+        for (int l = 0; l < c.L; ++l) add(H * H, 0, d.part_wu[l], c.grid_gemm, H * H);
+        const int hw = (3 * H + K) * c.D;
+        add(H * c.D, 0, d.part_head + (2 * H + K) * c.D, c.ncta_red, hw);
+        add((2 * H + K) * c.D, 0, d.part_head, c.ncta_red, hw);
+        launch(c, "grad_reduce", k_grad_reduce, c.grid_reduce, 256, 0, d, tab);
+    }
+
+    static void opt(Ctx& c) {
+        Dev d = make_dev(c);
+        launch(c, "opt_norm", k_opt_norm, c.grid_opt, 256, 0, d, c.opt_G, c.opt_inv_g, c.opt_clip);
+        launch(c, "opt_step", k_opt_step, c.grid_opt, 256, 0, d, c.opt_inv_g, c.opt_lr, c.opt_decay, c.opt_eps);
+    }
+
+    static constexpr Ops ops{setup, prep, nlist, forward, loss, backward, opt};
+};
+
+const Ops* select_ops(int H, int K) {
+    if (H == 128 && K == 16) return &Model<128, 16>::ops;
+    if (H == 64 && K == 16) return &Model<64, 16>::ops;
+    if (H == 32 && K == 8) return &Model<32, 8>::ops;
+    return nullptr;
+}
+
+// ------------------------------------------------------------- staging ----
+inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+void ensure_stage(Ctx& c, size_t bytes) {
+    if (bytes > c.h_stage_cap) {
+        if (c.h_stage) CK(cudaFreeHost(c.h_stage));
+        const size_t cap = bytes + bytes / 4 + 4096;
+        CK(cudaMallocHost(reinterpret_cast<void**>(&c.h_stage), cap));
+        c.h_stage_cap = cap;
+    }
+    if (bytes > c.d_stage.bytes) {
+        if (c.d_stage.p) CK(cudaFree(c.d_stage.p));
+        const size_t cap = bytes + bytes / 4 + 4096;
+        CK(cudaMalloc(&c.d_stage.p, cap));
+        c.d_stage.bytes = cap;
+        c.graph_dirty = true;
+    }
+}
+
+// Validates a device-batch like the reference does (validate_system,
+// validate_labels, masked_loss shape checks) and records the host mirror.
+void validate_batch(Ctx& c, const lamm_batch_view* b) {
+    require(b != nullptr && b->atom_ptr && b->positions && b->atomic_numbers, "batch: null arrays");
+    require(b->n_samples >= 1, "batch: no samples");
+    require(b->atom_ptr[0] == 0 && b->atom_ptr[b->n_samples] == b->n_atoms, "batch: atom_ptr/n_atoms mismatch");
+    require(b->n_atoms < (int64_t(1) << 31), "batch: too many atoms for one device-batch");
+    for (int32_t s = 0; s < b->n_samples; ++s) {
+        require(b->atom_ptr[s + 1] > b->atom_ptr[s], "system has no atoms");
+        const int d = b->dataset_index ? b->dataset_index[s] : 0;
+        require(d >= 0, "negative dataset index");
+        require(d < c.D, "masked_loss: dataset index outside prediction heads");
+        if (c.use_table) require(d < c.ntab, "dataset index outside reference table");
+    }
+    for (int64_t k = 0; k < 3 * b->n_atoms; ++k) require(std::isfinite(b->positions[k]), "non-finite coordinate");
+    for (int64_t a = 0; a < b->n_atoms; ++a)
+        require(b->atomic_numbers[a] >= 1 && b->atomic_numbers[a] <= kMaxZ, "atomic number outside [1, 118]");
+}
+
+// Packs [StepHeader | atom_ptr | pos | Z | z2s | dsidx | emask | fmask | denoise
+// | E | F | noise] into the pinned blob; returns its size. Effective masks:
+// denoising samples train forces only (make_denoising_sample).
+size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const lamm_train_config* tc, int64_t step,
+                  int32_t rank) {
+    const int32_t B = b->n_samples;
+    const int64_t N = b->n_atoms;
+    bool any_dn = false;
+    if (apply_denoise && b->denoise)
+        for (int32_t s = 0; s < B; ++s) any_dn |= b->denoise[s] != 0;
+    StepHeader h{};
+    size_t off = align16(sizeof(StepHeader));
+    auto place = [&](int64_t& field, size_t bytes) {
+        field = static_cast<int64_t>(off);
+        off = align16(off + bytes);
+    };
+    place(h.off_atom_ptr, 8 * (B + 1));
+    place(h.off_pos, 24 * N);
+    place(h.off_Z, 4 * N);
+    place(h.off_z2s, 4 * 119);
+    place(h.off_dsidx, 4 * B);
+    place(h.off_emask, B);
+    place(h.off_fmask, B);
+    place(h.off_denoise, B);
+    place(h.off_E, 8 * B);
+    place(h.off_F, 24 * N);
+    if (any_dn) place(h.off_noise, 24 * N);
+    else h.off_noise = h.off_F;
+    h.blob_bytes = static_cast<int64_t>(off);
+    ensure_stage(c, off);
+    char* base = c.h_stage;
+    std::memcpy(base + h.off_atom_ptr, b->atom_ptr, 8 * (B + 1));
+    std::memcpy(base + h.off_pos, b->positions, 24 * N);
+    std::memcpy(base + h.off_Z, b->atomic_numbers, 4 * N);
+    int32_t* z2s = reinterpret_cast<int32_t*>(base + h.off_z2s);
+    std::fill(z2s, z2s + 119, -1);
+    int nslots = 0;
+    for (int64_t a = 0; a < N; ++a)
+        if (z2s[b->atomic_numbers[a]] < 0) z2s[b->atomic_numbers[a]] = nslots++;
+    int32_t* ds = reinterpret_cast<int32_t*>(base + h.off_dsidx);
+    uint8_t* em = reinterpret_cast<uint8_t*>(base + h.off_emask);
+    uint8_t* fm = reinterpret_cast<uint8_t*>(base + h.off_fmask);
+    uint8_t* dn = reinterpret_cast<uint8_t*>(base + h.off_denoise);
+    double* E = reinterpret_cast<double*>(base + h.off_E);
+    double* F = reinterpret_cast<double*>(base + h.off_F);
+    int me = 0, mf = 0;
+    for (int32_t s = 0; s < B; ++s) {
+        ds[s] = b->dataset_index ? b->dataset_index[s] : 0;
+        const bool is_dn = any_dn && b->denoise[s];
+        dn[s] = is_dn ? 1 : 0;
+        em[s] = is_dn ? 0 : (b->energy_mask ? b->energy_mask[s] : 0);
+        fm[s] = is_dn ? 1 : (b->force_mask ? b->force_mask[s] : 0);
+        require(!em[s] || b->energy, "energy mask set but energy missing");
+        require(!(fm[s] && !is_dn) || b->forces, "force mask set but force rows != atom count");
+        if (em[s] && c.use_table)
+            require(c.h_thas[ds[s]] != 0, "normalize_labels: dataset has no fitted energy statistics");
+        E[s] = em[s] ? b->energy[s] : 0.0;
+        me += em[s], mf += fm[s];
+    }
+    if (b->forces) std::memcpy(F, b->forces, 24 * N);
+    else std::memset(F, 0, 24 * N);
+    if (any_dn) {
+        // Raw displacement draws of make_denoising_sample: Rng(seed').normal(0, sigma)
+        // per atom, x, y, z in order (S/denoise.cpp:31-40), with
+        // seed' = mix_seed(mix_seed(seed, kNoiseTag + step), rank*B + b) (S/trainer.cpp:276-277).
+        require(tc->noise_sigma > 0.0, "apply_noise: sigma must be positive");
+        double* nz = reinterpret_cast<double*>(base + h.off_noise);
+        constexpr uint64_t kNoiseTag = 0x4e4f4953;
+        const uint64_t step_seed = splitmix_mix(tc->seed, kNoiseTag + static_cast<uint64_t>(step));
+        for (int32_t s = 0; s < B; ++s) {
+            if (!dn[s]) continue;
+            Stream st(splitmix_mix(step_seed, static_cast<uint64_t>(rank) * B + s));
+            for (int64_t k = 3 * b->atom_ptr[s]; k < 3 * b->atom_ptr[s + 1]; ++k) nz[k] = st.gauss(0.0, tc->noise_sigma);
+        }
+    }
+    h.B = B;
+    h.N = static_cast<int32_t>(N);
+    h.me = me, h.mf = mf;
+    h.nslots = nslots;
+    h.lambda_e = tc ? tc->lambda_energy : 1.0;
+    h.lambda_f = tc ? tc->lambda_force : 1.0;
+    h.workers = 1;
+    std::memcpy(base, &h, sizeof(StepHeader));
+    // host mirror
+    c.B = B, c.N = N, c.me = me, c.mf = mf;
+    c.h_atom_ptr.assign(b->atom_ptr, b->atom_ptr + B + 1);
+    c.h_Z.assign(b->atomic_numbers, b->atomic_numbers + N);
+    c.h_dsidx.assign(ds, ds + B);
+    c.h_emask.assign(em, em + B);
+    c.h_fmask.assign(fm, fm + B);
+    return off;
+}
+
+StepHeader read_header(Ctx& c) {
+    CK(cudaMemcpyAsync(c.h_result, c.d_stage.p, sizeof(StepHeader), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    collect_kernel_times(c);
+    return *c.h_result;
+}
+
+// First guess of the directed-pair capacity; overflow regrows it exactly.
+int64_t edge_guess(int64_t N) { return 32 * N; }
+
+// Runs the neighbour list, regrowing the edge capacity until it fits.
+void run_nlist(Ctx& c) {
+    for (int attempt = 0;; ++attempt) {
+        c.slot_cursor = 0;
+        c.ops->nlist(c);
+        const StepHeader h = read_header(c);
+        if (!h.overflow) break;
+        require(attempt < 4, "neighbour list capacity regrowth did not converge");
+        ensure_capacity(c, c.N, c.B, h.P);
+    }
+    c.nlist_valid = true;
+}
+
+void destroy_graphs(Ctx& c) {
+    if (c.g_step) cudaGraphExecDestroy(c.g_step);
+    if (c.g_opt) cudaGraphExecDestroy(c.g_opt);
+    c.g_step = c.g_opt = nullptr;
+}
+
+cudaGraphExec_t capture(Ctx& c, void (*body)(Ctx&)) {
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        body(c);
+    } catch (...) {
+        cudaStreamEndCapture(c.stream, &g);
+        if (g) cudaGraphDestroy(g);
+        throw;
+    }
+    CK(cudaStreamEndCapture(c.stream, &g));
+    cudaGraphExec_t ex = nullptr;
+    CK(cudaGraphInstantiate(&ex, g, 0));
+    CK(cudaGraphDestroy(g));
+    return ex;
+}
+
+void step_body(Ctx& c) {
+    c.ops->prep(c);
+    c.ops->nlist(c);
+    c.ops->forward(c);
+    c.ops->loss(c);
+    c.ops->backward(c, false);
+}
+
+void opt_body(Ctx& c) { c.ops->opt(c); }
+
+// One train step on the already-staged blob; returns the header after it.
+StepHeader run_train_step(Ctx& c, size_t bytes) {
+    for (int attempt = 0;; ++attempt) {
+        ensure_capacity(c, c.N, c.B, edge_guess(c.N));
+        CK(cudaMemcpyAsync(c.d_stage.p, c.h_stage, bytes, cudaMemcpyHostToDevice, c.stream));
+        const int64_t l0 = c.launches;
+        if (c.use_graph) {
+            if (c.graph_dirty || !c.g_step) {
+                destroy_graphs(c);
+                c.slot_cursor = 0;
+                c.g_step = capture(c, step_body);
+                c.g_opt = capture(c, opt_body);
+                c.graph_dirty = false;
+                c.graph_launches = c.launches - l0;
+            }
+            CK(cudaGraphLaunch(c.g_step, c.stream));
+        } else {
+            c.slot_cursor = 0;
+            step_body(c);
+        }
+        if (c.nranks > 1)
+            nccl_check(nccl().all_reduce(c.grads.p, c.grads.p, static_cast<size_t>(c.NP + 4), ncclFloat32, ncclSum,
+                                         c.comm, c.stream),
+                       "ncclAllReduce");
+        if (c.use_graph) CK(cudaGraphLaunch(c.g_opt, c.stream));
+        else opt_body(c);
+        c.last_step_launches = c.use_graph ? c.graph_launches : c.launches - l0;
+        const StepHeader h = read_header(c);
+        if (h.status != 2) {
+            c.batch_valid = c.nlist_valid = c.fwd_valid = c.loss_valid = true;
+            return h;
+        }
+        require(attempt < 4, "edge capacity regrowth did not converge");
+        ensure_capacity(c, c.N, c.B, h.overflow ? h.P : 0);
+    }
+}
+
+template <class T>
+std::vector<T> d2h(Ctx& c, const void* src, size_t count) {
+    std::vector<T> out(count);
+    if (count) CK(cudaMemcpyAsync(out.data(), src, sizeof(T) * count, cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaStreamSynchronize(c.stream));
+    return out;
+}
+
+void require_batch(Ctx& c) { require(c.batch_valid, "no batch: call lamm_batch_set first"); }
+
+void ensure_forward(Ctx& c) {
+    require_batch(c);
+    if (!c.nlist_valid) run_nlist(c);
+    if (!c.fwd_valid) {
+        c.slot_cursor = 0;
+        c.ops->forward(c);
+        read_header(c);
+        c.fwd_valid = true;
+    }
+}
+
+}  // namespace lamm_b200
+
+using namespace lamm_b200;
+
+// =================================================================== C ABI ==
+LAMM_API int lamm_ctx_create(int device, const lamm_model_config* cfg, lamm_ctx** out) {
+    return lamm_guard([&] {
+        require(cfg && out, "ctx_create: null argument");
+        require(cfg->hidden >= 1 && cfg->layers >= 0 && cfg->rbf >= 2 && cfg->cutoff > 0.0 && cfg->heads >= 1,
+                "model: invalid config");
+        require(cfg->layers >= 1 && cfg->layers <= kMaxLayers, "model: device path supports 1..8 layers");
+        require(cfg->heads <= kMaxHeads, "model: device path supports at most 32 heads");
+        const Ops* ops = select_ops(cfg->hidden, cfg->rbf);
+        require(ops != nullptr, "model: (hidden, rbf) must be one of (128,16), (64,16), (32,8)");
+        int ndev = 0;
+        CK(cudaGetDeviceCount(&ndev));
+        require(device >= 0 && device < ndev, "ctx_create: no such CUDA device");
+        auto* c = new lamm_ctx();
+        try {
+            c->device = device;
+            CK(cudaSetDevice(device));
+            CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            c->cfg = *cfg;
+            c->H = cfg->hidden, c->L = cfg->layers, c->K = cfg->rbf, c->D = cfg->heads;
+            c->NP = lamm_param_count(cfg);
+            CK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device));
+            c->ops = ops;
+            alloc_param_state(*c);
+            c->ops->setup(*c);
+            CK(cudaMallocHost(reinterpret_cast<void**>(&c->h_result), sizeof(StepHeader)));
+            ensure_stage(*c, 1 << 20);
+            for (auto& e : c->ev) CK(cudaEventCreate(&e));
+            ensure_capacity(*c, 1024, 64, 4096);
+            // empty reference table buffers so the device pointers are valid
+            bool ch = false;
+            for (const char* n : {"rho", "rho_has", "tmean", "tstd", "tfstd", "thas"}) ensure_buf(*c, n, 256, ch);
+        } catch (...) {
+            lamm_ctx_destroy(c);
+            throw;
+        }
+        *out = c;
+    });
+}
+
+LAMM_API void lamm_ctx_destroy(lamm_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    destroy_graphs(*c);
+    if (c->comm) nccl().comm_destroy(c->comm);
+    for (auto& kv : c->bufs)
+        if (kv.second.p) cudaFree(kv.second.p);
+    for (Buf* b : {&c->p64, &c->v64, &c->g64, &c->p32, &c->tanh_emb, &c->grads, &c->block_scratch, &c->d_stage})
+        if (b->p) cudaFree(b->p);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->h_result) cudaFreeHost(c->h_result);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& s : c->slots) {
+        if (s.a) cudaEventDestroy(s.a);
+        if (s.b) cudaEventDestroy(s.b);
+    }
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+LAMM_API int lamm_ctx_set_option(lamm_ctx* c, const char* name, int64_t value) {
+    return lamm_guard([&] {
+        require(c && name, "set_option: null argument");
+        const std::string n(name);
+        if (n == "graph") c->use_graph = value != 0;
+        else if (n == "profile") c->profile = value != 0;
+        else if (n == "export_fp64") {
+            c->export64 = value != 0;
+            CK(cudaSetDevice(c->device));
+            ensure_capacity(*c, 0, 0, 0);
+            bool ch = false;
+            if (c->export64) {
+                ensure_buf(*c, "dist64", 8 * c->Pcap, ch);
+                ensure_buf(*c, "unit64", 24 * c->Pcap, ch);
+            }
+            c->nlist_valid = false;
+        } else throw InputErr("set_option: unknown option " + n);
+        c->graph_dirty = true;
+    });
+}
+
+LAMM_API int lamm_params_set(lamm_ctx* c, const double* flat, size_t n) {
+    return lamm_guard([&] {
+        require(c && flat && static_cast<int64_t>(n) == c->NP, "params_set: size mismatch");
+        CK(cudaSetDevice(c->device));
+        CK(cudaMemcpyAsync(c->p64.p, flat, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        Dev d = make_dev(*c);
+        k_params_cast<<<c->grid_opt, 256, 0, c->stream>>>(d);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(c->stream));
+        c->fwd_valid = c->loss_valid = false;
+    });
+}
+
+LAMM_API int lamm_params_get(lamm_ctx* c, double* flat, size_t n) {
+    return lamm_guard([&] {
+        require(c && flat && static_cast<int64_t>(n) == c->NP, "params_get: size mismatch");
+        CK(cudaSetDevice(c->device));
+        CK(cudaMemcpyAsync(flat, c->p64.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+LAMM_API int lamm_rms_state_set(lamm_ctx* c, const double* flat, size_t n) {
+    return lamm_guard([&] {
+        require(c && flat && static_cast<int64_t>(n) == c->NP, "rms_state_set: size mismatch");
+        CK(cudaSetDevice(c->device));
+        CK(cudaMemcpyAsync(c->v64.p, flat, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+LAMM_API int lamm_rms_state_get(lamm_ctx* c, double* flat, size_t n) {
+    return lamm_guard([&] {
+        require(c && flat && static_cast<int64_t>(n) == c->NP, "rms_state_get: size mismatch");
+        CK(cudaSetDevice(c->device));
+        CK(cudaMemcpyAsync(flat, c->v64.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+LAMM_API int lamm_ref_table_set(lamm_ctx* c, const lamm_ref_table* t) {
+    return lamm_guard([&] {
+        require(c != nullptr, "ref_table_set: null ctx");
+        CK(cudaSetDevice(c->device));
+        if (!t) {
+            c->use_table = false;
+            c->ntab = 0;
+            c->graph_dirty = true;
+            return;
+        }
+        require(t->n_tables >= 1 && t->rho && t->rho_has && t->energy_mean && t->energy_std && t->force_std &&
+                    t->has_energy_stats,
+                "ref_table_set: incomplete table");
+        const int n = t->n_tables;
+        bool ch = false;
+        ensure_buf(*c, "rho", 8 * 119 * n, ch);
+        ensure_buf(*c, "rho_has", 119 * n, ch);
+        ensure_buf(*c, "tmean", 8 * n, ch);
+        ensure_buf(*c, "tstd", 8 * n, ch);
+        ensure_buf(*c, "tfstd", 8 * n, ch);
+        ensure_buf(*c, "thas", n, ch);
+        auto up = [&](const char* name, const void* src, size_t bytes) {
+            CK(cudaMemcpyAsync(buf(*c, name).p, src, bytes, cudaMemcpyHostToDevice, c->stream));
+        };
+        up("rho", t->rho, 8 * 119 * n);
+        up("rho_has", t->rho_has, 119 * n);
+        up("tmean", t->energy_mean, 8 * n);
+        up("tstd", t->energy_std, 8 * n);
+        up("tfstd", t->force_std, 8 * n);
+        up("thas", t->has_energy_stats, n);
+        CK(cudaStreamSynchronize(c->stream));
+        c->h_thas.assign(t->has_energy_stats, t->has_energy_stats + n);
+        c->use_table = true;
+        c->ntab = n;
+        c->graph_dirty = true;
+    });
+}
+
+LAMM_API int lamm_batch_set(lamm_ctx* c, const lamm_batch_view* b) {
+    return lamm_guard([&] {
+        require(c != nullptr, "batch_set: null ctx");
+        CK(cudaSetDevice(c->device));
+        validate_batch(*c, b);
+        const size_t bytes = pack_batch(*c, b, false, nullptr, 0, 0);
+        ensure_capacity(*c, c->N, c->B, edge_guess(c->N));
+        CK(cudaMemcpyAsync(c->d_stage.p, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream));
+        c->slot_cursor = 0;
+        c->ops->prep(*c);
+        read_header(*c);
+        c->batch_valid = true;
+        c->nlist_valid = c->fwd_valid = c->loss_valid = false;
+    });
+}
+
+LAMM_API int lamm_labels_get(lamm_ctx* c, double* energy, double* forces) {
+    return lamm_guard([&] {
+        require(c != nullptr, "labels_get: null ctx");
+        require_batch(*c);
+        CK(cudaSetDevice(c->device));
+        if (energy) CK(cudaMemcpyAsync(energy, buf(*c, "En").p, 8 * c->B, cudaMemcpyDeviceToHost, c->stream));
+        if (forces) CK(cudaMemcpyAsync(forces, buf(*c, "Fn").p, 24 * c->N, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+LAMM_API int lamm_neighbor_list(lamm_ctx* c, int64_t* n_pairs) {
+    return lamm_guard([&] {
+        require(c != nullptr, "neighbor_list: null ctx");
+        require_batch(*c);
+        CK(cudaSetDevice(c->device));
+        if (!c->nlist_valid) run_nlist(*c);
+        const StepHeader h = read_header(*c);
+        if (n_pairs) *n_pairs = h.P;
+    });
+}
+
+LAMM_API int lamm_neighbor_list_copy(lamm_ctx* c, int64_t* sample_pair_ptr, int32_t* oi, int32_t* oj, double* dist,
+                                     double* unit) {
+    return lamm_guard([&] {
+        require(c != nullptr, "neighbor_list_copy: null ctx");
+        require_batch(*c);
+        CK(cudaSetDevice(c->device));
+        if (!c->nlist_valid) run_nlist(*c);
+        const StepHeader h = read_header(*c);
+        const int64_t P = h.P;
+        const auto rp = d2h<int32_t>(*c, buf(*c, "row_ptr").p, c->N + 1);
+        const auto col = d2h<int32_t>(*c, buf(*c, "col").p, P);
+        for (int32_t s = 0; s < c->B; ++s) {
+            const int64_t lo = c->h_atom_ptr[s], hi = c->h_atom_ptr[s + 1];
+            if (sample_pair_ptr) sample_pair_ptr[s] = rp[lo];
+            for (int64_t i = lo; i < hi; ++i)
+                for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+                    if (oi) oi[p] = static_cast<int32_t>(i - lo);
+                    if (oj) oj[p] = static_cast<int32_t>(col[p] - lo);
+                }
+        }
+        if (sample_pair_ptr) sample_pair_ptr[c->B] = P;
+        if (dist || unit) {
+            require(c->export64, "neighbor_list_copy: set option export_fp64 for fp64 distances");
+            if (dist) CK(cudaMemcpyAsync(dist, buf(*c, "dist64").p, 8 * P, cudaMemcpyDeviceToHost, c->stream));
+            if (unit) CK(cudaMemcpyAsync(unit, buf(*c, "unit64").p, 24 * P, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+    });
+}
+
+namespace lamm_b200 {
+// [N][D][3] (device) -> per-sample (d*n+j)*3+c (reference Prediction layout)
+void to_ref_layout(Ctx& c, const float* src, double* dst) {
+    const int D = c.D;
+    for (int32_t s = 0; s < c.B; ++s) {
+        const int64_t lo = c.h_atom_ptr[s], n = c.h_atom_ptr[s + 1] - lo;
+        double* o = dst + 3 * D * lo;
+        for (int64_t j = 0; j < n; ++j)
+            for (int d = 0; d < D; ++d)
+                for (int x = 0; x < 3; ++x) o[(d * n + j) * 3 + x] = src[((lo + j) * D + d) * 3 + x];
+    }
+}
+void from_ref_layout(Ctx& c, const double* src, float* dst) {
+    const int D = c.D;
+    for (int32_t s = 0; s < c.B; ++s) {
+        const int64_t lo = c.h_atom_ptr[s], n = c.h_atom_ptr[s + 1] - lo;
+        const double* in = src + 3 * D * lo;
+        for (int64_t j = 0; j < n; ++j)
+            for (int d = 0; d < D; ++d)
+                for (int x = 0; x < 3; ++x) dst[((lo + j) * D + d) * 3 + x] = static_cast<float>(in[(d * n + j) * 3 + x]);
+    }
+}
+}  // namespace lamm_b200
+
+LAMM_API int lamm_forward(lamm_ctx* c, double* energy, double* forces) {
+    return lamm_guard([&] {
+        require(c != nullptr, "forward: null ctx");
+        CK(cudaSetDevice(c->device));
+        c->fwd_valid = false;
+        ensure_forward(*c);
+        if (energy) {
+            CK(cudaMemcpyAsync(energy, buf(*c, "Epred").p, 8 * c->B * c->D, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        }
+        if (forces) {
+            const auto F = d2h<float>(*c, buf(*c, "F").p, 3 * c->N * c->D);
+            to_ref_layout(*c, F.data(), forces);
+        }
+    });
+}
+
+LAMM_API int lamm_forward_cache_get(lamm_ctx* c, int which, int layer, double* out) {
+    return lamm_guard([&] {
+        require(c && out, "forward_cache_get: null argument");
+        require_batch(*c);
+        require(c->fwd_valid, "forward_cache_get: run lamm_forward first");
+        CK(cudaSetDevice(c->device));
+        const int H = c->H;
+        std::vector<float> v;
+        if (which == 0) {
+            require(layer >= 0 && layer <= c->L, "forward_cache_get: layer out of range");
+            if (layer == 0) {
+                const auto emb = d2h<float>(*c, c->p32.p, static_cast<size_t>(kMaxZ) * H);
+                v.resize(static_cast<size_t>(c->N) * H);
+                for (int64_t i = 0; i < c->N; ++i)
+                    std::copy_n(emb.begin() + static_cast<int64_t>(c->h_Z[i] - 1) * H, H, v.begin() + i * H);
+            } else {
+                v = d2h<float>(*c, buf(*c, "h" + std::to_string(layer)).p, static_cast<size_t>(c->N) * H);
+            }
+        } else {
+            require(layer >= 0 && layer < c->L, "forward_cache_get: layer out of range");
+            v = d2h<float>(*c, buf(*c, "mu" + std::to_string(layer)).p, static_cast<size_t>(c->N) * H);
+        }
+        for (size_t k = 0; k < v.size(); ++k) out[k] = v[k];
+    });
+}
+
+LAMM_API int lamm_loss_grad(lamm_ctx* c, const lamm_loss_config* cfg, lamm_loss_breakdown* out, double* g_energy,
+                            double* g_forces) {
+    return lamm_guard([&] {
+        require(c != nullptr, "loss_grad: null ctx");
+        CK(cudaSetDevice(c->device));
+        const double le = cfg ? cfg->lambda_energy : 1.0, lf = cfg ? cfg->lambda_force : 1.0;
+        require(le >= 0.0 && lf >= 0.0, "masked_loss: lambdas must be non-negative");
+        ensure_forward(*c);
+        StepHeader* hd = reinterpret_cast<StepHeader*>(c->h_stage);  // staged header copy
+        hd->lambda_e = le, hd->lambda_f = lf;
+        CK(cudaMemcpyAsync(c->d_stage.as<char>() + offsetof(StepHeader, lambda_e), &hd->lambda_e, 16,
+                           cudaMemcpyHostToDevice, c->stream));
+        c->slot_cursor = 0;
+        c->ops->loss(*c);
+        const StepHeader h = read_header(*c);
+        if (out) {
+            out->total = h.loss_total;
+            out->energy_term = h.loss_energy;
+            out->force_term = h.loss_force;
+            out->energy_labeled = c->me;
+            out->force_labeled = c->mf;
+            out->energy_empty = c->me == 0;
+            out->force_empty = c->mf == 0;
+        }
+        if (g_energy) {
+            const auto ge = d2h<float>(*c, buf(*c, "gE").p, static_cast<size_t>(c->B) * c->D);
+            for (size_t k = 0; k < ge.size(); ++k) g_energy[k] = ge[k];
+        }
+        if (g_forces) {
+            const auto gf = d2h<float>(*c, buf(*c, "gF").p, 3 * c->N * c->D);
+            to_ref_layout(*c, gf.data(), g_forces);
+        }
+        c->loss_valid = true;
+    });
+}
+
+LAMM_API int lamm_backward(lamm_ctx* c, const double* up_energy, const double* up_forces, double* grads_accum) {
+    return lamm_guard([&] {
+        require(c != nullptr, "backward: null ctx");
+        CK(cudaSetDevice(c->device));
+        ensure_forward(*c);
+        const bool general = up_energy || up_forces;
+        if (general) {
+            std::vector<float> ge(static_cast<size_t>(c->B) * c->D, 0.f), gf(3 * c->N * c->D, 0.f);
+            if (up_energy)
+                for (size_t k = 0; k < ge.size(); ++k) ge[k] = static_cast<float>(up_energy[k]);
+            if (up_forces) from_ref_layout(*c, up_forces, gf.data());
+            CK(cudaMemcpyAsync(buf(*c, "gE").p, ge.data(), 4 * ge.size(), cudaMemcpyHostToDevice, c->stream));
+            CK(cudaMemcpyAsync(buf(*c, "gF").p, gf.data(), 4 * gf.size(), cudaMemcpyHostToDevice, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+        } else {
+            require(c->loss_valid, "backward: no upstream gradient (pass one or call lamm_loss_grad)");
+        }
+        c->slot_cursor = 0;
+        c->ops->backward(*c, general);
+        read_header(*c);
+        if (grads_accum) {
+            const auto g = d2h<float>(*c, c->grads.p, c->NP);
+            for (int64_t k = 0; k < c->NP; ++k) grads_accum[k] += g[k];
+        }
+    });
+}
+
+LAMM_API int lamm_grads_get(lamm_ctx* c, double* flat, size_t n) {
+    return lamm_guard([&] {
+        require(c && flat && static_cast<int64_t>(n) == c->NP, "grads_get: size mismatch");
+        CK(cudaSetDevice(c->device));
+        const auto g = d2h<float>(*c, c->grads.p, c->NP);
+        for (int64_t k = 0; k < c->NP; ++k) flat[k] = g[k];
+    });
+}
+
+LAMM_API int lamm_comm_unique_id(void* out128) {
+    return lamm_guard([&] {
+        require(out128 != nullptr, "comm_unique_id: null output");
+        if (!nccl().ok) throw NcclErr("libnccl.so.2 could not be loaded");
+        ncclUniqueId id;
+        nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+        std::memcpy(out128, &id, sizeof(id));
+    });
+}
+
+LAMM_API int lamm_comm_init(lamm_ctx* c, int nranks, int rank, const void* id128) {
+    return lamm_guard([&] {
+        require(c && id128, "comm_init: null argument");
+        require(nranks >= 1 && rank >= 0 && rank < nranks, "comm_init: bad rank layout");
+        CK(cudaSetDevice(c->device));
+        if (nranks == 1) {
+            c->nranks = 1, c->rank = 0;
+            return;
+        }
+        if (!nccl().ok) throw NcclErr("libnccl.so.2 could not be loaded");
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof(id));
+        nccl_check(nccl().comm_init_rank(&c->comm, nranks, id, rank), "ncclCommInitRank");
+        c->nranks = nranks, c->rank = rank;
+    });
+}
+
+LAMM_API int lamm_train_step(lamm_ctx* c, const lamm_batch_view* b, const lamm_train_config* tc, int64_t step,
+                             int32_t workers, int32_t rank, lamm_step_result* res) {
+    return lamm_guard([&] {
+        require(c && b && tc, "train_step: null argument");
+        require(workers >= 1 && rank >= 0 && rank < workers, "train_step: bad worker layout");
+        require(workers == c->nranks || c->nranks == 1,
+                "train_step: workers must equal the communicator size (or 1 rank simulating)");
+        require(tc->learning_rate > 0.0, "train: learning_rate must be positive");
+        require(tc->clip_norm >= 0.0, "train: clip_norm must be >= 0");
+        require(tc->rms_decay >= 0.0 && tc->rms_decay < 1.0, "train: rms_decay must be in [0, 1)");
+        require(tc->rms_epsilon > 0.0, "train: rms_epsilon must be positive");
+        require(tc->lambda_energy >= 0.0 && tc->lambda_force >= 0.0, "train: lambdas must be >= 0");
+        CK(cudaSetDevice(c->device));
+        validate_batch(*c, b);
+        if (c->denoise_scheme != (tc->noise_scheme ? 1 : 0)) {
+            c->denoise_scheme = tc->noise_scheme ? 1 : 0;
+            c->graph_dirty = true;
+        }
+        const size_t bytes = pack_batch(*c, b, true, tc, step, rank);
+        const double inv_g = 1.0 / static_cast<double>(workers);
+        if (c->opt_inv_g != inv_g || c->opt_lr != tc->learning_rate || c->opt_decay != tc->rms_decay ||
+            c->opt_eps != tc->rms_epsilon || c->opt_clip != tc->clip_norm || c->opt_G != workers) {
+            c->opt_inv_g = inv_g, c->opt_lr = tc->learning_rate, c->opt_decay = tc->rms_decay;
+            c->opt_eps = tc->rms_epsilon, c->opt_clip = tc->clip_norm, c->opt_G = workers;
+            c->graph_dirty = true;
+        }
+        int retries = 0;
+        const StepHeader h = run_train_step(*c, bytes);
+        if (res) {
+            res->loss = h.global_loss;
+            res->grad_norm = h.grad_norm;
+            res->local.total = h.loss_total;
+            res->local.energy_term = h.loss_energy;
+            res->local.force_term = h.loss_force;
+            res->local.energy_labeled = c->me;
+            res->local.force_labeled = c->mf;
+            res->local.energy_empty = c->me == 0;
+            res->local.force_empty = c->mf == 0;
+            res->n_atoms = c->N;
+            res->n_edges = h.P;
+            res->status = h.status == 1 ? LAMM_ENONFINITE : LAMM_OK;
+            res->retries = retries;
+        }
+        if (h.status == 1)
+            throw NonFinite("non-finite loss or gradient at step " + std::to_string(step));
+    });
+}
+
+LAMM_API int lamm_optimizer_step(lamm_ctx* c, const double* grad_sum, int32_t workers, const lamm_train_config* tc,
+                                 double* grad_norm) {
+    return lamm_guard([&] {
+        require(c && grad_sum && tc, "optimizer_step: null argument");
+        require(workers >= 1, "optimizer_step: workers must be >= 1");
+        CK(cudaSetDevice(c->device));
+        CK(cudaMemcpyAsync(c->g64.p, grad_sum, sizeof(double) * c->NP, cudaMemcpyHostToDevice, c->stream));
+        Dev d = make_dev(*c);
+        d.g64_in = c->g64.as<double>();
+        const double inv_g = 1.0 / static_cast<double>(workers);
+        k_opt_norm<<<c->grid_opt, 256, 0, c->stream>>>(d, workers, inv_g, tc->clip_norm);
+        CK(cudaGetLastError());
+        k_opt_step<<<c->grid_opt, 256, 0, c->stream>>>(d, inv_g, tc->learning_rate, tc->rms_decay, tc->rms_epsilon);
+        CK(cudaGetLastError());
+        const StepHeader h = read_header(*c);
+        if (grad_norm) *grad_norm = h.grad_norm;
+        c->fwd_valid = c->loss_valid = false;
+        if (h.status == 1) throw NonFinite("non-finite gradient");
+    });
+}
+
+LAMM_API int lamm_sync(lamm_ctx* c) {
+    return lamm_guard([&] {
+        require(c != nullptr, "sync: null ctx");
+        CK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+LAMM_API int lamm_event_record(lamm_ctx* c, int slot) {
+    return lamm_guard([&] {
+        require(c && slot >= 0 && slot < 64, "event_record: bad slot");
+        CK(cudaEventRecord(c->ev[slot], c->stream));
+    });
+}
+
+LAMM_API int lamm_event_elapsed_ms(lamm_ctx* c, int a, int b, float* ms) {
+    return lamm_guard([&] {
+        require(c && ms && a >= 0 && a < 64 && b >= 0 && b < 64, "event_elapsed: bad slot");
+        CK(cudaEventSynchronize(c->ev[b]));
+        CK(cudaEventElapsedTime(ms, c->ev[a], c->ev[b]));
+    });
+}
+
+LAMM_API int lamm_kernel_times(lamm_ctx* c, int max_kernels, const char** names, double* total_ms, int64_t* launches,
+                               int* n_kernels) {
+    return lamm_guard([&] {
+        require(c != nullptr, "kernel_times: null ctx");
+        int k = 0;
+        for (const auto& kv : c->ktimes) {
+            if (k < max_kernels) {
+                if (names) names[k] = kv.first.c_str();
+                if (total_ms) total_ms[k] = kv.second.first;
+                if (launches) launches[k] = kv.second.second;
+            }
+            ++k;
+        }
+        if (n_kernels) *n_kernels = k;
+    });
+}
+
+LAMM_API int lamm_kernel_times_reset(lamm_ctx* c) {
+    return lamm_guard([&] {
+        require(c != nullptr, "kernel_times_reset: null ctx");
+        c->ktimes.clear();
+    });
+}
+
+LAMM_API int64_t lamm_last_step_launches(lamm_ctx* c) { return c ? c->last_step_launches : -1; }

@@ -1,0 +1,161 @@
+// device.cuh - device-side state of one lamm_ctx and the helpers shared by the
+// sm_100a kernels (kernels.cuh) and the host orchestration (device.cu).
+//
+// HBM layout of one device-batch (all row-major, atoms in batch order, every
+// sample's atoms contiguous — the CSR the host packs):
+//   positions  x/y/z        fp64 SoA [N]           (bit-exact neighbour test)
+//   edges      row_ptr      int32 [N+1]            (CSR by destination atom i,
+//              col          int32 [P]               j ascending = reference order)
+//              geo          float4 [P]  {u_x,u_y,u_z,fcut}
+//              rbf          fp32 [P][K]             (Gaussians of the fp64 distance)
+//   features   t[l], h[l]   fp32 [N][H]  l = 1..L   (t = tanh h; t[0] = tanh(E[Z]))
+//              mu[l]        fp32 [N][H]  l = 0..L-1 (tanh of the message)
+//   heads      e_atom, A    fp32 [N][D]            (per-atom energy, force-head split)
+//              F            fp32 [N][D][3]
+//   backward   gh, gm       fp32 [N][H]
+//              Q            fp32 [N][H+K+1]         (per-atom force-head terms)
+//   gradients  partials     fp32 [ncta][tensor]     (deterministic per-CTA sums)
+//              grads        fp32 [NP + 4]           (flat for_each_tensor order +
+//                                                    loss hi/lo, overflow, count)
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lamm_b200 {
+
+constexpr int kMaxLayers = 8;
+constexpr int kMaxHeads = 32;
+constexpr int kMaxZ = 118;
+
+// Per-step scalars that live in device memory so one captured CUDA graph can
+// be replayed for device-batches of any size.
+struct StepHeader {
+    int32_t B, N, P, overflow;   // P written by the scan; overflow if P > capacity
+    int32_t me, mf;              // this rank's sum m_E, sum m_F (after denoise relabelling)
+    int32_t nslots, status;      // distinct atomic numbers; non-finite flag
+    int32_t workers, pad0;
+    double lambda_e, lambda_f;
+    double loss_energy, loss_force, loss_total;  // this rank's Eq. (5) breakdown
+    double grad_norm, clip_scale, global_loss;
+    uint32_t done_counter, pad1;
+    // byte offsets of the staged input arrays inside the upload blob (the blob
+    // starts with this header), see device.cu:pack_batch
+    int64_t off_atom_ptr, off_pos, off_Z, off_z2s, off_dsidx, off_emask, off_fmask, off_denoise, off_E, off_F,
+        off_noise, blob_bytes;
+};
+
+struct Dev {
+    int H, L, K, D;
+    double rc;
+    int64_t Ncap, Bcap, Pcap;
+    StepHeader* hdr;
+    // batch (uploaded blob + prep outputs)
+    const int64_t* atom_ptr;
+    const double* pos_in;      // [3N] AoS from the host
+    const int32_t* Z;          // [N]
+    const int32_t* zslot;      // [N]  slot of Z among the batch's distinct Z
+    const int32_t* z_to_slot;  // [119] (-1: absent)
+    const int32_t* dsidx;      // [B]
+    const uint8_t* emask;      // [B]  effective m_E (0 for denoising samples)
+    const uint8_t* fmask;      // [B]  effective m_F (1 for denoising samples)
+    const uint8_t* denoise;    // [B]
+    const double* E_raw;       // [B]
+    const double* F_raw;       // [3N]
+    const double* noise;       // [3N] raw Gaussian displacement draws (denoising samples)
+    int32_t* sample_of;        // [N]
+    double *x, *y, *z;         // [N] fp64 (noisy) positions, SoA
+    double* En;                // [B]  normalized energy labels
+    double* Fn;                // [3N] normalized force labels
+    int use_table, denoise_scheme, ntab;
+    const double* rho;         // [ntab][119]
+    const uint8_t* rho_has;
+    const double *tmean, *tstd, *tfstd;
+    const uint8_t* thas;
+    // edges
+    int32_t *cnt, *row_ptr, *col;
+    float4* geo;
+    float* rbf;
+    double *dist64, *unit64;
+    int export64;
+    // fp32 working parameters
+    const float* emb;        // [118][H]
+    const float* tanh_emb;   // [118][H]
+    const float* wf[kMaxLayers];  // [H][K]
+    const float* wu[kMaxLayers];  // [H][H]  (row b = output, col a = input)
+    const float* we;         // [H][D]
+    const float* wfh;        // [2H+K][D]
+    // activations
+    float* t[kMaxLayers + 1];
+    float* h[kMaxLayers + 1];
+    float* mu[kMaxLayers];
+    float *e_atom, *A, *F;
+    double* Epred;           // [B][D]
+    // loss gradients
+    float* gE;               // [B][D]
+    float* gF;               // [N][D][3]
+    double* sample_terms;    // [B][2]
+    double* block_scratch;   // reduction scratch
+    // backward
+    float *gh, *gm, *Q;
+    float* part_wf[kMaxLayers];
+    float* part_wu[kMaxLayers];
+    float* part_head;
+    float* part_emb;
+    int ncta_edge, ncta_gemm, ncta_red;
+    float* grads;            // [NP + 4]
+    // fp64 master state
+    double *p64, *v64;
+    const double* g64_in;    // optional fp64 gradient input for the optimizer
+    float* p32;              // [NP] fp32 working copy (emb/wf/wu/... point into it)
+    float* tanh_emb_w;       // writable alias of tanh_emb
+    int64_t NP;
+    int32_t emb_rows;
+};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int N>
+struct VecF {
+    float v[N];
+};
+
+template <int N>
+__device__ __forceinline__ VecF<N> ldv(const float* __restrict__ p) {
+    VecF<N> r;
+    if constexpr (N == 4) {
+        const float4 q = *reinterpret_cast<const float4*>(p);
+        r.v[0] = q.x, r.v[1] = q.y, r.v[2] = q.z, r.v[3] = q.w;
+    } else if constexpr (N == 2) {
+        const float2 q = *reinterpret_cast<const float2*>(p);
+        r.v[0] = q.x, r.v[1] = q.y;
+    } else {
+#pragma unroll
+        for (int c = 0; c < N; ++c) r.v[c] = p[c];
+    }
+    return r;
+}
+
+template <int N>
+__device__ __forceinline__ void stv(float* p, const VecF<N>& r) {
+    if constexpr (N == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(r.v[0], r.v[1], r.v[2], r.v[3]);
+    } else if constexpr (N == 2) {
+        *reinterpret_cast<float2*>(p) = make_float2(r.v[0], r.v[1]);
+    } else {
+#pragma unroll
+        for (int c = 0; c < N; ++c) p[c] = r.v[c];
+    }
+}
+
+}  // namespace lamm_b200

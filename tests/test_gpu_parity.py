@@ -1,0 +1,258 @@
+"""GPU parity: liblamm_b200.so (sm_100a) through its C ABI vs the CPU oracle.
+
+Bars: neighbour lists bit-exact (pair set, order, fp64 distance
+and unit); energies, forces, loss and every gradient tensor within 1e-4 per
+tensor (max|d|/max|ref| and ||d||/||ref||) in fp32 against the fp64 oracle;
+the RMS optimizer bit-exact in fp64 given the same gradient.
+"""
+import numpy as np
+import pytest
+
+from conftest import TOL, assert_close, has_gpu, rel_err
+import cases
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import paper_2505_22208_b200 as pk
+    return pk
+
+
+@pytest.fixture(scope="module")
+def dev(pk):
+    d = pk.Device(pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4]), seed=7)
+    d.set_option("export_fp64", 1)
+    yield d
+    d.close()
+
+
+def tensors(cfg, flat):
+    """Splits a flat parameter/gradient vector in for_each_tensor order."""
+    H, L, K, _, D = cfg
+    sizes = [("embedding", 118 * H)] + [(f"filter{l}", H * K) for l in range(L)] + \
+            [(f"update{l}", H * H) for l in range(L)] + [("energy_head", H * D), ("force_head", (2 * H + K) * D)]
+    out, o = {}, 0
+    for name, n in sizes:
+        out[name] = flat[o:o + n]
+        o += n
+    return out
+
+
+def check_nlist(dev, oracle_ref, batch):
+    dev.set_batch(batch)
+    ptr, oi, oj, dist, unit = dev.build_neighbor_list()
+    ap = batch["atom_ptr"]
+    for s in range(len(ap) - 1):
+        lo, hi = ap[s], ap[s + 1]
+        ri, rj, rd, ru = oracle_ref.neighbor_list(batch["pos"][lo:hi], batch["Z"][lo:hi], 5.0)
+        sl = slice(ptr[s], ptr[s + 1])
+        assert np.array_equal(oi[sl], ri) and np.array_equal(oj[sl], rj), f"pair set/order differs in sample {s}"
+        assert np.array_equal(dist[sl].view(np.uint64), rd.view(np.uint64)), f"fp64 distance bits differ ({s})"
+        assert np.array_equal(unit[sl].view(np.uint64), ru.view(np.uint64)), f"fp64 unit bits differ ({s})"
+    return ptr
+
+
+def test_neighbor_list_bit_exact_molecules(pk, dev, oracle_ref):
+    check_nlist(dev, oracle_ref, cases.molecules(pk, 64, 42))
+
+
+def test_neighbor_list_edge_cases(pk, dev, oracle_ref):
+    rng = np.random.default_rng(0)
+    batch = cases.pack(cases.edge_systems(rng))
+    ptr = check_nlist(dev, oracle_ref, batch)
+    counts = np.diff(ptr)
+    assert counts[0] == 0 and counts[1] == 2 and counts[2] == 0 and counts[3] == 0 and counts[4] == 2
+    assert counts[5] == 0  # (0,0,0)-(3,4,0) and (0,0,0)-(0,0,5) are exactly 5 A: excluded
+
+
+def test_neighbor_list_large_cluster(pk, dev, oracle_ref):
+    # max-size samples: 2000-atom cluster next to small ones (ragged rows)
+    big = pk.synth_generate(1, 3, mode=2000, sigma=0.01, min_atoms=2000, max_atoms=2000, elements=(14,),
+                            relax_steps=0)
+    small = cases.molecules(pk, 5, 9)
+    check_nlist(dev, oracle_ref, pk.concat([small, big]))
+
+
+def test_forward_matches_oracle(pk, dev, oracle_port):
+    batch = cases.molecules(pk, 48, 11)
+    params = oracle_port.init_params(cases.CFG, 7)
+    dev.set_params(params)
+    dev.set_batch(batch)
+    e, f = dev.forward()
+    re, rf = oracle_port.forward(cases.CFG, params, batch)
+    assert_close(e, re, what="energy")
+    assert_close(f, rf, what="forces")
+    # ForwardCache of one sample (h per layer, tanh(m) per layer)
+    ap = batch["atom_ptr"]
+    h, mt = oracle_port.forward_cache(cases.CFG, params, batch["pos"][ap[0]:ap[1]], batch["Z"][ap[0]:ap[1]])
+    for l in range(cases.CFG[1] + 1):
+        assert_close(dev.forward_cache("h", l)[ap[0]:ap[1]], h[l], what=f"h[{l}]")
+    for l in range(cases.CFG[1]):
+        assert_close(dev.forward_cache("mu", l)[ap[0]:ap[1]], mt[l], what=f"tanh(m)[{l}]")
+
+
+def test_forward_momentum_conservation(pk, dev):
+    batch = cases.molecules(pk, 16, 12)
+    dev.set_params(pk.init_params(dev.cfg, 3))
+    dev.set_batch(batch)
+    _, f = dev.forward()
+    D, ap = dev.cfg.heads, batch["atom_ptr"]
+    for s in range(len(ap) - 1):
+        blk = f[3 * D * ap[s]:3 * D * ap[s + 1]].reshape(D, -1, 3)
+        scale = np.abs(blk).max() + 1e-30
+        assert np.abs(blk.sum(axis=1)).max() / scale < 1e-4
+
+
+def test_loss_grad_matches_oracle(pk, dev, oracle_port):
+    batch = cases.with_heads(cases.molecules(pk, 40, 13), cases.CFG[4], seed=1)
+    batch["energy_mask"][::3] = 0
+    batch["force_mask"][::4] = 0
+    params = oracle_port.init_params(cases.CFG, 5)
+    dev.set_params(params)
+    dev.set_reference_table(None)
+    dev.set_batch(batch)
+    bd, ge, gf = dev.masked_loss_grad()
+    pe, pf = oracle_port.forward(cases.CFG, params, batch)
+    rbd, rge, rgf = oracle_port.loss_grad(batch, cases.CFG[4], pe, pf)
+    for k in ("total", "energy_term", "force_term"):
+        assert abs(bd[k] - rbd[k]) <= TOL * max(abs(rbd[k]), 1e-12), k
+    assert bd["energy_labeled"] == rbd["energy_labeled"] and bd["force_labeled"] == rbd["force_labeled"]
+    assert np.array_equal(np.sign(ge), np.sign(rge))
+    assert_close(ge, rge, what="dL/dE")
+    assert_close(gf, rgf, what="dL/dF")
+
+
+def test_backward_general_upstream(pk, dev, oracle_port):
+    batch = cases.molecules(pk, 24, 14)
+    params = oracle_port.init_params(cases.CFG, 9)
+    rng = np.random.default_rng(3)
+    ap = batch["atom_ptr"]
+    up_e = rng.normal(size=(len(ap) - 1, cases.CFG[4]))
+    up_f = rng.normal(size=3 * cases.CFG[4] * int(ap[-1]))
+    dev.set_params(params)
+    dev.set_batch(batch)
+    g = dev.backward(up_e, up_f)
+    rg = oracle_port.backward(cases.CFG, params, batch, up_e, up_f)
+    for name, t in tensors(cases.CFG, g).items():
+        assert_close(t, tensors(cases.CFG, rg)[name], what=f"d/d{name}")
+
+
+def test_backward_accumulates(pk, dev, oracle_port):
+    batch = cases.molecules(pk, 8, 15)
+    dev.set_batch(batch)
+    rng = np.random.default_rng(4)
+    ue = rng.normal(size=(8, cases.CFG[4]))
+    uf = rng.normal(size=3 * cases.CFG[4] * int(batch["atom_ptr"][-1]))
+    g1 = dev.backward(ue, uf)
+    g2 = dev.backward(ue, uf, grads=g1.copy())
+    assert np.allclose(g2, 2 * g1, rtol=1e-6, atol=1e-12)
+    zero = dev.backward(np.zeros_like(ue), np.zeros_like(uf))
+    assert not np.any(zero)  # SPEC: zero loss gradient in -> zero parameter gradient out
+
+
+def _train_cfg(pk, **kw):
+    return pk.TrainConfig(seed=kw.pop("seed", 17), **kw)
+
+
+def test_train_step_matches_oracle(pk, oracle_ref):
+    """One full step (denoise -> normalize -> fwd -> per-rank loss -> bwd -> /G -> clip -> RMS)."""
+    mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
+    dev = pk.Device(mcfg, seed=0)
+    params = oracle_ref.init_params(cases.CFG, 21)
+    batch = cases.mixed_batch(pk, D=cases.CFG[4], seed=5, count=24)
+    table = cases.random_table(cases.CFG[4], seed=2)
+    tc = _train_cfg(pk, clip_norm=1e9)
+    v0 = np.zeros_like(params)
+    ref = oracle_ref.train_step(cases.CFG, 1, 24, batch, table, params, v0, noise_sigma=tc.noise_sigma,
+                                noise_scheme=1, seed=tc.seed, step=3, clip=tc.clip_norm)
+    dev.set_params(params)
+    dev.set_rms_state(v0)
+    dev.set_reference_table(table)
+    res = dev.train_step(batch, tc, step=3, workers=1, rank=0)
+    assert abs(res.loss - ref["loss"]) <= TOL * abs(ref["loss"])
+    assert abs(res.grad_norm - ref["grad_norm"]) <= TOL * ref["grad_norm"]
+    g = dev.grads()
+    for name, t in tensors(cases.CFG, g).items():
+        assert_close(t, tensors(cases.CFG, ref["grads"])[name], what=f"step d/d{name}")
+    # RMS state after one step from v=0 is 0.01 g^2: relative parity of g^2
+    assert_close(dev.rms_state(), ref["rms_v"], tol=3 * TOL, what="rms v")
+    dev.close()
+
+
+def test_denoise_labels_match_reference(pk, oracle_ref):
+    mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
+    dev = pk.Device(mcfg, seed=0)
+    batch = cases.mixed_batch(pk, D=cases.CFG[4], seed=8, count=12)
+    table = cases.random_table(cases.CFG[4], seed=3)
+    dev.set_reference_table(table)
+    tc = _train_cfg(pk)
+    B, G, rank, step = 12, 3, 2, 5
+    dev.train_step(batch, tc, step=step, workers=G, rank=rank)
+    # worker-major position of sample b on rank r is r*B + b (S/trainer.cpp:268)
+    e_dev, f_dev = dev.labels()
+    ap = batch["atom_ptr"]
+    for s in np.nonzero(batch["denoise"])[0]:
+        seed = oracle_ref.mix_seed(oracle_ref.mix_seed(tc.seed, 0x4e4f4953 + step), rank * B + s)
+        noisy, lab = oracle_ref.apply_noise(batch["pos"][ap[s]:ap[s + 1]], batch["Z"][ap[s]:ap[s + 1]], 0.3, 1, seed)
+        d = batch["dataset_index"][s]
+        assert np.array_equal(f_dev[ap[s]:ap[s + 1]], (1.0 / table["fstd"][d]) * lab), f"denoise labels {s}"
+    dev.close()
+
+
+def test_optimizer_bit_exact(pk, dev, oracle_ref):
+    rng = np.random.default_rng(6)
+    params = oracle_ref.init_params(cases.CFG, 4)
+    v = rng.uniform(0, 1e-3, len(params))
+    g = rng.normal(size=len(params)) * 1e-2
+    tc = pk.TrainConfig(clip_norm=1e9)
+    dev.set_params(params)
+    dev.set_rms_state(v)
+    dev.optimizer_step(g * 2, 2, tc)  # worker-summed grads, G = 2
+    gs = g * 2 * (1.0 / 2)
+    vv = 0.99 * v + (1.0 - 0.99) * gs * gs
+    pp = params - 1e-3 * gs / (np.sqrt(vv) + 1e-8)
+    assert np.array_equal(dev.rms_state().view(np.uint64), vv.view(np.uint64))
+    assert np.array_equal(dev.params().view(np.uint64), pp.view(np.uint64))
+
+
+def test_train_step_deterministic(pk):
+    mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
+    batch = cases.mixed_batch(pk, D=cases.CFG[4], seed=9, count=32)
+    table = cases.random_table(cases.CFG[4], seed=1)
+    outs = []
+    for _ in range(2):
+        dev = pk.Device(mcfg, seed=3)
+        dev.set_reference_table(table)
+        for step in range(3):
+            dev.train_step(batch, _train_cfg(pk), step=step)
+        outs.append(dev.params())
+        dev.close()
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_multi_worker_sum_semantics(pk, oracle_ref):
+    """G simulated workers: per-rank loss/grad on one GPU == the reference's G-worker step."""
+    G, B = 2, 8
+    mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
+    params = oracle_ref.init_params(cases.CFG, 2)
+    batch = cases.mixed_batch(pk, D=cases.CFG[4], seed=12, count=G * B)
+    table = cases.random_table(cases.CFG[4], seed=4)
+    tc = _train_cfg(pk, clip_norm=1e9)
+    ref = oracle_ref.train_step(cases.CFG, G, B, batch, table, params, np.zeros_like(params), seed=tc.seed,
+                                step=1, clip=tc.clip_norm)
+    gsum = np.zeros_like(params)
+    loss = 0.0
+    for r in range(G):
+        dev = pk.Device(mcfg, seed=0)
+        dev.set_params(params)
+        dev.set_reference_table(table)
+        shard = pk.select(batch, np.arange(r * B, (r + 1) * B))
+        res = dev.train_step(shard, tc, step=1, workers=G, rank=r)
+        gsum += dev.grads()
+        loss += res.local["total"]
+        dev.close()
+    assert abs(loss / G - ref["loss"]) <= TOL * abs(ref["loss"])
+    assert_close(gsum / G, ref["grads"], what="G-worker mean gradient")
+    assert rel_err(gsum / G, ref["grads"])[0] < TOL
