@@ -1,0 +1,432 @@
+#!/usr/bin/env python3
+"""Throughput of the load-balanced LaMM energy/force train step on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], "cfg2"): per rank a device-batch of 256
+synthetic organic molecules (reference generator, lognormal mode 20 sigma 0.5,
+5-60 atoms, elements H/C/N/O, Morse labels), model ModelConfig{hidden 128,
+layers 3, rbf 16, cutoff 5 A, heads 10} (the reference's model family at the
+north star's PaiNN size), scheduled by the balanced plan (G = N workers, B = 256,
+S = 16). One step = denoise/normalize -> neighbour list -> forward -> Eq.(5)
+loss -> backward -> NCCL allreduce (N > 1) -> clip -> RMS update.
+
+value  : atoms/s over all ranks with inputs resident in HBM (staged slots),
+         device time (CUDA events around each step, L2 flushed between steps,
+         max over ranks).
+e2e    : same metric through the public API lamm_train_step with host
+         batches: host packing, H2D, the step, D2H of the result, per step.
+Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "atoms/sec per train step"
+CFG = dict(hidden=128, layers=3, rbf=16, cutoff=5.0, heads=10)
+BATCH_PER_GPU = 256
+EPOCH_STEPS = 8
+SPLITS = 16
+GEN = dict(mode=20.0, sigma=0.5, min_atoms=5, max_atoms=60, elements=(1, 6, 7, 8))
+L2_FLUSH = 256 << 20
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ------------------------------------------------------------ distributed
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as td
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            td.init_process_group("gloo", rank=self.rank, world_size=self.world)
+            self.td = td
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def allreduce(self, x: float, op: str) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX if op == "max" else self.td.ReduceOp.SUM)
+        return float(t.item())
+
+    def bcast_bytes(self, b: bytes | None) -> bytes:
+        if self.world == 1:
+            return b
+        obj = [b]
+        self.td.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def close(self):
+        if self.world > 1:
+            self.td.destroy_process_group()
+
+
+# ------------------------------------------------------------ workload
+def make_workload(pk, world: int, seed: int = 42):
+    """The pool, its reference table and the balanced schedule (identical on all ranks)."""
+    pool_n = BATCH_PER_GPU * world * EPOCH_STEPS
+    pool = pk.synth_generate(pool_n, seed, threads=os.cpu_count() or 8, **GEN)
+    atoms = np.diff(pool["atom_ptr"])
+    sched = pk.plan(atoms, world, BATCH_PER_GPU, SPLITS, seed=7, mode="balanced")
+    return pool, fit_table(pool, CFG["heads"]), sched
+
+
+def fit_table(pool, D):
+    """Setup-only stand-in for fit_normalizer (S/loss.cpp:64-111): least-squares
+    per-element reference energies, residual mean/std, force std; head 0."""
+    ap, Z = pool["atom_ptr"], pool["Z"]
+    B = len(ap) - 1
+    comp = np.zeros((B, 119))
+    np.add.at(comp, (np.repeat(np.arange(B), np.diff(ap)), Z), 1.0)
+    cols = np.nonzero(comp.sum(0))[0]
+    rho_c, *_ = np.linalg.lstsq(comp[:, cols], pool["energy"], rcond=None)
+    t = dict(rho=np.zeros((D, 119)), rho_has=np.zeros((D, 119), np.uint8), mean=np.zeros(D), std=np.ones(D),
+             fstd=np.ones(D), has=np.ones(D, np.uint8))
+    t["rho"][0, cols] = rho_c
+    t["rho_has"][0, cols] = 1
+    resid = pool["energy"] - comp[:, cols] @ rho_c
+    t["mean"][0] = resid.mean()
+    t["std"][0] = max(resid.std(), 1e-8)
+    t["fstd"][0] = max(pool["forces"].std(), 1e-8)
+    return t
+
+
+def shard(pk, pool, sched, step, rank, world):
+    per = BATCH_PER_GPU * world
+    ids = sched["sample"][step * per:(step + 1) * per][rank * BATCH_PER_GPU:(rank + 1) * BATCH_PER_GPU]
+    return pk.select(pool, ids)
+
+
+# ------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(self.rows[0][1]),
+                "samples": len(self.rows), "reasons": reasons}
+
+
+# ------------------------------------------------------------ roofline
+def kernel_bytes(name, N, P, H=128, K=16, D=10):
+    """Algorithmic (compulsory, gather-inclusive) HBM-side bytes per launch, fp32
+    storage, from the data each kernel must touch."""
+    e = {
+        "message": P * (4 + 4 + 4 * K + 4 * H) + N * (8 + 4 * H),
+        "bwd_edge": P * (4 + 4 + 4 * K + 8 * H) + N * (8 + 16 * H),
+        "force": P * (4 + 16 + 4 * K + 4 * H + 4 * D) + N * (8 + 4 * H + 4 * D + 12 * D),
+        "head_bwd": P * (4 + 16 + 12 + 4 * H + 4 * K) + N * (8 + 4 * H + 12 + 8 * H + 4 * (H + K + 4)),
+        "update": N * (4 * H + 4 * H + 8 * H) + 4 * H * H,
+        "bwd_gemm": N * (8 * H + 4 * H) + 4 * H * H,
+    }
+    return e.get(name)
+
+
+def kernel_flops(name, N, P, H=128, K=16, D=10):
+    return {"update": 2 * N * H * H, "bwd_gemm": 4 * N * H * H, "message": P * (2 * H * K + 3 * H),
+            "bwd_edge": P * (4 * H * K + 6 * H)}.get(name)
+
+
+# ------------------------------------------------------------ arms
+def run_ours(args, dist):
+    import paper_2505_22208_b200 as pk
+
+    if dist.world > 1:
+        os.environ.setdefault("CUDA_VISIBLE_DEVICES", os.environ.get("CUDA_VISIBLE_DEVICES", ""))
+    gpu = dist.local_rank
+    pool, table, sched = make_workload(pk, dist.world)
+    mcfg = pk.ModelConfig(**CFG)
+    dev = pk.Device(mcfg, device=gpu, seed=7)
+    if dist.world > 1:
+        uid = dist.bcast_bytes(pk.comm_unique_id() if dist.rank == 0 else None)
+        dev.comm_init(dist.world, dist.rank, uid)
+    dev.set_reference_table(table)
+    tc = pk.TrainConfig(seed=11)
+    n_steps = sched["n_batches"]
+    shards = [shard(pk, pool, sched, s, dist.rank, dist.world) for s in range(n_steps)]
+    for s, b in enumerate(shards):
+        dev.stage(b, tc, step=s, slot=s, workers=dist.world, rank=dist.rank)
+    dev.set_option("profile", 1)
+    # clocks are sampled from the start of the warm-up through the timed region
+    clk = ClockSampler(gpu).__enter__()
+    # warm-up: every slot once (grows all capacities, captures the graph), then W more
+    for k in range(max(args.warmup, 0) + n_steps):
+        dev.train_step_staged(k % n_steps, sync=True)
+    dev.kernel_times_reset()
+    anomalies0 = dev.anomalies()
+    # ---- timed region (device-resident inputs)
+    # Each step is bracketed by CUDA events on the ctx stream inside the library
+    # (upload -> step -> allreduce -> optimizer); the L2 flush and the result
+    # read-back sit outside the brackets.
+    K = args.steps
+    atoms_local = 0
+    dist.barrier()
+    dev.sync()
+    for k in range(K):
+        s = k % n_steps
+        dev.flush_l2(L2_FLUSH)
+        r = dev.train_step_staged(s, sync=True)
+        atoms_local += r.n_atoms
+    clk.__exit__(None, None, None)
+    dist.barrier()
+    dev_ms, nsteps = dev.step_times()
+    assert nsteps == K, (nsteps, K)
+    launches = dev.last_step_launches() * K
+    assert dev.anomalies() == anomalies0, "a timed step skipped its update (capacity overflow or non-finite)"
+    ktimes = dev.kernel_times()
+    ms_max = dist.allreduce(dev_ms, "max")
+    atoms_all = dist.allreduce(float(atoms_local), "sum")
+    value = atoms_all / (ms_max / 1e3)
+    # per-step edges for the roofline (one synced pass over the slots)
+    dev.set_option("profile", 0)
+    edge_counts = []
+    for s in range(n_steps):
+        r = dev.train_step_staged(s, sync=True)
+        edge_counts.append(r.n_edges)
+    # ---- e2e: public API with host batches (H2D + step + D2H per step)
+    e2e_s, h2d, d2h, e2e_atoms = 0.0, 0, 0, 0
+    dist.barrier()
+    for k in range(K):
+        s = k % n_steps
+        dev.flush_l2(L2_FLUSH)
+        dev.sync()
+        t0 = time.perf_counter()
+        r = dev.train_step(shards[s], tc, step=s, workers=dist.world, rank=dist.rank)
+        e2e_s += time.perf_counter() - t0
+        h2d += r.h2d_bytes
+        d2h += r.d2h_bytes
+        e2e_atoms += r.n_atoms
+    e2e_max = dist.allreduce(e2e_s, "max")
+    e2e_atoms_all = dist.allreduce(float(e2e_atoms), "sum")
+    e2e = e2e_atoms_all / e2e_max
+    # ---- roofline of the dominant kernel
+    hbm, tflops, src = peaks()
+    steps_done = K
+    N_mean = atoms_local / K
+    P_mean = float(np.mean([edge_counts[k % n_steps] for k in range(K)]))
+    tot_ms = sum(v[0] for v in ktimes.values())
+    top = max(ktimes.items(), key=lambda kv: kv[1][0]) if ktimes else ("none", (0.0, 1))
+    tname, (tms, tcount) = top
+    per_launch_ms = tms / max(tcount, 1)
+    launches_per_step = tcount / steps_done
+    byts = kernel_bytes(tname, N_mean, P_mean)
+    roof = {"kernel": tname, "bound": "hbm", "unit": "GB/s", "peak": hbm, "peak_source": src,
+            "share_of_step": tms / tot_ms if tot_ms else None, "avg_launch_us": per_launch_ms * 1e3,
+            "launches_per_step": launches_per_step}
+    if byts is not None:
+        ach = byts / (per_launch_ms / 1e3) / 1e9
+        roof.update(achieved=ach, frac=ach / hbm, traffic=None, algorithmic_bytes_per_launch=byts)
+    fl = kernel_flops(tname, N_mean, P_mean)
+    if fl is not None:
+        roof["fp32_flops_per_launch"] = fl
+    kern = {k: {"ms_per_step": v[0] / steps_done, "launches_per_step": v[1] / steps_done,
+                "share": v[0] / tot_ms if tot_ms else None} for k, v in sorted(ktimes.items(), key=lambda kv: -kv[1][0])}
+    out = {
+        "metric": METRIC, "value": value, "unit": "atoms/s", "n_gpus": dist.world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 (fp64 neighbour list/optimizer)", "data": "synthetic",
+        "config": {"workload": "cfg2: mixed organic molecules 5-60 atoms, batch 256 per GPU, non-periodic",
+                   "model": "LaMM MPNN hidden128 layers3 rbf16 cutoff5 heads10 (74,400 params)",
+                   "global_batch": BATCH_PER_GPU * dist.world, "atoms_per_step_per_gpu": N_mean,
+                   "edges_per_step_per_gpu": P_mean, "parallelism": f"dp{dist.world}",
+                   "schedule": "balanced (G=%d, B=%d, S=%d)" % (dist.world, BATCH_PER_GPU, SPLITS),
+                   "l2": "flushed between timed steps (256 MiB memset outside the events)",
+                   "inputs": "value: device-resident staged batches; e2e: host batches via lamm_train_step"},
+        "e2e": {"value": e2e, "unit": "atoms/s", "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
+                "ms_per_step": e2e_max / K * 1e3},
+        "gpu_launches": launches,
+        "roofline": roof,
+        "kernels": kern,
+        "clocks": clk.summary(),
+    }
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(shards[0], table, mcfg, budget_s=args.cpu_budget)
+    if dist.rank == 0 and dist.world == 1 and not args.no_imbalance:
+        out["rank_imbalance"] = rank_imbalance(pk, dev, pool, table, tc)
+    dev.close()
+    return out
+
+
+def cpu_baseline(batch, table, mcfg, budget_s=15.0, sample=64):
+    """The reference's own step (oracle/_ref, all host threads) on a bounded sample."""
+    import oracle
+    lib = oracle.ref() if oracle.ref_available() else oracle.port()
+    import paper_2505_22208_b200 as pk
+    sub = pk.select(batch, np.arange(min(sample, len(batch["atom_ptr"]) - 1)))
+    cfg = mcfg.astuple()
+    params = lib.init_params(cfg, 7)
+    v = np.zeros_like(params)
+    threads = os.cpu_count() or 1
+    n = len(sub["atom_ptr"]) - 1
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        r = lib.train_step(cfg, 1, n, sub, table, params, v, seed=11, step=reps, threads=threads) \
+            if lib.kind == "ref" else lib.train_step(cfg, 1, n, sub, table, params, v, seed=11, step=reps)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el > budget_s or reps >= 50:
+            break
+    atoms = int(sub["atom_ptr"][-1]) * reps
+    return {"value": atoms / el, "unit": "atoms/s", "cores": threads if lib.kind == "ref" else 1,
+            "kind": "reference" if lib.kind == "ref" else "port",
+            "sample": f"{reps} step(s) of the first {n} molecules of the step-0 batch ({int(sub['atom_ptr'][-1])} "
+                      f"atoms), oracle/_ref lref_train_step (S/trainer.cpp:258-327), {el:.1f} s"}
+
+
+def rank_imbalance(pk, dev, pool, table, tc, G=8, steps=8):
+    """Per-rank step time on the one GPU: each of G ranks' shards timed as its own
+    device-batch (B = 256/G) for the balanced and naive plans; max/mean per step."""
+    out = {"G": G, "batch_per_rank": BATCH_PER_GPU // G}
+    atoms = np.diff(pool["atom_ptr"])
+    for mode in ("balanced", "naive"):
+        sched = pk.plan(atoms, G, BATCH_PER_GPU // G, SPLITS, seed=7, mode=mode)
+        ratios, aratios = [], []
+        per = BATCH_PER_GPU
+        for s in range(min(steps, sched["n_batches"])):
+            ids = sched["sample"][s * per:(s + 1) * per]
+            times = []
+            for g in range(G):
+                sub = pk.select(pool, ids[g * (per // G):(g + 1) * (per // G)])
+                dev.stage(sub, tc, step=s, slot=900 + g, workers=G, rank=g)
+                dev.train_step_staged(900 + g, sync=True)  # warm capacity
+                ms = []
+                for rep in range(3):
+                    dev.event_record(0)
+                    dev.train_step_staged(900 + g, sync=False)
+                    dev.event_record(1)
+                    ms.append(dev.event_elapsed_ms(0, 1))
+                times.append(min(ms))
+            ratios.append(max(times) / np.mean(times))
+            wa = sched["worker_atoms"][s * G:(s + 1) * G]
+            aratios.append(wa.max() / wa.mean())
+        out[mode] = {"time_mean": float(np.mean(ratios)), "time_p95": float(np.percentile(ratios, 95)),
+                     "atoms_mean": float(np.mean(aratios)), "atoms_max": float(np.max(aratios)),
+                     "steps": len(ratios)}
+    return out
+
+
+def run_reference(args, dist):
+    """--impl reference: the reference's own CPU step (oracle/_ref) on this box's
+    host cores, same metric/config, each step a bounded sample of the batch."""
+    if dist.rank != 0:
+        return None
+    import oracle
+    import paper_2505_22208_b200 as pk
+    lib = oracle.ref() if oracle.ref_available() else oracle.port()
+    pool, table, sched = make_workload(pk, 1)
+    cfg = tuple(CFG[k] for k in ("hidden", "layers", "rbf", "cutoff", "heads"))
+    params = lib.init_params(cfg, 7)
+    v = np.zeros_like(params)
+    threads = os.cpu_count() or 1
+    sample = args.ref_sample
+    total_atoms, total_s = 0, 0.0
+    for k in range(args.warmup + args.steps):
+        b = shard(pk, pool, sched, k % sched["n_batches"], 0, 1)
+        sub = pk.select(b, np.arange(sample))
+        t0 = time.perf_counter()
+        kw = dict(threads=threads) if lib.kind == "ref" else {}
+        r = lib.train_step(cfg, 1, sample, sub, table, params, v, seed=11, step=k, **kw)
+        el = time.perf_counter() - t0
+        params, v = r["params"], r["rms_v"]
+        if k >= args.warmup:
+            total_atoms += int(sub["atom_ptr"][-1])
+            total_s += el
+    value = total_atoms / total_s
+    kind = "reference" if lib.kind == "ref" else "port"
+    desc = (f"{sample} of the 256 molecules of each cfg2 step, {args.steps} timed steps, "
+            f"{'oracle/_ref lref_train_step' if kind == 'reference' else 'oracle port'} with {threads} threads")
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "atoms/s", "n_gpus": dist.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_s / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "cfg2: mixed organic molecules 5-60 atoms, batch 256 per GPU, non-periodic",
+                       "model": "LaMM MPNN hidden128 layers3 rbf16 cutoff5 heads10", "parallelism": "host threads"},
+            "cpu_baseline": {"value": value, "unit": "atoms/s", "cores": threads if kind == "reference" else 1,
+                             "kind": kind, "sample": desc},
+            "e2e": {"value": value, "unit": "atoms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-imbalance", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--ref-sample", type=int, default=64)
+    args = ap.parse_args()
+    dist = Dist()
+    try:
+        out = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)
+        if out is not None and dist.rank == 0:
+            print(json.dumps(out), flush=True)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

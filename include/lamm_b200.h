@@ -125,6 +125,8 @@ typedef struct {
     int64_t n_edges;      /* directed pairs built for it */
     int32_t status;       /* lamm_status of the step */
     int32_t retries;      /* edge-capacity regrowth re-runs */
+    int64_t h2d_bytes;    /* bytes copied host -> device for this step */
+    int64_t d2h_bytes;    /* bytes copied device -> host for this step's result */
 } lamm_step_result;
 
 /* ------------------------------------------------------------ context --- */
@@ -199,6 +201,21 @@ int lamm_comm_init(lamm_ctx* ctx, int nranks, int rank, const void* unique_id128
 int lamm_train_step(lamm_ctx* ctx, const lamm_batch_view* batch, const lamm_train_config* cfg, int64_t step,
                     int32_t workers, int32_t rank, lamm_step_result* result);
 
+/* Device-resident staging for throughput runs: packs a device-batch exactly as
+ * lamm_train_step would (denoise draws for `step`, `rank`) into HBM slot
+ * `slot` (0..1023); lamm_train_step_staged then runs the same step from that
+ * slot (device-to-device copy + graph) with no host work. sync = 0 returns
+ * without waiting (result may be NULL); errors are then counted on the device
+ * and reported by lamm_anomalies. */
+int lamm_stage(lamm_ctx* ctx, const lamm_batch_view* batch, const lamm_train_config* cfg, int64_t step,
+               int32_t workers, int32_t rank, int32_t slot);
+int lamm_train_step_staged(lamm_ctx* ctx, int32_t slot, int32_t sync, lamm_step_result* result);
+/* Steps since context creation whose update was skipped (non-finite or edge
+ * capacity overflow). */
+int64_t lamm_anomalies(lamm_ctx* ctx);
+/* Writes `bytes` of scratch on the ctx stream to evict L2 between timed steps. */
+int lamm_flush_l2(lamm_ctx* ctx, int64_t bytes);
+
 /* RmsOptimizer::step (S/trainer.cpp:37-53) after scale/norm/clip
  * (S/trainer.cpp:319-326) applied to a host fp64 worker-summed gradient. */
 int lamm_optimizer_step(lamm_ctx* ctx, const double* grad_sum, int32_t workers, const lamm_train_config* cfg,
@@ -215,6 +232,10 @@ int lamm_event_elapsed_ms(lamm_ctx* ctx, int slot_a, int slot_b, float* ms);
 int lamm_kernel_times(lamm_ctx* ctx, int max_kernels, const char** names, double* total_ms, int64_t* launches,
                       int* n_kernels);
 int lamm_kernel_times_reset(lamm_ctx* ctx);
+/* Device time of every synced train step since the last reset, from CUDA events
+ * on the ctx stream around upload -> step -> optimizer (the result D2H and any
+ * host work excluded). Reset by lamm_kernel_times_reset. */
+int lamm_step_times(lamm_ctx* ctx, double* total_ms, int64_t* steps);
 /* Number of this library's kernel launches issued by the last train step. */
 int64_t lamm_last_step_launches(lamm_ctx* ctx);
 

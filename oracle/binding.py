@@ -224,6 +224,24 @@ class OracleLib:
             self._check(st)
         return dict(params=p, rms_v=v, loss=loss.value, grad_norm=gn.value, grads=g, status=st)
 
+    def worker_step(self, cfg, G, B, g, batch, table, params, *, noise_sigma=0.3, noise_scheme=1, seed=0, step=0,
+                    lambda_e=1.0, lambda_f=1.0):
+        """Worker g's loss and gradient SUM (port only): one term of the step body."""
+        if self.kind != "port":
+            raise OracleError("worker_step is provided by the plain-C port only")
+        H, L, K, rc, D = cfg
+        keep = [_c(batch[k], dt) for k, dt in (("atom_ptr", np.int64), ("pos", np.float64), ("Z", np.int32),
+                                               ("dataset_index", np.int32), ("energy_mask", np.uint8),
+                                               ("force_mask", np.uint8), ("energy", np.float64),
+                                               ("forces", np.float64), ("denoise", np.uint8))]
+        loss = _f64()
+        g_out = np.empty(self.param_count(cfg))
+        self._check(self.lib.lor_worker_step(H, L, K, _f64(rc), D, G, B, g, *[_p(k) for k in keep],
+                                             *self._table_args(table), _f64(noise_sigma), noise_scheme, _u64(seed),
+                                             _i64(step), _f64(lambda_e), _f64(lambda_f),
+                                             _p(_c(params, np.float64)), C.byref(loss), _p(g_out)))
+        return loss.value, g_out
+
     # ---------------------------------------------------------- scheduler
     def greedy_assign(self, atoms, G, B):
         a = _c(atoms, np.int64)

@@ -61,7 +61,8 @@ class TrainConfigC(C.Structure):
 
 class StepResultC(C.Structure):
     _fields_ = [("loss", C.c_double), ("grad_norm", C.c_double), ("local", LossBreakdownC),
-                ("n_atoms", C.c_int64), ("n_edges", C.c_int64), ("status", C.c_int32), ("retries", C.c_int32)]
+                ("n_atoms", C.c_int64), ("n_edges", C.c_int64), ("status", C.c_int32), ("retries", C.c_int32),
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
 
 
 # Every symbol include/lamm_b200.h declares (tests check the export table).
@@ -74,7 +75,8 @@ EXPORTS = [
     "lamm_event_record", "lamm_event_elapsed_ms", "lamm_kernel_times", "lamm_kernel_times_reset",
     "lamm_last_step_launches", "lamm_greedy_assign", "lamm_plan", "lamm_schedule_metrics", "lamm_make_trace",
     "lamm_temperature_counts", "lamm_build_epoch_index", "lamm_synth_counts", "lamm_synth_fill",
-    "lamm_mix_seed", "lamm_rng_normals",
+    "lamm_mix_seed", "lamm_rng_normals", "lamm_stage", "lamm_train_step_staged", "lamm_anomalies",
+    "lamm_flush_l2", "lamm_step_times",
 ]
 
 _lib = None
@@ -93,6 +95,7 @@ def lib() -> C.CDLL:
         L.lamm_mix_seed.restype = C.c_uint64
         L.lamm_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
         L.lamm_last_step_launches.restype = C.c_int64
+        L.lamm_anomalies.restype = C.c_int64
         L.lamm_ctx_destroy.restype = None
         L.lamm_ctx_create.argtypes = [C.c_int, C.POINTER(ModelConfigC), C.POINTER(C.c_void_p)]
         for fn in ("lamm_ctx_destroy",):

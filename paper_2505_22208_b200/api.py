@@ -132,6 +132,8 @@ class StepResult:
     n_atoms: int
     n_edges: int
     status: int
+    h2d_bytes: int = 0
+    d2h_bytes: int = 0
 
 
 def _breakdown(b: LossBreakdownC) -> dict:
@@ -269,7 +271,29 @@ class Device:
         self.B = len(keep["atom_ptr"]) - 1
         self.N = int(keep["atom_ptr"][-1])
         check(st)
+        return StepResult(res.loss, res.grad_norm, _breakdown(res.local), res.n_atoms, res.n_edges, res.status,
+                          res.h2d_bytes, res.d2h_bytes)
+
+    def stage(self, batch: dict, tcfg: TrainConfig, step: int, slot: int, workers: int = 1, rank: int = 0) -> int:
+        """Packs a device-batch into HBM slot ``slot`` (inputs resident for timing);
+        returns the staged blob size in bytes."""
+        v, keep = _batch_view(batch)
+        tc = tcfg.c()
+        check(lib().lamm_stage(self._h, C.byref(v), C.byref(tc), C.c_int64(step), workers, rank, slot))
+        return int(keep["atom_ptr"][-1])
+
+    def train_step_staged(self, slot: int, sync: bool = True) -> StepResult | None:
+        res = StepResultC()
+        check(lib().lamm_train_step_staged(self._h, slot, 1 if sync else 0, C.byref(res) if sync else None))
+        if not sync:
+            return None
         return StepResult(res.loss, res.grad_norm, _breakdown(res.local), res.n_atoms, res.n_edges, res.status)
+
+    def anomalies(self) -> int:
+        return int(lib().lamm_anomalies(self._h))
+
+    def flush_l2(self, nbytes: int = 256 << 20):
+        check(lib().lamm_flush_l2(self._h, C.c_int64(nbytes)))
 
     def optimizer_step(self, grad_sum, workers: int, tcfg: TrainConfig) -> float:
         g = _c(grad_sum, np.float64)
@@ -299,6 +323,12 @@ class Device:
         cnt = np.zeros(max(k, 1), np.int64)
         check(lib().lamm_kernel_times(self._h, k, names, _p(ms), _p(cnt), C.byref(n)))
         return {names[i].decode(): (float(ms[i]), int(cnt[i])) for i in range(k)}
+
+    def step_times(self):
+        """(total device ms, steps) of the synced train steps since the last reset."""
+        ms, n = C.c_double(), C.c_int64()
+        check(lib().lamm_step_times(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def kernel_times_reset(self):
         check(lib().lamm_kernel_times_reset(self._h))

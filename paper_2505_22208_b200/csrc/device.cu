@@ -115,6 +115,16 @@ struct lamm_ctx {
     int denoise_scheme = 1;
     double opt_inv_g = 1.0, opt_lr = 0, opt_decay = 0, opt_eps = 0, opt_clip = 0;
     int opt_G = 1;
+    // device-resident staged batches (lamm_stage)
+    struct Slot {
+        lamm_b200::Buf blob;
+        size_t bytes = 0;
+        int32_t B = 0;
+        int64_t N = 0;
+        int me = 0, mf = 0;
+    };
+    std::vector<Slot> staged;
+    lamm_b200::Buf anomaly, flush;
     // NCCL
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
@@ -124,6 +134,12 @@ struct lamm_ctx {
     size_t slot_cursor = 0;
     std::map<std::string, std::pair<double, int64_t>> ktimes;
     int64_t launches = 0, last_step_launches = 0, graph_launches = 0;
+    int flush_flip = 0;
+    cudaEvent_t step_ev[2] = {};
+    double step_ms_total = 0.0;
+    int64_t step_count = 0;
+    bool step_ev_pending = false;
+    int64_t last_h2d = 0;
 };
 
 namespace lamm_b200 {
@@ -155,6 +171,7 @@ void alloc_param_state(Ctx& c) {
     mk(c.tanh_emb, sizeof(float) * kMaxZ * c.H);
     mk(c.grads, sizeof(float) * (c.NP + 4));
     mk(c.block_scratch, sizeof(double) * 4096);
+    mk(c.anomaly, 256);
 }
 
 // Grows every batch-sized buffer to hold N atoms, B samples and P pairs.
@@ -285,6 +302,7 @@ Dev make_dev(Ctx& c) {
     d.p32 = c.p32.as<float>();
     d.NP = c.NP;
     d.emb_rows = kMaxZ;
+    d.anomaly = c.anomaly.as<unsigned int>();
     return d;
 }
 
@@ -582,6 +600,13 @@ StepHeader read_header(Ctx& c) {
     CK(cudaMemcpyAsync(c.h_result, c.d_stage.p, sizeof(StepHeader), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     collect_kernel_times(c);
+    if (c.step_ev_pending) {  // device time of the last step: upload -> optimizer, before the result D2H
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c.step_ev[0], c.step_ev[1]));
+        c.step_ms_total += ms;
+        ++c.step_count;
+        c.step_ev_pending = false;
+    }
     return *c.h_result;
 }
 
@@ -634,11 +659,14 @@ void step_body(Ctx& c) {
 
 void opt_body(Ctx& c) { c.ops->opt(c); }
 
-// One train step on the already-staged blob; returns the header after it.
-StepHeader run_train_step(Ctx& c, size_t bytes) {
+// One train step from a staged blob (pinned host blob: H2D; resident slot:
+// D2D); returns the header after it, or a zeroed header when !sync.
+StepHeader run_train_step(Ctx& c, const void* src, size_t bytes, cudaMemcpyKind kind, bool sync = true) {
     for (int attempt = 0;; ++attempt) {
         ensure_capacity(c, c.N, c.B, edge_guess(c.N));
-        CK(cudaMemcpyAsync(c.d_stage.p, c.h_stage, bytes, cudaMemcpyHostToDevice, c.stream));
+        if (bytes > c.d_stage.bytes) ensure_stage(c, bytes);
+        CK(cudaEventRecord(c.step_ev[0], c.stream));
+        CK(cudaMemcpyAsync(c.d_stage.p, src, bytes, kind, c.stream));
         const int64_t l0 = c.launches;
         if (c.use_graph) {
             if (c.graph_dirty || !c.g_step) {
@@ -660,7 +688,10 @@ StepHeader run_train_step(Ctx& c, size_t bytes) {
                        "ncclAllReduce");
         if (c.use_graph) CK(cudaGraphLaunch(c.g_opt, c.stream));
         else opt_body(c);
+        CK(cudaEventRecord(c.step_ev[1], c.stream));
+        c.step_ev_pending = true;
         c.last_step_launches = c.use_graph ? c.graph_launches : c.launches - l0;
+        if (!sync) return StepHeader{};
         const StepHeader h = read_header(c);
         if (h.status != 2) {
             c.batch_valid = c.nlist_valid = c.fwd_valid = c.loss_valid = true;
@@ -724,6 +755,7 @@ LAMM_API int lamm_ctx_create(int device, const lamm_model_config* cfg, lamm_ctx*
             CK(cudaMallocHost(reinterpret_cast<void**>(&c->h_result), sizeof(StepHeader)));
             ensure_stage(*c, 1 << 20);
             for (auto& e : c->ev) CK(cudaEventCreate(&e));
+            for (auto& e : c->step_ev) CK(cudaEventCreate(&e));
             ensure_capacity(*c, 1024, 64, 4096);
             // empty reference table buffers so the device pointers are valid
             bool ch = false;
@@ -744,11 +776,16 @@ LAMM_API void lamm_ctx_destroy(lamm_ctx* c) {
     if (c->comm) nccl().comm_destroy(c->comm);
     for (auto& kv : c->bufs)
         if (kv.second.p) cudaFree(kv.second.p);
-    for (Buf* b : {&c->p64, &c->v64, &c->g64, &c->p32, &c->tanh_emb, &c->grads, &c->block_scratch, &c->d_stage})
+    for (auto& s : c->staged)
+        if (s.blob.p) cudaFree(s.blob.p);
+    for (Buf* b : {&c->p64, &c->v64, &c->g64, &c->p32, &c->tanh_emb, &c->grads, &c->block_scratch, &c->d_stage,
+                   &c->anomaly, &c->flush})
         if (b->p) cudaFree(b->p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->h_result) cudaFreeHost(c->h_result);
     for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : c->step_ev)
         if (e) cudaEventDestroy(e);
     for (auto& s : c->slots) {
         if (s.a) cudaEventDestroy(s.a);
@@ -1091,49 +1128,121 @@ LAMM_API int lamm_comm_init(lamm_ctx* c, int nranks, int rank, const void* id128
     });
 }
 
+namespace lamm_b200 {
+void apply_train_config(Ctx& c, const lamm_train_config* tc, int32_t workers, int32_t rank) {
+    require(workers >= 1 && rank >= 0 && rank < workers, "train_step: bad worker layout");
+    require(workers == c.nranks || c.nranks == 1,
+            "train_step: workers must equal the communicator size (or 1 rank simulating)");
+    require(tc->learning_rate > 0.0, "train: learning_rate must be positive");
+    require(tc->clip_norm >= 0.0, "train: clip_norm must be >= 0");
+    require(tc->rms_decay >= 0.0 && tc->rms_decay < 1.0, "train: rms_decay must be in [0, 1)");
+    require(tc->rms_epsilon > 0.0, "train: rms_epsilon must be positive");
+    require(tc->lambda_energy >= 0.0 && tc->lambda_force >= 0.0, "train: lambdas must be >= 0");
+    if (c.denoise_scheme != (tc->noise_scheme ? 1 : 0)) {
+        c.denoise_scheme = tc->noise_scheme ? 1 : 0;
+        c.graph_dirty = true;
+    }
+    const double inv_g = 1.0 / static_cast<double>(workers);
+    if (c.opt_inv_g != inv_g || c.opt_lr != tc->learning_rate || c.opt_decay != tc->rms_decay ||
+        c.opt_eps != tc->rms_epsilon || c.opt_clip != tc->clip_norm || c.opt_G != workers) {
+        c.opt_inv_g = inv_g, c.opt_lr = tc->learning_rate, c.opt_decay = tc->rms_decay;
+        c.opt_eps = tc->rms_epsilon, c.opt_clip = tc->clip_norm, c.opt_G = workers;
+        c.graph_dirty = true;
+    }
+}
+
+void fill_result(Ctx& c, const StepHeader& h, lamm_step_result* res) {
+    if (!res) return;
+    res->loss = h.global_loss;
+    res->grad_norm = h.grad_norm;
+    res->local.total = h.loss_total;
+    res->local.energy_term = h.loss_energy;
+    res->local.force_term = h.loss_force;
+    res->local.energy_labeled = c.me;
+    res->local.force_labeled = c.mf;
+    res->local.energy_empty = c.me == 0;
+    res->local.force_empty = c.mf == 0;
+    res->n_atoms = c.N;
+    res->n_edges = h.P;
+    res->status = h.status == 1 ? LAMM_ENONFINITE : LAMM_OK;
+    res->retries = 0;
+    res->h2d_bytes = c.last_h2d;
+    res->d2h_bytes = static_cast<int64_t>(sizeof(StepHeader));
+}
+}  // namespace lamm_b200
+
+LAMM_API int lamm_stage(lamm_ctx* c, const lamm_batch_view* b, const lamm_train_config* tc, int64_t step,
+                        int32_t workers, int32_t rank, int32_t slot) {
+    return lamm_guard([&] {
+        require(c && b && tc, "stage: null argument");
+        require(slot >= 0 && slot < 1024, "stage: slot out of range");
+        CK(cudaSetDevice(c->device));
+        validate_batch(*c, b);
+        apply_train_config(*c, tc, workers, rank);
+        const size_t bytes = pack_batch(*c, b, true, tc, step, rank);
+        if (static_cast<size_t>(slot) >= c->staged.size()) c->staged.resize(slot + 1);
+        auto& s = c->staged[slot];
+        if (s.blob.bytes < bytes) {
+            if (s.blob.p) CK(cudaFree(s.blob.p));
+            CK(cudaMalloc(&s.blob.p, bytes));
+            s.blob.bytes = bytes;
+        }
+        CK(cudaMemcpyAsync(s.blob.p, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        s.bytes = bytes, s.B = c->B, s.N = c->N, s.me = c->me, s.mf = c->mf;
+        ensure_capacity(*c, c->N, c->B, edge_guess(c->N));
+    });
+}
+
+LAMM_API int lamm_train_step_staged(lamm_ctx* c, int32_t slot, int32_t sync, lamm_step_result* res) {
+    return lamm_guard([&] {
+        require(c != nullptr, "train_step_staged: null ctx");
+        require(slot >= 0 && static_cast<size_t>(slot) < c->staged.size() && c->staged[slot].bytes > 0,
+                "train_step_staged: empty slot");
+        CK(cudaSetDevice(c->device));
+        auto& s = c->staged[slot];
+        c->B = s.B, c->N = s.N, c->me = s.me, c->mf = s.mf;
+        c->batch_valid = false;  // the host mirror of per-atom arrays is not kept for staged batches
+        const StepHeader h = run_train_step(*c, s.blob.p, s.bytes, cudaMemcpyDeviceToDevice, sync != 0);
+        c->last_h2d = 0;
+        c->batch_valid = c->nlist_valid = c->fwd_valid = c->loss_valid = false;
+        if (!sync) return;
+        fill_result(*c, h, res);
+        if (h.status == 1) throw NonFinite("non-finite loss or gradient");
+    });
+}
+
+LAMM_API int64_t lamm_anomalies(lamm_ctx* c) {
+    if (!c) return -1;
+    unsigned int v = 0;
+    if (cudaMemcpy(&v, c->anomaly.p, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return v;
+}
+
+LAMM_API int lamm_flush_l2(lamm_ctx* c, int64_t bytes) {
+    return lamm_guard([&] {
+        require(c != nullptr && bytes > 0, "flush_l2: bad argument");
+        CK(cudaSetDevice(c->device));
+        if (c->flush.bytes < static_cast<size_t>(bytes)) {
+            if (c->flush.p) CK(cudaFree(c->flush.p));
+            CK(cudaMalloc(&c->flush.p, bytes));
+            c->flush.bytes = bytes;
+        }
+        CK(cudaMemsetAsync(c->flush.p, c->flush_flip ^= 1, bytes, c->stream));
+    });
+}
+
 LAMM_API int lamm_train_step(lamm_ctx* c, const lamm_batch_view* b, const lamm_train_config* tc, int64_t step,
                              int32_t workers, int32_t rank, lamm_step_result* res) {
     return lamm_guard([&] {
         require(c && b && tc, "train_step: null argument");
-        require(workers >= 1 && rank >= 0 && rank < workers, "train_step: bad worker layout");
-        require(workers == c->nranks || c->nranks == 1,
-                "train_step: workers must equal the communicator size (or 1 rank simulating)");
-        require(tc->learning_rate > 0.0, "train: learning_rate must be positive");
-        require(tc->clip_norm >= 0.0, "train: clip_norm must be >= 0");
-        require(tc->rms_decay >= 0.0 && tc->rms_decay < 1.0, "train: rms_decay must be in [0, 1)");
-        require(tc->rms_epsilon > 0.0, "train: rms_epsilon must be positive");
-        require(tc->lambda_energy >= 0.0 && tc->lambda_force >= 0.0, "train: lambdas must be >= 0");
         CK(cudaSetDevice(c->device));
         validate_batch(*c, b);
-        if (c->denoise_scheme != (tc->noise_scheme ? 1 : 0)) {
-            c->denoise_scheme = tc->noise_scheme ? 1 : 0;
-            c->graph_dirty = true;
-        }
+        apply_train_config(*c, tc, workers, rank);
         const size_t bytes = pack_batch(*c, b, true, tc, step, rank);
-        const double inv_g = 1.0 / static_cast<double>(workers);
-        if (c->opt_inv_g != inv_g || c->opt_lr != tc->learning_rate || c->opt_decay != tc->rms_decay ||
-            c->opt_eps != tc->rms_epsilon || c->opt_clip != tc->clip_norm || c->opt_G != workers) {
-            c->opt_inv_g = inv_g, c->opt_lr = tc->learning_rate, c->opt_decay = tc->rms_decay;
-            c->opt_eps = tc->rms_epsilon, c->opt_clip = tc->clip_norm, c->opt_G = workers;
-            c->graph_dirty = true;
-        }
-        int retries = 0;
-        const StepHeader h = run_train_step(*c, bytes);
-        if (res) {
-            res->loss = h.global_loss;
-            res->grad_norm = h.grad_norm;
-            res->local.total = h.loss_total;
-            res->local.energy_term = h.loss_energy;
-            res->local.force_term = h.loss_force;
-            res->local.energy_labeled = c->me;
-            res->local.force_labeled = c->mf;
-            res->local.energy_empty = c->me == 0;
-            res->local.force_empty = c->mf == 0;
-            res->n_atoms = c->N;
-            res->n_edges = h.P;
-            res->status = h.status == 1 ? LAMM_ENONFINITE : LAMM_OK;
-            res->retries = retries;
-        }
+        const StepHeader h = run_train_step(*c, c->h_stage, bytes, cudaMemcpyHostToDevice);
+        c->last_h2d = static_cast<int64_t>(bytes);
+        fill_result(*c, h, res);
         if (h.status == 1)
             throw NonFinite("non-finite loss or gradient at step " + std::to_string(step));
     });
@@ -1203,6 +1312,16 @@ LAMM_API int lamm_kernel_times_reset(lamm_ctx* c) {
     return lamm_guard([&] {
         require(c != nullptr, "kernel_times_reset: null ctx");
         c->ktimes.clear();
+        c->step_ms_total = 0.0;
+        c->step_count = 0;
+    });
+}
+
+LAMM_API int lamm_step_times(lamm_ctx* c, double* total_ms, int64_t* steps) {
+    return lamm_guard([&] {
+        require(c != nullptr, "step_times: null ctx");
+        if (total_ms) *total_ms = c->step_ms_total;
+        if (steps) *steps = c->step_count;
     });
 }
 

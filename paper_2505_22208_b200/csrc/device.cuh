@@ -111,6 +111,7 @@ struct Dev {
     float* tanh_emb_w;       // writable alias of tanh_emb
     int64_t NP;
     int32_t emb_rows;
+    unsigned int* anomaly;   // steps whose update was skipped
 };
 
 __device__ __forceinline__ float warp_sum(float v) {

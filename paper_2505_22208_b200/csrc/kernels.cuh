@@ -954,6 +954,7 @@ __global__ void __launch_bounds__(256) k_opt_norm(Dev d, int G, double inv_g, do
         d.hdr->global_loss = loss;
         const bool overflow = !d.g64_in && d.grads[d.NP + 2] > 0.f;
         d.hdr->status = overflow ? 2 : ((!isfinite(loss) || !isfinite(gn)) ? 1 : 0);
+        if (d.hdr->status != 0 && !d.g64_in) atomicAdd(d.anomaly, 1u);
         d.hdr->clip_scale = (clip > 0.0 && gn > clip) ? clip / gn : 0.0;
         d.hdr->done_counter = 0;
     }

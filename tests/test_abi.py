@@ -1,0 +1,51 @@
+"""The C-ABI library loads without a GPU, exports every symbol include/lamm_b200.h
+declares, and fails loudly (no CPU fallback) when no CUDA device is present."""
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT, has_gpu
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "lamm_b200.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(lamm_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_exports_every_declared_symbol():
+    from paper_2505_22208_b200._lib import EXPORTS, LIB_PATH, lib
+    lib()
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB_PATH], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r" T (lamm_\w+)", out))
+    declared = header_symbols()
+    assert declared, "no declarations parsed"
+    missing = [s for s in declared if s not in exported]
+    assert not missing, f"declared but not exported: {missing}"
+    assert sorted(EXPORTS) == declared, "python EXPORTS list out of sync with the header"
+    # nothing but the C ABI leaks out of the library
+    assert all(s.startswith("lamm_") for s in exported)
+
+
+def test_library_is_sm100a_only():
+    from paper_2505_22208_b200._lib import LIB_PATH
+    out = subprocess.run(["cuobjdump", "--list-elf", LIB_PATH], capture_output=True, text=True).stdout
+    arches = set(re.findall(r"sm_(\d+a?)", out))
+    assert arches == {"100a"}, arches
+
+
+@pytest.mark.skipif(has_gpu(), reason="checks the no-GPU failure mode")
+def test_no_gpu_fails_loudly():
+    import paper_2505_22208_b200 as pk
+    with pytest.raises(pk.LammError):
+        pk.Device(pk.ModelConfig(128, 3, 16, 5.0, 10))
+
+
+def test_invalid_config_is_input_error():
+    import paper_2505_22208_b200 as pk
+    with pytest.raises(pk.InputError):
+        pk.Device(pk.ModelConfig(hidden=96, layers=2, rbf=16))
+    with pytest.raises(pk.InputError):
+        pk.init_params(pk.ModelConfig(hidden=0), 1)
