@@ -332,11 +332,13 @@ void launch(Ctx& c, const char* name, Kern kernel, int grid, int block, size_t s
         }
         slot = &c.slots[c.slot_cursor++];
         slot->name = name;
-        CK(cudaEventRecord(slot->a, c.stream));
+        // External records become real event-record nodes under graph capture
+        // (a plain record would only add a dependency edge).
+        CK(cudaEventRecordWithFlags(slot->a, c.stream, cudaEventRecordExternal));
     }
     kernel<<<grid, block, smem, c.stream>>>(args...);
     CK(cudaGetLastError());
-    if (slot) CK(cudaEventRecord(slot->b, c.stream));
+    if (slot) CK(cudaEventRecordWithFlags(slot->b, c.stream, cudaEventRecordExternal));
     ++c.launches;
 }
 
