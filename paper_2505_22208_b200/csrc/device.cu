@@ -12,7 +12,9 @@
 #include <vector>
 
 #include "common.hpp"
+#include "edge_kernels.cuh"
 #include "kernels.cuh"
+#include "gemm_kernels.cuh"
 #include "rng.hpp"
 
 namespace lamm_b200 {
@@ -108,6 +110,7 @@ struct lamm_ctx {
     bool batch_valid = false, nlist_valid = false, fwd_valid = false, loss_valid = false;
     // launch geometry
     int grid_warp = 0, grid_gemm = 0, grid_upd = 0, grid_small = 0, grid_opt = 0, ncta_red = 0, grid_reduce = 0;
+    int grid_edge = 0, slot_cap = 16, slot_cap_max = 16;
     // graphs
     cudaGraphExec_t g_step = nullptr, g_opt = nullptr;
     bool graph_dirty = true;
@@ -191,14 +194,18 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     ensure_buf(c, "fmask", Bc, changed);
     ensure_buf(c, "denoise", Bc, changed);
     ensure_buf(c, "sample_of", 4 * Nc, changed);
+    ensure_buf(c, "chan", 4 * Nc, changed);
     for (const char* n : {"x", "y", "z"}) ensure_buf(c, n, 8 * Nc, changed);
     ensure_buf(c, "En", 8 * Bc, changed);
     ensure_buf(c, "Fn", 24 * Nc, changed);
     ensure_buf(c, "cnt", 4 * Nc, changed);
     ensure_buf(c, "row_ptr", 4 * (Nc + 1), changed);
-    ensure_buf(c, "col", 4 * Pc, changed);
-    ensure_buf(c, "geo", 16 * Pc, changed);
-    ensure_buf(c, "rbf", 4 * static_cast<size_t>(Pc) * K, changed);
+    const int64_t Pp = Pc + kChunk;  // bulk copies may read up to a chunk past the end
+    ensure_buf(c, "col", 4 * Pp, changed);
+    ensure_buf(c, "dst", 4 * Pp, changed);
+    ensure_buf(c, "geo", 16 * Pp, changed);
+    ensure_buf(c, "rbf", 4 * static_cast<size_t>(Pp) * K, changed);
+    ensure_buf(c, "part_lo", 4 * (static_cast<size_t>(c.grid_edge) * kGroups + 1), changed);
     if (c.export64) {
         ensure_buf(c, "dist64", 8 * Pc, changed);
         ensure_buf(c, "unit64", 24 * Pc, changed);
@@ -217,13 +224,12 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     ensure_buf(c, "sample_terms", 16 * Bc, changed);
     ensure_buf(c, "gh", 4 * static_cast<size_t>(Nc) * H, changed);
     ensure_buf(c, "gm", 4 * static_cast<size_t>(Nc) * H, changed);
-    ensure_buf(c, "Q", 4 * static_cast<size_t>(Nc) * (H + K + 4), changed);
     for (int l = 0; l < L; ++l) {
-        ensure_buf(c, "part_wf" + std::to_string(l), 4 * static_cast<size_t>(c.grid_warp) * H * K, changed);
+        ensure_buf(c, "part_wf" + std::to_string(l), 4 * static_cast<size_t>(c.grid_edge) * H * K, changed);
         ensure_buf(c, "part_wu" + std::to_string(l), 4 * static_cast<size_t>(c.grid_gemm) * H * H, changed);
     }
-    ensure_buf(c, "part_head", 4 * static_cast<size_t>(c.ncta_red) * (3 * H + K) * D, changed);
-    ensure_buf(c, "part_emb", 4 * static_cast<size_t>(c.ncta_red) * kMaxZ * H, changed);
+    ensure_buf(c, "part_head", 4 * static_cast<size_t>(c.grid_edge) * (3 * H + K) * D, changed);
+    ensure_buf(c, "part_emb", 4 * static_cast<size_t>(c.grid_edge) * kMaxZ * H, changed);
     if (changed) c.graph_dirty = true;
 }
 
@@ -242,6 +248,7 @@ Dev make_dev(Ctx& c) {
     d.fmask = buf(c, "fmask").as<uint8_t>();
     d.denoise = buf(c, "denoise").as<uint8_t>();
     d.sample_of = buf(c, "sample_of").as<int32_t>();
+    d.chan = buf(c, "chan").as<int32_t>();
     d.x = buf(c, "x").as<double>(), d.y = buf(c, "y").as<double>(), d.z = buf(c, "z").as<double>();
     d.En = buf(c, "En").as<double>();
     d.Fn = buf(c, "Fn").as<double>();
@@ -257,6 +264,8 @@ Dev make_dev(Ctx& c) {
     d.cnt = buf(c, "cnt").as<int32_t>();
     d.row_ptr = buf(c, "row_ptr").as<int32_t>();
     d.col = buf(c, "col").as<int32_t>();
+    d.dst = buf(c, "dst").as<int32_t>();
+    d.part_lo = buf(c, "part_lo").as<int32_t>();
     d.geo = buf(c, "geo").as<float4>();
     d.rbf = buf(c, "rbf").as<float>();
     d.export64 = c.export64 ? 1 : 0;
@@ -287,14 +296,13 @@ Dev make_dev(Ctx& c) {
     d.block_scratch = c.block_scratch.as<double>();
     d.gh = buf(c, "gh").as<float>();
     d.gm = buf(c, "gm").as<float>();
-    d.Q = buf(c, "Q").as<float>();
     for (int l = 0; l < L; ++l) {
         d.part_wf[l] = buf(c, "part_wf" + std::to_string(l)).as<float>();
         d.part_wu[l] = buf(c, "part_wu" + std::to_string(l)).as<float>();
     }
     d.part_head = buf(c, "part_head").as<float>();
     d.part_emb = buf(c, "part_emb").as<float>();
-    d.ncta_edge = c.grid_warp, d.ncta_gemm = c.grid_gemm, d.ncta_red = c.ncta_red;
+    d.ncta_edge = c.grid_edge, d.ncta_gemm = c.grid_gemm, d.ncta_red = c.ncta_red;
     d.grads = c.grads.as<float>();
     d.p64 = c.p64.as<double>();
     d.v64 = c.v64.as<double>();
@@ -368,26 +376,49 @@ struct Ops {
 
 template <int H, int K>
 struct Model {
-    static size_t smem_update() { return sizeof(float) * (H * H + 2 * 32 * H); }
-    static size_t smem_bwd_gemm() { return sizeof(float) * (H * H + 2 * 32 * H); }
-    static size_t smem_bwd_edge() { return sizeof(float) * 8 * H * K; }
-    static size_t smem_force(int D) { return sizeof(float) * (D * H + K * D); }
-    static size_t smem_head_reduce(int D) { return sizeof(float) * (3 * H + K) * D; }
+    static constexpr size_t kEdgeBase = EdgeSmem<K>::extra_offset;
+    static constexpr size_t kGemmSmem = NodeGemmSmem<H>::bytes;
+    static constexpr size_t kDwuSmem = DwuSmem<H>::bytes;
+    static size_t smem_message() { return kEdgeBase; }
+    static size_t smem_force(int D) { return kEdgeBase + sizeof(float) * (D * H + K * D + kGroups * H); }
+    static size_t smem_head(int D) { return kEdgeBase + sizeof(float) * kGroups * (3 * D * H + D * K); }
+    static size_t smem_bwd(int slot_cap) {
+        return kEdgeBase + sizeof(float) * kGroups * (H * K + static_cast<size_t>(slot_cap) * H);
+    }
+
+    static void set_smem(const void* fn, size_t bytes) {
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    }
 
     static void setup(Ctx& c) {
-        CK(cudaFuncSetAttribute(k_update<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_update()));
-        CK(cudaFuncSetAttribute(k_bwd_gemm<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bwd_gemm()));
-        CK(cudaFuncSetAttribute(k_bwd_edge<H, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem_bwd_edge()));
-        CK(cudaFuncSetAttribute(k_embed_grad<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(sizeof(float) * kMaxZ * H)));
-        int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bwd_edge<H, K>, 256, smem_bwd_edge()));
-        c.grid_warp = c.nsm * std::max(1, occ);
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_bwd_gemm<H>, 256, smem_bwd_gemm()));
-        c.grid_gemm = c.nsm * std::max(1, occ);
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update<H>, 256, smem_update()));
-        c.grid_upd = c.nsm * std::max(1, occ);
+        set_smem((const void*)k_node_gemm<H>, kGemmSmem);
+        set_smem((const void*)k_dwu<H>, kDwuSmem);
+        set_smem((const void*)k_edge_message<H, K>, smem_message());
+        int smem_max = 0;
+        CK(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+        if (smem_head(c.D) > static_cast<size_t>(smem_max) || 3 * c.D > H)
+            throw InputErr("model: too many heads for the device path at this hidden size");
+        // embedding-gradient slots (distinct Z per device-batch) that fit next to the staging
+        c.slot_cap_max = static_cast<int>((smem_max - smem_bwd(0)) / (sizeof(float) * kGroups * H)) & ~7;
+        set_smem((const void*)k_edge_force<H, K>, smem_force(c.D));
+        set_smem((const void*)k_edge_head<H, K>, smem_head(c.D));
+        set_smem((const void*)k_edge_bwd<H, K>, smem_bwd(c.slot_cap_max));
+        if (c.D > kGemmMaxHeads) throw InputErr("model: the device path supports at most 16 heads");
+        c.grid_upd = c.nsm;            // one tcgen05 CTA per SM, persistent over 128-atom tiles
+        c.grid_gemm = c.nsm / 2;       // split-K CTAs of dW_u (one partial each)
+        // one edge partitioning (k_scan) serves all four edge kernels: size it so
+        // every CTA of the heaviest one is resident (no second wave)
+        int occ_e = 8, o = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_message<H, K>, kGroups * H, smem_message()));
+        occ_e = std::min(occ_e, o);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_force<H, K>, kGroups * H, smem_force(c.D)));
+        occ_e = std::min(occ_e, o);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_head<H, K>, kGroups * H, smem_head(c.D)));
+        occ_e = std::min(occ_e, o);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_bwd<H, K>, kGroups * H, smem_bwd(16)));
+        occ_e = std::min(occ_e, o);
+        c.grid_edge = c.nsm * std::max(1, occ_e);
+        c.grid_warp = 4 * c.nsm;
         c.grid_small = c.nsm * 4;
         c.ncta_red = c.nsm;
         c.grid_opt = static_cast<int>(std::min<int64_t>((c.NP + 255) / 256, 4 * c.nsm));
@@ -401,18 +432,18 @@ struct Model {
     static void nlist(Ctx& c) {
         const Dev d = make_dev(c);
         launch(c, "nbr_count", k_nbr_count, c.grid_warp, 256, 0, d);
-        launch(c, "nbr_scan", k_scan, 1, 1024, 0, d);
+        launch(c, "nbr_scan", k_scan, 1, 1024, 0, d, c.grid_edge * kGroups);
         launch(c, "nbr_fill", k_nbr_fill<K>, c.grid_warp, 256, 0, d);
     }
 
     static void forward(Ctx& c) {
         const Dev d = make_dev(c);
-        for (int l = 0; l < c.L; ++l) {
-            launch(c, "message", k_message<H, K>, c.grid_warp, 256, 0, d, l);
-            launch(c, "update", k_update<H>, c.grid_upd, 256, smem_update(), d, l, l == c.L - 1 ? 1 : 0);
-        }
         if (c.L == 0) throw InputErr("model: layers == 0 is not supported by the device path");
-        launch(c, "force", k_force<H, K>, c.grid_warp, 256, smem_force(c.D), d);
+        for (int l = 0; l < c.L; ++l) {
+            launch(c, "message", k_edge_message<H, K>, c.grid_edge, kGroups * H, smem_message(), d, l);
+            launch(c, "update", k_node_gemm<H>, c.grid_upd, 128, kGemmSmem, d, l, 0, l == c.L - 1 ? 1 : 0);
+        }
+        launch(c, "force", k_edge_force<H, K>, c.grid_edge, kGroups * H, smem_force(c.D), d);
         launch(c, "energy", k_energy, c.grid_small, 128, sizeof(double) * 128 * c.D, d);
     }
 
@@ -425,29 +456,27 @@ struct Model {
     static void backward(Ctx& c, bool general) {
         const Dev d = make_dev(c);
         const int passes = general ? c.D : 1;
-        for (int q = 0; q < passes; ++q) {
-            const int ch = general ? q : -1;
-            launch(c, "head_bwd", k_head_bwd<H, K>, c.grid_warp, 256, 0, d, ch, q == 0 ? 1 : 0);
-            launch(c, "head_reduce", k_head_reduce<H, K>, c.ncta_red, 128, smem_head_reduce(c.D), d, ch,
+        for (int q = 0; q < passes; ++q)
+            launch(c, "head_bwd", k_edge_head<H, K>, c.grid_edge, kGroups * H, smem_head(c.D), d, general ? q : -1,
                    q == 0 ? 1 : 0);
-        }
         for (int l = c.L - 1; l >= 0; --l) {
-            launch(c, "bwd_gemm", k_bwd_gemm<H>, c.grid_gemm, 256, smem_bwd_gemm(), d, l);
-            launch(c, "bwd_edge", k_bwd_edge<H, K>, c.grid_warp, 256, smem_bwd_edge(), d, l);
+            launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, 128, kGemmSmem, d, l, 1, 0);
+            launch(c, "dwu", k_dwu<H>, c.grid_gemm, 128, kDwuSmem, d, l);
+            launch(c, "bwd_edge", k_edge_bwd<H, K>, c.grid_edge, kGroups * H, smem_bwd(c.slot_cap), d, l,
+                   c.slot_cap);
         }
-        launch(c, "embed_grad", k_embed_grad<H>, c.ncta_red, H, sizeof(float) * kMaxZ * H, d);
         SegTable tab{};
         int64_t off = 0;
         auto add = [&](int64_t n, int kind, const float* src, int ncta, int stride) {
             tab.s[tab.nseg++] = Seg{off, static_cast<int32_t>(n), kind, src, ncta, stride};
             off += n;
         };
-        add(static_cast<int64_t>(kMaxZ) * H, 1, d.part_emb, c.ncta_red, 0);
-        for (int l = 0; l < c.L; ++l) add(H * K, 0, d.part_wf[l], c.grid_warp, H * K);
+        add(static_cast<int64_t>(kMaxZ) * H, 1, d.part_emb, c.grid_edge, 0);
+        for (int l = 0; l < c.L; ++l) add(H * K, 0, d.part_wf[l], c.grid_edge, H * K);
         for (int l = 0; l < c.L; ++l) add(H * H, 0, d.part_wu[l], c.grid_gemm, H * H);
         const int hw = (3 * H + K) * c.D;
-        add(H * c.D, 0, d.part_head + (2 * H + K) * c.D, c.ncta_red, hw);
-        add((2 * H + K) * c.D, 0, d.part_head, c.ncta_red, hw);
+        add(H * c.D, 0, d.part_head + (2 * H + K) * c.D, c.grid_edge, hw);
+        add((2 * H + K) * c.D, 0, d.part_head, c.grid_edge, hw);
         launch(c, "grad_reduce", k_grad_reduce, c.grid_reduce, 256, 0, d, tab);
     }
 
@@ -584,6 +613,11 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
     h.N = static_cast<int32_t>(N);
     h.me = me, h.mf = mf;
     h.nslots = nslots;
+    if (nslots > c.slot_cap) {  // the captured graph sized its embedding accumulators for slot_cap
+        require(nslots <= c.slot_cap_max, "batch: too many distinct atomic numbers in one device-batch");
+        c.slot_cap = std::min(c.slot_cap_max, (nslots + 7) & ~7);
+        c.graph_dirty = true;
+    }
     h.lambda_e = tc ? tc->lambda_energy : 1.0;
     h.lambda_f = tc ? tc->lambda_force : 1.0;
     h.workers = 1;
@@ -736,7 +770,7 @@ LAMM_API int lamm_ctx_create(int device, const lamm_model_config* cfg, lamm_ctx*
         require(cfg->hidden >= 1 && cfg->layers >= 0 && cfg->rbf >= 2 && cfg->cutoff > 0.0 && cfg->heads >= 1,
                 "model: invalid config");
         require(cfg->layers >= 1 && cfg->layers <= kMaxLayers, "model: device path supports 1..8 layers");
-        require(cfg->heads <= kMaxHeads, "model: device path supports at most 32 heads");
+        require(cfg->heads <= kMaxHeads, "model: device path supports at most 16 heads");
         const Ops* ops = select_ops(cfg->hidden, cfg->rbf);
         require(ops != nullptr, "model: (hidden, rbf) must be one of (128,16), (64,16), (32,8)");
         int ndev = 0;

@@ -7,7 +7,8 @@
 //   edges      row_ptr      int32 [N+1]            (CSR by destination atom i,
 //              col          int32 [P]               j ascending = reference order)
 //              geo          float4 [P]  {u_x,u_y,u_z,fcut}
-//              rbf          fp32 [P][K]             (Gaussians of the fp64 distance)
+//              dst          int32 [P]               (destination i of each edge)
+//              rbf          fp32 [P][K]             (fcut * Gaussians of the fp64 distance)
 //   features   t[l], h[l]   fp32 [N][H]  l = 1..L   (t = tanh h; t[0] = tanh(E[Z]))
 //              mu[l]        fp32 [N][H]  l = 0..L-1 (tanh of the message)
 //   heads      e_atom, A    fp32 [N][D]            (per-atom energy, force-head split)
@@ -25,7 +26,7 @@
 namespace lamm_b200 {
 
 constexpr int kMaxLayers = 8;
-constexpr int kMaxHeads = 32;
+constexpr int kMaxHeads = 16;
 constexpr int kMaxZ = 118;
 
 // Per-step scalars that live in device memory so one captured CUDA graph can
@@ -64,6 +65,7 @@ struct Dev {
     const double* F_raw;       // [3N]
     const double* noise;       // [3N] raw Gaussian displacement draws (denoising samples)
     int32_t* sample_of;        // [N]
+    int32_t* chan;             // [N]  head (dataset index) of the atom's sample
     double *x, *y, *z;         // [N] fp64 (noisy) positions, SoA
     double* En;                // [B]  normalized energy labels
     double* Fn;                // [3N] normalized force labels
@@ -73,9 +75,10 @@ struct Dev {
     const double *tmean, *tstd, *tfstd;
     const uint8_t* thas;
     // edges
-    int32_t *cnt, *row_ptr, *col;
+    int32_t *cnt, *row_ptr, *col, *dst;
+    int32_t* part_lo;          // [Q+1] edge-balanced atom partitions (edge kernels)
     float4* geo;
-    float* rbf;
+    float* rbf;                // [P][K] fcut * Gaussians
     double *dist64, *unit64;
     int export64;
     // fp32 working parameters

@@ -9,14 +9,8 @@
 // Reference semantics (S = /root/reference/proj/core/src):
 //   k_prep .......... S/denoise.cpp:7-29 (centering) + S/loss.cpp:113-126 (normalize)
 //   k_nbr_* ......... S/core.cpp:30-48  (bit-exact fp64 pair test, i-major, j ascending)
-//   k_message ....... S/model.cpp:78-92 (filter = W_f rbf fcut; m_i = sum_j t_j * filter)
-//   k_update ........ S/model.cpp:93-102 (h' = h + W_u tanh(m)), + :208-218 energy head
-//   k_force ......... S/model.cpp:223-253 (pair force head; A_i + A_j split)
 //   k_energy/k_loss . S/loss.cpp:140-213 (Eq. 5, per-rank mask denominators)
-//   k_head_bwd ...... S/model.cpp:318-366 (scatter-free: gather over the symmetric CSR)
-//   k_bwd_gemm ...... S/model.cpp:377-390 (dW_u, gm)
-//   k_bwd_edge ...... S/model.cpp:393-418 (gt_l gather, dW_f)
-//   k_embed_grad .... S/model.cpp:421-424
+//   (edge kernels in edge_kernels.cuh, tensor-core GEMMs in gemm_kernels.cuh)
 //   k_opt_* ......... S/trainer.cpp:319-327 + RmsOptimizer :37-53
 //
 // Determinism: no floating-point atomics. Parameter gradients are reduced into
@@ -104,6 +98,7 @@ __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out) {
         const double fs = d.use_table ? __ddiv_rn(1.0, d.tfstd[dsi]) : 1.0;
         for (int64_t a = lo + threadIdx.x; a < hi; a += blockDim.x) {
             d.sample_of[a] = s;
+            d.chan[a] = dsi;
             out.Z[a] = Z[a];
             out.zslot[a] = z2s[Z[a]];
             double xyz[3];
@@ -163,7 +158,10 @@ __global__ void __launch_bounds__(256) k_nbr_count(Dev d) {
 
 // Single-CTA exclusive scan of the per-atom pair counts into row_ptr; writes P
 // and the capacity-overflow flag.
-__global__ void __launch_bounds__(1024) k_scan(Dev d) {
+// Also cuts the edge list into Q edge-balanced partitions of whole atoms for
+// the edge kernels: part_lo[q] = first atom i with row_ptr[i] >= floor(P q / Q),
+// part_lo[Q] = N (computed while writing row_ptr, no searches).
+__global__ void __launch_bounds__(1024) k_scan(Dev d, int Q) {
     __shared__ int warp_tot[32];
     const int N = d.hdr->N;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -190,12 +188,30 @@ __global__ void __launch_bounds__(1024) k_scan(Dev d) {
     }
     __syncthreads();
     int run = incl - s + (wid > 0 ? warp_tot[wid - 1] : 0);
+    const int64_t P = warp_tot[31];
+    int64_t prev = run - 1;  // row_ptr[b-1] seen as "< run" (exact value not needed: only the q range)
+    if (b > 0) prev = run - d.cnt[b - 1];
     for (int k = b; k < e; ++k) {
         d.row_ptr[k] = run;
+        // q in [ceil((prev+1)Q/P), ceil((run+1)Q/P) - 1] start at atom k
+        if (P > 0) {
+            const int64_t qlo = k == 0 ? 0 : ((prev + 1) * Q + P - 1) / P;
+            int64_t qhi = ((static_cast<int64_t>(run) + 1) * Q + P - 1) / P - 1;
+            if (qhi > Q - 1) qhi = Q - 1;
+            for (int64_t q = qlo; q <= qhi; ++q) d.part_lo[q] = k;
+        }
+        prev = run;
         run += d.cnt[k];
     }
+    if (P > 0 && e == N && b < e) {  // targets in (row_ptr[N-1], P] start at atom N
+        const int64_t qlo = ((prev + 1) * Q + P - 1) / P;
+        for (int64_t q = qlo; q < Q; ++q) d.part_lo[q] = N;
+    }
+    if (P == 0)
+        for (int q = t; q < Q; q += 1024) d.part_lo[q] = 0;
     if (t == 1023) {
         d.row_ptr[N] = run;
+        d.part_lo[Q] = N;
         d.hdr->P = run;
         d.hdr->overflow = static_cast<int64_t>(run) > d.Pcap ? 1 : 0;
     }
@@ -230,6 +246,7 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d) {
             if (in) {
                 const int p = base + __popc(mask & ((1u << lane) - 1u));
                 d.col[p] = j;
+                d.dst[p] = i;
                 const double sc = __ddiv_rn(1.0, r);
                 const double ux = __dmul_rn(sc, dx), uy = __dmul_rn(sc, dy), uz = __dmul_rn(sc, dz);
                 const double fc = 0.5 * (cos(kPiD * r / d.rc) + 1.0);
@@ -239,7 +256,7 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d) {
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const double dd = r - width * static_cast<double>(k);
-                    rb[k] = static_cast<float>(exp(-dd * dd * inv));
+                    rb[k] = static_cast<float>(fc * exp(-dd * dd * inv));  // fcut folded in
                 }
                 float4* dst = reinterpret_cast<float4*>(d.rbf + static_cast<int64_t>(p) * K);
 #pragma unroll
@@ -263,244 +280,6 @@ __device__ __forceinline__ void load_rbf(const float* __restrict__ src, float (&
     for (int k = 0; k < K / 4; ++k) {
         const float4 q = __ldg(s4 + k);
         rb[4 * k] = q.x, rb[4 * k + 1] = q.y, rb[4 * k + 2] = q.z, rb[4 * k + 3] = q.w;
-    }
-}
-
-// --------------------------------------------------------------- encoder ---
-// Message of layer l, warp per destination atom: lane owns channels
-// [lane*C, lane*C+C), keeps its C x K slice of W_f in registers, walks the
-// atom's CSR row (edges contiguous, j ascending), gathers t_j rows with one
-// coalesced vector load per lane, and reduces in registers (no atomics).
-// Writes mu_l = tanh(m_l).
-template <int H, int K>
-__global__ void __launch_bounds__(256) k_message(Dev d, int l) {
-    constexpr int C = H / 32;
-    const int lane = threadIdx.x & 31;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    float w[C][K];
-    const float* __restrict__ wf = d.wf[l];
-#pragma unroll
-    for (int c = 0; c < C; ++c)
-#pragma unroll
-        for (int k = 0; k < K; ++k) w[c][k] = wf[(lane * C + c) * K + k];
-    const float* __restrict__ tsrc = l == 0 ? d.tanh_emb : d.t[l];
-    const int N = d.hdr->N;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
-        const int p0 = d.row_ptr[i], p1 = d.row_ptr[i + 1];
-        float m[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) m[c] = 0.f;
-#pragma unroll 2
-        for (int p = p0; p < p1; ++p) {
-            const int j = __ldg(d.col + p);
-            const float fc = __ldg(&d.geo[p].w);
-            float rb[K];
-            load_rbf<K>(d.rbf + static_cast<int64_t>(p) * K, rb);
-            const int jrow = l == 0 ? __ldg(d.Z + j) - 1 : j;
-            const VecF<C> tj = ldv<C>(tsrc + static_cast<int64_t>(jrow) * H + lane * C);
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                float acc = 0.f;
-#pragma unroll
-                for (int k = 0; k < K; ++k) acc = fmaf(w[c][k], rb[k], acc);
-                m[c] = fmaf(tj.v[c], acc * fc, m[c]);
-            }
-        }
-        VecF<C> o;
-#pragma unroll
-        for (int c = 0; c < C; ++c) o.v[c] = tanhf(m[c]);
-        stv<C>(d.mu[l] + static_cast<int64_t>(i) * H + lane * C, o);
-    }
-}
-
-// Update of layer l: h_{l+1} = h_l + mu_l W_u^T as a persistent tile GEMM
-// (32 atoms x H per tile, W_u^T staged once per CTA in shared memory), fused
-// epilogue writes h_{l+1} and t_{l+1} = tanh(h_{l+1}). On the last layer the
-// epilogue also produces the per-atom energy e_i[d] = W_e^T h^L_i and the
-// force-head split A_i[d] = W_fh[0:H]^T t^L_i.
-template <int H>
-__global__ void __launch_bounds__(256) k_update(Dev d, int l, int last) {
-    constexpr int C = H / 32, TM = 32, RPW = TM / 8;
-    float* sm = dyn_smem<float>();
-    float* WuT = sm;           // [H][H], WuT[a][b] = W_u[b][a]
-    float* tile = sm + H * H;  // [TM][H]
-    float* tile2 = tile + TM * H;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const float* __restrict__ wu = d.wu[l];
-    for (int idx = tid; idx < H * H; idx += blockDim.x) {
-        const int a = idx / H, b = idx % H;
-        WuT[idx] = wu[b * H + a];
-    }
-    const int N = d.hdr->N, D = d.D;
-    const int ntiles = (N + TM - 1) / TM;
-    __syncthreads();
-    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-        const int base = ti * TM;
-        for (int idx = tid * 4; idx < TM * H; idx += blockDim.x * 4) {
-            const int r = idx / H, atom = base + r;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (atom < N) v = *reinterpret_cast<const float4*>(d.mu[l] + static_cast<int64_t>(atom) * H + idx % H);
-            *reinterpret_cast<float4*>(tile + idx) = v;
-        }
-        __syncthreads();
-        float acc[RPW][C];
-#pragma unroll
-        for (int r = 0; r < RPW; ++r)
-#pragma unroll
-            for (int c = 0; c < C; ++c) acc[r][c] = 0.f;
-        const int r0 = warp * RPW;
-#pragma unroll 4
-        for (int a = 0; a < H; ++a) {
-            const VecF<C> wv = ldv<C>(WuT + a * H + lane * C);
-#pragma unroll
-            for (int r = 0; r < RPW; ++r) {
-                const float mv = tile[(r0 + r) * H + a];
-#pragma unroll
-                for (int c = 0; c < C; ++c) acc[r][c] = fmaf(mv, wv.v[c], acc[r][c]);
-            }
-        }
-        if (last) __syncthreads();  // tile is reused for h^L below
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-            const int atom = base + r0 + r;
-            if (atom >= N) continue;
-            const float* hp = l == 0 ? d.emb + static_cast<int64_t>(__ldg(d.Z + atom) - 1) * H
-                                     : d.h[l] + static_cast<int64_t>(atom) * H;
-            const VecF<C> hv = ldv<C>(hp + lane * C);
-            VecF<C> hn, tn;
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                hn.v[c] = hv.v[c] + acc[r][c];
-                tn.v[c] = tanhf(hn.v[c]);
-            }
-            stv<C>(d.h[l + 1] + static_cast<int64_t>(atom) * H + lane * C, hn);
-            stv<C>(d.t[l + 1] + static_cast<int64_t>(atom) * H + lane * C, tn);
-            if (last) {
-                stv<C>(tile + (r0 + r) * H + lane * C, hn);
-                stv<C>(tile2 + (r0 + r) * H + lane * C, tn);
-            }
-        }
-        if (last) {
-            __syncthreads();
-            for (int o = tid; o < TM * D * 2; o += blockDim.x) {
-                const int r = o / (2 * D), q = o % (2 * D), which = q / D, dd = q % D;
-                const int atom = base + r;
-                if (atom >= N) continue;
-                const float* src = (which ? tile2 : tile) + r * H;
-                const float* W = which ? d.wfh : d.we;
-                float s = 0.f;
-#pragma unroll 8
-                for (int a = 0; a < H; ++a) s = fmaf(src[a], __ldg(W + a * D + dd), s);
-                (which ? d.A : d.e_atom)[static_cast<int64_t>(atom) * D + dd] = s;
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// ------------------------------------------------------------ force head ---
-// In-warp reduce-scatter of 32 per-lane values: after 31 shuffles lane k holds
-// the warp sum of value k.
-__device__ __forceinline__ float reduce_scatter32(float (&v)[32], int lane) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int k = 0; k < o; ++k) {
-            const float send = up ? v[k] : v[k + o];
-            const float keep = up ? v[k + o] : v[k];
-            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-    }
-    return v[0];
-}
-
-// F_i^d = sum_j w_ijd fcut_ij u_ij with w_ijd = A_id + A_jd + sum_a Wb[a,d] T_ia T_ja
-// + sum_k Wc[k,d] rbf_ijk. Re-associated per destination atom: the Wb term is
-// sum_a Wb[a,d] T_ia Y_i[a] with Y_i = sum_j T_j fcut u (accumulated per lane in
-// registers), so the only per-edge work is one T_j gather plus O(K + D) scalar
-// flops; the 3D outputs are produced by one reduce-scatter per atom.
-template <int H, int K>
-__global__ void __launch_bounds__(256) k_force(Dev d) {
-    constexpr int C = H / 32;
-    float* sm = dyn_smem<float>();
-    const int D = d.D, ND = 3 * D;
-    float* WbT = sm;              // [D][H]
-    float* Wc = sm + D * H;       // [K][D]
-    for (int idx = threadIdx.x; idx < D * H; idx += blockDim.x) {
-        const int dd = idx / H, a = idx % H;
-        WbT[idx] = d.wfh[(H + a) * D + dd];
-    }
-    for (int idx = threadIdx.x; idx < K * D; idx += blockDim.x) Wc[idx] = d.wfh[2 * H * D + idx];
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    const int N = d.hdr->N, L = d.L;
-    const float* __restrict__ T = L > 0 ? d.t[L] : d.tanh_emb;
-    const int R = (ND + 31) / 32;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
-        const int irow = L > 0 ? i : __ldg(d.Z + i) - 1;
-        const VecF<C> Ti = ldv<C>(T + static_cast<int64_t>(irow) * H + lane * C);
-        float Ai[3], Fs[3];
-        int ddl[3], xl[3];
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-            const int idx = 32 * r + lane;
-            ddl[r] = idx / 3, xl[r] = idx % 3;
-            Ai[r] = (r < R && idx < ND) ? d.A[static_cast<int64_t>(i) * D + ddl[r]] : 0.f;
-            Fs[r] = 0.f;
-        }
-        float Y[C][3];
-#pragma unroll
-        for (int c = 0; c < C; ++c) Y[c][0] = Y[c][1] = Y[c][2] = 0.f;
-        const int p0 = d.row_ptr[i], p1 = d.row_ptr[i + 1];
-        for (int p = p0; p < p1; ++p) {
-            const int j = __ldg(d.col + p);
-            const float4 g = __ldg(d.geo + p);
-            float rb[K];
-            load_rbf<K>(d.rbf + static_cast<int64_t>(p) * K, rb);
-            const int jrow = L > 0 ? j : __ldg(d.Z + j) - 1;
-            const VecF<C> Tj = ldv<C>(T + static_cast<int64_t>(jrow) * H + lane * C);
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                const float tf = Tj.v[c] * g.w;
-                Y[c][0] = fmaf(tf, g.x, Y[c][0]);
-                Y[c][1] = fmaf(tf, g.y, Y[c][1]);
-                Y[c][2] = fmaf(tf, g.z, Y[c][2]);
-            }
-            const float u[3] = {g.x, g.y, g.z};
-#pragma unroll
-            for (int r = 0; r < 3; ++r) {
-                const int idx = 32 * r + lane;
-                if (r < R && idx < ND) {
-                    float w = Ai[r] + __ldg(d.A + static_cast<int64_t>(j) * D + ddl[r]);
-#pragma unroll
-                    for (int k = 0; k < K; ++k) w = fmaf(Wc[k * D + ddl[r]], rb[k], w);
-                    const float ux = xl[r] == 0 ? u[0] : (xl[r] == 1 ? u[1] : u[2]);
-                    Fs[r] = fmaf(w * g.w, ux, Fs[r]);
-                }
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < 3; ++r) {
-            if (r >= R) break;
-            float v[32];
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                const int idx = 32 * r + k;
-                float s = 0.f;
-                if (idx < ND) {
-                    const int dd = idx / 3, x = idx % 3;
-                    const VecF<C> wb = ldv<C>(WbT + dd * H + lane * C);
-#pragma unroll
-                    for (int c = 0; c < C; ++c) s = fmaf(wb.v[c] * Ti.v[c], Y[c][x], s);
-                }
-                v[k] = s;
-            }
-            const float tot = reduce_scatter32(v, lane);
-            const int idx = 32 * r + lane;
-            if (idx < ND) d.F[static_cast<int64_t>(i) * ND + idx] = Fs[r] + tot;
-        }
     }
 }
 
@@ -606,280 +385,6 @@ __global__ void __launch_bounds__(1024) k_loss_final(Dev d) {
         d.grads[d.NP + 2] = d.hdr->overflow ? 1.f : 0.f;
         d.grads[d.NP + 3] = 1.f;
     }
-}
-
-// ------------------------------------------------------ head backward ---
-// Scatter-free reverse pass of both heads for one channel per sample (the
-// sample's d_s in the train step; a fixed d per pass for a general upstream).
-// With s_ij = fcut (gF_i - gF_j).u_ij (u_ji = -u_ij on the symmetric CSR):
-//   gT_i = S_i Wa[:,d] + Wb[:,d] (.) W_i,  S_i = sum_j s_ij,  W_i = sum_j s_ij T_j
-//   gh_i = We gE_s + gT_i (.) (1 - T_i^2)
-// and the per-atom terms Q_i = [T_i (.) W_i / 2 | R_i | S_i] with
-// R_ik = sum_j fcut (gF_i.u_ij) rbf_ijk feed dW_fh in k_head_reduce.
-template <int H, int K>
-__global__ void __launch_bounds__(256) k_head_bwd(Dev d, int pass_ch, int first) {
-    constexpr int C = H / 32, QW = H + K + 4;  // row padded to 16 B
-    const int lane = threadIdx.x & 31;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    const int N = d.hdr->N, L = d.L, D = d.D;
-    const float* __restrict__ T = L > 0 ? d.t[L] : d.tanh_emb;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
-        const int s = d.sample_of[i];
-        const int ch = pass_ch >= 0 ? pass_ch : d.dsidx[s];
-        const int irow = L > 0 ? i : __ldg(d.Z + i) - 1;
-        const VecF<C> Ti = ldv<C>(T + static_cast<int64_t>(irow) * H + lane * C);
-        const float* gfi_p = d.gF + (static_cast<int64_t>(i) * D + ch) * 3;
-        const float gfi0 = gfi_p[0], gfi1 = gfi_p[1], gfi2 = gfi_p[2];
-        float S = 0.f, Rk = 0.f, W[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) W[c] = 0.f;
-        const int p0 = d.row_ptr[i], p1 = d.row_ptr[i + 1];
-        for (int p = p0; p < p1; ++p) {
-            const int j = __ldg(d.col + p);
-            const float4 g = __ldg(d.geo + p);
-            const float* gfj_p = d.gF + (static_cast<int64_t>(j) * D + ch) * 3;
-            const float di = gfi0 * g.x + gfi1 * g.y + gfi2 * g.z;
-            const float dj = __ldg(gfj_p) * g.x + __ldg(gfj_p + 1) * g.y + __ldg(gfj_p + 2) * g.z;
-            const float sij = g.w * (di - dj);
-            const int jrow = L > 0 ? j : __ldg(d.Z + j) - 1;
-            const VecF<C> Tj = ldv<C>(T + static_cast<int64_t>(jrow) * H + lane * C);
-            S += sij;
-#pragma unroll
-            for (int c = 0; c < C; ++c) W[c] = fmaf(sij, Tj.v[c], W[c]);
-            if (lane < K) Rk = fmaf(g.w * di, __ldg(d.rbf + static_cast<int64_t>(p) * K + lane), Rk);
-        }
-        float* ghp = d.gh + static_cast<int64_t>(i) * H + lane * C;
-        VecF<C> gh;
-        if (first) {
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                float e = 0.f;
-                for (int dd = 0; dd < D; ++dd)
-                    e = fmaf(d.we[(lane * C + c) * D + dd], d.gE[static_cast<int64_t>(s) * D + dd], e);
-                gh.v[c] = e;
-            }
-        } else {
-            gh = ldv<C>(ghp);
-        }
-        VecF<C> q;
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            const int a = lane * C + c;
-            const float gt = S * d.wfh[a * D + ch] + d.wfh[(H + a) * D + ch] * W[c];
-            gh.v[c] = fmaf(gt, 1.f - Ti.v[c] * Ti.v[c], gh.v[c]);
-            q.v[c] = 0.5f * Ti.v[c] * W[c];
-        }
-        stv<C>(ghp, gh);
-        float* Qi = d.Q + static_cast<int64_t>(i) * QW;
-        stv<C>(Qi + lane * C, q);
-        if (lane < K) Qi[H + lane] = Rk;
-        if (lane == 0) Qi[H + K] = S;
-    }
-}
-
-// Per-CTA partial dW_fh (all 2H+K rows, channel ch) and dW_e from a
-// contiguous atom chunk, summed in atom order with one thread per column.
-template <int H, int K>
-__global__ void __launch_bounds__(128) k_head_reduce(Dev d, int pass_ch, int first) {
-    constexpr int QW = H + K + 4, NQ = 2 * H + K;
-    float* acc = dyn_smem<float>();  // [NQ*D] fhead | [H*D] ehead
-    const int D = d.D, L = d.L;
-    const int W = (NQ + H) * D;
-    float* part = d.part_head + static_cast<int64_t>(blockIdx.x) * W;
-    for (int e = threadIdx.x; e < W; e += blockDim.x) acc[e] = first ? 0.f : part[e];
-    __syncthreads();
-    const int N = d.hdr->N;
-    const int chunk = (N + gridDim.x - 1) / gridDim.x;
-    const int i0 = blockIdx.x * chunk, i1 = min(N, i0 + chunk);
-    const float* __restrict__ T = L > 0 ? d.t[L] : d.tanh_emb;
-    const float* __restrict__ hL = L > 0 ? d.h[L] : d.emb;
-    for (int i = i0; i < i1; ++i) {
-        const int s = d.sample_of[i];
-        const int ch = pass_ch >= 0 ? pass_ch : d.dsidx[s];
-        const float* Qi = d.Q + static_cast<int64_t>(i) * QW;
-        const int irow = L > 0 ? i : d.Z[i] - 1;
-        const float S = Qi[H + K];
-        for (int q = threadIdx.x; q < NQ; q += blockDim.x) {
-            float v;
-            if (q < H) v = S * T[static_cast<int64_t>(irow) * H + q];
-            else if (q < 2 * H) v = Qi[q - H];
-            else v = Qi[H + (q - 2 * H)];
-            acc[q * D + ch] += v;
-        }
-        if (first)
-            for (int a = threadIdx.x; a < H; a += blockDim.x) {
-                const float hv = hL[static_cast<int64_t>(irow) * H + a];
-                for (int dd = 0; dd < D; ++dd) acc[NQ * D + a * D + dd] += hv * d.gE[static_cast<int64_t>(s) * D + dd];
-            }
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < W; e += blockDim.x) part[e] = acc[e];
-}
-
-// ------------------------------------------------------- layer backward ---
-// gm = (gh W_u) (.) (1 - mu^2) as a persistent 32-atom tile GEMM, plus the
-// per-CTA partial dW_u = sum_i gh_i^T mu_i accumulated in registers across the
-// CTA's tiles (16x16 thread grid, (H/16)^2 outputs per thread).
-template <int H>
-__global__ void __launch_bounds__(256) k_bwd_gemm(Dev d, int l) {
-    constexpr int C = H / 32, TM = 32, RPW = TM / 8, RB = H / 16;
-    float* sm = dyn_smem<float>();
-    float* Wu = sm;             // [H][H] row b, col a
-    float* ght = sm + H * H;    // [TM][H]
-    float* mut = ght + TM * H;  // [TM][H]
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const float* __restrict__ wu = d.wu[l];
-    for (int idx = tid * 4; idx < H * H; idx += blockDim.x * 4)
-        *reinterpret_cast<float4*>(Wu + idx) = *reinterpret_cast<const float4*>(wu + idx);
-    const int bb = (tid / 16) * RB, aa = (tid % 16) * RB;
-    float dW[RB][RB];
-#pragma unroll
-    for (int x = 0; x < RB; ++x)
-#pragma unroll
-        for (int y = 0; y < RB; ++y) dW[x][y] = 0.f;
-    const int N = d.hdr->N;
-    const int ntiles = (N + TM - 1) / TM;
-    __syncthreads();
-    for (int ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-        const int base = ti * TM;
-        for (int idx = tid * 4; idx < TM * H; idx += blockDim.x * 4) {
-            const int r = idx / H, atom = base + r;
-            float4 g = make_float4(0.f, 0.f, 0.f, 0.f), m = g;
-            if (atom < N) {
-                g = *reinterpret_cast<const float4*>(d.gh + static_cast<int64_t>(atom) * H + idx % H);
-                m = *reinterpret_cast<const float4*>(d.mu[l] + static_cast<int64_t>(atom) * H + idx % H);
-            }
-            *reinterpret_cast<float4*>(ght + idx) = g;
-            *reinterpret_cast<float4*>(mut + idx) = m;
-        }
-        __syncthreads();
-        float acc[RPW][C];
-#pragma unroll
-        for (int r = 0; r < RPW; ++r)
-#pragma unroll
-            for (int c = 0; c < C; ++c) acc[r][c] = 0.f;
-        const int r0 = warp * RPW;
-#pragma unroll 4
-        for (int b = 0; b < H; ++b) {
-            const VecF<C> wv = ldv<C>(Wu + b * H + lane * C);
-#pragma unroll
-            for (int r = 0; r < RPW; ++r) {
-                const float gv = ght[(r0 + r) * H + b];
-#pragma unroll
-                for (int c = 0; c < C; ++c) acc[r][c] = fmaf(gv, wv.v[c], acc[r][c]);
-            }
-        }
-#pragma unroll
-        for (int r = 0; r < RPW; ++r) {
-            const int atom = base + r0 + r;
-            if (atom >= N) continue;
-            const VecF<C> mv = ldv<C>(mut + (r0 + r) * H + lane * C);
-            VecF<C> o;
-#pragma unroll
-            for (int c = 0; c < C; ++c) o.v[c] = acc[r][c] * (1.f - mv.v[c] * mv.v[c]);
-            stv<C>(d.gm + static_cast<int64_t>(atom) * H + lane * C, o);
-        }
-#pragma unroll 4
-        for (int i = 0; i < TM; ++i) {
-            float gv[RB], mv[RB];
-#pragma unroll
-            for (int x = 0; x < RB; ++x) gv[x] = ght[i * H + bb + x], mv[x] = mut[i * H + aa + x];
-#pragma unroll
-            for (int x = 0; x < RB; ++x)
-#pragma unroll
-                for (int y = 0; y < RB; ++y) dW[x][y] = fmaf(gv[x], mv[y], dW[x][y]);
-        }
-        __syncthreads();
-    }
-    float* part = d.part_wu[l] + static_cast<int64_t>(blockIdx.x) * H * H;
-#pragma unroll
-    for (int x = 0; x < RB; ++x)
-#pragma unroll
-        for (int y = 0; y < RB; ++y) part[(bb + x) * H + aa + y] = dW[x][y];
-}
-
-// Edge part of layer l's reverse pass, warp per atom, gather form:
-//   gt_i = sum_j gm_j (.) filter_ij        (filter symmetric in i, j)
-//   dW_f[a,k] += gm_ia t_ja fcut_ij rbf_ijk (per-warp registers, CTA-reduced)
-//   gh_i += gt_i (.) (1 - t_i^2)
-template <int H, int K>
-__global__ void __launch_bounds__(256) k_bwd_edge(Dev d, int l) {
-    constexpr int C = H / 32;
-    float* red = dyn_smem<float>();  // [warps][H*K]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    float w[C][K], dW[C][K];
-    const float* __restrict__ wf = d.wf[l];
-#pragma unroll
-    for (int c = 0; c < C; ++c)
-#pragma unroll
-        for (int k = 0; k < K; ++k) w[c][k] = wf[(lane * C + c) * K + k], dW[c][k] = 0.f;
-    const float* __restrict__ tsrc = l == 0 ? d.tanh_emb : d.t[l];
-    const int N = d.hdr->N;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
-        const VecF<C> gmi = ldv<C>(d.gm + static_cast<int64_t>(i) * H + lane * C);
-        float gt[C];
-#pragma unroll
-        for (int c = 0; c < C; ++c) gt[c] = 0.f;
-        const int p0 = d.row_ptr[i], p1 = d.row_ptr[i + 1];
-#pragma unroll 2
-        for (int p = p0; p < p1; ++p) {
-            const int j = __ldg(d.col + p);
-            const float fc = __ldg(&d.geo[p].w);
-            float rb[K];
-            load_rbf<K>(d.rbf + static_cast<int64_t>(p) * K, rb);
-            const VecF<C> gmj = ldv<C>(d.gm + static_cast<int64_t>(j) * H + lane * C);
-            const int jrow = l == 0 ? __ldg(d.Z + j) - 1 : j;
-            const VecF<C> tj = ldv<C>(tsrc + static_cast<int64_t>(jrow) * H + lane * C);
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                float acc = 0.f;
-#pragma unroll
-                for (int k = 0; k < K; ++k) acc = fmaf(w[c][k], rb[k], acc);
-                gt[c] = fmaf(gmj.v[c], acc * fc, gt[c]);
-                const float gg = gmi.v[c] * tj.v[c] * fc;
-#pragma unroll
-                for (int k = 0; k < K; ++k) dW[c][k] = fmaf(gg, rb[k], dW[c][k]);
-            }
-        }
-        const int irow = l == 0 ? __ldg(d.Z + i) - 1 : i;
-        const VecF<C> ti = ldv<C>(tsrc + static_cast<int64_t>(irow) * H + lane * C);
-        float* ghp = d.gh + static_cast<int64_t>(i) * H + lane * C;
-        VecF<C> gh = ldv<C>(ghp);
-#pragma unroll
-        for (int c = 0; c < C; ++c) gh.v[c] = fmaf(gt[c], 1.f - ti.v[c] * ti.v[c], gh.v[c]);
-        stv<C>(ghp, gh);
-    }
-    float* mine = red + warp * H * K;
-#pragma unroll
-    for (int c = 0; c < C; ++c)
-#pragma unroll
-        for (int k = 0; k < K; ++k) mine[(lane * C + c) * K + k] = dW[c][k];
-    __syncthreads();
-    const int nwarp = blockDim.x >> 5;
-    float* part = d.part_wf[l] + static_cast<int64_t>(blockIdx.x) * H * K;
-    for (int e = threadIdx.x; e < H * K; e += blockDim.x) {
-        float s = 0.f;
-        for (int q = 0; q < nwarp; ++q) s += red[q * H * K + e];
-        part[e] = s;
-    }
-}
-
-// Embedding gradient dE[Z_i - 1] += gh_i, per-CTA partial over a contiguous
-// atom chunk, one thread per channel, rows indexed by the batch's Z slots.
-template <int H>
-__global__ void __launch_bounds__(H) k_embed_grad(Dev d) {
-    float* acc = dyn_smem<float>();  // [nslots][H]
-    const int ns = d.hdr->nslots;
-    for (int e = threadIdx.x; e < ns * H; e += blockDim.x) acc[e] = 0.f;
-    __syncthreads();
-    const int N = d.hdr->N;
-    const int chunk = (N + gridDim.x - 1) / gridDim.x;
-    const int i0 = blockIdx.x * chunk, i1 = min(N, i0 + chunk);
-    for (int i = i0; i < i1; ++i) acc[d.zslot[i] * H + threadIdx.x] += d.gh[static_cast<int64_t>(i) * H + threadIdx.x];
-    __syncthreads();
-    float* part = d.part_emb + static_cast<int64_t>(blockIdx.x) * ns * H;
-    for (int e = threadIdx.x; e < ns * H; e += blockDim.x) part[e] = acc[e];
 }
 
 // ------------------------------------------------------- grad reduction ---

@@ -1,0 +1,124 @@
+// umma.cuh - minimal tcgen05 (5th-gen tensor core) + TMEM toolkit for sm_100a,
+// written against the PTX ISA: shared-memory matrix descriptors, the kind::tf32
+// instruction descriptor, MMA issue/commit, TMEM alloc and loads.
+//
+// Operand layout used throughout: K-major, no swizzle ("interleaved") canonical
+// tiles of fp32/tf32. A core matrix is 8 rows x 16 bytes (4 elements) stored
+// contiguously (128 B); core matrices adjacent in K are 128 B apart (LBO) and
+// 8-row groups are (KW/4)*128 B apart (SBO) for a tile KW elements wide. One
+// kind::tf32 MMA consumes K = 8 (two core matrices), so K-step s starts s*256 B
+// into the tile.
+//
+// fp32 accuracy from tf32 tensor cores: every operand x is split
+// x = hi + lo with hi = tf32(x) (round-to-nearest) and lo = x - hi (exact in
+// fp32, its tf32 truncation keeps ~22 significant bits of x in total), and each
+// product is accumulated as hi*hi + hi*lo + lo*hi ("3xTF32"): ~1e-7 relative,
+// well inside the 1e-4 parity bar, at one third of the tf32 tensor rate.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lamm_b200 {
+namespace umma {
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+// Element (row m, col k) of a [rows][KW] K-major canonical fp32 tile.
+__device__ __forceinline__ int kidx(int m, int k, int KW) {
+    return (((m >> 3) * (KW >> 2) + (k >> 2)) << 5) + ((m & 7) << 2) + (k & 3);
+}
+
+// SM100 shared-memory matrix descriptor, SWIZZLE_NONE, version 1.
+__device__ __forceinline__ uint64_t sdesc(const void* tile, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr(tile) >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+    d |= static_cast<uint64_t>(1) << 46;  // descriptor version (sm100)
+    return d;                              // base offset 0, layout SWIZZLE_NONE (bits 61-63 = 0)
+}
+
+// Descriptor of K-step s of a K-major canonical tile KW elements wide.
+__device__ __forceinline__ uint64_t kdesc(const float* tile, int s, int KW) {
+    return sdesc(tile + s * 64, 128u, static_cast<uint32_t>((KW >> 2) * 128));
+}
+
+// kind::tf32 instruction descriptor: D fp32, A/B tf32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// 3xTF32 product accumulation for one K-step: D (+)= Ahi Bhi + Ahi Blo + Alo Bhi.
+__device__ __forceinline__ void mma3(uint32_t tmem_d, uint64_t ahi, uint64_t alo, uint64_t bhi, uint64_t blo,
+                                     uint32_t idesc, uint32_t acc) {
+    mma_tf32(tmem_d, ahi, bhi, idesc, acc);
+    mma_tf32(tmem_d, ahi, blo, idesc, 1u);
+    mma_tf32(tmem_d, alo, bhi, idesc, 1u);
+}
+
+// Arrives on an mbarrier when all previously issued MMAs of this thread finish.
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// Generic-proxy shared-memory writes -> visible to the tensor core (async proxy).
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Whole-warp TMEM allocation; the base address lands in *dst (shared).
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(dst)), "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+
+// 32 TMEM lanes x 16 consecutive 32-bit columns: thread t of the warp receives
+// lane (32*(warp%4) + t), columns [col, col+16).
+__device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = __uint_as_float(r[k]);
+}
+
+__device__ __forceinline__ void ld8(uint32_t taddr, float (&v)[8]) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(r[k]);
+}
+
+// fp32 -> (tf32 hi, fp32 lo) split for 3xTF32.
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+    uint32_t h;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+    hi = __uint_as_float(h);
+    lo = x - hi;
+}
+
+}  // namespace umma
+}  // namespace lamm_b200
