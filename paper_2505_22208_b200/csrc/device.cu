@@ -87,7 +87,7 @@ struct lamm_ctx {
     int nsm = 148;
     const lamm_b200::Ops* ops = nullptr;
     // persistent parameter state
-    lamm_b200::Buf p64, v64, g64, p32, tanh_emb, grads, block_scratch;
+    lamm_b200::Buf p64, v64, g64, p32, tanh_emb, grads, block_scratch, wpack;
     // staging (pinned host -> device blob, header first)
     char* h_stage = nullptr;
     size_t h_stage_cap = 0;
@@ -110,7 +110,7 @@ struct lamm_ctx {
     bool batch_valid = false, nlist_valid = false, fwd_valid = false, loss_valid = false;
     // launch geometry
     int grid_warp = 0, grid_gemm = 0, grid_upd = 0, grid_small = 0, grid_opt = 0, ncta_red = 0, grid_reduce = 0;
-    int grid_edge = 0, slot_cap = 16, slot_cap_max = 16;
+    int grid_edge = 0, slot_cap = 16, slot_cap_max = 16, node_ns = 1;
     // graphs
     cudaGraphExec_t g_step = nullptr, g_opt = nullptr;
     bool graph_dirty = true;
@@ -175,6 +175,7 @@ void alloc_param_state(Ctx& c) {
     mk(c.grads, sizeof(float) * (c.NP + 4));
     mk(c.block_scratch, sizeof(double) * 4096);
     mk(c.anomaly, 256);
+    mk(c.wpack, sizeof(float) * 4 * c.H * c.H * std::max(c.L, 1));
 }
 
 // Grows every batch-sized buffer to hold N atoms, B samples and P pairs.
@@ -200,11 +201,13 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     ensure_buf(c, "Fn", 24 * Nc, changed);
     ensure_buf(c, "cnt", 4 * Nc, changed);
     ensure_buf(c, "row_ptr", 4 * (Nc + 1), changed);
-    const int64_t Pp = Pc + kChunk;  // bulk copies may read up to a chunk past the end
+    const int64_t Pp = ((Pc + kChunk + 16 + 7) / 8) * 8;  // CSR padding for the chunk staging
     ensure_buf(c, "col", 4 * Pp, changed);
     ensure_buf(c, "dst", 4 * Pp, changed);
     ensure_buf(c, "geo", 16 * Pp, changed);
     ensure_buf(c, "rbf", 4 * static_cast<size_t>(Pp) * K, changed);
+    ensure_buf(c, "rbfl", 4 * static_cast<size_t>(Pp) * K, changed);
+    ensure_buf(c, "rbfp", 4 * static_cast<size_t>(Pp) * K, changed);
     ensure_buf(c, "part_lo", 4 * (static_cast<size_t>(c.grid_edge) * kGroups + 1), changed);
     if (c.export64) {
         ensure_buf(c, "dist64", 8 * Pc, changed);
@@ -215,8 +218,7 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
         ensure_buf(c, "h" + std::to_string(l), 4 * static_cast<size_t>(Nc) * H, changed);
     }
     for (int l = 0; l < L; ++l) ensure_buf(c, "mu" + std::to_string(l), 4 * static_cast<size_t>(Nc) * H, changed);
-    ensure_buf(c, "e_atom", 4 * Nc * D, changed);
-    ensure_buf(c, "A", 4 * Nc * D, changed);
+    ensure_buf(c, "e_atom", 4 * Nc * D * c.node_ns, changed);
     ensure_buf(c, "F", 12 * Nc * D, changed);
     ensure_buf(c, "Epred", 8 * Bc * D, changed);
     ensure_buf(c, "gE", 4 * Bc * D, changed);
@@ -268,6 +270,8 @@ Dev make_dev(Ctx& c) {
     d.part_lo = buf(c, "part_lo").as<int32_t>();
     d.geo = buf(c, "geo").as<float4>();
     d.rbf = buf(c, "rbf").as<float>();
+    d.rbfl = buf(c, "rbfl").as<float>();
+    d.rbfp = buf(c, "rbfp").as<float>();
     d.export64 = c.export64 ? 1 : 0;
     d.dist64 = c.export64 ? buf(c, "dist64").as<double>() : nullptr;
     d.unit64 = c.export64 ? buf(c, "unit64").as<double>() : nullptr;
@@ -287,7 +291,6 @@ Dev make_dev(Ctx& c) {
     }
     for (int l = 0; l < L; ++l) d.mu[l] = buf(c, "mu" + std::to_string(l)).as<float>();
     d.e_atom = buf(c, "e_atom").as<float>();
-    d.A = buf(c, "A").as<float>();
     d.F = buf(c, "F").as<float>();
     d.Epred = buf(c, "Epred").as<double>();
     d.gE = buf(c, "gE").as<float>();
@@ -311,6 +314,8 @@ Dev make_dev(Ctx& c) {
     d.NP = c.NP;
     d.emb_rows = kMaxZ;
     d.anomaly = c.anomaly.as<unsigned int>();
+    d.wpack = c.wpack.as<float>();
+    d.NS = c.node_ns;
     return d;
 }
 
@@ -372,19 +377,18 @@ struct Ops {
     void (*loss)(Ctx&);
     void (*backward)(Ctx&, bool general);
     void (*opt)(Ctx&);
+    void (*pack)(Ctx&);
 };
 
 template <int H, int K>
 struct Model {
-    static constexpr size_t kEdgeBase = EdgeSmem<K>::extra_offset;
+    using ES = EdgeKernelSmem<H, K>;
     static constexpr size_t kGemmSmem = NodeGemmSmem<H>::bytes;
     static constexpr size_t kDwuSmem = DwuSmem<H>::bytes;
-    static size_t smem_message() { return kEdgeBase; }
-    static size_t smem_force(int D) { return kEdgeBase + sizeof(float) * (D * H + K * D + kGroups * H); }
-    static size_t smem_head(int D) { return kEdgeBase + sizeof(float) * kGroups * (3 * D * H + D * K); }
-    static size_t smem_bwd(int slot_cap) {
-        return kEdgeBase + sizeof(float) * kGroups * (H * K + static_cast<size_t>(slot_cap) * H);
-    }
+    static size_t smem_message() { return ES::message(); }
+    static size_t smem_force(int D) { return ES::force(D); }
+    static size_t smem_head(int D) { return ES::head(D); }
+    static size_t smem_bwd(int slot_cap) { return ES::bwd(slot_cap); }
 
     static void set_smem(const void* fn, size_t bytes) {
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
@@ -405,6 +409,7 @@ struct Model {
         set_smem((const void*)k_edge_bwd<H, K>, smem_bwd(c.slot_cap_max));
         if (c.D > kGemmMaxHeads) throw InputErr("model: the device path supports at most 16 heads");
         c.grid_upd = c.nsm;            // one tcgen05 CTA per SM, persistent over 128-atom tiles
+        c.node_ns = NodeGemmCfg<H>::NS;
         c.grid_gemm = c.nsm / 2;       // split-K CTAs of dW_u (one partial each)
         // one edge partitioning (k_scan) serves all four edge kernels: size it so
         // every CTA of the heaviest one is resident (no second wave)
@@ -422,7 +427,7 @@ struct Model {
         c.grid_small = c.nsm * 4;
         c.ncta_red = c.nsm;
         c.grid_opt = static_cast<int>(std::min<int64_t>((c.NP + 255) / 256, 4 * c.nsm));
-        c.grid_reduce = static_cast<int>(std::min<int64_t>((c.NP + 255) / 256, 8 * c.nsm));
+        c.grid_reduce = static_cast<int>(std::min<int64_t>((c.NP + 31) / 32, 16 * c.nsm));
     }
 
     static void prep(Ctx& c) {
@@ -441,7 +446,7 @@ struct Model {
         if (c.L == 0) throw InputErr("model: layers == 0 is not supported by the device path");
         for (int l = 0; l < c.L; ++l) {
             launch(c, "message", k_edge_message<H, K>, c.grid_edge, kGroups * H, smem_message(), d, l);
-            launch(c, "update", k_node_gemm<H>, c.grid_upd, 128, kGemmSmem, d, l, 0, l == c.L - 1 ? 1 : 0);
+            launch(c, "update", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 0, l == c.L - 1 ? 1 : 0);
         }
         launch(c, "force", k_edge_force<H, K>, c.grid_edge, kGroups * H, smem_force(c.D), d);
         launch(c, "energy", k_energy, c.grid_small, 128, sizeof(double) * 128 * c.D, d);
@@ -460,8 +465,8 @@ struct Model {
             launch(c, "head_bwd", k_edge_head<H, K>, c.grid_edge, kGroups * H, smem_head(c.D), d, general ? q : -1,
                    q == 0 ? 1 : 0);
         for (int l = c.L - 1; l >= 0; --l) {
-            launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, 128, kGemmSmem, d, l, 1, 0);
-            launch(c, "dwu", k_dwu<H>, c.grid_gemm, 128, kDwuSmem, d, l);
+            launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 1, 0);
+            launch(c, "dwu", k_dwu<H>, c.grid_gemm, 256, kDwuSmem, d, l);
             launch(c, "bwd_edge", k_edge_bwd<H, K>, c.grid_edge, kGroups * H, smem_bwd(c.slot_cap), d, l,
                    c.slot_cap);
         }
@@ -484,9 +489,15 @@ struct Model {
         Dev d = make_dev(c);
         launch(c, "opt_norm", k_opt_norm, c.grid_opt, 256, 0, d, c.opt_G, c.opt_inv_g, c.opt_clip);
         launch(c, "opt_step", k_opt_step, c.grid_opt, 256, 0, d, c.opt_inv_g, c.opt_lr, c.opt_decay, c.opt_eps);
+        pack(c);
     }
 
-    static constexpr Ops ops{setup, prep, nlist, forward, loss, backward, opt};
+    // Packs the tensor-core weight operands from the fp32 working parameters.
+    static void pack(Ctx& c) {
+        launch(c, "pack_weights", k_pack_weights<H>, 2 * c.nsm, 256, 0, make_dev(c));
+    }
+
+    static constexpr Ops ops{setup, prep, nlist, forward, loss, backward, opt, pack};
 };
 
 const Ops* select_ops(int H, int K) {
@@ -815,7 +826,7 @@ LAMM_API void lamm_ctx_destroy(lamm_ctx* c) {
     for (auto& s : c->staged)
         if (s.blob.p) cudaFree(s.blob.p);
     for (Buf* b : {&c->p64, &c->v64, &c->g64, &c->p32, &c->tanh_emb, &c->grads, &c->block_scratch, &c->d_stage,
-                   &c->anomaly, &c->flush})
+                   &c->anomaly, &c->flush, &c->wpack})
         if (b->p) cudaFree(b->p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->h_result) cudaFreeHost(c->h_result);
@@ -860,6 +871,7 @@ LAMM_API int lamm_params_set(lamm_ctx* c, const double* flat, size_t n) {
         Dev d = make_dev(*c);
         k_params_cast<<<c->grid_opt, 256, 0, c->stream>>>(d);
         CK(cudaGetLastError());
+        c->ops->pack(*c);
         CK(cudaStreamSynchronize(c->stream));
         c->fwd_valid = c->loss_valid = false;
     });
@@ -1298,6 +1310,7 @@ LAMM_API int lamm_optimizer_step(lamm_ctx* c, const double* grad_sum, int32_t wo
         CK(cudaGetLastError());
         k_opt_step<<<c->grid_opt, 256, 0, c->stream>>>(d, inv_g, tc->learning_rate, tc->rms_decay, tc->rms_epsilon);
         CK(cudaGetLastError());
+        c->ops->pack(*c);
         const StepHeader h = read_header(*c);
         if (grad_norm) *grad_norm = h.grad_norm;
         c->fwd_valid = c->loss_valid = false;

@@ -11,7 +11,8 @@
 //              rbf          fp32 [P][K]             (fcut * Gaussians of the fp64 distance)
 //   features   t[l], h[l]   fp32 [N][H]  l = 1..L   (t = tanh h; t[0] = tanh(E[Z]))
 //              mu[l]        fp32 [N][H]  l = 0..L-1 (tanh of the message)
-//   heads      e_atom, A    fp32 [N][D]            (per-atom energy, force-head split)
+//   heads      e_atom       fp32 [N][NS][D]        (per-atom energy, one partial per node-GEMM
+//                                                   column split)
 //              F            fp32 [N][D][3]
 //   backward   gh, gm       fp32 [N][H]
 //              Q            fp32 [N][H+K+1]         (per-atom force-head terms)
@@ -78,7 +79,9 @@ struct Dev {
     int32_t *cnt, *row_ptr, *col, *dst;
     int32_t* part_lo;          // [Q+1] edge-balanced atom partitions (edge kernels)
     float4* geo;
-    float* rbf;                // [P][K] fcut * Gaussians
+    float* rbf;                // [P][K] fcut * Gaussians, canonical tcgen05 layout, tf32 hi part
+    float* rbfl;               //        ... and the fp32 lo remainder
+    float* rbfp;               // [P][K] fcut * Gaussians, edge-major (FFMA consumers)
     double *dist64, *unit64;
     int export64;
     // fp32 working parameters
@@ -92,7 +95,7 @@ struct Dev {
     float* t[kMaxLayers + 1];
     float* h[kMaxLayers + 1];
     float* mu[kMaxLayers];
-    float *e_atom, *A, *F;
+    float *e_atom, *F;
     double* Epred;           // [B][D]
     // loss gradients
     float* gE;               // [B][D]
@@ -115,6 +118,8 @@ struct Dev {
     int64_t NP;
     int32_t emb_rows;
     unsigned int* anomaly;   // steps whose update was skipped
+    float* wpack;            // [L][4][H*H] packed tcgen05 weight operands (k_pack_weights)
+    int NS;                  // column splits of the node GEMM: e_atom is [N][NS][D]
 };
 
 __device__ __forceinline__ float warp_sum(float v) {

@@ -2,35 +2,55 @@
 // message, force head, head backward, layer backward), sm_100a.
 //
 // Shape of every kernel: the CSR edge list (grouped by destination atom i, j
-// ascending) is cut into Q = gridDim.x * kGroups edge-balanced partitions of
-// whole atoms. A CTA runs kGroups independent "groups" of H threads; thread a
-// of a group owns feature channel a. A group walks its partition's edges in
-// order: edge metadata (j, i, unit/fcut, fcut*rbf) arrives in shared memory in
-// 128-edge chunks by TMA bulk copies (cp.async.bulk + mbarrier, double
-// buffered); source-atom rows are gathered with one coalesced 4*H-byte load per
-// edge across the group (8 edges in flight per thread); the per-destination
-// segmented sum is a register accumulation flushed when the destination
-// changes. No atomics: parameter-gradient contributions accumulate in
-// thread-owned registers / shared memory and leave the kernel as one per-CTA
-// partial, summed across CTAs in index order by k_grad_reduce.
+// ascending) is cut by k_scan into Q = gridDim.x * kGroups edge-balanced
+// partitions of whole atoms. A CTA runs kGroups independent "groups" of H
+// threads; thread a of a group owns feature channel a. A group walks its
+// partition's edges in order:
+//   * edge metadata (j, i, unit/fcut, fcut*rbf) arrives in shared memory in
+//     64-edge chunks by TMA bulk copies (cp.async.bulk + mbarrier, double
+//     buffered);
+//   * edges are consumed in 8-edge blocks: vector reads of j/i, 8 independent
+//     coalesced source-row gathers per thread issued up front (the CSR is padded
+//     so every staged j is a valid atom), a uniform validity mask, and the
+//     per-destination segmented sum as a register accumulation flushed when the
+//     destination changes;
+//   * for H = 128 the per-edge radial filter W_f (fcut rbf_e) of the message and
+//     of the layer backward runs on the tensor core: the group leader issues
+//     D[a][e] = sum_k W_f[a][k] fcut rbf[e][k] (M = 128 channels = TMEM lanes,
+//     N = 64 edges, K = 16, 3xTF32 tcgen05.mma) for chunk c+1 while the group
+//     drains chunk c, and thread a reads its filter row 8 edges at a time with
+//     tcgen05.ld 32x32b.x8.
+// No atomics: parameter-gradient contributions accumulate in thread-owned
+// registers / shared memory and leave each kernel as one per-CTA partial,
+// summed across CTAs in index order by k_grad_reduce.
 #pragma once
 #include <cuda_runtime.h>
 
 #include "device.cuh"
+#include "umma.cuh"
 
 namespace lamm_b200 {
 
 constexpr int kGroups = 4;   // independent edge streams per CTA
-constexpr int kChunk = 64;   // edges per staged chunk
+constexpr int kChunk = 64;   // edges per staged chunk (= MMA N of the filter)
 constexpr int kStages = 2;   // staging double buffer
-constexpr int kUnroll = 8;   // gathers in flight per thread
+
+// fcut*rbf of the edges for the tensor core: K-major canonical ("interleaved")
+// layout in blocks of 8 edges, element (e, k) at ((e/8)*(K/4) + k/4)*32 +
+// (e%8)*4 + k%4, as a tf32 hi part and an fp32 lo remainder (hi + lo == fcut*rbf).
+template <int K>
+__host__ __device__ __forceinline__ int64_t rbf_idx(int64_t e, int k) {
+    return (((e >> 3) * (K / 4) + (k >> 2)) << 5) + ((e & 7) << 2) + (k & 3);
+}
 
 template <int K>
 struct EdgeStage {
     int32_t col[kChunk];
     int32_t dst[kChunk];
-    float4 geo[kChunk];
-    float fcrbf[kChunk * K];
+    float4 geo[kChunk];     // u_x, u_y, u_z, fcut
+    float fcp[kChunk * K];  // fcut*rbf, edge-major
+    float fch[kChunk * K];  // fcut*rbf, canonical tf32 hi (tensor-core filter)
+    float fcl[kChunk * K];  // fcut*rbf, canonical lo
 };
 
 // --------------------------------------------------------------- PTX glue --
@@ -67,88 +87,47 @@ __device__ __forceinline__ void group_sync(int g, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(nthreads) : "memory");
 }
 
-// Walks the edges of atoms [lo, hi) for one group. Body provides:
-//   struct Reg;                                  per-edge gathered registers
-//   void load(const EdgeStage<K>&, int e, Reg&); issue the edge's gathers
-//   void edge(const EdgeStage<K>&, int e, const Reg&);
-//   void begin(int i); void end(int i);          destination-atom brackets
-template <int H, int K, class Body>
-__device__ __forceinline__ void walk_edges(const Dev& d, EdgeStage<K>* st, uint64_t* bar, int g, int lt, int lo,
-                                           int hi, Body& body) {
-    if (lo >= hi) return;
-    const int e0 = d.row_ptr[lo], e1 = d.row_ptr[hi];
-    int cur = lo;
-    body.begin(cur);
-    if (e1 > e0) {
-        const int base = e0 & ~3;  // 16-byte aligned chunk origin
-        const int nchunks = (e1 - base + kChunk - 1) / kChunk;
-        auto issue = [&](int k) {
-            const int cb = base + k * kChunk;
-            const int n = min(kChunk, ((e1 - cb) + 3) & ~3);
-            EdgeStage<K>& s = st[k % kStages];
-            uint64_t* b = &bar[k % kStages];
-            mbar_expect_tx(b, static_cast<uint32_t>(n * (8 + 16 + 4 * K)));
-            bulk_g2s(s.col, d.col + cb, 4 * n, b);
-            bulk_g2s(s.dst, d.dst + cb, 4 * n, b);
-            bulk_g2s(s.geo, d.geo + cb, 16 * n, b);
-            bulk_g2s(s.fcrbf, d.rbf + static_cast<int64_t>(cb) * K, 4 * K * n, b);
-        };
-        if (lt == 0) {
-            issue(0);
-            if (nchunks > 1) issue(1);
-        }
-        for (int k = 0; k < nchunks; ++k) {
-            mbar_wait(&bar[k % kStages], (k / kStages) & 1);
-            const EdgeStage<K>& s = st[k % kStages];
-            const int cb = base + k * kChunk;
-            const int ea = max(cb, e0) - cb, eb = min(cb + kChunk, e1) - cb;
-            for (int el = ea; el < eb; el += kUnroll) {
-                typename Body::Reg r[kUnroll];
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u)
-                    if (el + u < eb) body.load(s, el + u, r[u]);
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    if (el + u < eb) {
-                        const int i = s.dst[el + u];
-                        while (cur < i) {
-                            body.end(cur);
-                            ++cur;
-                            body.begin(cur);
-                        }
-                        body.edge(s, el + u, r[u]);
-                    }
-                }
-            }
-            group_sync(g, H);  // every thread is done with this stage
-            if (lt == 0 && k + kStages < nchunks) issue(k + kStages);
-        }
-    }
-    body.end(cur);
-    for (int i = cur + 1; i < hi; ++i) {
-        body.begin(i);
-        body.end(i);
+enum StageParts : int { kPartGeo = 1, kPartPlain = 2, kPartCanon = 4 };
+
+// One TMA stage: edges [cb, cb + n), n = min(kChunk, e1 - cb) rounded up to a
+// whole 8-edge block (the tail reads into the CSR padding).
+template <int K>
+__device__ __forceinline__ void stage_chunk(const Dev& d, EdgeStage<K>& s, uint64_t* b, int cb, int e1, int parts) {
+    const int n = min(kChunk, ((e1 - cb) + 7) & ~7);
+    uint32_t bytes = 8u * n;
+    if (parts & kPartGeo) bytes += 16u * n;
+    if (parts & kPartPlain) bytes += 4u * K * n;
+    if (parts & kPartCanon) bytes += 8u * K * n;
+    mbar_expect_tx(b, bytes);
+    bulk_g2s(s.col, d.col + cb, 4 * n, b);
+    bulk_g2s(s.dst, d.dst + cb, 4 * n, b);
+    if (parts & kPartGeo) bulk_g2s(s.geo, d.geo + cb, 16 * n, b);
+    if (parts & kPartPlain) bulk_g2s(s.fcp, d.rbfp + static_cast<int64_t>(cb) * K, 4 * K * n, b);
+    if (parts & kPartCanon) {
+        bulk_g2s(s.fch, d.rbf + static_cast<int64_t>(cb) * K, 4 * K * n, b);
+        bulk_g2s(s.fcl, d.rbfl + static_cast<int64_t>(cb) * K, 4 * K * n, b);
     }
 }
 
 // Shared-memory layout common to the edge kernels: per group kStages staged
-// chunks + barriers, then the kernel's own region.
+// chunks + TMA barriers + filter-MMA barriers, then the kernel's own region.
 template <int K>
 struct EdgeSmem {
     static constexpr size_t stage_bytes = sizeof(EdgeStage<K>) * kStages * kGroups;
-    static constexpr size_t bar_bytes = 16 * kStages * kGroups;
+    static constexpr size_t bar_bytes = 16 * kStages * kGroups * 2 + 16;
     static constexpr size_t extra_offset = stage_bytes + bar_bytes;
 };
 
 template <int H, int K>
 struct EdgeCta {
     EdgeStage<K>* st;
-    uint64_t* bar;
+    uint64_t* bar;   // [kStages] TMA
+    uint64_t* mbar;  // [kStages] filter MMA
+    uint32_t* tslot;
     char* extra;
     int g, lt, lo, hi;
 };
 
-// Common prologue: carve shared memory, init barriers, find the partition.
 template <int H, int K>
 __device__ __forceinline__ EdgeCta<H, K> edge_prologue(const Dev& d) {
     extern __shared__ __align__(128) unsigned char lamm_edge_smem[];
@@ -156,117 +135,293 @@ __device__ __forceinline__ EdgeCta<H, K> edge_prologue(const Dev& d) {
     c.g = threadIdx.x / H;
     c.lt = threadIdx.x % H;
     c.st = reinterpret_cast<EdgeStage<K>*>(lamm_edge_smem) + c.g * kStages;
-    c.bar = reinterpret_cast<uint64_t*>(lamm_edge_smem + EdgeSmem<K>::stage_bytes) + c.g * kStages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(lamm_edge_smem + EdgeSmem<K>::stage_bytes);
+    c.bar = bars + c.g * kStages;
+    c.mbar = bars + kGroups * kStages + c.g * kStages;
+    c.tslot = reinterpret_cast<uint32_t*>(bars + 2 * kGroups * kStages);
     c.extra = reinterpret_cast<char*>(lamm_edge_smem + EdgeSmem<K>::extra_offset);
     if (c.lt == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&c.bar[s], 1);
+        for (int s = 0; s < kStages; ++s) mbar_init(&c.bar[s], 1), mbar_init(&c.mbar[s], 1);
         mbar_fence_init();
     }
     const int q = blockIdx.x * kGroups + c.g;  // partitions cut by k_scan
     c.lo = d.part_lo[q];
     c.hi = d.part_lo[q + 1];
-    __syncthreads();
     return c;
 }
 
+// Tensor-core filter state of a group: W_f as canonical hi/lo K-major tiles in
+// shared memory, this group's 2 x 64 TMEM columns.
+struct FilterTc {
+    const float* Wh;
+    const float* Wl;
+    uint32_t tg;  // TMEM address of the group's first column
+    uint32_t idesc;
+};
+
+template <int K>
+__device__ __forceinline__ void filter_mma(uint32_t tcol, const FilterTc& f, const EdgeStage<K>& s) {
+    umma::fence_after();
+#pragma unroll
+    for (int ks = 0; ks < K / 8; ++ks) {
+        const uint64_t ah = umma::kdesc(f.Wh, ks, K), al = umma::kdesc(f.Wl, ks, K);
+        const uint64_t bh = umma::sdesc(s.fch + ks * 64, 128u, (K / 4) * 128u);
+        const uint64_t bl = umma::sdesc(s.fcl + ks * 64, 128u, (K / 4) * 128u);
+        umma::mma3(tcol, ah, al, bh, bl, f.idesc, ks ? 1u : 0u);
+    }
+}
+
+// Walks the edges of the group's atoms [lo, hi). Body provides:
+//   static constexpr bool kFilter;   tensor-core filter values passed to edge()
+//   static constexpr int  kParts;    staged arrays besides col/dst
+//   struct Reg;  void load(const EdgeStage<K>&, int e, int j, Reg&);
+//   void edge(const EdgeStage<K>&, int e, const Reg&, float filter);
+//   void begin(int i); void end(int i);     destination-atom brackets
+template <int H, int K, class Body>
+__device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c, Body& body, const FilterTc& ft) {
+    constexpr bool kF = Body::kFilter;
+    constexpr int parts = Body::kParts | (kF ? kPartCanon : 0);
+    if (c.lo >= c.hi) return;
+    const int e0 = d.row_ptr[c.lo], e1 = d.row_ptr[c.hi];
+    const bool lead = c.lt == 0;
+    const uint32_t quad = (threadIdx.x >> 5) & 3;
+    int cur = c.lo;
+    body.begin(cur);
+    if (e1 > e0) {
+        const int base = e0 & ~7;  // chunks start on 8-edge blocks
+        const int nchunks = (e1 - base + kChunk - 1) / kChunk;
+        if (lead) {
+            stage_chunk<K>(d, c.st[0], &c.bar[0], base, e1, parts);
+            if (nchunks > 1) stage_chunk<K>(d, c.st[1], &c.bar[1], base + kChunk, e1, parts);
+            if constexpr (kF) {
+                mbar_wait(&c.bar[0], 0);
+                filter_mma<K>(ft.tg, ft, c.st[0]);
+                umma::commit(&c.mbar[0]);
+            }
+        }
+        for (int k = 0; k < nchunks; ++k) {
+            const int s = k & 1;
+            if constexpr (kF) {
+                if (lead && k + 1 < nchunks) {  // next chunk's filter overlaps this chunk's drain
+                    mbar_wait(&c.bar[s ^ 1], ((k + 1) >> 1) & 1);
+                    filter_mma<K>(ft.tg + (s ^ 1) * kChunk, ft, c.st[s ^ 1]);
+                    umma::commit(&c.mbar[s ^ 1]);
+                }
+            }
+            mbar_wait(&c.bar[s], (k >> 1) & 1);
+            if constexpr (kF) {
+                mbar_wait(&c.mbar[s], (k >> 1) & 1);
+                umma::fence_after();
+            }
+            const EdgeStage<K>& st = c.st[s];
+            const int cb = base + k * kChunk;
+            const int ea = max(cb, e0) - cb, eb = min(cb + kChunk, e1) - cb;
+            const uint32_t trow = ft.tg + s * kChunk + (quad * 32u << 16);
+            for (int blk = ea >> 3; blk * 8 < eb; ++blk) {
+                const int4 j0 = reinterpret_cast<const int4*>(st.col)[2 * blk];
+                const int4 j1 = reinterpret_cast<const int4*>(st.col)[2 * blk + 1];
+                const int4 i0 = reinterpret_cast<const int4*>(st.dst)[2 * blk];
+                const int4 i1 = reinterpret_cast<const int4*>(st.dst)[2 * blk + 1];
+                const int jj[8] = {j0.x, j0.y, j0.z, j0.w, j1.x, j1.y, j1.z, j1.w};
+                const int ii[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+                const int ulo = max(ea - blk * 8, 0), uhi = min(eb - blk * 8, 8);
+                typename Body::Reg r[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) body.load(st, blk * 8 + u, jj[u], r[u]);
+                float f[8];
+                if constexpr (kF) {
+                    umma::ld8(trow + blk * 8, f);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) f[u] = 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    if (u >= ulo && u < uhi) {
+                        const int i = ii[u];
+                        if (i != cur) {
+                            do {
+                                body.end(cur);
+                                ++cur;
+                                body.begin(cur);
+                            } while (cur < i);
+                        }
+                        body.edge(st, blk * 8 + u, r[u], f[u]);
+                    }
+                }
+            }
+            if constexpr (kF) umma::fence_before();
+            group_sync(c.g, H);  // every thread is done with this stage (smem + TMEM)
+            if (lead && k + 2 < nchunks) stage_chunk<K>(d, c.st[s], &c.bar[s], base + (k + 2) * kChunk, e1, parts);
+        }
+    }
+    body.end(cur);
+    for (int i = cur + 1; i < c.hi; ++i) {
+        body.begin(i);
+        body.end(i);
+    }
+}
+
+// Loads W_f of layer l as canonical hi/lo tiles and allocates the CTA's TMEM
+// (all 512 columns: kGroups x 2 stages x 64). Call from all threads.
+template <int H, int K>
+__device__ __forceinline__ FilterTc filter_setup(const Dev& d, const EdgeCta<H, K>& c, int l, float* Wh, float* Wl) {
+    if (threadIdx.x < 32) umma::tmem_alloc(c.tslot, 512);
+    const float* __restrict__ wf = d.wf[l];
+    for (int idx = threadIdx.x; idx < H * K; idx += blockDim.x) {
+        const int a = idx / K, k = idx % K;
+        umma::split_tf32(wf[idx], Wh[umma::kidx(a, k, K)], Wl[umma::kidx(a, k, K)]);
+    }
+    umma::fence_proxy_async();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    return FilterTc{Wh, Wl, *c.tslot + static_cast<uint32_t>(c.g * 2 * kChunk), umma::idesc_tf32(128, kChunk)};
+}
+
+__device__ __forceinline__ void filter_teardown(const uint32_t* tslot) {
+    umma::fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) umma::tmem_dealloc(*tslot, 512);
+}
+
+template <int K>
+__device__ __forceinline__ float filter_ffma(const float (&w)[K], const EdgeStage<K>& s, int e) {
+    const float4* fr = reinterpret_cast<const float4*>(s.fcp + e * K);
+    float f = 0.f;
+#pragma unroll
+    for (int k4 = 0; k4 < K / 4; ++k4) {
+        const float4 q = fr[k4];
+        f = fmaf(w[4 * k4], q.x, f);
+        f = fmaf(w[4 * k4 + 1], q.y, f);
+        f = fmaf(w[4 * k4 + 2], q.z, f);
+        f = fmaf(w[4 * k4 + 3], q.w, f);
+    }
+    return f;
+}
+
+template <int H, int K>
+struct EdgeKernelSmem {
+    static constexpr bool TC = H == 128;
+    static constexpr size_t base = EdgeSmem<K>::extra_offset;
+    static constexpr size_t filter = TC ? 4 * 2 * H * K : 0;
+    static constexpr size_t one_cta = 120 * 1024;  // > half the SM: one CTA owns the 512 TMEM columns
+    static size_t pad(size_t b) { return TC && b < one_cta ? one_cta : b; }
+    static size_t message() { return pad(base + filter); }
+    static size_t force(int D) { return base + 4 * (3 * D * H + kGroups * (H / 32) * 96); }
+    static size_t head(int D) { return base + 4 * kGroups * (3 * D * H + D * K); }
+    static size_t bwd(int slot_cap) { return pad(base + filter + 4 * kGroups * (H * K + slot_cap * H)); }
+};
+
 // ---------------------------------------------------------------- message --
 // m_i[a] = sum_j t_j[a] * sum_k Wf[a,k] fcut_ij rbf_ijk ; mu_i = tanh(m_i)   (S/model.cpp:78-93)
-template <int H, int K>
+template <int H, int K, bool TC>
 struct MessageBody {
+    static constexpr bool kFilter = TC;
+    static constexpr int kParts = TC ? 0 : kPartPlain;
     struct Reg {
         float t;
     };
     const Dev& d;
     const float* __restrict__ tsrc;
+    float* mu;
     int l, a;
     float w[K];
     float m;
-    __device__ void load(const EdgeStage<K>& s, int e, Reg& r) const {
-        const int j = s.col[e];
+    __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
         const int row = l == 0 ? __ldg(d.Z + j) - 1 : j;
         r.t = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
     }
-    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r) {
-        const float4* fr = reinterpret_cast<const float4*>(s.fcrbf + e * K);
-        float f = 0.f;
-#pragma unroll
-        for (int k4 = 0; k4 < K / 4; ++k4) {
-            const float4 q = fr[k4];
-            f = fmaf(w[4 * k4], q.x, f);
-            f = fmaf(w[4 * k4 + 1], q.y, f);
-            f = fmaf(w[4 * k4 + 2], q.z, f);
-            f = fmaf(w[4 * k4 + 3], q.w, f);
-        }
+    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f) {
+        if constexpr (!TC) f = filter_ffma<K>(w, s, e);
         m = fmaf(r.t, f, m);
     }
     __device__ void begin(int) { m = 0.f; }
-    __device__ void end(int i) { d.mu[l][static_cast<int64_t>(i) * H + a] = tanhf(m); }
+    __device__ void end(int i) { mu[static_cast<int64_t>(i) * H + a] = tanhf(m); }
 };
 
 template <int H, int K>
-__global__ void __launch_bounds__(kGroups* H) k_edge_message(Dev d, int l) {
+__global__ void __launch_bounds__(kGroups* H, 1) k_edge_message(Dev d, int l) {
+    constexpr bool TC = EdgeKernelSmem<H, K>::TC;
     EdgeCta<H, K> c = edge_prologue<H, K>(d);
-    MessageBody<H, K> b{d, l == 0 ? d.tanh_emb : d.t[l], l, c.lt};
+    FilterTc ft{};
+    if constexpr (TC) {
+        float* Wh = reinterpret_cast<float*>(c.extra);
+        ft = filter_setup<H, K>(d, c, l, Wh, Wh + H * K);
+    } else {
+        __syncthreads();
+    }
+    MessageBody<H, K, TC> b{d, l == 0 ? d.tanh_emb : d.t[l], d.mu[l], l, c.lt};
+    if constexpr (!TC) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) b.w[k] = d.wf[l][c.lt * K + k];
-    walk_edges<H, K>(d, c.st, c.bar, c.g, c.lt, c.lo, c.hi, b);
+        for (int k = 0; k < K; ++k) b.w[k] = d.wf[l][c.lt * K + k];
+    }
+    walk_edges<H, K>(d, c, b, ft);
+    if constexpr (TC) filter_teardown(c.tslot);
 }
 
 // ------------------------------------------------------------ force head --
-// F_i^d = sum_j [ (A_i^d + A_j^d) fcut + sum_k Wc[k,d] fcut rbf_k ] u_ij
-//       + sum_a Wb[a,d] T_ia Y_i[a],  Y_i[a] = sum_j T_ja fcut_ij u_ij     (S/model.cpp:223-253)
-// Thread lt < 3D also owns output (d, x) = (lt / 3, lt % 3) of the scalar part.
+// F_i^d = sum_j w_ijd fcut_ij u_ij with w_ijd = A_i^d + A_j^d + sum_a Wb[a,d] T_ia T_ja
+// + sum_k Wc[k,d] rbf_ijk and A = T Wa (S/model.cpp:223-253), re-associated per
+// destination atom so that every edge costs one T_j gather and 3 FMAs:
+//   Y_i[a] = sum_j T_ja fcut u_ij,  U_i = sum_j fcut u_ij,  V_i[k] = sum_j fcut rbf_ijk u_ij
+//   F_i^d = sum_a [ Wa[a,d] (T_ia U_i + Y_i[a]) + Wb[a,d] T_ia Y_i[a] ] + sum_k Wc[k,d] V_i[k]
+// (sum_j A_j^d fcut u_ij = sum_a Wa[a,d] Y_i[a]). The 3D outputs per atom are one
+// group reduction (warp reduce-scatter + shared memory across the group's warps).
 template <int H, int K>
 struct ForceBody {
+    static constexpr bool kFilter = false;
+    static constexpr int kParts = kPartGeo | kPartPlain;
     struct Reg {
-        float t, aj;
+        float t;
     };
     const Dev& d;
     const float* __restrict__ T;
-    const float* WbT;  // smem [D][H]
-    const float* Wc;   // smem [K][D]
-    float* red;        // smem [H/32][32] group reduction scratch
+    const float* W;  // smem [3][D][H]: Wa^T, Wb^T, Wc^T (rows k < K)
+    float* red;      // smem [H/32][96] group reduction scratch
     int a, g, D, ND, L;
-    int dd, xx;
-    float Ti, Y0, Y1, Y2, Fs, Ai;
-    __device__ void load(const EdgeStage<K>& s, int e, Reg& r) const {
-        const int j = s.col[e];
+    float Ti, Y0, Y1, Y2, U0, U1, U2, V0, V1, V2;
+    __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
         const int row = L > 0 ? j : __ldg(d.Z + j) - 1;
         r.t = __ldg(T + static_cast<int64_t>(row) * H + a);
-        r.aj = a < ND ? __ldg(d.A + static_cast<int64_t>(j) * D + dd) : 0.f;
     }
-    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r) {
+    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float) {
         const float4 gv = s.geo[e];
         const float tf = r.t * gv.w;
         Y0 = fmaf(tf, gv.x, Y0);
         Y1 = fmaf(tf, gv.y, Y1);
         Y2 = fmaf(tf, gv.z, Y2);
-        if (a < ND) {
-            float wc = 0.f;
-            const float* fr = s.fcrbf + e * K;
-#pragma unroll
-            for (int k = 0; k < K; ++k) wc = fmaf(Wc[k * D + dd], fr[k], wc);
-            const float ux = xx == 0 ? gv.x : (xx == 1 ? gv.y : gv.z);
-            Fs = fmaf(fmaf(Ai + r.aj, gv.w, wc), ux, Fs);
+        U0 = fmaf(gv.w, gv.x, U0);
+        U1 = fmaf(gv.w, gv.y, U1);
+        U2 = fmaf(gv.w, gv.z, U2);
+        if (a < K) {
+            const float fr = s.fcp[e * K + a];
+            V0 = fmaf(fr, gv.x, V0);
+            V1 = fmaf(fr, gv.y, V1);
+            V2 = fmaf(fr, gv.z, V2);
         }
     }
     __device__ void begin(int i) {
         const int row = L > 0 ? i : __ldg(d.Z + i) - 1;
         Ti = __ldg(T + static_cast<int64_t>(row) * H + a);
-        Y0 = Y1 = Y2 = Fs = 0.f;
-        Ai = a < ND ? d.A[static_cast<int64_t>(i) * D + dd] : 0.f;
+        Y0 = Y1 = Y2 = U0 = U1 = U2 = V0 = V1 = V2 = 0.f;
     }
     __device__ void end(int i) {
         const int lane = a & 31, warp = a >> 5;
-        const float y[3] = {Y0, Y1, Y2};
-        float total = 0.f;
+        const float ya[3] = {fmaf(Ti, U0, Y0), fmaf(Ti, U1, Y1), fmaf(Ti, U2, Y2)};
+        const float yb[3] = {Ti * Y0, Ti * Y1, Ti * Y2};
+        const float vk[3] = {V0, V1, V2};
         for (int r0 = 0; r0 < ND; r0 += 32) {
             float v[32];
 #pragma unroll
             for (int k = 0; k < 32; ++k) {
                 const int idx = r0 + k;
                 float s = 0.f;
-                if (idx < ND) s = WbT[(idx / 3) * H + a] * Ti * y[idx % 3];
+                if (idx < ND) {
+                    const int dd = idx / 3, x = idx % 3;
+                    s = fmaf(W[dd * H + a], ya[x], W[(D + dd) * H + a] * yb[x]);
+                    if (a < K) s = fmaf(W[(2 * D + dd) * H + a], vk[x], s);
+                }
                 v[k] = s;
             }
 #pragma unroll
@@ -279,35 +434,34 @@ struct ForceBody {
                     v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                 }
             }
-            red[warp * 32 + lane] = v[0];
-            group_sync(g, H);
-            if (a >= r0 && a < r0 + 32 && a < ND) {
-                float t = 0.f;
-                for (int w = 0; w < H / 32; ++w) t += red[w * 32 + (a - r0)];
-                total = t;
-            }
-            group_sync(g, H);
+            red[warp * 96 + r0 + lane] = v[0];
         }
-        if (a < ND) d.F[static_cast<int64_t>(i) * ND + a] = Fs + total;
+        group_sync(g, H);
+        if (a < ND) {
+            float t = 0.f;
+            for (int w = 0; w < H / 32; ++w) t += red[w * 96 + a];
+            d.F[static_cast<int64_t>(i) * ND + a] = t;
+        }
+        group_sync(g, H);
     }
 };
 
 template <int H, int K>
-__global__ void __launch_bounds__(kGroups* H) k_edge_force(Dev d) {
+__global__ void __launch_bounds__(kGroups* H, 1) k_edge_force(Dev d) {
     EdgeCta<H, K> c = edge_prologue<H, K>(d);
     const int D = d.D;
-    float* WbT = reinterpret_cast<float*>(c.extra);  // [D][H]
-    float* Wc = WbT + D * H;                          // [K][D]
-    float* red = Wc + K * D + c.g * H;                // [kGroups][H]
-    for (int idx = threadIdx.x; idx < D * H; idx += blockDim.x) {
-        const int dd = idx / H, a = idx % H;
-        WbT[idx] = d.wfh[(H + a) * D + dd];
+    float* W = reinterpret_cast<float*>(c.extra);  // [3][D][H]
+    float* red = W + 3 * D * H + c.g * (H / 32) * 96;
+    for (int idx = threadIdx.x; idx < 3 * D * H; idx += blockDim.x) {
+        const int part = idx / (D * H), dd = (idx / H) % D, a = idx % H;
+        float w = 0.f;
+        if (part < 2) w = d.wfh[(part * H + a) * D + dd];
+        else if (a < K) w = d.wfh[(2 * H + a) * D + dd];
+        W[idx] = w;
     }
-    for (int idx = threadIdx.x; idx < K * D; idx += blockDim.x) Wc[idx] = d.wfh[2 * H * D + idx];
     __syncthreads();
-    ForceBody<H, K> b{d, d.L > 0 ? d.t[d.L] : d.tanh_emb, WbT, Wc, red, c.lt, c.g, D, 3 * D, d.L};
-    b.dd = c.lt / 3, b.xx = c.lt % 3;
-    walk_edges<H, K>(d, c.st, c.bar, c.g, c.lt, c.lo, c.hi, b);
+    ForceBody<H, K> b{d, d.L > 0 ? d.t[d.L] : d.tanh_emb, W, red, c.lt, c.g, D, 3 * D, d.L};
+    walk_edges<H, K>(d, c, b, FilterTc{});
 }
 
 // --------------------------------------------------------- head backward --
@@ -319,6 +473,8 @@ __global__ void __launch_bounds__(kGroups* H) k_edge_force(Dev d) {
 //   dWe[:,d] += h^L_i gE_s[d]      (per-CTA partials, thread-owned columns)
 template <int H, int K>
 struct HeadBody {
+    static constexpr bool kFilter = false;
+    static constexpr int kParts = kPartGeo | kPartPlain;
     struct Reg {
         float t, g0, g1, g2;
     };
@@ -329,23 +485,22 @@ struct HeadBody {
     int a, D, L, pass_ch, first;
     int s, ch;
     float Ti, S, W, R, gf0, gf1, gf2;
-    __device__ void load(const EdgeStage<K>& st, int e, Reg& r) const {
-        const int j = st.col[e];
+    __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
         const int row = L > 0 ? j : __ldg(d.Z + j) - 1;
         r.t = __ldg(T + static_cast<int64_t>(row) * H + a);
-        // channel of the edge's own sample (the unrolled window may run ahead of begin())
+        // channel of the edge's own sample (the block may run ahead of begin())
         const int chj = pass_ch >= 0 ? pass_ch : __ldg(d.chan + j);
         const float* gp = d.gF + (static_cast<int64_t>(j) * D + chj) * 3;
         r.g0 = __ldg(gp), r.g1 = __ldg(gp + 1), r.g2 = __ldg(gp + 2);
     }
-    __device__ void edge(const EdgeStage<K>& st, int e, const Reg& r) {
+    __device__ void edge(const EdgeStage<K>& st, int e, const Reg& r, float) {
         const float4 gv = st.geo[e];
         const float di = gf0 * gv.x + gf1 * gv.y + gf2 * gv.z;
         const float dj = r.g0 * gv.x + r.g1 * gv.y + r.g2 * gv.z;
         const float sij = gv.w * (di - dj);
         S += sij;
         W = fmaf(sij, r.t, W);
-        if (a < K) R = fmaf(di, st.fcrbf[e * K + a], R);
+        if (a < K) R = fmaf(di, st.fcp[e * K + a], R);
     }
     __device__ void begin(int i) {
         s = d.sample_of[i];
@@ -379,17 +534,17 @@ struct HeadBody {
 };
 
 template <int H, int K>
-__global__ void __launch_bounds__(kGroups* H) k_edge_head(Dev d, int pass_ch, int first) {
+__global__ void __launch_bounds__(kGroups* H, 1) k_edge_head(Dev d, int pass_ch, int first) {
     EdgeCta<H, K> c = edge_prologue<H, K>(d);
     const int D = d.D;
     const int AW = 3 * D * H + D * K;  // per-group accumulator floats
     float* accs = reinterpret_cast<float*>(c.extra);
     float* acc = accs + c.g * AW;
     for (int e = c.lt; e < AW; e += H) acc[e] = 0.f;
-    group_sync(c.g, H);
+    __syncthreads();
     HeadBody<H, K> b{d, d.L > 0 ? d.t[d.L] : d.tanh_emb, d.L > 0 ? d.h[d.L] : d.emb, acc, c.lt, D, d.L, pass_ch,
                      first};
-    walk_edges<H, K>(d, c.st, c.bar, c.g, c.lt, c.lo, c.hi, b);
+    walk_edges<H, K>(d, c, b, FilterTc{});
     __syncthreads();
     // combine groups in order; emit the CTA partial in parameter layout:
     //   [ (2H+K) x D force head | H x D energy head ]
@@ -410,10 +565,13 @@ __global__ void __launch_bounds__(kGroups* H) k_edge_head(Dev d, int pass_ch, in
 
 // ------------------------------------------------------- layer backward --
 // Gather form of S/model.cpp:393-418 for layer l:
-//   gt_i = sum_j gm_j (.) filter_ij ;  dWf[a,k] += gm_ia t_ja fcut_ij rbf_ijk ;
+//   gt_i = sum_j gm_j (.) filter_ij        (filter symmetric in i, j)
+//   dWf[a,k] += gm_ia t_ja fcut_ij rbf_ijk (per-thread registers, CTA-reduced)
 //   gh_i += gt_i (.) (1 - t_i^2) ; on layer 0 also dE[Z_i] += gh_i (S/model.cpp:421-424).
-template <int H, int K>
+template <int H, int K, bool TC>
 struct BwdBody {
+    static constexpr bool kFilter = TC;
+    static constexpr int kParts = kPartPlain;
     struct Reg {
         float gm, t;
     };
@@ -423,27 +581,24 @@ struct BwdBody {
     int l, a;
     float w[K], dw[K];
     float gmi, gt;
-    __device__ void load(const EdgeStage<K>& s, int e, Reg& r) const {
-        const int j = s.col[e];
+    __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
         r.gm = __ldg(d.gm + static_cast<int64_t>(j) * H + a);
         const int row = l == 0 ? __ldg(d.Z + j) - 1 : j;
         r.t = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
     }
-    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r) {
-        const float4* fr = reinterpret_cast<const float4*>(s.fcrbf + e * K);
-        float q[K];
-#pragma unroll
-        for (int k4 = 0; k4 < K / 4; ++k4) {
-            const float4 v = fr[k4];
-            q[4 * k4] = v.x, q[4 * k4 + 1] = v.y, q[4 * k4 + 2] = v.z, q[4 * k4 + 3] = v.w;
-        }
-        float f = 0.f;
-#pragma unroll
-        for (int k = 0; k < K; ++k) f = fmaf(w[k], q[k], f);
+    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f) {
+        if constexpr (!TC) f = filter_ffma<K>(w, s, e);
         gt = fmaf(r.gm, f, gt);
         const float gg = gmi * r.t;
+        const float4* fr = reinterpret_cast<const float4*>(s.fcp + e * K);
 #pragma unroll
-        for (int k = 0; k < K; ++k) dw[k] = fmaf(gg, q[k], dw[k]);
+        for (int k4 = 0; k4 < K / 4; ++k4) {
+            const float4 q = fr[k4];
+            dw[4 * k4] = fmaf(gg, q.x, dw[4 * k4]);
+            dw[4 * k4 + 1] = fmaf(gg, q.y, dw[4 * k4 + 1]);
+            dw[4 * k4 + 2] = fmaf(gg, q.z, dw[4 * k4 + 2]);
+            dw[4 * k4 + 3] = fmaf(gg, q.w, dw[4 * k4 + 3]);
+        }
     }
     __device__ void begin(int i) {
         gmi = d.gm[static_cast<int64_t>(i) * H + a];
@@ -460,21 +615,32 @@ struct BwdBody {
 };
 
 template <int H, int K>
-__global__ void __launch_bounds__(kGroups* H) k_edge_bwd(Dev d, int l, int slot_cap) {
+__global__ void __launch_bounds__(kGroups* H, 1) k_edge_bwd(Dev d, int l, int slot_cap) {
+    constexpr bool TC = EdgeKernelSmem<H, K>::TC;
     EdgeCta<H, K> c = edge_prologue<H, K>(d);
-    float* red = reinterpret_cast<float*>(c.extra);          // [kGroups][H*K]
-    float* emb = red + kGroups * H * K;                      // [kGroups][slot_cap][H]
+    float* Wh = reinterpret_cast<float*>(c.extra);
+    float* red = Wh + (TC ? 2 * H * K : 0);  // [kGroups][H*K]
+    float* emb = red + kGroups * H * K;      // [kGroups][slot_cap][H]
     const int ns = d.hdr->nslots;
     if (l == 0)
         for (int e = c.lt; e < ns * H; e += H) emb[c.g * slot_cap * H + e] = 0.f;
-    group_sync(c.g, H);
-    BwdBody<H, K> b{d, l == 0 ? d.tanh_emb : d.t[l], emb + c.g * slot_cap * H, l, c.lt};
+    FilterTc ft{};
+    if constexpr (TC) {
+        ft = filter_setup<H, K>(d, c, l, Wh, Wh + H * K);
+    } else {
+        __syncthreads();
+    }
+    BwdBody<H, K, TC> b{d, l == 0 ? d.tanh_emb : d.t[l], emb + c.g * slot_cap * H, l, c.lt};
 #pragma unroll
-    for (int k = 0; k < K; ++k) b.w[k] = d.wf[l][c.lt * K + k], b.dw[k] = 0.f;
-    walk_edges<H, K>(d, c.st, c.bar, c.g, c.lt, c.lo, c.hi, b);
+    for (int k = 0; k < K; ++k) b.w[k] = TC ? 0.f : d.wf[l][c.lt * K + k], b.dw[k] = 0.f;
+    walk_edges<H, K>(d, c, b, ft);
 #pragma unroll
     for (int k = 0; k < K; ++k) red[c.g * H * K + c.lt * K + k] = b.dw[k];
-    __syncthreads();
+    if constexpr (TC) {
+        filter_teardown(c.tslot);
+    } else {
+        __syncthreads();
+    }
     float* part = d.part_wf[l] + static_cast<int64_t>(blockIdx.x) * H * K;
     for (int e = threadIdx.x; e < H * K; e += blockDim.x) {
         float s = 0.f;

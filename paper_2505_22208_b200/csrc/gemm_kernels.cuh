@@ -2,8 +2,8 @@
 // tensor cores (3xTF32, fp32-accurate), accumulators in TMEM.
 //
 //   k_node_gemm mode 0 (update, S/model.cpp:93-102):   Y = mu_l W_u^T   (M = 128 atoms, N = H, K = H)
-//               epilogue h_{l+1} = h_l + Y, t_{l+1} = tanh h_{l+1}; last layer also
-//               e_i = W_e^T h^L_i and A_i = W_fh[0:H]^T t^L_i   (S/model.cpp:208-218, 232-240)
+//               epilogue h_{l+1} = h_l + Y, t_{l+1} = tanh h_{l+1}; last layer also the
+//               per-atom energy e_i = W_e^T h^L_i   (S/model.cpp:208-218)
 //   k_node_gemm mode 1 (S/model.cpp:380-390):          gm = (gh W_u) (.) (1 - mu^2)
 //   k_dwu              (S/model.cpp:381-383):          dW_u = gh^T mu, split-K over atoms
 //                                                       (one per-CTA partial, summed by k_grad_reduce)
@@ -28,123 +28,168 @@ constexpr int kGemmM = 128;      // atoms per tile (TMEM lanes)
 constexpr int kGemmKC = 32;      // K chunk of the staged activations
 constexpr int kGemmMaxHeads = 16;
 
+// Column split of a node-GEMM tile: for H = 128 two CTAs share a 128-atom
+// tile (64 output columns each) so small batches still fill the GPU.
 template <int H>
-struct NodeGemmSmem {
-    static constexpr size_t b_floats = 2 * H * H;                    // W hi | lo
-    static constexpr size_t a_floats = 2 * 2 * kGemmM * kGemmKC;     // 2 stages x (hi | lo)
-    static constexpr size_t heads_floats = 2 * H * kGemmMaxHeads;    // W_e | W_fh[0:H] (last layer)
-    static constexpr size_t bytes = 4 * (b_floats + a_floats + heads_floats) + 64;
+struct NodeGemmCfg {
+    static constexpr int NS = H == 128 ? 2 : 1;
+    static constexpr int NC = H / NS;                       // output columns per CTA tile
+    static constexpr size_t a_floats = 2 * kGemmM * H;      // activation tile hi | lo (full K)
+    static constexpr size_t b_floats = 2 * NC * H;          // weight rows [NC][H] hi | lo
+    static constexpr size_t heads_floats = NC * kGemmMaxHeads;
+    static constexpr size_t red_floats = kGemmM * kGemmMaxHeads;
+    static constexpr size_t bytes = 4 * (a_floats + b_floats + heads_floats + red_floats) + 64;
 };
-
-// Stages rows [base, base+128) x cols [k0, k0+KC) of a row-major [N][H] fp32
-// array into hi/lo K-major canonical tiles (rows >= N are zero).
 template <int H>
-__device__ __forceinline__ void stage_rows(const float* __restrict__ src, int N, int base, int k0, float* Ahi,
-                                           float* Alo) {
-    constexpr int Q = kGemmKC / 4;
-    for (int q = threadIdx.x; q < kGemmM * Q; q += blockDim.x) {
-        const int m = q / Q, k4 = q % Q, atom = base + m;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (atom < N) v = *reinterpret_cast<const float4*>(src + static_cast<int64_t>(atom) * H + k0 + 4 * k4);
-        float4 hi, lo;
-        umma::split_tf32(v.x, hi.x, lo.x);
-        umma::split_tf32(v.y, hi.y, lo.y);
-        umma::split_tf32(v.z, hi.z, lo.z);
-        umma::split_tf32(v.w, hi.w, lo.w);
-        const int o = umma::kidx(m, 4 * k4, kGemmKC);
-        *reinterpret_cast<float4*>(Ahi + o) = hi;
-        *reinterpret_cast<float4*>(Alo + o) = lo;
+using NodeGemmSmem = NodeGemmCfg<H>;
+
+// Weight operands of the node GEMMs, packed once per parameter update by
+// k_pack_weights: per layer [4][H*H] = {W_u hi, W_u lo, W_u^T hi, W_u^T lo}.
+// Each is split into NS row blocks of NC rows, every block a K-major canonical
+// [NC][H] tile (B[n][k] = W_u[n][k] for the update, W_u[k][n] for gm), hi and
+// lo blocks adjacent, so a CTA fetches its operand with one TMA bulk copy.
+template <int H>
+__global__ void __launch_bounds__(256) k_pack_weights(Dev d) {
+    constexpr int NC = NodeGemmCfg<H>::NC;
+    const int64_t per = static_cast<int64_t>(H) * H;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < d.L * per;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int l = static_cast<int>(e / per), idx = static_cast<int>(e % per);
+        const int n = idx / H, k = idx % H;
+        const float* wu = d.wu[l];
+        const int blk = n / NC, o = umma::kidx(n % NC, k, H);
+        // layout per layer and mode: [block][hi | lo][NC*H]
+        float* upd = d.wpack + 4 * per * l + static_cast<int64_t>(blk) * 2 * NC * H;
+        float* gm = upd + 2 * per;
+        umma::split_tf32(wu[idx], upd[o], upd[NC * H + o]);
+        umma::split_tf32(wu[k * H + n], gm[o], gm[NC * H + o]);
     }
 }
 
+// One tile = 128 atoms x NC output columns, K = H, 256 threads: the whole
+// activation tile is staged at once (16 independent float4 loads per thread),
+// the weight block arrives by TMA, 3*H/8 MMAs accumulate into TMEM, and the
+// epilogue inputs (residual / mu) are prefetched while the tensor core runs.
+// Warps w and w+4 share TMEM lanes 32*(w%4).. and split the NC columns.
 template <int H>
-__global__ void __launch_bounds__(128, 1) k_node_gemm(Dev d, int l, int mode, int last) {
-    static_assert(H % kGemmKC == 0 && H >= 32 && H <= 128, "node GEMM supports H in {32, 64, 128}");
-    constexpr int NKC = H / kGemmKC;
+__global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, int last) {
+    using Cfg = NodeGemmCfg<H>;
+    constexpr int NS = Cfg::NS, NC = Cfg::NC, CW = NC / 2;  // columns per thread
+    static_assert(CW % 16 == 0, "epilogue reads 16 columns at a time");
     float* sm = dyn_smem<float>();
-    float* Bhi = sm;
-    float* Blo = Bhi + H * H;
-    float* Ast = Blo + H * H;
-    float* We = Ast + 2 * 2 * kGemmM * kGemmKC;
-    float* Wa = We + H * kGemmMaxHeads;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(Wa + H * kGemmMaxHeads);
+    float* Ahi = sm;
+    float* Alo = Ahi + kGemmM * H;
+    float* Bhi = Alo + kGemmM * H;
+    float* We = Bhi + Cfg::b_floats;
+    float* red = We + NC * kGemmMaxHeads;  // [128][kGemmMaxHeads] energy partials of column half 1
+    uint64_t* bar = reinterpret_cast<uint64_t*>(red + Cfg::red_floats);  // [0] weights TMA, [1] MMA done
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int quad = warp & 3, half = warp >> 2;
     const int D = d.D;
-    if (warp == 0) umma::tmem_alloc(tslot, H);
+    constexpr uint32_t kCols = NC < 32 ? 32 : NC;
+    if (warp == 0) umma::tmem_alloc(tslot, kCols);
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         mbar_fence_init();
     }
-    const float* __restrict__ wu = d.wu[l];
-    for (int idx = tid; idx < H * H; idx += blockDim.x) {
-        const int n = idx / H, k = idx % H;  // B[n][k]: update W_u[n][k]; gm W_u[k][n]
-        float hi, lo;
-        umma::split_tf32(mode == 0 ? wu[idx] : wu[k * H + n], hi, lo);
-        Bhi[umma::kidx(n, k, H)] = hi;
-        Blo[umma::kidx(n, k, H)] = lo;
-    }
-    if (last)
-        for (int idx = tid; idx < H * D; idx += blockDim.x) We[idx] = d.we[idx], Wa[idx] = d.wfh[idx];
-    umma::fence_proxy_async();
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
     const uint32_t tbase = *tslot;
-    const uint32_t idesc = umma::idesc_tf32(kGemmM, H);
+    const uint32_t idesc = umma::idesc_tf32(kGemmM, NC);
     const int N = d.hdr->N;
-    const int ntiles = (N + kGemmM - 1) / kGemmM;
+    const int ntiles = (N + kGemmM - 1) / kGemmM * NS;
     const float* __restrict__ src = mode == 0 ? d.mu[l] : d.gh;
-    int chunk = 0;
+    uint32_t wphase = 0, mphase = 0;
+    int loaded_np = -1;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int base = tile * kGemmM;
-        for (int kc = 0; kc < NKC; ++kc, ++chunk) {
-            const int st = chunk & 1;
-            if (chunk >= 2) mbar_wait(&bar[st], ((chunk - 2) >> 1) & 1);  // MMAs that read this stage are done
-            float* Ahi = Ast + st * 2 * kGemmM * kGemmKC;
-            float* Alo = Ahi + kGemmM * kGemmKC;
-            stage_rows<H>(src, N, base, kc * kGemmKC, Ahi, Alo);
-            umma::fence_proxy_async();
-            __syncthreads();
+        const int at = tile / NS, np = tile % NS, base = at * kGemmM;
+        const bool new_w = np != loaded_np;
+        if (new_w) {  // weight block of this column split (TMA)
             if (tid == 0) {
-                umma::fence_after();
+                const float* wsrc = d.wpack + static_cast<int64_t>(4 * l + 2 * mode) * H * H +
+                                    static_cast<int64_t>(np) * 2 * NC * H;
+                mbar_expect_tx(&bar[0], static_cast<uint32_t>(Cfg::b_floats * 4));
+                bulk_g2s(Bhi, wsrc, static_cast<uint32_t>(Cfg::b_floats * 4), &bar[0]);
+            }
+            if (last)
+                for (int idx = tid; idx < NC * D; idx += blockDim.x) We[idx] = d.we[np * NC * D + idx];
+        }
+        // stage the full activation tile (hi/lo), all loads first
+        {
+            constexpr int Q = H / 4, IT = kGemmM * Q / 256;
+            float4 v[IT];
 #pragma unroll
-                for (int s = 0; s < kGemmKC / 8; ++s) {
-                    const int sg = kc * (kGemmKC / 8) + s;
-                    umma::mma3(tbase, umma::kdesc(Ahi, s, kGemmKC), umma::kdesc(Alo, s, kGemmKC),
-                               umma::kdesc(Bhi, sg, H), umma::kdesc(Blo, sg, H), idesc, (kc | s) ? 1u : 0u);
-                }
-                umma::commit(&bar[st]);
+            for (int it = 0; it < IT; ++it) {
+                const int q = tid + 256 * it, m = q / Q, k4 = q % Q, atom = base + m;
+                v[it] = atom < N
+                            ? __ldg(reinterpret_cast<const float4*>(src + static_cast<int64_t>(atom) * H + 4 * k4))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int it = 0; it < IT; ++it) {
+                const int q = tid + 256 * it, m = q / Q, k4 = q % Q;
+                float4 hi, lo;
+                umma::split_tf32(v[it].x, hi.x, lo.x);
+                umma::split_tf32(v[it].y, hi.y, lo.y);
+                umma::split_tf32(v[it].z, hi.z, lo.z);
+                umma::split_tf32(v[it].w, hi.w, lo.w);
+                const int o = umma::kidx(m, 4 * k4, H);
+                *reinterpret_cast<float4*>(Ahi + o) = hi;
+                *reinterpret_cast<float4*>(Alo + o) = lo;
             }
         }
-        const int lc = chunk - 1;
-        mbar_wait(&bar[lc & 1], (lc >> 1) & 1);
-        umma::fence_after();
-        const int row = warp * 32 + lane, atom = base + row;
-        const bool live = atom < N;
-        float eacc[kGemmMaxHeads], aacc[kGemmMaxHeads];
+        umma::fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            if (new_w) {
+                mbar_wait(&bar[0], wphase);
+                wphase ^= 1u;
+            }
+            umma::fence_after();
+            const float* Blo = Bhi + NC * H;
 #pragma unroll
-        for (int q = 0; q < kGemmMaxHeads; ++q) eacc[q] = aacc[q] = 0.f;
-#pragma unroll 1
-        for (int c0 = 0; c0 < H; c0 += 16) {
+            for (int s = 0; s < H / 8; ++s)
+                umma::mma3(tbase, umma::kdesc(Ahi, s, H), umma::kdesc(Alo, s, H), umma::kdesc(Bhi, s, H),
+                           umma::kdesc(Blo, s, H), idesc, s ? 1u : 0u);
+            umma::commit(&bar[1]);
+        }
+        loaded_np = np;
+        // epilogue inputs for this thread's row/columns, fetched while the MMAs run
+        const int row = quad * 32 + lane, atom = base + row, c0 = np * NC + half * CW;
+        const bool live = atom < N;
+        float pre[CW];
+#pragma unroll
+        for (int q = 0; q < CW; ++q) pre[q] = 0.f;
+        if (live) {
+            const float* p = mode == 0 ? (l == 0 ? d.emb + static_cast<int64_t>(__ldg(d.Z + atom) - 1) * H
+                                                 : d.h[l] + static_cast<int64_t>(atom) * H)
+                                       : d.mu[l] + static_cast<int64_t>(atom) * H;
+#pragma unroll
+            for (int q = 0; q < CW; q += 4) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(p + c0 + q));
+                pre[q] = x.x, pre[q + 1] = x.y, pre[q + 2] = x.z, pre[q + 3] = x.w;
+            }
+        }
+        mbar_wait(&bar[1], mphase);
+        mphase ^= 1u;
+        umma::fence_after();
+        float eacc[kGemmMaxHeads];
+#pragma unroll
+        for (int q = 0; q < kGemmMaxHeads; ++q) eacc[q] = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < CW; cc += 16) {
             float v[16];
-            umma::ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+            umma::ld16(tbase + (static_cast<uint32_t>(quad * 32) << 16) + half * CW + cc, v);
             if (!live) continue;
             if (mode == 0) {
-                const float* hp = l == 0 ? d.emb + static_cast<int64_t>(__ldg(d.Z + atom) - 1) * H
-                                         : d.h[l] + static_cast<int64_t>(atom) * H;
                 float hn[16], tn[16];
 #pragma unroll
-                for (int q = 0; q < 16; q += 4) {
-                    const float4 hv = *reinterpret_cast<const float4*>(hp + c0 + q);
-                    hn[q] = hv.x + v[q], hn[q + 1] = hv.y + v[q + 1], hn[q + 2] = hv.z + v[q + 2],
-                    hn[q + 3] = hv.w + v[q + 3];
-                }
-#pragma unroll
-                for (int q = 0; q < 16; ++q) tn[q] = tanhf(hn[q]);
-                float* ho = d.h[l + 1] + static_cast<int64_t>(atom) * H + c0;
-                float* to = d.t[l + 1] + static_cast<int64_t>(atom) * H + c0;
+                for (int q = 0; q < 16; ++q) hn[q] = pre[cc + q] + v[q], tn[q] = tanhf(hn[q]);
+                float* ho = d.h[l + 1] + static_cast<int64_t>(atom) * H + c0 + cc;
+                float* to = d.t[l + 1] + static_cast<int64_t>(atom) * H + c0 + cc;
 #pragma unroll
                 for (int q = 0; q < 16; q += 4) {
                     *reinterpret_cast<float4*>(ho + q) = make_float4(hn[q], hn[q + 1], hn[q + 2], hn[q + 3]);
@@ -153,39 +198,40 @@ __global__ void __launch_bounds__(128, 1) k_node_gemm(Dev d, int l, int mode, in
                 if (last) {
 #pragma unroll
                     for (int q = 0; q < 16; ++q) {
-                        const float* we = We + (c0 + q) * D;
-                        const float* wa = Wa + (c0 + q) * D;
+                        const float* we = We + (half * CW + cc + q) * D;
 #pragma unroll
                         for (int dd = 0; dd < kGemmMaxHeads; ++dd)
-                            if (dd < D) eacc[dd] = fmaf(hn[q], we[dd], eacc[dd]), aacc[dd] = fmaf(tn[q], wa[dd], aacc[dd]);
+                            if (dd < D) eacc[dd] = fmaf(hn[q], we[dd], eacc[dd]);
                     }
                 }
             } else {
-                const float* mp = d.mu[l] + static_cast<int64_t>(atom) * H + c0;
-                float* go = d.gm + static_cast<int64_t>(atom) * H + c0;
+                float* go = d.gm + static_cast<int64_t>(atom) * H + c0 + cc;
 #pragma unroll
-                for (int q = 0; q < 16; q += 4) {
-                    const float4 m4 = *reinterpret_cast<const float4*>(mp + q);
+                for (int q = 0; q < 16; q += 4)
                     *reinterpret_cast<float4*>(go + q) =
-                        make_float4(v[q] * (1.f - m4.x * m4.x), v[q + 1] * (1.f - m4.y * m4.y),
-                                    v[q + 2] * (1.f - m4.z * m4.z), v[q + 3] * (1.f - m4.w * m4.w));
-                }
+                        make_float4(v[q] * (1.f - pre[cc + q] * pre[cc + q]),
+                                    v[q + 1] * (1.f - pre[cc + q + 1] * pre[cc + q + 1]),
+                                    v[q + 2] * (1.f - pre[cc + q + 2] * pre[cc + q + 2]),
+                                    v[q + 3] * (1.f - pre[cc + q + 3] * pre[cc + q + 3]));
             }
         }
-        if (mode == 0 && last && live) {
-#pragma unroll
-            for (int dd = 0; dd < kGemmMaxHeads; ++dd)
-                if (dd < D) {
-                    d.e_atom[static_cast<int64_t>(atom) * D + dd] = eacc[dd];
-                    d.A[static_cast<int64_t>(atom) * D + dd] = aacc[dd];
-                }
+        if (mode == 0 && last) {
+            // partial energy over this CTA's NC columns: the two column halves meet
+            // in shared memory; the NS splits land in separate slots of e_atom
+            // ([N][NS][D]) that k_energy sums in a fixed order
+            if (half == 1)
+                for (int dd = 0; dd < D; ++dd) red[row * kGemmMaxHeads + dd] = eacc[dd];
+            __syncthreads();
+            if (half == 0 && live)
+                for (int dd = 0; dd < D; ++dd)
+                    d.e_atom[(static_cast<int64_t>(atom) * NS + np) * D + dd] = eacc[dd] + red[row * kGemmMaxHeads + dd];
         }
         umma::fence_before();
-        __syncthreads();  // accumulator drained before the next tile's first MMA
+        __syncthreads();  // accumulator and activation tile drained before the next tile
         umma::fence_after();
     }
     __syncthreads();
-    if (warp == 0) umma::tmem_dealloc(tbase, H);
+    if (warp == 0) umma::tmem_dealloc(tbase, kCols);
 }
 
 template <int H>
@@ -195,22 +241,27 @@ struct DwuSmem {
 };
 
 // dW_u[b][a] = sum_atoms gh[atom][b] mu[atom][a]: M = b (rows >= H zero), N = H,
-// K = atoms in 32-atom chunks; CTA c reduces a contiguous chunk range.
+// K = atoms in 32-atom chunks (double buffered); CTA c reduces a contiguous
+// chunk range into one TMEM accumulator and writes one [H][H] partial.
+// Staging: thread -> (column b, 4 consecutive atoms), coalesced scalar loads
+// across the warp, one 16-byte store per operand into the canonical tile.
 template <int H>
-__global__ void __launch_bounds__(128, 1) k_dwu(Dev d, int l) {
-    constexpr int Q = H / 4;
+__global__ void __launch_bounds__(256, 1) k_dwu(Dev d, int l) {
+    constexpr int TPC = 256 / H;                   // threads per column
+    constexpr int GPT = (kGemmKC / 4) / TPC;       // 4-atom groups per thread
+    constexpr uint32_t kCols = H < 32 ? 32 : H;
     float* sm = dyn_smem<float>();
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 2 * DwuSmem<H>::stage_floats);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (warp == 0) umma::tmem_alloc(tslot, H);
+    const int quad = warp & 3, half = warp >> 2;
+    if (warp == 0) umma::tmem_alloc(tslot, kCols);
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         mbar_fence_init();
     }
-    // rows H..127 of the A tiles stay zero
-    for (int e = tid; e < 2 * DwuSmem<H>::stage_floats; e += blockDim.x) sm[e] = 0.f;
+    for (int e = tid; e < 2 * DwuSmem<H>::stage_floats; e += blockDim.x) sm[e] = 0.f;  // rows >= H stay 0
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
@@ -222,6 +273,7 @@ __global__ void __launch_bounds__(128, 1) k_dwu(Dev d, int l) {
     const int c1 = static_cast<int>((static_cast<int64_t>(nch) * (blockIdx.x + 1)) / gridDim.x);
     const float* __restrict__ gh = d.gh;
     const float* __restrict__ mu = d.mu[l];
+    const int col = tid % H, g0 = tid / H;
     int q = 0;
     for (int ch = c0; ch < c1; ++ch, ++q) {
         const int st = q & 1;
@@ -230,20 +282,32 @@ __global__ void __launch_bounds__(128, 1) k_dwu(Dev d, int l) {
         float* Alo = Ahi + kGemmM * kGemmKC;
         float* Bhi = Alo + kGemmM * kGemmKC;
         float* Blo = Bhi + kGemmM * kGemmKC;
-        for (int it = tid; it < kGemmKC * Q; it += blockDim.x) {
-            const int al = it / Q, c4 = it % Q, atom = ch * kGemmKC + al;
-            float4 g = make_float4(0.f, 0.f, 0.f, 0.f), m = g;
-            if (atom < N) {
-                g = *reinterpret_cast<const float4*>(gh + static_cast<int64_t>(atom) * H + 4 * c4);
-                m = *reinterpret_cast<const float4*>(mu + static_cast<int64_t>(atom) * H + 4 * c4);
-            }
-            const float gv[4] = {g.x, g.y, g.z, g.w}, mv[4] = {m.x, m.y, m.z, m.w};
+        float gv[GPT][4], mv[GPT][4];
+#pragma unroll
+        for (int gi = 0; gi < GPT; ++gi)
 #pragma unroll
             for (int r = 0; r < 4; ++r) {
-                const int o = umma::kidx(4 * c4 + r, al, kGemmKC);
-                umma::split_tf32(gv[r], Ahi[o], Alo[o]);
-                umma::split_tf32(mv[r], Bhi[o], Blo[o]);
+                const int atom = ch * kGemmKC + 4 * (g0 + TPC * gi) + r;
+                const bool ok = atom < N;
+                gv[gi][r] = ok ? __ldg(gh + static_cast<int64_t>(atom) * H + col) : 0.f;
+                mv[gi][r] = ok ? __ldg(mu + static_cast<int64_t>(atom) * H + col) : 0.f;
             }
+#pragma unroll
+        for (int gi = 0; gi < GPT; ++gi) {
+            const int o = umma::kidx(col, 4 * (g0 + TPC * gi), kGemmKC);
+            float4 h4, l4, hm, lm;
+            umma::split_tf32(gv[gi][0], h4.x, l4.x);
+            umma::split_tf32(gv[gi][1], h4.y, l4.y);
+            umma::split_tf32(gv[gi][2], h4.z, l4.z);
+            umma::split_tf32(gv[gi][3], h4.w, l4.w);
+            umma::split_tf32(mv[gi][0], hm.x, lm.x);
+            umma::split_tf32(mv[gi][1], hm.y, lm.y);
+            umma::split_tf32(mv[gi][2], hm.z, lm.z);
+            umma::split_tf32(mv[gi][3], hm.w, lm.w);
+            *reinterpret_cast<float4*>(Ahi + o) = h4;
+            *reinterpret_cast<float4*>(Alo + o) = l4;
+            *reinterpret_cast<float4*>(Bhi + o) = hm;
+            *reinterpret_cast<float4*>(Blo + o) = lm;
         }
         umma::fence_proxy_async();
         __syncthreads();
@@ -261,21 +325,22 @@ __global__ void __launch_bounds__(128, 1) k_dwu(Dev d, int l) {
         mbar_wait(&bar[(q - 1) & 1], ((q - 1) >> 1) & 1);
         umma::fence_after();
     }
-    const int row = warp * 32 + lane;
+    const int row = quad * 32 + lane;
+    constexpr int CW = H / 2;
     float* part = d.part_wu[l] + static_cast<int64_t>(blockIdx.x) * H * H;
-#pragma unroll 1
-    for (int c = 0; c < H; c += 16) {
+#pragma unroll
+    for (int c = 0; c < CW; c += 16) {
         float v[16];
-        umma::ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+        umma::ld16(tbase + (static_cast<uint32_t>(quad * 32) << 16) + half * CW + c, v);
         if (row < H)
 #pragma unroll
             for (int k = 0; k < 16; k += 4)
-                *reinterpret_cast<float4*>(part + row * H + c + k) =
+                *reinterpret_cast<float4*>(part + row * H + half * CW + c + k) =
                     q > 0 ? make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     umma::fence_before();
     __syncthreads();
-    if (warp == 0) umma::tmem_dealloc(tbase, H);
+    if (warp == 0) umma::tmem_dealloc(tbase, kCols);
 }
 
 }  // namespace lamm_b200

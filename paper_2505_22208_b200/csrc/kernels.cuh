@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include "device.cuh"
+#include "edge_kernels.cuh"
+#include "umma.cuh"
 
 namespace lamm_b200 {
 
@@ -209,6 +211,9 @@ __global__ void __launch_bounds__(1024) k_scan(Dev d, int Q) {
     }
     if (P == 0)
         for (int q = t; q < Q; q += 1024) d.part_lo[q] = 0;
+    // CSR padding read by the edge kernels' block staging: valid source atom 0
+    if (P <= d.Pcap)
+        for (int x = t; x < kChunk + 8; x += 1024) d.col[P + x] = 0, d.dst[P + x] = N;
     if (t == 1023) {
         d.row_ptr[N] = run;
         d.part_lo[Q] = N;
@@ -258,9 +263,19 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d) {
                     const double dd = r - width * static_cast<double>(k);
                     rb[k] = static_cast<float>(fc * exp(-dd * dd * inv));  // fcut folded in
                 }
-                float4* dst = reinterpret_cast<float4*>(d.rbf + static_cast<int64_t>(p) * K);
 #pragma unroll
-                for (int k = 0; k < K / 4; ++k) dst[k] = make_float4(rb[4 * k], rb[4 * k + 1], rb[4 * k + 2], rb[4 * k + 3]);
+                for (int q = 0; q < K / 4; ++q) {  // canonical tcgen05 layout, tf32 hi + fp32 lo
+                    float4 hi, lo;
+                    umma::split_tf32(rb[4 * q], hi.x, lo.x);
+                    umma::split_tf32(rb[4 * q + 1], hi.y, lo.y);
+                    umma::split_tf32(rb[4 * q + 2], hi.z, lo.z);
+                    umma::split_tf32(rb[4 * q + 3], hi.w, lo.w);
+                    const int64_t o = rbf_idx<K>(p, 4 * q);
+                    *reinterpret_cast<float4*>(d.rbf + o) = hi;
+                    *reinterpret_cast<float4*>(d.rbfl + o) = lo;
+                    *reinterpret_cast<float4*>(d.rbfp + static_cast<int64_t>(p) * K + 4 * q) =
+                        make_float4(rb[4 * q], rb[4 * q + 1], rb[4 * q + 2], rb[4 * q + 3]);
+                }
                 if (d.export64) {
                     d.dist64[p] = r;
                     d.unit64[3 * static_cast<int64_t>(p)] = ux;
@@ -292,7 +307,11 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
         const int64_t lo = d.atom_ptr[s], hi = d.atom_ptr[s + 1];
         for (int dd = 0; dd < D; ++dd) red[dd * 128 + threadIdx.x] = 0.0;
         for (int64_t a = lo + threadIdx.x; a < hi; a += 128)
-            for (int dd = 0; dd < D; ++dd) red[dd * 128 + threadIdx.x] += static_cast<double>(d.e_atom[a * D + dd]);
+            for (int dd = 0; dd < D; ++dd) {
+                float e = 0.f;
+                for (int q = 0; q < d.NS; ++q) e += d.e_atom[(a * d.NS + q) * D + dd];
+                red[dd * 128 + threadIdx.x] += static_cast<double>(e);
+            }
         __syncthreads();
         for (int o = 64; o > 0; o >>= 1) {
             if (threadIdx.x < o)
@@ -399,27 +418,41 @@ struct SegTable {
     Seg s[2 * kMaxLayers + 4];
 };
 
-// grads[e] = sum over CTAs (index order) of the partials of the tensor that
-// owns flat index e (for_each_tensor order).
+// grads[e] = sum over CTAs of the partials of the tensor that owns flat index e
+// (for_each_tensor order). Block = 32 consecutive elements x 8 CTA-strided
+// partial streams (coalesced loads, 8 independent sums per element), combined
+// in a fixed order: deterministic for a fixed grid.
 __global__ void __launch_bounds__(256) k_grad_reduce(Dev d, SegTable tab) {
+    __shared__ float red[8][33];
     const int H = d.H;
-    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int ns = d.hdr->nslots;
-    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < d.NP; e += stride) {
-        int q = 0;
-        while (q + 1 < tab.nseg && e >= tab.s[q + 1].dst) ++q;
-        const Seg& sg = tab.s[q];
-        const int64_t off = e - sg.dst;
+    const int k = threadIdx.x & 31, g = threadIdx.x >> 5;
+    for (int64_t e0 = static_cast<int64_t>(blockIdx.x) * 32; e0 < d.NP; e0 += static_cast<int64_t>(gridDim.x) * 32) {
+        const int64_t e = e0 + k;
         float acc = 0.f;
-        if (sg.kind == 1) {
-            const int zrow = static_cast<int>(off / H), a = static_cast<int>(off % H);
-            const int slot = d.z_to_slot[zrow + 1];
-            if (slot >= 0)
-                for (int c = 0; c < sg.ncta; ++c) acc += sg.src[static_cast<int64_t>(c) * ns * H + slot * H + a];
-        } else {
-            for (int c = 0; c < sg.ncta; ++c) acc += sg.src[static_cast<int64_t>(c) * sg.stride + off];
+        if (e < d.NP) {
+            int q = 0;
+            while (q + 1 < tab.nseg && e >= tab.s[q + 1].dst) ++q;
+            const Seg& sg = tab.s[q];
+            const int64_t off = e - sg.dst;
+            if (sg.kind == 1) {
+                const int zrow = static_cast<int>(off / H), a = static_cast<int>(off % H);
+                const int slot = d.z_to_slot[zrow + 1];
+                if (slot >= 0)
+                    for (int c = g; c < sg.ncta; c += 8) acc += sg.src[static_cast<int64_t>(c) * ns * H + slot * H + a];
+            } else {
+                for (int c = g; c < sg.ncta; c += 8) acc += sg.src[static_cast<int64_t>(c) * sg.stride + off];
+            }
         }
-        d.grads[e] = acc;
+        red[g][k] = acc;
+        __syncthreads();
+        if (g == 0 && e < d.NP) {
+            float s = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) s += red[q][k];
+            d.grads[e] = s;
+        }
+        __syncthreads();
     }
 }
 
