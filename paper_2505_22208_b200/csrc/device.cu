@@ -220,6 +220,7 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     for (int l = 0; l < L; ++l) ensure_buf(c, "mu" + std::to_string(l), 4 * static_cast<size_t>(Nc) * H, changed);
     ensure_buf(c, "e_atom", 4 * Nc * D * c.node_ns, changed);
     ensure_buf(c, "F", 12 * Nc * D, changed);
+    ensure_buf(c, "Yf", 4 * static_cast<size_t>(Nc) * (3 * H + 3 + 3 * K), changed);
     ensure_buf(c, "Epred", 8 * Bc * D, changed);
     ensure_buf(c, "gE", 4 * Bc * D, changed);
     ensure_buf(c, "gF", 12 * Nc * D, changed);
@@ -292,6 +293,7 @@ Dev make_dev(Ctx& c) {
     for (int l = 0; l < L; ++l) d.mu[l] = buf(c, "mu" + std::to_string(l)).as<float>();
     d.e_atom = buf(c, "e_atom").as<float>();
     d.F = buf(c, "F").as<float>();
+    d.Yf = buf(c, "Yf").as<float>();
     d.Epred = buf(c, "Epred").as<double>();
     d.gE = buf(c, "gE").as<float>();
     d.gF = buf(c, "gF").as<float>();
@@ -449,6 +451,7 @@ struct Model {
             launch(c, "update", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 0, l == c.L - 1 ? 1 : 0);
         }
         launch(c, "force", k_edge_force<H, K>, c.grid_edge, kGroups * H, smem_force(c.D), d);
+        launch(c, "force_out", k_force_out<H, K>, c.grid_warp, 256, 0, d);
         launch(c, "energy", k_energy, c.grid_small, 128, sizeof(double) * 128 * c.D, d);
     }
 

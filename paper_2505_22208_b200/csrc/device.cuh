@@ -96,6 +96,7 @@ struct Dev {
     float* h[kMaxLayers + 1];
     float* mu[kMaxLayers];
     float *e_atom, *F;
+    float* Yf;               // [N][3H + 3 + 3K] per-atom force-head features (k_edge_force)
     double* Epred;           // [B][D]
     // loss gradients
     float* gE;               // [B][D]

@@ -175,7 +175,9 @@ __device__ __forceinline__ void filter_mma(uint32_t tcol, const FilterTc& f, con
 //   static constexpr bool kFilter;   tensor-core filter values passed to edge()
 //   static constexpr int  kParts;    staged arrays besides col/dst
 //   struct Reg;  void load(const EdgeStage<K>&, int e, int j, Reg&);
-//   void edge(const EdgeStage<K>&, int e, const Reg&, float filter);
+//   void edge(const EdgeStage<K>&, int e, const Reg&, float filter, float w);
+//        (w is 1 for the edges of the current segment, 0 otherwise: bodies must
+//        be linear in w so masked edges contribute exactly nothing)
 //   void begin(int i); void end(int i);     destination-atom brackets
 template <int H, int K, class Body>
 __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c, Body& body, const FilterTc& ft) {
@@ -217,17 +219,31 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
             const int cb = base + k * kChunk;
             const int ea = max(cb, e0) - cb, eb = min(cb + kChunk, e1) - cb;
             const uint32_t trow = ft.tg + s * kChunk + (quad * 32u << 16);
-            for (int blk = ea >> 3; blk * 8 < eb; ++blk) {
-                const int4 j0 = reinterpret_cast<const int4*>(st.col)[2 * blk];
-                const int4 j1 = reinterpret_cast<const int4*>(st.col)[2 * blk + 1];
-                const int4 i0 = reinterpret_cast<const int4*>(st.dst)[2 * blk];
-                const int4 i1 = reinterpret_cast<const int4*>(st.dst)[2 * blk + 1];
+            // gathers of block b+1 are issued before block b is consumed
+            typename Body::Reg rn[8];
+            const int blk0 = ea >> 3, blk1 = (eb + 7) >> 3;
+            {
+                const int4 j0 = reinterpret_cast<const int4*>(st.col)[2 * blk0];
+                const int4 j1 = reinterpret_cast<const int4*>(st.col)[2 * blk0 + 1];
                 const int jj[8] = {j0.x, j0.y, j0.z, j0.w, j1.x, j1.y, j1.z, j1.w};
-                const int ii[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
-                const int ulo = max(ea - blk * 8, 0), uhi = min(eb - blk * 8, 8);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) body.load(st, blk0 * 8 + u, jj[u], rn[u]);
+            }
+            for (int blk = blk0; blk < blk1; ++blk) {
                 typename Body::Reg r[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) body.load(st, blk * 8 + u, jj[u], r[u]);
+                for (int u = 0; u < 8; ++u) r[u] = rn[u];
+                if (blk + 1 < blk1) {
+                    const int4 j0 = reinterpret_cast<const int4*>(st.col)[2 * blk + 2];
+                    const int4 j1 = reinterpret_cast<const int4*>(st.col)[2 * blk + 3];
+                    const int jj[8] = {j0.x, j0.y, j0.z, j0.w, j1.x, j1.y, j1.z, j1.w};
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) body.load(st, (blk + 1) * 8 + u, jj[u], rn[u]);
+                }
+                const int4 i0 = reinterpret_cast<const int4*>(st.dst)[2 * blk];
+                const int4 i1 = reinterpret_cast<const int4*>(st.dst)[2 * blk + 1];
+                const int ii[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+                const int ulo = max(ea - blk * 8, 0), uhi = min(eb - blk * 8, 8);
                 float f[8];
                 if constexpr (kF) {
                     umma::ld8(trow + blk * 8, f);
@@ -235,19 +251,28 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
 #pragma unroll
                     for (int u = 0; u < 8; ++u) f[u] = 0.f;
                 }
+                // destination segments of the block: one flush call site per
+                // block (keeps end()/begin() inlined once), branch-free edges
+                const unsigned vm = ((1u << uhi) - 1u) & ~((1u << ulo) - 1u);
+                unsigned seg = 1u << ulo;
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (u >= ulo && u < uhi) {
-                        const int i = ii[u];
-                        if (i != cur) {
-                            do {
-                                body.end(cur);
-                                ++cur;
-                                body.begin(cur);
-                            } while (cur < i);
-                        }
-                        body.edge(st, blk * 8 + u, r[u], f[u]);
+                for (int u = 1; u < 8; ++u) seg |= (ii[u] != ii[u - 1] ? 1u : 0u) << u;
+                seg &= vm;
+                while (seg) {
+                    const int u0 = __ffs(seg) - 1;
+                    seg &= seg - 1u;
+                    const int u1 = seg ? __ffs(seg) - 1 : uhi;
+                    const int i = st.dst[blk * 8 + u0];
+                    if (i != cur) {
+                        do {
+                            body.end(cur);
+                            ++cur;
+                            body.begin(cur);
+                        } while (cur < i);
                     }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        body.edge(st, blk * 8 + u, r[u], f[u], (u >= u0 && u < u1) ? 1.f : 0.f);
                 }
             }
             if constexpr (kF) umma::fence_before();
@@ -308,7 +333,7 @@ struct EdgeKernelSmem {
     static constexpr size_t one_cta = 120 * 1024;  // > half the SM: one CTA owns the 512 TMEM columns
     static size_t pad(size_t b) { return TC && b < one_cta ? one_cta : b; }
     static size_t message() { return pad(base + filter); }
-    static size_t force(int D) { return base + 4 * (3 * D * H + kGroups * (H / 32) * 96); }
+    static size_t force(int) { return base; }
     static size_t head(int D) { return base + 4 * kGroups * (3 * D * H + D * K); }
     static size_t bwd(int slot_cap) { return pad(base + filter + 4 * kGroups * (H * K + slot_cap * H)); }
 };
@@ -332,9 +357,9 @@ struct MessageBody {
         const int row = l == 0 ? __ldg(d.Z + j) - 1 : j;
         r.t = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
     }
-    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f) {
+    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f, float wt) {
         if constexpr (!TC) f = filter_ffma<K>(w, s, e);
-        m = fmaf(r.t, f, m);
+        m = fmaf(r.t * wt, f, m);
     }
     __device__ void begin(int) { m = 0.f; }
     __device__ void end(int i) { mu[static_cast<int64_t>(i) * H + a] = tanhf(m); }
@@ -366,51 +391,84 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_message(Dev d, int l) {
 // destination atom so that every edge costs one T_j gather and 3 FMAs:
 //   Y_i[a] = sum_j T_ja fcut u_ij,  U_i = sum_j fcut u_ij,  V_i[k] = sum_j fcut rbf_ijk u_ij
 //   F_i^d = sum_a [ Wa[a,d] (T_ia U_i + Y_i[a]) + Wb[a,d] T_ia Y_i[a] ] + sum_k Wc[k,d] V_i[k]
-// (sum_j A_j^d fcut u_ij = sum_a Wa[a,d] Y_i[a]). The 3D outputs per atom are one
-// group reduction (warp reduce-scatter + shared memory across the group's warps).
+// (sum_j A_j^d fcut u_ij = sum_a Wa[a,d] Y_i[a]). k_edge_force walks the edges
+// and writes the per-atom features Yf[i] = [Y (H x 3) | U (3) | V (K x 3)];
+// k_force_out contracts them with the head weights, warp per atom.
 template <int H, int K>
 struct ForceBody {
     static constexpr bool kFilter = false;
     static constexpr int kParts = kPartGeo | kPartPlain;
+    static constexpr int kYW = 3 * H + 3 + 3 * K;  // per-atom feature floats
     struct Reg {
         float t;
     };
     const Dev& d;
     const float* __restrict__ T;
-    const float* W;  // smem [3][D][H]: Wa^T, Wb^T, Wc^T (rows k < K)
-    float* red;      // smem [H/32][96] group reduction scratch
-    int a, g, D, ND, L;
-    float Ti, Y0, Y1, Y2, U0, U1, U2, V0, V1, V2;
+    int a, L;
+    float Y0, Y1, Y2, U0, U1, U2, V0, V1, V2;
     __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
         const int row = L > 0 ? j : __ldg(d.Z + j) - 1;
         r.t = __ldg(T + static_cast<int64_t>(row) * H + a);
     }
-    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float) {
+    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float, float wt) {
         const float4 gv = s.geo[e];
-        const float tf = r.t * gv.w;
+        const float fw = gv.w * wt;
+        const float tf = r.t * fw;
         Y0 = fmaf(tf, gv.x, Y0);
         Y1 = fmaf(tf, gv.y, Y1);
         Y2 = fmaf(tf, gv.z, Y2);
-        U0 = fmaf(gv.w, gv.x, U0);
-        U1 = fmaf(gv.w, gv.y, U1);
-        U2 = fmaf(gv.w, gv.z, U2);
+        U0 = fmaf(fw, gv.x, U0);
+        U1 = fmaf(fw, gv.y, U1);
+        U2 = fmaf(fw, gv.z, U2);
         if (a < K) {
-            const float fr = s.fcp[e * K + a];
+            const float fr = s.fcp[e * K + a] * wt;
             V0 = fmaf(fr, gv.x, V0);
             V1 = fmaf(fr, gv.y, V1);
             V2 = fmaf(fr, gv.z, V2);
         }
     }
-    __device__ void begin(int i) {
-        const int row = L > 0 ? i : __ldg(d.Z + i) - 1;
-        Ti = __ldg(T + static_cast<int64_t>(row) * H + a);
-        Y0 = Y1 = Y2 = U0 = U1 = U2 = V0 = V1 = V2 = 0.f;
-    }
+    __device__ void begin(int) { Y0 = Y1 = Y2 = U0 = U1 = U2 = V0 = V1 = V2 = 0.f; }
     __device__ void end(int i) {
-        const int lane = a & 31, warp = a >> 5;
-        const float ya[3] = {fmaf(Ti, U0, Y0), fmaf(Ti, U1, Y1), fmaf(Ti, U2, Y2)};
-        const float yb[3] = {Ti * Y0, Ti * Y1, Ti * Y2};
-        const float vk[3] = {V0, V1, V2};
+        float* y = d.Yf + static_cast<int64_t>(i) * kYW;
+        y[a] = Y0, y[H + a] = Y1, y[2 * H + a] = Y2;
+        if (a == 0) y[3 * H] = U0, y[3 * H + 1] = U1, y[3 * H + 2] = U2;
+        if (a < K) y[3 * H + 3 + a] = V0, y[3 * H + 3 + K + a] = V1, y[3 * H + 3 + 2 * K + a] = V2;
+    }
+};
+
+template <int H, int K>
+__global__ void __launch_bounds__(kGroups* H, 1) k_edge_force(Dev d) {
+    EdgeCta<H, K> c = edge_prologue<H, K>(d);
+    __syncthreads();
+    ForceBody<H, K> b{d, d.L > 0 ? d.t[d.L] : d.tanh_emb, c.lt, d.L};
+    walk_edges<H, K>(d, c, b, FilterTc{});
+}
+
+// F_i[d][x] from the per-atom features, warp per atom: lane owns channels
+// [lane*C, lane*C+C) and k = lane (< K); 3D partial sums per lane, one warp
+// reduce-scatter (lane o ends with output o), coalesced store of F_i.
+template <int H, int K>
+__global__ void __launch_bounds__(256) k_force_out(Dev d) {
+    constexpr int C = H / 32, YW = ForceBody<H, K>::kYW;
+    const int D = d.D, ND = 3 * D, L = d.L;
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const float* __restrict__ T = L > 0 ? d.t[L] : d.tanh_emb;
+    const float* __restrict__ wfh = d.wfh;
+    const int N = d.hdr->N;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
+        const float* y = d.Yf + static_cast<int64_t>(i) * YW;
+        const int row = L > 0 ? i : __ldg(d.Z + i) - 1;
+        float ti[C], yv[3][C];
+#pragma unroll
+        for (int cc = 0; cc < C; ++cc) {
+            const int aa = lane * C + cc;
+            ti[cc] = __ldg(T + static_cast<int64_t>(row) * H + aa);
+            yv[0][cc] = y[aa], yv[1][cc] = y[H + aa], yv[2][cc] = y[2 * H + aa];
+        }
+        const float u[3] = {y[3 * H], y[3 * H + 1], y[3 * H + 2]};
+        float vk[3] = {0.f, 0.f, 0.f};
+        if (lane < K) vk[0] = y[3 * H + 3 + lane], vk[1] = y[3 * H + 3 + K + lane], vk[2] = y[3 * H + 3 + 2 * K + lane];
         for (int r0 = 0; r0 < ND; r0 += 32) {
             float v[32];
 #pragma unroll
@@ -418,9 +476,16 @@ struct ForceBody {
                 const int idx = r0 + k;
                 float s = 0.f;
                 if (idx < ND) {
-                    const int dd = idx / 3, x = idx % 3;
-                    s = fmaf(W[dd * H + a], ya[x], W[(D + dd) * H + a] * yb[x]);
-                    if (a < K) s = fmaf(W[(2 * D + dd) * H + a], vk[x], s);
+                    const int dd = idx / 3, x = idx - 3 * (idx / 3);
+#pragma unroll
+                    for (int cc = 0; cc < C; ++cc) {
+                        const int aa = lane * C + cc;
+                        const float yx = x == 0 ? yv[0][cc] : (x == 1 ? yv[1][cc] : yv[2][cc]);
+                        const float ux = x == 0 ? u[0] : (x == 1 ? u[1] : u[2]);
+                        s = fmaf(__ldg(wfh + aa * D + dd), fmaf(ti[cc], ux, yx), s);
+                        s = fmaf(__ldg(wfh + (H + aa) * D + dd), ti[cc] * yx, s);
+                    }
+                    if (lane < K) s = fmaf(__ldg(wfh + (2 * H + lane) * D + dd), x == 0 ? vk[0] : (x == 1 ? vk[1] : vk[2]), s);
                 }
                 v[k] = s;
             }
@@ -434,34 +499,9 @@ struct ForceBody {
                     v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                 }
             }
-            red[warp * 96 + r0 + lane] = v[0];
+            if (r0 + lane < ND) d.F[static_cast<int64_t>(i) * ND + r0 + lane] = v[0];
         }
-        group_sync(g, H);
-        if (a < ND) {
-            float t = 0.f;
-            for (int w = 0; w < H / 32; ++w) t += red[w * 96 + a];
-            d.F[static_cast<int64_t>(i) * ND + a] = t;
-        }
-        group_sync(g, H);
     }
-};
-
-template <int H, int K>
-__global__ void __launch_bounds__(kGroups* H, 1) k_edge_force(Dev d) {
-    EdgeCta<H, K> c = edge_prologue<H, K>(d);
-    const int D = d.D;
-    float* W = reinterpret_cast<float*>(c.extra);  // [3][D][H]
-    float* red = W + 3 * D * H + c.g * (H / 32) * 96;
-    for (int idx = threadIdx.x; idx < 3 * D * H; idx += blockDim.x) {
-        const int part = idx / (D * H), dd = (idx / H) % D, a = idx % H;
-        float w = 0.f;
-        if (part < 2) w = d.wfh[(part * H + a) * D + dd];
-        else if (a < K) w = d.wfh[(2 * H + a) * D + dd];
-        W[idx] = w;
-    }
-    __syncthreads();
-    ForceBody<H, K> b{d, d.L > 0 ? d.t[d.L] : d.tanh_emb, W, red, c.lt, c.g, D, 3 * D, d.L};
-    walk_edges<H, K>(d, c, b, FilterTc{});
 }
 
 // --------------------------------------------------------- head backward --
@@ -493,10 +533,10 @@ struct HeadBody {
         const float* gp = d.gF + (static_cast<int64_t>(j) * D + chj) * 3;
         r.g0 = __ldg(gp), r.g1 = __ldg(gp + 1), r.g2 = __ldg(gp + 2);
     }
-    __device__ void edge(const EdgeStage<K>& st, int e, const Reg& r, float) {
+    __device__ void edge(const EdgeStage<K>& st, int e, const Reg& r, float, float wt) {
         const float4 gv = st.geo[e];
-        const float di = gf0 * gv.x + gf1 * gv.y + gf2 * gv.z;
-        const float dj = r.g0 * gv.x + r.g1 * gv.y + r.g2 * gv.z;
+        const float di = (gf0 * gv.x + gf1 * gv.y + gf2 * gv.z) * wt;
+        const float dj = (r.g0 * gv.x + r.g1 * gv.y + r.g2 * gv.z) * wt;
         const float sij = gv.w * (di - dj);
         S += sij;
         W = fmaf(sij, r.t, W);
@@ -586,10 +626,10 @@ struct BwdBody {
         const int row = l == 0 ? __ldg(d.Z + j) - 1 : j;
         r.t = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
     }
-    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f) {
+    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f, float wt) {
         if constexpr (!TC) f = filter_ffma<K>(w, s, e);
-        gt = fmaf(r.gm, f, gt);
-        const float gg = gmi * r.t;
+        gt = fmaf(r.gm * wt, f, gt);
+        const float gg = gmi * r.t * wt;
         const float4* fr = reinterpret_cast<const float4*>(s.fcp + e * K);
 #pragma unroll
         for (int k4 = 0; k4 < K / 4; ++k4) {
