@@ -446,61 +446,79 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_force(Dev d) {
 
 // F_i[d][x] from the per-atom features, warp per atom: lane owns channels
 // [lane*C, lane*C+C) and k = lane (< K); 3D partial sums per lane, one warp
-// reduce-scatter (lane o ends with output o), coalesced store of F_i.
+// reduce-scatter (lane o ends with output o), coalesced store of F_i. The head
+// weights sit transposed in shared memory ([D][H] rows, vector reads).
+template <int H, int K, int R0>
+__device__ __forceinline__ void force_out_round(const float* WaT, const float* WbT, const float* WcT, int D, int ND,
+                                                int lane, const float (&ti)[H / 32], const float (&yv)[3][H / 32],
+                                                const float (&u)[3], const float (&vk)[3], float* out) {
+    constexpr int C = H / 32;
+    float v[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        const int idx = R0 + k, dd = idx / 3, x = idx % 3;
+        float s = 0.f;
+        if (idx < ND) {
+            const VecF<C> wa = ldv<C>(WaT + dd * H + lane * C);
+            const VecF<C> wb = ldv<C>(WbT + dd * H + lane * C);
+#pragma unroll
+            for (int cc = 0; cc < C; ++cc) {
+                s = fmaf(wa.v[cc], fmaf(ti[cc], u[x], yv[x][cc]), s);
+                s = fmaf(wb.v[cc], ti[cc] * yv[x][cc], s);
+            }
+            if (lane < K) s = fmaf(WcT[dd * 32 + lane], vk[x], s);
+        }
+        v[k] = s;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int k = 0; k < o; ++k) {
+            const float send = up ? v[k] : v[k + o];
+            const float keep = up ? v[k + o] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    if (R0 + lane < ND) out[R0 + lane] = v[0];
+}
+
 template <int H, int K>
 __global__ void __launch_bounds__(256) k_force_out(Dev d) {
     constexpr int C = H / 32, YW = ForceBody<H, K>::kYW;
+    __shared__ __align__(16) float WaT[kMaxHeads * H], WbT[kMaxHeads * H], WcT[kMaxHeads * 32];
     const int D = d.D, ND = 3 * D, L = d.L;
+    for (int idx = threadIdx.x; idx < D * H; idx += blockDim.x) {
+        const int dd = idx / H, aa = idx % H;
+        WaT[idx] = d.wfh[aa * D + dd];
+        WbT[idx] = d.wfh[(H + aa) * D + dd];
+    }
+    for (int idx = threadIdx.x; idx < D * 32; idx += blockDim.x) {
+        const int dd = idx / 32, k = idx % 32;
+        WcT[idx] = k < K ? d.wfh[(2 * H + k) * D + dd] : 0.f;
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     const float* __restrict__ T = L > 0 ? d.t[L] : d.tanh_emb;
-    const float* __restrict__ wfh = d.wfh;
     const int N = d.hdr->N;
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
         const float* y = d.Yf + static_cast<int64_t>(i) * YW;
         const int row = L > 0 ? i : __ldg(d.Z + i) - 1;
         float ti[C], yv[3][C];
+        const VecF<C> tv = ldv<C>(T + static_cast<int64_t>(row) * H + lane * C);
 #pragma unroll
         for (int cc = 0; cc < C; ++cc) {
             const int aa = lane * C + cc;
-            ti[cc] = __ldg(T + static_cast<int64_t>(row) * H + aa);
+            ti[cc] = tv.v[cc];
             yv[0][cc] = y[aa], yv[1][cc] = y[H + aa], yv[2][cc] = y[2 * H + aa];
         }
         const float u[3] = {y[3 * H], y[3 * H + 1], y[3 * H + 2]};
         float vk[3] = {0.f, 0.f, 0.f};
         if (lane < K) vk[0] = y[3 * H + 3 + lane], vk[1] = y[3 * H + 3 + K + lane], vk[2] = y[3 * H + 3 + 2 * K + lane];
-        for (int r0 = 0; r0 < ND; r0 += 32) {
-            float v[32];
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-                const int idx = r0 + k;
-                float s = 0.f;
-                if (idx < ND) {
-                    const int dd = idx / 3, x = idx - 3 * (idx / 3);
-#pragma unroll
-                    for (int cc = 0; cc < C; ++cc) {
-                        const int aa = lane * C + cc;
-                        const float yx = x == 0 ? yv[0][cc] : (x == 1 ? yv[1][cc] : yv[2][cc]);
-                        const float ux = x == 0 ? u[0] : (x == 1 ? u[1] : u[2]);
-                        s = fmaf(__ldg(wfh + aa * D + dd), fmaf(ti[cc], ux, yx), s);
-                        s = fmaf(__ldg(wfh + (H + aa) * D + dd), ti[cc] * yx, s);
-                    }
-                    if (lane < K) s = fmaf(__ldg(wfh + (2 * H + lane) * D + dd), x == 0 ? vk[0] : (x == 1 ? vk[1] : vk[2]), s);
-                }
-                v[k] = s;
-            }
-#pragma unroll
-            for (int o = 16; o >= 1; o >>= 1) {
-                const bool up = (lane & o) != 0;
-#pragma unroll
-                for (int k = 0; k < o; ++k) {
-                    const float send = up ? v[k] : v[k + o];
-                    const float keep = up ? v[k + o] : v[k];
-                    v[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-                }
-            }
-            if (r0 + lane < ND) d.F[static_cast<int64_t>(i) * ND + r0 + lane] = v[0];
-        }
+        float* out = d.F + static_cast<int64_t>(i) * ND;
+        force_out_round<H, K, 0>(WaT, WbT, WcT, D, ND, lane, ti, yv, u, vk, out);
+        if (ND > 32) force_out_round<H, K, 32>(WaT, WbT, WcT, D, ND, lane, ti, yv, u, vk, out);
     }
 }
 
