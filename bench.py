@@ -24,7 +24,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -50,43 +49,6 @@ def peaks():
         return p["hbm_gbs"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
     except Exception:
         return 6650.0, 1590.0, "fallback"
-
-
-# ------------------------------------------------------------ distributed
-class Dist:
-    def __init__(self):
-        self.world = int(os.environ.get("WORLD_SIZE", "1"))
-        self.rank = int(os.environ.get("RANK", "0"))
-        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-        self.pg = None
-        if self.world > 1:
-            import torch.distributed as td
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            td.init_process_group("gloo", rank=self.rank, world_size=self.world)
-            self.td = td
-
-    def barrier(self):
-        if self.world > 1:
-            self.td.barrier()
-
-    def allreduce(self, x: float, op: str) -> float:
-        if self.world == 1:
-            return x
-        import torch
-        t = torch.tensor([x], dtype=torch.float64)
-        self.td.all_reduce(t, op=self.td.ReduceOp.MAX if op == "max" else self.td.ReduceOp.SUM)
-        return float(t.item())
-
-    def bcast_bytes(self, b: bytes | None) -> bytes:
-        if self.world == 1:
-            return b
-        obj = [b]
-        self.td.broadcast_object_list(obj, src=0)
-        return obj[0]
-
-    def close(self):
-        if self.world > 1:
-            self.td.destroy_process_group()
 
 
 # ------------------------------------------------------------ workload
@@ -119,54 +81,64 @@ def fit_table(pool, D):
     return t
 
 
-def shard(pk, pool, sched, step, rank, world):
-    per = BATCH_PER_GPU * world
-    ids = sched["sample"][step * per:(step + 1) * per][rank * BATCH_PER_GPU:(rank + 1) * BATCH_PER_GPU]
-    return pk.select(pool, ids)
-
-
 # ------------------------------------------------------------ clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """NVML poll (about every 2 ms) of SM clock and clock-event reasons from a
+    thread; start() returns once the first sample is in, so the samples cover
+    the timed region that follows."""
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
 
-    def __init__(self, gpu: int):
-        self.gpu, self.rows, self.proc = gpu, [], None
+    def __init__(self, local_rank: int):
+        self.rows, self.max_mhz, self.err = [], None, None
+        self._stop = threading.Event()
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [v for v in vis.split(",") if v.strip()]
+        self.index = int(ids[local_rank]) if ids and ids[local_rank].strip().isdigit() else local_rank
 
-    def __enter__(self):
+    def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.masks = [(n, getattr(nv, m)) for n, m in self.REASONS]
+            self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
-        except Exception:
-            self.proc = None
+            t0 = time.perf_counter()
+            while not self.rows and time.perf_counter() - t0 < 2.0:
+                time.sleep(0.001)
+        except Exception as e:  # no NVML: report unsampled
+            self.err = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 8:
-                self.rows.append(parts)
-
-    def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
+    def _poll(self):
+        nv = self.nv
+        while not self._stop.is_set():
             try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((float(sm), int(rs)))
+            except Exception as e:
+                self.err = repr(e)
+                return
+            time.sleep(0.002)
+
+    def stop(self):
+        self._stop.set()
+        if getattr(self, "thread", None):
+            self.thread.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[4 + k].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(self.rows[0][1]),
-                "samples": len(self.rows), "reasons": reasons}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "error": self.err}
+        reasons = sorted({n for _, rs in self.rows for n, m in self.masks if rs & m})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_min_mhz": min(r[0] for r in self.rows),
+                "sm_max_mhz": self.max_mhz, "samples": len(self.rows), "reasons": reasons, "source": "nvml"}
 
 
 # ------------------------------------------------------------ roofline
@@ -192,6 +164,7 @@ def kernel_flops(name, N, P, H=128, K=16, D=10):
 # ------------------------------------------------------------ arms
 def run_ours(args, dist):
     import paper_2505_22208_b200 as pk
+    from paper_2505_22208_b200.dist import shard
 
     if dist.world > 1:
         os.environ.setdefault("CUDA_VISIBLE_DEVICES", os.environ.get("CUDA_VISIBLE_DEVICES", ""))
@@ -205,42 +178,49 @@ def run_ours(args, dist):
     dev.set_reference_table(table)
     tc = pk.TrainConfig(seed=11)
     n_steps = sched["n_batches"]
-    shards = [shard(pk, pool, sched, s, dist.rank, dist.world) for s in range(n_steps)]
+    shards = [shard(pool, sched, s, dist.rank, dist.world, BATCH_PER_GPU) for s in range(n_steps)]
     for s, b in enumerate(shards):
         dev.stage(b, tc, step=s, slot=s, workers=dist.world, rank=dist.rank)
-    dev.set_option("profile", 1)
-    # clocks are sampled from the start of the warm-up through the timed region
-    clk = ClockSampler(gpu).__enter__()
     # warm-up: every slot once (grows all capacities, captures the graph), then W more
     for k in range(max(args.warmup, 0) + n_steps):
         dev.train_step_staged(k % n_steps, sync=True)
-    dev.kernel_times_reset()
     anomalies0 = dev.anomalies()
-    # ---- timed region (device-resident inputs)
-    # Each step is bracketed by CUDA events on the ctx stream inside the library
-    # (upload -> step -> allreduce -> optimizer); the L2 flush and the result
-    # read-back sit outside the brackets.
     K = args.steps
-    atoms_local = 0
-    dist.barrier()
-    dev.sync()
-    for k in range(K):
-        s = k % n_steps
-        dev.flush_l2(L2_FLUSH)
-        r = dev.train_step_staged(s, sync=True)
-        atoms_local += r.n_atoms
-    clk.__exit__(None, None, None)
-    dist.barrier()
-    dev_ms, nsteps = dev.step_times()
-    assert nsteps == K, (nsteps, K)
+
+    def timed_region():
+        """K steps, each bracketed by CUDA events on the ctx stream inside the
+        library (upload -> step -> allreduce -> optimizer); the L2 flush and the
+        header read-back sit outside the brackets. Returns (device ms, atoms)."""
+        dev.kernel_times_reset()  # also resets the step-time accumulator
+        atoms = 0
+        dist.barrier()
+        dev.sync()
+        for k in range(K):
+            dev.flush_l2(L2_FLUSH)
+            r = dev.train_step_staged(k % n_steps, sync=True)
+            atoms += r.n_atoms
+        dist.barrier()
+        ms, nsteps = dev.step_times()
+        assert nsteps == K, (nsteps, K)
+        return ms, atoms
+
+    # ---- timed region (device-resident inputs, no per-kernel events)
+    clk = ClockSampler(gpu).start()
+    dev_ms, atoms_local = timed_region()
+    clk.stop()
     launches = dev.last_step_launches() * K
-    assert dev.anomalies() == anomalies0, "a timed step skipped its update (capacity overflow or non-finite)"
-    ktimes = dev.kernel_times()
     ms_max = dist.allreduce(dev_ms, "max")
     atoms_all = dist.allreduce(float(atoms_local), "sum")
     value = atoms_all / (ms_max / 1e3)
-    # per-step edges for the roofline (one synced pass over the slots)
+    # ---- the same K steps again with an event pair around every kernel (the
+    # graph is re-captured with event-record nodes): per-kernel durations
+    dev.set_option("profile", 1)
+    dev.train_step_staged(0, sync=True)
+    prof_ms, _ = timed_region()
+    ktimes = dev.kernel_times()
     dev.set_option("profile", 0)
+    assert dev.anomalies() == anomalies0, "a timed step skipped its update (capacity overflow or non-finite)"
+    # per-step edges for the roofline (one synced pass over the slots)
     edge_counts = []
     for s in range(n_steps):
         r = dev.train_step_staged(s, sync=True)
@@ -274,7 +254,9 @@ def run_ours(args, dist):
     byts = kernel_bytes(tname, N_mean, P_mean)
     roof = {"kernel": tname, "bound": "hbm", "unit": "GB/s", "peak": hbm, "peak_source": src,
             "share_of_step": tms / tot_ms if tot_ms else None, "avg_launch_us": per_launch_ms * 1e3,
-            "launches_per_step": launches_per_step}
+            "launches_per_step": launches_per_step,
+            "timing": "CUDA event pair around each launch on the ctx stream, second pass over the same K steps "
+                      "(profiled step %.3f ms vs %.3f ms unprofiled)" % (prof_ms / K, dev_ms / K)}
     if byts is not None:
         ach = byts / (per_launch_ms / 1e3) / 1e9
         roof.update(achieved=ach, frac=ach / hbm, traffic=None, algorithmic_bytes_per_launch=byts)
@@ -327,7 +309,7 @@ def cpu_baseline(batch, table, mcfg, budget_s=15.0, sample=64):
             if lib.kind == "ref" else lib.train_step(cfg, 1, n, sub, table, params, v, seed=11, step=reps)
         reps += 1
         el = time.perf_counter() - t0
-        if el > budget_s or reps >= 50:
+        if el > budget_s or reps >= 400:
             break
     atoms = int(sub["atom_ptr"][-1]) * reps
     return {"value": atoms / el, "unit": "atoms/s", "cores": threads if lib.kind == "ref" else 1,
@@ -375,6 +357,7 @@ def run_reference(args, dist):
         return None
     import oracle
     import paper_2505_22208_b200 as pk
+    from paper_2505_22208_b200.dist import shard
     lib = oracle.ref() if oracle.ref_available() else oracle.port()
     pool, table, sched = make_workload(pk, 1)
     cfg = tuple(CFG[k] for k in ("hidden", "layers", "rbf", "cutoff", "heads"))
@@ -384,7 +367,7 @@ def run_reference(args, dist):
     sample = args.ref_sample
     total_atoms, total_s = 0, 0.0
     for k in range(args.warmup + args.steps):
-        b = shard(pk, pool, sched, k % sched["n_batches"], 0, 1)
+        b = shard(pool, sched, k % sched["n_batches"], 0, 1, BATCH_PER_GPU)
         sub = pk.select(b, np.arange(sample))
         t0 = time.perf_counter()
         kw = dict(threads=threads) if lib.kind == "ref" else {}
@@ -411,7 +394,7 @@ def run_reference(args, dist):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -419,7 +402,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-sample", type=int, default=64)
     args = ap.parse_args()
-    dist = Dist()
+    from paper_2505_22208_b200.dist import Dist
+    dist = Dist("gloo")
     try:
         out = run_reference(args, dist) if args.impl == "reference" else run_ours(args, dist)
         if out is not None and dist.rank == 0:

@@ -51,7 +51,7 @@ typedef struct lamm_ctx lamm_ctx;
 
 /* lamm::model::ModelConfig, H/model.hpp:34-40. The sm_100a kernels are
  * instantiated for (hidden, rbf) in {(128,16), (64,16), (32,8)}; layers <= 8,
- * heads <= 32. */
+ * heads <= 16. */
 typedef struct {
     int32_t hidden;
     int32_t layers;
