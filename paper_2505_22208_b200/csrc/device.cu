@@ -357,6 +357,37 @@ void launch(Ctx& c, const char* name, Kern kernel, int grid, int block, size_t s
     ++c.launches;
 }
 
+// Cooperative launch (all CTAs co-resident, for kernels with grid barriers);
+// capturable into the step graph like a plain launch.
+template <class... KArgs, class... Args>
+void launch_coop(Ctx& c, const char* name, void (*kernel)(KArgs...), int grid, int block, Args... args) {
+    KernelSlot* slot = nullptr;
+    if (c.profile) {
+        if (c.slot_cursor >= c.slots.size()) {
+            KernelSlot s;
+            CK(cudaEventCreate(&s.a));
+            CK(cudaEventCreate(&s.b));
+            c.slots.push_back(s);
+        }
+        slot = &c.slots[c.slot_cursor++];
+        slot->name = name;
+        CK(cudaEventRecordWithFlags(slot->a, c.stream, cudaEventRecordExternal));
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kernel, args...));
+    if (slot) CK(cudaEventRecordWithFlags(slot->b, c.stream, cudaEventRecordExternal));
+    ++c.launches;
+}
+
 void collect_kernel_times(Ctx& c) {
     if (!c.profile) return;
     for (size_t k = 0; k < c.slot_cursor && k < c.slots.size(); ++k) {
@@ -375,10 +406,10 @@ struct Ops {
     void (*setup)(Ctx&);
     void (*prep)(Ctx&);
     void (*nlist)(Ctx&);
-    void (*forward)(Ctx&);
-    void (*loss)(Ctx&);
+    void (*forward)(Ctx&, bool energy);
+    void (*loss)(Ctx&, bool energy);
     void (*backward)(Ctx&, bool general);
-    void (*opt)(Ctx&);
+    void (*opt)(Ctx&, const Dev&, int G, double inv_g, double clip, double lr, double decay, double eps);
     void (*pack)(Ctx&);
 };
 
@@ -428,7 +459,7 @@ struct Model {
         c.grid_warp = 4 * c.nsm;
         c.grid_small = c.nsm * 4;
         c.ncta_red = c.nsm;
-        c.grid_opt = static_cast<int>(std::min<int64_t>((c.NP + 255) / 256, 4 * c.nsm));
+        c.grid_opt = static_cast<int>(std::min<int64_t>((c.NP + 255) / 256, std::min(c.nsm, 256)));  // cooperative, <= 256 CTAs
         c.grid_reduce = static_cast<int>(std::min<int64_t>((c.NP + 31) / 32, 16 * c.nsm));
     }
 
@@ -443,7 +474,8 @@ struct Model {
         launch(c, "nbr_fill", k_nbr_fill<K>, c.grid_warp, 256, 0, d);
     }
 
-    static void forward(Ctx& c) {
+    // energy = false leaves the per-sample energies to the fused loss kernel.
+    static void forward(Ctx& c, bool energy) {
         const Dev d = make_dev(c);
         if (c.L == 0) throw InputErr("model: layers == 0 is not supported by the device path");
         for (int l = 0; l < c.L; ++l) {
@@ -452,13 +484,12 @@ struct Model {
         }
         launch(c, "force", k_edge_force<H, K>, c.grid_edge, kGroups * H, smem_force(c.D), d);
         launch(c, "force_out", k_force_out<H, K>, c.grid_warp, 256, 0, d);
-        launch(c, "energy", k_energy, c.grid_small, 128, sizeof(double) * 128 * c.D, d);
+        if (energy) launch(c, "energy", k_energy, c.grid_small, 128, sizeof(double) * 128 * c.D, d);
     }
 
-    static void loss(Ctx& c) {
+    static void loss(Ctx& c, bool energy) {
         const Dev d = make_dev(c);
-        launch(c, "loss", k_loss, c.grid_small, 128, 0, d);
-        launch(c, "loss_final", k_loss_final, 1, 1024, 0, d);
+        launch(c, "loss", k_loss, c.grid_small, 128, energy ? sizeof(double) * 128 * c.D : 0, d, energy ? 1 : 0);
     }
 
     static void backward(Ctx& c, bool general) {
@@ -488,11 +519,8 @@ struct Model {
         launch(c, "grad_reduce", k_grad_reduce, c.grid_reduce, 256, 0, d, tab);
     }
 
-    static void opt(Ctx& c) {
-        Dev d = make_dev(c);
-        launch(c, "opt_norm", k_opt_norm, c.grid_opt, 256, 0, d, c.opt_G, c.opt_inv_g, c.opt_clip);
-        launch(c, "opt_step", k_opt_step, c.grid_opt, 256, 0, d, c.opt_inv_g, c.opt_lr, c.opt_decay, c.opt_eps);
-        pack(c);
+    static void opt(Ctx& c, const Dev& d, int G, double inv_g, double clip, double lr, double decay, double eps) {
+        launch_coop(c, "optimizer", k_opt<H>, c.grid_opt, 256, d, G, inv_g, clip, lr, decay, eps);
     }
 
     // Packs the tensor-core weight operands from the fp32 working parameters.
@@ -702,12 +730,14 @@ cudaGraphExec_t capture(Ctx& c, void (*body)(Ctx&)) {
 void step_body(Ctx& c) {
     c.ops->prep(c);
     c.ops->nlist(c);
-    c.ops->forward(c);
-    c.ops->loss(c);
+    c.ops->forward(c, false);
+    c.ops->loss(c, true);
     c.ops->backward(c, false);
 }
 
-void opt_body(Ctx& c) { c.ops->opt(c); }
+void opt_body(Ctx& c) {
+    c.ops->opt(c, make_dev(c), c.opt_G, c.opt_inv_g, c.opt_clip, c.opt_lr, c.opt_decay, c.opt_eps);
+}
 
 // One train step from a staged blob (pinned host blob: H2D; resident slot:
 // D2D); returns the header after it, or a zeroed header when !sync.
@@ -767,7 +797,7 @@ void ensure_forward(Ctx& c) {
     if (!c.nlist_valid) run_nlist(c);
     if (!c.fwd_valid) {
         c.slot_cursor = 0;
-        c.ops->forward(c);
+        c.ops->forward(c, true);
         read_header(c);
         c.fwd_valid = true;
     }
@@ -1093,7 +1123,7 @@ LAMM_API int lamm_loss_grad(lamm_ctx* c, const lamm_loss_config* cfg, lamm_loss_
         CK(cudaMemcpyAsync(c->d_stage.as<char>() + offsetof(StepHeader, lambda_e), &hd->lambda_e, 16,
                            cudaMemcpyHostToDevice, c->stream));
         c->slot_cursor = 0;
-        c->ops->loss(*c);
+        c->ops->loss(*c, false);
         const StepHeader h = read_header(*c);
         if (out) {
             out->total = h.loss_total;
@@ -1309,11 +1339,7 @@ LAMM_API int lamm_optimizer_step(lamm_ctx* c, const double* grad_sum, int32_t wo
         Dev d = make_dev(*c);
         d.g64_in = c->g64.as<double>();
         const double inv_g = 1.0 / static_cast<double>(workers);
-        k_opt_norm<<<c->grid_opt, 256, 0, c->stream>>>(d, workers, inv_g, tc->clip_norm);
-        CK(cudaGetLastError());
-        k_opt_step<<<c->grid_opt, 256, 0, c->stream>>>(d, inv_g, tc->learning_rate, tc->rms_decay, tc->rms_epsilon);
-        CK(cudaGetLastError());
-        c->ops->pack(*c);
+        c->ops->opt(*c, d, workers, inv_g, tc->clip_norm, tc->learning_rate, tc->rms_decay, tc->rms_epsilon);
         const StepHeader h = read_header(*c);
         if (grad_norm) *grad_norm = h.grad_norm;
         c->fwd_valid = c->loss_valid = false;

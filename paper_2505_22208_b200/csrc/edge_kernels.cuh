@@ -179,6 +179,8 @@ __device__ __forceinline__ void filter_mma(uint32_t tcol, const FilterTc& f, con
 //        (w is 1 for the edges of the current segment, 0 otherwise: bodies must
 //        be linear in w so masked edges contribute exactly nothing)
 //   void begin(int i); void end(int i);     destination-atom brackets
+//   static constexpr bool kBlockHook;  if set, block(st, e0, r) runs once per
+//        8-edge block after its segments (segment-independent per-edge work)
 template <int H, int K, class Body>
 __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c, Body& body, const FilterTc& ft) {
     constexpr bool kF = Body::kFilter;
@@ -274,6 +276,7 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
                     for (int u = 0; u < 8; ++u)
                         body.edge(st, blk * 8 + u, r[u], f[u], (u >= u0 && u < u1) ? 1.f : 0.f);
                 }
+                if constexpr (Body::kBlockHook) body.block(st, blk * 8, r);
             }
             if constexpr (kF) umma::fence_before();
             group_sync(c.g, H);  // every thread is done with this stage (smem + TMEM)
@@ -344,6 +347,7 @@ template <int H, int K, bool TC>
 struct MessageBody {
     static constexpr bool kFilter = TC;
     static constexpr int kParts = TC ? 0 : kPartPlain;
+    static constexpr bool kBlockHook = false;
     struct Reg {
         float t;
     };
@@ -398,6 +402,7 @@ template <int H, int K>
 struct ForceBody {
     static constexpr bool kFilter = false;
     static constexpr int kParts = kPartGeo | kPartPlain;
+    static constexpr bool kBlockHook = false;
     static constexpr int kYW = 3 * H + 3 + 3 * K;  // per-atom feature floats
     struct Reg {
         float t;
@@ -533,6 +538,7 @@ template <int H, int K>
 struct HeadBody {
     static constexpr bool kFilter = false;
     static constexpr int kParts = kPartGeo | kPartPlain;
+    static constexpr bool kBlockHook = false;
     struct Reg {
         float t, g0, g1, g2;
     };
@@ -630,6 +636,7 @@ template <int H, int K, bool TC>
 struct BwdBody {
     static constexpr bool kFilter = TC;
     static constexpr int kParts = kPartPlain;
+    static constexpr bool kBlockHook = true;
     struct Reg {
         float gm, t;
     };
@@ -639,6 +646,7 @@ struct BwdBody {
     int l, a;
     float w[K], dw[K];
     float gmi, gt;
+    float gi[8];  // gm of the destination of each edge of the block (0: masked)
     __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
         r.gm = __ldg(d.gm + static_cast<int64_t>(j) * H + a);
         const int row = l == 0 ? __ldg(d.Z + j) - 1 : j;
@@ -647,15 +655,23 @@ struct BwdBody {
     __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f, float wt) {
         if constexpr (!TC) f = filter_ffma<K>(w, s, e);
         gt = fmaf(r.gm * wt, f, gt);
-        const float gg = gmi * r.t * wt;
-        const float4* fr = reinterpret_cast<const float4*>(s.fcp + e * K);
+        gi[e & 7] = fmaf(gmi, wt, gi[e & 7]);
+    }
+    // dWf[a,k] += gm_ia t_ja fcut rbf_k, once per edge (segment-independent)
+    __device__ void block(const EdgeStage<K>& s, int e0, const Reg (&r)[8]) {
 #pragma unroll
-        for (int k4 = 0; k4 < K / 4; ++k4) {
-            const float4 q = fr[k4];
-            dw[4 * k4] = fmaf(gg, q.x, dw[4 * k4]);
-            dw[4 * k4 + 1] = fmaf(gg, q.y, dw[4 * k4 + 1]);
-            dw[4 * k4 + 2] = fmaf(gg, q.z, dw[4 * k4 + 2]);
-            dw[4 * k4 + 3] = fmaf(gg, q.w, dw[4 * k4 + 3]);
+        for (int u = 0; u < 8; ++u) {
+            const float gg = gi[u] * r[u].t;
+            gi[u] = 0.f;
+            const float4* fr = reinterpret_cast<const float4*>(s.fcp + (e0 + u) * K);
+#pragma unroll
+            for (int k4 = 0; k4 < K / 4; ++k4) {
+                const float4 q = fr[k4];
+                dw[4 * k4] = fmaf(gg, q.x, dw[4 * k4]);
+                dw[4 * k4 + 1] = fmaf(gg, q.y, dw[4 * k4 + 1]);
+                dw[4 * k4 + 2] = fmaf(gg, q.z, dw[4 * k4 + 2]);
+                dw[4 * k4 + 3] = fmaf(gg, q.w, dw[4 * k4 + 3]);
+            }
         }
     }
     __device__ void begin(int i) {
@@ -691,6 +707,8 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_bwd(Dev d, int l, int sl
     BwdBody<H, K, TC> b{d, l == 0 ? d.tanh_emb : d.t[l], emb + c.g * slot_cap * H, l, c.lt};
 #pragma unroll
     for (int k = 0; k < K; ++k) b.w[k] = TC ? 0.f : d.wf[l][c.lt * K + k], b.dw[k] = 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) b.gi[u] = 0.f;
     walk_edges<H, K>(d, c, b, ft);
 #pragma unroll
     for (int k = 0; k < K; ++k) red[c.g * H * K + c.lt * K + k] = b.dw[k];

@@ -49,7 +49,7 @@ using NodeGemmSmem = NodeGemmCfg<H>;
 // [NC][H] tile (B[n][k] = W_u[n][k] for the update, W_u[k][n] for gm), hi and
 // lo blocks adjacent, so a CTA fetches its operand with one TMA bulk copy.
 template <int H>
-__global__ void __launch_bounds__(256) k_pack_weights(Dev d) {
+__device__ __forceinline__ void pack_weights(const Dev& d) {
     constexpr int NC = NodeGemmCfg<H>::NC;
     const int64_t per = static_cast<int64_t>(H) * H;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < d.L * per;
@@ -64,6 +64,24 @@ __global__ void __launch_bounds__(256) k_pack_weights(Dev d) {
         umma::split_tf32(wu[idx], upd[o], upd[NC * H + o]);
         umma::split_tf32(wu[k * H + n], gm[o], gm[NC * H + o]);
     }
+}
+
+template <int H>
+__global__ void __launch_bounds__(256) k_pack_weights(Dev d) {
+    pack_weights<H>(d);
+}
+
+// The optimizer tail of the step as ONE cooperative kernel (grid <= 256 CTAs of
+// 256 threads, all co-resident): norm -> barrier -> clip + RMS update ->
+// barrier -> tensor-core weight packing of the updated parameters.
+template <int H>
+__global__ void __launch_bounds__(256) k_opt(Dev d, int G, double inv_g, double clip, double lr, double decay,
+                                             double eps) {
+    unsigned int* bar = d.anomaly + 16;
+    const int status = opt_update(d, G, inv_g, clip, lr, decay, eps, bar);
+    if (status != 0) return;  // uniform across the grid: parameters unchanged, packing still valid
+    grid_barrier(bar, bar + 32);
+    pack_weights<H>(d);
 }
 
 // One tile = 128 atoms x NC output columns, K = H, 256 threads: the whole

@@ -299,41 +299,51 @@ __device__ __forceinline__ void load_rbf(const float* __restrict__ src, float (&
 }
 
 // ---------------------------------------------------------------- energy ---
-// Per-sample energies for every head, E_s^d = sum_{i in s} e_i^d, in fp64.
-__global__ void __launch_bounds__(128) k_energy(Dev d) {
-    double* red = dyn_smem<double>();  // [D][128]
-    const int B = d.hdr->B, D = d.D;
-    for (int s = blockIdx.x; s < B; s += gridDim.x) {
-        const int64_t lo = d.atom_ptr[s], hi = d.atom_ptr[s + 1];
-        for (int dd = 0; dd < D; ++dd) red[dd * 128 + threadIdx.x] = 0.0;
-        for (int64_t a = lo + threadIdx.x; a < hi; a += 128)
-            for (int dd = 0; dd < D; ++dd) {
-                float e = 0.f;
-                for (int q = 0; q < d.NS; ++q) e += d.e_atom[(a * d.NS + q) * D + dd];
-                red[dd * 128 + threadIdx.x] += static_cast<double>(e);
-            }
-        __syncthreads();
-        for (int o = 64; o > 0; o >>= 1) {
-            if (threadIdx.x < o)
-                for (int dd = 0; dd < D; ++dd) red[dd * 128 + threadIdx.x] += red[dd * 128 + threadIdx.x + o];
-            __syncthreads();
+// Per-sample energies for every head, E_s^d = sum_{i in s} e_i^d, in fp64
+// (block of 128 threads per sample; red is [D][128] shared doubles).
+__device__ __forceinline__ void sample_energy(const Dev& d, int s, double* red) {
+    const int D = d.D;
+    const int64_t lo = d.atom_ptr[s], hi = d.atom_ptr[s + 1];
+    for (int dd = 0; dd < D; ++dd) red[dd * 128 + threadIdx.x] = 0.0;
+    for (int64_t a = lo + threadIdx.x; a < hi; a += 128)
+        for (int dd = 0; dd < D; ++dd) {
+            float e = 0.f;
+            for (int q = 0; q < d.NS; ++q) e += d.e_atom[(a * d.NS + q) * D + dd];
+            red[dd * 128 + threadIdx.x] += static_cast<double>(e);
         }
-        if (threadIdx.x < D) d.Epred[static_cast<int64_t>(s) * D + threadIdx.x] = red[threadIdx.x * 128];
+    __syncthreads();
+    for (int o = 64; o > 0; o >>= 1) {
+        if (threadIdx.x < o)
+            for (int dd = 0; dd < D; ++dd) red[dd * 128 + threadIdx.x] += red[dd * 128 + threadIdx.x + o];
         __syncthreads();
     }
+    if (threadIdx.x < D) d.Epred[static_cast<int64_t>(s) * D + threadIdx.x] = red[threadIdx.x * 128];
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(128) k_energy(Dev d) {
+    double* red = dyn_smem<double>();  // [D][128]
+    const int B = d.hdr->B;
+    for (int s = blockIdx.x; s < B; s += gridDim.x) sample_energy(d, s, red);
 }
 
 // ------------------------------------------------------------------ loss ---
 // Eq. (5) with the per-rank denominators sum m_E, sum m_F (S/loss.cpp:175-212):
-// block per sample computes its energy/force terms and writes d(loss)/d(pred)
-// for the selected head d_s only (every other channel is zeroed).
-__global__ void __launch_bounds__(128) k_loss(Dev d) {
-    __shared__ double red[128];
+// block per sample (optionally computing its energies first) writes its energy
+// and force terms and d(loss)/d(pred) for the selected head d_s only (every
+// other channel is zeroed). The last block to finish sums the per-sample terms
+// in index order (deterministic), publishes the rank's loss to the header and,
+// as an fp32 hi/lo pair, into the allreduce payload after the gradients.
+__global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy) {
+    double* ered = dyn_smem<double>();  // [D][128] when with_energy
+    __shared__ double red[128], red2[128];
+    __shared__ bool last;
     const int B = d.hdr->B, D = d.D;
     const int me = d.hdr->me, mf = d.hdr->mf;
     const double we = me > 0 ? d.hdr->lambda_e / static_cast<double>(me) : 0.0;
     const double wf = mf > 0 ? d.hdr->lambda_f / static_cast<double>(mf) : 0.0;
     for (int s = blockIdx.x; s < B; s += gridDim.x) {
+        if (with_energy) sample_energy(d, s, ered);
         const int64_t lo = d.atom_ptr[s], hi = d.atom_ptr[s + 1];
         const int ds = d.dsidx[s];
         const bool em = d.emask[s], fm = d.fmask[s];
@@ -378,31 +388,32 @@ __global__ void __launch_bounds__(128) k_loss(Dev d) {
         }
         __syncthreads();
     }
-}
-
-// Fixed-order tree sum of the per-sample terms; the rank's loss goes to the
-// header and (as an fp32 hi/lo pair) into the allreduce payload after the grads.
-__global__ void __launch_bounds__(1024) k_loss_final(Dev d) {
-    __shared__ double re[1024], rf[1024];
-    const int B = d.hdr->B;
-    double e = 0.0, f = 0.0;
-    for (int s = threadIdx.x; s < B; s += 1024) e += d.sample_terms[2 * s], f += d.sample_terms[2 * s + 1];
-    re[threadIdx.x] = e, rf[threadIdx.x] = f;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&d.hdr->done_counter, 1u) == gridDim.x - 1;
+    }
     __syncthreads();
-    for (int o = 512; o > 0; o >>= 1) {
-        if (threadIdx.x < o) re[threadIdx.x] += re[threadIdx.x + o], rf[threadIdx.x] += rf[threadIdx.x + o];
+    if (!last) return;
+    __threadfence();
+    double e = 0.0, f = 0.0;
+    for (int s = threadIdx.x; s < B; s += 128) e += d.sample_terms[2 * s], f += d.sample_terms[2 * s + 1];
+    red[threadIdx.x] = e, red2[threadIdx.x] = f;
+    __syncthreads();
+    for (int o = 64; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o], red2[threadIdx.x] += red2[threadIdx.x + o];
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        const double tot = re[0] + rf[0];
-        d.hdr->loss_energy = re[0];
-        d.hdr->loss_force = rf[0];
+        const double tot = red[0] + red2[0];
+        d.hdr->loss_energy = red[0];
+        d.hdr->loss_force = red2[0];
         d.hdr->loss_total = tot;
         const float hi = static_cast<float>(tot);
         d.grads[d.NP] = hi;
         d.grads[d.NP + 1] = static_cast<float>(tot - static_cast<double>(hi));
         d.grads[d.NP + 2] = d.hdr->overflow ? 1.f : 0.f;
         d.grads[d.NP + 3] = 1.f;
+        d.hdr->done_counter = 0;
     }
 }
 
@@ -457,9 +468,35 @@ __global__ void __launch_bounds__(256) k_grad_reduce(Dev d, SegTable tab) {
 }
 
 // ------------------------------------------------------------ optimizer ---
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident): arrival
+// counter + generation word, the last arrival resets the counter and bumps the
+// generation.
+__device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int* vgen = gen;
+        const unsigned int g = *vgen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            *count = 0;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*vgen == g) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 // Mean over ranks (x 1/G as scale_params does), global norm (fp64, fixed-order
-// tree), non-finite check, clip factor; the last CTA finalizes.
-__global__ void __launch_bounds__(256) k_opt_norm(Dev d, int G, double inv_g, double clip) {
+// tree over a fixed grid), non-finite check and clip factor, then
+// RmsOptimizer::step with bit-exact fp64 arithmetic given the same gradient
+// (S/trainer.cpp:37-53, 319-326); refreshes the fp32 working copy and tanh(E)
+// for layer 0's gathers. Every CTA reduces the per-CTA norms itself, so no
+// second barrier is needed before the update. Returns the step status.
+__device__ __forceinline__ int opt_update(const Dev& d, int G, double inv_g, double clip, double lr, double decay,
+                                          double eps, unsigned int* bar) {
     __shared__ double red[256];
     double s = 0.0;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < d.NP;
@@ -473,36 +510,29 @@ __global__ void __launch_bounds__(256) k_opt_norm(Dev d, int G, double inv_g, do
         if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
         __syncthreads();
     }
-    __shared__ bool is_last;
-    if (threadIdx.x == 0) {
-        d.block_scratch[blockIdx.x] = red[0];
-        __threadfence();
-        is_last = atomicAdd(&d.hdr->done_counter, 1u) == gridDim.x - 1;
-    }
+    if (threadIdx.x == 0) d.block_scratch[blockIdx.x] = red[0];
+    grid_barrier(bar, bar + 32);
+    red[threadIdx.x] = threadIdx.x < gridDim.x ? d.block_scratch[threadIdx.x] : 0.0;
     __syncthreads();
-    if (is_last && threadIdx.x == 0) {
-        __threadfence();
-        double tot = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) tot += d.block_scratch[b];
-        const double gn = sqrt(tot);
-        double loss = 0.0;
-        if (!d.g64_in) loss = (static_cast<double>(d.grads[d.NP]) + static_cast<double>(d.grads[d.NP + 1])) /
-                   static_cast<double>(G);
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    const double gn = sqrt(red[0]);
+    double loss = 0.0;
+    if (!d.g64_in)
+        loss = (static_cast<double>(d.grads[d.NP]) + static_cast<double>(d.grads[d.NP + 1])) / static_cast<double>(G);
+    const bool overflow = !d.g64_in && d.grads[d.NP + 2] > 0.f;
+    const int status = overflow ? 2 : ((!isfinite(loss) || !isfinite(gn)) ? 1 : 0);
+    const double cs = (clip > 0.0 && gn > clip) ? clip / gn : 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         d.hdr->grad_norm = gn;
         d.hdr->global_loss = loss;
-        const bool overflow = !d.g64_in && d.grads[d.NP + 2] > 0.f;
-        d.hdr->status = overflow ? 2 : ((!isfinite(loss) || !isfinite(gn)) ? 1 : 0);
-        if (d.hdr->status != 0 && !d.g64_in) atomicAdd(d.anomaly, 1u);
-        d.hdr->clip_scale = (clip > 0.0 && gn > clip) ? clip / gn : 0.0;
-        d.hdr->done_counter = 0;
+        d.hdr->status = status;
+        d.hdr->clip_scale = cs;
+        if (status != 0 && !d.g64_in) atomicAdd(d.anomaly, 1u);
     }
-}
-
-// RmsOptimizer::step with bit-exact fp64 arithmetic given the same gradient;
-// refreshes the fp32 working copy and tanh(E) for layer 0's gathers.
-__global__ void __launch_bounds__(256) k_opt_step(Dev d, double inv_g, double lr, double decay, double eps) {
-    if (d.hdr->status != 0) return;
-    const double cs = d.hdr->clip_scale;
+    if (status != 0) return status;
     const int64_t emb_n = static_cast<int64_t>(kMaxZ) * d.H;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < d.NP;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -516,6 +546,7 @@ __global__ void __launch_bounds__(256) k_opt_step(Dev d, double inv_g, double lr
         d.p32[e] = pf;
         if (e < emb_n) d.tanh_emb_w[e] = tanhf(pf);
     }
+    return status;
 }
 
 // fp64 master -> fp32 working copy (+ tanh(E)) after a host parameter upload.
