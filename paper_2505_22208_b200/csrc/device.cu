@@ -110,7 +110,7 @@ struct lamm_ctx {
     bool batch_valid = false, nlist_valid = false, fwd_valid = false, loss_valid = false;
     // launch geometry
     int grid_warp = 0, grid_gemm = 0, grid_upd = 0, grid_small = 0, grid_opt = 0, ncta_red = 0, grid_reduce = 0;
-    int grid_edge = 0, slot_cap = 16, slot_cap_max = 16, node_ns = 1;
+    int grid_edge = 0, slot_cap = 16, slot_cap_max = 16;
     // graphs
     cudaGraphExec_t g_step = nullptr, g_opt = nullptr;
     bool graph_dirty = true;
@@ -218,7 +218,6 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
         ensure_buf(c, "h" + std::to_string(l), 4 * static_cast<size_t>(Nc) * H, changed);
     }
     for (int l = 0; l < L; ++l) ensure_buf(c, "mu" + std::to_string(l), 4 * static_cast<size_t>(Nc) * H, changed);
-    ensure_buf(c, "e_atom", 4 * Nc * D * c.node_ns, changed);
     ensure_buf(c, "F", 12 * Nc * D, changed);
     ensure_buf(c, "Yf", 4 * static_cast<size_t>(Nc) * (3 * H + 3 + 3 * K), changed);
     ensure_buf(c, "Epred", 8 * Bc * D, changed);
@@ -291,7 +290,6 @@ Dev make_dev(Ctx& c) {
         d.h[l] = buf(c, "h" + std::to_string(l)).as<float>();
     }
     for (int l = 0; l < L; ++l) d.mu[l] = buf(c, "mu" + std::to_string(l)).as<float>();
-    d.e_atom = buf(c, "e_atom").as<float>();
     d.F = buf(c, "F").as<float>();
     d.Yf = buf(c, "Yf").as<float>();
     d.Epred = buf(c, "Epred").as<double>();
@@ -317,7 +315,6 @@ Dev make_dev(Ctx& c) {
     d.emb_rows = kMaxZ;
     d.anomaly = c.anomaly.as<unsigned int>();
     d.wpack = c.wpack.as<float>();
-    d.NS = c.node_ns;
     return d;
 }
 
@@ -440,9 +437,7 @@ struct Model {
         set_smem((const void*)k_edge_force<H, K>, smem_force(c.D));
         set_smem((const void*)k_edge_head<H, K>, smem_head(c.D));
         set_smem((const void*)k_edge_bwd<H, K>, smem_bwd(c.slot_cap_max));
-        if (c.D > kGemmMaxHeads) throw InputErr("model: the device path supports at most 16 heads");
         c.grid_upd = c.nsm;            // one tcgen05 CTA per SM, persistent over 128-atom tiles
-        c.node_ns = NodeGemmCfg<H>::NS;
         c.grid_gemm = c.nsm / 2;       // split-K CTAs of dW_u (one partial each)
         // one edge partitioning (k_scan) serves all four edge kernels: size it so
         // every CTA of the heaviest one is resident (no second wave)
@@ -480,7 +475,7 @@ struct Model {
         if (c.L == 0) throw InputErr("model: layers == 0 is not supported by the device path");
         for (int l = 0; l < c.L; ++l) {
             launch(c, "message", k_edge_message<H, K>, c.grid_edge, kGroups * H, smem_message(), d, l);
-            launch(c, "update", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 0, l == c.L - 1 ? 1 : 0);
+            launch(c, "update", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 0);
         }
         launch(c, "force", k_edge_force<H, K>, c.grid_edge, kGroups * H, smem_force(c.D), d);
         launch(c, "force_out", k_force_out<H, K>, c.grid_warp, 256, 0, d);
@@ -499,7 +494,7 @@ struct Model {
             launch(c, "head_bwd", k_edge_head<H, K>, c.grid_edge, kGroups * H, smem_head(c.D), d, general ? q : -1,
                    q == 0 ? 1 : 0);
         for (int l = c.L - 1; l >= 0; --l) {
-            launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 1, 0);
+            launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 1);
             launch(c, "dwu", k_dwu<H>, c.grid_gemm, 256, kDwuSmem, d, l);
             launch(c, "bwd_edge", k_edge_bwd<H, K>, c.grid_edge, kGroups * H, smem_bwd(c.slot_cap), d, l,
                    c.slot_cap);

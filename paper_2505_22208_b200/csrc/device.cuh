@@ -95,7 +95,7 @@ struct Dev {
     float* t[kMaxLayers + 1];
     float* h[kMaxLayers + 1];
     float* mu[kMaxLayers];
-    float *e_atom, *F;
+    float* F;
     float* Yf;               // [N][3H + 3 + 3K] per-atom force-head features (k_edge_force)
     double* Epred;           // [B][D]
     // loss gradients
@@ -120,7 +120,6 @@ struct Dev {
     int32_t emb_rows;
     unsigned int* anomaly;   // steps whose update was skipped
     float* wpack;            // [L][4][H*H] packed tcgen05 weight operands (k_pack_weights)
-    int NS;                  // column splits of the node GEMM: e_atom is [N][NS][D]
 };
 
 __device__ __forceinline__ float warp_sum(float v) {

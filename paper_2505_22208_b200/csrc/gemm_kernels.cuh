@@ -2,8 +2,7 @@
 // tensor cores (3xTF32, fp32-accurate), accumulators in TMEM.
 //
 //   k_node_gemm mode 0 (update, S/model.cpp:93-102):   Y = mu_l W_u^T   (M = 128 atoms, N = H, K = H)
-//               epilogue h_{l+1} = h_l + Y, t_{l+1} = tanh h_{l+1}; last layer also the
-//               per-atom energy e_i = W_e^T h^L_i   (S/model.cpp:208-218)
+//               epilogue h_{l+1} = h_l + Y, t_{l+1} = tanh h_{l+1}
 //   k_node_gemm mode 1 (S/model.cpp:380-390):          gm = (gh W_u) (.) (1 - mu^2)
 //   k_dwu              (S/model.cpp:381-383):          dW_u = gh^T mu, split-K over atoms
 //                                                       (one per-CTA partial, summed by k_grad_reduce)
@@ -26,7 +25,6 @@ namespace lamm_b200 {
 
 constexpr int kGemmM = 128;      // atoms per tile (TMEM lanes)
 constexpr int kGemmKC = 32;      // K chunk of the staged activations
-constexpr int kGemmMaxHeads = 16;
 
 // Column split of a node-GEMM tile: for H = 128 two CTAs share a 128-atom
 // tile (64 output columns each) so small batches still fill the GPU.
@@ -36,9 +34,7 @@ struct NodeGemmCfg {
     static constexpr int NC = H / NS;                       // output columns per CTA tile
     static constexpr size_t a_floats = 2 * kGemmM * H;      // activation tile hi | lo (full K)
     static constexpr size_t b_floats = 2 * NC * H;          // weight rows [NC][H] hi | lo
-    static constexpr size_t heads_floats = NC * kGemmMaxHeads;
-    static constexpr size_t red_floats = kGemmM * kGemmMaxHeads;
-    static constexpr size_t bytes = 4 * (a_floats + b_floats + heads_floats + red_floats) + 64;
+    static constexpr size_t bytes = 4 * (a_floats + b_floats) + 64;
 };
 template <int H>
 using NodeGemmSmem = NodeGemmCfg<H>;
@@ -90,7 +86,7 @@ __global__ void __launch_bounds__(256) k_opt(Dev d, int G, double inv_g, double 
 // epilogue inputs (residual / mu) are prefetched while the tensor core runs.
 // Warps w and w+4 share TMEM lanes 32*(w%4).. and split the NC columns.
 template <int H>
-__global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, int last) {
+__global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
     using Cfg = NodeGemmCfg<H>;
     constexpr int NS = Cfg::NS, NC = Cfg::NC, CW = NC / 2;  // columns per thread
     static_assert(CW % 16 == 0, "epilogue reads 16 columns at a time");
@@ -98,13 +94,10 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, in
     float* Ahi = sm;
     float* Alo = Ahi + kGemmM * H;
     float* Bhi = Alo + kGemmM * H;
-    float* We = Bhi + Cfg::b_floats;
-    float* red = We + NC * kGemmMaxHeads;  // [128][kGemmMaxHeads] energy partials of column half 1
-    uint64_t* bar = reinterpret_cast<uint64_t*>(red + Cfg::red_floats);  // [0] weights TMA, [1] MMA done
+    uint64_t* bar = reinterpret_cast<uint64_t*>(Bhi + Cfg::b_floats);  // [0] weights TMA, [1] MMA done
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int quad = warp & 3, half = warp >> 2;
-    const int D = d.D;
     constexpr uint32_t kCols = NC < 32 ? 32 : NC;
     if (warp == 0) umma::tmem_alloc(tslot, kCols);
     if (tid == 0) {
@@ -132,8 +125,6 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, in
                 mbar_expect_tx(&bar[0], static_cast<uint32_t>(Cfg::b_floats * 4));
                 bulk_g2s(Bhi, wsrc, static_cast<uint32_t>(Cfg::b_floats * 4), &bar[0]);
             }
-            if (last)
-                for (int idx = tid; idx < NC * D; idx += blockDim.x) We[idx] = d.we[np * NC * D + idx];
         }
         // stage the full activation tile (hi/lo), all loads first
         {
@@ -194,9 +185,6 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, in
         mbar_wait(&bar[1], mphase);
         mphase ^= 1u;
         umma::fence_after();
-        float eacc[kGemmMaxHeads];
-#pragma unroll
-        for (int q = 0; q < kGemmMaxHeads; ++q) eacc[q] = 0.f;
 #pragma unroll
         for (int cc = 0; cc < CW; cc += 16) {
             float v[16];
@@ -213,15 +201,6 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, in
                     *reinterpret_cast<float4*>(ho + q) = make_float4(hn[q], hn[q + 1], hn[q + 2], hn[q + 3]);
                     *reinterpret_cast<float4*>(to + q) = make_float4(tn[q], tn[q + 1], tn[q + 2], tn[q + 3]);
                 }
-                if (last) {
-#pragma unroll
-                    for (int q = 0; q < 16; ++q) {
-                        const float* we = We + (half * CW + cc + q) * D;
-#pragma unroll
-                        for (int dd = 0; dd < kGemmMaxHeads; ++dd)
-                            if (dd < D) eacc[dd] = fmaf(hn[q], we[dd], eacc[dd]);
-                    }
-                }
             } else {
                 float* go = d.gm + static_cast<int64_t>(atom) * H + c0 + cc;
 #pragma unroll
@@ -233,21 +212,11 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, in
                                     v[q + 3] * (1.f - pre[cc + q + 3] * pre[cc + q + 3]));
             }
         }
-        if (mode == 0 && last) {
-            // partial energy over this CTA's NC columns: the two column halves meet
-            // in shared memory; the NS splits land in separate slots of e_atom
-            // ([N][NS][D]) that k_energy sums in a fixed order
-            if (half == 1)
-                for (int dd = 0; dd < D; ++dd) red[row * kGemmMaxHeads + dd] = eacc[dd];
-            __syncthreads();
-            if (half == 0 && live)
-                for (int dd = 0; dd < D; ++dd)
-                    d.e_atom[(static_cast<int64_t>(atom) * NS + np) * D + dd] = eacc[dd] + red[row * kGemmMaxHeads + dd];
-        }
         umma::fence_before();
         __syncthreads();  // accumulator and activation tile drained before the next tile
         umma::fence_after();
     }
+    umma::fence_before();
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc(tbase, kCols);
 }

@@ -299,18 +299,32 @@ __device__ __forceinline__ void load_rbf(const float* __restrict__ src, float (&
 }
 
 // ---------------------------------------------------------------- energy ---
-// Per-sample energies for every head, E_s^d = sum_{i in s} e_i^d, in fp64
+// Per-sample energies for every head (S/model.cpp:208-218),
+// E_s^d = sum_{i in s} sum_a W_e[a,d] h^L_ia: thread a accumulates its channel
+// over the sample's atoms in fp64, then a fixed-order tree over the channels
 // (block of 128 threads per sample; red is [D][128] shared doubles).
 __device__ __forceinline__ void sample_energy(const Dev& d, int s, double* red) {
-    const int D = d.D;
+    const int D = d.D, H = d.H;
     const int64_t lo = d.atom_ptr[s], hi = d.atom_ptr[s + 1];
-    for (int dd = 0; dd < D; ++dd) red[dd * 128 + threadIdx.x] = 0.0;
-    for (int64_t a = lo + threadIdx.x; a < hi; a += 128)
-        for (int dd = 0; dd < D; ++dd) {
-            float e = 0.f;
-            for (int q = 0; q < d.NS; ++q) e += d.e_atom[(a * d.NS + q) * D + dd];
-            red[dd * 128 + threadIdx.x] += static_cast<double>(e);
+    const float* __restrict__ hL = d.h[d.L];
+    double acc[kMaxHeads];
+#pragma unroll
+    for (int dd = 0; dd < kMaxHeads; ++dd) acc[dd] = 0.0;
+    const int a = threadIdx.x;
+    if (a < H) {
+        float w[kMaxHeads];
+#pragma unroll
+        for (int dd = 0; dd < kMaxHeads; ++dd) w[dd] = dd < D ? d.we[a * D + dd] : 0.f;
+        for (int64_t i = lo; i < hi; ++i) {
+            const double hv = static_cast<double>(__ldg(hL + i * H + a));
+#pragma unroll
+            for (int dd = 0; dd < kMaxHeads; ++dd)
+                if (dd < D) acc[dd] = fma(hv, static_cast<double>(w[dd]), acc[dd]);
         }
+    }
+#pragma unroll
+    for (int dd = 0; dd < kMaxHeads; ++dd)
+        if (dd < D) red[dd * 128 + threadIdx.x] = acc[dd];
     __syncthreads();
     for (int o = 64; o > 0; o >>= 1) {
         if (threadIdx.x < o)
