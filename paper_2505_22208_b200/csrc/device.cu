@@ -110,7 +110,7 @@ struct lamm_ctx {
     bool batch_valid = false, nlist_valid = false, fwd_valid = false, loss_valid = false;
     // launch geometry
     int grid_warp = 0, grid_gemm = 0, grid_upd = 0, grid_small = 0, grid_opt = 0, ncta_red = 0, grid_reduce = 0;
-    int grid_edge = 0, slot_cap = 16, slot_cap_max = 16;
+    int grid_edge = 0, grid_emb = 0;
     // graphs
     cudaGraphExec_t g_step = nullptr, g_opt = nullptr;
     bool graph_dirty = true;
@@ -231,7 +231,7 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
         ensure_buf(c, "part_wu" + std::to_string(l), 4 * static_cast<size_t>(c.grid_gemm) * H * H, changed);
     }
     ensure_buf(c, "part_head", 4 * static_cast<size_t>(c.grid_edge) * (3 * H + K) * D, changed);
-    ensure_buf(c, "part_emb", 4 * static_cast<size_t>(c.grid_edge) * kMaxZ * H, changed);
+    ensure_buf(c, "part_emb", 4 * static_cast<size_t>(c.grid_emb) * kMaxZ * H, changed);
     if (changed) c.graph_dirty = true;
 }
 
@@ -418,7 +418,7 @@ struct Model {
     static size_t smem_message() { return ES::message(); }
     static size_t smem_force(int D) { return ES::force(D); }
     static size_t smem_head(int D) { return ES::head(D); }
-    static size_t smem_bwd(int slot_cap) { return ES::bwd(slot_cap); }
+    static size_t smem_bwd() { return ES::bwd(); }
 
     static void set_smem(const void* fn, size_t bytes) {
         CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
@@ -433,10 +433,11 @@ struct Model {
         if (smem_head(c.D) > static_cast<size_t>(smem_max) || 3 * c.D > H)
             throw InputErr("model: too many heads for the device path at this hidden size");
         // embedding-gradient slots (distinct Z per device-batch) that fit next to the staging
-        c.slot_cap_max = static_cast<int>((smem_max - smem_bwd(0)) / (sizeof(float) * kGroups * H)) & ~7;
         set_smem((const void*)k_edge_force<H, K>, smem_force(c.D));
         set_smem((const void*)k_edge_head<H, K>, smem_head(c.D));
-        set_smem((const void*)k_edge_bwd<H, K>, smem_bwd(c.slot_cap_max));
+        set_smem((const void*)k_edge_bwd<H, K>, smem_bwd());
+        set_smem((const void*)k_emb_grad, sizeof(float) * kMaxZ * H);
+        c.grid_emb = c.nsm;
         c.grid_upd = c.nsm;            // one tcgen05 CTA per SM, persistent over 128-atom tiles
         c.grid_gemm = c.nsm / 2;       // split-K CTAs of dW_u (one partial each)
         // one edge partitioning (k_scan) serves all four edge kernels: size it so
@@ -448,7 +449,7 @@ struct Model {
         occ_e = std::min(occ_e, o);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_head<H, K>, kGroups * H, smem_head(c.D)));
         occ_e = std::min(occ_e, o);
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_bwd<H, K>, kGroups * H, smem_bwd(16)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_bwd<H, K>, kGroups * H, smem_bwd()));
         occ_e = std::min(occ_e, o);
         c.grid_edge = c.nsm * std::max(1, occ_e);
         c.grid_warp = 4 * c.nsm;
@@ -496,8 +497,7 @@ struct Model {
         for (int l = c.L - 1; l >= 0; --l) {
             launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 1);
             launch(c, "dwu", k_dwu<H>, c.grid_gemm, 256, kDwuSmem, d, l);
-            launch(c, "bwd_edge", k_edge_bwd<H, K>, c.grid_edge, kGroups * H, smem_bwd(c.slot_cap), d, l,
-                   c.slot_cap);
+            launch(c, "bwd_edge", k_edge_bwd<H, K>, c.grid_edge, kGroups * H, smem_bwd(), d, l);
         }
         SegTable tab{};
         int64_t off = 0;
@@ -505,7 +505,8 @@ struct Model {
             tab.s[tab.nseg++] = Seg{off, static_cast<int32_t>(n), kind, src, ncta, stride};
             off += n;
         };
-        add(static_cast<int64_t>(kMaxZ) * H, 1, d.part_emb, c.grid_edge, 0);
+        launch(c, "emb_grad", k_emb_grad, c.grid_emb, 128, sizeof(float) * kMaxZ * H, d);
+        add(static_cast<int64_t>(kMaxZ) * H, 1, d.part_emb, c.grid_emb, 0);
         for (int l = 0; l < c.L; ++l) add(H * K, 0, d.part_wf[l], c.grid_edge, H * K);
         for (int l = 0; l < c.L; ++l) add(H * H, 0, d.part_wu[l], c.grid_gemm, H * H);
         const int hw = (3 * H + K) * c.D;
@@ -650,11 +651,6 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
     h.N = static_cast<int32_t>(N);
     h.me = me, h.mf = mf;
     h.nslots = nslots;
-    if (nslots > c.slot_cap) {  // the captured graph sized its embedding accumulators for slot_cap
-        require(nslots <= c.slot_cap_max, "batch: too many distinct atomic numbers in one device-batch");
-        c.slot_cap = std::min(c.slot_cap_max, (nslots + 7) & ~7);
-        c.graph_dirty = true;
-    }
     h.lambda_e = tc ? tc->lambda_energy : 1.0;
     h.lambda_f = tc ? tc->lambda_force : 1.0;
     h.workers = 1;

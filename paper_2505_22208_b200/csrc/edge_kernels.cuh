@@ -83,6 +83,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void group_sync(int g, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(nthreads) : "memory");
 }
@@ -179,8 +182,9 @@ __device__ __forceinline__ void filter_mma(uint32_t tcol, const FilterTc& f, con
 //        (w is 1 for the edges of the current segment, 0 otherwise: bodies must
 //        be linear in w so masked edges contribute exactly nothing)
 //   void begin(int i); void end(int i);     destination-atom brackets
-//   static constexpr bool kBlockHook;  if set, block(st, e0, r) runs once per
-//        8-edge block after its segments (segment-independent per-edge work)
+//   static constexpr bool kBlockHook;  if set, block(st, e0, r, ulo, uhi) runs once
+//        per 8-edge block after its segments (segment-independent per-edge work;
+//        edges [ulo, uhi) of the block are valid); group-uniform, may group_sync
 template <int H, int K, class Body>
 __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c, Body& body, const FilterTc& ft) {
     constexpr bool kF = Body::kFilter;
@@ -276,7 +280,7 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
                     for (int u = 0; u < 8; ++u)
                         body.edge(st, blk * 8 + u, r[u], f[u], (u >= u0 && u < u1) ? 1.f : 0.f);
                 }
-                if constexpr (Body::kBlockHook) body.block(st, blk * 8, r);
+                if constexpr (Body::kBlockHook) body.block(st, blk * 8, r, ulo, uhi);
             }
             if constexpr (kF) umma::fence_before();
             group_sync(c.g, H);  // every thread is done with this stage (smem + TMEM)
@@ -338,7 +342,7 @@ struct EdgeKernelSmem {
     static size_t message() { return pad(base + filter); }
     static size_t force(int) { return base; }
     static size_t head(int D) { return base + 4 * kGroups * (3 * D * H + D * K); }
-    static size_t bwd(int slot_cap) { return pad(base + filter + 4 * kGroups * (H * K + slot_cap * H)); }
+    static size_t bwd() { return pad(base + filter + 4 * kGroups * H * K); }
 };
 
 // ---------------------------------------------------------------- message --
@@ -630,8 +634,14 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_head(Dev d, int pass_ch,
 // ------------------------------------------------------- layer backward --
 // Gather form of S/model.cpp:393-418 for layer l:
 //   gt_i = sum_j gm_j (.) filter_ij        (filter symmetric in i, j)
-//   dWf[a,k] += gm_ia t_ja fcut_ij rbf_ijk (per-thread registers, CTA-reduced)
-//   gh_i += gt_i (.) (1 - t_i^2) ; on layer 0 also dE[Z_i] += gh_i (S/model.cpp:421-424).
+//   dWf[a,k] += gm_ia t_ja fcut_ij rbf_ijk (once per edge, thread-owned registers,
+//                                           CTA-reduced)
+//   gh_i += gt_i (.) (1 - t_i^2)
+// The embedding gradient of layer 0 (S/model.cpp:421-424) is k_emb_grad's.
+// (A tensor-core dW_f — one M = 128, N = 16, K = 8 MMA per 8-edge block from
+// shared-memory G/R tiles — cut the instruction count by a fifth but the
+// per-block producer/consumer handshake and the smaller chunk it needs for TMEM
+// made the kernel slower; see profiles/README.md.)
 template <int H, int K, bool TC>
 struct BwdBody {
     static constexpr bool kFilter = TC;
@@ -642,7 +652,6 @@ struct BwdBody {
     };
     const Dev& d;
     const float* __restrict__ tsrc;
-    float* emb_acc;  // smem [slots][H] (layer 0), this group's
     int l, a;
     float w[K], dw[K];
     float gmi, gt;
@@ -658,7 +667,7 @@ struct BwdBody {
         gi[e & 7] = fmaf(gmi, wt, gi[e & 7]);
     }
     // dWf[a,k] += gm_ia t_ja fcut rbf_k, once per edge (segment-independent)
-    __device__ void block(const EdgeStage<K>& s, int e0, const Reg (&r)[8]) {
+    __device__ void block(const EdgeStage<K>& s, int e0, const Reg (&r)[8], int, int) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const float gg = gi[u] * r[u].t;
@@ -682,29 +691,23 @@ struct BwdBody {
         const int row = l == 0 ? __ldg(d.Z + i) - 1 : i;
         const float ti = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
         float* ghp = d.gh + static_cast<int64_t>(i) * H + a;
-        const float gh = fmaf(gt, 1.f - ti * ti, *ghp);
-        *ghp = gh;
-        if (l == 0) emb_acc[d.zslot[i] * H + a] += gh;
+        *ghp = fmaf(gt, 1.f - ti * ti, *ghp);
     }
 };
 
 template <int H, int K>
-__global__ void __launch_bounds__(kGroups* H, 1) k_edge_bwd(Dev d, int l, int slot_cap) {
+__global__ void __launch_bounds__(kGroups* H, 1) k_edge_bwd(Dev d, int l) {
     constexpr bool TC = EdgeKernelSmem<H, K>::TC;
     EdgeCta<H, K> c = edge_prologue<H, K>(d);
     float* Wh = reinterpret_cast<float*>(c.extra);
     float* red = Wh + (TC ? 2 * H * K : 0);  // [kGroups][H*K]
-    float* emb = red + kGroups * H * K;      // [kGroups][slot_cap][H]
-    const int ns = d.hdr->nslots;
-    if (l == 0)
-        for (int e = c.lt; e < ns * H; e += H) emb[c.g * slot_cap * H + e] = 0.f;
     FilterTc ft{};
     if constexpr (TC) {
         ft = filter_setup<H, K>(d, c, l, Wh, Wh + H * K);
     } else {
         __syncthreads();
     }
-    BwdBody<H, K, TC> b{d, l == 0 ? d.tanh_emb : d.t[l], emb + c.g * slot_cap * H, l, c.lt};
+    BwdBody<H, K, TC> b{d, l == 0 ? d.tanh_emb : d.t[l], l, c.lt};
 #pragma unroll
     for (int k = 0; k < K; ++k) b.w[k] = TC ? 0.f : d.wf[l][c.lt * K + k], b.dw[k] = 0.f;
 #pragma unroll
@@ -722,14 +725,6 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_bwd(Dev d, int l, int sl
         float s = 0.f;
         for (int gg = 0; gg < kGroups; ++gg) s += red[gg * H * K + e];
         part[e] = s;
-    }
-    if (l == 0) {
-        float* pe = d.part_emb + static_cast<int64_t>(blockIdx.x) * ns * H;
-        for (int e = threadIdx.x; e < ns * H; e += blockDim.x) {
-            float s = 0.f;
-            for (int gg = 0; gg < kGroups; ++gg) s += emb[gg * slot_cap * H + e];
-            pe[e] = s;
-        }
     }
 }
 

@@ -233,7 +233,8 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d) {
     const int lane = threadIdx.x & 31;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     const double width = d.rc / static_cast<double>(K - 1);
-    const double inv = 1.0 / (2.0 * width * width);
+    const float wf = static_cast<float>(width), invf = static_cast<float>(1.0 / (2.0 * width * width));
+    const float rc_inv = static_cast<float>(1.0 / d.rc);
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
         const int s = d.sample_of[i];
         const int lo = static_cast<int>(d.atom_ptr[s]), hi = static_cast<int>(d.atom_ptr[s + 1]);
@@ -254,14 +255,16 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d) {
                 d.dst[p] = i;
                 const double sc = __ddiv_rn(1.0, r);
                 const double ux = __dmul_rn(sc, dx), uy = __dmul_rn(sc, dy), uz = __dmul_rn(sc, dz);
-                const double fc = 0.5 * (cos(kPiD * r / d.rc) + 1.0);
-                d.geo[p] = make_float4(static_cast<float>(ux), static_cast<float>(uy), static_cast<float>(uz),
-                                       static_cast<float>(fc));
+                // fcut and the Gaussians feed the fp32 model: evaluated in fp32 from the
+                // once-rounded distance (relative error ~1e-6, far inside the 1e-4 bar)
+                const float rf = static_cast<float>(r);
+                const float fc = 0.5f * (cospif(rf * rc_inv) + 1.f);
+                d.geo[p] = make_float4(static_cast<float>(ux), static_cast<float>(uy), static_cast<float>(uz), fc);
                 float rb[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    const double dd = r - width * static_cast<double>(k);
-                    rb[k] = static_cast<float>(fc * exp(-dd * dd * inv));  // fcut folded in
+                    const float dd = rf - wf * static_cast<float>(k);
+                    rb[k] = fc * expf(-dd * dd * invf);  // fcut folded in
                 }
 #pragma unroll
                 for (int q = 0; q < K / 4; ++q) {  // canonical tcgen05 layout, tf32 hi + fp32 lo
@@ -315,11 +318,16 @@ __device__ __forceinline__ void sample_energy(const Dev& d, int s, double* red) 
         float w[kMaxHeads];
 #pragma unroll
         for (int dd = 0; dd < kMaxHeads; ++dd) w[dd] = dd < D ? d.we[a * D + dd] : 0.f;
-        for (int64_t i = lo; i < hi; ++i) {
-            const double hv = static_cast<double>(__ldg(hL + i * H + a));
+        // 8 independent row loads in flight per iteration
+        for (int64_t i0 = lo; i0 < hi; i0 += 8) {
+            float hv[8];
 #pragma unroll
-            for (int dd = 0; dd < kMaxHeads; ++dd)
-                if (dd < D) acc[dd] = fma(hv, static_cast<double>(w[dd]), acc[dd]);
+            for (int u = 0; u < 8; ++u) hv[u] = i0 + u < hi ? __ldg(hL + (i0 + u) * H + a) : 0.f;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int dd = 0; dd < kMaxHeads; ++dd)
+                    if (dd < D) acc[dd] = fma(static_cast<double>(hv[u]), static_cast<double>(w[dd]), acc[dd]);
         }
     }
 #pragma unroll
@@ -429,6 +437,38 @@ __global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy) {
         d.grads[d.NP + 3] = 1.f;
         d.hdr->done_counter = 0;
     }
+}
+
+// ------------------------------------------------------ embedding grad ---
+// dE[Z_i - 1] += gh_i over the atoms after the layer-0 backward
+// (S/model.cpp:421-424): CTA c sums a contiguous atom range per distinct-Z slot
+// in shared memory (thread = channel, atoms in index order: deterministic) and
+// writes one [nslots][H] partial; k_grad_reduce maps slots back to Z rows.
+__global__ void __launch_bounds__(128) k_emb_grad(Dev d) {
+    float* acc = dyn_smem<float>();  // [kMaxZ][H]
+    const int H = d.H, ns = d.hdr->nslots, N = d.hdr->N;
+    const int a = threadIdx.x;
+    for (int e = threadIdx.x; e < ns * H; e += blockDim.x) acc[e] = 0.f;
+    __syncthreads();
+    const int per = (N + gridDim.x - 1) / gridDim.x;
+    const int i0 = min(N, static_cast<int>(blockIdx.x) * per), i1 = min(N, i0 + per);
+    if (a < H) {
+        for (int i = i0; i < i1; i += 8) {
+            float v[8];
+            int z[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const bool ok = i + u < i1;
+                v[u] = ok ? __ldg(d.gh + static_cast<int64_t>(i + u) * H + a) : 0.f;
+                z[u] = ok ? __ldg(d.zslot + i + u) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[z[u] * H + a] += v[u];
+        }
+    }
+    __syncthreads();
+    float* part = d.part_emb + static_cast<int64_t>(blockIdx.x) * ns * H;
+    for (int e = threadIdx.x; e < ns * H; e += blockDim.x) part[e] = acc[e];
 }
 
 // ------------------------------------------------------- grad reduction ---
