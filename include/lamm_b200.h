@@ -135,7 +135,8 @@ int lamm_ctx_create(int device, const lamm_model_config* cfg, lamm_ctx** out);
 void lamm_ctx_destroy(lamm_ctx* ctx);
 /* Options: "graph" (CUDA-graph capture of the step, default 1),
  * "profile" (per-kernel CUDA events inside the step, default 0),
- * "export_fp64" (keep fp64 pair distance/unit for lamm_neighbor_list_copy). */
+ * "export_fp64" (keep fp64 pair distance/unit for lamm_neighbor_list_copy),
+ * "pdl" (programmatic dependent launch between the step's kernels, default 1). */
 int lamm_ctx_set_option(lamm_ctx* ctx, const char* name, int64_t value);
 
 /* ---------------------------------------------------------- parameters --- */

@@ -114,7 +114,7 @@ struct lamm_ctx {
     // graphs
     cudaGraphExec_t g_step = nullptr, g_opt = nullptr;
     bool graph_dirty = true;
-    bool use_graph = true, profile = false, export64 = false;
+    bool use_graph = true, profile = false, export64 = false, pdl = true;
     int denoise_scheme = 1;
     double opt_inv_g = 1.0, opt_lr = 0, opt_decay = 0, opt_eps = 0, opt_clip = 0;
     int opt_G = 1;
@@ -348,8 +348,19 @@ void launch(Ctx& c, const char* name, Kern kernel, int grid, int block, size_t s
         // (a plain record would only add a dependency edge).
         CK(cudaEventRecordWithFlags(slot->a, c.stream, cudaEventRecordExternal));
     }
-    kernel<<<grid, block, smem, c.stream>>>(args...);
-    CK(cudaGetLastError());
+    // programmatic dependent launch: the kernel calls pdl_enter() before it
+    // touches the previous kernel's outputs (device.cuh)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = c.pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, kernel, args...));
     if (slot) CK(cudaEventRecordWithFlags(slot->b, c.stream, cudaEventRecordExternal));
     ++c.launches;
 }
@@ -872,6 +883,7 @@ LAMM_API int lamm_ctx_set_option(lamm_ctx* c, const char* name, int64_t value) {
         const std::string n(name);
         if (n == "graph") c->use_graph = value != 0;
         else if (n == "profile") c->profile = value != 0;
+        else if (n == "pdl") c->pdl = value != 0;
         else if (n == "export_fp64") {
             c->export64 = value != 0;
             CK(cudaSetDevice(c->device));

@@ -122,6 +122,17 @@ struct Dev {
     float* wpack;            // [L][4][H*H] packed tcgen05 weight operands (k_pack_weights)
 };
 
+// Programmatic dependent launch: every kernel of the step is launched with
+// programmatic stream serialization, so its CTAs may start while the previous
+// kernel drains. pdl_enter() waits until that kernel has completed (its writes
+// visible) and immediately lets the next kernel launch. Code before pdl_enter()
+// may only read data produced two or more kernels back (weights, the CSR
+// partition) and must not write anything a running kernel could read.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

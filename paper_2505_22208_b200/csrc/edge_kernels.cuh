@@ -189,6 +189,7 @@ template <int H, int K, class Body>
 __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c, Body& body, const FilterTc& ft) {
     constexpr bool kF = Body::kFilter;
     constexpr int parts = Body::kParts | (kF ? kPartCanon : 0);
+    pdl_enter();  // the kernel's prologue (weights, TMEM, accumulators) overlapped the previous kernel
     if (c.lo >= c.hi) return;
     const int e0 = d.row_ptr[c.lo], e1 = d.row_ptr[c.hi];
     const bool lead = c.lt == 0;
@@ -507,6 +508,7 @@ __global__ void __launch_bounds__(256) k_force_out(Dev d) {
         WcT[idx] = k < K ? d.wfh[(2 * H + k) * D + dd] : 0.f;
     }
     __syncthreads();
+    pdl_enter();
     const int lane = threadIdx.x & 31;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     const float* __restrict__ T = L > 0 ? d.t[L] : d.tanh_emb;

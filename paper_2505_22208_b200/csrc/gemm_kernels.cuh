@@ -64,6 +64,7 @@ __device__ __forceinline__ void pack_weights(const Dev& d) {
 
 template <int H>
 __global__ void __launch_bounds__(256) k_pack_weights(Dev d) {
+    pdl_enter();
     pack_weights<H>(d);
 }
 
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(256) k_pack_weights(Dev d) {
 template <int H>
 __global__ void __launch_bounds__(256) k_opt(Dev d, int G, double inv_g, double clip, double lr, double decay,
                                              double eps) {
+    pdl_enter();
     unsigned int* bar = d.anomaly + 16;
     const int status = opt_update(d, G, inv_g, clip, lr, decay, eps, bar);
     if (status != 0) return;  // uniform across the grid: parameters unchanged, packing still valid
@@ -108,6 +110,7 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
+    pdl_enter();
     const uint32_t tbase = *tslot;
     const uint32_t idesc = umma::idesc_tf32(kGemmM, NC);
     const int N = d.hdr->N;
@@ -252,6 +255,7 @@ __global__ void __launch_bounds__(256, 1) k_dwu(Dev d, int l) {
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
+    pdl_enter();
     const uint32_t tbase = *tslot;
     const uint32_t idesc = umma::idesc_tf32(kGemmM, H);
     const int N = d.hdr->N;

@@ -47,6 +47,7 @@ struct BatchArrays {
 };
 
 __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out) {
+    pdl_enter();
     const StepHeader& hd = *d.hdr;
     const char* base = reinterpret_cast<const char*>(d.hdr);
     const int B = hd.B;
@@ -137,6 +138,7 @@ __device__ __forceinline__ double pair_dist(double xi, double yi, double zi, dou
 // Warp per destination atom i; lanes sweep the sample's atoms j in order and
 // count with ballot/popc.
 __global__ void __launch_bounds__(256) k_nbr_count(Dev d) {
+    pdl_enter();
     const int N = d.hdr->N;
     const int lane = threadIdx.x & 31;
     const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -164,6 +166,7 @@ __global__ void __launch_bounds__(256) k_nbr_count(Dev d) {
 // the edge kernels: part_lo[q] = first atom i with row_ptr[i] >= floor(P q / Q),
 // part_lo[Q] = N (computed while writing row_ptr, no searches).
 __global__ void __launch_bounds__(1024) k_scan(Dev d, int Q) {
+    pdl_enter();
     __shared__ int warp_tot[32];
     const int N = d.hdr->N;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
@@ -228,6 +231,7 @@ __global__ void __launch_bounds__(1024) k_scan(Dev d, int Q) {
 // (S/model.cpp:20-27).
 template <int K>
 __global__ void __launch_bounds__(256) k_nbr_fill(Dev d) {
+    pdl_enter();
     if (d.hdr->overflow) return;
     const int N = d.hdr->N;
     const int lane = threadIdx.x & 31;
@@ -344,6 +348,7 @@ __device__ __forceinline__ void sample_energy(const Dev& d, int s, double* red) 
 }
 
 __global__ void __launch_bounds__(128) k_energy(Dev d) {
+    pdl_enter();
     double* red = dyn_smem<double>();  // [D][128]
     const int B = d.hdr->B;
     for (int s = blockIdx.x; s < B; s += gridDim.x) sample_energy(d, s, red);
@@ -357,6 +362,7 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
 // in index order (deterministic), publishes the rank's loss to the header and,
 // as an fp32 hi/lo pair, into the allreduce payload after the gradients.
 __global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy) {
+    pdl_enter();
     double* ered = dyn_smem<double>();  // [D][128] when with_energy
     __shared__ double red[128], red2[128];
     __shared__ bool last;
@@ -445,6 +451,7 @@ __global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy) {
 // in shared memory (thread = channel, atoms in index order: deterministic) and
 // writes one [nslots][H] partial; k_grad_reduce maps slots back to Z rows.
 __global__ void __launch_bounds__(128) k_emb_grad(Dev d) {
+    pdl_enter();
     float* acc = dyn_smem<float>();  // [kMaxZ][H]
     const int H = d.H, ns = d.hdr->nslots, N = d.hdr->N;
     const int a = threadIdx.x;
@@ -488,6 +495,7 @@ struct SegTable {
 // partial streams (coalesced loads, 8 independent sums per element), combined
 // in a fixed order: deterministic for a fixed grid.
 __global__ void __launch_bounds__(256) k_grad_reduce(Dev d, SegTable tab) {
+    pdl_enter();
     __shared__ float red[8][33];
     const int H = d.H;
     const int ns = d.hdr->nslots;
@@ -605,6 +613,7 @@ __device__ __forceinline__ int opt_update(const Dev& d, int G, double inv_g, dou
 
 // fp64 master -> fp32 working copy (+ tanh(E)) after a host parameter upload.
 __global__ void __launch_bounds__(256) k_params_cast(Dev d) {
+    pdl_enter();
     const int64_t emb_n = static_cast<int64_t>(kMaxZ) * d.H;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < d.NP;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
