@@ -110,25 +110,29 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
-    pdl_enter();
     const uint32_t tbase = *tslot;
     const uint32_t idesc = umma::idesc_tf32(kGemmM, NC);
-    const int N = d.hdr->N;
+    const int N = d.hdr->N;  // from the staged upload, not from the previous kernel
     const int ntiles = (N + kGemmM - 1) / kGemmM * NS;
     const float* __restrict__ src = mode == 0 ? d.mu[l] : d.gh;
     uint32_t wphase = 0, mphase = 0;
     int loaded_np = -1;
+    bool w_pending = false;
+    auto fetch_weights = [&](int np) {  // weight block of a column split (TMA), packed by the last optimizer step
+        if (tid == 0) {
+            const float* wsrc =
+                d.wpack + static_cast<int64_t>(4 * l + 2 * mode) * H * H + static_cast<int64_t>(np) * 2 * NC * H;
+            mbar_expect_tx(&bar[0], static_cast<uint32_t>(Cfg::b_floats * 4));
+            bulk_g2s(Bhi, wsrc, static_cast<uint32_t>(Cfg::b_floats * 4), &bar[0]);
+        }
+        loaded_np = np;
+        w_pending = true;
+    };
+    if (static_cast<int>(blockIdx.x) < ntiles) fetch_weights(blockIdx.x % NS);  // overlaps the previous kernel
+    pdl_enter();
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int at = tile / NS, np = tile % NS, base = at * kGemmM;
-        const bool new_w = np != loaded_np;
-        if (new_w) {  // weight block of this column split (TMA)
-            if (tid == 0) {
-                const float* wsrc = d.wpack + static_cast<int64_t>(4 * l + 2 * mode) * H * H +
-                                    static_cast<int64_t>(np) * 2 * NC * H;
-                mbar_expect_tx(&bar[0], static_cast<uint32_t>(Cfg::b_floats * 4));
-                bulk_g2s(Bhi, wsrc, static_cast<uint32_t>(Cfg::b_floats * 4), &bar[0]);
-            }
-        }
+        if (np != loaded_np) fetch_weights(np);
         // stage the full activation tile (hi/lo), all loads first
         {
             constexpr int Q = H / 4, IT = kGemmM * Q / 256;
@@ -155,11 +159,12 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
         }
         umma::fence_proxy_async();
         __syncthreads();
+        if (w_pending) {
+            if (tid == 0) mbar_wait(&bar[0], wphase);
+            wphase ^= 1u;
+            w_pending = false;
+        }
         if (tid == 0) {
-            if (new_w) {
-                mbar_wait(&bar[0], wphase);
-                wphase ^= 1u;
-            }
             umma::fence_after();
             const float* Blo = Bhi + NC * H;
 #pragma unroll
@@ -168,7 +173,6 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
                            umma::kdesc(Blo, s, H), idesc, s ? 1u : 0u);
             umma::commit(&bar[1]);
         }
-        loaded_np = np;
         // epilogue inputs for this thread's row/columns, fetched while the MMAs run
         const int row = quad * 32 + lane, atom = base + row, c0 = np * NC + half * CW;
         const bool live = atom < N;
