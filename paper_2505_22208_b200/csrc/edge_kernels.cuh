@@ -86,6 +86,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Packed fp32 pair FMA (FFMA2 on sm_100a): two IEEE fmaf in one instruction.
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t f32x2_splat(float x) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void f32x2_unpack(uint64_t v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
 __device__ __forceinline__ void group_sync(int g, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(nthreads) : "memory");
 }
@@ -655,7 +669,8 @@ struct BwdBody {
     const Dev& d;
     const float* __restrict__ tsrc;
     int l, a;
-    float w[K], dw[K];
+    float w[K];
+    uint64_t dw2[K / 2];  // dW_f accumulators as packed fp32 pairs (k, k+1)
     float gmi, gt;
     float gi[8];  // gm of the destination of each edge of the block (0: masked)
     __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
@@ -668,20 +683,19 @@ struct BwdBody {
         gt = fmaf(r.gm * wt, f, gt);
         gi[e & 7] = fmaf(gmi, wt, gi[e & 7]);
     }
-    // dWf[a,k] += gm_ia t_ja fcut rbf_k, once per edge (segment-independent)
+    // dWf[a,k] += gm_ia t_ja fcut rbf_k, once per edge (segment-independent),
+    // two k per FFMA2
     __device__ void block(const EdgeStage<K>& s, int e0, const Reg (&r)[8], int, int) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const float gg = gi[u] * r[u].t;
+            const uint64_t gg = f32x2_splat(gi[u] * r[u].t);
             gi[u] = 0.f;
-            const float4* fr = reinterpret_cast<const float4*>(s.fcp + (e0 + u) * K);
+            const ulonglong2* fr = reinterpret_cast<const ulonglong2*>(s.fcp + (e0 + u) * K);
 #pragma unroll
             for (int k4 = 0; k4 < K / 4; ++k4) {
-                const float4 q = fr[k4];
-                dw[4 * k4] = fmaf(gg, q.x, dw[4 * k4]);
-                dw[4 * k4 + 1] = fmaf(gg, q.y, dw[4 * k4 + 1]);
-                dw[4 * k4 + 2] = fmaf(gg, q.z, dw[4 * k4 + 2]);
-                dw[4 * k4 + 3] = fmaf(gg, q.w, dw[4 * k4 + 3]);
+                const ulonglong2 q = fr[k4];
+                dw2[2 * k4] = ffma2(gg, q.x, dw2[2 * k4]);
+                dw2[2 * k4 + 1] = ffma2(gg, q.y, dw2[2 * k4 + 1]);
             }
         }
     }
@@ -711,12 +725,15 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_bwd(Dev d, int l) {
     }
     BwdBody<H, K, TC> b{d, l == 0 ? d.tanh_emb : d.t[l], l, c.lt};
 #pragma unroll
-    for (int k = 0; k < K; ++k) b.w[k] = TC ? 0.f : d.wf[l][c.lt * K + k], b.dw[k] = 0.f;
+    for (int k = 0; k < K; ++k) b.w[k] = TC ? 0.f : d.wf[l][c.lt * K + k];
+#pragma unroll
+    for (int k = 0; k < K / 2; ++k) b.dw2[k] = 0ull;
 #pragma unroll
     for (int u = 0; u < 8; ++u) b.gi[u] = 0.f;
     walk_edges<H, K>(d, c, b, ft);
 #pragma unroll
-    for (int k = 0; k < K; ++k) red[c.g * H * K + c.lt * K + k] = b.dw[k];
+    for (int k = 0; k < K / 2; ++k)
+        f32x2_unpack(b.dw2[k], red[c.g * H * K + c.lt * K + 2 * k], red[c.g * H * K + c.lt * K + 2 * k + 1]);
     if constexpr (TC) {
         filter_teardown(c.tslot);
     } else {
