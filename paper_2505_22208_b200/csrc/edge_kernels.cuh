@@ -192,9 +192,9 @@ __device__ __forceinline__ void filter_mma(uint32_t tcol, const FilterTc& f, con
 //   static constexpr bool kFilter;   tensor-core filter values passed to edge()
 //   static constexpr int  kParts;    staged arrays besides col/dst
 //   struct Reg;  void load(const EdgeStage<K>&, int e, int j, Reg&);
-//   void edge(const EdgeStage<K>&, int e, const Reg&, float filter, float w);
-//        (w is 1 for the edges of the current segment, 0 otherwise: bodies must
-//        be linear in w so masked edges contribute exactly nothing)
+//   void edge(const EdgeStage<K>&, int e, const Reg&, float filter, unsigned on);
+//        (on is 1 for the edges of the current segment, 0 otherwise: bodies
+//        predicate their accumulation on it; every edge is "on" exactly once)
 //   void begin(int i); void end(int i);     destination-atom brackets
 //   static constexpr bool kBlockHook;  if set, block(st, e0, r, ulo, uhi) runs once
 //        per 8-edge block after its segments (segment-independent per-edge work;
@@ -291,9 +291,9 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
                             body.begin(cur);
                         } while (cur < i);
                     }
+                    const unsigned on = ((1u << u1) - 1u) & ~((1u << u0) - 1u);  // this segment's edges
 #pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        body.edge(st, blk * 8 + u, r[u], f[u], (u >= u0 && u < u1) ? 1.f : 0.f);
+                    for (int u = 0; u < 8; ++u) body.edge(st, blk * 8 + u, r[u], f[u], (on >> u) & 1u);
                 }
                 if constexpr (Body::kBlockHook) body.block(st, blk * 8, r, ulo, uhi);
             }
@@ -380,9 +380,9 @@ struct MessageBody {
         const int row = l == 0 ? __ldg(d.Z + j) - 1 : j;
         r.t = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
     }
-    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f, float wt) {
+    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f, unsigned on) {
         if constexpr (!TC) f = filter_ffma<K>(w, s, e);
-        m = fmaf(r.t * wt, f, m);
+        if (on) m = fmaf(r.t, f, m);
     }
     __device__ void begin(int) { m = 0.f; }
     __device__ void end(int i) { mu[static_cast<int64_t>(i) * H + a] = tanhf(m); }
@@ -434,9 +434,10 @@ struct ForceBody {
         const int row = L > 0 ? j : __ldg(d.Z + j) - 1;
         r.t = __ldg(T + static_cast<int64_t>(row) * H + a);
     }
-    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float, float wt) {
+    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float, unsigned on) {
+        if (!on) return;
         const float4 gv = s.geo[e];
-        const float fw = gv.w * wt;
+        const float fw = gv.w;
         const float tf = r.t * fw;
         Y0 = fmaf(tf, gv.x, Y0);
         Y1 = fmaf(tf, gv.y, Y1);
@@ -445,7 +446,7 @@ struct ForceBody {
         U1 = fmaf(fw, gv.y, U1);
         U2 = fmaf(fw, gv.z, U2);
         if (a < K) {
-            const float fr = s.fcp[e * K + a] * wt;
+            const float fr = s.fcp[e * K + a];
             V0 = fmaf(fr, gv.x, V0);
             V1 = fmaf(fr, gv.y, V1);
             V2 = fmaf(fr, gv.z, V2);
@@ -577,10 +578,11 @@ struct HeadBody {
         const float* gp = d.gF + (static_cast<int64_t>(j) * D + chj) * 3;
         r.g0 = __ldg(gp), r.g1 = __ldg(gp + 1), r.g2 = __ldg(gp + 2);
     }
-    __device__ void edge(const EdgeStage<K>& st, int e, const Reg& r, float, float wt) {
+    __device__ void edge(const EdgeStage<K>& st, int e, const Reg& r, float, unsigned on) {
+        if (!on) return;
         const float4 gv = st.geo[e];
-        const float di = (gf0 * gv.x + gf1 * gv.y + gf2 * gv.z) * wt;
-        const float dj = (r.g0 * gv.x + r.g1 * gv.y + r.g2 * gv.z) * wt;
+        const float di = gf0 * gv.x + gf1 * gv.y + gf2 * gv.z;
+        const float dj = r.g0 * gv.x + r.g1 * gv.y + r.g2 * gv.z;
         const float sij = gv.w * (di - dj);
         S += sij;
         W = fmaf(sij, r.t, W);
@@ -678,10 +680,11 @@ struct BwdBody {
         const int row = l == 0 ? __ldg(d.Z + j) - 1 : j;
         r.t = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
     }
-    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f, float wt) {
+    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f, unsigned on) {
+        if (!on) return;
         if constexpr (!TC) f = filter_ffma<K>(w, s, e);
-        gt = fmaf(r.gm * wt, f, gt);
-        gi[e & 7] = fmaf(gmi, wt, gi[e & 7]);
+        gt = fmaf(r.gm, f, gt);
+        gi[e & 7] = gmi;
     }
     // dWf[a,k] += gm_ia t_ja fcut rbf_k, once per edge (segment-independent),
     // two k per FFMA2
