@@ -223,6 +223,7 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     ensure_buf(c, "Epred", 8 * Bc * D, changed);
     ensure_buf(c, "gE", 4 * Bc * D, changed);
     ensure_buf(c, "gF", 12 * Nc * D, changed);
+    ensure_buf(c, "gFc", 16 * Nc, changed);
     ensure_buf(c, "sample_terms", 16 * Bc, changed);
     ensure_buf(c, "gh", 4 * static_cast<size_t>(Nc) * H, changed);
     ensure_buf(c, "gm", 4 * static_cast<size_t>(Nc) * H, changed);
@@ -295,6 +296,7 @@ Dev make_dev(Ctx& c) {
     d.Epred = buf(c, "Epred").as<double>();
     d.gE = buf(c, "gE").as<float>();
     d.gF = buf(c, "gF").as<float>();
+    d.gFc = buf(c, "gFc").as<float4>();
     d.sample_terms = buf(c, "sample_terms").as<double>();
     d.block_scratch = c.block_scratch.as<double>();
     d.gh = buf(c, "gh").as<float>();

@@ -101,6 +101,7 @@ struct Dev {
     // loss gradients
     float* gE;               // [B][D]
     float* gF;               // [N][D][3]
+    float4* gFc;             // [N] dL/dF of the atom's own head (loss path), w = 0
     double* sample_terms;    // [B][2]
     double* block_scratch;   // reduction scratch
     // backward

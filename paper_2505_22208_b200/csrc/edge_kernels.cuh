@@ -561,7 +561,8 @@ struct HeadBody {
     static constexpr int kParts = kPartGeo | kPartPlain;
     static constexpr bool kBlockHook = false;
     struct Reg {
-        float t, g0, g1, g2;
+        float t;
+        float4 g;  // upstream dL/dF of the source atom for its own head
     };
     const Dev& d;
     const float* __restrict__ T;
@@ -569,20 +570,25 @@ struct HeadBody {
     float* acc;  // smem [3][D][H] + [D][K], this group's
     int a, D, L, pass_ch, first;
     int s, ch;
-    float Ti, S, W, R, gf0, gf1, gf2;
+    float Ti, S, W, R;
+    float4 gf;
+    // loss path (pass_ch < 0): the compact per-atom gradient of k_loss (one head
+    // per atom); general upstream: head pass_ch of gF
+    __device__ float4 upstream(int j) const {
+        if (pass_ch < 0) return __ldg(d.gFc + j);
+        const float* gp = d.gF + (static_cast<int64_t>(j) * D + pass_ch) * 3;
+        return make_float4(__ldg(gp), __ldg(gp + 1), __ldg(gp + 2), 0.f);
+    }
     __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
         const int row = L > 0 ? j : __ldg(d.Z + j) - 1;
         r.t = __ldg(T + static_cast<int64_t>(row) * H + a);
-        // channel of the edge's own sample (the block may run ahead of begin())
-        const int chj = pass_ch >= 0 ? pass_ch : __ldg(d.chan + j);
-        const float* gp = d.gF + (static_cast<int64_t>(j) * D + chj) * 3;
-        r.g0 = __ldg(gp), r.g1 = __ldg(gp + 1), r.g2 = __ldg(gp + 2);
+        r.g = upstream(j);
     }
     __device__ void edge(const EdgeStage<K>& st, int e, const Reg& r, float, unsigned on) {
         if (!on) return;
         const float4 gv = st.geo[e];
-        const float di = gf0 * gv.x + gf1 * gv.y + gf2 * gv.z;
-        const float dj = r.g0 * gv.x + r.g1 * gv.y + r.g2 * gv.z;
+        const float di = gf.x * gv.x + gf.y * gv.y + gf.z * gv.z;
+        const float dj = r.g.x * gv.x + r.g.y * gv.y + r.g.z * gv.z;
         const float sij = gv.w * (di - dj);
         S += sij;
         W = fmaf(sij, r.t, W);
@@ -593,8 +599,7 @@ struct HeadBody {
         ch = pass_ch >= 0 ? pass_ch : d.dsidx[s];
         const int row = L > 0 ? i : __ldg(d.Z + i) - 1;
         Ti = __ldg(T + static_cast<int64_t>(row) * H + a);
-        const float* gp = d.gF + (static_cast<int64_t>(i) * D + ch) * 3;
-        gf0 = gp[0], gf1 = gp[1], gf2 = gp[2];
+        gf = upstream(i);
         S = W = R = 0.f;
     }
     __device__ void end(int i) {
@@ -604,11 +609,18 @@ struct HeadBody {
         float gh;
         const float* gE = d.gE + static_cast<int64_t>(s) * D;
         if (first) {
-            gh = 0.f;
-            for (int dd = 0; dd < D; ++dd) gh = fmaf(d.we[a * D + dd], gE[dd], gh);
             const int row = L > 0 ? i : __ldg(d.Z + i) - 1;
             const float hv = hL[static_cast<int64_t>(row) * H + a];
-            for (int dd = 0; dd < D; ++dd) acc[(2 * D + dd) * H + a] = fmaf(hv, gE[dd], acc[(2 * D + dd) * H + a]);
+            if (pass_ch < 0) {  // k_loss zeroes every head but the sample's own: same sums, one term
+                const float ge = gE[ch];
+                gh = d.we[a * D + ch] * ge;
+                acc[(2 * D + ch) * H + a] = fmaf(hv, ge, acc[(2 * D + ch) * H + a]);
+            } else {
+                gh = 0.f;
+                for (int dd = 0; dd < D; ++dd) gh = fmaf(d.we[a * D + dd], gE[dd], gh);
+                for (int dd = 0; dd < D; ++dd)
+                    acc[(2 * D + dd) * H + a] = fmaf(hv, gE[dd], acc[(2 * D + dd) * H + a]);
+            }
         } else {
             gh = *ghp;
         }

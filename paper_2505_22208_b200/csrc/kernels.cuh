@@ -380,6 +380,7 @@ __global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy) {
         for (int64_t a = lo + threadIdx.x; a < hi; a += 128) {
             float* g = d.gF + a * 3 * D;
             for (int q = 0; q < 3 * D; ++q) g[q] = 0.f;
+            float4 gc = make_float4(0.f, 0.f, 0.f, 0.f);
             if (fm) {
                 double df[3], sq = 0.0;
 #pragma unroll
@@ -389,10 +390,14 @@ __global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy) {
                 }
                 const double dist = sqrt(sq);
                 fsum += ws * dist;
-                if (dist > 0.0)
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) g[ds * 3 + c] = static_cast<float>(ws * df[c] / dist);
+                if (dist > 0.0) {
+                    gc.x = static_cast<float>(ws * df[0] / dist);
+                    gc.y = static_cast<float>(ws * df[1] / dist);
+                    gc.z = static_cast<float>(ws * df[2] / dist);
+                    g[ds * 3] = gc.x, g[ds * 3 + 1] = gc.y, g[ds * 3 + 2] = gc.z;
+                }
             }
+            d.gFc[a] = gc;
         }
         red[threadIdx.x] = fsum;
         __syncthreads();
