@@ -229,7 +229,8 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     ensure_buf(c, "gm", 4 * static_cast<size_t>(Nc) * H, changed);
     for (int l = 0; l < L; ++l) {
         ensure_buf(c, "part_wf" + std::to_string(l), 4 * static_cast<size_t>(c.grid_edge) * H * K, changed);
-        ensure_buf(c, "part_wu" + std::to_string(l), 4 * static_cast<size_t>(c.grid_gemm) * H * H, changed);
+        ensure_buf(c, "part_wu" + std::to_string(l),
+                   4 * static_cast<size_t>(std::max(c.grid_gemm, c.grid_upd)) * H * H, changed);
     }
     ensure_buf(c, "part_head", 4 * static_cast<size_t>(c.grid_edge) * (3 * H + K) * D, changed);
     ensure_buf(c, "part_emb", 4 * static_cast<size_t>(c.grid_emb) * kMaxZ * H, changed);
@@ -428,6 +429,7 @@ struct Model {
     using ES = EdgeKernelSmem<H, K>;
     static constexpr size_t kGemmSmem = NodeGemmSmem<H>::bytes;
     static constexpr size_t kDwuSmem = DwuSmem<H>::bytes;
+    static constexpr bool kFusedBwd = H == 128;  // k_bwd_gemm: update backward + dW_u in one kernel
     static size_t smem_message() { return ES::message(); }
     static size_t smem_force(int D) { return ES::force(D); }
     static size_t smem_head(int D) { return ES::head(D); }
@@ -440,6 +442,7 @@ struct Model {
     static void setup(Ctx& c) {
         set_smem((const void*)k_node_gemm<H>, kGemmSmem);
         set_smem((const void*)k_dwu<H>, kDwuSmem);
+        if constexpr (kFusedBwd) set_smem((const void*)k_bwd_gemm<H>, BwdGemmSmem<H>::bytes);
         set_smem((const void*)k_edge_message<H, K>, smem_message());
         int smem_max = 0;
         CK(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
@@ -451,7 +454,9 @@ struct Model {
         set_smem((const void*)k_edge_bwd<H, K>, smem_bwd());
         set_smem((const void*)k_emb_grad, sizeof(float) * kMaxZ * H);
         c.grid_emb = c.nsm;
-        c.grid_upd = c.nsm;            // one tcgen05 CTA per SM, persistent over 128-atom tiles
+        // one tcgen05 CTA per SM, persistent over 128-atom tiles; a multiple of the
+        // column split so a CTA keeps one column block (k_bwd_gemm's dW_u partials)
+        c.grid_upd = c.nsm / NodeGemmCfg<H>::NS * NodeGemmCfg<H>::NS;
         c.grid_gemm = c.nsm / 2;       // split-K CTAs of dW_u (one partial each)
         // one edge partitioning (k_scan) serves all four edge kernels: size it so
         // every CTA of the heaviest one is resident (no second wave)
@@ -508,8 +513,12 @@ struct Model {
             launch(c, "head_bwd", k_edge_head<H, K>, c.grid_edge, kGroups * H, smem_head(c.D), d, general ? q : -1,
                    q == 0 ? 1 : 0);
         for (int l = c.L - 1; l >= 0; --l) {
-            launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 1);
-            launch(c, "dwu", k_dwu<H>, c.grid_gemm, 256, kDwuSmem, d, l);
+            if constexpr (kFusedBwd) {
+                launch(c, "bwd_gemm", k_bwd_gemm<H>, c.grid_upd, 256, BwdGemmSmem<H>::bytes, d, l);
+            } else {
+                launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 1);
+                launch(c, "dwu", k_dwu<H>, c.grid_gemm, 256, kDwuSmem, d, l);
+            }
             launch(c, "bwd_edge", k_edge_bwd<H, K>, c.grid_edge, kGroups * H, smem_bwd(), d, l);
         }
         SegTable tab{};
@@ -521,7 +530,12 @@ struct Model {
         launch(c, "emb_grad", k_emb_grad, c.grid_emb, 128, sizeof(float) * kMaxZ * H, d);
         add(static_cast<int64_t>(kMaxZ) * H, 1, d.part_emb, c.grid_emb, 0);
         for (int l = 0; l < c.L; ++l) add(H * K, 0, d.part_wf[l], c.grid_edge, H * K);
-        for (int l = 0; l < c.L; ++l) add(H * H, 0, d.part_wu[l], c.grid_gemm, H * H);
+        for (int l = 0; l < c.L; ++l) {
+            if constexpr (kFusedBwd)  // CTA c holds column block c % NS as [H][NC]
+                add(H * H, 2, d.part_wu[l], c.grid_upd, H * NodeGemmCfg<H>::NC);
+            else
+                add(H * H, 0, d.part_wu[l], c.grid_gemm, H * H);
+        }
         const int hw = (3 * H + K) * c.D;
         add(H * c.D, 0, d.part_head + (2 * H + K) * c.D, c.grid_edge, hw);
         add((2 * H + K) * c.D, 0, d.part_head, c.grid_edge, hw);

@@ -228,6 +228,203 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
     if (warp == 0) umma::tmem_dealloc(tbase, kCols);
 }
 
+// Backward of the update GEMM fused with its weight gradient (H = 128):
+//   gm = (gh W_u) (.) (1 - mu^2)        MMA1: A = the gh tile from TMEM (lane = atom),
+//                                       B = W_u block (K-major, TMA)   (S/model.cpp:380-390)
+//   dW_u[:, cols] += gh^T mu[:, cols]   MMA2: A = the same gh tile from shared memory
+//                                       as an MN-major operand (M = rows of W_u, K =
+//                                       atoms), B = the mu rows the epilogue loads
+//                                       anyway, MN-major in the weights' place once
+//                                       MMA1 is done                     (S/model.cpp:381-383)
+// The dW_u accumulator stays in TMEM across the CTA's tiles; one [H][NC] partial
+// per CTA (its column block never changes: gridDim.x % NS == 0), summed by
+// k_grad_reduce. TMEM: [0, NC) gm accumulator, [NC, 2 NC) dW_u, [256, 384) gh hi,
+// [384, 512) gh lo.
+template <int H>
+struct BwdGemmSmem {
+    static constexpr int NC = NodeGemmCfg<H>::NC;
+    static constexpr size_t g_floats = 2 * kGemmM * H;  // gh tile hi | lo, MN-major (M = H rows)
+    static constexpr size_t b_floats = NodeGemmCfg<H>::b_floats > 2 * kGemmM * NC ? NodeGemmCfg<H>::b_floats
+                                                                                   : 2 * kGemmM * NC;
+    static constexpr size_t bytes = 4 * (g_floats + b_floats) + 64 + 1024;  // + alignment slack
+};
+
+template <int H>
+__global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
+    using Cfg = NodeGemmCfg<H>;
+    constexpr int NS = Cfg::NS, NC = Cfg::NC, CW = NC / 2;
+    static_assert(H == 128 && CW % 16 == 0, "fused update backward: H = 128");
+    constexpr int GA = H / 32, MA = NC / 32;  // MN atoms of the gh and mu tiles
+    float* sm = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(dyn_smem<float>()) + 1023) & ~uintptr_t(1023));
+    float* Ghi = sm;
+    float* Glo = Ghi + kGemmM * H;
+    float* Bhi = Glo + kGemmM * H;  // weights [NC][H] hi | lo, then the mu tile hi | lo
+    uint64_t* bar = reinterpret_cast<uint64_t*>(Bhi + BwdGemmSmem<H>::b_floats);  // weights, MMA1, MMA2
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int quad = warp & 3, half = warp >> 2;
+    if (warp == 0) umma::tmem_alloc(tslot, 512);
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init(&bar[2], 1);
+        mbar_fence_init();
+    }
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+    const uint32_t tbase = *tslot;
+    const uint32_t tD1 = tbase, tD2 = tbase + NC, tAh = tbase + 256, tAl = tbase + 384;
+    const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
+    const uint32_t idesc = umma::idesc_tf32(kGemmM, NC);
+    const uint32_t idesc_mn = umma::idesc_tf32(kGemmM, NC) | (1u << 15) | (1u << 16);
+    const int N = d.hdr->N;  // staged upload
+    const int ntiles = (N + kGemmM - 1) / kGemmM * NS;
+    const int np = blockIdx.x % NS;
+    uint32_t wphase = 0, mphase = 0, dphase = 0;
+    auto fetch_weights = [&]() {
+        if (tid == 0) {
+            const float* wsrc = d.wpack + static_cast<int64_t>(4 * l + 2) * H * H + static_cast<int64_t>(np) * 2 * NC * H;
+            mbar_expect_tx(&bar[0], static_cast<uint32_t>(Cfg::b_floats * 4));
+            bulk_g2s(Bhi, wsrc, static_cast<uint32_t>(Cfg::b_floats * 4), &bar[0]);
+        }
+    };
+    if (static_cast<int>(blockIdx.x) < ntiles) fetch_weights();
+    pdl_enter();
+    const float* __restrict__ gh = d.gh;
+    const float* __restrict__ mu = d.mu[l];
+    int done = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++done) {
+        const int base = (tile / NS) * kGemmM;
+        const int row = quad * 32 + lane, atom = base + row;
+        const bool live = atom < N;
+        if (done > 0) {  // MMA2 of the previous tile read the gh tile and the mu tile in B
+            mbar_wait(&bar[2], dphase);
+            dphase ^= 1u;
+            umma::fence_after();
+            fetch_weights();
+        }
+        // gh row of this thread's atom, columns [half*64, half*64+64): TMEM (MMA1's A)
+        // and the MN-major shared tile (MMA2's A), tf32 hi | lo
+#pragma unroll
+        for (int c = 0; c < H / 2; c += 16) {
+            const int b0 = half * (H / 2) + c;
+            float v[16], hv[16], lv[16];
+#pragma unroll
+            for (int q = 0; q < 16; q += 4) {
+                const float4 x = live ? __ldg(reinterpret_cast<const float4*>(gh + static_cast<int64_t>(atom) * H + b0 + q))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                v[q] = x.x, v[q + 1] = x.y, v[q + 2] = x.z, v[q + 3] = x.w;
+            }
+#pragma unroll
+            for (int q = 0; q < 16; ++q) umma::split_tf32(v[q], hv[q], lv[q]);
+            umma::st16(tAh + lane_off + b0, hv);
+            umma::st16(tAl + lane_off + b0, lv);
+#pragma unroll
+            for (int q = 0; q < 16; q += 4) {
+                const int o = umma::mn32_idx(b0 + q, row, GA);
+                *reinterpret_cast<float4*>(Ghi + o) = make_float4(hv[q], hv[q + 1], hv[q + 2], hv[q + 3]);
+                *reinterpret_cast<float4*>(Glo + o) = make_float4(lv[q], lv[q + 1], lv[q + 2], lv[q + 3]);
+            }
+        }
+        umma::st_wait();
+        umma::fence_proxy_async();
+        umma::fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            mbar_wait(&bar[0], wphase);
+            umma::fence_after();
+            const float* Blo = Bhi + NC * H;
+#pragma unroll
+            for (int s = 0; s < H / 8; ++s) {
+                umma::mma_tf32_ts(tD1, tAh + s * 8, umma::kdesc(Bhi, s, H), idesc, s ? 1u : 0u);
+                umma::mma_tf32_ts(tD1, tAh + s * 8, umma::kdesc(Blo, s, H), idesc, 1u);
+                umma::mma_tf32_ts(tD1, tAl + s * 8, umma::kdesc(Bhi, s, H), idesc, 1u);
+            }
+            umma::commit(&bar[1]);
+        }
+        wphase ^= 1u;
+        // mu row of this thread's atom, this CTA's columns: epilogue (1 - mu^2) and MMA2's B
+        const int c0 = np * NC + half * CW;
+        float pre[CW];
+#pragma unroll
+        for (int q = 0; q < CW; q += 4) {
+            const float4 x = live ? __ldg(reinterpret_cast<const float4*>(mu + static_cast<int64_t>(atom) * H + c0 + q))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            pre[q] = x.x, pre[q + 1] = x.y, pre[q + 2] = x.z, pre[q + 3] = x.w;
+        }
+        mbar_wait(&bar[1], mphase);
+        mphase ^= 1u;
+        umma::fence_after();
+        {
+            float* Mhi = Bhi;  // the weight block is free
+            float* Mlo = Bhi + kGemmM * NC;
+#pragma unroll
+            for (int q = 0; q < CW; q += 4) {
+                float4 h4, l4;
+                umma::split_tf32(pre[q], h4.x, l4.x);
+                umma::split_tf32(pre[q + 1], h4.y, l4.y);
+                umma::split_tf32(pre[q + 2], h4.z, l4.z);
+                umma::split_tf32(pre[q + 3], h4.w, l4.w);
+                const int o = umma::mn32_idx(half * CW + q, row, MA);
+                *reinterpret_cast<float4*>(Mhi + o) = h4;
+                *reinterpret_cast<float4*>(Mlo + o) = l4;
+            }
+            umma::fence_proxy_async();
+            umma::fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                umma::fence_after();
+#pragma unroll
+                for (int s = 0; s < kGemmM / 8; ++s) {  // K-step s: atoms 8s..8s+7 = two 4-row groups
+                    const uint64_t ah = umma::mn32_desc(Ghi + s * 2 * (GA << 7), GA);
+                    const uint64_t al = umma::mn32_desc(Glo + s * 2 * (GA << 7), GA);
+                    const uint64_t bh = umma::mn32_desc(Mhi + s * 2 * (MA << 7), MA);
+                    const uint64_t bl = umma::mn32_desc(Mlo + s * 2 * (MA << 7), MA);
+                    umma::mma3(tD2, ah, al, bh, bl, idesc_mn, (done | s) ? 1u : 0u);
+                }
+                umma::commit(&bar[2]);
+            }
+        }
+        // gm = (gh W_u) (.) (1 - mu^2)
+#pragma unroll
+        for (int cc = 0; cc < CW; cc += 16) {
+            float v[16];
+            umma::ld16(tD1 + lane_off + half * CW + cc, v);
+            if (!live) continue;
+            float* go = d.gm + static_cast<int64_t>(atom) * H + c0 + cc;
+#pragma unroll
+            for (int q = 0; q < 16; q += 4)
+                *reinterpret_cast<float4*>(go + q) =
+                    make_float4(v[q] * (1.f - pre[cc + q] * pre[cc + q]), v[q + 1] * (1.f - pre[cc + q + 1] * pre[cc + q + 1]),
+                                v[q + 2] * (1.f - pre[cc + q + 2] * pre[cc + q + 2]),
+                                v[q + 3] * (1.f - pre[cc + q + 3] * pre[cc + q + 3]));
+        }
+        umma::fence_before();
+        __syncthreads();  // the gm accumulator is drained before the next tile's MMA1
+        umma::fence_after();
+    }
+    // this CTA's dW_u partial: rows b = TMEM lanes, columns of block np
+    if (done > 0) {
+        mbar_wait(&bar[2], dphase);
+        umma::fence_after();
+    }
+    const int row = quad * 32 + lane;
+    float* part = d.part_wu[l] + static_cast<int64_t>(blockIdx.x) * H * NC;
+#pragma unroll
+    for (int cc = 0; cc < CW; cc += 16) {
+        float v[16];
+        umma::ld16(tD2 + lane_off + half * CW + cc, v);
+#pragma unroll
+        for (int k = 0; k < 16; k += 4)
+            *reinterpret_cast<float4*>(part + row * NC + half * CW + cc + k) =
+                done > 0 ? make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 0) umma::tmem_dealloc(tbase, 512);
+}
+
 template <int H>
 struct DwuSmem {
     static constexpr size_t stage_floats = 4 * kGemmM * kGemmKC;  // A hi|lo, B hi|lo

@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(128) k_emb_grad(Dev d) {
 // ------------------------------------------------------- grad reduction ---
 struct Seg {
     int64_t dst;
-    int32_t n, kind;  // kind 0: dense, 1: embedding rows through z_to_slot
+    int32_t n, kind;  // kind 0: dense, 1: embedding rows through z_to_slot, 2: column-split
     const float* src;
     int32_t ncta, stride;
 };
@@ -518,6 +518,12 @@ __global__ void __launch_bounds__(256) k_grad_reduce(Dev d, SegTable tab) {
                 const int slot = d.z_to_slot[zrow + 1];
                 if (slot >= 0)
                     for (int c = g; c < sg.ncta; c += 8) acc += sg.src[static_cast<int64_t>(c) * ns * H + slot * H + a];
+            } else if (sg.kind == 2) {
+                // column-split partials: CTA c holds columns [np*nc, np*nc+nc), np = c % (H/nc)
+                const int nc = sg.stride / H, nsplit = H / nc;
+                const int b = static_cast<int>(off / H), a = static_cast<int>(off % H), np = a / nc;
+                for (int c = np + nsplit * g; c < sg.ncta; c += 8 * nsplit)
+                    acc += sg.src[static_cast<int64_t>(c) * sg.stride + b * nc + (a - np * nc)];
             } else {
                 for (int c = g; c < sg.ncta; c += 8) acc += sg.src[static_cast<int64_t>(c) * sg.stride + off];
             }

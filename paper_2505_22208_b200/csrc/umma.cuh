@@ -112,6 +112,39 @@ __device__ __forceinline__ void ld8(uint32_t taddr, float (&v)[8]) {
     for (int k = 0; k < 8; ++k) v[k] = __uint_as_float(r[k]);
 }
 
+// MMA with A from TMEM (lane = row m, 32-bit column = k) and B from shared memory.
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// 32 TMEM lanes x 16 columns from registers (thread t of the warp -> lane 32*(warp%4) + t).
+__device__ __forceinline__ void st16(uint32_t taddr, const float (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// MN-major operand in the SWIZZLE_128B_BASE32B layout (the MN-major form the
+// tensor core accepts for 32-bit types): atoms of 4 K-rows x 128 B along MN,
+// 32-byte chunks XOR-swizzled by the K-row; MN atoms `lbo` bytes apart, 4-row K
+// groups `sbo` bytes apart. Element (mn, k) of such a tile, in floats, with
+// `mn_atoms` = MN extent / 32; the tile must be 512-byte aligned.
+__device__ __forceinline__ int mn32_idx(int mn, int k, int mn_atoms) {
+    return ((mn >> 5) << 7) + (k >> 2) * (mn_atoms << 7) + ((k & 3) << 5) + (((((mn & 31) >> 3) ^ (k & 3))) << 3) +
+           (mn & 7);
+}
+__device__ __forceinline__ uint64_t mn32_desc(const float* tile, int mn_atoms) {
+    return sdesc(tile, 512u, static_cast<uint32_t>(mn_atoms) * 512u) | (1ull << 61);  // layout 1: 128B_BASE32B
+}
+
 // fp32 -> (tf32 hi, fp32 lo) split for 3xTF32.
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
     uint32_t h;
