@@ -77,6 +77,7 @@ struct Dev {
     const uint8_t* thas;
     // edges
     int32_t *cnt, *row_ptr, *col, *dst;
+    uint32_t* segw;            // bit p set: edge p is the first of its destination atom
     int32_t* part_lo;          // [Q+1] edge-balanced atom partitions (edge kernels)
     float4* geo;
     float* rbf;                // [P][K] fcut * Gaussians, canonical tcgen05 layout, tf32 hi part

@@ -47,6 +47,7 @@ template <int K>
 struct EdgeStage {
     int32_t col[kChunk];
     int32_t dst[kChunk];
+    uint32_t segw[8];       // segment-start bits of the 256 edges from word (cb >> 5) & ~3
     float4 geo[kChunk];     // u_x, u_y, u_z, fcut
     float fcp[kChunk * K];  // fcut*rbf, edge-major
     float fch[kChunk * K];  // fcut*rbf, canonical tf32 hi (tensor-core filter)
@@ -111,13 +112,14 @@ enum StageParts : int { kPartGeo = 1, kPartPlain = 2, kPartCanon = 4 };
 template <int K>
 __device__ __forceinline__ void stage_chunk(const Dev& d, EdgeStage<K>& s, uint64_t* b, int cb, int e1, int parts) {
     const int n = min(kChunk, ((e1 - cb) + 7) & ~7);
-    uint32_t bytes = 8u * n;
+    uint32_t bytes = 8u * n + 32u;
     if (parts & kPartGeo) bytes += 16u * n;
     if (parts & kPartPlain) bytes += 4u * K * n;
     if (parts & kPartCanon) bytes += 8u * K * n;
     mbar_expect_tx(b, bytes);
     bulk_g2s(s.col, d.col + cb, 4 * n, b);
     bulk_g2s(s.dst, d.dst + cb, 4 * n, b);
+    bulk_g2s(s.segw, d.segw + ((cb >> 5) & ~3), 32, b);
     if (parts & kPartGeo) bulk_g2s(s.geo, d.geo + cb, 16 * n, b);
     if (parts & kPartPlain) bulk_g2s(s.fcp, d.rbfp + static_cast<int64_t>(cb) * K, 4 * K * n, b);
     if (parts & kPartCanon) {
@@ -261,9 +263,6 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
 #pragma unroll
                     for (int u = 0; u < 8; ++u) body.load(st, (blk + 1) * 8 + u, jj[u], rn[u]);
                 }
-                const int4 i0 = reinterpret_cast<const int4*>(st.dst)[2 * blk];
-                const int4 i1 = reinterpret_cast<const int4*>(st.dst)[2 * blk + 1];
-                const int ii[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
                 const int ulo = max(ea - blk * 8, 0), uhi = min(eb - blk * 8, 8);
                 float f[8];
                 if constexpr (kF) {
@@ -275,10 +274,8 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
                 // destination segments of the block: one flush call site per
                 // block (keeps end()/begin() inlined once), branch-free edges
                 const unsigned vm = ((1u << uhi) - 1u) & ~((1u << ulo) - 1u);
-                unsigned seg = 1u << ulo;
-#pragma unroll
-                for (int u = 1; u < 8; ++u) seg |= (ii[u] != ii[u - 1] ? 1u : 0u) << u;
-                seg &= vm;
+                const int bp = cb - (((cb >> 5) & ~3) << 5) + blk * 8;  // bit of the block's first edge
+                unsigned seg = (((st.segw[bp >> 5] >> (bp & 31)) & 0xFFu) | (1u << ulo)) & vm;
                 while (seg) {
                     const int u0 = __ffs(seg) - 1;
                     seg &= seg - 1u;

@@ -215,8 +215,11 @@ __global__ void __launch_bounds__(1024) k_scan(Dev d, int Q) {
     if (P == 0)
         for (int q = t; q < Q; q += 1024) d.part_lo[q] = 0;
     // CSR padding read by the edge kernels' block staging: valid source atom 0
-    if (P <= d.Pcap)
+    if (P <= d.Pcap) {
         for (int x = t; x < kChunk + 8; x += 1024) d.col[P + x] = 0, d.dst[P + x] = N;
+        // segment-start bits, set by k_nbr_fill (+ the padding words the staging reads)
+        for (int x = t; x < (P + kChunk + 8) / 32 + 16; x += 1024) d.segw[x] = 0u;
+    }
     if (t == 1023) {
         d.row_ptr[N] = run;
         d.part_lo[Q] = N;
@@ -244,6 +247,7 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d) {
         const int lo = static_cast<int>(d.atom_ptr[s]), hi = static_cast<int>(d.atom_ptr[s + 1]);
         const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
         int base = d.row_ptr[i];
+        if (lane == 0 && d.row_ptr[i + 1] > base) atomicOr(d.segw + (base >> 5), 1u << (base & 31));
         for (int j0 = lo; j0 < hi; j0 += 32) {
             const int j = j0 + lane;
             bool in = false;
