@@ -198,6 +198,9 @@ __device__ __forceinline__ void filter_mma(uint32_t tcol, const FilterTc& f, con
 //        (on is 1 for the edges of the current segment, 0 otherwise: bodies
 //        predicate their accumulation on it; every edge is "on" exactly once)
 //   void begin(int i); void end(int i);     destination-atom brackets
+//   static constexpr bool kPrepare;  if set, prepare(st, e0) runs once per 8-edge
+//        block before its segments, warp-converged (per-edge scalar work done by 8
+//        lanes and broadcast with shuffles instead of by every channel thread)
 //   static constexpr bool kBlockHook;  if set, block(st, e0, r, ulo, uhi) runs once
 //        per 8-edge block after its segments (segment-independent per-edge work;
 //        edges [ulo, uhi) of the block are valid); group-uniform, may group_sync
@@ -264,6 +267,7 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
                     for (int u = 0; u < 8; ++u) body.load(st, (blk + 1) * 8 + u, jj[u], rn[u]);
                 }
                 const int ulo = max(ea - blk * 8, 0), uhi = min(eb - blk * 8, 8);
+                if constexpr (Body::kPrepare) body.prepare(st, blk * 8);
                 float f[8];
                 if constexpr (kF) {
                     umma::ld8(trow + blk * 8, f);
@@ -364,6 +368,7 @@ struct MessageBody {
     static constexpr bool kFilter = TC;
     static constexpr int kParts = TC ? 0 : kPartPlain;
     static constexpr bool kBlockHook = false;
+    static constexpr bool kPrepare = false;
     struct Reg {
         float t;
     };
@@ -419,6 +424,7 @@ struct ForceBody {
     static constexpr bool kFilter = false;
     static constexpr int kParts = kPartGeo | kPartPlain;
     static constexpr bool kBlockHook = false;
+    static constexpr bool kPrepare = false;
     static constexpr int kYW = 3 * H + 3 + 3 * K;  // per-atom feature floats
     struct Reg {
         float t;
@@ -439,10 +445,10 @@ struct ForceBody {
         Y0 = fmaf(tf, gv.x, Y0);
         Y1 = fmaf(tf, gv.y, Y1);
         Y2 = fmaf(tf, gv.z, Y2);
-        U0 = fmaf(fw, gv.x, U0);
-        U1 = fmaf(fw, gv.y, U1);
-        U2 = fmaf(fw, gv.z, U2);
-        if (a < K) {
+        if (a < K) {  // channel-independent sums: first warp only
+            U0 = fmaf(fw, gv.x, U0);
+            U1 = fmaf(fw, gv.y, U1);
+            U2 = fmaf(fw, gv.z, U2);
             const float fr = s.fcp[e * K + a];
             V0 = fmaf(fr, gv.x, V0);
             V1 = fmaf(fr, gv.y, V1);
@@ -557,18 +563,18 @@ struct HeadBody {
     static constexpr bool kFilter = false;
     static constexpr int kParts = kPartGeo | kPartPlain;
     static constexpr bool kBlockHook = false;
+    static constexpr bool kPrepare = true;
     struct Reg {
         float t;
-        float4 g;  // upstream dL/dF of the source atom for its own head
     };
     const Dev& d;
     const float* __restrict__ T;
     const float* __restrict__ hL;
     float* acc;  // smem [3][D][H] + [D][K], this group's
-    int a, D, L, pass_ch, first;
+    int a, D, L, pass_ch, first, N;
     int s, ch;
     float Ti, S, W, R;
-    float4 gf;
+    float es[8], ed[8];  // per edge of the block: s_ij and gF_i.u_ij
     // loss path (pass_ch < 0): the compact per-atom gradient of k_loss (one head
     // per atom); general upstream: head pass_ch of gF
     __device__ float4 upstream(int j) const {
@@ -579,24 +585,39 @@ struct HeadBody {
     __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
         const int row = L > 0 ? j : __ldg(d.Z + j) - 1;
         r.t = __ldg(T + static_cast<int64_t>(row) * H + a);
-        r.g = upstream(j);
+    }
+    // s_ij = fcut (gF_i - gF_j).u_ij is channel-independent: lane u computes edge u
+    __device__ void prepare(const EdgeStage<K>& st, int e0) {
+        const int lane = threadIdx.x & 31;
+        float sij = 0.f, di = 0.f;
+        if (lane < 8) {
+            const int e = e0 + lane;
+            const int i = st.dst[e], j = st.col[e];
+            const float4 gv = st.geo[e];
+            const float4 gi = i < N ? upstream(i) : make_float4(0.f, 0.f, 0.f, 0.f);  // padding: dst = N
+            const float4 gj = upstream(j);
+            di = gi.x * gv.x + gi.y * gv.y + gi.z * gv.z;
+            const float dj = gj.x * gv.x + gj.y * gv.y + gj.z * gv.z;
+            sij = gv.w * (di - dj);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            es[u] = __shfl_sync(0xffffffffu, sij, u);
+            ed[u] = __shfl_sync(0xffffffffu, di, u);
+        }
     }
     __device__ void edge(const EdgeStage<K>& st, int e, const Reg& r, float, unsigned on) {
         if (!on) return;
-        const float4 gv = st.geo[e];
-        const float di = gf.x * gv.x + gf.y * gv.y + gf.z * gv.z;
-        const float dj = r.g.x * gv.x + r.g.y * gv.y + r.g.z * gv.z;
-        const float sij = gv.w * (di - dj);
+        const float sij = es[e & 7];
         S += sij;
         W = fmaf(sij, r.t, W);
-        if (a < K) R = fmaf(di, st.fcp[e * K + a], R);
+        if (a < K) R = fmaf(ed[e & 7], st.fcp[e * K + a], R);
     }
     __device__ void begin(int i) {
         s = d.sample_of[i];
         ch = pass_ch >= 0 ? pass_ch : d.dsidx[s];
         const int row = L > 0 ? i : __ldg(d.Z + i) - 1;
         Ti = __ldg(T + static_cast<int64_t>(row) * H + a);
-        gf = upstream(i);
         S = W = R = 0.f;
     }
     __device__ void end(int i) {
@@ -638,7 +659,7 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_head(Dev d, int pass_ch,
     for (int e = c.lt; e < AW; e += H) acc[e] = 0.f;
     __syncthreads();
     HeadBody<H, K> b{d, d.L > 0 ? d.t[d.L] : d.tanh_emb, d.L > 0 ? d.h[d.L] : d.emb, acc, c.lt, D, d.L, pass_ch,
-                     first};
+                     first, d.hdr->N};
     walk_edges<H, K>(d, c, b, FilterTc{});
     __syncthreads();
     // combine groups in order; emit the CTA partial in parameter layout:
@@ -674,6 +695,7 @@ struct BwdBody {
     static constexpr bool kFilter = TC;
     static constexpr int kParts = kPartPlain;
     static constexpr bool kBlockHook = true;
+    static constexpr bool kPrepare = false;
     struct Reg {
         float gm, t;
     };
