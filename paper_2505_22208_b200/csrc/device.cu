@@ -485,7 +485,6 @@ struct Model {
 
     static void nlist(Ctx& c) {
         const Dev d = make_dev(c);
-        launch(c, "nbr_count", k_nbr_count, c.grid_warp, 256, 0, d);
         launch(c, "nbr_scan", k_scan, 1, 1024, 0, d, c.grid_edge * kGroups);
         launch(c, "nbr_fill", k_nbr_fill<K>, c.grid_warp, 256, 0, d);
     }
@@ -505,7 +504,9 @@ struct Model {
 
     static void loss(Ctx& c, bool energy) {
         const Dev d = make_dev(c);
-        launch(c, "loss", k_loss, c.grid_small, 128, energy ? sizeof(double) * 128 * c.D : 0, d, energy ? 1 : 0);
+        // the train step (energy fused here) only needs the compact per-atom force gradient
+        launch(c, "loss", k_loss, c.grid_small, 128, energy ? sizeof(double) * 128 * c.D : 0, d, energy ? 1 : 0,
+               energy ? 0 : 1);
     }
 
     static void backward(Ctx& c, bool general) {

@@ -8,10 +8,13 @@
 //
 // Reference semantics (S = /root/reference/proj/core/src):
 //   k_prep .......... S/denoise.cpp:7-29 (centering) + S/loss.cpp:113-126 (normalize)
-//   k_nbr_* ......... S/core.cpp:30-48  (bit-exact fp64 pair test, i-major, j ascending)
-//   k_energy/k_loss . S/loss.cpp:140-213 (Eq. 5, per-rank mask denominators)
-//   (edge kernels in edge_kernels.cuh, tensor-core GEMMs in gemm_kernels.cuh)
-//   k_opt_* ......... S/trainer.cpp:319-327 + RmsOptimizer :37-53
+//                     + the per-atom pair counts of S/core.cpp:30-48
+//   k_scan, k_nbr_fill S/core.cpp:30-48  (bit-exact fp64 pair test, i-major, j ascending)
+//   k_energy/k_loss . S/model.cpp:208-218 + S/loss.cpp:140-213 (Eq. 5, per-rank mask denominators)
+//   k_emb_grad ...... S/model.cpp:421-424
+//   k_grad_reduce ... sum of the per-CTA gradient partials
+//   (edge kernels in edge_kernels.cuh; tensor-core GEMMs and k_opt — S/trainer.cpp:319-327
+//    + RmsOptimizer :37-53 — in gemm_kernels.cuh)
 //
 // Determinism: no floating-point atomics. Parameter gradients are reduced into
 // per-CTA partials in a fixed order and summed across CTAs in index order by
@@ -45,6 +48,18 @@ struct BatchArrays {
     int32_t *Z, *zslot, *z_to_slot, *dsidx;
     uint8_t *emask, *fmask, *denoise;
 };
+
+// ------------------------------------------------------- neighbour list ---
+// Bit-exact with S/core.cpp:40-43: d = p_i - p_j, r = sqrt((dx*dx + dy*dy) + dz*dz)
+// with every operation individually rounded (no FMA contraction), r < cutoff.
+__device__ __forceinline__ double pair_dist(double xi, double yi, double zi, double xj, double yj, double zj,
+                                            double& dx, double& dy, double& dz) {
+    dx = __dsub_rn(xi, xj);
+    dy = __dsub_rn(yi, yj);
+    dz = __dsub_rn(zi, zj);
+    return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+}
+
 
 __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out) {
     pdl_enter();
@@ -121,42 +136,23 @@ __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out) {
             d.x[a] = xyz[0], d.y[a] = xyz[1], d.z[a] = xyz[2];
         }
         __syncthreads();
-    }
-}
-
-// ------------------------------------------------------- neighbour list ---
-// Bit-exact with S/core.cpp:40-43: d = p_i - p_j, r = sqrt((dx*dx + dy*dy) + dz*dz)
-// with every operation individually rounded (no FMA contraction), r < cutoff.
-__device__ __forceinline__ double pair_dist(double xi, double yi, double zi, double xj, double yj, double zj,
-                                            double& dx, double& dy, double& dz) {
-    dx = __dsub_rn(xi, xj);
-    dy = __dsub_rn(yi, yj);
-    dz = __dsub_rn(zi, zj);
-    return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-}
-
-// Warp per destination atom i; lanes sweep the sample's atoms j in order and
-// count with ballot/popc.
-__global__ void __launch_bounds__(256) k_nbr_count(Dev d) {
-    pdl_enter();
-    const int N = d.hdr->N;
-    const int lane = threadIdx.x & 31;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
-        const int s = d.sample_of[i];
-        const int lo = static_cast<int>(d.atom_ptr[s]), hi = static_cast<int>(d.atom_ptr[s + 1]);
-        const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
-        int cnt = 0;
-        for (int j0 = lo; j0 < hi; j0 += 32) {
-            const int j = j0 + lane;
-            bool in = false;
-            if (j < hi && j != i) {
-                double dx, dy, dz;
-                in = pair_dist(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz) < d.rc;
+        // neighbour counts of the sample (S/core.cpp:30-48), warp per atom, from the
+        // positions this block just wrote (plain loads: visible after the barrier)
+        const int lane = threadIdx.x & 31;
+        for (int64_t i = lo + (threadIdx.x >> 5); i < hi; i += blockDim.x >> 5) {
+            const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
+            int cnt = 0;
+            for (int64_t j0 = lo; j0 < hi; j0 += 32) {
+                const int64_t j = j0 + lane;
+                bool in = false;
+                if (j < hi && j != i) {
+                    double dx, dy, dz;
+                    in = pair_dist(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz) < d.rc;
+                }
+                cnt += __popc(__ballot_sync(0xffffffffu, in));
             }
-            cnt += __popc(__ballot_sync(0xffffffffu, in));
+            if (lane == 0) d.cnt[i] = cnt;
         }
-        if (lane == 0) d.cnt[i] = cnt;
     }
 }
 
@@ -228,7 +224,7 @@ __global__ void __launch_bounds__(1024) k_scan(Dev d, int Q) {
     }
 }
 
-// Same sweep as k_nbr_count; lanes that hold a neighbour compact into the CSR
+// Same sweep as the count in k_prep; lanes that hold a neighbour compact into the CSR
 // row with popc(ballot & lanes_below). Edge geometry is computed in fp64 and
 // rounded once: unit (1/r)*d (S/core.cpp:43), fcut (S/model.cpp:17), Gaussians
 // (S/model.cpp:20-27).
@@ -338,16 +334,23 @@ __device__ __forceinline__ void sample_energy(const Dev& d, int s, double* red) 
                     if (dd < D) acc[dd] = fma(static_cast<double>(hv[u]), static_cast<double>(w[dd]), acc[dd]);
         }
     }
+    // fixed-order reduction over the channels: butterfly within each warp, then
+    // the 4 warp sums in order
 #pragma unroll
     for (int dd = 0; dd < kMaxHeads; ++dd)
-        if (dd < D) red[dd * 128 + threadIdx.x] = acc[dd];
+        if (dd < D)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[dd] += __shfl_xor_sync(0xffffffffu, acc[dd], o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0)
+#pragma unroll
+        for (int dd = 0; dd < kMaxHeads; ++dd)
+            if (dd < D) red[dd * 4 + warp] = acc[dd];
     __syncthreads();
-    for (int o = 64; o > 0; o >>= 1) {
-        if (threadIdx.x < o)
-            for (int dd = 0; dd < D; ++dd) red[dd * 128 + threadIdx.x] += red[dd * 128 + threadIdx.x + o];
-        __syncthreads();
+    if (threadIdx.x < D) {
+        const double* r = red + threadIdx.x * 4;
+        d.Epred[static_cast<int64_t>(s) * D + threadIdx.x] = ((r[0] + r[1]) + r[2]) + r[3];
     }
-    if (threadIdx.x < D) d.Epred[static_cast<int64_t>(s) * D + threadIdx.x] = red[threadIdx.x * 128];
     __syncthreads();
 }
 
@@ -365,7 +368,7 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
 // other channel is zeroed). The last block to finish sums the per-sample terms
 // in index order (deterministic), publishes the rank's loss to the header and,
 // as an fp32 hi/lo pair, into the allreduce payload after the gradients.
-__global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy) {
+__global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy, int full_gF) {
     pdl_enter();
     double* ered = dyn_smem<double>();  // [D][128] when with_energy
     __shared__ double red[128], red2[128];
@@ -382,8 +385,9 @@ __global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy) {
         const double ws = wf / static_cast<double>(hi - lo);
         double fsum = 0.0;
         for (int64_t a = lo + threadIdx.x; a < hi; a += 128) {
-            float* g = d.gF + a * 3 * D;
-            for (int q = 0; q < 3 * D; ++q) g[q] = 0.f;
+            float* g = d.gF + a * 3 * D;  // prediction-layout gradient: only for the API (lamm_loss_grad)
+            if (full_gF)
+                for (int q = 0; q < 3 * D; ++q) g[q] = 0.f;
             float4 gc = make_float4(0.f, 0.f, 0.f, 0.f);
             if (fm) {
                 double df[3], sq = 0.0;
@@ -398,17 +402,17 @@ __global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy) {
                     gc.x = static_cast<float>(ws * df[0] / dist);
                     gc.y = static_cast<float>(ws * df[1] / dist);
                     gc.z = static_cast<float>(ws * df[2] / dist);
-                    g[ds * 3] = gc.x, g[ds * 3 + 1] = gc.y, g[ds * 3 + 2] = gc.z;
+                    if (full_gF) g[ds * 3] = gc.x, g[ds * 3 + 1] = gc.y, g[ds * 3 + 2] = gc.z;
                 }
             }
             d.gFc[a] = gc;
         }
-        red[threadIdx.x] = fsum;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, o);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = fsum;
         __syncthreads();
-        for (int o = 64; o > 0; o >>= 1) {
-            if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-            __syncthreads();
-        }
+        if (threadIdx.x == 0) red[0] = ((red[0] + red[1]) + red[2]) + red[3];
+        __syncthreads();
         if (threadIdx.x < D) {
             float ge = 0.f;
             if (threadIdx.x == ds && em) {
