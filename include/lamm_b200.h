@@ -186,6 +186,20 @@ int lamm_loss_grad(lamm_ctx* ctx, const lamm_loss_config* cfg, lamm_loss_breakdo
  * grads_accum is non-NULL the batch gradient is ADDED into it (fp64, flat). */
 int lamm_backward(lamm_ctx* ctx, const double* up_energy, const double* up_forces, double* grads_accum);
 
+/* trainer::EvalResult, H/trainer.hpp:129-134 */
+typedef struct {
+    double energy_mae;    /* meV per atom over energy-labelled samples, NaN if none */
+    double force_mae;     /* meV/Angstrom over force-labelled samples, NaN if none */
+    int64_t energy_count;
+    int64_t force_count;
+} lamm_eval_result;
+
+/* lamm::trainer::evaluate (H/trainer.hpp:143-144, S/trainer.cpp:528-553): the
+ * current parameters on `batch` (raw labels, no denoising), each sample's own
+ * head denormalized with the installed reference table, physical-unit MAEs.
+ * Replaces the context's current batch. */
+int lamm_evaluate(lamm_ctx* ctx, const lamm_batch_view* batch, lamm_eval_result* out);
+
 /* ----------------------------------------------------------- train step --- */
 /* NCCL communicator for data parallelism over `nranks` GPUs (one ctx per GPU,
  * one process per GPU). unique_id is the 128-byte ncclUniqueId from rank 0. */

@@ -18,6 +18,7 @@
 //   lamm::scheduler::plan              H/scheduler.hpp:74     -> plan<Schedule>(atoms, cfg)
 //   lamm::model::init_params           H/model.hpp:75         -> init_params(params&, cfg, seed)
 //   run_loop step body (file-local)    S/trainer.cpp:258-327  -> train_step(dev, samples, denoise, cfg, step, G, rank)
+//   lamm::trainer::evaluate            H/trainer.hpp:143-144  -> evaluate<EvalResult>(dev, cfg, params, refs, samples)
 //
 // Batched variants (forward_batch, build_neighbor_lists) take a span of
 // systems and run them as one device-batch; the per-sample forms are the
@@ -282,6 +283,10 @@ public:
         ++generation_;
     }
     const std::vector<int64_t>& batch_atom_ptr() const { return batch_atom_ptr_; }
+    void batch_replaced(const std::vector<int64_t>& atom_ptr) {  // a call uploaded its own batch
+        batch_atom_ptr_ = atom_ptr;
+        ++generation_;
+    }
     uint64_t generation() const { return generation_; }
 
     void comm_init(int nranks, int rank, const void* unique_id128) {
@@ -502,6 +507,37 @@ StepResult train_step(Device& dev, std::span<const Sample> samples, std::span<co
     dev.params_changed_on_device();
     check(st);
     return StepResult{r.loss, r.grad_norm, r.local, r.n_atoms, r.n_edges};
+}
+
+// ------------------------------------------------------------ evaluation -----
+// lamm::trainer::evaluate (H/trainer.hpp:143-144, S/trainer.cpp:528-553):
+// EvalResult {energy_mae, force_mae, energy_count, force_count} of the device's
+// parameters on `samples` (raw labels), denormalized with its reference table.
+template <class EvalResult, class Sample>
+EvalResult evaluate(Device& dev, std::span<const Sample> samples) {
+    PackedBatch b;
+    for (const auto& s : samples) b.add_sample(s);
+    const lamm_batch_view v = b.view();
+    lamm_eval_result r{};
+    check(lamm_evaluate(dev.get(), &v, &r));
+    dev.batch_replaced(b.atom_ptr);
+    EvalResult out{};
+    out.energy_mae = r.energy_mae;
+    out.force_mae = r.force_mae;
+    out.energy_count = r.energy_count;
+    out.force_count = r.force_count;
+    return out;
+}
+
+// The reference signature: parameters and table installed first.
+template <class EvalResult, class ModelConfig, class Params, class ReferenceTable, class Sample>
+EvalResult evaluate(Device& dev, const ModelConfig& cfg, const Params& params, const ReferenceTable& refs,
+                    std::span<const Sample> samples) {
+    const lamm_model_config c = to_c(cfg);
+    if (std::memcmp(&c, &dev.config(), sizeof c) != 0) throw InputError("evaluate: model config differs from the device's");
+    dev.set_params_from(params);
+    dev.set_reference_table(refs);
+    return evaluate<EvalResult>(dev, samples);
 }
 
 // ------------------------------------------------------------- scheduler -----

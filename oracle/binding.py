@@ -133,6 +133,21 @@ class OracleLib:
                                        _p(Z), _p(e), _p(f)))
         return e, f
 
+    def evaluate(self, cfg, params, batch, table):
+        """trainer::evaluate (S/trainer.cpp:528-553): physical-unit MAEs (meV)."""
+        if self.kind != "ref":
+            raise NotImplementedError("evaluate is checked against the compiled reference only")
+        H, L, K, rc, D = cfg
+        ap = _c(batch["atom_ptr"], np.int64)
+        B = len(ap) - 1
+        out = np.empty(4, np.float64)
+        keep = [_c(batch[k], dt) for k, dt in (("pos", np.float64), ("Z", np.int32), ("dataset_index", np.int32),
+                                               ("energy_mask", np.uint8), ("force_mask", np.uint8),
+                                               ("energy", np.float64), ("forces", np.float64))]
+        self._check(self._f("evaluate")(H, L, K, _f64(rc), D, _p(_c(params, np.float64)), _i32(B), _p(ap),
+                                        *[_p(k) for k in keep], *self._table_args(table), _p(out)))
+        return dict(energy_mae=out[0], force_mae=out[1], energy_count=int(out[2]), force_count=int(out[3]))
+
     def forward_cache(self, cfg, params, pos, Z):
         H, L, K, rc, D = cfg
         pos, Z = _c(pos, np.float64), _c(Z, np.int32)

@@ -35,6 +35,7 @@
 #include "lamm/rng.hpp"
 #include "lamm/scheduler.hpp"
 #include "lamm/trace.hpp"
+#include "lamm/trainer.hpp"
 
 #define LREF_API extern "C" __attribute__((visibility("default")))
 
@@ -239,6 +240,29 @@ LREF_API int lref_backward(int H, int L, int K, double rc, int D, const double* 
             lamm::model::backward(cache, p, cfg, up, g);
         }
         params_to_flat(g, grads_accum);
+    });
+}
+
+// ---- evaluation (S/trainer.cpp:491-553) -------------------------------------
+/// trainer::evaluate on a packed batch with raw labels; out = {energy_mae,
+/// force_mae, energy_count, force_count} (MAEs in meV, NaN without labels).
+LREF_API int lref_evaluate(int H, int L, int K, double rc, int D, const double* params, int32_t B,
+                           const int64_t* atom_ptr, const double* pos, const int32_t* Z, const int32_t* dsidx,
+                           const uint8_t* emask, const uint8_t* fmask, const double* energy, const double* forces,
+                           int ntab, const double* rho, const uint8_t* rho_has, const double* mean,
+                           const double* stdv, const double* fstd, const uint8_t* has, double* out) {
+    return guarded([&] {
+        const auto cfg = make_cfg(H, L, K, rc, D);
+        const auto p = params_from_flat(cfg, params);
+        const auto t = table_from(ntab, rho, rho_has, mean, stdv, fstd, has);
+        std::vector<lamm::Sample> samples;
+        for (int s = 0; s < B; ++s)
+            samples.push_back(sample_at(atom_ptr, pos, Z, dsidx, emask, fmask, energy, forces, s));
+        const auto r = lamm::trainer::evaluate(cfg, p, t, samples);
+        out[0] = r.energy_mae;
+        out[1] = r.force_mae;
+        out[2] = static_cast<double>(r.energy_count);
+        out[3] = static_cast<double>(r.force_count);
     });
 }
 

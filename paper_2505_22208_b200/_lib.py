@@ -65,6 +65,11 @@ class StepResultC(C.Structure):
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
 
 
+class EvalResultC(C.Structure):
+    _fields_ = [("energy_mae", C.c_double), ("force_mae", C.c_double), ("energy_count", C.c_int64),
+                ("force_count", C.c_int64)]
+
+
 # Every symbol include/lamm_b200.h declares (tests check the export table).
 EXPORTS = [
     "lamm_last_error", "lamm_ctx_create", "lamm_ctx_destroy", "lamm_ctx_set_option", "lamm_param_count",
@@ -76,7 +81,7 @@ EXPORTS = [
     "lamm_last_step_launches", "lamm_greedy_assign", "lamm_plan", "lamm_schedule_metrics", "lamm_make_trace",
     "lamm_temperature_counts", "lamm_build_epoch_index", "lamm_synth_counts", "lamm_synth_fill",
     "lamm_mix_seed", "lamm_rng_normals", "lamm_stage", "lamm_train_step_staged", "lamm_anomalies",
-    "lamm_flush_l2", "lamm_step_times",
+    "lamm_flush_l2", "lamm_step_times", "lamm_evaluate",
 ]
 
 _lib = None

@@ -26,7 +26,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import (BatchViewC, InputError, LossBreakdownC, LossConfigC, ModelConfigC, NonFiniteError,  # noqa: F401
+from ._lib import (BatchViewC, EvalResultC, InputError, LossBreakdownC, LossConfigC, ModelConfigC, NonFiniteError,  # noqa: F401
                    RefTableC, StepResultC, TrainConfigC, check, lib)
 
 
@@ -201,6 +201,18 @@ class Device:
         self._batch, self._keep = batch, keep
         self.B = len(keep["atom_ptr"]) - 1
         self.N = int(keep["atom_ptr"][-1])
+
+    def evaluate(self, batch: dict) -> dict:
+        """trainer::evaluate (S/trainer.cpp:528-553): MAEs in meV of the current
+        parameters on `batch` (raw labels; replaces the current batch)."""
+        v, keep = _batch_view(batch)
+        r = EvalResultC()
+        check(lib().lamm_evaluate(self._h, C.byref(v), C.byref(r)))
+        self._batch, self._keep = batch, keep
+        self.B = len(keep["atom_ptr"]) - 1
+        self.N = int(keep["atom_ptr"][-1])
+        return dict(energy_mae=r.energy_mae, force_mae=r.force_mae, energy_count=r.energy_count,
+                    force_count=r.force_count)
 
     def labels(self):
         e, f = np.empty(self.B), np.empty((self.N, 3))

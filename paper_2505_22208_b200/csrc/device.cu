@@ -1106,6 +1106,33 @@ LAMM_API int lamm_forward(lamm_ctx* c, double* energy, double* forces) {
     });
 }
 
+LAMM_API int lamm_evaluate(lamm_ctx* c, const lamm_batch_view* b, lamm_eval_result* out) {
+    return lamm_guard([&] {
+        require(c && b && out, "evaluate: null argument");
+        CK(cudaSetDevice(c->device));
+        lamm_batch_view v = *b;
+        v.denoise = nullptr;  // evaluate() takes the samples as given
+        validate_batch(*c, &v);
+        const size_t bytes = pack_batch(*c, &v, false, nullptr, 0, 0);
+        ensure_capacity(*c, c->N, c->B, edge_guess(c->N));
+        CK(cudaMemcpyAsync(c->d_stage.p, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream));
+        c->slot_cursor = 0;
+        c->ops->prep(*c);
+        read_header(*c);
+        c->batch_valid = true;
+        c->nlist_valid = c->fwd_valid = c->loss_valid = false;
+        ensure_forward(*c);
+        launch(*c, "eval", k_eval, c->grid_small, 128, 0, make_dev(*c));
+        const StepHeader h = read_header(*c);
+        int64_t ne = 0, nf = 0;
+        for (int32_t s = 0; s < c->B; ++s) ne += c->h_emask[s] ? 1 : 0, nf += c->h_fmask[s] ? 1 : 0;
+        out->energy_count = ne;
+        out->force_count = nf;
+        out->energy_mae = ne > 0 ? 1000.0 * h.loss_energy / static_cast<double>(ne) : std::nan("");
+        out->force_mae = nf > 0 ? 1000.0 * h.loss_force / static_cast<double>(nf) : std::nan("");
+    });
+}
+
 LAMM_API int lamm_forward_cache_get(lamm_ctx* c, int which, int layer, double* out) {
     return lamm_guard([&] {
         require(c && out, "forward_cache_get: null argument");

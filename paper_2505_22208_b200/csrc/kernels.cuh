@@ -458,6 +458,80 @@ __global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy, int full_g
     }
 }
 
+// ------------------------------------------------------------ evaluation ---
+// trainer::evaluate (S/trainer.cpp:491-553) on the forward predictions: the
+// sample's own head denormalized (S/loss.cpp:128-136), |E - E_label| / n and
+// sum |F - F_label| / 3n per sample from the raw labels of the staged blob; the
+// last block sums the per-sample terms in index order into the header
+// (loss_energy, loss_force).
+__global__ void __launch_bounds__(128) k_eval(Dev d) {
+    pdl_enter();
+    __shared__ double red[4];
+    __shared__ bool last;
+    const StepHeader& hd = *d.hdr;
+    const char* base = reinterpret_cast<const char*>(d.hdr);
+    const double* E = reinterpret_cast<const double*>(base + hd.off_E);
+    const double* F = reinterpret_cast<const double*>(base + hd.off_F);
+    const int B = hd.B, D = d.D;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int s = blockIdx.x; s < B; s += gridDim.x) {
+        const int64_t lo = d.atom_ptr[s], hi = d.atom_ptr[s + 1];
+        const double n = static_cast<double>(hi - lo);
+        const int ds = d.dsidx[s];
+        const bool em = d.emask[s], fm = d.fmask[s];
+        if (threadIdx.x == 0) {
+            double et = 0.0;
+            if (em) {
+                double e = d.Epred[static_cast<int64_t>(s) * D + ds];
+                if (d.use_table) {
+                    double refsum = 0.0;  // reference_sum, atoms in order
+                    for (int64_t a = lo; a < hi; ++a)
+                        if (d.rho_has[ds * 119 + d.Z[a]]) refsum = __dadd_rn(refsum, d.rho[ds * 119 + d.Z[a]]);
+                    e = e * d.tstd[ds] + d.tmean[ds] + refsum;
+                }
+                et = fabs(e - E[s]) / n;
+            }
+            d.sample_terms[2 * s] = et;
+        }
+        double fsum = 0.0;
+        if (fm) {
+            const double fs = d.use_table ? d.tfstd[ds] : 1.0;
+            for (int64_t a = lo + threadIdx.x; a < hi; a += blockDim.x)
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    fsum += fabs(static_cast<double>(d.F[(a * D + ds) * 3 + c]) * fs - F[3 * a + c]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) fsum += __shfl_xor_sync(0xffffffffu, fsum, o);
+        if (lane == 0) red[warp] = fsum;
+        __syncthreads();
+        if (threadIdx.x == 0) d.sample_terms[2 * s + 1] = fm ? (((red[0] + red[1]) + red[2]) + red[3]) / (3.0 * n) : 0.0;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(&d.hdr->done_counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double e = 0.0, f = 0.0;
+    for (int s = threadIdx.x; s < B; s += blockDim.x) e += d.sample_terms[2 * s], f += d.sample_terms[2 * s + 1];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+        f += __shfl_xor_sync(0xffffffffu, f, o);
+    }
+    __shared__ double re[4], rf[4];
+    if (lane == 0) re[warp] = e, rf[warp] = f;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        d.hdr->loss_energy = ((re[0] + re[1]) + re[2]) + re[3];
+        d.hdr->loss_force = ((rf[0] + rf[1]) + rf[2]) + rf[3];
+        d.hdr->done_counter = 0;
+    }
+}
+
 // ------------------------------------------------------ embedding grad ---
 // dE[Z_i - 1] += gh_i over the atoms after the layer-0 backward
 // (S/model.cpp:421-424): CTA c sums a contiguous atom range per distinct-Z slot

@@ -27,6 +27,7 @@
 #include "lamm/model.hpp"
 #include "lamm/rng.hpp"
 #include "lamm/scheduler.hpp"
+#include "lamm/trainer.hpp"
 #include "lamm_b200.hpp"
 
 namespace {
@@ -276,6 +277,18 @@ void check_train_step(const std::vector<lamm::Sample>& samples, const lamm::mode
     report(rel(dev.rms_state(), v) <= 3 * kTol, "train_step RMS state", fmt(rel(dev.rms_state(), v)));
 }
 
+void check_evaluate(const std::vector<lamm::Sample>& samples, const lamm::model::ModelConfig& cfg,
+                    const lamm::model::ModelParams& params, const lamm::loss::ReferenceTable& table) {
+    const auto ref = lamm::trainer::evaluate(cfg, params, table, samples);
+    lamm_b200::Device dev(cfg, 0);
+    const auto got = lamm_b200::evaluate<lamm::trainer::EvalResult>(dev, cfg, params, table,
+                                                                    std::span<const lamm::Sample>(samples));
+    const double re = std::abs(got.energy_mae - ref.energy_mae) / std::abs(ref.energy_mae);
+    const double rf = std::abs(got.force_mae - ref.force_mae) / std::abs(ref.force_mae);
+    report(re <= kTol && rf <= kTol && got.energy_count == ref.energy_count && got.force_count == ref.force_count,
+           "trainer::evaluate MAEs and counts", fmt(std::max(re, rf)));
+}
+
 }  // namespace
 
 int main() {
@@ -292,6 +305,7 @@ int main() {
         check_model(dev, samples, cfg, params, table);
         check_scheduler();
         check_train_step(samples, cfg, params, table);
+        check_evaluate(samples, cfg, params, table);
         bool threw = false;
         try {
             lamm::model::ModelConfig bad = cfg;

@@ -256,3 +256,44 @@ def test_multi_worker_sum_semantics(pk, oracle_ref):
     assert abs(loss / G - ref["loss"]) <= TOL * abs(ref["loss"])
     assert_close(gsum / G, ref["grads"], what="G-worker mean gradient")
     assert rel_err(gsum / G, ref["grads"])[0] < TOL
+
+
+def test_nccl_allreduce_path_single_rank(pk):
+    """The data-parallel path (NCCL communicator, allreduce between the two graph
+    halves) on one rank: identical to the communicator-free step, bit for bit."""
+    mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
+    batch = cases.mixed_batch(pk, D=cases.CFG[4], seed=17, count=16)
+    table = cases.random_table(cases.CFG[4], seed=6)
+    outs = []
+    for use_comm in (False, True):
+        dev = pk.Device(mcfg, seed=5)
+        dev.set_reference_table(table)
+        if use_comm:
+            dev.comm_init(1, 0, pk.comm_unique_id())
+        res = [dev.train_step(batch, _train_cfg(pk), step=s) for s in range(2)]
+        dev.stage(batch, _train_cfg(pk), step=2, slot=0)
+        res.append(dev.train_step_staged(0, sync=True))
+        outs.append((dev.params(), dev.grads(), [r.loss for r in res]))
+        dev.close()
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
+
+
+def test_evaluate_matches_reference(pk, oracle_ref):
+    """trainer::evaluate (S/trainer.cpp:528-553): physical-unit MAEs of the
+    current parameters, each sample's own head denormalized with the table."""
+    mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
+    params = oracle_ref.init_params(cases.CFG, 13)
+    batch = cases.mixed_batch(pk, D=cases.CFG[4], seed=21, count=40)
+    batch["denoise"][:] = 0
+    table = cases.random_table(cases.CFG[4], seed=9)
+    dev = pk.Device(mcfg, seed=0)
+    dev.set_params(params)
+    dev.set_reference_table(table)
+    got = dev.evaluate(batch)
+    want = oracle_ref.evaluate(cases.CFG, params, batch, table)
+    dev.close()
+    assert got["energy_count"] == want["energy_count"] and got["force_count"] == want["force_count"]
+    for k in ("energy_mae", "force_mae"):
+        assert abs(got[k] - want[k]) <= TOL * abs(want[k]), (k, got[k], want[k])
