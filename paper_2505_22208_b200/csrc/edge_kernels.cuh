@@ -227,16 +227,31 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
                 umma::commit(&c.mbar[0]);
             }
         }
+        // gathers of the next block are issued before the current block is
+        // consumed, across chunk boundaries (the next chunk's stage is waited for
+        // at the start of the current chunk)
+        typename Body::Reg rn[8];
+        auto load_block = [&](const EdgeStage<K>& sst, int blk) {
+            const int4 j0 = reinterpret_cast<const int4*>(sst.col)[2 * blk];
+            const int4 j1 = reinterpret_cast<const int4*>(sst.col)[2 * blk + 1];
+            const int jj[8] = {j0.x, j0.y, j0.z, j0.w, j1.x, j1.y, j1.z, j1.w};
+#pragma unroll
+            for (int u = 0; u < 8; ++u) body.load(sst, blk * 8 + u, jj[u], rn[u]);
+        };
+        mbar_wait(&c.bar[0], 0);
+        load_block(c.st[0], (e0 - base) >> 3);
         for (int k = 0; k < nchunks; ++k) {
             const int s = k & 1;
-            if constexpr (kF) {
-                if (lead && k + 1 < nchunks) {  // next chunk's filter overlaps this chunk's drain
-                    mbar_wait(&c.bar[s ^ 1], ((k + 1) >> 1) & 1);
-                    filter_mma<K>(ft.tg + (s ^ 1) * kChunk, ft, c.st[s ^ 1]);
-                    umma::commit(&c.mbar[s ^ 1]);
+            const bool more = k + 1 < nchunks;
+            if (more) {
+                mbar_wait(&c.bar[s ^ 1], ((k + 1) >> 1) & 1);
+                if constexpr (kF) {
+                    if (lead) {  // next chunk's filter overlaps this chunk's drain
+                        filter_mma<K>(ft.tg + (s ^ 1) * kChunk, ft, c.st[s ^ 1]);
+                        umma::commit(&c.mbar[s ^ 1]);
+                    }
                 }
             }
-            mbar_wait(&c.bar[s], (k >> 1) & 1);
             if constexpr (kF) {
                 mbar_wait(&c.mbar[s], (k >> 1) & 1);
                 umma::fence_after();
@@ -245,27 +260,13 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
             const int cb = base + k * kChunk;
             const int ea = max(cb, e0) - cb, eb = min(cb + kChunk, e1) - cb;
             const uint32_t trow = ft.tg + s * kChunk + (quad * 32u << 16);
-            // gathers of block b+1 are issued before block b is consumed
-            typename Body::Reg rn[8];
             const int blk0 = ea >> 3, blk1 = (eb + 7) >> 3;
-            {
-                const int4 j0 = reinterpret_cast<const int4*>(st.col)[2 * blk0];
-                const int4 j1 = reinterpret_cast<const int4*>(st.col)[2 * blk0 + 1];
-                const int jj[8] = {j0.x, j0.y, j0.z, j0.w, j1.x, j1.y, j1.z, j1.w};
-#pragma unroll
-                for (int u = 0; u < 8; ++u) body.load(st, blk0 * 8 + u, jj[u], rn[u]);
-            }
             for (int blk = blk0; blk < blk1; ++blk) {
                 typename Body::Reg r[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) r[u] = rn[u];
-                if (blk + 1 < blk1) {
-                    const int4 j0 = reinterpret_cast<const int4*>(st.col)[2 * blk + 2];
-                    const int4 j1 = reinterpret_cast<const int4*>(st.col)[2 * blk + 3];
-                    const int jj[8] = {j0.x, j0.y, j0.z, j0.w, j1.x, j1.y, j1.z, j1.w};
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) body.load(st, (blk + 1) * 8 + u, jj[u], rn[u]);
-                }
+                if (blk + 1 < blk1) load_block(st, blk + 1);
+                else if (more) load_block(c.st[s ^ 1], 0);  // first block of the next chunk
                 const int ulo = max(ea - blk * 8, 0), uhi = min(eb - blk * 8, 8);
                 if constexpr (Body::kPrepare) body.prepare(st, blk * 8);
                 float f[8];
