@@ -156,6 +156,18 @@ def kernel_bytes(name, N, P, H=128, K=16, D=10):
     return e.get(name)
 
 
+def ncu_traffic(name, algorithmic_bytes):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the
+    kernel from the committed ncu --set full capture (profiles/r01_ncu_traffic.json),
+    scaled from the captured step to this workload by the algorithmic bytes."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            k = json.load(f)["kernels"][name]
+        return k["ratio"] * algorithmic_bytes
+    except Exception:
+        return None
+
+
 def kernel_flops(name, N, P, H=128, K=16, D=10):
     return {"update": 2 * N * H * H, "bwd_gemm": 4 * N * H * H, "message": P * (2 * H * K + 3 * H),
             "bwd_edge": P * (4 * H * K + 6 * H)}.get(name)
@@ -253,13 +265,15 @@ def run_ours(args, dist):
     launches_per_step = tcount / steps_done
     byts = kernel_bytes(tname, N_mean, P_mean)
     roof = {"kernel": tname, "bound": "hbm", "unit": "GB/s", "peak": hbm, "peak_source": src,
+            "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, DRAM bytes / algorithmic bytes of the "
+                              "captured step, times this workload's algorithmic bytes)",
             "share_of_step": tms / tot_ms if tot_ms else None, "avg_launch_us": per_launch_ms * 1e3,
             "launches_per_step": launches_per_step,
             "timing": "CUDA event pair around each launch on the ctx stream, second pass over the same K steps "
                       "(profiled step %.3f ms vs %.3f ms unprofiled)" % (prof_ms / K, dev_ms / K)}
     if byts is not None:
         ach = byts / (per_launch_ms / 1e3) / 1e9
-        roof.update(achieved=ach, frac=ach / hbm, traffic=None, algorithmic_bytes_per_launch=byts)
+        roof.update(achieved=ach, frac=ach / hbm, traffic=ncu_traffic(tname, byts), algorithmic_bytes_per_launch=byts)
     fl = kernel_flops(tname, N_mean, P_mean)
     if fl is not None:
         roof["fp32_flops_per_launch"] = fl
