@@ -297,3 +297,53 @@ def test_evaluate_matches_reference(pk, oracle_ref):
     assert got["energy_count"] == want["energy_count"] and got["force_count"] == want["force_count"]
     for k in ("energy_mae", "force_mae"):
         assert abs(got[k] - want[k]) <= TOL * abs(want[k]), (k, got[k], want[k])
+
+
+def test_train_step_large_structures(pk, oracle_ref):
+    """cfg4-like: two 500-700 atom clusters (dense lists, ~30+ edges per atom,
+    partitions cutting through one atom's row run) through the full step."""
+    mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
+    batch = cases.synth(pk, 2, 77, mode=600, sigma=0.1, min_atoms=500, max_atoms=700, elements=cases.ORGANIC)
+    batch = cases.with_heads(batch, cases.CFG[4], seed=3)
+    table = cases.random_table(cases.CFG[4], seed=12)
+    params = oracle_ref.init_params(cases.CFG, 31)
+    tc = _train_cfg(pk, clip_norm=1e9)
+    ref = oracle_ref.train_step(cases.CFG, 1, 2, batch, table, params, np.zeros_like(params), seed=tc.seed, step=0,
+                                clip=tc.clip_norm)
+    dev = pk.Device(mcfg, seed=0)
+    dev.set_params(params)
+    dev.set_rms_state(np.zeros_like(params))
+    dev.set_reference_table(table)
+    res = dev.train_step(batch, tc, step=0)
+    assert res.n_edges > 25 * res.n_atoms
+    assert abs(res.loss - ref["loss"]) <= TOL * abs(ref["loss"])
+    g = dev.grads()
+    for name, t in tensors(cases.CFG, g).items():
+        assert_close(t, tensors(cases.CFG, ref["grads"])[name], what=f"large d/d{name}")
+    dev.close()
+
+
+def test_staged_steps_match_host_steps(pk):
+    """Device-resident staged slots of different sizes replayed through one
+    captured graph give the same trajectory as host-batch steps."""
+    mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
+    batches = [cases.mixed_batch(pk, D=cases.CFG[4], seed=40 + k, count=n) for k, n in enumerate((24, 8, 40))]
+    table = cases.random_table(cases.CFG[4], seed=5)
+    tc = _train_cfg(pk)
+    outs = []
+    for staged in (False, True):
+        dev = pk.Device(mcfg, seed=8)
+        dev.set_reference_table(table)
+        if staged:
+            for k, b in enumerate(batches):
+                dev.stage(b, tc, step=k, slot=k)
+        losses = []
+        for rep in range(2):
+            for k, b in enumerate(batches):
+                step = k  # the staged slot carries its step's denoise draws
+                r = dev.train_step_staged(k, sync=True) if staged else dev.train_step(b, tc, step=step)
+                losses.append(r.loss)
+        outs.append((dev.params(), losses))
+        dev.close()
+    assert outs[0][1] == outs[1][1]
+    assert np.array_equal(outs[0][0], outs[1][0])
