@@ -301,6 +301,7 @@ def run_ours(args, dist):
         out["cpu_baseline"] = cpu_baseline(shards[0], table, mcfg, budget_s=args.cpu_budget)
     if dist.rank == 0 and dist.world == 1 and not args.no_imbalance:
         out["rank_imbalance"] = rank_imbalance(pk, dev, pool, table, tc)
+        out["rank_imbalance_heavy_tail"] = rank_imbalance_heavy(pk, dev, tc)
     dev.close()
     return out
 
@@ -361,6 +362,56 @@ def rank_imbalance(pk, dev, pool, table, tc, G=8, steps=8):
         out[mode] = {"time_mean": float(np.mean(ratios)), "time_p95": float(np.percentile(ratios, 95)),
                      "atoms_mean": float(np.mean(aratios)), "atoms_max": float(np.max(aratios)),
                      "steps": len(ratios)}
+    return out
+
+
+def rank_imbalance_heavy(pk, dev, tc, G=8, B=4, S=64, steps=8):
+    """cfg5-like load-balancer stress: heavy-tailed sizes (lognormal mode 20,
+    sigma 1.0, 2-2000 atoms) scheduled for G ranks x B samples, the per-rank
+    device steps timed on this GPU; plus the schedule-only atom imbalance of a
+    1M-sample trace at G = 2/4/8 (B = 4, S = 10,000)."""
+    out = {"pool": "synthetic clusters, lognormal(mode 20, sigma 1.0), 2-2000 atoms", "G": G, "batch_per_rank": B}
+    n_pool = G * B * S
+    pool = pk.synth_generate(n_pool, 5, threads=os.cpu_count() or 8, mode=20.0, sigma=1.0, min_atoms=2,
+                             max_atoms=2000, elements=(1, 6, 7, 8))
+    atoms = np.diff(pool["atom_ptr"])
+    out["pool_atoms_mean"], out["pool_atoms_max"] = float(atoms.mean()), int(atoms.max())
+    table = fit_table(pool, CFG["heads"])
+    dev.set_reference_table(table)
+    for mode in ("balanced", "naive"):
+        sched = pk.plan(atoms, G, B, 4, seed=7, mode=mode)
+        per = G * B
+        ratios, aratios = [], []
+        for s in range(min(steps, sched["n_batches"])):
+            ids = sched["sample"][s * per:(s + 1) * per]
+            times = []
+            for g in range(G):
+                sub = pk.select(pool, ids[g * B:(g + 1) * B])
+                dev.stage(sub, tc, step=s, slot=950 + g, workers=G, rank=g)
+                dev.train_step_staged(950 + g, sync=True)
+                ms = []
+                for rep in range(3):
+                    dev.event_record(0)
+                    dev.train_step_staged(950 + g, sync=False)
+                    dev.event_record(1)
+                    ms.append(dev.event_elapsed_ms(0, 1))
+                times.append(min(ms))
+            ratios.append(max(times) / np.mean(times))
+            wa = sched["worker_atoms"][s * G:(s + 1) * G]
+            aratios.append(wa.max() / wa.mean())
+        out[mode] = {"time_mean": float(np.mean(ratios)), "time_p95": float(np.percentile(ratios, 95)),
+                     "atoms_mean": float(np.mean(aratios)), "atoms_max": float(np.max(aratios)),
+                     "steps": len(ratios)}
+    trace = pk.make_trace("lognormal", count=1_000_000, min_atoms=2, max_atoms=2000, mode=20.0, sigma=1.0, seed=3)
+    sched_1m = {}
+    for g in (2, 4, 8):
+        row = {}
+        for mode in ("balanced", "naive"):
+            sc = pk.plan(trace, g, 4, 10_000, seed=3, mode=mode)
+            row[mode] = {"mean_imbalance": sc["mean_imbalance"], "max_imbalance": sc["max_imbalance"],
+                         "steps": sc["n_batches"], "dropped": sc["dropped"]}
+        sched_1m[f"G{g}"] = row
+    out["schedule_1M_trace_atoms"] = sched_1m
     return out
 
 
