@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -337,8 +338,16 @@ BatchArrays make_batch_arrays(Ctx& c) {
 }
 
 // ------------------------------------------------------------- launches ---
+// Timing experiments only: LAMM_SKIP_KERNEL=<name> leaves that kernel out of the
+// step (results are then wrong; used to measure a kernel's marginal cost).
+inline bool skipped(const char* name) {
+    const char* s = std::getenv("LAMM_SKIP_KERNEL");
+    return s != nullptr && std::strcmp(s, name) == 0;
+}
+
 template <class Kern, class... Args>
 void launch(Ctx& c, const char* name, Kern kernel, int grid, int block, size_t smem, Args... args) {
+    if (skipped(name)) return;
     KernelSlot* slot = nullptr;
     if (c.profile) {
         if (c.slot_cursor >= c.slots.size()) {
@@ -374,6 +383,7 @@ void launch(Ctx& c, const char* name, Kern kernel, int grid, int block, size_t s
 // capturable into the step graph like a plain launch.
 template <class... KArgs, class... Args>
 void launch_coop(Ctx& c, const char* name, void (*kernel)(KArgs...), int grid, int block, Args... args) {
+    if (skipped(name)) return;
     KernelSlot* slot = nullptr;
     if (c.profile) {
         if (c.slot_cursor >= c.slots.size()) {
