@@ -69,17 +69,31 @@ __global__ void __launch_bounds__(256) k_pack_weights(Dev d) {
 }
 
 // The optimizer tail of the step as ONE cooperative kernel (grid <= 256 CTAs of
-// 256 threads, all co-resident): norm -> barrier -> clip + RMS update ->
-// barrier -> tensor-core weight packing of the updated parameters.
+// 256 threads, all co-resident): norm -> barrier -> clip + RMS update, each
+// updated W_u element scattered straight into both tensor-core weight packs
+// (its W_u and W_u^T positions), so no second grid barrier is needed.
 template <int H>
 __global__ void __launch_bounds__(256) k_opt(Dev d, int G, double inv_g, double clip, double lr, double decay,
                                              double eps) {
     pdl_enter();
+    constexpr int NC = NodeGemmCfg<H>::NC;
+    const int64_t per = static_cast<int64_t>(H) * H;
+    const int64_t wu0 = static_cast<int64_t>(kMaxZ) * H + static_cast<int64_t>(d.L) * H * d.K;  // W_u[0] offset
     unsigned int* bar = d.anomaly + 16;
-    const int status = opt_update(d, G, inv_g, clip, lr, decay, eps, bar);
-    if (status != 0) return;  // uniform across the grid: parameters unchanged, packing still valid
-    grid_barrier(bar, bar + 32);
-    pack_weights<H>(d);
+    opt_update(d, G, inv_g, clip, lr, decay, eps, bar, [&](int64_t e, float w) {
+        const int64_t r = e - wu0;
+        if (r < 0 || r >= d.L * per) return;
+        const int l = static_cast<int>(r / per), idx = static_cast<int>(r % per);
+        const int n = idx / H, k = idx % H;  // W_u[n][k]: output n, input k
+        float* upd = d.wpack + 4 * per * l;
+        float* gm = upd + 2 * per;
+        // update operand B[n][k] = W_u[n][k]; backward operand B'[k][n] = W_u[n][k]
+        float* ub = upd + static_cast<int64_t>(n / NC) * 2 * NC * H;
+        float* gb = gm + static_cast<int64_t>(k / NC) * 2 * NC * H;
+        const int ou = umma::kidx(n % NC, k, H), og = umma::kidx(k % NC, n, H);
+        umma::split_tf32(w, ub[ou], ub[NC * H + ou]);
+        umma::split_tf32(w, gb[og], gb[NC * H + og]);
+    });
 }
 
 // One tile = 128 atoms x NC output columns, K = H, 256 threads: the whole

@@ -650,8 +650,9 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* 
 // (S/trainer.cpp:37-53, 319-326); refreshes the fp32 working copy and tanh(E)
 // for layer 0's gathers. Every CTA reduces the per-CTA norms itself, so no
 // second barrier is needed before the update. Returns the step status.
+template <class OnParam>
 __device__ __forceinline__ int opt_update(const Dev& d, int G, double inv_g, double clip, double lr, double decay,
-                                          double eps, unsigned int* bar) {
+                                          double eps, unsigned int* bar, OnParam on_param) {
     __shared__ double red[256];
     double s = 0.0;
     for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < d.NP;
@@ -700,6 +701,7 @@ __device__ __forceinline__ int opt_update(const Dev& d, int G, double inv_g, dou
         const float pf = static_cast<float>(p);
         d.p32[e] = pf;
         if (e < emb_n) d.tanh_emb_w[e] = tanhf(pf);
+        on_param(e, pf);
     }
     return status;
 }
