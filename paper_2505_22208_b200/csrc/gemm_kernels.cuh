@@ -147,28 +147,30 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int at = tile / NS, np = tile % NS, base = at * kGemmM;
         if (np != loaded_np) fetch_weights(np);
-        // stage the full activation tile (hi/lo), all loads first
+        // stage the full activation tile (hi/lo), all loads first. Thread -> 16-byte
+        // chunk c of the canonical tile in storage order (c = ((m/8)*(H/4) + k4)*8 + m%8),
+        // so each warp's shared stores are one contiguous 512 B run (no bank conflicts);
+        // the global loads are then 8 rows x 64 B per warp.
         {
             constexpr int Q = H / 4, IT = kGemmM * Q / 256;
             float4 v[IT];
 #pragma unroll
             for (int it = 0; it < IT; ++it) {
-                const int q = tid + 256 * it, m = q / Q, k4 = q % Q, atom = base + m;
+                const int c = tid + 256 * it, m = (c / (8 * Q)) * 8 + (c & 7), k4 = (c >> 3) % Q, atom = base + m;
                 v[it] = atom < N
                             ? __ldg(reinterpret_cast<const float4*>(src + static_cast<int64_t>(atom) * H + 4 * k4))
                             : make_float4(0.f, 0.f, 0.f, 0.f);
             }
 #pragma unroll
             for (int it = 0; it < IT; ++it) {
-                const int q = tid + 256 * it, m = q / Q, k4 = q % Q;
+                const int c = tid + 256 * it;
                 float4 hi, lo;
                 umma::split_tf32(v[it].x, hi.x, lo.x);
                 umma::split_tf32(v[it].y, hi.y, lo.y);
                 umma::split_tf32(v[it].z, hi.z, lo.z);
                 umma::split_tf32(v[it].w, hi.w, lo.w);
-                const int o = umma::kidx(m, 4 * k4, H);
-                *reinterpret_cast<float4*>(Ahi + o) = hi;
-                *reinterpret_cast<float4*>(Alo + o) = lo;
+                *reinterpret_cast<float4*>(Ahi + 4 * c) = hi;
+                *reinterpret_cast<float4*>(Alo + 4 * c) = lo;
             }
         }
         umma::fence_proxy_async();
