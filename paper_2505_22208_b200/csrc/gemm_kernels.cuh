@@ -245,36 +245,38 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
 }
 
 // Backward of the update GEMM fused with its weight gradient (H = 128):
-//   gm = (gh W_u) (.) (1 - mu^2)        MMA1: A = the gh tile from TMEM (lane = atom),
-//                                       B = W_u block (K-major, TMA)   (S/model.cpp:380-390)
-//   dW_u[:, cols] += gh^T mu[:, cols]   MMA2: A = the same gh tile from shared memory
-//                                       as an MN-major operand (M = rows of W_u, K =
-//                                       atoms), B = the mu rows the epilogue loads
-//                                       anyway, MN-major in the weights' place once
-//                                       MMA1 is done                     (S/model.cpp:381-383)
-// The dW_u accumulator stays in TMEM across the CTA's tiles; one [H][NC] partial
-// per CTA (its column block never changes: gridDim.x % NS == 0), summed by
-// k_grad_reduce. TMEM: [0, NC) gm accumulator, [NC, 2 NC) dW_u, [256, 384) gh hi,
-// [384, 512) gh lo.
+//   gm = (gh W_u) (.) (1 - mu^2)        MMA1: A = the gh tile (shared, K-major canonical),
+//                                       B = W_u block (K-major, TMA)       (S/model.cpp:380-390)
+//   dW_u[:, cols] += gh^T mu[:, cols]   MMA2: A = gh^T from TMEM (lane = row b of W_u,
+//                                       column = atom), B = the mu tile, MN-major
+//                                       (128B_BASE32B) in the weights' place once MMA1
+//                                       is done                            (S/model.cpp:381-383)
+// Every shared-memory tile is written in its storage order (thread -> 16-byte
+// chunk), so the staging stores are free of bank conflicts. The dW_u
+// accumulator stays in TMEM across the CTA's tiles; one [H][NC] partial per CTA
+// (its column block never changes: gridDim.x % NS == 0), summed by
+// k_grad_reduce. TMEM: [0, NC) gm accumulator, [NC, 2 NC) dW_u, [256, 384)
+// gh^T hi, [384, 512) gh^T lo.
 template <int H>
 struct BwdGemmSmem {
     static constexpr int NC = NodeGemmCfg<H>::NC;
-    static constexpr size_t g_floats = 2 * kGemmM * H;  // gh tile hi | lo, MN-major (M = H rows)
+    static constexpr size_t a_floats = 2 * kGemmM * H;  // gh tile hi | lo (MMA1's A)
     static constexpr size_t b_floats = NodeGemmCfg<H>::b_floats > 2 * kGemmM * NC ? NodeGemmCfg<H>::b_floats
                                                                                    : 2 * kGemmM * NC;
-    static constexpr size_t bytes = 4 * (g_floats + b_floats) + 64 + 1024;  // + alignment slack
+    static constexpr size_t bytes = 4 * (a_floats + b_floats) + 64 + 1024;  // + alignment slack
 };
 
 template <int H>
 __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
     using Cfg = NodeGemmCfg<H>;
-    constexpr int NS = Cfg::NS, NC = Cfg::NC, CW = NC / 2;
+    constexpr int NS = Cfg::NS, NC = Cfg::NC, CW = NC / 2, Q = H / 4;
     static_assert(H == 128 && CW % 16 == 0, "fused update backward: H = 128");
-    constexpr int GA = H / 32, MA = NC / 32;  // MN atoms of the gh and mu tiles
-    float* sm = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(dyn_smem<float>()) + 1023) & ~uintptr_t(1023));
-    float* Ghi = sm;
-    float* Glo = Ghi + kGemmM * H;
-    float* Bhi = Glo + kGemmM * H;  // weights [NC][H] hi | lo, then the mu tile hi | lo
+    constexpr int MA = NC / 32;  // MN atoms of the mu tile
+    extern __shared__ __align__(1024) unsigned char bwd_gemm_smem[];
+    float* sm = reinterpret_cast<float*>(bwd_gemm_smem + ((1024u - (smem_u32(bwd_gemm_smem) & 1023u)) & 1023u));
+    float* Ahi = sm;
+    float* Alo = Ahi + kGemmM * H;
+    float* Bhi = Alo + kGemmM * H;  // weights [NC][H] hi | lo, then the mu tile hi | lo
     uint64_t* bar = reinterpret_cast<uint64_t*>(Bhi + BwdGemmSmem<H>::b_floats);  // weights, MMA1, MMA2
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
     const uint32_t tD1 = tbase, tD2 = tbase + NC, tAh = tbase + 256, tAl = tbase + 384;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const uint32_t idesc = umma::idesc_tf32(kGemmM, NC);
-    const uint32_t idesc_mn = umma::idesc_tf32(kGemmM, NC) | (1u << 15) | (1u << 16);
+    const uint32_t idesc_mn = umma::idesc_tf32(kGemmM, NC) | (1u << 16);  // B MN-major
     const int N = d.hdr->N;  // staged upload
     const int ntiles = (N + kGemmM - 1) / kGemmM * NS;
     const int np = blockIdx.x % NS;
@@ -314,34 +316,54 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
         const int base = (tile / NS) * kGemmM;
         const int row = quad * 32 + lane, atom = base + row;
         const bool live = atom < N;
-        if (done > 0) {  // MMA2 of the previous tile read the gh tile and the mu tile in B
+        const int c0 = np * NC + half * CW;
+        if (done > 0) {  // MMA2 of the previous tile read TMEM A and the mu tile in B
             mbar_wait(&bar[2], dphase);
             dphase ^= 1u;
             umma::fence_after();
             fetch_weights();
         }
-        // gh row of this thread's atom, columns [half*64, half*64+64): TMEM (MMA1's A)
-        // and the MN-major shared tile (MMA2's A), tf32 hi | lo
+        // loads first: the gh tile by 16-byte chunk in canonical storage order (MMA1's A),
+        // gh columns for the TMEM A of MMA2 (thread = channel, warps w and w+4 split the
+        // atoms), and this thread's mu row segment for the epilogue
+        constexpr int IT = kGemmM * Q / 256;
+        float4 va[IT];
 #pragma unroll
-        for (int c = 0; c < H / 2; c += 16) {
-            const int b0 = half * (H / 2) + c;
-            float v[16], hv[16], lv[16];
+        for (int it = 0; it < IT; ++it) {
+            const int c = tid + 256 * it, m = (c / (8 * Q)) * 8 + (c & 7), k4 = (c >> 3) % Q;
+            va[it] = base + m < N ? __ldg(reinterpret_cast<const float4*>(gh + static_cast<int64_t>(base + m) * H) + k4)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        float pre[CW];
 #pragma unroll
-            for (int q = 0; q < 16; q += 4) {
-                const float4 x = live ? __ldg(reinterpret_cast<const float4*>(gh + static_cast<int64_t>(atom) * H + b0 + q))
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
-                v[q] = x.x, v[q + 1] = x.y, v[q + 2] = x.z, v[q + 3] = x.w;
+        for (int q = 0; q < CW; q += 4) {
+            const float4 x = live ? __ldg(reinterpret_cast<const float4*>(mu + static_cast<int64_t>(atom) * H + c0 + q))
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            pre[q] = x.x, pre[q + 1] = x.y, pre[q + 2] = x.z, pre[q + 3] = x.w;
+        }
+#pragma unroll
+        for (int it = 0; it < IT; ++it) {
+            const int c = tid + 256 * it;
+            float4 hi, lo;
+            umma::split_tf32(va[it].x, hi.x, lo.x);
+            umma::split_tf32(va[it].y, hi.y, lo.y);
+            umma::split_tf32(va[it].z, hi.z, lo.z);
+            umma::split_tf32(va[it].w, hi.w, lo.w);
+            *reinterpret_cast<float4*>(Ahi + 4 * c) = hi;
+            *reinterpret_cast<float4*>(Alo + 4 * c) = lo;
+        }
+        // gh^T into TMEM: lane = channel b = row, columns = atoms [half*64, half*64+64)
+#pragma unroll
+        for (int cc = 0; cc < kGemmM / 2; cc += 16) {
+            const int a0 = half * (kGemmM / 2) + cc;
+            float hv[16], lv[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const float x = base + a0 + q < N ? __ldg(gh + static_cast<int64_t>(base + a0 + q) * H + row) : 0.f;
+                umma::split_tf32(x, hv[q], lv[q]);
             }
-#pragma unroll
-            for (int q = 0; q < 16; ++q) umma::split_tf32(v[q], hv[q], lv[q]);
-            umma::st16(tAh + lane_off + b0, hv);
-            umma::st16(tAl + lane_off + b0, lv);
-#pragma unroll
-            for (int q = 0; q < 16; q += 4) {
-                const int o = umma::mn32_idx(b0 + q, row, GA);
-                *reinterpret_cast<float4*>(Ghi + o) = make_float4(hv[q], hv[q + 1], hv[q + 2], hv[q + 3]);
-                *reinterpret_cast<float4*>(Glo + o) = make_float4(lv[q], lv[q + 1], lv[q + 2], lv[q + 3]);
-            }
+            umma::st16(tAh + lane_off + a0, hv);
+            umma::st16(tAl + lane_off + a0, lv);
         }
         umma::st_wait();
         umma::fence_proxy_async();
@@ -352,22 +374,26 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
             umma::fence_after();
             const float* Blo = Bhi + NC * H;
 #pragma unroll
-            for (int s = 0; s < H / 8; ++s) {
-                umma::mma_tf32_ts(tD1, tAh + s * 8, umma::kdesc(Bhi, s, H), idesc, s ? 1u : 0u);
-                umma::mma_tf32_ts(tD1, tAh + s * 8, umma::kdesc(Blo, s, H), idesc, 1u);
-                umma::mma_tf32_ts(tD1, tAl + s * 8, umma::kdesc(Bhi, s, H), idesc, 1u);
-            }
+            for (int s = 0; s < H / 8; ++s)
+                umma::mma3(tD1, umma::kdesc(Ahi, s, H), umma::kdesc(Alo, s, H), umma::kdesc(Bhi, s, H),
+                           umma::kdesc(Blo, s, H), idesc, s ? 1u : 0u);
             umma::commit(&bar[1]);
         }
         wphase ^= 1u;
-        // mu row of this thread's atom, this CTA's columns: epilogue (1 - mu^2) and MMA2's B
-        const int c0 = np * NC + half * CW;
-        float pre[CW];
+        // the mu tile for MMA2's B (N = this CTA's NC columns, K = atoms), MN-major
+        // 128B_BASE32B, written chunk by chunk in storage order once MMA1 is done
+        constexpr int MIT = kGemmM * NC / 4 / 256;
+        float4 vm[MIT];
+        int mo[MIT];
 #pragma unroll
-        for (int q = 0; q < CW; q += 4) {
-            const float4 x = live ? __ldg(reinterpret_cast<const float4*>(mu + static_cast<int64_t>(atom) * H + c0 + q))
+        for (int it = 0; it < MIT; ++it) {
+            const int c = tid + 256 * it;  // 16-byte chunk c of the tile in storage order
+            const int mna = (c >> 5) % MA, kg = (c >> 5) / MA, kr = (c >> 3) & 3, x = (c >> 1) & 3, hl = c & 1;
+            const int mn = mna * 32 + ((x ^ kr) << 3) + (hl << 2), k = kg * 4 + kr;  // column, atom
+            vm[it] = base + k < N ? __ldg(reinterpret_cast<const float4*>(mu + static_cast<int64_t>(base + k) * H +
+                                                                          np * NC + mn))
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-            pre[q] = x.x, pre[q + 1] = x.y, pre[q + 2] = x.z, pre[q + 3] = x.w;
+            mo[it] = 4 * c;
         }
         mbar_wait(&bar[1], mphase);
         mphase ^= 1u;
@@ -376,15 +402,14 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
             float* Mhi = Bhi;  // the weight block is free
             float* Mlo = Bhi + kGemmM * NC;
 #pragma unroll
-            for (int q = 0; q < CW; q += 4) {
+            for (int it = 0; it < MIT; ++it) {
                 float4 h4, l4;
-                umma::split_tf32(pre[q], h4.x, l4.x);
-                umma::split_tf32(pre[q + 1], h4.y, l4.y);
-                umma::split_tf32(pre[q + 2], h4.z, l4.z);
-                umma::split_tf32(pre[q + 3], h4.w, l4.w);
-                const int o = umma::mn32_idx(half * CW + q, row, MA);
-                *reinterpret_cast<float4*>(Mhi + o) = h4;
-                *reinterpret_cast<float4*>(Mlo + o) = l4;
+                umma::split_tf32(vm[it].x, h4.x, l4.x);
+                umma::split_tf32(vm[it].y, h4.y, l4.y);
+                umma::split_tf32(vm[it].z, h4.z, l4.z);
+                umma::split_tf32(vm[it].w, h4.w, l4.w);
+                *reinterpret_cast<float4*>(Mhi + mo[it]) = h4;
+                *reinterpret_cast<float4*>(Mlo + mo[it]) = l4;
             }
             umma::fence_proxy_async();
             umma::fence_before();
@@ -393,11 +418,11 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
                 umma::fence_after();
 #pragma unroll
                 for (int s = 0; s < kGemmM / 8; ++s) {  // K-step s: atoms 8s..8s+7 = two 4-row groups
-                    const uint64_t ah = umma::mn32_desc(Ghi + s * 2 * (GA << 7), GA);
-                    const uint64_t al = umma::mn32_desc(Glo + s * 2 * (GA << 7), GA);
                     const uint64_t bh = umma::mn32_desc(Mhi + s * 2 * (MA << 7), MA);
                     const uint64_t bl = umma::mn32_desc(Mlo + s * 2 * (MA << 7), MA);
-                    umma::mma3(tD2, ah, al, bh, bl, idesc_mn, (done | s) ? 1u : 0u);
+                    umma::mma_tf32_ts(tD2, tAh + s * 8, bh, idesc_mn, (done | s) ? 1u : 0u);
+                    umma::mma_tf32_ts(tD2, tAh + s * 8, bl, idesc_mn, 1u);
+                    umma::mma_tf32_ts(tD2, tAl + s * 8, bh, idesc_mn, 1u);
                 }
                 umma::commit(&bar[2]);
             }
@@ -417,7 +442,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
                                 v[q + 3] * (1.f - pre[cc + q + 3] * pre[cc + q + 3]));
         }
         umma::fence_before();
-        __syncthreads();  // the gm accumulator is drained before the next tile's MMA1
+        __syncthreads();  // the gm accumulator and the A tile are drained before the next tile
         umma::fence_after();
     }
     // this CTA's dW_u partial: rows b = TMEM lanes, columns of block np
