@@ -614,25 +614,35 @@ struct HeadBody {
         W = fmaf(sij, r.t, W);
         if (a < K) R = fmaf(ed[e & 7], st.fcp[e * K + a], R);
     }
+    // per-atom operands are loaded when the atom begins and used at its end, so
+    // their latency hides behind the atom's edges
+    float p_wa, p_wb, p_hv, p_ge, p_we, p_gh;
     __device__ void begin(int i) {
         s = d.sample_of[i];
         ch = pass_ch >= 0 ? pass_ch : d.dsidx[s];
         const int row = L > 0 ? i : __ldg(d.Z + i) - 1;
         Ti = __ldg(T + static_cast<int64_t>(row) * H + a);
         S = W = R = 0.f;
+        p_wa = __ldg(d.wfh + a * D + ch);
+        p_wb = __ldg(d.wfh + (H + a) * D + ch);
+        if (first) {
+            p_hv = __ldg(hL + static_cast<int64_t>(row) * H + a);
+            p_ge = __ldg(d.gE + static_cast<int64_t>(s) * D + ch);
+            p_we = __ldg(d.we + a * D + ch);
+        } else {
+            p_gh = d.gh[static_cast<int64_t>(i) * H + a];
+        }
     }
     __device__ void end(int i) {
-        const float wa = d.wfh[a * D + ch], wb = d.wfh[(H + a) * D + ch];
-        const float gT = S * wa + wb * W;
+        const float gT = S * p_wa + p_wb * W;
         float* ghp = d.gh + static_cast<int64_t>(i) * H + a;
         float gh;
         const float* gE = d.gE + static_cast<int64_t>(s) * D;
         if (first) {
-            const int row = L > 0 ? i : __ldg(d.Z + i) - 1;
-            const float hv = hL[static_cast<int64_t>(row) * H + a];
+            const float hv = p_hv;
             if (pass_ch < 0) {  // k_loss zeroes every head but the sample's own: same sums, one term
-                const float ge = gE[ch];
-                gh = d.we[a * D + ch] * ge;
+                const float ge = p_ge;
+                gh = p_we * ge;
                 acc[(2 * D + ch) * H + a] = fmaf(hv, ge, acc[(2 * D + ch) * H + a]);
             } else {
                 gh = 0.f;
@@ -641,7 +651,7 @@ struct HeadBody {
                     acc[(2 * D + dd) * H + a] = fmaf(hv, gE[dd], acc[(2 * D + dd) * H + a]);
             }
         } else {
-            gh = *ghp;
+            gh = p_gh;
         }
         *ghp = fmaf(gT, 1.f - Ti * Ti, gh);
         acc[ch * H + a] = fmaf(S, Ti, acc[ch * H + a]);
@@ -734,15 +744,16 @@ struct BwdBody {
             }
         }
     }
+    float p_ti, p_gh;  // per-atom operands, loaded at begin() and used at end()
     __device__ void begin(int i) {
         gmi = d.gm[static_cast<int64_t>(i) * H + a];
         gt = 0.f;
+        const int row = l == 0 ? __ldg(d.Z + i) - 1 : i;
+        p_ti = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
+        p_gh = d.gh[static_cast<int64_t>(i) * H + a];
     }
     __device__ void end(int i) {
-        const int row = l == 0 ? __ldg(d.Z + i) - 1 : i;
-        const float ti = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
-        float* ghp = d.gh + static_cast<int64_t>(i) * H + a;
-        *ghp = fmaf(gt, 1.f - ti * ti, *ghp);
+        d.gh[static_cast<int64_t>(i) * H + a] = fmaf(gt, 1.f - p_ti * p_ti, p_gh);
     }
 };
 
