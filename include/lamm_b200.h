@@ -21,7 +21,8 @@
  *       energy_mask[B]/force_mask[B] uint8 (m_E, m_F), energy[B] f64,
  *       forces[3N] f64 (rows of force-labelled samples; ignored otherwise),
  *       denoise[B] uint8 (nullable: sample comes from a denoising subset and
- *       gets labels from make_denoising_sample, S/denoise.cpp:42-53).
+ *       gets labels from make_denoising_sample, S/denoise.cpp:42-53),
+ *       cell[B][3][3] f64 (nullable: periodic cells, minimum image).
  *   - Parameters: fp64, flat, for_each_tensor order (H/model.hpp:59-66):
  *       embedding 118xH, filter[L] HxK, update[L] HxH, energy_head HxD,
  *       force_head (2H+K)xD, each row-major.
@@ -72,6 +73,12 @@ typedef struct {
     const double* energy;
     const double* forces;
     const uint8_t* denoise;
+    /* Periodic cells (extension; the reference has none): [n_samples][3][3], row k =
+     * lattice vector k (Angstrom); an all-zero cell marks a non-periodic sample.
+     * NULL: every sample is non-periodic (the reference's behaviour, bit-exact).
+     * Periodic samples use the minimum image, which requires every perpendicular
+     * cell width >= 2 * cutoff (else LAMM_EINPUT). */
+    const double* cell;
 } lamm_batch_view;
 
 /* lamm::loss::ReferenceTable / DatasetNormalizer, H/loss.hpp:31-44. rho and
@@ -292,6 +299,10 @@ int lamm_synth_fill(int32_t task, int64_t count, double mode, double sigma, int3
                     uint64_t seed, int32_t threads, const int64_t* atom_ptr, double* positions,
                     int32_t* atomic_numbers, uint8_t* energy_mask, uint8_t* force_mask, double* energy,
                     double* forces);
+/* Inverse of a 3x3 cell (row-major, rows = lattice vectors) by cofactors: the
+ * exact bits the minimum-image test uses. Returns LAMM_EINPUT if singular. */
+int lamm_cell_inverse(const double* cell, double* out);
+
 /* Reference RNG streams (H/rng.hpp): mix_seed and Box-Muller normals. */
 uint64_t lamm_mix_seed(uint64_t a, uint64_t b);
 int lamm_rng_normals(uint64_t seed, int64_t n, double* out);

@@ -140,12 +140,19 @@ struct PackedBatch {
     std::vector<double> positions, energy, forces;
     std::vector<int32_t> Z, dataset_index;
     std::vector<uint8_t> energy_mask, force_mask, denoise;
+    std::vector<double> cell;  // [B][9] periodic cells, empty if none was given (extension; see lamm_b200.h)
 
     int32_t size() const { return static_cast<int32_t>(atom_ptr.size() - 1); }
     int64_t atoms() const { return atom_ptr.back(); }
 
+    // cell9: optional periodic cell of this system (rows = lattice vectors); the
+    // reference's AtomicSystem has none
     template <class System>
-    void add_system(const System& s) {
+    void add_system(const System& s, const double* cell9 = nullptr) {
+        if (cell9 != nullptr && cell.empty()) cell.assign(9 * static_cast<size_t>(size()), 0.0);
+        if (!cell.empty()) {
+            for (int k = 0; k < 9; ++k) cell.push_back(cell9 ? cell9[k] : 0.0);
+        }
         const size_t n = s.positions.size();
         if (s.atomic_numbers.size() != n) throw InputError("system: positions / atomic_numbers size mismatch");
         for (size_t i = 0; i < n; ++i) {
@@ -195,6 +202,7 @@ struct PackedBatch {
         v.energy = energy.data();
         v.forces = forces.data();
         v.denoise = denoise.data();
+        v.cell = cell.empty() ? nullptr : cell.data();
         return v;
     }
 };

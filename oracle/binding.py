@@ -16,6 +16,7 @@ with ``rho``/``rho_has`` ([ntab,119]), ``mean``, ``std``, ``fstd``, ``has``.
 from __future__ import annotations
 
 import ctypes as C
+import contextlib
 import os
 
 import numpy as np
@@ -67,6 +68,30 @@ class OracleLib:
     def _check(self, st):
         if st != 0:
             raise OracleError(f"{self.pre}: status {st}: {self._f('last_error')().decode()}")
+
+    # ----------------------------------------------------- periodic cells
+    def cell_inverse(self, cell):
+        """lor_cell_inverse (port): the cofactor inverse the minimum image uses."""
+        out = np.empty(9, np.float64)
+        self._check(self.lib.lor_cell_inverse(_p(_c(np.asarray(cell).reshape(9), np.float64)), _p(out)))
+        return out
+
+    @contextlib.contextmanager
+    def periodic(self, cells):
+        """Port only: batch calls inside use these cells ([B, 3, 3], all-zero = non-periodic),
+        minimum image (parity-unpinned extension: the reference has no cells)."""
+        if self.kind != "port":
+            raise NotImplementedError("the reference has no periodic cells")
+        cells = _c(np.asarray(cells).reshape(-1, 9), np.float64)
+        inv = np.zeros_like(cells)
+        for s in range(len(cells)):
+            if np.any(cells[s] != 0.0):
+                inv[s] = self.cell_inverse(cells[s])
+        self.lib.lor_set_cells(_p(cells), _p(inv))
+        try:
+            yield
+        finally:
+            self.lib.lor_set_cells(None, None)
 
     # ---------------------------------------------------------------- rng
     def mix_seed(self, a, b):

@@ -155,8 +155,63 @@ static int validate_system(int32_t n, const double* pos, const int32_t* Z) { /* 
     return 0;
 }
 
-/* S/core.cpp:30-48: all ordered pairs, r < cutoff strictly, i-major, j-ascending. */
-static int build_pairs(int32_t n, const double* pos, const int32_t* Z, double cutoff, Pairs* out) {
+/* Periodic cells (SURVEY.md §8(f) extension; the reference has none, so this is
+ * parity-unpinned): sample s is periodic when g_cells holds a nonzero 3x3 cell
+ * (rows = lattice vectors) for it; pairs then use the minimum image,
+ *   f_k = sum_c d_c cinv[c][k], f_k -= rint(f_k), d_c = sum_k f_k cell[k][c],
+ * evaluated left to right without contraction (the device kernels use the same
+ * sequence with __dmul_rn/__dadd_rn), which is exact for cells whose
+ * perpendicular widths are at least 2 * cutoff. */
+static _Thread_local const double* g_cells = NULL;
+static _Thread_local const double* g_cellinv = NULL;
+
+/* 3x3 inverse by cofactors (rows = lattice vectors), the same expression
+ * sequence as the device library's cell_inverse (device.cuh); 1 if singular. */
+int lor_cell_inverse(const double* m, double* inv) {
+    const double c00 = m[4] * m[8] - m[5] * m[7], c01 = m[5] * m[6] - m[3] * m[8], c02 = m[3] * m[7] - m[4] * m[6];
+    const double c10 = m[2] * m[7] - m[1] * m[8], c11 = m[0] * m[8] - m[2] * m[6], c12 = m[1] * m[6] - m[0] * m[7];
+    const double c20 = m[1] * m[5] - m[2] * m[4], c21 = m[2] * m[3] - m[0] * m[5], c22 = m[0] * m[4] - m[1] * m[3];
+    const double det = (m[0] * c00 + m[1] * c01) + m[2] * c02;
+    if (!(det != 0.0)) return set_err("cell: singular"), 1;
+    const double cof[9] = {c00, c10, c20, c01, c11, c21, c02, c12, c22};
+    for (int k = 0; k < 9; ++k) inv[k] = cof[k] / det;
+    return 0;
+}
+
+void lor_set_cells(const double* cells, const double* cellinv) {
+    g_cells = cells;
+    g_cellinv = cellinv;
+}
+
+static const double* cell_of(int64_t s) {
+    if (!g_cells) return NULL;
+    const double* c = g_cells + 9 * s;
+    for (int k = 0; k < 9; ++k)
+        if (c[k] != 0.0) return c;
+    return NULL;
+}
+
+static void min_image(const double* cell, const double* ci, double* d0, double* d1, double* d2) {
+    double f[3];
+    for (int k = 0; k < 3; ++k) {
+        const double a = *d0 * ci[k], b = *d1 * ci[3 + k], c = *d2 * ci[6 + k];
+        f[k] = (a + b) + c;
+        f[k] = f[k] - rint(f[k]);
+    }
+    double o[3];
+    for (int c = 0; c < 3; ++c) {
+        const double a = f[0] * cell[c], b = f[1] * cell[3 + c], e = f[2] * cell[6 + c];
+        o[c] = (a + b) + e;
+    }
+    *d0 = o[0], *d1 = o[1], *d2 = o[2];
+}
+
+/* S/core.cpp:30-48: all ordered pairs, r < cutoff strictly, i-major, j-ascending.
+ * cell/ci non-NULL: minimum-image pairs of a periodic sample. */
+static int build_pairs_cell(int32_t n, const double* pos, const int32_t* Z, double cutoff, const double* cell,
+                            const double* ci, Pairs* out);
+static int build_pairs_cell(int32_t n, const double* pos, const int32_t* Z, double cutoff, const double* cell,
+                            const double* ci, Pairs* out) {
     if (validate_system(n, pos, Z)) return 1;
     if (!(cutoff > 0.0)) return set_err("cutoff must be positive"), 1;
     int64_t cap = 64, cnt = 0;
@@ -167,8 +222,8 @@ static int build_pairs(int32_t n, const double* pos, const int32_t* Z, double cu
     for (int32_t i = 0; i < n; ++i) {
         for (int32_t j = 0; j < n; ++j) {
             if (j == i) continue;
-            const double d0 = pos[3 * i] - pos[3 * j], d1 = pos[3 * i + 1] - pos[3 * j + 1],
-                         d2 = pos[3 * i + 2] - pos[3 * j + 2];
+            double d0 = pos[3 * i] - pos[3 * j], d1 = pos[3 * i + 1] - pos[3 * j + 1], d2 = pos[3 * i + 2] - pos[3 * j + 2];
+            if (cell) min_image(cell, ci, &d0, &d1, &d2);
             const double r = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
             if (r < cutoff) {
                 if (cnt == cap) {
@@ -203,7 +258,8 @@ static void free_pairs(Pairs* p) {
 int64_t lor_neighbor_list(int32_t n, const double* pos, const int32_t* Z, double cutoff, int64_t cap, int32_t* oi,
                           int32_t* oj, double* odist, double* ounit) {
     Pairs p;
-    if (build_pairs(n, pos, Z, cutoff, &p)) return -1;
+    const double* cell = cell_of(0);
+    if (build_pairs_cell(n, pos, Z, cutoff, cell, cell ? g_cellinv : NULL, &p)) return -1;
     for (int64_t k = 0; k < p.n && k < cap; ++k) {
         oi[k] = p.i[k];
         oj[k] = p.j[k];
@@ -288,10 +344,16 @@ typedef struct {
     const int32_t* Z;
 } Cache;
 
+static int run_encoder_s(const Params* p, int32_t n, const double* pos, const int32_t* Z, int64_t s, Cache* c);
 static int run_encoder(const Params* p, int32_t n, const double* pos, const int32_t* Z, Cache* c) {
+    return run_encoder_s(p, n, pos, Z, 0, c);
+}
+/* s: the sample's index for its (optional) cell */
+static int run_encoder_s(const Params* p, int32_t n, const double* pos, const int32_t* Z, int64_t s, Cache* c) {
     /* S/model.cpp:37-110 */
     const int H = p->H, K = p->K, L = p->L;
-    if (build_pairs(n, pos, Z, p->rc, &c->pr)) return 1;
+    const double* cell = cell_of(s);
+    if (build_pairs_cell(n, pos, Z, p->rc, cell, cell ? g_cellinv + 9 * s : NULL, &c->pr)) return 1;
     const int64_t P = c->pr.n;
     c->n = n;
     c->Z = Z;
@@ -396,7 +458,7 @@ int lor_forward(int H, int L, int K, double rc, int D, const double* params, int
     for (int s = 0; s < B && !st; ++s) {
         Cache c;
         const int32_t n = (int32_t)(atom_ptr[s + 1] - atom_ptr[s]);
-        st = run_encoder(&p, n, pos + 3 * atom_ptr[s], Z + atom_ptr[s], &c);
+        st = run_encoder_s(&p, n, pos + 3 * atom_ptr[s], Z + atom_ptr[s], s, &c);
         if (st) break;
         heads_forward(&p, &c, out_energy + (int64_t)s * D, out_forces + 3 * D * atom_ptr[s]);
         cache_free(&c);
@@ -544,7 +606,7 @@ int lor_backward(int H, int L, int K, double rc, int D, const double* params, in
     for (int s = 0; s < B; ++s) {
         Cache c;
         const int32_t n = (int32_t)(atom_ptr[s + 1] - atom_ptr[s]);
-        st = run_encoder(&p, n, pos + 3 * atom_ptr[s], Z + atom_ptr[s], &c);
+        st = run_encoder_s(&p, n, pos + 3 * atom_ptr[s], Z + atom_ptr[s], s, &c);
         if (st) break;
         backward_one(&p, &c, up_energy + (int64_t)s * D, up_forces + 3 * D * atom_ptr[s], &g);
         cache_free(&c);
@@ -727,7 +789,7 @@ static int worker_body(const Params* pp, Params* gg, int gi, int B, int D, const
             st = normalize_one(n, Z + o, ld[b], lem[b], lfm[b], energy[pos_], forces + 3 * o, ntab, rho, rho_has,
                                mean, stdv, fstd, has, le + b, lf + 3 * lo);
         }
-        if (!st) st = run_encoder(&p, n, xs + 3 * lo, Z + o, &caches[b]);
+        if (!st) st = run_encoder_s(&p, n, xs + 3 * lo, Z + o, pos_, &caches[b]);
         if (!st) heads_forward(&p, &caches[b], pe + (int64_t)b * D, pf + 3 * D * lo);
     }
     double bd[7];

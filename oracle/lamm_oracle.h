@@ -23,6 +23,11 @@ void lor_rng_u64(uint64_t seed, int64_t n, uint64_t* out);
 void lor_rng_bounded(uint64_t seed, int64_t n, uint64_t bound, uint64_t* out);
 void lor_rng_permutation(uint64_t seed, int64_t n, int64_t* out);
 
+/* Periodic cells for the batch calls that follow ([B][3][3] rows = lattice
+ * vectors, all-zero rows block = non-periodic sample; cellinv its inverse), or
+ * NULL. Minimum image; parity-unpinned extension (the reference has no cells). */
+void lor_set_cells(const double* cells, const double* cellinv);
+int lor_cell_inverse(const double* cell, double* out);
 int64_t lor_neighbor_list(int32_t n, const double* pos, const int32_t* Z, double cutoff, int64_t cap,
                           int32_t* oi, int32_t* oj, double* odist, double* ounit);
 

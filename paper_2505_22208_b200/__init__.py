@@ -6,7 +6,7 @@ with hand-written sm_100a CUDA kernels, host C++ for the atom-count load
 balancer, and NCCL for the one gradient allreduce per step. This package is
 the host-side mirror of the reference API; there is no CPU compute fallback.
 """
-from .api import (Device, LossConfig, ModelConfig, TrainConfig, build_epoch_index, comm_unique_id,  # noqa: F401
+from .api import (Device, LossConfig, ModelConfig, TrainConfig, build_epoch_index, cell_inverse, comm_unique_id,  # noqa: F401
                   concat, empty_table, greedy_assign, init_params, make_trace, mix_seed, param_count, plan,
                   rng_normals, select, synth_generate, temperature_counts)
 from ._lib import InputError, LammError, NonFiniteError, LIB_PATH  # noqa: F401

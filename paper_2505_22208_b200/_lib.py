@@ -34,7 +34,7 @@ class BatchViewC(C.Structure):
     _fields_ = [("n_samples", C.c_int32), ("n_atoms", C.c_int64), ("atom_ptr", C.c_void_p),
                 ("positions", C.c_void_p), ("atomic_numbers", C.c_void_p), ("dataset_index", C.c_void_p),
                 ("energy_mask", C.c_void_p), ("force_mask", C.c_void_p), ("energy", C.c_void_p),
-                ("forces", C.c_void_p), ("denoise", C.c_void_p)]
+                ("forces", C.c_void_p), ("denoise", C.c_void_p), ("cell", C.c_void_p)]
 
 
 class RefTableC(C.Structure):
@@ -81,7 +81,7 @@ EXPORTS = [
     "lamm_last_step_launches", "lamm_greedy_assign", "lamm_plan", "lamm_schedule_metrics", "lamm_make_trace",
     "lamm_temperature_counts", "lamm_build_epoch_index", "lamm_synth_counts", "lamm_synth_fill",
     "lamm_mix_seed", "lamm_rng_normals", "lamm_stage", "lamm_train_step_staged", "lamm_anomalies",
-    "lamm_flush_l2", "lamm_step_times", "lamm_evaluate",
+    "lamm_flush_l2", "lamm_step_times", "lamm_evaluate", "lamm_cell_inverse",
 ]
 
 _lib = None

@@ -104,9 +104,11 @@ def _batch_view(b: dict):
         "denoise": _c(b.get("denoise", np.zeros(len(b["atom_ptr"]) - 1)), np.uint8),
     }
     B = len(keep["atom_ptr"]) - 1
+    if b.get("cell") is not None:  # periodic cells [B, 3, 3] (all-zero: non-periodic sample)
+        keep["cell"] = _c(np.asarray(b["cell"]).reshape(B, 9), np.float64)
     v = BatchViewC(B, int(keep["atom_ptr"][-1]), _p(keep["atom_ptr"]), _p(keep["pos"]), _p(keep["Z"]),
                    _p(keep["dataset_index"]), _p(keep["energy_mask"]), _p(keep["force_mask"]), _p(keep["energy"]),
-                   _p(keep["forces"]), _p(keep["denoise"]))
+                   _p(keep["forces"]), _p(keep["denoise"]), _p(keep["cell"]) if "cell" in keep else None)
     return v, keep
 
 
@@ -116,6 +118,13 @@ def _table_view(t: dict):
     v = RefTableC(len(keep["mean"]), _p(keep["rho"]), _p(keep["rho_has"]), _p(keep["mean"]), _p(keep["std"]),
                   _p(keep["fstd"]), _p(keep["has"]))
     return v, keep
+
+
+def cell_inverse(cell) -> np.ndarray:
+    """The 3x3 cofactor inverse the minimum-image test uses (lamm_cell_inverse)."""
+    out = np.empty(9)
+    check(lib().lamm_cell_inverse(_p(_c(np.asarray(cell).reshape(9), np.float64)), _p(out)))
+    return out
 
 
 def empty_table(n: int) -> dict:
@@ -473,6 +482,8 @@ def select(batch: dict, ids) -> dict:
         out[k] = np.ascontiguousarray(batch[k][rows])
     for k in ("dataset_index", "energy_mask", "force_mask", "energy", "denoise"):
         out[k] = np.ascontiguousarray(batch[k][ids])
+    if batch.get("cell") is not None:
+        out["cell"] = np.ascontiguousarray(np.asarray(batch["cell"]).reshape(-1, 3, 3)[ids])
     return out
 
 
@@ -484,4 +495,7 @@ def concat(batches) -> dict:
         out[k] = np.concatenate([b[k] for b in batches])
     sizes = np.concatenate([np.diff(b["atom_ptr"]) for b in batches])
     out["atom_ptr"] = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    if any(b.get("cell") is not None for b in batches):  # non-periodic parts get all-zero cells
+        out["cell"] = np.concatenate([np.asarray(b["cell"]).reshape(-1, 3, 3) if b.get("cell") is not None
+                                      else np.zeros((len(b["atom_ptr"]) - 1, 3, 3)) for b in batches])
     return out

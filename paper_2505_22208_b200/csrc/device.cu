@@ -640,6 +640,8 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
     place(h.off_F, 24 * N);
     if (any_dn) place(h.off_noise, 24 * N);
     else h.off_noise = h.off_F;
+    if (b->cell) place(h.off_cell, 8 * kCellDoubles * B);
+    else h.off_cell = 0;
     h.blob_bytes = static_cast<int64_t>(off);
     ensure_stage(c, off);
     char* base = c.h_stage;
@@ -673,6 +675,31 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
     }
     if (b->forces) std::memcpy(F, b->forces, 24 * N);
     else std::memset(F, 0, 24 * N);
+    if (b->cell) {  // {flag, cell, cell^-1} per sample; minimum image needs widths >= 2 rc
+        double* cs = reinterpret_cast<double*>(base + h.off_cell);
+        for (int32_t s = 0; s < B; ++s) {
+            const double* m = b->cell + 9 * static_cast<int64_t>(s);
+            double* o = cs + static_cast<int64_t>(kCellDoubles) * s;
+            bool periodic = false;
+            for (int k = 0; k < 9; ++k) periodic |= m[k] != 0.0;
+            std::memset(o, 0, sizeof(double) * kCellDoubles);
+            if (!periodic) continue;
+            for (int k = 0; k < 9; ++k) require(std::isfinite(m[k]), "cell: non-finite entry");
+            require(cell_inverse(m, o + 10), "cell: singular");
+            const double det = std::fabs((m[0] * (m[4] * m[8] - m[5] * m[7]) + m[1] * (m[5] * m[6] - m[3] * m[8])) +
+                                         m[2] * (m[3] * m[7] - m[4] * m[6]));
+            for (int k = 0; k < 3; ++k) {  // perpendicular width along lattice vector k
+                const double* u = m + 3 * ((k + 1) % 3);
+                const double* v = m + 3 * ((k + 2) % 3);
+                const double cx = u[1] * v[2] - u[2] * v[1], cy = u[2] * v[0] - u[0] * v[2], cz = u[0] * v[1] - u[1] * v[0];
+                const double width = det / std::sqrt(cx * cx + cy * cy + cz * cz);
+                require(width >= 2.0 * c.cfg.cutoff,
+                        "cell: perpendicular width below 2 * cutoff (minimum image); replicate the cell");
+            }
+            o[0] = 1.0;
+            std::memcpy(o + 1, m, sizeof(double) * 9);
+        }
+    }
     if (any_dn) {
         // Raw displacement draws of make_denoising_sample: Rng(seed').normal(0, sigma)
         // per atom, x, y, z in order (S/denoise.cpp:31-40), with
@@ -1463,3 +1490,10 @@ LAMM_API int lamm_step_times(lamm_ctx* c, double* total_ms, int64_t* steps) {
 }
 
 LAMM_API int64_t lamm_last_step_launches(lamm_ctx* c) { return c ? c->last_step_launches : -1; }
+
+LAMM_API int lamm_cell_inverse(const double* cell, double* out) {
+    return lamm_guard([&] {
+        require(cell && out, "cell_inverse: null argument");
+        require(cell_inverse(cell, out), "cell: singular");
+    });
+}

@@ -44,7 +44,7 @@ struct StepHeader {
     // byte offsets of the staged input arrays inside the upload blob (the blob
     // starts with this header), see device.cu:pack_batch
     int64_t off_atom_ptr, off_pos, off_Z, off_z2s, off_dsidx, off_emask, off_fmask, off_denoise, off_E, off_F,
-        off_noise, blob_bytes;
+        off_noise, off_cell, blob_bytes;  // off_cell: [B] x {periodic flag, cell[9], cell^-1[9]} (0: none)
 };
 
 struct Dev {
@@ -133,6 +133,40 @@ struct Dev {
 __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Periodic cells: per sample 19 doubles {flag, cell[9] (rows = lattice vectors),
+// cell^-1[9]} in the staged blob. The minimum image uses
+//   f_k = sum_c d_c cinv[c][k] - rint(.),  d_c = sum_k f_k cell[k][c],
+// left to right, correctly rounded (oracle/lamm_oracle.c:min_image is the same).
+constexpr int kCellDoubles = 19;
+
+__host__ __device__ inline bool cell_inverse(const double* m, double* inv) {
+    const double c00 = m[4] * m[8] - m[5] * m[7], c01 = m[5] * m[6] - m[3] * m[8], c02 = m[3] * m[7] - m[4] * m[6];
+    const double c10 = m[2] * m[7] - m[1] * m[8], c11 = m[0] * m[8] - m[2] * m[6], c12 = m[1] * m[6] - m[0] * m[7];
+    const double c20 = m[1] * m[5] - m[2] * m[4], c21 = m[2] * m[3] - m[0] * m[5], c22 = m[0] * m[4] - m[1] * m[3];
+    const double det = (m[0] * c00 + m[1] * c01) + m[2] * c02;
+    if (!(det != 0.0)) return false;
+    const double cof[9] = {c00, c10, c20, c01, c11, c21, c02, c12, c22};  // adjugate, row-major
+    for (int k = 0; k < 9; ++k) inv[k] = cof[k] / det;
+    return true;
+}
+
+__device__ __forceinline__ void min_image(const double* cell, const double* ci, double& d0, double& d1, double& d2) {
+    double f[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double a = __dmul_rn(d0, ci[k]), b = __dmul_rn(d1, ci[3 + k]), c = __dmul_rn(d2, ci[6 + k]);
+        f[k] = __dadd_rn(__dadd_rn(a, b), c);
+        f[k] = __dsub_rn(f[k], rint(f[k]));
+    }
+    double o[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double a = __dmul_rn(f[0], cell[c]), b = __dmul_rn(f[1], cell[3 + c]), e = __dmul_rn(f[2], cell[6 + c]);
+        o[c] = __dadd_rn(__dadd_rn(a, b), e);
+    }
+    d0 = o[0], d1 = o[1], d2 = o[2];
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

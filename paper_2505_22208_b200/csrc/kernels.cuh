@@ -52,12 +52,23 @@ struct BatchArrays {
 // ------------------------------------------------------- neighbour list ---
 // Bit-exact with S/core.cpp:40-43: d = p_i - p_j, r = sqrt((dx*dx + dy*dy) + dz*dz)
 // with every operation individually rounded (no FMA contraction), r < cutoff.
+// cell: nullptr, or {cell[9], cell^-1[9]} of a periodic sample (minimum image)
 __device__ __forceinline__ double pair_dist(double xi, double yi, double zi, double xj, double yj, double zj,
-                                            double& dx, double& dy, double& dz) {
+                                            double& dx, double& dy, double& dz, const double* cell = nullptr) {
     dx = __dsub_rn(xi, xj);
     dy = __dsub_rn(yi, yj);
     dz = __dsub_rn(zi, zj);
+    if (cell) min_image(cell, cell + 9, dx, dy, dz);
     return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+}
+
+// The sample's periodic cell in the staged blob, or nullptr.
+__device__ __forceinline__ const double* sample_cell(const Dev& d, int s) {
+    const StepHeader& hd = *d.hdr;
+    if (hd.off_cell == 0) return nullptr;
+    const double* c = reinterpret_cast<const double*>(reinterpret_cast<const char*>(d.hdr) + hd.off_cell) +
+                      static_cast<int64_t>(kCellDoubles) * s;
+    return c[0] != 0.0 ? c + 1 : nullptr;
 }
 
 
@@ -139,6 +150,7 @@ __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out) {
         // neighbour counts of the sample (S/core.cpp:30-48), warp per atom, from the
         // positions this block just wrote (plain loads: visible after the barrier)
         const int lane = threadIdx.x & 31;
+        const double* cell = sample_cell(d, s);
         for (int64_t i = lo + (threadIdx.x >> 5); i < hi; i += blockDim.x >> 5) {
             const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
             int cnt = 0;
@@ -147,7 +159,7 @@ __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out) {
                 bool in = false;
                 if (j < hi && j != i) {
                     double dx, dy, dz;
-                    in = pair_dist(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz) < d.rc;
+                    in = pair_dist(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz, cell) < d.rc;
                 }
                 cnt += __popc(__ballot_sync(0xffffffffu, in));
             }
@@ -242,6 +254,7 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d) {
         const int s = d.sample_of[i];
         const int lo = static_cast<int>(d.atom_ptr[s]), hi = static_cast<int>(d.atom_ptr[s + 1]);
         const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
+        const double* cell = sample_cell(d, s);
         int base = d.row_ptr[i];
         if (lane == 0 && d.row_ptr[i + 1] > base) atomicOr(d.segw + (base >> 5), 1u << (base & 31));
         for (int j0 = lo; j0 < hi; j0 += 32) {
@@ -249,7 +262,7 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d) {
             bool in = false;
             double dx = 0, dy = 0, dz = 0, r = 0;
             if (j < hi && j != i) {
-                r = pair_dist(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz);
+                r = pair_dist(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz, cell);
                 in = r < d.rc;
             }
             const unsigned mask = __ballot_sync(0xffffffffu, in);

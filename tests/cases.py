@@ -74,3 +74,66 @@ def mixed_batch(lib, D=10, seed=5, count=24, denoise_frac=0.3):
     b["energy_mask"] = (kind != 2).astype(np.uint8)
     b["denoise"] = (kind == 2).astype(np.uint8)
     return b
+
+
+def diamond_supercell(reps=2, a=5.43, jitter=0.05, seed=0, Z=14):
+    """cfg1's periodic bulk: an reps^3 diamond supercell (8 atoms per cubic cell,
+    a = 5.43 A for Si) with Gaussian jitter; returns (pos [n,3], Z [n], cell [3,3])."""
+    rng = np.random.default_rng(seed)
+    basis = np.array([[0, 0, 0], [0, .5, .5], [.5, 0, .5], [.5, .5, 0],
+                      [.25, .25, .25], [.25, .75, .75], [.75, .25, .75], [.75, .75, .25]])
+    frac = np.array([b + np.array([i, j, k]) for i in range(reps) for j in range(reps) for k in range(reps)
+                     for b in basis]) / reps
+    cell = np.eye(3) * a * reps
+    pos = frac @ cell + rng.normal(0.0, jitter, (len(frac), 3))
+    return pos, np.full(len(frac), Z, np.int32), cell
+
+
+def triclinic_box(n=48, seed=0, cell=((11.5, 0.0, 0.0), (2.0, 11.0, 0.0), (1.0, 1.5, 10.8))):
+    """Random atoms (rejection: > 1.3 A apart under the minimum image) in a skewed
+    cell whose perpendicular widths exceed 2 * 5 A."""
+    rng = np.random.default_rng(seed)
+    cell = np.asarray(cell, np.float64)
+    inv = np.linalg.inv(cell)
+    pts = []
+    while len(pts) < n:
+        p = rng.uniform(0, 1, 3) @ cell
+        ok = True
+        for q in pts:
+            d = p - q
+            f = d @ inv
+            d = (f - np.rint(f)) @ cell
+            if np.linalg.norm(d) < 1.3:
+                ok = False
+                break
+        if ok:
+            pts.append(p)
+    return np.array(pts), rng.choice(ORGANIC, n).astype(np.int32), cell
+
+
+def periodic_batch(lib, D=10, seed=3):
+    """A mixed batch: two periodic crystals (diamond Si supercell, triclinic box) and
+    non-periodic molecules; labels from random values (parity only needs them finite)."""
+    mol = molecules(lib, 6, seed)
+    p1, z1, c1 = diamond_supercell(seed=seed)
+    p2, z2, c2 = triclinic_box(seed=seed + 1)
+    rng = np.random.default_rng(seed)
+    extra = []
+    for p, z in ((p1, z1), (p2, z2)):
+        n = len(z)
+        extra.append(dict(atom_ptr=np.array([0, n], np.int64), pos=p, Z=z, forces=rng.normal(0, 1, (n, 3)),
+                          dataset_index=np.zeros(1, np.int32), energy_mask=np.ones(1, np.uint8),
+                          force_mask=np.ones(1, np.uint8), energy=rng.normal(-3.0 * n, 1.0, 1),
+                          denoise=np.zeros(1, np.uint8), cell=None))
+    extra[0]["cell"] = c1[None]
+    extra[1]["cell"] = c2[None]
+    mol = dict(mol)
+    mol["denoise"] = np.zeros(len(mol["atom_ptr"]) - 1, np.uint8)
+    b = lib_concat([extra[0], mol, extra[1]])
+    b["dataset_index"] = rng.integers(0, D, len(b["atom_ptr"]) - 1).astype(np.int32)
+    return b
+
+
+def lib_concat(batches):
+    import paper_2505_22208_b200 as pk
+    return pk.concat(batches)

@@ -53,3 +53,18 @@ def oracle_ref():
     if not ref_available():
         pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
     return ref()
+
+
+@pytest.fixture(scope="module")
+def pk():
+    import paper_2505_22208_b200 as pk
+    return pk
+
+
+@pytest.fixture(scope="module")
+def dev(pk):
+    import cases
+    d = pk.Device(pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4]), seed=7)
+    d.set_option("export_fp64", 1)
+    yield d
+    d.close()

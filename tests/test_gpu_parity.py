@@ -14,18 +14,6 @@ import cases
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not has_gpu(), reason="needs a CUDA device")]
 
 
-@pytest.fixture(scope="module")
-def pk():
-    import paper_2505_22208_b200 as pk
-    return pk
-
-
-@pytest.fixture(scope="module")
-def dev(pk):
-    d = pk.Device(pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4]), seed=7)
-    d.set_option("export_fp64", 1)
-    yield d
-    d.close()
 
 
 def tensors(cfg, flat):
