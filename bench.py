@@ -302,6 +302,7 @@ def run_ours(args, dist):
     if dist.rank == 0 and dist.world == 1 and not args.no_imbalance:
         out["rank_imbalance"] = rank_imbalance(pk, dev, pool, table, tc)
         out["rank_imbalance_heavy_tail"] = rank_imbalance_heavy(pk, dev, tc)
+        out["periodic_cfg1"] = periodic_cfg1(pk, mcfg, tc)
     dev.close()
     return out
 
@@ -363,6 +364,37 @@ def rank_imbalance(pk, dev, pool, table, tc, G=8, steps=8):
                      "atoms_mean": float(np.mean(aratios)), "atoms_max": float(np.max(aratios)),
                      "steps": len(ratios)}
     return out
+
+
+def periodic_cfg1(pk, mcfg, tc, steps=20):
+    """BASELINE configs[0] on the GPU: 32 periodic 64-atom bulk cells (2x2x2 diamond
+    Si supercells, 0.05 A jitter, minimum image), full train step per batch;
+    a separate context so the headline run is untouched."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import cases
+    parts = []
+    for s in range(32):
+        pos, Z, cell = cases.diamond_supercell(seed=100 + s)
+        n = len(Z)
+        parts.append(dict(atom_ptr=np.array([0, n], np.int64), pos=pos, Z=Z, forces=np.zeros((n, 3)),
+                          dataset_index=np.zeros(1, np.int32), energy_mask=np.ones(1, np.uint8),
+                          force_mask=np.ones(1, np.uint8), energy=np.array([-4.6 * n]),
+                          denoise=np.zeros(1, np.uint8), cell=cell[None]))
+    batch = pk.concat(parts)
+    dev = pk.Device(mcfg, seed=7)
+    dev.stage(batch, tc, step=0, slot=0)
+    for _ in range(3):
+        dev.train_step_staged(0, sync=True)
+    dev.kernel_times_reset()
+    edges = 0
+    for _ in range(steps):
+        dev.flush_l2(L2_FLUSH)
+        edges = dev.train_step_staged(0, sync=True).n_edges
+    ms, n = dev.step_times()
+    dev.close()
+    atoms = int(batch["atom_ptr"][-1])
+    return {"workload": "cfg1: 32 periodic 64-atom Si diamond supercells (minimum image), train step",
+            "atoms_per_step": atoms, "edges_per_step": edges, "ms_per_step": ms / n, "atoms_per_s": atoms / (ms / n / 1e3)}
 
 
 def rank_imbalance_heavy(pk, dev, tc, G=8, B=4, S=64, steps=8):
