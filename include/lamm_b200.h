@@ -299,6 +299,26 @@ int lamm_synth_fill(int32_t task, int64_t count, double mode, double sigma, int3
                     uint64_t seed, int32_t threads, const int64_t* atom_ptr, double* positions,
                     int32_t* atomic_numbers, uint8_t* energy_mask, uint8_t* force_mask, double* energy,
                     double* forces);
+/* ------------------------------------------------------ on-disk formats --- */
+/* LAMMCKPT checkpoints, byte-compatible with lamm::model::save_checkpoint /
+ * load_checkpoint (H/model.hpp:131-139, S/model.cpp:429-497): params flat in
+ * for_each_tensor order. load with params == NULL returns the config and the
+ * parameter count only. */
+int lamm_checkpoint_save(const char* path, const lamm_model_config* cfg, const double* params, size_t n);
+int lamm_checkpoint_load(const char* path, lamm_model_config* cfg, double* params, size_t cap, size_t* n_out);
+/* The RMS optimizer state v in the same layout (magic "LAMMRMS1"; the reference
+ * keeps it in memory only), for bit-exact resumption. */
+int lamm_rms_state_save(const char* path, const lamm_model_config* cfg, const double* v, size_t n);
+int lamm_rms_state_load(const char* path, lamm_model_config* cfg, double* v, size_t cap, size_t* n_out);
+/* LAMMDS1 catalog subsets (S/dataset.cpp:273-330) read straight into the packed
+ * batch layout of lamm_batch_view: info gives the sample and atom counts to size
+ * the arrays (atom_ptr[count+1], positions[3N], Z[N], per-sample masks/energy,
+ * forces[3N]); dataset_index is set to head_index (read_catalog). */
+int lamm_subset_info(const char* path, int64_t* count, int64_t* total_atoms);
+int lamm_subset_read(const char* path, int32_t head_index, int64_t* atom_ptr, double* positions,
+                     int32_t* atomic_numbers, int32_t* dataset_index, uint8_t* energy_mask, uint8_t* force_mask,
+                     double* energy, double* forces);
+
 /* Inverse of a 3x3 cell (row-major, rows = lattice vectors) by cofactors: the
  * exact bits the minimum-image test uses. Returns LAMM_EINPUT if singular. */
 int lamm_cell_inverse(const double* cell, double* out);

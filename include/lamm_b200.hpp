@@ -19,6 +19,7 @@
 //   lamm::model::init_params           H/model.hpp:75         -> init_params(params&, cfg, seed)
 //   run_loop step body (file-local)    S/trainer.cpp:258-327  -> train_step(dev, samples, denoise, cfg, step, G, rank)
 //   lamm::trainer::evaluate            H/trainer.hpp:143-144  -> evaluate<EvalResult>(dev, cfg, params, refs, samples)
+//   lamm::model::save/load_checkpoint  H/model.hpp:131-139    -> save_checkpoint(path, cfg, params), load_checkpoint
 //
 // Batched variants (forward_batch, build_neighbor_lists) take a span of
 // systems and run them as one device-batch; the per-sample forms are the
@@ -546,6 +547,36 @@ EvalResult evaluate(Device& dev, const ModelConfig& cfg, const Params& params, c
     dev.set_params_from(params);
     dev.set_reference_table(refs);
     return evaluate<EvalResult>(dev, samples);
+}
+
+// ------------------------------------------------------------ checkpoints ----
+// lamm::model::save_checkpoint / load_checkpoint (H/model.hpp:131-139): the same
+// LAMMCKPT bytes. Checkpoint = {config, params} like the reference's struct; the
+// params object must come shaped (e.g. init_params of the config, or the
+// reference's own load) - unflatten checks the size.
+template <class ModelConfig, class Params>
+void save_checkpoint(const std::string& path, const ModelConfig& cfg, const Params& params) {
+    const lamm_model_config c = to_c(cfg);
+    const std::vector<double> flat = flatten(params);
+    check(lamm_checkpoint_save(path.c_str(), &c, flat.data(), flat.size()));
+}
+
+// Reads a checkpoint into caller-shaped params; returns its config.
+template <class ModelConfig, class Params>
+ModelConfig load_checkpoint(const std::string& path, Params& params) {
+    lamm_model_config c{};
+    size_t n = 0;
+    check(lamm_checkpoint_load(path.c_str(), &c, nullptr, 0, &n));
+    std::vector<double> flat(n);
+    check(lamm_checkpoint_load(path.c_str(), &c, flat.data(), flat.size(), &n));
+    unflatten(flat, params);
+    ModelConfig out{};
+    out.hidden = c.hidden;
+    out.layers = c.layers;
+    out.rbf = c.rbf;
+    out.heads = c.heads;
+    out.cutoff = c.cutoff;
+    return out;
 }
 
 // ------------------------------------------------------------- scheduler -----

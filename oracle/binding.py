@@ -93,6 +93,50 @@ class OracleLib:
         finally:
             self.lib.lor_set_cells(None, None)
 
+    def _samples_from_handle(self, h):
+        cnt, tot = _i64(), _i64()
+        self.lib.lref_samples_info(_P(h), C.byref(cnt), C.byref(tot))
+        B, N = cnt.value, tot.value
+        b = dict(atom_ptr=np.empty(B + 1, np.int64), pos=np.empty((N, 3)), Z=np.empty(N, np.int32),
+                 energy_mask=np.empty(B, np.uint8), force_mask=np.empty(B, np.uint8), energy=np.empty(B),
+                 forces=np.empty((N, 3)))
+        self.lib.lref_samples_copy(_P(h), _p(b["atom_ptr"]), _p(b["pos"]), _p(b["Z"]), _p(b["energy_mask"]),
+                                   _p(b["force_mask"]), _p(b["energy"]), _p(b["forces"]))
+        return b
+
+    # ------------------------------------------------- on-disk formats (ref)
+    def write_demo_catalog(self, directory, count, seed):
+        self._check(self.lib.lref_write_demo_catalog(os.fsencode(directory), _i64(count), _u64(seed)))
+
+    def read_catalog(self, directory):
+        """lamm::dataset::read_catalog, every subset concatenated: (batch, subset sizes)."""
+        self.lib.lref_read_catalog.restype = _P
+        ns = C.c_int32()
+        sizes = np.zeros(64, np.int64)
+        h = self.lib.lref_read_catalog(os.fsencode(directory), C.byref(ns), _p(sizes))
+        if not h:
+            raise OracleError(self._f("last_error")().decode())
+        try:
+            b = self._samples_from_handle(h)
+            b["dataset_index"] = np.empty(len(b["atom_ptr"]) - 1, np.int32)
+            self.lib.lref_samples_heads(_P(h), _p(b["dataset_index"]))
+        finally:
+            self.lib.lref_samples_free(_P(h))
+        return b, sizes[:ns.value]
+
+    def checkpoint_save(self, path, cfg, params):
+        H, L, K, rc, D = cfg
+        self._check(self.lib.lref_checkpoint_save(os.fsencode(path), H, L, K, _f64(rc), D,
+                                                  _p(_c(params, np.float64))))
+
+    def checkpoint_load(self, path, cap=10_000_000):
+        c = np.zeros(4, np.int32)
+        rc = C.c_double()
+        out = np.empty(cap, np.float64)
+        self._check(self.lib.lref_checkpoint_load(os.fsencode(path), _p(c), C.byref(rc), _p(out), _i64(cap)))
+        H, L, K, D = (int(x) for x in c)
+        return (H, L, K, rc.value, D), out[:self.param_count((H, L, K, rc.value, D))]
+
     # ---------------------------------------------------------------- rng
     def mix_seed(self, a, b):
         return int(self._f("mix_seed")(_u64(a), _u64(b)))

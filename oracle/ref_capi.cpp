@@ -654,3 +654,63 @@ LREF_API void lref_samples_copy(void* h, int64_t* atom_ptr, double* pos, int32_t
 }
 
 LREF_API void lref_samples_free(void* h) { delete static_cast<SamplesHandle*>(h); }
+
+// ---- on-disk formats (S/dataset.cpp:273-393, S/model.cpp:429-497) -----------
+/// synth_catalog of three small subsets (energy+forces, energy-only, denoising)
+/// written with write_catalog into dir.
+LREF_API int lref_write_demo_catalog(const char* dir, int64_t count, uint64_t seed) {
+    return guarded([&] {
+        std::vector<lamm::dataset::SynthSpec> specs(3);
+        const char* names[3] = {"ef", "energy", "denoise"};
+        for (int k = 0; k < 3; ++k) {
+            specs[k].name = names[k];
+            specs[k].task = static_cast<lamm::dataset::TaskKind>(k);
+            specs[k].count = count;
+            specs[k].atom_count_mode = 10.0 + 5.0 * k;
+            specs[k].min_atoms = 2;
+            specs[k].max_atoms = 40;
+            specs[k].elements = {1, 6, 7, 8};
+        }
+        lamm::dataset::write_catalog(dir, lamm::dataset::synth_catalog(specs, seed));
+    });
+}
+
+/// read_catalog: every subset's samples concatenated (dataset_index = head_index).
+LREF_API void* lref_read_catalog(const char* dir, int32_t* n_subsets, int64_t* subset_sizes) {
+    SamplesHandle* h = nullptr;
+    guarded([&] {
+        const auto cat = lamm::dataset::read_catalog(dir);
+        auto hp = std::make_unique<SamplesHandle>();
+        *n_subsets = static_cast<int32_t>(cat.subsets.size());
+        for (std::size_t k = 0; k < cat.subsets.size(); ++k) {
+            subset_sizes[k] = static_cast<int64_t>(cat.subsets[k].samples.size());
+            for (const auto& smp : cat.subsets[k].samples) hp->v.push_back(smp);
+        }
+        h = hp.release();
+    });
+    return h;
+}
+
+LREF_API void lref_samples_heads(void* h, int32_t* dataset_index) {
+    auto* p = static_cast<SamplesHandle*>(h);
+    for (std::size_t s = 0; s < p->v.size(); ++s) dataset_index[s] = p->v[s].labels.dataset_index;
+}
+
+LREF_API int lref_checkpoint_save(const char* path, int H, int L, int K, double rc, int D, const double* params) {
+    return guarded([&] {
+        const auto cfg = make_cfg(H, L, K, rc, D);
+        lamm::model::save_checkpoint(path, cfg, params_from_flat(cfg, params));
+    });
+}
+
+/// load_checkpoint; cfg_out = {H, L, K, D} and rc, params (capacity from param_count).
+LREF_API int lref_checkpoint_load(const char* path, int32_t* cfg_out, double* rc, double* params, int64_t cap) {
+    return guarded([&] {
+        const auto ck = lamm::model::load_checkpoint(path);
+        cfg_out[0] = ck.config.hidden, cfg_out[1] = ck.config.layers, cfg_out[2] = ck.config.rbf;
+        cfg_out[3] = ck.config.heads;
+        *rc = ck.config.cutoff;
+        if (static_cast<int64_t>(lamm::model::param_count(ck.params)) > cap) throw lamm::InputError("capacity");
+        params_to_flat(ck.params, params);
+    });
+}

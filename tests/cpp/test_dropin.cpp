@@ -289,6 +289,18 @@ void check_evaluate(const std::vector<lamm::Sample>& samples, const lamm::model:
            "trainer::evaluate MAEs and counts", fmt(std::max(re, rf)));
 }
 
+void check_checkpoint(const lamm::model::ModelConfig& cfg, const lamm::model::ModelParams& params) {
+    const std::string ours = "/tmp/lamm_b200_dropin_ours.ckpt", theirs = "/tmp/lamm_b200_dropin_ref.ckpt";
+    lamm_b200::save_checkpoint(ours, cfg, params);
+    lamm::model::save_checkpoint(theirs, cfg, params);
+    const auto ref = lamm::model::load_checkpoint(ours);  // the reference reads ours
+    auto mine = lamm::model::zero_like(params);
+    const auto c = lamm_b200::load_checkpoint<lamm::model::ModelConfig>(theirs, mine);  // ours reads theirs
+    report(ref.params == params && mine == params && c.hidden == cfg.hidden && c.heads == cfg.heads &&
+               c.cutoff == cfg.cutoff,
+           "LAMMCKPT save/load both ways, bit-exact");
+}
+
 }  // namespace
 
 int main() {
@@ -306,6 +318,7 @@ int main() {
         check_scheduler();
         check_train_step(samples, cfg, params, table);
         check_evaluate(samples, cfg, params, table);
+        check_checkpoint(cfg, params);
         bool threw = false;
         try {
             lamm::model::ModelConfig bad = cfg;
