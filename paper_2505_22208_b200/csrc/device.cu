@@ -508,7 +508,7 @@ struct Model {
             launch(c, "update", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 0);
         }
         launch(c, "force", k_edge_force<H, K>, c.grid_edge, kGroups * H, smem_force(c.D), d);
-        launch(c, "force_out", k_force_out<H, K>, c.grid_warp, 256, 0, d);
+        launch(c, "force_out", k_force_out<H, K>, c.grid_warp, 256, 0, d, energy ? 0 : 1);
         if (energy) launch(c, "energy", k_energy, c.grid_small, 128, sizeof(double) * 128 * c.D, d);
     }
 

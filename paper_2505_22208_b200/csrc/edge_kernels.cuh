@@ -512,8 +512,10 @@ __device__ __forceinline__ void force_out_round(const float* WaT, const float* W
     if (R0 + lane < ND) out[R0 + lane] = v[0];
 }
 
+// own_head: the train step reads only each atom's own head (its sample's
+// dataset index) from F, so only those three components are formed.
 template <int H, int K>
-__global__ void __launch_bounds__(256) k_force_out(Dev d) {
+__global__ void __launch_bounds__(256) k_force_out(Dev d, int own_head) {
     constexpr int C = H / 32, YW = ForceBody<H, K>::kYW;
     __shared__ __align__(16) float WaT[kMaxHeads * H], WbT[kMaxHeads * H], WcT[kMaxHeads * 32];
     const int D = d.D, ND = 3 * D, L = d.L;
@@ -547,6 +549,27 @@ __global__ void __launch_bounds__(256) k_force_out(Dev d) {
         float vk[3] = {0.f, 0.f, 0.f};
         if (lane < K) vk[0] = y[3 * H + 3 + lane], vk[1] = y[3 * H + 3 + K + lane], vk[2] = y[3 * H + 3 + 2 * K + lane];
         float* out = d.F + static_cast<int64_t>(i) * ND;
+        if (own_head) {
+            const int dd = d.chan[i];
+            const VecF<C> wa = ldv<C>(WaT + dd * H + lane * C);
+            const VecF<C> wb = ldv<C>(WbT + dd * H + lane * C);
+            const float wc = lane < K ? WcT[dd * 32 + lane] : 0.f;
+            float sx[3];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                float acc = 0.f;
+#pragma unroll
+                for (int cc = 0; cc < C; ++cc) {
+                    acc = fmaf(wa.v[cc], fmaf(ti[cc], u[x], yv[x][cc]), acc);
+                    acc = fmaf(wb.v[cc], ti[cc] * yv[x][cc], acc);
+                }
+                sx[x] = fmaf(wc, vk[x], acc);
+            }
+#pragma unroll
+            for (int x = 0; x < 3; ++x) sx[x] = warp_sum(sx[x]);
+            if (lane < 3) out[dd * 3 + lane] = lane == 0 ? sx[0] : (lane == 1 ? sx[1] : sx[2]);
+            continue;
+        }
         force_out_round<H, K, 0>(WaT, WbT, WcT, D, ND, lane, ti, yv, u, vk, out);
         if (ND > 32) force_out_round<H, K, 32>(WaT, WbT, WcT, D, ND, lane, ti, yv, u, vk, out);
     }

@@ -367,6 +367,32 @@ __device__ __forceinline__ void sample_energy(const Dev& d, int s, double* red) 
     __syncthreads();
 }
 
+// The train step's loss reads only the sample's own head: E_s^{d_s} alone.
+__device__ __forceinline__ void sample_energy_own(const Dev& d, int s, int ds, double* red) {
+    const int D = d.D, H = d.H;
+    const int64_t lo = d.atom_ptr[s], hi = d.atom_ptr[s + 1];
+    const float* __restrict__ hL = d.h[d.L];
+    double acc = 0.0;
+    const int a = threadIdx.x;
+    if (a < H) {
+        const double w = static_cast<double>(d.we[a * D + ds]);
+        for (int64_t i0 = lo; i0 < hi; i0 += 8) {
+            float hv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) hv[u] = i0 + u < hi ? __ldg(hL + (i0 + u) * H + a) : 0.f;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = fma(static_cast<double>(hv[u]), w, acc);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) d.Epred[static_cast<int64_t>(s) * D + ds] = ((red[0] + red[1]) + red[2]) + red[3];
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(128) k_energy(Dev d) {
     pdl_enter();
     double* red = dyn_smem<double>();  // [D][128]
@@ -391,9 +417,9 @@ __global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy, int full_g
     const double we = me > 0 ? d.hdr->lambda_e / static_cast<double>(me) : 0.0;
     const double wf = mf > 0 ? d.hdr->lambda_f / static_cast<double>(mf) : 0.0;
     for (int s = blockIdx.x; s < B; s += gridDim.x) {
-        if (with_energy) sample_energy(d, s, ered);
-        const int64_t lo = d.atom_ptr[s], hi = d.atom_ptr[s + 1];
         const int ds = d.dsidx[s];
+        if (with_energy) sample_energy_own(d, s, ds, ered);
+        const int64_t lo = d.atom_ptr[s], hi = d.atom_ptr[s + 1];
         const bool em = d.emask[s], fm = d.fmask[s];
         const double ws = wf / static_cast<double>(hi - lo);
         double fsum = 0.0;
