@@ -223,6 +223,16 @@ int lamm_comm_init(lamm_ctx* ctx, int nranks, int rank, const void* unique_id128
 int lamm_train_step(lamm_ctx* ctx, const lamm_batch_view* batch, const lamm_train_config* cfg, int64_t step,
                     int32_t workers, int32_t rank, lamm_step_result* result);
 
+/* The same step for `workers` SIMULATED workers on this one device, the
+ * reference's own semantics (S/trainer.cpp:262-319): batches[g] holds worker
+ * g's B samples; each worker's denoise -> forward -> masked loss -> backward
+ * runs in worker order, the gradients and loss terms are summed in fp64, then
+ * /G -> norm -> clip -> RMS step. result->n_atoms/n_edges are totals over the
+ * workers, result->local is the last worker's breakdown. Needs a context
+ * without a communicator. */
+int lamm_train_step_workers(lamm_ctx* ctx, const lamm_batch_view* batches, int32_t workers,
+                            const lamm_train_config* cfg, int64_t step, lamm_step_result* result);
+
 /* Device-resident staging for throughput runs: packs a device-batch exactly as
  * lamm_train_step would (denoise draws for `step`, `rank`) into HBM slot
  * `slot` (0..1023); lamm_train_step_staged then runs the same step from that

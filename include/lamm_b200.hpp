@@ -18,6 +18,7 @@
 //   lamm::scheduler::plan              H/scheduler.hpp:74     -> plan<Schedule>(atoms, cfg)
 //   lamm::model::init_params           H/model.hpp:75         -> init_params(params&, cfg, seed)
 //   run_loop step body (file-local)    S/trainer.cpp:258-327  -> train_step(dev, samples, denoise, cfg, step, G, rank)
+//                                                                train_step_workers(dev, samples, denoise, cfg, step, G)
 //   lamm::trainer::evaluate            H/trainer.hpp:143-144  -> evaluate<EvalResult>(dev, cfg, params, refs, samples)
 //   lamm::model::save/load_checkpoint  H/model.hpp:131-139    -> save_checkpoint(path, cfg, params), load_checkpoint
 //
@@ -514,6 +515,35 @@ StepResult train_step(Device& dev, std::span<const Sample> samples, std::span<co
     lamm_step_result r{};
     const int st = lamm_train_step(dev.get(), &v, &c, step, workers, rank, &r);
     dev.params_changed_on_device();
+    check(st);
+    return StepResult{r.loss, r.grad_norm, r.local, r.n_atoms, r.n_edges};
+}
+
+// The step of S/trainer.cpp:258-327 for all G workers SIMULATED on this one
+// device, in worker order: `samples` is the whole MiniBatch (G*B, worker-major),
+// denoise[k] marks samples of denoising subsets (empty: none).
+template <class Sample, class TrainConfig>
+StepResult train_step_workers(Device& dev, std::span<const Sample> samples, std::span<const uint8_t> denoise,
+                              const TrainConfig& tcfg, int64_t step, int workers) {
+    if (workers < 1 || samples.size() % static_cast<size_t>(workers) != 0)
+        throw InputError("train_step_workers: samples must split into `workers` equal device-batches");
+    if (!denoise.empty() && denoise.size() != samples.size())
+        throw InputError("train_step_workers: one denoise flag per sample");
+    const size_t B = samples.size() / static_cast<size_t>(workers);
+    std::vector<PackedBatch> packs(static_cast<size_t>(workers));
+    std::vector<lamm_batch_view> views;
+    for (int g = 0; g < workers; ++g) {
+        for (size_t b = 0; b < B; ++b) {
+            const size_t k = static_cast<size_t>(g) * B + b;
+            packs[static_cast<size_t>(g)].add_sample(samples[k], !denoise.empty() && denoise[k] != 0);
+        }
+    }
+    for (auto& p : packs) views.push_back(p.view());
+    const lamm_train_config c = train_config_to_c(tcfg);
+    lamm_step_result r{};
+    const int st = lamm_train_step_workers(dev.get(), views.data(), workers, &c, step, &r);
+    dev.params_changed_on_device();
+    if (st == LAMM_OK || st == LAMM_ENONFINITE) dev.batch_replaced(packs.back().atom_ptr);
     check(st);
     return StepResult{r.loss, r.grad_norm, r.local, r.n_atoms, r.n_edges};
 }

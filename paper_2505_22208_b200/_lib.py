@@ -83,7 +83,7 @@ EXPORTS = [
     "lamm_mix_seed", "lamm_rng_normals", "lamm_stage", "lamm_train_step_staged", "lamm_anomalies",
     "lamm_flush_l2", "lamm_step_times", "lamm_evaluate", "lamm_cell_inverse",
     "lamm_checkpoint_save", "lamm_checkpoint_load", "lamm_rms_state_save", "lamm_rms_state_load",
-    "lamm_subset_info", "lamm_subset_read",
+    "lamm_subset_info", "lamm_subset_read", "lamm_train_step_workers",
 ]
 
 _lib = None

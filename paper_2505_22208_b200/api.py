@@ -295,6 +295,26 @@ class Device:
         return StepResult(res.loss, res.grad_norm, _breakdown(res.local), res.n_atoms, res.n_edges, res.status,
                           res.h2d_bytes, res.d2h_bytes)
 
+    def train_step_workers(self, batches, tcfg: TrainConfig, step: int) -> StepResult:
+        """One optimizer step over G SIMULATED workers on this device
+        (S/trainer.cpp:262-319): ``batches[g]`` is worker g's device-batch."""
+        G = len(batches)
+        views = (BatchViewC * G)()
+        keeps = []
+        for g, b in enumerate(batches):
+            v, keep = _batch_view(b)
+            views[g] = v
+            keeps.append(keep)
+        res = StepResultC()
+        tc = tcfg.c()
+        st = lib().lamm_train_step_workers(self._h, views, G, C.byref(tc), C.c_int64(step), C.byref(res))
+        self._keep = keeps[-1]
+        self.B = len(keeps[-1]["atom_ptr"]) - 1
+        self.N = int(keeps[-1]["atom_ptr"][-1])
+        check(st)
+        return StepResult(res.loss, res.grad_norm, _breakdown(res.local), res.n_atoms, res.n_edges, res.status,
+                          res.h2d_bytes, res.d2h_bytes)
+
     def stage(self, batch: dict, tcfg: TrainConfig, step: int, slot: int, workers: int = 1, rank: int = 0) -> int:
         """Packs a device-batch into HBM slot ``slot`` (inputs resident for timing);
         returns the staged blob size in bytes."""

@@ -170,7 +170,7 @@ void alloc_param_state(Ctx& c) {
     };
     mk(c.p64, sizeof(double) * c.NP);
     mk(c.v64, sizeof(double) * c.NP);
-    mk(c.g64, sizeof(double) * c.NP);
+    mk(c.g64, sizeof(double) * (c.NP + 4));
     mk(c.p32, sizeof(float) * c.NP);
     mk(c.tanh_emb, sizeof(float) * kMaxZ * c.H);
     mk(c.grads, sizeof(float) * (c.NP + 4));
@@ -316,6 +316,8 @@ Dev make_dev(Ctx& c) {
     d.p64 = c.p64.as<double>();
     d.v64 = c.v64.as<double>();
     d.g64_in = nullptr;
+    d.g64_loss = 0;
+    d.g64_acc = c.g64.as<double>();
     d.p32 = c.p32.as<float>();
     d.NP = c.NP;
     d.emb_rows = kMaxZ;
@@ -837,6 +839,35 @@ StepHeader run_train_step(Ctx& c, const void* src, size_t bytes, cudaMemcpyKind 
         }
         require(attempt < 4, "edge capacity regrowth did not converge");
         ensure_capacity(c, c.N, c.B, h.overflow ? h.P : 0);
+    }
+}
+
+// Upload + step graph without the optimizer (one simulated worker); regrows
+// the edge capacity and reruns on overflow. Returns the header after the pass.
+StepHeader run_pass(Ctx& c, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    for (int attempt = 0;; ++attempt) {
+        ensure_capacity(c, c.N, c.B, edge_guess(c.N));
+        if (bytes > c.d_stage.bytes) ensure_stage(c, bytes);
+        CK(cudaMemcpyAsync(c.d_stage.p, src, bytes, kind, c.stream));
+        if (c.use_graph) {
+            if (c.graph_dirty || !c.g_step) {
+                destroy_graphs(c);
+                c.slot_cursor = 0;
+                const int64_t l0 = c.launches;
+                c.g_step = capture(c, step_body);
+                c.g_opt = capture(c, opt_body);
+                c.graph_dirty = false;
+                c.graph_launches = c.launches - l0;
+            }
+            CK(cudaGraphLaunch(c.g_step, c.stream));
+        } else {
+            c.slot_cursor = 0;
+            step_body(c);
+        }
+        const StepHeader h = read_header(c);
+        if (!h.overflow) return h;
+        require(attempt < 4, "edge capacity regrowth did not converge");
+        ensure_capacity(c, c.N, c.B, h.P);
     }
 }
 
@@ -1410,6 +1441,38 @@ LAMM_API int lamm_train_step(lamm_ctx* c, const lamm_batch_view* b, const lamm_t
         const StepHeader h = run_train_step(*c, c->h_stage, bytes, cudaMemcpyHostToDevice);
         c->last_h2d = static_cast<int64_t>(bytes);
         fill_result(*c, h, res);
+        if (h.status == 1)
+            throw NonFinite("non-finite loss or gradient at step " + std::to_string(step));
+    });
+}
+
+LAMM_API int lamm_train_step_workers(lamm_ctx* c, const lamm_batch_view* batches, int32_t workers,
+                                     const lamm_train_config* tc, int64_t step, lamm_step_result* res) {
+    return lamm_guard([&] {
+        require(c && batches && tc, "train_step_workers: null argument");
+        require(workers >= 1, "train_step_workers: workers must be >= 1");
+        require(c->nranks == 1, "train_step_workers: simulated workers need a context without a communicator");
+        CK(cudaSetDevice(c->device));
+        int64_t atoms = 0, edges = 0;
+        for (int32_t g = 0; g < workers; ++g) {  // worker order, like S/trainer.cpp:262
+            validate_batch(*c, &batches[g]);
+            apply_train_config(*c, tc, workers, g);
+            const size_t bytes = pack_batch(*c, &batches[g], true, tc, step, g);
+            const StepHeader h = run_pass(*c, c->h_stage, bytes, cudaMemcpyHostToDevice);
+            atoms += c->N, edges += h.P;
+            launch(*c, "grad_accum", k_grad_accum, c->grid_small, 256, 0, make_dev(*c), g == 0 ? 1 : 0);
+        }
+        Dev d = make_dev(*c);
+        d.g64_in = c->g64.as<double>();
+        d.g64_loss = 1;
+        c->ops->opt(*c, d, workers, 1.0 / static_cast<double>(workers), tc->clip_norm, tc->learning_rate,
+                    tc->rms_decay, tc->rms_epsilon);
+        const StepHeader h = read_header(*c);
+        c->batch_valid = c->nlist_valid = true;  // the last worker's batch stays current
+        c->fwd_valid = c->loss_valid = false;    // its parameters changed
+        c->last_h2d = 0;
+        fill_result(*c, h, res);
+        if (res) res->n_atoms = atoms, res->n_edges = edges;
         if (h.status == 1)
             throw NonFinite("non-finite loss or gradient at step " + std::to_string(step));
     });

@@ -116,6 +116,8 @@ struct Dev {
     // fp64 master state
     double *p64, *v64;
     const double* g64_in;    // optional fp64 gradient input for the optimizer
+    int g64_loss;            // g64_in carries the loss terms at [NP], [NP + 1] (simulated workers)
+    double* g64_acc;         // fp64 worker-gradient accumulator [NP + 4]
     float* p32;              // [NP] fp32 working copy (emb/wf/wu/... point into it)
     float* tanh_emb_w;       // writable alias of tanh_emb
     int64_t NP;

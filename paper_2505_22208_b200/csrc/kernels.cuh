@@ -717,6 +717,8 @@ __device__ __forceinline__ int opt_update(const Dev& d, int G, double inv_g, dou
     double loss = 0.0;
     if (!d.g64_in)
         loss = (static_cast<double>(d.grads[d.NP]) + static_cast<double>(d.grads[d.NP + 1])) / static_cast<double>(G);
+    else if (d.g64_loss)
+        loss = (d.g64_in[d.NP] + d.g64_in[d.NP + 1]) / static_cast<double>(G);
     const bool overflow = !d.g64_in && d.grads[d.NP + 2] > 0.f;
     const int status = overflow ? 2 : ((!isfinite(loss) || !isfinite(gn)) ? 1 : 0);
     const double cs = (clip > 0.0 && gn > clip) ? clip / gn : 0.0;
@@ -743,6 +745,18 @@ __device__ __forceinline__ int opt_update(const Dev& d, int G, double inv_g, dou
         on_param(e, pf);
     }
     return status;
+}
+
+// Simulated workers on one device (S/trainer.cpp:262-319: G device-batches in
+// worker order, gradients summed before one optimizer step): worker g's packed
+// gradient and loss terms added to the fp64 accumulator in worker order.
+__global__ void __launch_bounds__(256) k_grad_accum(Dev d, int first) {
+    pdl_enter();
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < d.NP + 2;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double v = static_cast<double>(d.grads[e]);
+        d.g64_acc[e] = first ? v : d.g64_acc[e] + v;
+    }
 }
 
 // fp64 master -> fp32 working copy (+ tanh(E)) after a host parameter upload.

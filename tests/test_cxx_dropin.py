@@ -34,3 +34,20 @@ def test_cxx_dropin_with_reference_types():
     assert r.returncode == 0, r.stdout + r.stderr
     assert "FAIL" not in r.stdout
     assert r.stdout.count("PASS") >= 20
+
+
+TRAINER_BIN = os.path.join(ROOT, "oracle", "_ref", "test_trainer")
+
+
+@pytest.mark.gpu
+def test_cxx_trainer_orchestration_matches_reference():
+    """include/lamm_b200_trainer.hpp: pretrain / finetune / denoise_bench with the
+    device step vs the reference's own trainer on the same catalog and seeds."""
+    if not os.path.exists(TRAINER_BIN):
+        pytest.skip("oracle/_ref/test_trainer not built (needs /root/reference at build time)")
+    r = subprocess.run([TRAINER_BIN], capture_output=True, text=True, timeout=900,
+                       env={**os.environ, "LAMM_THREADS": os.environ.get("LAMM_THREADS", "8")})
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "FAIL" not in r.stdout
+    assert r.stdout.count("PASS") >= 20

@@ -246,6 +246,40 @@ def test_multi_worker_sum_semantics(pk, oracle_ref):
     assert rel_err(gsum / G, ref["grads"])[0] < TOL
 
 
+def test_simulated_workers_step_matches_reference(pk, oracle_ref):
+    """lamm_train_step_workers: G simulated workers in worker order on one device,
+    fp64 gradient sum, one optimizer step == the reference's step (S/trainer.cpp:262-326),
+    denoising draws at positions g*B + b included."""
+    G, B = 3, 6
+    mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
+    params = oracle_ref.init_params(cases.CFG, 8)
+    batch = cases.mixed_batch(pk, D=cases.CFG[4], seed=31, count=G * B)
+    table = cases.random_table(cases.CFG[4], seed=6)
+    tc = _train_cfg(pk, clip_norm=1e9)
+    v0 = np.zeros_like(params)
+    ref = oracle_ref.train_step(cases.CFG, G, B, batch, table, params, v0, seed=tc.seed, step=4,
+                                clip=tc.clip_norm)
+    dev = pk.Device(mcfg, seed=0)
+    dev.set_params(params)
+    dev.set_rms_state(v0)
+    dev.set_reference_table(table)
+    shards = [pk.select(batch, np.arange(g * B, (g + 1) * B)) for g in range(G)]
+    res = dev.train_step_workers(shards, tc, step=4)
+    assert res.n_atoms == int(batch["atom_ptr"][-1])
+    assert abs(res.loss - ref["loss"]) <= TOL * abs(ref["loss"])
+    assert abs(res.grad_norm - ref["grad_norm"]) <= TOL * ref["grad_norm"]
+    assert_close(dev.rms_state(), ref["rms_v"], tol=3 * TOL, what="rms v after the G-worker step")
+    # a second step continues from the device state (graph reuse, accumulator reset)
+    ref2 = oracle_ref.train_step(cases.CFG, G, B, batch, table, ref["params"], ref["rms_v"], seed=tc.seed, step=5,
+                                 clip=tc.clip_norm)
+    dev.set_params(ref["params"])
+    dev.set_rms_state(ref["rms_v"])
+    res2 = dev.train_step_workers(shards, tc, step=5)
+    assert abs(res2.loss - ref2["loss"]) <= TOL * abs(ref2["loss"])
+    assert abs(res2.grad_norm - ref2["grad_norm"]) <= TOL * ref2["grad_norm"]
+    dev.close()
+
+
 def test_nccl_allreduce_path_single_rank(pk):
     """The data-parallel path (NCCL communicator, allreduce between the two graph
     halves) on one rank: identical to the communicator-free step, bit for bit."""
