@@ -410,10 +410,11 @@ def rank_imbalance_heavy(pk, dev, tc, G=8, B=4, S=64, steps=8):
     out["pool_atoms_mean"], out["pool_atoms_max"] = float(atoms.mean()), int(atoms.max())
     table = fit_table(pool, CFG["heads"])
     dev.set_reference_table(table)
+    samples = []  # (rank atoms, device ms) for the simulator's cost-model fit
     for mode in ("balanced", "naive"):
         sched = pk.plan(atoms, G, B, 4, seed=7, mode=mode)
         per = G * B
-        ratios, aratios = [], []
+        ratios, aratios, pred = [], [], []
         for s in range(min(steps, sched["n_batches"])):
             ids = sched["sample"][s * per:(s + 1) * per]
             times = []
@@ -431,9 +432,22 @@ def rank_imbalance_heavy(pk, dev, tc, G=8, B=4, S=64, steps=8):
             ratios.append(max(times) / np.mean(times))
             wa = sched["worker_atoms"][s * G:(s + 1) * G]
             aratios.append(wa.max() / wa.mean())
+            samples += list(zip(wa.tolist(), times))
+            pred.append(wa)
         out[mode] = {"time_mean": float(np.mean(ratios)), "time_p95": float(np.percentile(ratios, 95)),
                      "atoms_mean": float(np.mean(aratios)), "atoms_max": float(np.max(aratios)),
-                     "steps": len(ratios)}
+                     "steps": len(ratios), "_worker_atoms": pred}
+    # the reference's step-time simulator (S/simulator.cpp:19-59: per worker
+    # alpha + beta * atoms, step = slowest worker) with alpha/beta fitted to these
+    # B200 per-rank times: predicted vs measured max/mean per step
+    a, t = np.array([x[0] for x in samples], float), np.array([x[1] for x in samples], float)
+    beta, alpha = np.polyfit(a, t, 1)
+    sim = {"alpha_ms": float(alpha), "beta_us_per_atom": float(beta * 1e3),
+           "fit_r2": float(1 - np.sum((t - alpha - beta * a) ** 2) / np.sum((t - t.mean()) ** 2))}
+    for mode in ("balanced", "naive"):
+        p = [(alpha + beta * wa).max() / (alpha + beta * wa).mean() for wa in out[mode].pop("_worker_atoms")]
+        sim[mode] = {"predicted_time_mean": float(np.mean(p)), "measured_time_mean": out[mode]["time_mean"]}
+    out["simulator_cross_check"] = sim
     trace = pk.make_trace("lognormal", count=1_000_000, min_atoms=2, max_atoms=2000, mode=20.0, sigma=1.0, seed=3)
     sched_1m = {}
     for g in (2, 4, 8):
