@@ -11,6 +11,9 @@
         utilisation and pipe activity of every kernel in an `ncu --set full`
         capture; with the step's atoms N and edges P, the algorithmic bytes of
         the edge kernels (bench.kernel_bytes) next to the measured DRAM bytes.
+    python profiles/summarize.py traffic <capture.ncu-rep> <out.json> N P slot
+        DRAM bytes per launch of each edge kernel in the capture and their ratio
+        to the algorithmic bytes (bench.py reads roofline.traffic from it).
 """
 import collections
 import csv
@@ -134,8 +137,39 @@ def full(path, out, N=None, P=None):
     open(out, "w").write("\n".join(lines) + "\n")
 
 
+def traffic(path, out, N, P, slot):
+    import json
+    import bench
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--metrics",
+                          "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True,
+                         check=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr, units, data = rows[0], rows[1], rows[2:]
+    kn, rd, wr = hdr.index("Kernel Name"), hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    short = {"k_edge_message": "message", "k_edge_force": "force", "k_edge_head": "head_bwd", "k_edge_bwd": "bwd_edge"}
+    acc = collections.OrderedDict()
+    for r in data:
+        name = short.get(r[kn].split("<")[0].split("(")[0].strip().split(" ")[-1])
+        if name is None:
+            continue
+        b = float(r[rd].replace(",", "")) * scale[units[rd]] + float(r[wr].replace(",", "")) * scale[units[wr]]
+        n, t = acc.get(name, (0, 0.0))
+        acc[name] = (n + 1, t + b)
+    res = {"source": f"ncu --set full --clock-control none (cache flush before each replayed kernel), capture "
+                     f"{os.path.basename(path)}, profiles/r01_ncu_edge_kernels.md",
+           "step": {"N": N, "P": P, "slot": slot}, "kernels": {}}
+    for name, (n, t) in acc.items():
+        alg = bench.kernel_bytes(name, N, P)
+        res["kernels"][name] = {"launches": n, "dram_bytes_per_launch": t / n, "algorithmic_bytes_per_launch": alg,
+                                "ratio": t / n / alg}
+    json.dump(res, open(out, "w"), indent=1)
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3], int(sys.argv[4]), int(sys.argv[5]), int(sys.argv[6]))
+    elif sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
         n = int(sys.argv[4]) if len(sys.argv) > 4 else None
