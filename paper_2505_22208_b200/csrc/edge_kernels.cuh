@@ -211,7 +211,9 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
     pdl_enter();  // the kernel's prologue (weights, TMEM, accumulators) overlapped the previous kernel
     if (c.lo >= c.hi) return;
     const int e0 = d.row_ptr[c.lo], e1 = d.row_ptr[c.hi];
-    const bool lead = c.lt == 0;
+    // the staging / MMA-issuing thread: lane 0 of warp g % (H/32) of the group, so the
+    // four groups' leaders sit on different SM sub-partitions (warp id % 4)
+    const bool lead = c.lt == 32 * (c.g % (H / 32));
     const uint32_t quad = (threadIdx.x >> 5) & 3;
     int cur = c.lo;
     body.begin(cur);
@@ -433,6 +435,9 @@ struct ForceBody {
     const Dev& d;
     const float* __restrict__ T;
     int a, L;
+    bool kv;  // lanes 0..K-1 of warp g % (H/32): the channel-independent sums (one warp per
+              // group, a different SM sub-partition per group)
+    int k;
     float Y0, Y1, Y2, U0, U1, U2, V0, V1, V2;
     __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
         const int row = L > 0 ? j : __ldg(d.Z + j) - 1;
@@ -446,11 +451,11 @@ struct ForceBody {
         Y0 = fmaf(tf, gv.x, Y0);
         Y1 = fmaf(tf, gv.y, Y1);
         Y2 = fmaf(tf, gv.z, Y2);
-        if (a < K) {  // channel-independent sums: first warp only
+        if (kv) {  // channel-independent sums
             U0 = fmaf(fw, gv.x, U0);
             U1 = fmaf(fw, gv.y, U1);
             U2 = fmaf(fw, gv.z, U2);
-            const float fr = s.fcp[e * K + a];
+            const float fr = s.fcp[e * K + k];
             V0 = fmaf(fr, gv.x, V0);
             V1 = fmaf(fr, gv.y, V1);
             V2 = fmaf(fr, gv.z, V2);
@@ -460,8 +465,8 @@ struct ForceBody {
     __device__ void end(int i) {
         float* y = d.Yf + static_cast<int64_t>(i) * kYW;
         y[a] = Y0, y[H + a] = Y1, y[2 * H + a] = Y2;
-        if (a == 0) y[3 * H] = U0, y[3 * H + 1] = U1, y[3 * H + 2] = U2;
-        if (a < K) y[3 * H + 3 + a] = V0, y[3 * H + 3 + K + a] = V1, y[3 * H + 3 + 2 * K + a] = V2;
+        if (kv && k == 0) y[3 * H] = U0, y[3 * H + 1] = U1, y[3 * H + 2] = U2;
+        if (kv) y[3 * H + 3 + k] = V0, y[3 * H + 3 + K + k] = V1, y[3 * H + 3 + 2 * K + k] = V2;
     }
 };
 
@@ -469,7 +474,9 @@ template <int H, int K>
 __global__ void __launch_bounds__(kGroups* H, 1) k_edge_force(Dev d) {
     EdgeCta<H, K> c = edge_prologue<H, K>(d);
     __syncthreads();
-    ForceBody<H, K> b{d, d.L > 0 ? d.t[d.L] : d.tanh_emb, c.lt, d.L};
+    const int kw = c.g % (H / 32);
+    ForceBody<H, K> b{d, d.L > 0 ? d.t[d.L] : d.tanh_emb, c.lt, d.L,
+                      (c.lt >> 5) == kw && (c.lt & 31) < K, c.lt & 31};
     walk_edges<H, K>(d, c, b, FilterTc{});
 }
 
@@ -596,6 +603,8 @@ struct HeadBody {
     const float* __restrict__ hL;
     float* acc;  // smem [3][D][H] + [D][K], this group's
     int a, D, L, pass_ch, first, N;
+    bool kv;  // lanes 0..K-1 of warp g % (H/32) carry the rbf-column sums R
+    int k;
     int s, ch;
     float Ti, S, W, R;
     float es[8], ed[8];  // per edge of the block: s_ij and gF_i.u_ij
@@ -635,7 +644,7 @@ struct HeadBody {
         const float sij = es[e & 7];
         S += sij;
         W = fmaf(sij, r.t, W);
-        if (a < K) R = fmaf(ed[e & 7], st.fcp[e * K + a], R);
+        if (kv) R = fmaf(ed[e & 7], st.fcp[e * K + k], R);
     }
     // per-atom operands are loaded when the atom begins and used at its end, so
     // their latency hides behind the atom's edges
@@ -679,7 +688,7 @@ struct HeadBody {
         *ghp = fmaf(gT, 1.f - Ti * Ti, gh);
         acc[ch * H + a] = fmaf(S, Ti, acc[ch * H + a]);
         acc[(D + ch) * H + a] = fmaf(0.5f * Ti, W, acc[(D + ch) * H + a]);
-        if (a < K) acc[3 * D * H + ch * K + a] += R;
+        if (kv) acc[3 * D * H + ch * K + k] += R;
     }
 };
 
@@ -692,8 +701,9 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_head(Dev d, int pass_ch,
     float* acc = accs + c.g * AW;
     for (int e = c.lt; e < AW; e += H) acc[e] = 0.f;
     __syncthreads();
+    const int kw = c.g % (H / 32);
     HeadBody<H, K> b{d, d.L > 0 ? d.t[d.L] : d.tanh_emb, d.L > 0 ? d.h[d.L] : d.emb, acc, c.lt, D, d.L, pass_ch,
-                     first, d.hdr->N};
+                     first, d.hdr->N, (c.lt >> 5) == kw && (c.lt & 31) < K, c.lt & 31};
     walk_edges<H, K>(d, c, b, FilterTc{});
     __syncthreads();
     // combine groups in order; emit the CTA partial in parameter layout:
