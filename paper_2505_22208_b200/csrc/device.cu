@@ -457,7 +457,8 @@ struct Model {
         set_smem((const void*)k_node_gemm<H>, kGemmSmem);
         set_smem((const void*)k_dwu<H>, kDwuSmem);
         if constexpr (kFusedBwd) set_smem((const void*)k_bwd_gemm<H>, BwdGemmSmem<H>::bytes);
-        set_smem((const void*)k_edge_message<H, K>, smem_message());
+        set_smem((const void*)k_edge_message<H, K, true>, smem_message());
+        set_smem((const void*)k_edge_message<H, K, false>, smem_message());
         int smem_max = 0;
         CK(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
         if (smem_head(c.D) > static_cast<size_t>(smem_max) || 3 * c.D > H)
@@ -465,7 +466,8 @@ struct Model {
         // embedding-gradient slots (distinct Z per device-batch) that fit next to the staging
         set_smem((const void*)k_edge_force<H, K>, smem_force(c.D));
         set_smem((const void*)k_edge_head<H, K>, smem_head(c.D));
-        set_smem((const void*)k_edge_bwd<H, K>, smem_bwd());
+        set_smem((const void*)k_edge_bwd<H, K, true>, smem_bwd());
+        set_smem((const void*)k_edge_bwd<H, K, false>, smem_bwd());
         set_smem((const void*)k_emb_grad, sizeof(float) * kMaxZ * H);
         c.grid_emb = c.nsm;
         // one tcgen05 CTA per SM, persistent over 128-atom tiles; a multiple of the
@@ -475,13 +477,13 @@ struct Model {
         // one edge partitioning (k_scan) serves all four edge kernels: size it so
         // every CTA of the heaviest one is resident (no second wave)
         int occ_e = 8, o = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_message<H, K>, kGroups * H, smem_message()));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_message<H, K, false>, kGroups * H, smem_message()));
         occ_e = std::min(occ_e, o);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_force<H, K>, kGroups * H, smem_force(c.D)));
         occ_e = std::min(occ_e, o);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_head<H, K>, kGroups * H, smem_head(c.D)));
         occ_e = std::min(occ_e, o);
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_bwd<H, K>, kGroups * H, smem_bwd()));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_bwd<H, K, false>, kGroups * H, smem_bwd()));
         occ_e = std::min(occ_e, o);
         c.grid_edge = c.nsm * std::max(1, occ_e);
         c.grid_warp = 4 * c.nsm;
@@ -506,7 +508,8 @@ struct Model {
         const Dev d = make_dev(c);
         if (c.L == 0) throw InputErr("model: layers == 0 is not supported by the device path");
         for (int l = 0; l < c.L; ++l) {
-            launch(c, "message", k_edge_message<H, K>, c.grid_edge, kGroups * H, smem_message(), d, l);
+            launch(c, "message", l == 0 ? k_edge_message<H, K, true> : k_edge_message<H, K, false>, c.grid_edge,
+                   kGroups * H, smem_message(), d, l);
             launch(c, "update", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 0);
         }
         launch(c, "force", k_edge_force<H, K>, c.grid_edge, kGroups * H, smem_force(c.D), d);
@@ -534,7 +537,8 @@ struct Model {
                 launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 1);
                 launch(c, "dwu", k_dwu<H>, c.grid_gemm, 256, kDwuSmem, d, l);
             }
-            launch(c, "bwd_edge", k_edge_bwd<H, K>, c.grid_edge, kGroups * H, smem_bwd(), d, l);
+            launch(c, "bwd_edge", l == 0 ? k_edge_bwd<H, K, true> : k_edge_bwd<H, K, false>, c.grid_edge,
+                   kGroups * H, smem_bwd(), d, l);
         }
         SegTable tab{};
         int64_t off = 0;

@@ -366,7 +366,9 @@ struct EdgeKernelSmem {
 
 // ---------------------------------------------------------------- message --
 // m_i[a] = sum_j t_j[a] * sum_k Wf[a,k] fcut_ij rbf_ijk ; mu_i = tanh(m_i)   (S/model.cpp:78-93)
-template <int H, int K, bool TC>
+// kZ: layer 0, whose source rows are tanh(E)[Z_j - 1] (compile-time, so layers
+// >= 1 carry no predicated-off Z gathers)
+template <int H, int K, bool TC, bool kZ>
 struct MessageBody {
     static constexpr bool kFilter = TC;
     static constexpr int kParts = TC ? 0 : kPartPlain;
@@ -382,18 +384,18 @@ struct MessageBody {
     float w[K];
     float m;
     __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
-        const int row = l == 0 ? __ldg(d.Z + j) - 1 : j;
+        const int row = kZ ? __ldg(d.Z + j) - 1 : j;
         r.t = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
     }
     __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f, unsigned on) {
         if constexpr (!TC) f = filter_ffma<K>(w, s, e);
-        if (on) m = fmaf(r.t, f, m);
+        m = fmaf(r.t, on ? f : 0.f, m);
     }
     __device__ void begin(int) { m = 0.f; }
     __device__ void end(int i) { mu[static_cast<int64_t>(i) * H + a] = tanhf(m); }
 };
 
-template <int H, int K>
+template <int H, int K, bool kZ>
 __global__ void __launch_bounds__(kGroups* H, 1) k_edge_message(Dev d, int l) {
     constexpr bool TC = EdgeKernelSmem<H, K>::TC;
     EdgeCta<H, K> c = edge_prologue<H, K>(d);
@@ -404,7 +406,7 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_message(Dev d, int l) {
     } else {
         __syncthreads();
     }
-    MessageBody<H, K, TC> b{d, l == 0 ? d.tanh_emb : d.t[l], d.mu[l], l, c.lt};
+    MessageBody<H, K, TC, kZ> b{d, kZ ? d.tanh_emb : d.t[l], d.mu[l], l, c.lt};
     if constexpr (!TC) {
 #pragma unroll
         for (int k = 0; k < K; ++k) b.w[k] = d.wf[l][c.lt * K + k];
@@ -440,13 +442,13 @@ struct ForceBody {
     int k;
     float Y0, Y1, Y2, U0, U1, U2, V0, V1, V2;
     __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
-        const int row = L > 0 ? j : __ldg(d.Z + j) - 1;
-        r.t = __ldg(T + static_cast<int64_t>(row) * H + a);
+        r.t = __ldg(T + static_cast<int64_t>(j) * H + a);  // t[L], L >= 1 (ctx creation)
     }
+    // branch-free: edges outside the segment contribute exact zeros
     __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float, unsigned on) {
-        if (!on) return;
         const float4 gv = s.geo[e];
-        const float fw = gv.w;
+        const float mk = on ? 1.f : 0.f;
+        const float fw = gv.w * mk;
         const float tf = r.t * fw;
         Y0 = fmaf(tf, gv.x, Y0);
         Y1 = fmaf(tf, gv.y, Y1);
@@ -455,7 +457,7 @@ struct ForceBody {
             U0 = fmaf(fw, gv.x, U0);
             U1 = fmaf(fw, gv.y, U1);
             U2 = fmaf(fw, gv.z, U2);
-            const float fr = s.fcp[e * K + k];
+            const float fr = s.fcp[e * K + k] * mk;
             V0 = fmaf(fr, gv.x, V0);
             V1 = fmaf(fr, gv.y, V1);
             V2 = fmaf(fr, gv.z, V2);
@@ -475,7 +477,7 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_force(Dev d) {
     EdgeCta<H, K> c = edge_prologue<H, K>(d);
     __syncthreads();
     const int kw = c.g % (H / 32);
-    ForceBody<H, K> b{d, d.L > 0 ? d.t[d.L] : d.tanh_emb, c.lt, d.L,
+    ForceBody<H, K> b{d, d.t[d.L], c.lt, d.L,
                       (c.lt >> 5) == kw && (c.lt & 31) < K, c.lt & 31};
     walk_edges<H, K>(d, c, b, FilterTc{});
 }
@@ -616,8 +618,7 @@ struct HeadBody {
         return make_float4(__ldg(gp), __ldg(gp + 1), __ldg(gp + 2), 0.f);
     }
     __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
-        const int row = L > 0 ? j : __ldg(d.Z + j) - 1;
-        r.t = __ldg(T + static_cast<int64_t>(row) * H + a);
+        r.t = __ldg(T + static_cast<int64_t>(j) * H + a);  // t[L], L >= 1
     }
     // s_ij = fcut (gF_i - gF_j).u_ij is channel-independent: lane u computes edge u
     __device__ void prepare(const EdgeStage<K>& st, int e0) {
@@ -640,11 +641,10 @@ struct HeadBody {
         }
     }
     __device__ void edge(const EdgeStage<K>& st, int e, const Reg& r, float, unsigned on) {
-        if (!on) return;
-        const float sij = es[e & 7];
+        const float sij = on ? es[e & 7] : 0.f;
         S += sij;
         W = fmaf(sij, r.t, W);
-        if (kv) R = fmaf(ed[e & 7], st.fcp[e * K + k], R);
+        if (kv) R = fmaf(on ? ed[e & 7] : 0.f, st.fcp[e * K + k], R);
     }
     // per-atom operands are loaded when the atom begins and used at its end, so
     // their latency hides behind the atom's edges
@@ -652,7 +652,7 @@ struct HeadBody {
     __device__ void begin(int i) {
         s = d.sample_of[i];
         ch = pass_ch >= 0 ? pass_ch : d.dsidx[s];
-        const int row = L > 0 ? i : __ldg(d.Z + i) - 1;
+        const int row = i;
         Ti = __ldg(T + static_cast<int64_t>(row) * H + a);
         S = W = R = 0.f;
         p_wa = __ldg(d.wfh + a * D + ch);
@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_head(Dev d, int pass_ch,
     for (int e = c.lt; e < AW; e += H) acc[e] = 0.f;
     __syncthreads();
     const int kw = c.g % (H / 32);
-    HeadBody<H, K> b{d, d.L > 0 ? d.t[d.L] : d.tanh_emb, d.L > 0 ? d.h[d.L] : d.emb, acc, c.lt, D, d.L, pass_ch,
+    HeadBody<H, K> b{d, d.t[d.L], d.h[d.L], acc, c.lt, D, d.L, pass_ch,
                      first, d.hdr->N, (c.lt >> 5) == kw && (c.lt & 31) < K, c.lt & 31};
     walk_edges<H, K>(d, c, b, FilterTc{});
     __syncthreads();
@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_head(Dev d, int pass_ch,
 // shared-memory G/R tiles — cut the instruction count by a fifth but the
 // per-block producer/consumer handshake and the smaller chunk it needs for TMEM
 // made the kernel slower; see profiles/README.md.)
-template <int H, int K, bool TC>
+template <int H, int K, bool TC, bool kZ>
 struct BwdBody {
     static constexpr bool kFilter = TC;
     static constexpr int kParts = kPartPlain;
@@ -752,14 +752,13 @@ struct BwdBody {
     float gi[8];  // gm of the destination of each edge of the block (0: masked)
     __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
         r.gm = __ldg(d.gm + static_cast<int64_t>(j) * H + a);
-        const int row = l == 0 ? __ldg(d.Z + j) - 1 : j;
+        const int row = kZ ? __ldg(d.Z + j) - 1 : j;
         r.t = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
     }
     __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f, unsigned on) {
-        if (!on) return;
         if constexpr (!TC) f = filter_ffma<K>(w, s, e);
-        gt = fmaf(r.gm, f, gt);
-        gi[e & 7] = gmi;
+        gt = fmaf(r.gm, on ? f : 0.f, gt);
+        if (on) gi[e & 7] = gmi;
     }
     // dWf[a,k] += gm_ia t_ja fcut rbf_k, once per edge (segment-independent),
     // two k per FFMA2
@@ -781,7 +780,7 @@ struct BwdBody {
     __device__ void begin(int i) {
         gmi = d.gm[static_cast<int64_t>(i) * H + a];
         gt = 0.f;
-        const int row = l == 0 ? __ldg(d.Z + i) - 1 : i;
+        const int row = kZ ? __ldg(d.Z + i) - 1 : i;
         p_ti = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
         p_gh = d.gh[static_cast<int64_t>(i) * H + a];
     }
@@ -790,7 +789,7 @@ struct BwdBody {
     }
 };
 
-template <int H, int K>
+template <int H, int K, bool kZ>
 __global__ void __launch_bounds__(kGroups* H, 1) k_edge_bwd(Dev d, int l) {
     constexpr bool TC = EdgeKernelSmem<H, K>::TC;
     EdgeCta<H, K> c = edge_prologue<H, K>(d);
@@ -802,7 +801,7 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_bwd(Dev d, int l) {
     } else {
         __syncthreads();
     }
-    BwdBody<H, K, TC> b{d, l == 0 ? d.tanh_emb : d.t[l], l, c.lt};
+    BwdBody<H, K, TC, kZ> b{d, kZ ? d.tanh_emb : d.t[l], l, c.lt};
 #pragma unroll
     for (int k = 0; k < K; ++k) b.w[k] = TC ? 0.f : d.wf[l][c.lt * K + k];
 #pragma unroll
