@@ -1,6 +1,7 @@
 // device.cu - host orchestration of the sm_100a LaMM step: lamm_ctx, device
 // buffers, batch staging, the captured CUDA graph of the step, NCCL, and the
 // device half of the C ABI declared in include/lamm_b200.h.
+#include <cudaTypedefs.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -89,6 +90,9 @@ struct lamm_ctx {
     const lamm_b200::Ops* ops = nullptr;
     // persistent parameter state
     lamm_b200::Buf p64, v64, g64, p32, tanh_emb, grads, block_scratch, wpack;
+    // TMA descriptors of the [Ncap][H] activation buffers the node GEMMs read,
+    // by base address (rebuilt when ensure_capacity reallocates)
+    std::map<const void*, CUtensorMap> tmaps;
     // staging (pinned host -> device blob, header first)
     char* h_stage = nullptr;
     size_t h_stage_cap = 0;
@@ -236,7 +240,39 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     }
     ensure_buf(c, "part_head", 4 * static_cast<size_t>(c.grid_edge) * (3 * H + K) * D, changed);
     ensure_buf(c, "part_emb", 4 * static_cast<size_t>(c.grid_emb) * kMaxZ * H, changed);
-    if (changed) c.graph_dirty = true;
+    if (changed) {
+        c.graph_dirty = true;
+        c.tmaps.clear();
+    }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// TMA map of an fp32 [Ncap][H] activation buffer: 32 x 128 boxes (one 128-atom
+// tile's K block), SWIZZLE_128B, the layout umma::sw128_desc describes.
+CUtensorMap act_map(Ctx& c, const float* base) {
+    auto it = c.tmaps.find(base);
+    if (it != c.tmaps.end()) return it->second;
+    CUtensorMap m{};
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(c.H), static_cast<cuuint64_t>(c.Ncap)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(c.H) * 4};
+    const cuuint32_t box[2] = {32, 128}, es[2] = {1, 1};
+    const CUresult r = tensor_map_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+    c.tmaps[base] = m;
+    return m;
 }
 
 Dev make_dev(Ctx& c) {
@@ -510,7 +546,7 @@ struct Model {
         for (int l = 0; l < c.L; ++l) {
             launch(c, "message", l == 0 ? k_edge_message<H, K, true> : k_edge_message<H, K, false>, c.grid_edge,
                    kGroups * H, smem_message(), d, l);
-            launch(c, "update", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 0);
+            launch(c, "update", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 0, act_map(c, d.mu[l]));
         }
         launch(c, "force", k_edge_force<H, K>, c.grid_edge, kGroups * H, smem_force(c.D), d);
         launch(c, "force_out", k_force_out<H, K>, c.grid_warp, 256, 0, d, energy ? 0 : 1);
@@ -534,7 +570,7 @@ struct Model {
             if constexpr (kFusedBwd) {
                 launch(c, "bwd_gemm", k_bwd_gemm<H>, c.grid_upd, 256, BwdGemmSmem<H>::bytes, d, l);
             } else {
-                launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 1);
+                launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 1, act_map(c, d.gh));
                 launch(c, "dwu", k_dwu<H>, c.grid_gemm, 256, kDwuSmem, d, l);
             }
             launch(c, "bwd_edge", l == 0 ? k_edge_bwd<H, K, true> : k_edge_bwd<H, K, false>, c.grid_edge,

@@ -34,7 +34,7 @@ struct NodeGemmCfg {
     static constexpr int NC = H / NS;                       // output columns per CTA tile
     static constexpr size_t a_floats = 2 * kGemmM * H;      // activation tile hi | lo (full K)
     static constexpr size_t b_floats = 2 * NC * H;          // weight rows [NC][H] hi | lo
-    static constexpr size_t bytes = 4 * (a_floats + b_floats) + 64;
+    static constexpr size_t bytes = 4 * (a_floats + b_floats) + 64 + 1024;  // + alignment slack
 };
 template <int H>
 using NodeGemmSmem = NodeGemmCfg<H>;
@@ -102,16 +102,17 @@ __global__ void __launch_bounds__(256) k_opt(Dev d, int G, double inv_g, double 
 // epilogue inputs (residual / mu) are prefetched while the tensor core runs.
 // Warps w and w+4 share TMEM lanes 32*(w%4).. and split the NC columns.
 template <int H>
-__global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
+__global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, const __grid_constant__ CUtensorMap amap) {
     using Cfg = NodeGemmCfg<H>;
     constexpr int NS = Cfg::NS, NC = Cfg::NC, CW = NC / 2;  // columns per thread
     static_assert(CW % 16 == 0, "epilogue reads 16 columns at a time");
-    float* sm = dyn_smem<float>();
-    float* Ahi = sm;
+    extern __shared__ __align__(1024) unsigned char node_gemm_smem[];
+    float* sm = reinterpret_cast<float*>(node_gemm_smem + ((1024u - (smem_u32(node_gemm_smem) & 1023u)) & 1023u));
+    float* Ahi = sm;  // the raw activation tile (TMA, SWIZZLE_128B): the tf32 "hi" operand as is
     float* Alo = Ahi + kGemmM * H;
     float* Bhi = Alo + kGemmM * H;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(Bhi + Cfg::b_floats);  // [0] weights TMA, [1] MMA done
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(Bhi + Cfg::b_floats);  // weights TMA, MMA done, activations TMA
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int quad = warp & 3, half = warp >> 2;
     constexpr uint32_t kCols = NC < 32 ? 32 : NC;
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
     if (tid == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
+        mbar_init(&bar[2], 1);
         mbar_fence_init();
     }
     umma::fence_before();
@@ -128,8 +130,7 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
     const uint32_t idesc = umma::idesc_tf32(kGemmM, NC);
     const int N = d.hdr->N;  // from the staged upload, not from the previous kernel
     const int ntiles = (N + kGemmM - 1) / kGemmM * NS;
-    const float* __restrict__ src = mode == 0 ? d.mu[l] : d.gh;
-    uint32_t wphase = 0, mphase = 0;
+    uint32_t wphase = 0, mphase = 0, aphase = 0;
     int loaded_np = -1;
     bool w_pending = false;
     auto fetch_weights = [&](int np) {  // weight block of a column split (TMA), packed by the last optimizer step
@@ -147,30 +148,24 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int at = tile / NS, np = tile % NS, base = at * kGemmM;
         if (np != loaded_np) fetch_weights(np);
-        // stage the full activation tile (hi/lo), all loads first. Thread -> 16-byte
-        // chunk c of the canonical tile in storage order (c = ((m/8)*(H/4) + k4)*8 + m%8),
-        // so each warp's shared stores are one contiguous 512 B run (no bank conflicts);
-        // the global loads are then 8 rows x 64 B per warp.
-        {
-            constexpr int Q = H / 4, IT = kGemmM * Q / 256;
-            float4 v[IT];
+        // the activation tile (mu_l or gh rows base..base+127, all H columns) by TMA
+        // in H/32 SWIZZLE_128B blocks; rows past the batch are never stored
+        if (tid == 0) {
+            mbar_expect_tx(&bar[2], static_cast<uint32_t>(kGemmM * H * 4));
 #pragma unroll
-            for (int it = 0; it < IT; ++it) {
-                const int c = tid + 256 * it, m = (c / (8 * Q)) * 8 + (c & 7), k4 = (c >> 3) % Q, atom = base + m;
-                v[it] = atom < N
-                            ? __ldg(reinterpret_cast<const float4*>(src + static_cast<int64_t>(atom) * H + 4 * k4))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
+            for (int kb = 0; kb < H / 32; ++kb) umma::tma_load_2d(Ahi + kb * kGemmM * 32, &amap, kb * 32, base, &bar[2]);
+        }
+        mbar_wait(&bar[2], aphase);
+        aphase ^= 1u;
+        {  // lo = x - trunc_tf32(x), same swizzled positions; thread -> consecutive 16-byte chunks
+            constexpr int IT = kGemmM * H / 4 / 256;
 #pragma unroll
             for (int it = 0; it < IT; ++it) {
                 const int c = tid + 256 * it;
-                float4 hi, lo;
-                umma::split_tf32(v[it].x, hi.x, lo.x);
-                umma::split_tf32(v[it].y, hi.y, lo.y);
-                umma::split_tf32(v[it].z, hi.z, lo.z);
-                umma::split_tf32(v[it].w, hi.w, lo.w);
-                *reinterpret_cast<float4*>(Ahi + 4 * c) = hi;
-                *reinterpret_cast<float4*>(Alo + 4 * c) = lo;
+                const float4 x = *reinterpret_cast<const float4*>(Ahi + 4 * c);
+                *reinterpret_cast<float4*>(Alo + 4 * c) =
+                    make_float4(umma::tf32_trunc_lo(x.x), umma::tf32_trunc_lo(x.y), umma::tf32_trunc_lo(x.z),
+                                umma::tf32_trunc_lo(x.w));
             }
         }
         umma::fence_proxy_async();
@@ -185,8 +180,8 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode) {
             const float* Blo = Bhi + NC * H;
 #pragma unroll
             for (int s = 0; s < H / 8; ++s)
-                umma::mma3(tbase, umma::kdesc(Ahi, s, H), umma::kdesc(Alo, s, H), umma::kdesc(Bhi, s, H),
-                           umma::kdesc(Blo, s, H), idesc, s ? 1u : 0u);
+                umma::mma3(tbase, umma::sw128_kdesc(Ahi, s, kGemmM), umma::sw128_kdesc(Alo, s, kGemmM),
+                           umma::kdesc(Bhi, s, H), umma::kdesc(Blo, s, H), idesc, s ? 1u : 0u);
             umma::commit(&bar[1]);
         }
         // epilogue inputs for this thread's row/columns, fetched while the MMAs run

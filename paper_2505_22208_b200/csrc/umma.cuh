@@ -15,6 +15,7 @@
 // product is accumulated as hi*hi + hi*lo + lo*hi ("3xTF32"): ~1e-7 relative,
 // well inside the 1e-4 parity bar, at one third of the tf32 tensor rate.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -143,6 +144,41 @@ __device__ __forceinline__ int mn32_idx(int mn, int k, int mn_atoms) {
 }
 __device__ __forceinline__ uint64_t mn32_desc(const float* tile, int mn_atoms) {
     return sdesc(tile, 512u, static_cast<uint32_t>(mn_atoms) * 512u) | (1ull << 61);  // layout 1: 128B_BASE32B
+}
+
+// K-major SWIZZLE_128B operand (the layout a TMA tensor load with
+// CU_TENSOR_MAP_SWIZZLE_128B and a 32-float box width writes): per 32-element K
+// block, rows of 128 B with their 16-byte chunks XOR-swizzled by row % 8, 8-row
+// groups 1024 B apart. `p` is the K-step's start: block base + (k % 32) floats;
+// the block base must be 1024-byte aligned.
+__device__ __forceinline__ uint64_t sw128_desc(const float* p) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr(p) >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>(1) << 16;          // LBO: unused for swizzled K-major
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;  // SBO: 8 rows x 128 B
+    d |= static_cast<uint64_t>(1) << 46;          // descriptor version (sm100)
+    d |= static_cast<uint64_t>(2) << 61;          // SWIZZLE_128B
+    return d;
+}
+// K-step s (8 elements) of a [rows][KW] SW128 tile stored as KW/32 blocks of rows x 32.
+__device__ __forceinline__ uint64_t sw128_kdesc(const float* tile, int s, int rows) {
+    return sw128_desc(tile + (s >> 2) * rows * 32 + (s & 3) * 8);
+}
+
+// TMA: 2D tile of a tensor map into shared memory, completion on an mbarrier.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            saddr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(saddr(bar))
+        : "memory");
+}
+
+// The tensor core reads a kind::tf32 operand's 32-bit container as tf32 by
+// TRUNCATION (measured: scratch/sw128_test.cu), so raw fp32 data in shared
+// memory is a valid "hi" operand and lo = x - trunc_tf32(x) completes the split.
+__device__ __forceinline__ float tf32_trunc_lo(float x) {
+    return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
 // fp32 -> (tf32 hi, fp32 lo) split for 3xTF32.
