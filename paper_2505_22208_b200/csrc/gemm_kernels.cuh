@@ -262,7 +262,7 @@ struct BwdGemmSmem {
 };
 
 template <int H>
-__global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
+__global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l, const __grid_constant__ CUtensorMap ghmap) {
     using Cfg = NodeGemmCfg<H>;
     constexpr int NS = Cfg::NS, NC = Cfg::NC, CW = NC / 2, Q = H / 4;
     static_assert(H == 128 && CW % 16 == 0, "fused update backward: H = 128");
@@ -272,8 +272,8 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
     float* Ahi = sm;
     float* Alo = Ahi + kGemmM * H;
     float* Bhi = Alo + kGemmM * H;  // weights [NC][H] hi | lo, then the mu tile hi | lo
-    uint64_t* bar = reinterpret_cast<uint64_t*>(Bhi + BwdGemmSmem<H>::b_floats);  // weights, MMA1, MMA2
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(Bhi + BwdGemmSmem<H>::b_floats);  // weights, MMA1, MMA2, gh TMA
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int quad = warp & 3, half = warp >> 2;
     if (warp == 0) umma::tmem_alloc(tslot, 512);
@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
         mbar_init(&bar[2], 1);
+        mbar_init(&bar[3], 1);
         mbar_fence_init();
     }
     umma::fence_before();
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
     umma::fence_after();
     const uint32_t tbase = *tslot;
     const uint32_t tD1 = tbase, tD2 = tbase + NC, tAh = tbase + 256, tAl = tbase + 384;
+    uint32_t gphase = 0;
     const uint32_t lane_off = static_cast<uint32_t>(quad * 32) << 16;
     const uint32_t idesc = umma::idesc_tf32(kGemmM, NC);
     const uint32_t idesc_mn = umma::idesc_tf32(kGemmM, NC) | (1u << 16);  // B MN-major
@@ -304,7 +306,6 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
     };
     if (static_cast<int>(blockIdx.x) < ntiles) fetch_weights();
     pdl_enter();
-    const float* __restrict__ gh = d.gh;
     const float* __restrict__ mu = d.mu[l];
     int done = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++done) {
@@ -318,16 +319,12 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
             umma::fence_after();
             fetch_weights();
         }
-        // loads first: the gh tile by 16-byte chunk in canonical storage order (MMA1's A),
-        // gh columns for the TMEM A of MMA2 (thread = channel, warps w and w+4 split the
-        // atoms), and this thread's mu row segment for the epilogue
-        constexpr int IT = kGemmM * Q / 256;
-        float4 va[IT];
+        // the gh tile by TMA (SWIZZLE_128B; raw fp32 = MMA1's tf32 hi operand), and this
+        // thread's mu row segment for the epilogue
+        if (tid == 0) {
+            mbar_expect_tx(&bar[3], static_cast<uint32_t>(kGemmM * H * 4));
 #pragma unroll
-        for (int it = 0; it < IT; ++it) {
-            const int c = tid + 256 * it, m = (c / (8 * Q)) * 8 + (c & 7), k4 = (c >> 3) % Q;
-            va[it] = base + m < N ? __ldg(reinterpret_cast<const float4*>(gh + static_cast<int64_t>(base + m) * H) + k4)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int kb = 0; kb < H / 32; ++kb) umma::tma_load_2d(Ahi + kb * kGemmM * 32, &ghmap, kb * 32, base, &bar[3]);
         }
         float pre[CW];
 #pragma unroll
@@ -336,29 +333,38 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
                                   : make_float4(0.f, 0.f, 0.f, 0.f);
             pre[q] = x.x, pre[q + 1] = x.y, pre[q + 2] = x.z, pre[q + 3] = x.w;
         }
+        mbar_wait(&bar[3], gphase);
+        gphase ^= 1u;
+        {  // MMA1's lo operand: x - trunc_tf32(x) at the same swizzled positions
+            constexpr int IT = kGemmM * Q / 256;
 #pragma unroll
-        for (int it = 0; it < IT; ++it) {
-            const int c = tid + 256 * it;
-            float4 hi, lo;
-            umma::split_tf32(va[it].x, hi.x, lo.x);
-            umma::split_tf32(va[it].y, hi.y, lo.y);
-            umma::split_tf32(va[it].z, hi.z, lo.z);
-            umma::split_tf32(va[it].w, hi.w, lo.w);
-            *reinterpret_cast<float4*>(Ahi + 4 * c) = hi;
-            *reinterpret_cast<float4*>(Alo + 4 * c) = lo;
-        }
-        // gh^T into TMEM: lane = channel b = row, columns = atoms [half*64, half*64+64)
-#pragma unroll
-        for (int cc = 0; cc < kGemmM / 2; cc += 16) {
-            const int a0 = half * (kGemmM / 2) + cc;
-            float hv[16], lv[16];
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                const float x = base + a0 + q < N ? __ldg(gh + static_cast<int64_t>(base + a0 + q) * H + row) : 0.f;
-                umma::split_tf32(x, hv[q], lv[q]);
+            for (int it = 0; it < IT; ++it) {
+                const int c = tid + 256 * it;
+                const float4 x = *reinterpret_cast<const float4*>(Ahi + 4 * c);
+                *reinterpret_cast<float4*>(Alo + 4 * c) =
+                    make_float4(umma::tf32_trunc_lo(x.x), umma::tf32_trunc_lo(x.y), umma::tf32_trunc_lo(x.z),
+                                umma::tf32_trunc_lo(x.w));
             }
-            umma::st16(tAh + lane_off + a0, hv);
-            umma::st16(tAl + lane_off + a0, lv);
+        }
+        // gh^T into TMEM from the staged tile: lane = channel b = row, columns = atoms
+        // [half*64, half*64+64); element (atom m, channel b) of the SW128 tile sits in
+        // K block b/32, row m, 16-byte chunk ((b%32)/4) ^ (m%8) (a warp reads one 128 B row)
+        {
+            const float* blk = Ahi + (row >> 5) * kGemmM * 32;
+            const int j = (row & 31) >> 2, w = row & 3;
+#pragma unroll
+            for (int cc = 0; cc < kGemmM / 2; cc += 16) {
+                const int a0 = half * (kGemmM / 2) + cc;
+                float hv[16], lv[16];
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    const int m = a0 + q;
+                    const float x = blk[m * 32 + ((j ^ (m & 7)) << 2) + w];  // rows past N: never read (MMA2 masks)
+                    umma::split_tf32(base + m < N ? x : 0.f, hv[q], lv[q]);
+                }
+                umma::st16(tAh + lane_off + a0, hv);
+                umma::st16(tAl + lane_off + a0, lv);
+            }
         }
         umma::st_wait();
         umma::fence_proxy_async();
@@ -370,8 +376,8 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l) {
             const float* Blo = Bhi + NC * H;
 #pragma unroll
             for (int s = 0; s < H / 8; ++s)
-                umma::mma3(tD1, umma::kdesc(Ahi, s, H), umma::kdesc(Alo, s, H), umma::kdesc(Bhi, s, H),
-                           umma::kdesc(Blo, s, H), idesc, s ? 1u : 0u);
+                umma::mma3(tD1, umma::sw128_kdesc(Ahi, s, kGemmM), umma::sw128_kdesc(Alo, s, kGemmM),
+                           umma::kdesc(Bhi, s, H), umma::kdesc(Blo, s, H), idesc, s ? 1u : 0u);
             umma::commit(&bar[1]);
         }
         wphase ^= 1u;
