@@ -214,7 +214,7 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     ensure_buf(c, "rbf", 4 * static_cast<size_t>(Pp) * K, changed);
     ensure_buf(c, "rbfl", 4 * static_cast<size_t>(Pp) * K, changed);
     ensure_buf(c, "rbfp", 4 * static_cast<size_t>(Pp) * K, changed);
-    ensure_buf(c, "part_lo", 4 * (static_cast<size_t>(c.grid_edge) * kGroups + 1), changed);
+    ensure_buf(c, "part_lo", 4 * (static_cast<size_t>(c.grid_edge) * kPartsPerCta + 1), changed);
     if (c.export64) {
         ensure_buf(c, "dist64", 8 * Pc, changed);
         ensure_buf(c, "unit64", 24 * Pc, changed);
@@ -513,7 +513,7 @@ struct Model {
         // one edge partitioning (k_scan) serves all four edge kernels: size it so
         // every CTA of the heaviest one is resident (no second wave)
         int occ_e = 8, o = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_message<H, K, false>, kGroups * H, smem_message()));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_message<H, K, false>, kMsgGroups * H, smem_message()));
         occ_e = std::min(occ_e, o);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_force<H, K>, kGroups * H, smem_force(c.D)));
         occ_e = std::min(occ_e, o);
@@ -535,7 +535,7 @@ struct Model {
 
     static void nlist(Ctx& c) {
         const Dev d = make_dev(c);
-        launch(c, "nbr_scan", k_scan, 1, 1024, 0, d, c.grid_edge * kGroups);
+        launch(c, "nbr_scan", k_scan, 1, 1024, 0, d, c.grid_edge * kPartsPerCta);
         launch(c, "nbr_fill", k_nbr_fill<K>, c.grid_warp, 256, 0, d);
     }
 
@@ -545,7 +545,7 @@ struct Model {
         if (c.L == 0) throw InputErr("model: layers == 0 is not supported by the device path");
         for (int l = 0; l < c.L; ++l) {
             launch(c, "message", l == 0 ? k_edge_message<H, K, true> : k_edge_message<H, K, false>, c.grid_edge,
-                   kGroups * H, smem_message(), d, l);
+                   kMsgGroups * H, smem_message(), d, l);
             launch(c, "update", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 0, act_map(c, d.mu[l]));
         }
         launch(c, "force", k_edge_force<H, K>, c.grid_edge, kGroups * H, smem_force(c.D), d);

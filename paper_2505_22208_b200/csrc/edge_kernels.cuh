@@ -31,9 +31,16 @@
 
 namespace lamm_b200 {
 
-constexpr int kGroups = 4;   // independent edge streams per CTA
+constexpr int kGroups = 4;   // independent edge streams per CTA (default geometry)
 constexpr int kChunk = 64;   // edges per staged chunk (= MMA N of the filter)
 constexpr int kStages = 2;   // staging double buffer
+// k_scan cuts kPartsPerCta partitions per CTA; a kernel with G groups gives
+// each group kPartsPerCta / G consecutive ones (G in {2, 3, 4, 6})
+constexpr int kPartsPerCta = 12;
+// geometry of the message kernel (measured: 6 groups of 32-edge chunks, 24
+// warps per SM, is slower than 4 x 64 - the per-chunk overhead doubles)
+constexpr int kMsgGroups = 4;
+constexpr int kMsgChunk = 64;
 
 // fcut*rbf of the edges for the tensor core: K-major canonical ("interleaved")
 // layout in blocks of 8 edges, element (e, k) at ((e/8)*(K/4) + k/4)*32 +
@@ -43,15 +50,16 @@ __host__ __device__ __forceinline__ int64_t rbf_idx(int64_t e, int k) {
     return (((e >> 3) * (K / 4) + (k >> 2)) << 5) + ((e & 7) << 2) + (k & 3);
 }
 
-template <int K>
+template <int K, int C = kChunk>
 struct EdgeStage {
-    int32_t col[kChunk];
-    int32_t dst[kChunk];
-    uint32_t segw[8];       // segment-start bits of the 256 edges from word (cb >> 5) & ~3
-    float4 geo[kChunk];     // u_x, u_y, u_z, fcut
-    float fcp[kChunk * K];  // fcut*rbf, edge-major
-    float fch[kChunk * K];  // fcut*rbf, canonical tf32 hi (tensor-core filter)
-    float fcl[kChunk * K];  // fcut*rbf, canonical lo
+    static constexpr int kC = C;
+    int32_t col[C];
+    int32_t dst[C];
+    uint32_t segw[8];  // segment-start bits of the 256 edges from word (cb >> 5) & ~3
+    float4 geo[C];     // u_x, u_y, u_z, fcut
+    float fcp[C * K];  // fcut*rbf, edge-major
+    float fch[C * K];  // fcut*rbf, canonical tf32 hi (tensor-core filter)
+    float fcl[C * K];  // fcut*rbf, canonical lo
 };
 
 // --------------------------------------------------------------- PTX glue --
@@ -109,9 +117,9 @@ enum StageParts : int { kPartGeo = 1, kPartPlain = 2, kPartCanon = 4 };
 
 // One TMA stage: edges [cb, cb + n), n = min(kChunk, e1 - cb) rounded up to a
 // whole 8-edge block (the tail reads into the CSR padding).
-template <int K>
-__device__ __forceinline__ void stage_chunk(const Dev& d, EdgeStage<K>& s, uint64_t* b, int cb, int e1, int parts) {
-    const int n = min(kChunk, ((e1 - cb) + 7) & ~7);
+template <int K, int C>
+__device__ __forceinline__ void stage_chunk(const Dev& d, EdgeStage<K, C>& s, uint64_t* b, int cb, int e1, int parts) {
+    const int n = min(C, ((e1 - cb) + 7) & ~7);
     uint32_t bytes = 8u * n + 32u;
     if (parts & kPartGeo) bytes += 16u * n;
     if (parts & kPartPlain) bytes += 4u * K * n;
@@ -130,16 +138,17 @@ __device__ __forceinline__ void stage_chunk(const Dev& d, EdgeStage<K>& s, uint6
 
 // Shared-memory layout common to the edge kernels: per group kStages staged
 // chunks + TMA barriers + filter-MMA barriers, then the kernel's own region.
-template <int K>
+template <int K, int G = kGroups, int C = kChunk>
 struct EdgeSmem {
-    static constexpr size_t stage_bytes = sizeof(EdgeStage<K>) * kStages * kGroups;
-    static constexpr size_t bar_bytes = 16 * kStages * kGroups * 2 + 16;
+    static constexpr size_t stage_bytes = sizeof(EdgeStage<K, C>) * kStages * G;
+    static constexpr size_t bar_bytes = 16 * kStages * G * 2 + 16;
     static constexpr size_t extra_offset = stage_bytes + bar_bytes;
 };
 
-template <int H, int K>
+template <int H, int K, int G = kGroups, int C = kChunk>
 struct EdgeCta {
-    EdgeStage<K>* st;
+    static constexpr int kG = G, kC = C;
+    EdgeStage<K, C>* st;
     uint64_t* bar;   // [kStages] TMA
     uint64_t* mbar;  // [kStages] filter MMA
     uint32_t* tslot;
@@ -147,25 +156,28 @@ struct EdgeCta {
     int g, lt, lo, hi;
 };
 
-template <int H, int K>
-__device__ __forceinline__ EdgeCta<H, K> edge_prologue(const Dev& d) {
+template <int H, int K, int G = kGroups, int C = kChunk>
+__device__ __forceinline__ EdgeCta<H, K, G, C> edge_prologue(const Dev& d) {
+    static_assert(kPartsPerCta % G == 0, "groups must divide the partitions of a CTA");
     extern __shared__ __align__(128) unsigned char lamm_edge_smem[];
-    EdgeCta<H, K> c;
+    using Smem = EdgeSmem<K, G, C>;
+    EdgeCta<H, K, G, C> c;
     c.g = threadIdx.x / H;
     c.lt = threadIdx.x % H;
-    c.st = reinterpret_cast<EdgeStage<K>*>(lamm_edge_smem) + c.g * kStages;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(lamm_edge_smem + EdgeSmem<K>::stage_bytes);
+    c.st = reinterpret_cast<EdgeStage<K, C>*>(lamm_edge_smem) + c.g * kStages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(lamm_edge_smem + Smem::stage_bytes);
     c.bar = bars + c.g * kStages;
-    c.mbar = bars + kGroups * kStages + c.g * kStages;
-    c.tslot = reinterpret_cast<uint32_t*>(bars + 2 * kGroups * kStages);
-    c.extra = reinterpret_cast<char*>(lamm_edge_smem + EdgeSmem<K>::extra_offset);
+    c.mbar = bars + G * kStages + c.g * kStages;
+    c.tslot = reinterpret_cast<uint32_t*>(bars + 2 * G * kStages);
+    c.extra = reinterpret_cast<char*>(lamm_edge_smem + Smem::extra_offset);
     if (c.lt == 0) {
         for (int s = 0; s < kStages; ++s) mbar_init(&c.bar[s], 1), mbar_init(&c.mbar[s], 1);
         mbar_fence_init();
     }
-    const int q = blockIdx.x * kGroups + c.g;  // partitions cut by k_scan
+    constexpr int per = kPartsPerCta / G;  // partitions cut by k_scan
+    const int q = blockIdx.x * kPartsPerCta + c.g * per;
     c.lo = d.part_lo[q];
-    c.hi = d.part_lo[q + 1];
+    c.hi = d.part_lo[q + per];
     return c;
 }
 
@@ -178,8 +190,8 @@ struct FilterTc {
     uint32_t idesc;
 };
 
-template <int K>
-__device__ __forceinline__ void filter_mma(uint32_t tcol, const FilterTc& f, const EdgeStage<K>& s) {
+template <int K, int C>
+__device__ __forceinline__ void filter_mma(uint32_t tcol, const FilterTc& f, const EdgeStage<K, C>& s) {
     umma::fence_after();
 #pragma unroll
     for (int ks = 0; ks < K / 8; ++ks) {
@@ -204,8 +216,8 @@ __device__ __forceinline__ void filter_mma(uint32_t tcol, const FilterTc& f, con
 //   static constexpr bool kBlockHook;  if set, block(st, e0, r, ulo, uhi) runs once
 //        per 8-edge block after its segments (segment-independent per-edge work;
 //        edges [ulo, uhi) of the block are valid); group-uniform, may group_sync
-template <int H, int K, class Body>
-__device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c, Body& body, const FilterTc& ft) {
+template <int H, int K, int G, int C, class Body>
+__device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K, G, C>& c, Body& body, const FilterTc& ft) {
     constexpr bool kF = Body::kFilter;
     constexpr int parts = Body::kParts | (kF ? kPartCanon : 0);
     pdl_enter();  // the kernel's prologue (weights, TMEM, accumulators) overlapped the previous kernel
@@ -219,13 +231,13 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
     body.begin(cur);
     if (e1 > e0) {
         const int base = e0 & ~7;  // chunks start on 8-edge blocks
-        const int nchunks = (e1 - base + kChunk - 1) / kChunk;
+        const int nchunks = (e1 - base + C - 1) / C;
         if (lead) {
-            stage_chunk<K>(d, c.st[0], &c.bar[0], base, e1, parts);
-            if (nchunks > 1) stage_chunk<K>(d, c.st[1], &c.bar[1], base + kChunk, e1, parts);
+            stage_chunk<K, C>(d, c.st[0], &c.bar[0], base, e1, parts);
+            if (nchunks > 1) stage_chunk<K, C>(d, c.st[1], &c.bar[1], base + C, e1, parts);
             if constexpr (kF) {
                 mbar_wait(&c.bar[0], 0);
-                filter_mma<K>(ft.tg, ft, c.st[0]);
+                filter_mma<K, C>(ft.tg, ft, c.st[0]);
                 umma::commit(&c.mbar[0]);
             }
         }
@@ -233,7 +245,7 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
         // consumed, across chunk boundaries (the next chunk's stage is waited for
         // at the start of the current chunk)
         typename Body::Reg rn[8];
-        auto load_block = [&](const EdgeStage<K>& sst, int blk) {
+        auto load_block = [&](const EdgeStage<K, C>& sst, int blk) {
             const int4 j0 = reinterpret_cast<const int4*>(sst.col)[2 * blk];
             const int4 j1 = reinterpret_cast<const int4*>(sst.col)[2 * blk + 1];
             const int jj[8] = {j0.x, j0.y, j0.z, j0.w, j1.x, j1.y, j1.z, j1.w};
@@ -249,7 +261,7 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
                 mbar_wait(&c.bar[s ^ 1], ((k + 1) >> 1) & 1);
                 if constexpr (kF) {
                     if (lead) {  // next chunk's filter overlaps this chunk's drain
-                        filter_mma<K>(ft.tg + (s ^ 1) * kChunk, ft, c.st[s ^ 1]);
+                        filter_mma<K, C>(ft.tg + (s ^ 1) * C, ft, c.st[s ^ 1]);
                         umma::commit(&c.mbar[s ^ 1]);
                     }
                 }
@@ -258,10 +270,10 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
                 mbar_wait(&c.mbar[s], (k >> 1) & 1);
                 umma::fence_after();
             }
-            const EdgeStage<K>& st = c.st[s];
-            const int cb = base + k * kChunk;
-            const int ea = max(cb, e0) - cb, eb = min(cb + kChunk, e1) - cb;
-            const uint32_t trow = ft.tg + s * kChunk + (quad * 32u << 16);
+            const EdgeStage<K, C>& st = c.st[s];
+            const int cb = base + k * C;
+            const int ea = max(cb, e0) - cb, eb = min(cb + C, e1) - cb;
+            const uint32_t trow = ft.tg + s * C + (quad * 32u << 16);
             const int blk0 = ea >> 3, blk1 = (eb + 7) >> 3;
             for (int blk = blk0; blk < blk1; ++blk) {
                 typename Body::Reg r[8];
@@ -303,7 +315,7 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
             }
             if constexpr (kF) umma::fence_before();
             group_sync(c.g, H);  // every thread is done with this stage (smem + TMEM)
-            if (lead && k + 2 < nchunks) stage_chunk<K>(d, c.st[s], &c.bar[s], base + (k + 2) * kChunk, e1, parts);
+            if (lead && k + 2 < nchunks) stage_chunk<K, C>(d, c.st[s], &c.bar[s], base + (k + 2) * C, e1, parts);
         }
     }
     body.end(cur);
@@ -315,8 +327,8 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K>& c,
 
 // Loads W_f of layer l as canonical hi/lo tiles and allocates the CTA's TMEM
 // (all 512 columns: kGroups x 2 stages x 64). Call from all threads.
-template <int H, int K>
-__device__ __forceinline__ FilterTc filter_setup(const Dev& d, const EdgeCta<H, K>& c, int l, float* Wh, float* Wl) {
+template <int H, int K, int G, int C>
+__device__ __forceinline__ FilterTc filter_setup(const Dev& d, const EdgeCta<H, K, G, C>& c, int l, float* Wh, float* Wl) {
     if (threadIdx.x < 32) umma::tmem_alloc(c.tslot, 512);
     const float* __restrict__ wf = d.wf[l];
     for (int idx = threadIdx.x; idx < H * K; idx += blockDim.x) {
@@ -327,7 +339,8 @@ __device__ __forceinline__ FilterTc filter_setup(const Dev& d, const EdgeCta<H, 
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
-    return FilterTc{Wh, Wl, *c.tslot + static_cast<uint32_t>(c.g * 2 * kChunk), umma::idesc_tf32(128, kChunk)};
+    static_assert(G * 2 * C <= 512, "TMEM: groups x 2 stages x chunk columns");
+    return FilterTc{Wh, Wl, *c.tslot + static_cast<uint32_t>(c.g * 2 * C), umma::idesc_tf32(128, C)};
 }
 
 __device__ __forceinline__ void filter_teardown(const uint32_t* tslot) {
@@ -336,8 +349,8 @@ __device__ __forceinline__ void filter_teardown(const uint32_t* tslot) {
     if (threadIdx.x < 32) umma::tmem_dealloc(*tslot, 512);
 }
 
-template <int K>
-__device__ __forceinline__ float filter_ffma(const float (&w)[K], const EdgeStage<K>& s, int e) {
+template <int K, int C>
+__device__ __forceinline__ float filter_ffma(const float (&w)[K], const EdgeStage<K, C>& s, int e) {
     const float4* fr = reinterpret_cast<const float4*>(s.fcp + e * K);
     float f = 0.f;
 #pragma unroll
@@ -358,7 +371,7 @@ struct EdgeKernelSmem {
     static constexpr size_t filter = TC ? 4 * 2 * H * K : 0;
     static constexpr size_t one_cta = 120 * 1024;  // > half the SM: one CTA owns the 512 TMEM columns
     static size_t pad(size_t b) { return TC && b < one_cta ? one_cta : b; }
-    static size_t message() { return pad(base + filter); }
+    static size_t message() { return pad(EdgeSmem<K, kMsgGroups, kMsgChunk>::extra_offset + filter); }
     static size_t force(int) { return base; }
     static size_t head(int D) { return base + 4 * kGroups * (3 * D * H + D * K); }
     static size_t bwd() { return pad(base + filter + 4 * kGroups * H * K); }
@@ -368,7 +381,7 @@ struct EdgeKernelSmem {
 // m_i[a] = sum_j t_j[a] * sum_k Wf[a,k] fcut_ij rbf_ijk ; mu_i = tanh(m_i)   (S/model.cpp:78-93)
 // kZ: layer 0, whose source rows are tanh(E)[Z_j - 1] (compile-time, so layers
 // >= 1 carry no predicated-off Z gathers)
-template <int H, int K, bool TC, bool kZ>
+template <int H, int K, bool TC, bool kZ, int C = kChunk>
 struct MessageBody {
     static constexpr bool kFilter = TC;
     static constexpr int kParts = TC ? 0 : kPartPlain;
@@ -383,11 +396,11 @@ struct MessageBody {
     int l, a;
     float w[K];
     float m;
-    __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
+    __device__ void load(const EdgeStage<K, C>&, int, int j, Reg& r) const {
         const int row = kZ ? __ldg(d.Z + j) - 1 : j;
         r.t = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
     }
-    __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f, unsigned on) {
+    __device__ void edge(const EdgeStage<K, C>& s, int e, const Reg& r, float f, unsigned on) {
         if constexpr (!TC) f = filter_ffma<K>(w, s, e);
         m = fmaf(r.t, on ? f : 0.f, m);
     }
@@ -396,9 +409,9 @@ struct MessageBody {
 };
 
 template <int H, int K, bool kZ>
-__global__ void __launch_bounds__(kGroups* H, 1) k_edge_message(Dev d, int l) {
+__global__ void __launch_bounds__(kMsgGroups* H, 1) k_edge_message(Dev d, int l) {
     constexpr bool TC = EdgeKernelSmem<H, K>::TC;
-    EdgeCta<H, K> c = edge_prologue<H, K>(d);
+    EdgeCta<H, K, kMsgGroups, kMsgChunk> c = edge_prologue<H, K, kMsgGroups, kMsgChunk>(d);
     FilterTc ft{};
     if constexpr (TC) {
         float* Wh = reinterpret_cast<float*>(c.extra);
@@ -406,7 +419,7 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_message(Dev d, int l) {
     } else {
         __syncthreads();
     }
-    MessageBody<H, K, TC, kZ> b{d, kZ ? d.tanh_emb : d.t[l], d.mu[l], l, c.lt};
+    MessageBody<H, K, TC, kZ, kMsgChunk> b{d, kZ ? d.tanh_emb : d.t[l], d.mu[l], l, c.lt};
     if constexpr (!TC) {
 #pragma unroll
         for (int k = 0; k < K; ++k) b.w[k] = d.wf[l][c.lt * K + k];
