@@ -205,6 +205,9 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     ensure_buf(c, "En", 8 * Bc, changed);
     ensure_buf(c, "Fn", 24 * Nc, changed);
     ensure_buf(c, "cnt", 4 * Nc, changed);
+    ensure_buf(c, "lptr", 4 * Nc, changed);
+    ensure_buf(c, "stot", 4 * Bc, changed);
+    ensure_buf(c, "soff", 4 * Bc, changed);
     ensure_buf(c, "row_ptr", 4 * (Nc + 1), changed);
     const int64_t Pp = ((Pc + kChunk + 16 + 7) / 8) * 8;  // CSR padding for the chunk staging
     ensure_buf(c, "col", 4 * Pp, changed);
@@ -304,6 +307,9 @@ Dev make_dev(Ctx& c) {
     d.tfstd = buf(c, "tfstd").as<double>();
     d.thas = buf(c, "thas").as<uint8_t>();
     d.cnt = buf(c, "cnt").as<int32_t>();
+    d.lptr = buf(c, "lptr").as<int32_t>();
+    d.stot = buf(c, "stot").as<int32_t>();
+    d.soff = buf(c, "soff").as<int32_t>();
     d.row_ptr = buf(c, "row_ptr").as<int32_t>();
     d.segw = buf(c, "segw").as<uint32_t>();
     d.col = buf(c, "col").as<int32_t>();
@@ -510,7 +516,7 @@ struct Model {
         // column split so a CTA keeps one column block (k_bwd_gemm's dW_u partials)
         c.grid_upd = c.nsm / NodeGemmCfg<H>::NS * NodeGemmCfg<H>::NS;
         c.grid_gemm = c.nsm / 2;       // split-K CTAs of dW_u (one partial each)
-        // one edge partitioning (k_scan) serves all four edge kernels: size it so
+        // one edge partitioning (k_nbr_fill) serves all four edge kernels: size it so
         // every CTA of the heaviest one is resident (no second wave)
         int occ_e = 8, o = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_message<H, K, false>, kMsgGroups * H, smem_message()));
@@ -530,13 +536,12 @@ struct Model {
     }
 
     static void prep(Ctx& c) {
-        launch(c, "prep", k_prep, c.grid_small, 128, 0, make_dev(c), make_batch_arrays(c));
+        launch(c, "prep", k_prep, c.grid_small, 128, 0, make_dev(c), make_batch_arrays(c), c.grid_edge * kPartsPerCta);
     }
 
     static void nlist(Ctx& c) {
         const Dev d = make_dev(c);
-        launch(c, "nbr_scan", k_scan, 1, 1024, 0, d, c.grid_edge * kPartsPerCta);
-        launch(c, "nbr_fill", k_nbr_fill<K>, c.grid_warp, 256, 0, d);
+        launch(c, "nbr_fill", k_nbr_fill<K>, c.grid_warp, 256, 0, d, c.grid_edge * kPartsPerCta);
     }
 
     // energy = false leaves the per-sample energies to the fused loss kernel.
@@ -795,6 +800,7 @@ int64_t edge_guess(int64_t N) { return 32 * N; }
 void run_nlist(Ctx& c) {
     for (int attempt = 0;; ++attempt) {
         c.slot_cursor = 0;
+        c.ops->prep(c);  // the per-sample counts and the row offsets live in k_prep
         c.ops->nlist(c);
         const StepHeader h = read_header(c);
         if (!h.overflow) break;

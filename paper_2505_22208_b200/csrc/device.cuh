@@ -33,7 +33,7 @@ constexpr int kMaxZ = 118;
 // Per-step scalars that live in device memory so one captured CUDA graph can
 // be replayed for device-batches of any size.
 struct StepHeader {
-    int32_t B, N, P, overflow;   // P written by the scan; overflow if P > capacity
+    int32_t B, N, P, overflow;   // P written by k_prep; overflow if P > capacity
     int32_t me, mf;              // this rank's sum m_E, sum m_F (after denoise relabelling)
     int32_t nslots, status;      // distinct atomic numbers; non-finite flag
     int32_t workers, pad0;
@@ -77,6 +77,7 @@ struct Dev {
     const uint8_t* thas;
     // edges
     int32_t *cnt, *row_ptr, *col, *dst;
+    int32_t *lptr, *stot, *soff;  // per-atom row offset inside its sample, per-sample edge totals / offsets
     uint32_t* segw;            // bit p set: edge p is the first of its destination atom
     int32_t* part_lo;          // [Q+1] edge-balanced atom partitions (edge kernels)
     float4* geo;

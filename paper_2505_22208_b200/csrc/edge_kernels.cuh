@@ -2,7 +2,7 @@
 // message, force head, head backward, layer backward), sm_100a.
 //
 // Shape of every kernel: the CSR edge list (grouped by destination atom i, j
-// ascending) is cut by k_scan into Q = gridDim.x * kGroups edge-balanced
+// ascending) is cut by k_nbr_fill into Q = gridDim.x * 12 edge-balanced
 // partitions of whole atoms. A CTA runs kGroups independent "groups" of H
 // threads; thread a of a group owns feature channel a. A group walks its
 // partition's edges in order:
@@ -34,7 +34,7 @@ namespace lamm_b200 {
 constexpr int kGroups = 4;   // independent edge streams per CTA (default geometry)
 constexpr int kChunk = 64;   // edges per staged chunk (= MMA N of the filter)
 constexpr int kStages = 2;   // staging double buffer
-// k_scan cuts kPartsPerCta partitions per CTA; a kernel with G groups gives
+// k_nbr_fill cuts kPartsPerCta partitions per CTA; a kernel with G groups gives
 // each group kPartsPerCta / G consecutive ones (G in {2, 3, 4, 6})
 constexpr int kPartsPerCta = 12;
 // geometry of the message kernel (measured: 6 groups of 32-edge chunks, 24
@@ -153,11 +153,15 @@ struct EdgeCta {
     uint64_t* mbar;  // [kStages] filter MMA
     uint32_t* tslot;
     char* extra;
-    int g, lt, lo, hi;
+    int g, lt, q, lo, hi;
+    bool late;
 };
 
+// late_parts: the partitions were cut by the previous kernel (k_nbr_fill before
+// the layer-0 message), so they are read after the dependency wait; otherwise
+// they are at least two kernels old and load with the prologue.
 template <int H, int K, int G = kGroups, int C = kChunk>
-__device__ __forceinline__ EdgeCta<H, K, G, C> edge_prologue(const Dev& d) {
+__device__ __forceinline__ EdgeCta<H, K, G, C> edge_prologue(const Dev& d, bool late_parts = false) {
     static_assert(kPartsPerCta % G == 0, "groups must divide the partitions of a CTA");
     extern __shared__ __align__(128) unsigned char lamm_edge_smem[];
     using Smem = EdgeSmem<K, G, C>;
@@ -174,10 +178,10 @@ __device__ __forceinline__ EdgeCta<H, K, G, C> edge_prologue(const Dev& d) {
         for (int s = 0; s < kStages; ++s) mbar_init(&c.bar[s], 1), mbar_init(&c.mbar[s], 1);
         mbar_fence_init();
     }
-    constexpr int per = kPartsPerCta / G;  // partitions cut by k_scan
-    const int q = blockIdx.x * kPartsPerCta + c.g * per;
-    c.lo = d.part_lo[q];
-    c.hi = d.part_lo[q + per];
+    c.q = blockIdx.x * kPartsPerCta + c.g * (kPartsPerCta / G);
+    c.late = late_parts;
+    c.lo = c.hi = 0;
+    if (!late_parts) c.lo = d.part_lo[c.q], c.hi = d.part_lo[c.q + kPartsPerCta / G];
     return c;
 }
 
@@ -221,13 +225,15 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K, G, 
     constexpr bool kF = Body::kFilter;
     constexpr int parts = Body::kParts | (kF ? kPartCanon : 0);
     pdl_enter();  // the kernel's prologue (weights, TMEM, accumulators) overlapped the previous kernel
-    if (c.lo >= c.hi) return;
-    const int e0 = d.row_ptr[c.lo], e1 = d.row_ptr[c.hi];
+    int plo = c.lo, phi = c.hi;
+    if (c.late) plo = d.part_lo[c.q], phi = d.part_lo[c.q + kPartsPerCta / G];
+    if (plo >= phi) return;
+    const int e0 = d.row_ptr[plo], e1 = d.row_ptr[phi];
     // the staging / MMA-issuing thread: lane 0 of warp g % (H/32) of the group, so the
     // four groups' leaders sit on different SM sub-partitions (warp id % 4)
     const bool lead = c.lt == 32 * (c.g % (H / 32));
     const uint32_t quad = (threadIdx.x >> 5) & 3;
-    int cur = c.lo;
+    int cur = plo;
     body.begin(cur);
     if (e1 > e0) {
         const int base = e0 & ~7;  // chunks start on 8-edge blocks
@@ -319,7 +325,7 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K, G, 
         }
     }
     body.end(cur);
-    for (int i = cur + 1; i < c.hi; ++i) {
+    for (int i = cur + 1; i < phi; ++i) {
         body.begin(i);
         body.end(i);
     }
@@ -411,7 +417,7 @@ struct MessageBody {
 template <int H, int K, bool kZ>
 __global__ void __launch_bounds__(kMsgGroups* H, 1) k_edge_message(Dev d, int l) {
     constexpr bool TC = EdgeKernelSmem<H, K>::TC;
-    EdgeCta<H, K, kMsgGroups, kMsgChunk> c = edge_prologue<H, K, kMsgGroups, kMsgChunk>(d);
+    EdgeCta<H, K, kMsgGroups, kMsgChunk> c = edge_prologue<H, K, kMsgGroups, kMsgChunk>(d, kZ);
     FilterTc ft{};
     if constexpr (TC) {
         float* Wh = reinterpret_cast<float*>(c.extra);

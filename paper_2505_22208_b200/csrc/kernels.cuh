@@ -9,7 +9,7 @@
 // Reference semantics (S = /root/reference/proj/core/src):
 //   k_prep .......... S/denoise.cpp:7-29 (centering) + S/loss.cpp:113-126 (normalize)
 //                     + the per-atom pair counts of S/core.cpp:30-48
-//   k_scan, k_nbr_fill S/core.cpp:30-48  (bit-exact fp64 pair test, i-major, j ascending)
+//   k_nbr_fill ...... S/core.cpp:30-48  (bit-exact fp64 pair test, i-major, j ascending)
 //   k_energy/k_loss . S/model.cpp:208-218 + S/loss.cpp:140-213 (Eq. 5, per-rank mask denominators)
 //   k_emb_grad ...... S/model.cpp:421-424
 //   k_grad_reduce ... sum of the per-CTA gradient partials
@@ -72,7 +72,33 @@ __device__ __forceinline__ const double* sample_cell(const Dev& d, int s) {
 }
 
 
-__global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out) {
+// Exclusive scan of one value per thread over a 128-thread block; *total gets
+// the block sum. Uses 4 ints of shared scratch; ends with a barrier.
+__device__ __forceinline__ int block_excl_scan128(int v, int* scratch, int* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+    }
+    if (lane == 31) scratch[w] = incl;
+    __syncthreads();
+    int off = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) off += k < w ? scratch[k] : 0;
+    *total = scratch[0] + scratch[1] + scratch[2] + scratch[3];
+    __syncthreads();
+    return off + incl - v;
+}
+
+// Also the CSR row offsets (S/core.cpp:30-48 order: i-major): each sample's
+// block scans its atoms' pair counts (lptr = offset inside the sample, stot =
+// sample total); the last block to finish scans the sample totals (soff), sets
+// P / the capacity-overflow flag / row_ptr[N] / the CSR padding, so the
+// neighbour fill can place every atom's row without a separate scan kernel.
+// Q: edge-kernel partitions (k_nbr_fill cuts them while writing row_ptr).
+__global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out, int Q) {
     pdl_enter();
     const StepHeader& hd = *d.hdr;
     const char* base = reinterpret_cast<const char*>(d.hdr);
@@ -92,7 +118,15 @@ __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out) {
         for (int k = threadIdx.x; k < 119; k += blockDim.x) out.z_to_slot[k] = z2s[k];
         if (threadIdx.x == 0) out.atom_ptr[B] = ap[B];
     }
+    {  // segment-start bits are OR-ed in by k_nbr_fill: clear the whole capacity
+        const int64_t words = (((static_cast<int64_t>(d.Pcap) + kChunk + 16 + 7) / 8) * 8) / 32 + 32;
+        for (int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < words;
+             x += static_cast<int64_t>(gridDim.x) * blockDim.x)
+            d.segw[x] = 0u;
+    }
     __shared__ double mean[3];
+    __shared__ int scan_scratch[4];
+    __shared__ bool last;
     for (int s = blockIdx.x; s < B; s += gridDim.x) {
         const int64_t lo = ap[s], hi = ap[s + 1];
         const int dsi = ds[s];
@@ -165,75 +199,50 @@ __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out) {
             }
             if (lane == 0) d.cnt[i] = cnt;
         }
-    }
-}
-
-// Single-CTA exclusive scan of the per-atom pair counts into row_ptr; writes P
-// and the capacity-overflow flag.
-// Also cuts the edge list into Q edge-balanced partitions of whole atoms for
-// the edge kernels: part_lo[q] = first atom i with row_ptr[i] >= floor(P q / Q),
-// part_lo[Q] = N (computed while writing row_ptr, no searches).
-__global__ void __launch_bounds__(1024) k_scan(Dev d, int Q) {
-    pdl_enter();
-    __shared__ int warp_tot[32];
-    const int N = d.hdr->N;
-    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-    const int per = (N + 1023) / 1024;
-    const int b = min(N, t * per), e = min(N, b + per);
-    int s = 0;
-    for (int k = b; k < e; ++k) s += d.cnt[k];
-    int incl = s;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-    }
-    if (lane == 31) warp_tot[wid] = incl;
-    __syncthreads();
-    if (wid == 0) {
-        int w = warp_tot[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += v;
+        __syncthreads();
+        int run = 0;  // the sample's row offsets, atoms in index order
+        for (int64_t c0 = lo; c0 < hi; c0 += blockDim.x) {
+            const int64_t a = c0 + threadIdx.x;
+            const int v = a < hi ? d.cnt[a] : 0;
+            int tot;
+            const int ex = block_excl_scan128(v, scan_scratch, &tot);
+            if (a < hi) d.lptr[a] = run + ex;
+            run += tot;
         }
-        warp_tot[lane] = w;
+        if (threadIdx.x == 0) d.stot[s] = run;
     }
+    // the last block: offsets of the samples, P, overflow, row_ptr[N], padding
+    __threadfence();
     __syncthreads();
-    int run = incl - s + (wid > 0 ? warp_tot[wid - 1] : 0);
-    const int64_t P = warp_tot[31];
-    int64_t prev = run - 1;  // row_ptr[b-1] seen as "< run" (exact value not needed: only the q range)
-    if (b > 0) prev = run - d.cnt[b - 1];
-    for (int k = b; k < e; ++k) {
-        d.row_ptr[k] = run;
-        // q in [ceil((prev+1)Q/P), ceil((run+1)Q/P) - 1] start at atom k
-        if (P > 0) {
-            const int64_t qlo = k == 0 ? 0 : ((prev + 1) * Q + P - 1) / P;
-            int64_t qhi = ((static_cast<int64_t>(run) + 1) * Q + P - 1) / P - 1;
-            if (qhi > Q - 1) qhi = Q - 1;
-            for (int64_t q = qlo; q <= qhi; ++q) d.part_lo[q] = k;
-        }
-        prev = run;
-        run += d.cnt[k];
+    if (threadIdx.x == 0) last = atomicAdd(&d.hdr->done_counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    int run = 0;
+    for (int c0 = 0; c0 < B; c0 += blockDim.x) {
+        const int s = c0 + threadIdx.x;
+        const int v = s < B ? d.stot[s] : 0;
+        int tot;
+        const int ex = block_excl_scan128(v, scan_scratch, &tot);
+        if (s < B) d.soff[s] = run + ex;
+        run += tot;
     }
-    if (P > 0 && e == N && b < e) {  // targets in (row_ptr[N-1], P] start at atom N
-        const int64_t qlo = ((prev + 1) * Q + P - 1) / P;
-        for (int64_t q = qlo; q < Q; ++q) d.part_lo[q] = N;
-    }
-    if (P == 0)
-        for (int q = t; q < Q; q += 1024) d.part_lo[q] = 0;
-    // CSR padding read by the edge kernels' block staging: valid source atom 0
-    if (P <= d.Pcap) {
-        for (int x = t; x < kChunk + 8; x += 1024) d.col[P + x] = 0, d.dst[P + x] = N;
-        // segment-start bits, set by k_nbr_fill (+ the padding words the staging reads)
-        for (int x = t; x < (P + kChunk + 8) / 32 + 16; x += 1024) d.segw[x] = 0u;
-    }
-    if (t == 1023) {
-        d.row_ptr[N] = run;
-        d.part_lo[Q] = N;
+    const int N = hd.N;
+    const bool over = static_cast<int64_t>(run) > d.Pcap;
+    if (threadIdx.x == 0) {
         d.hdr->P = run;
-        d.hdr->overflow = static_cast<int64_t>(run) > d.Pcap ? 1 : 0;
+        d.hdr->overflow = over ? 1 : 0;
+        d.row_ptr[N] = run;
+        d.hdr->done_counter = 0;
     }
+    // partitions: cut by k_nbr_fill when there are edges; all empty on overflow
+    // (the step is discarded and rerun with more capacity); no edges: the last
+    // partition walks every atom (edge-less begin/end)
+    if (over || run == 0)
+        for (int q = threadIdx.x; q < Q; q += blockDim.x) d.part_lo[q] = 0;
+    if (threadIdx.x == 0) d.part_lo[Q] = over ? 0 : N;
+    if (!over)  // CSR padding read by the edge kernels' block staging: valid source atom 0
+        for (int x = threadIdx.x; x < kChunk + 8; x += blockDim.x) d.col[run + x] = 0, d.dst[run + x] = N;
 }
 
 // Same sweep as the count in k_prep; lanes that hold a neighbour compact into the CSR
@@ -241,10 +250,11 @@ __global__ void __launch_bounds__(1024) k_scan(Dev d, int Q) {
 // rounded once: unit (1/r)*d (S/core.cpp:43), fcut (S/model.cpp:17), Gaussians
 // (S/model.cpp:20-27).
 template <int K>
-__global__ void __launch_bounds__(256) k_nbr_fill(Dev d) {
+__global__ void __launch_bounds__(256) k_nbr_fill(Dev d, int Q) {
     pdl_enter();
     if (d.hdr->overflow) return;
     const int N = d.hdr->N;
+    const int64_t P = d.hdr->P;
     const int lane = threadIdx.x & 31;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     const double width = d.rc / static_cast<double>(K - 1);
@@ -255,8 +265,22 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d) {
         const int lo = static_cast<int>(d.atom_ptr[s]), hi = static_cast<int>(d.atom_ptr[s + 1]);
         const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
         const double* cell = sample_cell(d, s);
-        int base = d.row_ptr[i];
-        if (lane == 0 && d.row_ptr[i + 1] > base) atomicOr(d.segw + (base >> 5), 1u << (base & 31));
+        int base = d.soff[s] + d.lptr[i];
+        if (lane == 0) {
+            const int ci = d.cnt[i];
+            d.row_ptr[i] = base;
+            if (ci > 0) atomicOr(d.segw + (base >> 5), 1u << (base & 31));
+            // edge-kernel partitions: part_lo[q] = first atom with row_ptr >= floor(P q / Q)
+            if (P > 0) {
+                const int64_t prev = i == 0 ? -1 : base - d.cnt[i - 1];  // row_ptr[i - 1]
+                const int64_t qlo = i == 0 ? 0 : ((prev + 1) * Q + P - 1) / P;
+                int64_t qhi = ((static_cast<int64_t>(base) + 1) * Q + P - 1) / P - 1;
+                if (qhi > Q - 1) qhi = Q - 1;
+                for (int64_t q = qlo; q <= qhi; ++q) d.part_lo[q] = i;
+                if (i == N - 1)  // targets in (row_ptr[N-1], P] start at atom N
+                    for (int64_t q = ((static_cast<int64_t>(base) + 1) * Q + P - 1) / P; q < Q; ++q) d.part_lo[q] = N;
+            }
+        }
         for (int j0 = lo; j0 < hi; j0 += 32) {
             const int j = j0 + lane;
             bool in = false;
