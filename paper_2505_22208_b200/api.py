@@ -31,10 +31,12 @@ from ._lib import (BatchViewC, EvalResultC, InputError, LossBreakdownC, LossConf
 
 
 def _p(a):
-    return None if a is None else a.ctypes.data_as(C.c_void_p)
+    return None if a is None else C.c_void_p(a.__array_interface__["data"][0])
 
 
 def _c(a, dt):
+    if isinstance(a, np.ndarray) and a.dtype == dt and a.flags.c_contiguous:
+        return a  # the per-step fast path: no copy, no conversion
     return np.ascontiguousarray(a, dtype=dt)
 
 
@@ -94,21 +96,27 @@ def init_params(cfg: ModelConfig, seed: int) -> np.ndarray:
 
 
 def _batch_view(b: dict):
+    ap = _c(b["atom_ptr"], np.int64)
+    B = len(ap) - 1
+
+    def opt(key, dt, shape):  # optional per-sample / per-atom arrays (zeros when absent)
+        v = b.get(key)
+        return _c(v, dt) if v is not None else np.zeros(shape, dt)
+
     keep = {
-        "atom_ptr": _c(b["atom_ptr"], np.int64), "pos": _c(b["pos"], np.float64), "Z": _c(b["Z"], np.int32),
-        "dataset_index": _c(b.get("dataset_index", np.zeros(len(b["atom_ptr"]) - 1)), np.int32),
-        "energy_mask": _c(b.get("energy_mask", np.zeros(len(b["atom_ptr"]) - 1)), np.uint8),
-        "force_mask": _c(b.get("force_mask", np.zeros(len(b["atom_ptr"]) - 1)), np.uint8),
-        "energy": _c(b.get("energy", np.zeros(len(b["atom_ptr"]) - 1)), np.float64),
-        "forces": _c(b.get("forces", np.zeros((len(b["Z"]), 3))), np.float64),
-        "denoise": _c(b.get("denoise", np.zeros(len(b["atom_ptr"]) - 1)), np.uint8),
+        "atom_ptr": ap, "pos": _c(b["pos"], np.float64), "Z": _c(b["Z"], np.int32),
+        "dataset_index": opt("dataset_index", np.int32, B), "energy_mask": opt("energy_mask", np.uint8, B),
+        "force_mask": opt("force_mask", np.uint8, B), "energy": opt("energy", np.float64, B),
+        "forces": opt("forces", np.float64, (len(b["Z"]), 3)), "denoise": opt("denoise", np.uint8, B),
     }
-    B = len(keep["atom_ptr"]) - 1
     if b.get("cell") is not None:  # periodic cells [B, 3, 3] (all-zero: non-periodic sample)
         keep["cell"] = _c(np.asarray(b["cell"]).reshape(B, 9), np.float64)
-    v = BatchViewC(B, int(keep["atom_ptr"][-1]), _p(keep["atom_ptr"]), _p(keep["pos"]), _p(keep["Z"]),
-                   _p(keep["dataset_index"]), _p(keep["energy_mask"]), _p(keep["force_mask"]), _p(keep["energy"]),
-                   _p(keep["forces"]), _p(keep["denoise"]), _p(keep["cell"]) if "cell" in keep else None)
+    def addr(k):  # c_void_p structure fields take the integer address directly
+        return keep[k].__array_interface__["data"][0]
+
+    v = BatchViewC(B, int(ap[-1]), addr("atom_ptr"), addr("pos"), addr("Z"), addr("dataset_index"),
+                   addr("energy_mask"), addr("force_mask"), addr("energy"), addr("forces"), addr("denoise"),
+                   addr("cell") if "cell" in keep else None)
     return v, keep
 
 
