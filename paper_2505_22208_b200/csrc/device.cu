@@ -218,6 +218,13 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     ensure_buf(c, "rbfl", 4 * static_cast<size_t>(Pp) * K, changed);
     ensure_buf(c, "rbfp", 4 * static_cast<size_t>(Pp) * K, changed);
     ensure_buf(c, "part_lo", 4 * (static_cast<size_t>(c.grid_edge) * kPartsPerCta + 1), changed);
+    ensure_buf(c, "cgrid", sizeof(CellGrid) * Bc, changed);
+    ensure_buf(c, "acell", 4 * Nc, changed);
+    ensure_buf(c, "cstart", 4 * (4 * Nc + 65 * Bc + 1), changed);
+    ensure_buf(c, "cpos", 32 * Nc, changed);
+    ensure_buf(c, "sdone", 4 * Bc, changed);
+    ensure_buf(c, "eatom", 8 * Nc, changed);
+    ensure_buf(c, "fterm", 8 * Nc, changed);
     if (c.export64) {
         ensure_buf(c, "dist64", 8 * Pc, changed);
         ensure_buf(c, "unit64", 24 * Pc, changed);
@@ -315,6 +322,13 @@ Dev make_dev(Ctx& c) {
     d.col = buf(c, "col").as<int32_t>();
     d.dst = buf(c, "dst").as<int32_t>();
     d.part_lo = buf(c, "part_lo").as<int32_t>();
+    d.cgrid = buf(c, "cgrid").as<CellGrid>();
+    d.acell = buf(c, "acell").as<int32_t>();
+    d.cstart = buf(c, "cstart").as<int32_t>();
+    d.cpos = buf(c, "cpos").as<double4>();
+    d.sdone = buf(c, "sdone").as<uint32_t>();
+    d.eatom = buf(c, "eatom").as<double>();
+    d.fterm = buf(c, "fterm").as<double>();
     d.geo = buf(c, "geo").as<float4>();
     d.rbf = buf(c, "rbf").as<float>();
     d.rbfl = buf(c, "rbfl").as<float>();
@@ -541,6 +555,7 @@ struct Model {
 
     static void nlist(Ctx& c) {
         const Dev d = make_dev(c);
+        launch(c, "cell_count", k_cell_count, c.grid_warp, 256, 0, d, c.grid_edge * kPartsPerCta);
         launch(c, "nbr_fill", k_nbr_fill<K>, c.grid_warp, 256, 0, d, c.grid_edge * kPartsPerCta);
     }
 
@@ -561,8 +576,8 @@ struct Model {
     static void loss(Ctx& c, bool energy) {
         const Dev d = make_dev(c);
         // the train step (energy fused here) only needs the compact per-atom force gradient
-        launch(c, "loss", k_loss, c.grid_small, 128, energy ? sizeof(double) * 128 * c.D : 0, d, energy ? 1 : 0,
-               energy ? 0 : 1);
+        // (with k_force_out's per-atom energies and force terms: forward(c, false))
+        launch(c, "loss", k_loss, c.grid_small, 128, 0, d, energy ? 2 : 0, energy ? 0 : 1);
     }
 
     static void backward(Ctx& c, bool general) {
@@ -768,6 +783,8 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
     h.lambda_e = tc ? tc->lambda_energy : 1.0;
     h.lambda_f = tc ? tc->lambda_force : 1.0;
     h.workers = 1;
+    h.n_large = 0;
+    for (int32_t s = 0; s < B; ++s) h.n_large += b->atom_ptr[s + 1] - b->atom_ptr[s] > kSmallAtoms ? 1 : 0;
     std::memcpy(base, &h, sizeof(StepHeader));
     // host mirror
     c.B = B, c.N = N, c.me = me, c.mf = mf;

@@ -32,15 +32,31 @@ constexpr int kMaxZ = 118;
 
 // Per-step scalars that live in device memory so one captured CUDA graph can
 // be replayed for device-batches of any size.
+// Samples with more atoms than this get a cell list (k_prep bins, k_cell_count
+// counts, k_nbr_fill walks the 27 neighbour cells); smaller ones are swept
+// brute force by the sample's own block.
+constexpr int kSmallAtoms = 128;
+
+// Uniform grid over one sample: non-periodic — the bounding box cut into cells of
+// width >= rc (1 + 1e-9); periodic — n[k] slabs of fractional coordinate k, each
+// at least rc (1 + 1e-9) wide perpendicular to the face. Either way two atoms
+// within rc sit in the same or adjacent cells (wrapped when periodic), so the
+// exact pair test over the neighbour cells finds the brute-force pair set.
+struct CellGrid {
+    double lo[3], scale[3];  // non-periodic: cell k = floor((x_k - lo_k) * scale_k)
+    int n[3], periodic;
+    int base, pad;           // region of the sample's cell offsets in Dev::cstart
+};
+
 struct StepHeader {
     int32_t B, N, P, overflow;   // P written by k_prep; overflow if P > capacity
     int32_t me, mf;              // this rank's sum m_E, sum m_F (after denoise relabelling)
     int32_t nslots, status;      // distinct atomic numbers; non-finite flag
-    int32_t workers, pad0;
+    int32_t workers, n_large;    // n_large: samples above kSmallAtoms (cell-list neighbour search)
     double lambda_e, lambda_f;
     double loss_energy, loss_force, loss_total;  // this rank's Eq. (5) breakdown
     double grad_norm, clip_scale, global_loss;
-    uint32_t done_counter, pad1;
+    uint32_t done_counter, large_done;
     // byte offsets of the staged input arrays inside the upload blob (the blob
     // starts with this header), see device.cu:pack_batch
     int64_t off_atom_ptr, off_pos, off_Z, off_z2s, off_dsidx, off_emask, off_fmask, off_denoise, off_E, off_F,
@@ -80,6 +96,12 @@ struct Dev {
     int32_t *lptr, *stot, *soff;  // per-atom row offset inside its sample, per-sample edge totals / offsets
     uint32_t* segw;            // bit p set: edge p is the first of its destination atom
     int32_t* part_lo;          // [Q+1] edge-balanced atom partitions (edge kernels)
+    // cell lists of the large samples (k_prep bins, k_cell_count / k_nbr_fill walk)
+    CellGrid* cgrid;           // [B]
+    int32_t* acell;            // [N]  linear cell of the atom inside its sample's grid
+    int32_t* cstart;           // [4 N + 65 B + 1] per-sample cell offsets (region 4 lo + 65 s)
+    double4* cpos;             // [N]  the sample's atoms ordered by cell: x, y, z, j (bits)
+    uint32_t* sdone;           // [B]  atoms of the sample counted (k_cell_count)
     float4* geo;
     float* rbf;                // [P][K] fcut * Gaussians, canonical tcgen05 layout, tf32 hi part
     float* rbfl;               //        ... and the fp32 lo remainder
@@ -104,6 +126,8 @@ struct Dev {
     float* gE;               // [B][D]
     float* gF;               // [N][D][3]
     float4* gFc;             // [N] dL/dF of the atom's own head (loss path), w = 0
+    double* eatom;           // [N] sum_a h^L[i,a] W_e[a,d_i] (train step: own head)
+    double* fterm;           // [N] the atom's Eq. (5) force term m_F w_F / n ||dF||
     double* sample_terms;    // [B][2]
     double* block_scratch;   // reduction scratch
     // backward

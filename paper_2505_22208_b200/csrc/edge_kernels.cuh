@@ -545,12 +545,13 @@ __device__ __forceinline__ void force_out_round(const float* WaT, const float* W
 template <int H, int K>
 __global__ void __launch_bounds__(256) k_force_out(Dev d, int own_head) {
     constexpr int C = H / 32, YW = ForceBody<H, K>::kYW;
-    __shared__ __align__(16) float WaT[kMaxHeads * H], WbT[kMaxHeads * H], WcT[kMaxHeads * 32];
+    __shared__ __align__(16) float WaT[kMaxHeads * H], WbT[kMaxHeads * H], WcT[kMaxHeads * 32], WeT[kMaxHeads * H];
     const int D = d.D, ND = 3 * D, L = d.L;
     for (int idx = threadIdx.x; idx < D * H; idx += blockDim.x) {
         const int dd = idx / H, aa = idx % H;
         WaT[idx] = d.wfh[aa * D + dd];
         WbT[idx] = d.wfh[(H + aa) * D + dd];
+        WeT[idx] = d.we[aa * D + dd];
     }
     for (int idx = threadIdx.x; idx < D * 32; idx += blockDim.x) {
         const int dd = idx / 32, k = idx % 32;
@@ -596,6 +597,39 @@ __global__ void __launch_bounds__(256) k_force_out(Dev d, int own_head) {
 #pragma unroll
             for (int x = 0; x < 3; ++x) sx[x] = warp_sum(sx[x]);
             if (lane < 3) out[dd * 3 + lane] = lane == 0 ? sx[0] : (lane == 1 ? sx[1] : sx[2]);
+            // the atom's share of its sample's loss (k_loss sums them per sample):
+            // energy e_i = sum_a h^L[i,a] W_e[a,d] (S/model.cpp:208-218) and the
+            // Eq. (5) force term with its gradient (S/loss.cpp:186-212)
+            const VecF<C> hv = ldv<C>(d.h[L] + static_cast<int64_t>(i) * H + lane * C);
+            const VecF<C> we = ldv<C>(WeT + dd * H + lane * C);
+            double e = 0.0;
+#pragma unroll
+            for (int cc = 0; cc < C; ++cc) e = fma(static_cast<double>(hv.v[cc]), static_cast<double>(we.v[cc]), e);
+            e = warp_sum_d(e);
+            if (lane == 0) {
+                const int s = d.sample_of[i];
+                float4 gc = make_float4(0.f, 0.f, 0.f, 0.f);
+                double ft = 0.0;
+                if (d.fmask[s]) {
+                    const int mf = d.hdr->mf;
+                    const double ws = (mf > 0 ? d.hdr->lambda_f / static_cast<double>(mf) : 0.0) /
+                                      static_cast<double>(d.atom_ptr[s + 1] - d.atom_ptr[s]);
+                    double df[3], sq = 0.0;
+#pragma unroll
+                    for (int x = 0; x < 3; ++x) {
+                        df[x] = static_cast<double>(sx[x]) - d.Fn[3 * static_cast<int64_t>(i) + x];
+                        sq += df[x] * df[x];
+                    }
+                    const double dist = sqrt(sq);
+                    ft = ws * dist;
+                    if (dist > 0.0)
+                        gc = make_float4(static_cast<float>(ws * df[0] / dist), static_cast<float>(ws * df[1] / dist),
+                                         static_cast<float>(ws * df[2] / dist), 0.f);
+                }
+                d.eatom[i] = e;
+                d.fterm[i] = ft;
+                d.gFc[i] = gc;
+            }
             continue;
         }
         force_out_round<H, K, 0>(WaT, WbT, WcT, D, ND, lane, ti, yv, u, vk, out);

@@ -92,6 +92,201 @@ __device__ __forceinline__ int block_excl_scan128(int v, int* scratch, int* tota
     return off + incl - v;
 }
 
+__device__ __forceinline__ int warp_incl_scan(int v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int x = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += x;
+    }
+    return v;
+}
+
+// ------------------------------------------------------------ cell lists ---
+// Cell of a position in its sample's grid (device.cuh:CellGrid). Binning need not
+// be exact — the pair test over the neighbour cells is — only consistent: the
+// cell is computed once per atom (k_prep) and stored in acell.
+__device__ __forceinline__ int cell_index(const CellGrid& g, const double* cell, double x, double y, double z) {
+    int q[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double t;
+        if (g.periodic) {
+            const double* ci = cell + 9;
+            t = (x * ci[k] + y * ci[3 + k]) + z * ci[6 + k];
+            t = (t - floor(t)) * g.n[k];
+        } else {
+            t = ((k == 0 ? x : (k == 1 ? y : z)) - g.lo[k]) * g.scale[k];
+        }
+        q[k] = min(max(static_cast<int>(t), 0), g.n[k] - 1);
+    }
+    return (q[0] * g.n[1] + q[1]) * g.n[2] + q[2];
+}
+
+// Neighbour cell along one axis: c + o (o in -1..1), wrapped when periodic with
+// each distinct cell visited once (n = 1: only o = 0; n = 2: o = 0, 1); false
+// when the cell does not exist.
+__device__ __forceinline__ bool cell_step(const CellGrid& g, int k, int c, int o, int& out) {
+    const int n = g.n[k];
+    if (g.periodic) {
+        if (n == 1 && o != 0) return false;
+        if (n == 2 && o < 0) return false;
+        out = (c + o + n) % n;
+        return true;
+    }
+    out = c + o;
+    return out >= 0 && out < n;
+}
+
+// Calls f(begin, end) — a range of the sample's cell-ordered atoms (cpos) — for
+// every distinct cell adjacent to (and including) cell c.
+template <class F>
+__device__ __forceinline__ void for_neighbour_cells(const Dev& d, const CellGrid& g, int c, F&& f) {
+    const int c2 = c % g.n[2], c1 = (c / g.n[2]) % g.n[1], c0 = c / (g.n[1] * g.n[2]);
+    const int32_t* cs = d.cstart + g.base;
+    for (int o0 = -1; o0 <= 1; ++o0) {
+        int x0;
+        if (!cell_step(g, 0, c0, o0, x0)) continue;
+        for (int o1 = -1; o1 <= 1; ++o1) {
+            int x1;
+            if (!cell_step(g, 1, c1, o1, x1)) continue;
+            for (int o2 = -1; o2 <= 1; ++o2) {
+                int x2;
+                if (!cell_step(g, 2, c2, o2, x2)) continue;
+                const int q = (x0 * g.n[1] + x1) * g.n[2] + x2;
+                f(__ldg(cs + q), __ldg(cs + q + 1));
+            }
+        }
+    }
+}
+
+// Block-wide (128 threads): the grid of sample s (bounding box or lattice), each
+// atom's cell, a counting sort of the atoms by cell into cpos, and the cell
+// offsets. lptr holds the atom's rank inside its cell until k_cell_count
+// overwrites it with the row offset.
+__device__ void bin_sample(const Dev& d, int s, int64_t lo, int64_t hi, const double* cell) {
+    __shared__ double red[4][6];
+    __shared__ CellGrid sg;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t a = lo + tid; a < hi; a += blockDim.x) {
+        const double p[3] = {d.x[a], d.y[a], d.z[a]};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) mn[k] = fmin(mn[k], p[k]), mx[k] = fmax(mx[k], p[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[k] = fmin(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
+            mx[k] = fmax(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
+        }
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) red[w][k] = mn[k], red[w][3 + k] = mx[k];
+    __syncthreads();
+    if (tid == 0) {
+        CellGrid g{};
+        const double s0 = d.rc * (1.0 + 1e-9);  // slack far above the binning's rounding
+        double amax = 0.0;
+        for (int k = 0; k < 3; ++k) {
+            for (int q = 1; q < 4; ++q) red[0][k] = fmin(red[0][k], red[q][k]), red[0][3 + k] = fmax(red[0][3 + k], red[q][3 + k]);
+            amax = fmax(amax, fmax(fabs(red[0][k]), fabs(red[0][3 + k])));
+        }
+        g.periodic = cell != nullptr;
+        bool ok = true;
+        for (int k = 0; k < 3; ++k) {
+            double cells;
+            if (g.periodic) {  // slab width along lattice direction k = 1 / |column k of cell^-1|
+                const double* ci = cell + 9;
+                const double b = sqrt(ci[k] * ci[k] + ci[3 + k] * ci[3 + k] + ci[6 + k] * ci[6 + k]);
+                cells = floor(1.0 / (b * s0));
+                ok &= amax * b < 1e3;  // fractional coordinates small enough to bin accurately
+            } else {
+                const double ext = red[0][3 + k] - red[0][k];
+                cells = floor(ext / s0);
+                ok &= ext < 1e7;
+                g.lo[k] = red[0][k];
+                g.scale[k] = cells >= 1.0 ? fmin(cells, 1024.0) / ext : 0.0;
+            }
+            g.n[k] = static_cast<int>(fmax(1.0, fmin(cells, 1024.0)));
+        }
+        if (!ok) g.n[0] = g.n[1] = g.n[2] = 1;  // degenerate input: one cell = brute force
+        // at most 4 cells per atom (+64): halve the finest axis (wider cells stay valid)
+        const int64_t cap = 4 * (hi - lo) + 64;
+        while (static_cast<int64_t>(g.n[0]) * g.n[1] * g.n[2] > cap) {
+            const int k = g.n[0] >= g.n[1] && g.n[0] >= g.n[2] ? 0 : (g.n[1] >= g.n[2] ? 1 : 2);
+            const int n2 = max(1, g.n[k] / 2);
+            if (!g.periodic && g.scale[k] != 0.0) g.scale[k] *= static_cast<double>(n2) / g.n[k];
+            g.n[k] = n2;
+        }
+        g.base = static_cast<int>(4 * lo + 65 * static_cast<int64_t>(s));
+        sg = g;
+        d.cgrid[s] = g;
+        d.sdone[s] = 0u;
+    }
+    __syncthreads();
+    const CellGrid g = sg;
+    const int ncell = g.n[0] * g.n[1] * g.n[2];
+    int32_t* cs = d.cstart + g.base;
+    for (int q = tid; q <= ncell; q += blockDim.x) cs[q] = 0;
+    __syncthreads();
+    for (int64_t a = lo + tid; a < hi; a += blockDim.x) {
+        const int c = cell_index(g, cell, d.x[a], d.y[a], d.z[a]);
+        d.acell[a] = c;
+        d.lptr[a] = atomicAdd(cs + c, 1);
+    }
+    __syncthreads();
+    __shared__ int scratch[4];
+    int run = 0;
+    for (int q0 = 0; q0 < ncell; q0 += blockDim.x) {
+        const int q = q0 + tid;
+        const int v = q < ncell ? __ldcg(cs + q) : 0;
+        int tot;
+        const int ex = block_excl_scan128(v, scratch, &tot);
+        if (q < ncell) cs[q] = run + ex;
+        run += tot;
+    }
+    if (tid == 0) cs[ncell] = run;
+    __syncthreads();
+    for (int64_t a = lo + tid; a < hi; a += blockDim.x) {
+        const int at = __ldcg(cs + d.acell[a]) + d.lptr[a];
+        d.cpos[lo + at] = make_double4(d.x[a], d.y[a], d.z[a], __longlong_as_double(a));
+    }
+}
+
+// The sample offsets (scan of the per-sample pair totals), P, the capacity flag,
+// row_ptr[N], the partition defaults and the CSR padding; one warp, after every
+// sample's total is final (the last block of k_prep, or the last sample of
+// k_cell_count when the batch has cell-list samples).
+__device__ void finalize_csr_warp(const Dev& d, int Q) {
+    const int lane = threadIdx.x & 31;
+    const int B = d.hdr->B, N = d.hdr->N;
+    int run = 0;
+    for (int s0 = 0; s0 < B; s0 += 32) {
+        const int s = s0 + lane;
+        const int v = s < B ? __ldcg(d.stot + s) : 0;
+        const int incl = warp_incl_scan(v);
+        if (s < B) d.soff[s] = run + incl - v;
+        run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    const bool over = static_cast<int64_t>(run) > d.Pcap;
+    if (lane == 0) {
+        d.hdr->P = run;
+        d.hdr->overflow = over ? 1 : 0;
+        d.row_ptr[N] = run;
+    }
+    // partitions: cut by k_nbr_fill when there are edges; all empty on overflow
+    // (the step is discarded and rerun with more capacity); no edges: the last
+    // partition walks every atom (edge-less begin/end)
+    if (over || run == 0)
+        for (int q = lane; q < Q; q += 32) d.part_lo[q] = 0;
+    if (lane == 0) d.part_lo[Q] = over ? 0 : N;
+    if (!over)  // CSR padding read by the edge kernels' block staging: valid source atom 0
+        for (int x = lane; x < kChunk + 8; x += 32) d.col[run + x] = 0, d.dst[run + x] = N;
+}
+
+
 // Also the CSR row offsets (S/core.cpp:30-48 order: i-major): each sample's
 // block scans its atoms' pair counts (lptr = offset inside the sample, stot =
 // sample total); the last block to finish scans the sample totals (soff), sets
@@ -125,6 +320,7 @@ __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out, int Q) {
             d.segw[x] = 0u;
     }
     __shared__ double mean[3];
+    __shared__ double stage[4][128];
     __shared__ int scan_scratch[4];
     __shared__ bool last;
     for (int s = blockIdx.x; s < B; s += gridDim.x) {
@@ -137,24 +333,44 @@ __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out, int Q) {
             out.emask[s] = em[s];
             out.fmask[s] = fm[s];
             out.denoise[s] = dn[s];
-            double m0 = 0.0, m1 = 0.0, m2 = 0.0;
-            if (is_dn && d.denoise_scheme) {  // S/denoise.cpp:14-19, sequential sum then (1/n)*sum
-                for (int64_t a = lo; a < hi; ++a) {
-                    m0 = __dadd_rn(m0, noise[3 * a]);
-                    m1 = __dadd_rn(m1, noise[3 * a + 1]);
-                    m2 = __dadd_rn(m2, noise[3 * a + 2]);
+        }
+        // S/denoise.cpp:14-19 (sequential sum, then (1/n) * sum) and S/loss.cpp:117-121
+        // (sequential sum of the reference energies): the per-atom terms are staged
+        // 128 at a time in shared memory and thread 0 adds them in index order
+        const bool need_mean = is_dn && d.denoise_scheme, need_tab = d.use_table && em[s];
+        double m0 = 0.0, m1 = 0.0, m2 = 0.0, total = 0.0;
+        if (need_mean || need_tab) {
+            for (int64_t c0 = lo; c0 < hi; c0 += 128) {
+                const int64_t a = c0 + threadIdx.x;
+                if (a < hi) {
+                    if (need_mean)
+                        stage[0][threadIdx.x] = noise[3 * a], stage[1][threadIdx.x] = noise[3 * a + 1],
+                        stage[2][threadIdx.x] = noise[3 * a + 2];
+                    if (need_tab) {  // absent element: -0.0 leaves the sum unchanged, as the skip does
+                        const int z = Z[a];
+                        stage[3][threadIdx.x] = d.rho_has[dsi * 119 + z] ? d.rho[dsi * 119 + z] : -0.0;
+                    }
                 }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    const int n = static_cast<int>(hi - c0 < 128 ? hi - c0 : 128);
+                    if (need_mean)
+                        for (int k = 0; k < n; ++k)
+                            m0 = __dadd_rn(m0, stage[0][k]), m1 = __dadd_rn(m1, stage[1][k]), m2 = __dadd_rn(m2, stage[2][k]);
+                    if (need_tab)
+                        for (int k = 0; k < n; ++k) total = __dadd_rn(total, stage[3][k]);
+                }
+                __syncthreads();
+            }
+        }
+        if (threadIdx.x == 0) {
+            if (need_mean) {
                 const double sc = __ddiv_rn(1.0, static_cast<double>(hi - lo));
                 m0 = __dmul_rn(sc, m0), m1 = __dmul_rn(sc, m1), m2 = __dmul_rn(sc, m2);
             }
             mean[0] = m0, mean[1] = m1, mean[2] = m2;
             double e = E[s];
-            if (d.use_table && em[s]) {  // S/loss.cpp:117-121
-                double total = 0.0;
-                for (int64_t a = lo; a < hi; ++a)
-                    if (d.rho_has[dsi * 119 + Z[a]]) total = __dadd_rn(total, d.rho[dsi * 119 + Z[a]]);
-                e = __ddiv_rn(__dsub_rn(__dsub_rn(e, total), d.tmean[dsi]), d.tstd[dsi]);
-            }
+            if (need_tab) e = __ddiv_rn(__dsub_rn(__dsub_rn(e, total), d.tmean[dsi]), d.tstd[dsi]);
             d.En[s] = e;
         }
         __syncthreads();
@@ -181,10 +397,15 @@ __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out, int Q) {
             d.x[a] = xyz[0], d.y[a] = xyz[1], d.z[a] = xyz[2];
         }
         __syncthreads();
+        const double* cell = sample_cell(d, s);
+        if (hi - lo > kSmallAtoms) {  // counted over its cell list by k_cell_count
+            bin_sample(d, s, lo, hi, cell);
+            __syncthreads();
+            continue;
+        }
         // neighbour counts of the sample (S/core.cpp:30-48), warp per atom, from the
         // positions this block just wrote (plain loads: visible after the barrier)
         const int lane = threadIdx.x & 31;
-        const double* cell = sample_cell(d, s);
         for (int64_t i = lo + (threadIdx.x >> 5); i < hi; i += blockDim.x >> 5) {
             const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
             int cnt = 0;
@@ -211,55 +432,150 @@ __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out, int Q) {
         }
         if (threadIdx.x == 0) d.stot[s] = run;
     }
-    // the last block: offsets of the samples, P, overflow, row_ptr[N], padding
+    // the last block: offsets of the samples, P, overflow, row_ptr[N], padding —
+    // unless cell-list samples are still to be counted (k_cell_count does it then)
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) last = atomicAdd(&d.hdr->done_counter, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!last) return;
     __threadfence();
-    int run = 0;
-    for (int c0 = 0; c0 < B; c0 += blockDim.x) {
-        const int s = c0 + threadIdx.x;
-        const int v = s < B ? d.stot[s] : 0;
-        int tot;
-        const int ex = block_excl_scan128(v, scan_scratch, &tot);
-        if (s < B) d.soff[s] = run + ex;
-        run += tot;
-    }
-    const int N = hd.N;
-    const bool over = static_cast<int64_t>(run) > d.Pcap;
-    if (threadIdx.x == 0) {
-        d.hdr->P = run;
-        d.hdr->overflow = over ? 1 : 0;
-        d.row_ptr[N] = run;
-        d.hdr->done_counter = 0;
-    }
-    // partitions: cut by k_nbr_fill when there are edges; all empty on overflow
-    // (the step is discarded and rerun with more capacity); no edges: the last
-    // partition walks every atom (edge-less begin/end)
-    if (over || run == 0)
-        for (int q = threadIdx.x; q < Q; q += blockDim.x) d.part_lo[q] = 0;
-    if (threadIdx.x == 0) d.part_lo[Q] = over ? 0 : N;
-    if (!over)  // CSR padding read by the edge kernels' block staging: valid source atom 0
-        for (int x = threadIdx.x; x < kChunk + 8; x += blockDim.x) d.col[run + x] = 0, d.dst[run + x] = N;
+    if (hd.n_large == 0 && threadIdx.x < 32) finalize_csr_warp(d, Q);
+    if (threadIdx.x == 0) d.hdr->done_counter = 0;
 }
 
-// Same sweep as the count in k_prep; lanes that hold a neighbour compact into the CSR
-// row with popc(ballot & lanes_below). Edge geometry is computed in fp64 and
-// rounded once: unit (1/r)*d (S/core.cpp:43), fcut (S/model.cpp:17), Gaussians
-// (S/model.cpp:20-27).
+// Pair counts of the atoms of cell-list samples (kSmallAtoms < n), warp per atom
+// over the grid: the exact test of k_prep's sweep against the atoms of the 27
+// neighbour cells. The warp that counts a sample's last atom scans the sample's
+// row offsets; the one that finishes the last such sample runs finalize_csr_warp.
+__global__ void __launch_bounds__(256) k_cell_count(Dev d, int Q) {
+    pdl_enter();
+    const StepHeader& hd = *d.hdr;
+    const int n_large = hd.n_large;
+    if (n_large == 0) return;
+    const int N = hd.N;
+    const int lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
+        const int s = d.sample_of[i];
+        const int lo = static_cast<int>(d.atom_ptr[s]), hi = static_cast<int>(d.atom_ptr[s + 1]);
+        if (hi - lo <= kSmallAtoms) continue;
+        const CellGrid g = d.cgrid[s];
+        const double* cell = sample_cell(d, s);
+        const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
+        int cnt = 0;
+        for_neighbour_cells(d, g, d.acell[i], [&](int b, int e) {
+            for (int k0 = b; k0 < e; k0 += 32) {
+                const int k = k0 + lane;
+                bool in = false;
+                if (k < e) {
+                    const double4 p = d.cpos[lo + k];
+                    double dx, dy, dz;
+                    in = __double_as_longlong(p.w) != i && pair_dist(xi, yi, zi, p.x, p.y, p.z, dx, dy, dz, cell) < d.rc;
+                }
+                cnt += __popc(__ballot_sync(0xffffffffu, in));
+            }
+        });
+        unsigned last = 0;
+        if (lane == 0) {
+            d.cnt[i] = cnt;
+            __threadfence();
+            last = atomicAdd(d.sdone + s, 1u) == static_cast<unsigned>(hi - lo - 1);
+        }
+        if (!__shfl_sync(0xffffffffu, last, 0)) continue;
+        __threadfence();
+        int run = 0;  // the sample's row offsets, atoms in index order
+        for (int a0 = lo; a0 < hi; a0 += 32) {
+            const int a = a0 + lane;
+            const int v = a < hi ? __ldcg(d.cnt + a) : 0;
+            const int incl = warp_incl_scan(v);
+            if (a < hi) d.lptr[a] = run + incl - v;
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        unsigned glast = 0;
+        if (lane == 0) {
+            d.stot[s] = run;
+            __threadfence();
+            glast = atomicAdd(&d.hdr->large_done, 1u) == static_cast<unsigned>(n_large - 1);
+        }
+        if (!__shfl_sync(0xffffffffu, glast, 0)) continue;
+        __threadfence();
+        finalize_csr_warp(d, Q);
+        if (lane == 0) d.hdr->large_done = 0;
+    }
+}
+
+// Edge geometry of pair p = (i, j) from its fp64 difference and distance: unit
+// (1/r)*d (S/core.cpp:43), fcut (S/model.cpp:17) and the Gaussians (S/model.cpp:20-27)
+// in the three layouts the edge kernels read.
+template <int K>
+__device__ __forceinline__ void emit_pair(const Dev& d, int p, int i, int j, double r, double dx, double dy, double dz,
+                                          float wf, float invf, float rc_inv) {
+    d.col[p] = j;
+    d.dst[p] = i;
+    const double sc = __ddiv_rn(1.0, r);
+    const double ux = __dmul_rn(sc, dx), uy = __dmul_rn(sc, dy), uz = __dmul_rn(sc, dz);
+    // fcut and the Gaussians feed the fp32 model: evaluated in fp32 from the
+    // once-rounded distance (relative error ~1e-6, far inside the 1e-4 bar)
+    const float rf = static_cast<float>(r);
+    const float fc = 0.5f * (cospif(rf * rc_inv) + 1.f);
+    d.geo[p] = make_float4(static_cast<float>(ux), static_cast<float>(uy), static_cast<float>(uz), fc);
+    float rb[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const float dd = rf - wf * static_cast<float>(k);
+        rb[k] = fc * expf(-dd * dd * invf);  // fcut folded in
+    }
+#pragma unroll
+    for (int q = 0; q < K / 4; ++q) {  // canonical tcgen05 layout, tf32 hi + fp32 lo
+        float4 hi, lo;
+        umma::split_tf32(rb[4 * q], hi.x, lo.x);
+        umma::split_tf32(rb[4 * q + 1], hi.y, lo.y);
+        umma::split_tf32(rb[4 * q + 2], hi.z, lo.z);
+        umma::split_tf32(rb[4 * q + 3], hi.w, lo.w);
+        const int64_t o = rbf_idx<K>(p, 4 * q);
+        *reinterpret_cast<float4*>(d.rbf + o) = hi;
+        *reinterpret_cast<float4*>(d.rbfl + o) = lo;
+        *reinterpret_cast<float4*>(d.rbfp + static_cast<int64_t>(p) * K + 4 * q) =
+            make_float4(rb[4 * q], rb[4 * q + 1], rb[4 * q + 2], rb[4 * q + 3]);
+    }
+    if (d.export64) {
+        d.dist64[p] = r;
+        d.unit64[3 * static_cast<int64_t>(p)] = ux;
+        d.unit64[3 * static_cast<int64_t>(p) + 1] = uy;
+        d.unit64[3 * static_cast<int64_t>(p) + 2] = uz;
+    }
+}
+
+// Warp per atom i, writing row i of the CSR (i-major, j ascending). Small samples:
+// the same sweep as the count in k_prep, lanes that hold a neighbour compact into
+// the row with popc(ballot & lanes_below). Cell-list samples: per window of 1024
+// consecutive j, the exact test over the neighbour cells sets bit j of a per-warp
+// shared-memory mask, the set bits are listed in ascending j (one mask word per
+// lane, warp scan of the popcounts) and the lanes emit the listed pairs.
 template <int K>
 __global__ void __launch_bounds__(256) k_nbr_fill(Dev d, int Q) {
+    constexpr int kWin = 1024;
+    __shared__ uint32_t wbits[8][kWin / 32];
+    __shared__ int wlist[8][kWin];
     pdl_enter();
     if (d.hdr->overflow) return;
     const int N = d.hdr->N;
     const int64_t P = d.hdr->P;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     const double width = d.rc / static_cast<double>(K - 1);
     const float wf = static_cast<float>(width), invf = static_cast<float>(1.0 / (2.0 * width * width));
     const float rc_inv = static_cast<float>(1.0 / d.rc);
+    if (blockIdx.x == 0)  // the CSR padding's geometry: finite zeros (masked edges must not carry stale NaN)
+        for (int x = threadIdx.x; x < (kChunk + 8) * K; x += blockDim.x) {
+            const int64_t p = P + x / K;
+            const int k = x % K;
+            if (k == 0) d.geo[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+            d.rbf[rbf_idx<K>(p, k)] = 0.f;
+            d.rbfl[rbf_idx<K>(p, k)] = 0.f;
+            d.rbfp[p * K + k] = 0.f;
+        }
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
         const int s = d.sample_of[i];
         const int lo = static_cast<int>(d.atom_ptr[s]), hi = static_cast<int>(d.atom_ptr[s + 1]);
@@ -281,53 +597,56 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d, int Q) {
                     for (int64_t q = ((static_cast<int64_t>(base) + 1) * Q + P - 1) / P; q < Q; ++q) d.part_lo[q] = N;
             }
         }
-        for (int j0 = lo; j0 < hi; j0 += 32) {
-            const int j = j0 + lane;
-            bool in = false;
-            double dx = 0, dy = 0, dz = 0, r = 0;
-            if (j < hi && j != i) {
-                r = pair_dist(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz, cell);
-                in = r < d.rc;
+        if (hi - lo <= kSmallAtoms) {
+            for (int j0 = lo; j0 < hi; j0 += 32) {
+                const int j = j0 + lane;
+                bool in = false;
+                double dx = 0, dy = 0, dz = 0, r = 0;
+                if (j < hi && j != i) {
+                    r = pair_dist(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz, cell);
+                    in = r < d.rc;
+                }
+                const unsigned mask = __ballot_sync(0xffffffffu, in);
+                if (in) emit_pair<K>(d, base + __popc(mask & ((1u << lane) - 1u)), i, j, r, dx, dy, dz, wf, invf, rc_inv);
+                base += __popc(mask);
             }
-            const unsigned mask = __ballot_sync(0xffffffffu, in);
-            if (in) {
-                const int p = base + __popc(mask & ((1u << lane) - 1u));
-                d.col[p] = j;
-                d.dst[p] = i;
-                const double sc = __ddiv_rn(1.0, r);
-                const double ux = __dmul_rn(sc, dx), uy = __dmul_rn(sc, dy), uz = __dmul_rn(sc, dz);
-                // fcut and the Gaussians feed the fp32 model: evaluated in fp32 from the
-                // once-rounded distance (relative error ~1e-6, far inside the 1e-4 bar)
-                const float rf = static_cast<float>(r);
-                const float fc = 0.5f * (cospif(rf * rc_inv) + 1.f);
-                d.geo[p] = make_float4(static_cast<float>(ux), static_cast<float>(uy), static_cast<float>(uz), fc);
-                float rb[K];
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const float dd = rf - wf * static_cast<float>(k);
-                    rb[k] = fc * expf(-dd * dd * invf);  // fcut folded in
+            continue;
+        }
+        const CellGrid g = d.cgrid[s];
+        const int ci = d.acell[i];
+        uint32_t* bits = wbits[wib];
+        int* list = wlist[wib];
+        for (int w0 = lo; w0 < hi; w0 += kWin) {
+            bits[lane] = 0u;
+            __syncwarp();
+            for_neighbour_cells(d, g, ci, [&](int b, int e) {
+                for (int k = b + lane; k < e; k += 32) {
+                    const double4 p = d.cpos[lo + k];
+                    const int j = static_cast<int>(__double_as_longlong(p.w));
+                    double dx, dy, dz;
+                    if (j >= w0 && j < w0 + kWin && j != i && pair_dist(xi, yi, zi, p.x, p.y, p.z, dx, dy, dz, cell) < d.rc)
+                        atomicOr(bits + ((j - w0) >> 5), 1u << ((j - w0) & 31));
                 }
-#pragma unroll
-                for (int q = 0; q < K / 4; ++q) {  // canonical tcgen05 layout, tf32 hi + fp32 lo
-                    float4 hi, lo;
-                    umma::split_tf32(rb[4 * q], hi.x, lo.x);
-                    umma::split_tf32(rb[4 * q + 1], hi.y, lo.y);
-                    umma::split_tf32(rb[4 * q + 2], hi.z, lo.z);
-                    umma::split_tf32(rb[4 * q + 3], hi.w, lo.w);
-                    const int64_t o = rbf_idx<K>(p, 4 * q);
-                    *reinterpret_cast<float4*>(d.rbf + o) = hi;
-                    *reinterpret_cast<float4*>(d.rbfl + o) = lo;
-                    *reinterpret_cast<float4*>(d.rbfp + static_cast<int64_t>(p) * K + 4 * q) =
-                        make_float4(rb[4 * q], rb[4 * q + 1], rb[4 * q + 2], rb[4 * q + 3]);
-                }
-                if (d.export64) {
-                    d.dist64[p] = r;
-                    d.unit64[3 * static_cast<int64_t>(p)] = ux;
-                    d.unit64[3 * static_cast<int64_t>(p) + 1] = uy;
-                    d.unit64[3 * static_cast<int64_t>(p) + 2] = uz;
-                }
+            });
+            __syncwarp();
+            uint32_t word = bits[lane];
+            const int c = __popc(word);
+            const int incl = warp_incl_scan(c);
+            int at = incl - c;
+            while (word) {
+                list[at++] = w0 + 32 * lane + __ffs(word) - 1;
+                word &= word - 1u;
             }
-            base += __popc(mask);
+            __syncwarp();
+            const int total = __shfl_sync(0xffffffffu, incl, 31);
+            for (int k = lane; k < total; k += 32) {
+                const int j = list[k];
+                double dx, dy, dz;
+                const double r = pair_dist(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz, cell);
+                emit_pair<K>(d, base + k, i, j, r, dx, dy, dz, wf, invf, rc_inv);
+            }
+            base += total;
+            __syncwarp();
         }
     }
 }
@@ -442,9 +761,38 @@ __global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy, int full_g
     const double wf = mf > 0 ? d.hdr->lambda_f / static_cast<double>(mf) : 0.0;
     for (int s = blockIdx.x; s < B; s += gridDim.x) {
         const int ds = d.dsidx[s];
-        if (with_energy) sample_energy_own(d, s, ds, ered);
         const int64_t lo = d.atom_ptr[s], hi = d.atom_ptr[s + 1];
         const bool em = d.emask[s], fm = d.fmask[s];
+        if (with_energy == 2) {  // train step: per-atom terms from k_force_out, summed in a fixed order
+            double es = 0.0, fs = 0.0;
+            for (int64_t a = lo + threadIdx.x; a < hi; a += 128) es += d.eatom[a], fs += d.fterm[a];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+                es += __shfl_xor_sync(0xffffffffu, es, o), fs += __shfl_xor_sync(0xffffffffu, fs, o);
+            if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = es, red2[threadIdx.x >> 5] = fs;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const double E = ((red[0] + red[1]) + red[2]) + red[3];
+                d.Epred[static_cast<int64_t>(s) * D + ds] = E;
+                red[0] = ((red2[0] + red2[1]) + red2[2]) + red2[3];
+                double et = 0.0;
+                if (em) et = we * fabs(E - d.En[s]);
+                d.sample_terms[2 * s] = et;
+                d.sample_terms[2 * s + 1] = fm ? red[0] : 0.0;
+            }
+            __syncthreads();
+            if (threadIdx.x < D) {
+                float ge = 0.f;
+                if (threadIdx.x == ds && em) {
+                    const double diff = d.Epred[static_cast<int64_t>(s) * D + ds] - d.En[s];
+                    ge = diff > 0.0 ? static_cast<float>(we) : (diff < 0.0 ? static_cast<float>(-we) : 0.f);
+                }
+                d.gE[static_cast<int64_t>(s) * D + threadIdx.x] = ge;
+            }
+            __syncthreads();
+            continue;
+        }
+        if (with_energy) sample_energy_own(d, s, ds, ered);
         const double ws = wf / static_cast<double>(hi - lo);
         double fsum = 0.0;
         for (int64_t a = lo + threadIdx.x; a < hi; a += 128) {

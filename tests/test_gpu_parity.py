@@ -63,6 +63,31 @@ def test_neighbor_list_large_cluster(pk, dev, oracle_ref):
     check_nlist(dev, oracle_ref, pk.concat([small, big]))
 
 
+def test_neighbor_list_cell_list_cases(pk, dev, oracle_ref):
+    """Samples above kSmallAtoms (128) go through the cell lists: lattices whose
+    pair distances sit exactly at the cutoff and at cell boundaries, degenerate
+    extents (a line, one point), the 128/129 threshold, several 1024-atom windows,
+    and a huge extent (the one-cell fallback)."""
+    rng = np.random.default_rng(7)
+    g = np.arange(6) * 2.5  # 6^3 lattice, spacing rc/2: pairs at exactly 5 A excluded
+    lat = np.array([[a, b, c] for a in g for b in g for c in g], float)
+    g5 = np.arange(5) * 5.0  # spacing rc: every nearest-neighbour distance is exactly the cutoff
+    lat5 = np.array([[a, b, c] for a in g5 for b in g5 for c in g5], float) + 1e-3 * (rng.random((125, 3)) < 0.5)
+    systems = [
+        (lat, rng.choice(cases.ORGANIC, len(lat))),
+        (lat5, rng.choice(cases.ORGANIC, 125)),
+        (np.c_[np.arange(300) * 1.0, np.zeros(300), np.zeros(300)], np.full(300, 6)),  # a line
+        (np.zeros((150, 3)), np.full(150, 1)),                                          # one point
+        (rng.uniform(0, 12, (128, 3)), rng.choice(cases.ORGANIC, 128)),                 # threshold
+        (rng.uniform(0, 12, (129, 3)), rng.choice(cases.ORGANIC, 129)),
+        (rng.uniform(0, 32, (3000, 3)), rng.choice(cases.ORGANIC, 3000)),               # 3 windows
+        (np.r_[rng.uniform(0, 1e8, (140, 3)), rng.uniform(0, 6, (20, 3))], np.full(160, 8)),  # huge extent
+    ]
+    mixed = pk.concat([cases.molecules(pk, 3, 4), cases.pack(systems), cases.molecules(pk, 2, 5)])
+    ptr = check_nlist(dev, oracle_ref, mixed)
+    assert np.diff(ptr)[3 + 3] == 150 * 149
+
+
 def test_forward_matches_oracle(pk, dev, oracle_port):
     batch = cases.molecules(pk, 48, 11)
     params = oracle_port.init_params(cases.CFG, 7)

@@ -66,6 +66,31 @@ def test_periodic_neighbor_list_bit_exact(pk, dev, oracle_port):
 
 
 @pytest.mark.gpu
+def test_periodic_cell_list_bit_exact(pk, dev, oracle_port):
+    """Periodic samples above kSmallAtoms: 3, 4 and 5 slabs per lattice direction
+    (diamond supercells) and 2 (a skewed cell just over 2 rc wide, where the -1 and
+    +1 neighbour slabs are the same one)."""
+    parts = []
+    for reps in (3, 4, 5):
+        pos, Z, cell = cases.diamond_supercell(reps=reps, seed=reps)
+        parts.append((pos, Z, cell))
+    parts.append(cases.triclinic_box(n=150, seed=4, cell=((12.0, 0.0, 0.0), (1.0, 11.5, 0.0), (0.5, 1.0, 11.2))))
+    b = pk.concat([dict(cases.pack([(p, z)]), cell=c[None]) for p, z, c in parts] + [cases.molecules(pk, 3, 2)])
+    dev.set_batch(b)
+    ptr, gi, gj, gd, gu = dev.build_neighbor_list(fp64=True)
+    ap = b["atom_ptr"]
+    for s in range(len(parts)):
+        cell = np.asarray(b["cell"][s])
+        with oracle_port.periodic(cell[None]):
+            i, j, dist, unit = oracle_port.neighbor_list(b["pos"][ap[s]:ap[s + 1]], b["Z"][ap[s]:ap[s + 1]], 5.0)
+        lo, hi = ptr[s], ptr[s + 1]
+        assert np.array_equal(gi[lo:hi], i) and np.array_equal(gj[lo:hi], j), s
+        assert np.array_equal(gd[lo:hi].view(np.uint64), dist.view(np.uint64)), s
+        assert np.array_equal(gu[lo:hi].view(np.uint64), unit.view(np.uint64)), s
+    assert ptr[1] - ptr[0] == 216 * 28
+
+
+@pytest.mark.gpu
 def test_periodic_train_step_matches_oracle(pk, oracle_port):
     mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
     b = cases.periodic_batch(pk, seed=5)
