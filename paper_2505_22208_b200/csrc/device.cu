@@ -225,6 +225,7 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     ensure_buf(c, "sdone", 4 * Bc, changed);
     ensure_buf(c, "eatom", 8 * Nc, changed);
     ensure_buf(c, "fterm", 8 * Nc, changed);
+    ensure_buf(c, "fw", 8 * Nc, changed);
     if (c.export64) {
         ensure_buf(c, "dist64", 8 * Pc, changed);
         ensure_buf(c, "unit64", 24 * Pc, changed);
@@ -329,6 +330,7 @@ Dev make_dev(Ctx& c) {
     d.sdone = buf(c, "sdone").as<uint32_t>();
     d.eatom = buf(c, "eatom").as<double>();
     d.fterm = buf(c, "fterm").as<double>();
+    d.fw = buf(c, "fw").as<double>();
     d.geo = buf(c, "geo").as<float4>();
     d.rbf = buf(c, "rbf").as<float>();
     d.rbfl = buf(c, "rbfl").as<float>();

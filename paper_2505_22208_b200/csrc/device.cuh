@@ -128,6 +128,7 @@ struct Dev {
     float4* gFc;             // [N] dL/dF of the atom's own head (loss path), w = 0
     double* eatom;           // [N] sum_a h^L[i,a] W_e[a,d_i] (train step: own head)
     double* fterm;           // [N] the atom's Eq. (5) force term m_F w_F / n ||dF||
+    double* fw;              // [N] m_F lambda_F / (sum m_F * n) of the atom's sample (k_prep)
     double* sample_terms;    // [B][2]
     double* block_scratch;   // reduction scratch
     // backward

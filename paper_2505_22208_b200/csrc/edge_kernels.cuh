@@ -607,13 +607,10 @@ __global__ void __launch_bounds__(256) k_force_out(Dev d, int own_head) {
             for (int cc = 0; cc < C; ++cc) e = fma(static_cast<double>(hv.v[cc]), static_cast<double>(we.v[cc]), e);
             e = warp_sum_d(e);
             if (lane == 0) {
-                const int s = d.sample_of[i];
                 float4 gc = make_float4(0.f, 0.f, 0.f, 0.f);
                 double ft = 0.0;
-                if (d.fmask[s]) {
-                    const int mf = d.hdr->mf;
-                    const double ws = (mf > 0 ? d.hdr->lambda_f / static_cast<double>(mf) : 0.0) /
-                                      static_cast<double>(d.atom_ptr[s + 1] - d.atom_ptr[s]);
+                const double ws = d.fw[i];  // 0 unless the sample trains forces
+                if (ws != 0.0) {
                     double df[3], sq = 0.0;
 #pragma unroll
                     for (int x = 0; x < 3; ++x) {
@@ -622,9 +619,11 @@ __global__ void __launch_bounds__(256) k_force_out(Dev d, int own_head) {
                     }
                     const double dist = sqrt(sq);
                     ft = ws * dist;
-                    if (dist > 0.0)
-                        gc = make_float4(static_cast<float>(ws * df[0] / dist), static_cast<float>(ws * df[1] / dist),
-                                         static_cast<float>(ws * df[2] / dist), 0.f);
+                    if (dist > 0.0) {
+                        const double q = ws / dist;
+                        gc = make_float4(static_cast<float>(q * df[0]), static_cast<float>(q * df[1]),
+                                         static_cast<float>(q * df[2]), 0.f);
+                    }
                 }
                 d.eatom[i] = e;
                 d.fterm[i] = ft;

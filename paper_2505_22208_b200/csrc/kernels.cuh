@@ -102,6 +102,35 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
     return v;
 }
 
+// Exclusive scan of src[0, n) into dst (dst may alias src) by one warp, 8
+// consecutive values per lane and round so the loads of a round are all in
+// flight together; returns the total. src is read through L2 (written by other
+// CTAs of this kernel).
+__device__ __forceinline__ int warp_excl_scan8(const int32_t* src, int32_t* dst, int n) {
+    const int lane = threadIdx.x & 31;
+    int run = 0;
+    for (int c0 = 0; c0 < n; c0 += 256) {
+        int v[8], sum = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = c0 + lane * 8 + u;
+            v[u] = k < n ? __ldcg(src + k) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) sum += v[u];
+        const int incl = warp_incl_scan(sum);
+        int at = run + incl - sum;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int k = c0 + lane * 8 + u;
+            if (k < n) dst[k] = at;
+            at += v[u];
+        }
+        run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    return run;
+}
+
 // ------------------------------------------------------------ cell lists ---
 // Cell of a position in its sample's grid (device.cuh:CellGrid). Binning need not
 // be exact — the pair test over the neighbour cells is — only consistent: the
@@ -138,26 +167,39 @@ __device__ __forceinline__ bool cell_step(const CellGrid& g, int k, int c, int o
     return out >= 0 && out < n;
 }
 
-// Calls f(begin, end) — a range of the sample's cell-ordered atoms (cpos) — for
-// every distinct cell adjacent to (and including) cell c.
-template <class F>
-__device__ __forceinline__ void for_neighbour_cells(const Dev& d, const CellGrid& g, int c, F&& f) {
+// The candidates of one atom as a flat index space: lane q < 27 owns neighbour
+// cell q (offsets -1..1 per axis, cell_step's distinct cells only), the warp scan
+// of the cell sizes maps candidate t in [0, total) to its slot in the sample's
+// cell-ordered atoms, so 32 candidates are tested per round whatever the cell
+// occupancy (instead of one round per cell).
+struct CellWalk {
+    int off, incl, total;
+};
+
+__device__ __forceinline__ CellWalk cell_walk_setup(const Dev& d, const CellGrid& g, int c) {
+    const int lane = threadIdx.x & 31;
     const int c2 = c % g.n[2], c1 = (c / g.n[2]) % g.n[1], c0 = c / (g.n[1] * g.n[2]);
-    const int32_t* cs = d.cstart + g.base;
-    for (int o0 = -1; o0 <= 1; ++o0) {
-        int x0;
-        if (!cell_step(g, 0, c0, o0, x0)) continue;
-        for (int o1 = -1; o1 <= 1; ++o1) {
-            int x1;
-            if (!cell_step(g, 1, c1, o1, x1)) continue;
-            for (int o2 = -1; o2 <= 1; ++o2) {
-                int x2;
-                if (!cell_step(g, 2, c2, o2, x2)) continue;
-                const int q = (x0 * g.n[1] + x1) * g.n[2] + x2;
-                f(__ldg(cs + q), __ldg(cs + q + 1));
-            }
-        }
+    int b = 0, n = 0, x0, x1, x2;
+    if (lane < 27 && cell_step(g, 0, c0, lane / 9 - 1, x0) && cell_step(g, 1, c1, (lane / 3) % 3 - 1, x1) &&
+        cell_step(g, 2, c2, lane % 3 - 1, x2)) {
+        const int q = (x0 * g.n[1] + x1) * g.n[2] + x2;
+        b = __ldg(d.cstart + g.base + q);
+        n = __ldg(d.cstart + g.base + q + 1) - b;
     }
+    CellWalk w;
+    w.incl = warp_incl_scan(n);
+    w.off = b - (w.incl - n);
+    w.total = __shfl_sync(0xffffffffu, w.incl, 31);
+    return w;
+}
+
+// Slot (in the sample's cpos) of candidate t < total; every lane must call it.
+__device__ __forceinline__ int cell_walk_slot(const CellWalk& w, int t) {
+    int q = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1)
+        if (t >= __shfl_sync(0xffffffffu, w.incl, q + step - 1)) q += step;
+    return t + __shfl_sync(0xffffffffu, w.off, q);
 }
 
 // Block-wide (128 threads): the grid of sample s (bounding box or lattice), each
@@ -231,10 +273,21 @@ __device__ void bin_sample(const Dev& d, int s, int64_t lo, int64_t hi, const do
     int32_t* cs = d.cstart + g.base;
     for (int q = tid; q <= ncell; q += blockDim.x) cs[q] = 0;
     __syncthreads();
-    for (int64_t a = lo + tid; a < hi; a += blockDim.x) {
-        const int c = cell_index(g, cell, d.x[a], d.y[a], d.z[a]);
-        d.acell[a] = c;
-        d.lptr[a] = atomicAdd(cs + c, 1);
+    for (int64_t a0 = lo + tid; a0 < hi; a0 += 4 * blockDim.x) {
+        int c[4], r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t a = a0 + u * blockDim.x;
+            if (a < hi) c[u] = cell_index(g, cell, d.x[a], d.y[a], d.z[a]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (a0 + u * blockDim.x < hi) r[u] = atomicAdd(cs + c[u], 1);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t a = a0 + u * blockDim.x;
+            if (a < hi) d.acell[a] = c[u], d.lptr[a] = r[u];
+        }
     }
     __syncthreads();
     __shared__ int scratch[4];
@@ -249,9 +302,20 @@ __device__ void bin_sample(const Dev& d, int s, int64_t lo, int64_t hi, const do
     }
     if (tid == 0) cs[ncell] = run;
     __syncthreads();
-    for (int64_t a = lo + tid; a < hi; a += blockDim.x) {
-        const int at = __ldcg(cs + d.acell[a]) + d.lptr[a];
-        d.cpos[lo + at] = make_double4(d.x[a], d.y[a], d.z[a], __longlong_as_double(a));
+    for (int64_t a0 = lo + tid; a0 < hi; a0 += 4 * blockDim.x) {
+        int at[4];
+        double4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t a = a0 + u * blockDim.x;
+            if (a < hi) at[u] = d.acell[a], v[u] = make_double4(d.x[a], d.y[a], d.z[a], __longlong_as_double(a));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (a0 + u * blockDim.x < hi) at[u] = __ldcg(cs + at[u]) + d.lptr[a0 + u * blockDim.x];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (a0 + u * blockDim.x < hi) d.cpos[lo + at[u]] = v[u];
     }
 }
 
@@ -262,14 +326,7 @@ __device__ void bin_sample(const Dev& d, int s, int64_t lo, int64_t hi, const do
 __device__ void finalize_csr_warp(const Dev& d, int Q) {
     const int lane = threadIdx.x & 31;
     const int B = d.hdr->B, N = d.hdr->N;
-    int run = 0;
-    for (int s0 = 0; s0 < B; s0 += 32) {
-        const int s = s0 + lane;
-        const int v = s < B ? __ldcg(d.stot + s) : 0;
-        const int incl = warp_incl_scan(v);
-        if (s < B) d.soff[s] = run + incl - v;
-        run += __shfl_sync(0xffffffffu, incl, 31);
-    }
+    const int run = warp_excl_scan8(d.stot, d.soff, B);
     const bool over = static_cast<int64_t>(run) > d.Pcap;
     if (lane == 0) {
         d.hdr->P = run;
@@ -293,7 +350,7 @@ __device__ void finalize_csr_warp(const Dev& d, int Q) {
 // P / the capacity-overflow flag / row_ptr[N] / the CSR padding, so the
 // neighbour fill can place every atom's row without a separate scan kernel.
 // Q: edge-kernel partitions (k_nbr_fill cuts them while writing row_ptr).
-__global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out, int Q) {
+__global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) {
     pdl_enter();
     const StepHeader& hd = *d.hdr;
     const char* base = reinterpret_cast<const char*>(d.hdr);
@@ -375,26 +432,48 @@ __global__ void __launch_bounds__(128) k_prep(Dev d, BatchArrays out, int Q) {
         }
         __syncthreads();
         const double fs = d.use_table ? __ddiv_rn(1.0, d.tfstd[dsi]) : 1.0;
-        for (int64_t a = lo + threadIdx.x; a < hi; a += blockDim.x) {
-            d.sample_of[a] = s;
-            d.chan[a] = dsi;
-            out.Z[a] = Z[a];
-            out.zslot[a] = z2s[Z[a]];
-            double xyz[3];
+        // the Eq. (5) weight of the atom's force term (S/loss.cpp:186-212): lambda_F / (sum m_F * n)
+        const int mfs = hd.mf;
+        const double fwa = fm[s] && mfs > 0 ? hd.lambda_f / (static_cast<double>(mfs) * static_cast<double>(hi - lo)) : 0.0;
+        // 4 atoms per thread and round, every load issued before the first store
+        // (large samples are latency-bound here: one block walks all their atoms)
+        for (int64_t a0 = lo + threadIdx.x; a0 < hi; a0 += 4 * blockDim.x) {
+            double pin[4][3], src[4][3];
+            int zz[4];
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                double lab;
-                if (is_dn) {
-                    const double eff = d.denoise_scheme ? __dsub_rn(noise[3 * a + c], mean[c]) : noise[3 * a + c];
-                    xyz[c] = __dadd_rn(pos[3 * a + c], eff);
-                    lab = __dmul_rn(-1.0, eff);
-                } else {
-                    xyz[c] = pos[3 * a + c];
-                    lab = F[3 * a + c];
+            for (int u = 0; u < 4; ++u) {
+                const int64_t a = a0 + u * blockDim.x;
+                if (a < hi) {
+                    zz[u] = Z[a];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) pin[u][c] = pos[3 * a + c], src[u][c] = is_dn ? noise[3 * a + c] : F[3 * a + c];
                 }
-                d.Fn[3 * a + c] = d.use_table ? __dmul_rn(fs, lab) : lab;
             }
-            d.x[a] = xyz[0], d.y[a] = xyz[1], d.z[a] = xyz[2];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t a = a0 + u * blockDim.x;
+                if (a >= hi) break;
+                d.sample_of[a] = s;
+                d.chan[a] = dsi;
+                d.fw[a] = fwa;
+                out.Z[a] = zz[u];
+                out.zslot[a] = z2s[zz[u]];
+                double xyz[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double lab;
+                    if (is_dn) {
+                        const double eff = d.denoise_scheme ? __dsub_rn(src[u][c], mean[c]) : src[u][c];
+                        xyz[c] = __dadd_rn(pin[u][c], eff);
+                        lab = __dmul_rn(-1.0, eff);
+                    } else {
+                        xyz[c] = pin[u][c];
+                        lab = src[u][c];
+                    }
+                    d.Fn[3 * a + c] = d.use_table ? __dmul_rn(fs, lab) : lab;
+                }
+                d.x[a] = xyz[0], d.y[a] = xyz[1], d.z[a] = xyz[2];
+            }
         }
         __syncthreads();
         const double* cell = sample_cell(d, s);
@@ -464,18 +543,17 @@ __global__ void __launch_bounds__(256) k_cell_count(Dev d, int Q) {
         const double* cell = sample_cell(d, s);
         const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
         int cnt = 0;
-        for_neighbour_cells(d, g, d.acell[i], [&](int b, int e) {
-            for (int k0 = b; k0 < e; k0 += 32) {
-                const int k = k0 + lane;
-                bool in = false;
-                if (k < e) {
-                    const double4 p = d.cpos[lo + k];
-                    double dx, dy, dz;
-                    in = __double_as_longlong(p.w) != i && pair_dist(xi, yi, zi, p.x, p.y, p.z, dx, dy, dz, cell) < d.rc;
-                }
-                cnt += __popc(__ballot_sync(0xffffffffu, in));
+        const CellWalk w = cell_walk_setup(d, g, d.acell[i]);
+        for (int t0 = 0; t0 < w.total; t0 += 32) {
+            const int k = cell_walk_slot(w, t0 + lane);
+            bool in = false;
+            if (t0 + lane < w.total) {
+                const double4 p = d.cpos[lo + k];
+                double dx, dy, dz;
+                in = __double_as_longlong(p.w) != i && pair_dist(xi, yi, zi, p.x, p.y, p.z, dx, dy, dz, cell) < d.rc;
             }
-        });
+            cnt += __popc(__ballot_sync(0xffffffffu, in));
+        }
         unsigned last = 0;
         if (lane == 0) {
             d.cnt[i] = cnt;
@@ -484,14 +562,7 @@ __global__ void __launch_bounds__(256) k_cell_count(Dev d, int Q) {
         }
         if (!__shfl_sync(0xffffffffu, last, 0)) continue;
         __threadfence();
-        int run = 0;  // the sample's row offsets, atoms in index order
-        for (int a0 = lo; a0 < hi; a0 += 32) {
-            const int a = a0 + lane;
-            const int v = a < hi ? __ldcg(d.cnt + a) : 0;
-            const int incl = warp_incl_scan(v);
-            if (a < hi) d.lptr[a] = run + incl - v;
-            run += __shfl_sync(0xffffffffu, incl, 31);
-        }
+        const int run = warp_excl_scan8(d.cnt + lo, d.lptr + lo, hi - lo);  // the sample's row offsets
         unsigned glast = 0;
         if (lane == 0) {
             d.stot[s] = run;
@@ -613,21 +684,22 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d, int Q) {
             continue;
         }
         const CellGrid g = d.cgrid[s];
-        const int ci = d.acell[i];
+        const CellWalk cw = cell_walk_setup(d, g, d.acell[i]);
         uint32_t* bits = wbits[wib];
         int* list = wlist[wib];
         for (int w0 = lo; w0 < hi; w0 += kWin) {
             bits[lane] = 0u;
             __syncwarp();
-            for_neighbour_cells(d, g, ci, [&](int b, int e) {
-                for (int k = b + lane; k < e; k += 32) {
+            for (int t0 = 0; t0 < cw.total; t0 += 32) {
+                const int k = cell_walk_slot(cw, t0 + lane);
+                if (t0 + lane < cw.total) {
                     const double4 p = d.cpos[lo + k];
                     const int j = static_cast<int>(__double_as_longlong(p.w));
                     double dx, dy, dz;
                     if (j >= w0 && j < w0 + kWin && j != i && pair_dist(xi, yi, zi, p.x, p.y, p.z, dx, dy, dz, cell) < d.rc)
                         atomicOr(bits + ((j - w0) >> 5), 1u << ((j - w0) & 31));
                 }
-            });
+            }
             __syncwarp();
             uint32_t word = bits[lane];
             const int c = __popc(word);
