@@ -303,6 +303,8 @@ def run_ours(args, dist):
         out["rank_imbalance"] = rank_imbalance(pk, dev, pool, table, tc)
         out["rank_imbalance_heavy_tail"] = rank_imbalance_heavy(pk, dev, tc)
         out["periodic_cfg1"] = periodic_cfg1(pk, mcfg, tc)
+        out["semisup_cfg3"] = semisup_cfg3(pk, mcfg, tc)
+        out["supercells_cfg4"] = supercells_cfg4(pk, mcfg, tc)
     dev.close()
     return out
 
@@ -458,6 +460,119 @@ def rank_imbalance_heavy(pk, dev, tc, G=8, B=4, S=64, steps=8):
                          "steps": sc["n_batches"], "dropped": sc["dropped"]}
         sched_1m[f"G{g}"] = row
     out["schedule_1M_trace_atoms"] = sched_1m
+    return out
+
+
+def time_rank_slices(pk, dev, pool, sched, G, B, tc, steps, slot0=970):
+    """Per scheduled mini-batch, each of the G ranks' B-sample slices staged and
+    timed as its own device step on this GPU (min of 3, CUDA events on the ctx
+    stream); returns [(rank atoms [G], rank ms [G])] per step."""
+    out = []
+    per = G * B
+    for s in range(min(steps, sched["n_batches"])):
+        ids = sched["sample"][s * per:(s + 1) * per]
+        atoms, times = [], []
+        for g in range(G):
+            sub = pk.select(pool, ids[g * B:(g + 1) * B])
+            dev.stage(sub, tc, step=s, slot=slot0 + g, workers=G, rank=g)
+            dev.train_step_staged(slot0 + g, sync=True)
+            ms = []
+            for _ in range(3):
+                dev.event_record(0)
+                dev.train_step_staged(slot0 + g, sync=False)
+                dev.event_record(1)
+                ms.append(dev.event_elapsed_ms(0, 1))
+            atoms.append(int(sub["atom_ptr"][-1]))
+            times.append(min(ms))
+        out.append((np.array(atoms), np.array(times)))
+    return out
+
+
+def slice_summary(rows):
+    """max/mean per-rank time per step, and the per-GPU throughput of the slices."""
+    r = [t.max() / t.mean() for _, t in rows]
+    a = sum(x.sum() for x, _ in rows)
+    t = sum(t.sum() for _, t in rows)
+    return {"time_imbalance_mean": float(np.mean(r)), "time_imbalance_p95": float(np.percentile(r, 95)),
+            "atoms_per_s_per_gpu": float(a / (t / 1e3)), "steps": len(rows)}
+
+
+def supercells_cfg4(pk, mcfg, tc, Gs=(2, 4, 8), B=4, steps=6):
+    """BASELINE configs[3]: periodic diamond-Si supercells of r0 x r1 x r2 cubic cells
+    (r in 3..5: 216-1000 atoms, 28 neighbours per atom within 5 A), B = 4 per rank;
+    the balanced and naive plans at G = 2/4/8 with every rank's slice timed as a
+    full train step on this GPU (per-rank device work; the allreduce is not in
+    these times). Also the single-GPU step throughput (G = 1)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import cases
+    rng = np.random.default_rng(11)
+    parts = []
+    for s in range(8 * B * steps):
+        pos, Z, cell = cases.diamond_supercell(reps=tuple(rng.integers(3, 6, 3)), seed=1000 + s)
+        n = len(Z)
+        parts.append(dict(atom_ptr=np.array([0, n], np.int64), pos=pos, Z=Z,
+                          forces=rng.normal(0, 0.1, (n, 3)), dataset_index=np.zeros(1, np.int32),
+                          energy_mask=np.ones(1, np.uint8), force_mask=np.ones(1, np.uint8),
+                          energy=np.array([-4.6 * n + rng.normal()]), denoise=np.zeros(1, np.uint8),
+                          cell=cell[None]))
+    pool = pk.concat(parts)
+    atoms = np.diff(pool["atom_ptr"])
+    dev = pk.Device(mcfg, seed=7)
+    dev.set_reference_table(fit_table(pool, CFG["heads"]))
+    out = {"workload": "cfg4: periodic diamond-Si supercells 216-1000 atoms (3-5 cubic cells per axis), "
+                       "B = 4 per rank, minimum image + cell lists",
+           "pool_atoms_mean": float(atoms.mean()), "B": B}
+    one = time_rank_slices(pk, dev, pool, pk.plan(atoms, 1, B, 4, seed=3, mode="balanced"), 1, B, tc, steps)
+    out["G1"] = {"atoms_per_s": slice_summary(one)["atoms_per_s_per_gpu"],
+                 "edges_per_atom": 28}
+    for G in Gs:
+        row = {}
+        for mode in ("balanced", "naive"):
+            sched = pk.plan(atoms, G, B, 4, seed=3, mode=mode)
+            row[mode] = slice_summary(time_rank_slices(pk, dev, pool, sched, G, B, tc, steps))
+        out[f"G{G}"] = row
+    dev.close()
+    return out
+
+
+def semisup_cfg3(pk, mcfg, tc, G=8, B=32, steps=6):
+    """BASELINE configs[2] (non-periodic twin): three subsets of
+    reference-generator structures clamped to 8-200 atoms — E+F labeled (mode 15),
+    energy-only (mode 60), coordinate-denoising (mode 30, sigma 0.3 A, centered) —
+    mixed at temperature T = 2 into the epoch index, one head per subset, the
+    balanced (and naive) plan at G = 8, B = 32; every rank's slice timed as a full
+    train step on this GPU."""
+    subs = []
+    for k, (task, mode, n) in enumerate((("energy_and_forces", 15.0, 3000), ("energy_only", 60.0, 600),
+                                         ("denoising", 30.0, 1500))):
+        b = pk.synth_generate(n, 21 + k, task=task, mode=mode, sigma=0.5, min_atoms=8, max_atoms=200,
+                              elements=(1, 6, 7, 8), threads=os.cpu_count() or 8, dataset_index=k)
+        subs.append(b)
+    sizes = [len(b["atom_ptr"]) - 1 for b in subs]
+    rep = pk.temperature_counts(sizes, 2.0)
+    osub, osam = pk.build_epoch_index(rep, sizes, seed=5)
+    pools = pk.concat(subs)
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    ids = offs[osub] + osam
+    pool = pk.select(pools, ids)
+    atoms = np.diff(pool["atom_ptr"])
+    D = CFG["heads"]
+    table = dict(rho=np.zeros((D, 119)), rho_has=np.zeros((D, 119), np.uint8), mean=np.zeros(D), std=np.ones(D),
+                 fstd=np.ones(D), has=np.ones(D, np.uint8))
+    t0 = fit_table(subs[0], D)
+    for key in table:
+        table[key][0] = t0[key][0]
+    table["fstd"][2] = 0.3
+    dev = pk.Device(mcfg, seed=7)
+    dev.set_reference_table(table)
+    out = {"workload": "cfg3: E+F / energy-only / denoising subsets (8-200 atoms, non-periodic twin), "
+                       "T = 2 mix, G = 8, B = 32",
+           "epoch_samples": int(len(ids)), "subset_share": [float(np.mean(osub == k)) for k in range(3)],
+           "pool_atoms_mean": float(atoms.mean())}
+    for mode in ("balanced", "naive"):
+        sched = pk.plan(atoms, G, B, 100, seed=3, mode=mode)
+        out[mode] = slice_summary(time_rank_slices(pk, dev, pool, sched, G, B, tc, steps))
+    dev.close()
     return out
 
 

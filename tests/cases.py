@@ -77,14 +77,16 @@ def mixed_batch(lib, D=10, seed=5, count=24, denoise_frac=0.3):
 
 
 def diamond_supercell(reps=2, a=5.43, jitter=0.05, seed=0, Z=14):
-    """cfg1's periodic bulk: an reps^3 diamond supercell (8 atoms per cubic cell,
-    a = 5.43 A for Si) with Gaussian jitter; returns (pos [n,3], Z [n], cell [3,3])."""
+    """cfg1's periodic bulk: an reps^3 (or r0 x r1 x r2) diamond supercell (8 atoms
+    per cubic cell, a = 5.43 A for Si) with Gaussian jitter; returns (pos [n,3],
+    Z [n], cell [3,3])."""
     rng = np.random.default_rng(seed)
+    r = np.broadcast_to(np.asarray(reps, int), (3,))
     basis = np.array([[0, 0, 0], [0, .5, .5], [.5, 0, .5], [.5, .5, 0],
                       [.25, .25, .25], [.25, .75, .75], [.75, .25, .75], [.75, .75, .25]])
-    frac = np.array([b + np.array([i, j, k]) for i in range(reps) for j in range(reps) for k in range(reps)
-                     for b in basis]) / reps
-    cell = np.eye(3) * a * reps
+    frac = np.array([b + np.array([i, j, k]) for i in range(r[0]) for j in range(r[1]) for k in range(r[2])
+                     for b in basis]) / r
+    cell = np.diag(a * r.astype(float))
     pos = frac @ cell + rng.normal(0.0, jitter, (len(frac), 3))
     return pos, np.full(len(frac), Z, np.int32), cell
 
