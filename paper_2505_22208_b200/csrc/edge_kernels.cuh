@@ -301,6 +301,13 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K, G, 
                 const unsigned vm = ((1u << uhi) - 1u) & ~((1u << ulo) - 1u);
                 const int bp = cb - (((cb >> 5) & ~3) << 5) + blk * 8;  // bit of the block's first edge
                 unsigned seg = (((st.segw[bp >> 5] >> (bp & 31)) & 0xFFu) | (1u << ulo)) & vm;
+                if (seg == 1u && vm == 0xFFu && st.dst[blk * 8] == cur) {
+                    // the common block: 8 edges, all of the current destination (no
+                    // segment start inside): the unpredicated body
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) body.edge(st, blk * 8 + u, r[u], f[u], 1u);
+                    seg = 0u;
+                }
                 while (seg) {
                     const int u0 = __ffs(seg) - 1;
                     seg &= seg - 1u;
