@@ -224,29 +224,37 @@ template <int H, int K, int G, int C, class Body>
 __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K, G, C>& c, Body& body, const FilterTc& ft) {
     constexpr bool kF = Body::kFilter;
     constexpr int parts = Body::kParts | (kF ? kPartCanon : 0);
-    pdl_enter();  // the kernel's prologue (weights, TMEM, accumulators) overlapped the previous kernel
+    // The CSR (partitions, row_ptr, edge metadata) and the weights are at least two
+    // kernels old unless c.late (layer-0 message): the first two chunks are staged
+    // and the first filter MMA issued before the dependency wait, overlapping the
+    // previous kernel's tail; the source-row gathers and body.begin come after it.
+    if (c.late) pdl_enter();
     int plo = c.lo, phi = c.hi;
     if (c.late) plo = d.part_lo[c.q], phi = d.part_lo[c.q + kPartsPerCta / G];
-    if (plo >= phi) return;
+    if (plo >= phi) {
+        if (!c.late) pdl_enter();
+        return;
+    }
     const int e0 = d.row_ptr[plo], e1 = d.row_ptr[phi];
     // the staging / MMA-issuing thread: lane 0 of warp g % (H/32) of the group, so the
     // four groups' leaders sit on different SM sub-partitions (warp id % 4)
     const bool lead = c.lt == 32 * (c.g % (H / 32));
     const uint32_t quad = (threadIdx.x >> 5) & 3;
+    const int base = e0 & ~7;  // chunks start on 8-edge blocks
+    const int nchunks = (e1 - base + C - 1) / C;
+    if (lead && e1 > e0) {
+        stage_chunk<K, C>(d, c.st[0], &c.bar[0], base, e1, parts);
+        if (nchunks > 1) stage_chunk<K, C>(d, c.st[1], &c.bar[1], base + C, e1, parts);
+        if constexpr (kF) {
+            mbar_wait(&c.bar[0], 0);
+            filter_mma<K, C>(ft.tg, ft, c.st[0]);
+            umma::commit(&c.mbar[0]);
+        }
+    }
+    if (!c.late) pdl_enter();
     int cur = plo;
     body.begin(cur);
     if (e1 > e0) {
-        const int base = e0 & ~7;  // chunks start on 8-edge blocks
-        const int nchunks = (e1 - base + C - 1) / C;
-        if (lead) {
-            stage_chunk<K, C>(d, c.st[0], &c.bar[0], base, e1, parts);
-            if (nchunks > 1) stage_chunk<K, C>(d, c.st[1], &c.bar[1], base + C, e1, parts);
-            if constexpr (kF) {
-                mbar_wait(&c.bar[0], 0);
-                filter_mma<K, C>(ft.tg, ft, c.st[0]);
-                umma::commit(&c.mbar[0]);
-            }
-        }
         // gathers of the next block are issued before the current block is
         // consumed, across chunk boundaries (the next chunk's stage is waited for
         // at the start of the current chunk)
