@@ -34,7 +34,7 @@ struct NodeGemmCfg {
     static constexpr int NC = H / NS;                       // output columns per CTA tile
     static constexpr size_t a_floats = 2 * kGemmM * H;      // activation tile hi | lo (full K)
     static constexpr size_t b_floats = 2 * NC * H;          // weight rows [NC][H] hi | lo
-    static constexpr size_t bytes = 4 * (a_floats + b_floats) + 64 + 1024;  // + alignment slack
+    static constexpr size_t bytes = 4 * (a_floats + b_floats) + 64 + 1024;  // + barriers, alignment slack
 };
 template <int H>
 using NodeGemmSmem = NodeGemmCfg<H>;
@@ -102,25 +102,28 @@ __global__ void __launch_bounds__(256) k_opt(Dev d, int G, double inv_g, double 
 // epilogue inputs (residual / mu) are prefetched while the tensor core runs.
 // Warps w and w+4 share TMEM lanes 32*(w%4).. and split the NC columns.
 template <int H>
-__global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, const __grid_constant__ CUtensorMap amap) {
+__global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, const __grid_constant__ CUtensorMap amap,
+                                                      const __grid_constant__ CUtensorMap omap0,
+                                                      const __grid_constant__ CUtensorMap omap1) {
     using Cfg = NodeGemmCfg<H>;
     constexpr int NS = Cfg::NS, NC = Cfg::NC, CW = NC / 2;  // columns per thread
+    constexpr int KB = H / 32;                               // 32-column activation boxes (TMA, SWIZZLE_128B)
+    constexpr bool kTmaOut = CW == 32;  // epilogue through shared memory + TMA stores (one box per thread row)
     static_assert(CW % 16 == 0, "epilogue reads 16 columns at a time");
     extern __shared__ __align__(1024) unsigned char node_gemm_smem[];
     float* sm = reinterpret_cast<float*>(node_gemm_smem + ((1024u - (smem_u32(node_gemm_smem) & 1023u)) & 1023u));
     float* Ahi = sm;  // the raw activation tile (TMA, SWIZZLE_128B): the tf32 "hi" operand as is
     float* Alo = Ahi + kGemmM * H;
     float* Bhi = Alo + kGemmM * H;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(Bhi + Cfg::b_floats);  // weights TMA, MMA done, activations TMA
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
+    // barriers: [0] weights TMA, [1] MMA done, [2, 2 + KB) activation boxes
+    uint64_t* bar = reinterpret_cast<uint64_t*>(Bhi + Cfg::b_floats);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2 + KB);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int quad = warp & 3, half = warp >> 2;
     constexpr uint32_t kCols = NC < 32 ? 32 : NC;
     if (warp == 0) umma::tmem_alloc(tslot, kCols);
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_init(&bar[2], 1);
+        for (int b = 0; b < 2 + KB; ++b) mbar_init(&bar[b], 1);
         mbar_fence_init();
     }
     umma::fence_before();
@@ -149,41 +152,45 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, co
         const int at = tile / NS, np = tile % NS, base = at * kGemmM;
         if (np != loaded_np) fetch_weights(np);
         // the activation tile (mu_l or gh rows base..base+127, all H columns) by TMA
-        // in H/32 SWIZZLE_128B blocks; rows past the batch are never stored
+        // in KB SWIZZLE_128B boxes, one barrier each; rows past the batch are never stored
         if (tid == 0) {
-            mbar_expect_tx(&bar[2], static_cast<uint32_t>(kGemmM * H * 4));
+            if constexpr (kTmaOut) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // last tile's stores
 #pragma unroll
-            for (int kb = 0; kb < H / 32; ++kb) umma::tma_load_2d(Ahi + kb * kGemmM * 32, &amap, kb * 32, base, &bar[2]);
+            for (int kb = 0; kb < KB; ++kb) {
+                mbar_expect_tx(&bar[2 + kb], static_cast<uint32_t>(kGemmM * 32 * 4));
+                umma::tma_load_2d(Ahi + kb * kGemmM * 32, &amap, kb * 32, base, &bar[2 + kb]);
+            }
         }
-        mbar_wait(&bar[2], aphase);
-        aphase ^= 1u;
-        {  // lo = x - trunc_tf32(x), same swizzled positions; thread -> consecutive 16-byte chunks
-            constexpr int IT = kGemmM * H / 4 / 256;
+        // per box as it lands: lo = x - trunc_tf32(x) at the same swizzled positions,
+        // then its 4 k-steps (3 MMAs each) — the tensor core works on box kb while
+        // the threads split box kb + 1
+#pragma unroll
+        for (int kb = 0; kb < KB; ++kb) {
+            mbar_wait(&bar[2 + kb], aphase);
+            constexpr int IT = kGemmM * 32 / 4 / 256;
 #pragma unroll
             for (int it = 0; it < IT; ++it) {
-                const int c = tid + 256 * it;
+                const int c = kb * kGemmM * 8 + tid + 256 * it;
                 const float4 x = *reinterpret_cast<const float4*>(Ahi + 4 * c);
                 *reinterpret_cast<float4*>(Alo + 4 * c) =
                     make_float4(umma::tf32_trunc_lo(x.x), umma::tf32_trunc_lo(x.y), umma::tf32_trunc_lo(x.z),
                                 umma::tf32_trunc_lo(x.w));
             }
-        }
-        umma::fence_proxy_async();
-        __syncthreads();
-        if (w_pending) {
-            if (tid == 0) mbar_wait(&bar[0], wphase);
-            wphase ^= 1u;
-            w_pending = false;
-        }
-        if (tid == 0) {
-            umma::fence_after();
-            const float* Blo = Bhi + NC * H;
+            umma::fence_proxy_async();
+            __syncthreads();
+            if (tid == 0) {
+                if (kb == 0 && w_pending) mbar_wait(&bar[0], wphase);
+                umma::fence_after();
+                const float* Blo = Bhi + NC * H;
 #pragma unroll
-            for (int s = 0; s < H / 8; ++s)
-                umma::mma3(tbase, umma::sw128_kdesc(Ahi, s, kGemmM), umma::sw128_kdesc(Alo, s, kGemmM),
-                           umma::kdesc(Bhi, s, H), umma::kdesc(Blo, s, H), idesc, s ? 1u : 0u);
-            umma::commit(&bar[1]);
+                for (int s = 4 * kb; s < 4 * kb + 4; ++s)
+                    umma::mma3(tbase, umma::sw128_kdesc(Ahi, s, kGemmM), umma::sw128_kdesc(Alo, s, kGemmM),
+                               umma::kdesc(Bhi, s, H), umma::kdesc(Blo, s, H), idesc, s ? 1u : 0u);
+                if (kb == KB - 1) umma::commit(&bar[1]);
+            }
         }
+        aphase ^= 1u;
+        if (w_pending) wphase ^= 1u, w_pending = false;
         // epilogue inputs for this thread's row/columns, fetched while the MMAs run
         const int row = quad * 32 + lane, atom = base + row, c0 = np * NC + half * CW;
         const bool live = atom < N;
@@ -203,6 +210,54 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, co
         mbar_wait(&bar[1], mphase);
         mphase ^= 1u;
         umma::fence_after();
+        if constexpr (kTmaOut) {
+            // outputs as SWIZZLE_128B boxes [128 rows][32 columns] in the (now free)
+            // activation tiles: box (array, half) = Ahi + (2 * array + half) * 4096;
+            // thread row r writes its 16-byte chunk q at chunk position q ^ (r % 8)
+            float* ob = Ahi + half * kGemmM * 32 + row * 32;
+#pragma unroll
+            for (int cc = 0; cc < CW; cc += 16) {
+                float v[16];
+                umma::ld16(tbase + (static_cast<uint32_t>(quad * 32) << 16) + half * CW + cc, v);
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const int q = cc / 4 + q4, pos = (q ^ (row & 7)) * 4;
+                    float4 a, b;
+                    if (mode == 0) {
+                        float hn[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) hn[e] = pre[cc + 4 * q4 + e] + v[4 * q4 + e];
+                        a = make_float4(hn[0], hn[1], hn[2], hn[3]);
+                        b = make_float4(tanhf(hn[0]), tanhf(hn[1]), tanhf(hn[2]), tanhf(hn[3]));
+                    } else {
+                        float g[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float m = pre[cc + 4 * q4 + e];
+                            g[e] = v[4 * q4 + e] * (1.f - m * m);
+                        }
+                        a = b = make_float4(g[0], g[1], g[2], g[3]);
+                    }
+                    *reinterpret_cast<float4*>(ob + pos) = a;
+                    if (mode == 0) *reinterpret_cast<float4*>(ob + 2 * kGemmM * 32 + pos) = b;
+                }
+            }
+            umma::fence_proxy_async();  // generic-proxy writes -> visible to the TMA engine
+            umma::fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                const int nbox = mode == 0 ? 2 : 1;
+                for (int arr = 0; arr < nbox; ++arr)
+                    for (int hf = 0; hf < 2; ++hf)
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                reinterpret_cast<uint64_t>(arr == 0 ? &omap0 : &omap1)),
+                            "r"(np * NC + hf * CW), "r"(base), "r"(smem_u32(Ahi + (2 * arr + hf) * kGemmM * 32))
+                            : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            umma::fence_after();
+        } else {
 #pragma unroll
         for (int cc = 0; cc < CW; cc += 16) {
             float v[16];
@@ -233,7 +288,10 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, co
         umma::fence_before();
         __syncthreads();  // accumulator and activation tile drained before the next tile
         umma::fence_after();
+        }
     }
+    if constexpr (kTmaOut)  // the stores have read shared memory (grid completion publishes the writes)
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     umma::fence_before();
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc(tbase, kCols);
@@ -258,7 +316,7 @@ struct BwdGemmSmem {
     static constexpr size_t a_floats = 2 * kGemmM * H;  // gh tile hi | lo (MMA1's A)
     static constexpr size_t b_floats = NodeGemmCfg<H>::b_floats > 2 * kGemmM * NC ? NodeGemmCfg<H>::b_floats
                                                                                    : 2 * kGemmM * NC;
-    static constexpr size_t bytes = 4 * (a_floats + b_floats) + 64 + 1024;  // + alignment slack
+    static constexpr size_t bytes = 4 * (a_floats + b_floats) + 64 + 1024;  // + barriers, alignment slack
 };
 
 template <int H>
