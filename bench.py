@@ -14,7 +14,7 @@ loss -> backward -> NCCL allreduce (N > 1) -> clip -> RMS update.
 value  : atoms/s over all ranks with inputs resident in HBM (staged slots),
          device time (CUDA events around each step, L2 flushed between steps,
          max over ranks).
-e2e    : same metric through the public API lamm_train_step with host
+e2e    : same metric through the public API (pipelined lamm_train_step_submit/_wait) with host
          batches: host packing, H2D, the step, D2H of the result, per step.
 Rank 0 prints one JSON line.
 """
@@ -237,19 +237,30 @@ def run_ours(args, dist):
     for s in range(n_steps):
         r = dev.train_step_staged(s, sync=True)
         edge_counts.append(r.n_edges)
-    # ---- e2e: public API with host batches (H2D + step + D2H per step)
-    e2e_s, h2d, d2h, e2e_atoms = 0.0, 0, 0, 0
+    # ---- e2e: public API with host batches, pipelined (lamm_train_step_submit /
+    # lamm_train_step_wait: the host packs step k+1 while the device runs step k).
+    # Every step's H2D of its packed batch and D2H of its result header are inside
+    # the wall-clock region, and so is the L2 flush enqueued between steps.
+    def e2e_pass(n):
+        h2d = d2h = atoms = 0
+        pending = None
+        for k in range(n):
+            s = k % n_steps
+            t = dev.train_step_submit(shards[s], tc, step=s, workers=dist.world, rank=dist.rank)
+            dev.flush_l2(L2_FLUSH)
+            if pending is not None:
+                r = dev.train_step_wait(pending)
+                h2d, d2h, atoms = h2d + r.h2d_bytes, d2h + r.d2h_bytes, atoms + r.n_atoms
+            pending = t
+        r = dev.train_step_wait(pending)
+        return h2d + r.h2d_bytes, d2h + r.d2h_bytes, atoms + r.n_atoms
+
+    e2e_pass(max(args.warmup, 3))
     dist.barrier()
-    for k in range(K):
-        s = k % n_steps
-        dev.flush_l2(L2_FLUSH)
-        dev.sync()
-        t0 = time.perf_counter()
-        r = dev.train_step(shards[s], tc, step=s, workers=dist.world, rank=dist.rank)
-        e2e_s += time.perf_counter() - t0
-        h2d += r.h2d_bytes
-        d2h += r.d2h_bytes
-        e2e_atoms += r.n_atoms
+    dev.sync()
+    t0 = time.perf_counter()
+    h2d, d2h, e2e_atoms = e2e_pass(K)
+    e2e_s = time.perf_counter() - t0
     e2e_max = dist.allreduce(e2e_s, "max")
     e2e_atoms_all = dist.allreduce(float(e2e_atoms), "sum")
     e2e = e2e_atoms_all / e2e_max
@@ -289,9 +300,12 @@ def run_ours(args, dist):
                    "edges_per_step_per_gpu": P_mean, "parallelism": f"dp{dist.world}",
                    "schedule": "balanced (G=%d, B=%d, S=%d)" % (dist.world, BATCH_PER_GPU, SPLITS),
                    "l2": "flushed between timed steps (256 MiB memset outside the events)",
-                   "inputs": "value: device-resident staged batches; e2e: host batches via lamm_train_step"},
+                   "inputs": "value: device-resident staged batches; e2e: host batches via lamm_train_step_submit/_wait"},
         "e2e": {"value": e2e, "unit": "atoms/s", "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
-                "ms_per_step": e2e_max / K * 1e3},
+                "ms_per_step": e2e_max / K * 1e3,
+                "method": "wall clock over K pipelined lamm_train_step_submit/_wait calls with host batches "
+                          "(pack + H2D + step + D2H of the result per step; the 256 MiB L2 flush between "
+                          "steps is inside the timed region)"},
         "gpu_launches": launches,
         "roofline": roof,
         "kernels": kern,

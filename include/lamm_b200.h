@@ -233,6 +233,21 @@ int lamm_train_step(lamm_ctx* ctx, const lamm_batch_view* batch, const lamm_trai
 int lamm_train_step_workers(lamm_ctx* ctx, const lamm_batch_view* batches, int32_t workers,
                             const lamm_train_config* cfg, int64_t step, lamm_step_result* result);
 
+/* Pipelined train steps (the step body of S/trainer.cpp:258-327, same results as
+ * lamm_train_step in the same order): lamm_train_step_submit packs the batch into
+ * one of two pinned host blobs and enqueues upload -> step -> optimizer -> header
+ * read-back without waiting, so the host packs step k+1 while the device runs
+ * step k; lamm_train_step_wait(ticket) waits for the oldest outstanding step and
+ * fills its result. At most two steps in flight; tickets are waited for in
+ * order. A step that overflows the edge capacity (or runs non-finite) makes the
+ * steps behind it skip their update on the device; the wait then reruns the
+ * chain in order, so parameters and results equal the synchronous sequence
+ * (a non-finite step still reports LAMM_ENONFINITE at its wait). The synchronous
+ * step calls are refused while tickets are outstanding. */
+int lamm_train_step_submit(lamm_ctx* ctx, const lamm_batch_view* batch, const lamm_train_config* cfg, int64_t step,
+                           int32_t workers, int32_t rank, int64_t* ticket);
+int lamm_train_step_wait(lamm_ctx* ctx, int64_t ticket, lamm_step_result* result);
+
 /* Device-resident staging for throughput runs: packs a device-batch exactly as
  * lamm_train_step would (denoise draws for `step`, `rank`) into HBM slot
  * `slot` (0..1023); lamm_train_step_staged then runs the same step from that

@@ -81,6 +81,7 @@ EXPORTS = [
     "lamm_last_step_launches", "lamm_greedy_assign", "lamm_plan", "lamm_schedule_metrics", "lamm_make_trace",
     "lamm_temperature_counts", "lamm_build_epoch_index", "lamm_synth_counts", "lamm_synth_fill",
     "lamm_mix_seed", "lamm_rng_normals", "lamm_stage", "lamm_train_step_staged", "lamm_anomalies",
+    "lamm_train_step_submit", "lamm_train_step_wait",
     "lamm_flush_l2", "lamm_step_times", "lamm_evaluate", "lamm_cell_inverse",
     "lamm_checkpoint_save", "lamm_checkpoint_load", "lamm_rms_state_save", "lamm_rms_state_load",
     "lamm_subset_info", "lamm_subset_read", "lamm_train_step_workers",

@@ -303,6 +303,37 @@ class Device:
         return StepResult(res.loss, res.grad_norm, _breakdown(res.local), res.n_atoms, res.n_edges, res.status,
                           res.h2d_bytes, res.d2h_bytes)
 
+    def train_step_submit(self, batch: dict, tcfg: TrainConfig, step: int, workers: int = 1, rank: int = 0) -> int:
+        """Pipelined train step (lamm_train_step_submit): packs and enqueues the
+        step without waiting; returns the ticket for train_step_wait. At most two
+        in flight, waited for in order."""
+        v, keep = _batch_view(batch)
+        tc = tcfg.c()
+        t = C.c_int64()
+        check(lib().lamm_train_step_submit(self._h, C.byref(v), C.byref(tc), C.c_int64(step), workers, rank,
+                                           C.byref(t)))
+        return t.value
+
+    def train_step_wait(self, ticket: int) -> StepResult:
+        """Waits for the oldest submitted step and returns its result."""
+        res = StepResultC()
+        check(lib().lamm_train_step_wait(self._h, C.c_int64(ticket), C.byref(res)))
+        return StepResult(res.loss, res.grad_norm, _breakdown(res.local), res.n_atoms, res.n_edges, res.status,
+                          res.h2d_bytes, res.d2h_bytes)
+
+    def train_steps_pipelined(self, batches, tcfg: TrainConfig, steps, workers: int = 1, rank: int = 0):
+        """Runs the steps (batch, step index) in order, the host packing step k+1
+        while the device runs step k; returns the results in order."""
+        out, pending = [], None
+        for b, st in zip(batches, steps):
+            t = self.train_step_submit(b, tcfg, st, workers, rank)
+            if pending is not None:
+                out.append(self.train_step_wait(pending))
+            pending = t
+        if pending is not None:
+            out.append(self.train_step_wait(pending))
+        return out
+
     def train_step_workers(self, batches, tcfg: TrainConfig, step: int) -> StepResult:
         """One optimizer step over G SIMULATED workers on this device
         (S/trainer.cpp:262-319): ``batches[g]`` is worker g's device-batch."""

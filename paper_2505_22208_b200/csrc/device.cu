@@ -132,6 +132,20 @@ struct lamm_ctx {
         int me = 0, mf = 0;
     };
     std::vector<Slot> staged;
+    // pipelined steps (lamm_train_step_submit / _wait): at most two in flight,
+    // each with its own pinned blob and pinned result header
+    struct Inflight {
+        char* blob = nullptr;
+        size_t cap = 0, bytes = 0;
+        lamm_b200::StepHeader* result = nullptr;
+        cudaEvent_t done = nullptr;
+        int32_t B = 0, workers = 1, rank = 0;
+        int64_t N = 0, step = 0;
+        int me = 0, mf = 0;
+        lamm_train_config tc{};
+    };
+    Inflight ring[2];
+    int64_t next_ticket = 0, oldest_ticket = 0;
     lamm_b200::Buf anomaly, flush;
     // NCCL
     ncclComm_t comm = nullptr;
@@ -868,36 +882,45 @@ void opt_body(Ctx& c) {
 
 // One train step from a staged blob (pinned host blob: H2D; resident slot:
 // D2D); returns the header after it, or a zeroed header when !sync.
-StepHeader run_train_step(Ctx& c, const void* src, size_t bytes, cudaMemcpyKind kind, bool sync = true) {
+// The step after its upload: the step graph, the allreduce (G > 1), the optimizer graph.
+void launch_step(Ctx& c) {
+    const int64_t l0 = c.launches;
+    if (c.use_graph) {
+        if (c.graph_dirty || !c.g_step) {
+            destroy_graphs(c);
+            c.slot_cursor = 0;
+            c.g_step = capture(c, step_body);
+            c.g_opt = capture(c, opt_body);
+            c.graph_dirty = false;
+            c.graph_launches = c.launches - l0;
+        }
+        CK(cudaGraphLaunch(c.g_step, c.stream));
+    } else {
+        c.slot_cursor = 0;
+        step_body(c);
+    }
+    if (c.nranks > 1)
+        nccl_check(nccl().all_reduce(c.grads.p, c.grads.p, static_cast<size_t>(c.NP + 4), ncclFloat32, ncclSum,
+                                     c.comm, c.stream),
+                   "ncclAllReduce");
+    if (c.use_graph) CK(cudaGraphLaunch(c.g_opt, c.stream));
+    else opt_body(c);
+    c.last_step_launches = c.use_graph ? c.graph_launches : c.launches - l0;
+}
+
+// clear_poison: a rerun of a pipelined (chain) step; every attempt starts with
+// the in-flight poison cleared (an overflowing attempt sets it again).
+StepHeader run_train_step(Ctx& c, const void* src, size_t bytes, cudaMemcpyKind kind, bool sync = true,
+                          bool clear_poison = false) {
     for (int attempt = 0;; ++attempt) {
         ensure_capacity(c, c.N, c.B, edge_guess(c.N));
         if (bytes > c.d_stage.bytes) ensure_stage(c, bytes);
+        if (clear_poison) CK(cudaMemsetAsync(c.anomaly.as<unsigned int>() + 8, 0, sizeof(unsigned int), c.stream));
         CK(cudaEventRecord(c.step_ev[0], c.stream));
         CK(cudaMemcpyAsync(c.d_stage.p, src, bytes, kind, c.stream));
-        const int64_t l0 = c.launches;
-        if (c.use_graph) {
-            if (c.graph_dirty || !c.g_step) {
-                destroy_graphs(c);
-                c.slot_cursor = 0;
-                c.g_step = capture(c, step_body);
-                c.g_opt = capture(c, opt_body);
-                c.graph_dirty = false;
-                c.graph_launches = c.launches - l0;
-            }
-            CK(cudaGraphLaunch(c.g_step, c.stream));
-        } else {
-            c.slot_cursor = 0;
-            step_body(c);
-        }
-        if (c.nranks > 1)
-            nccl_check(nccl().all_reduce(c.grads.p, c.grads.p, static_cast<size_t>(c.NP + 4), ncclFloat32, ncclSum,
-                                         c.comm, c.stream),
-                       "ncclAllReduce");
-        if (c.use_graph) CK(cudaGraphLaunch(c.g_opt, c.stream));
-        else opt_body(c);
+        launch_step(c);
         CK(cudaEventRecord(c.step_ev[1], c.stream));
         c.step_ev_pending = true;
-        c.last_step_launches = c.use_graph ? c.graph_launches : c.launches - l0;
         if (!sync) return StepHeader{};
         const StepHeader h = read_header(c);
         if (h.status != 2) {
@@ -1019,6 +1042,11 @@ LAMM_API void lamm_ctx_destroy(lamm_ctx* c) {
         if (b->p) cudaFree(b->p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->h_result) cudaFreeHost(c->h_result);
+    for (auto& f : c->ring) {
+        if (f.blob) cudaFreeHost(f.blob);
+        if (f.result) cudaFreeHost(f.result);
+        if (f.done) cudaEventDestroy(f.done);
+    }
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : c->step_ev)
@@ -1434,6 +1462,26 @@ void fill_result(Ctx& c, const StepHeader& h, lamm_step_result* res) {
     res->h2d_bytes = c.last_h2d;
     res->d2h_bytes = static_cast<int64_t>(sizeof(StepHeader));
 }
+// Enqueues one pipelined step: upload of the slot's pinned blob, the step and
+// optimizer graphs, and the read-back of its header into the slot's pinned
+// result, then the slot's completion event. Capacity growth or a graph
+// recapture first drains the stream (nothing in flight is reallocated).
+void enqueue_chained(Ctx& c, Ctx::Inflight& f) {
+    c.B = f.B, c.N = f.N, c.me = f.me, c.mf = f.mf;
+    apply_train_config(c, &f.tc, f.workers, f.rank);
+    if (c.graph_dirty || f.N > c.Ncap || f.B > c.Bcap || edge_guess(f.N) > c.Pcap || f.bytes > c.d_stage.bytes)
+        CK(cudaStreamSynchronize(c.stream));
+    ensure_capacity(c, f.N, f.B, edge_guess(f.N));
+    if (f.bytes > c.d_stage.bytes) ensure_stage(c, f.bytes);
+    CK(cudaMemcpyAsync(c.d_stage.p, f.blob, f.bytes, cudaMemcpyHostToDevice, c.stream));
+    launch_step(c);
+    CK(cudaMemcpyAsync(f.result, c.d_stage.p, sizeof(StepHeader), cudaMemcpyDeviceToHost, c.stream));
+    CK(cudaEventRecord(f.done, c.stream));
+}
+
+void require_no_chain(const Ctx& c) {
+    require(c.oldest_ticket == c.next_ticket, "synchronous step while pipelined steps are in flight (lamm_train_step_wait)");
+}
 }  // namespace lamm_b200
 
 LAMM_API int lamm_stage(lamm_ctx* c, const lamm_batch_view* b, const lamm_train_config* tc, int64_t step,
@@ -1464,6 +1512,7 @@ LAMM_API int lamm_train_step_staged(lamm_ctx* c, int32_t slot, int32_t sync, lam
         require(c != nullptr, "train_step_staged: null ctx");
         require(slot >= 0 && static_cast<size_t>(slot) < c->staged.size() && c->staged[slot].bytes > 0,
                 "train_step_staged: empty slot");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         auto& s = c->staged[slot];
         c->B = s.B, c->N = s.N, c->me = s.me, c->mf = s.mf;
@@ -1501,6 +1550,7 @@ LAMM_API int lamm_train_step(lamm_ctx* c, const lamm_batch_view* b, const lamm_t
                              int32_t workers, int32_t rank, lamm_step_result* res) {
     return lamm_guard([&] {
         require(c && b && tc, "train_step: null argument");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         validate_batch(*c, b);
         apply_train_config(*c, tc, workers, rank);
@@ -1510,6 +1560,76 @@ LAMM_API int lamm_train_step(lamm_ctx* c, const lamm_batch_view* b, const lamm_t
         fill_result(*c, h, res);
         if (h.status == 1)
             throw NonFinite("non-finite loss or gradient at step " + std::to_string(step));
+    });
+}
+
+
+LAMM_API int lamm_train_step_submit(lamm_ctx* c, const lamm_batch_view* b, const lamm_train_config* tc, int64_t step,
+                                    int32_t workers, int32_t rank, int64_t* ticket) {
+    return lamm_guard([&] {
+        require(c && b && tc && ticket, "train_step_submit: null argument");
+        require(c->next_ticket - c->oldest_ticket < 2, "train_step_submit: two steps in flight; wait for the oldest");
+        CK(cudaSetDevice(c->device));
+        validate_batch(*c, b);
+        apply_train_config(*c, tc, workers, rank);  // validation (enqueue re-applies it)
+        auto& f = c->ring[c->next_ticket & 1];
+        if (!f.result) CK(cudaMallocHost(reinterpret_cast<void**>(&f.result), sizeof(StepHeader)));
+        if (!f.done) CK(cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming));
+        // pack into the slot's own pinned blob (its previous step has completed:
+        // at most two in flight and this slot's ticket was waited for)
+        std::swap(c->h_stage, f.blob);
+        std::swap(c->h_stage_cap, f.cap);
+        size_t bytes = 0;
+        try {
+            bytes = pack_batch(*c, b, true, tc, step, rank);
+        } catch (...) {
+            std::swap(c->h_stage, f.blob);
+            std::swap(c->h_stage_cap, f.cap);
+            throw;
+        }
+        std::swap(c->h_stage, f.blob);
+        std::swap(c->h_stage_cap, f.cap);
+        reinterpret_cast<StepHeader*>(f.blob)->chain = 1;
+        f.bytes = bytes, f.B = c->B, f.N = c->N, f.me = c->me, f.mf = c->mf;
+        f.step = step, f.workers = workers, f.rank = rank, f.tc = *tc;
+        c->batch_valid = c->nlist_valid = c->fwd_valid = c->loss_valid = false;
+        enqueue_chained(*c, f);
+        *ticket = c->next_ticket++;
+    });
+}
+
+LAMM_API int lamm_train_step_wait(lamm_ctx* c, int64_t ticket, lamm_step_result* res) {
+    return lamm_guard([&] {
+        require(c != nullptr, "train_step_wait: null ctx");
+        require(ticket == c->oldest_ticket && ticket < c->next_ticket, "train_step_wait: not the oldest ticket in flight");
+        CK(cudaSetDevice(c->device));
+        auto& f = c->ring[ticket & 1];
+        CK(cudaEventSynchronize(f.done));
+        if (f.result->status == 2 || f.result->status == 3) {
+            // capacity overflow, or skipped behind a failed in-flight step: drain, clear
+            // the poison, rerun this step and the later in-flight ones in order
+            // (run_train_step regrows capacity until the step fits)
+            CK(cudaStreamSynchronize(c->stream));
+            CK(cudaMemsetAsync(c->anomaly.as<unsigned int>() + 8, 0, sizeof(unsigned int), c->stream));
+            for (int64_t t = ticket; t < c->next_ticket; ++t) {
+                auto& g = c->ring[t & 1];
+                c->B = g.B, c->N = g.N, c->me = g.me, c->mf = g.mf;
+                apply_train_config(*c, &g.tc, g.workers, g.rank);
+                *g.result = run_train_step(*c, g.blob, g.bytes, cudaMemcpyHostToDevice, true, true);
+                if (g.result->status == 1) {  // later ones stay "skipped" and rerun at their wait
+                    for (int64_t u = t + 1; u < c->next_ticket; ++u) c->ring[u & 1].result->status = 3;
+                    break;
+                }
+            }
+        }
+        const StepHeader h = *f.result;
+        c->oldest_ticket = ticket + 1;
+        if (h.status == 1 && c->oldest_ticket == c->next_ticket)  // nothing behind it: clear the poison now
+            CK(cudaMemsetAsync(c->anomaly.as<unsigned int>() + 8, 0, sizeof(unsigned int), c->stream));
+        c->B = f.B, c->N = f.N, c->me = f.me, c->mf = f.mf;
+        c->last_h2d = static_cast<int64_t>(f.bytes);
+        fill_result(*c, h, res);
+        if (h.status == 1) throw NonFinite("non-finite loss or gradient at step " + std::to_string(f.step));
     });
 }
 

@@ -53,6 +53,7 @@ struct StepHeader {
     int32_t me, mf;              // this rank's sum m_E, sum m_F (after denoise relabelling)
     int32_t nslots, status;      // distinct atomic numbers; non-finite flag
     int32_t workers, n_large;    // n_large: samples above kSmallAtoms (cell-list neighbour search)
+    int32_t chain, pad2;         // chain: submitted by lamm_train_step_submit (in-flight poison applies)
     double lambda_e, lambda_f;
     double loss_energy, loss_force, loss_total;  // this rank's Eq. (5) breakdown
     double grad_norm, clip_scale, global_loss;
@@ -148,7 +149,7 @@ struct Dev {
     float* tanh_emb_w;       // writable alias of tanh_emb
     int64_t NP;
     int32_t emb_rows;
-    unsigned int* anomaly;   // steps whose update was skipped
+    unsigned int* anomaly;   // [0] steps whose update was skipped, [8] in-flight poison, [16..] grid barrier
     float* wpack;            // [L][4][H*H] packed tcgen05 weight operands (k_pack_weights)
 };
 

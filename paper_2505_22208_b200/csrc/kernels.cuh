@@ -1178,14 +1178,19 @@ __device__ __forceinline__ int opt_update(const Dev& d, int G, double inv_g, dou
     else if (d.g64_loss)
         loss = (d.g64_in[d.NP] + d.g64_in[d.NP + 1]) / static_cast<double>(G);
     const bool overflow = !d.g64_in && d.grads[d.NP + 2] > 0.f;
-    const int status = overflow ? 2 : ((!isfinite(loss) || !isfinite(gn)) ? 1 : 0);
+    // a step submitted behind a failed (overflow / non-finite) in-flight step is
+    // skipped (status 3) so the host can rerun the chain in order
+    const bool chain = d.hdr->chain != 0;
+    const bool poisoned = chain && *reinterpret_cast<volatile unsigned int*>(d.anomaly + 8) != 0u;
+    const int status = overflow ? 2 : ((!isfinite(loss) || !isfinite(gn)) ? 1 : (poisoned ? 3 : 0));
     const double cs = (clip > 0.0 && gn > clip) ? clip / gn : 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         d.hdr->grad_norm = gn;
         d.hdr->global_loss = loss;
         d.hdr->status = status;
         d.hdr->clip_scale = cs;
-        if (status != 0 && !d.g64_in) atomicAdd(d.anomaly, 1u);
+        if ((status == 1 || status == 2) && !d.g64_in) atomicAdd(d.anomaly, 1u);
+        if ((status == 1 || status == 2) && chain) d.anomaly[8] = 1u;
     }
     if (status != 0) return status;
     const int64_t emb_n = static_cast<int64_t>(kMaxZ) * d.H;
