@@ -137,6 +137,8 @@ struct lamm_ctx {
     struct Inflight {
         char* blob = nullptr;
         size_t cap = 0, bytes = 0;
+        lamm_b200::Buf inbox;          // device copy of the blob, uploaded on copy_stream
+        cudaEvent_t uploaded = nullptr;
         lamm_b200::StepHeader* result = nullptr;
         cudaEvent_t done = nullptr;
         int32_t B = 0, workers = 1, rank = 0;
@@ -145,6 +147,7 @@ struct lamm_ctx {
         lamm_train_config tc{};
     };
     Inflight ring[2];
+    cudaStream_t copy_stream = nullptr;  // uploads of pipelined steps (overlap the running step)
     int64_t next_ticket = 0, oldest_ticket = 0;
     lamm_b200::Buf anomaly, flush;
     // NCCL
@@ -1042,7 +1045,10 @@ LAMM_API void lamm_ctx_destroy(lamm_ctx* c) {
         if (b->p) cudaFree(b->p);
     if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->h_result) cudaFreeHost(c->h_result);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream), cudaStreamDestroy(c->copy_stream);
     for (auto& f : c->ring) {
+        if (f.inbox.p) cudaFree(f.inbox.p);
+        if (f.uploaded) cudaEventDestroy(f.uploaded);
         if (f.blob) cudaFreeHost(f.blob);
         if (f.result) cudaFreeHost(f.result);
         if (f.done) cudaEventDestroy(f.done);
@@ -1473,7 +1479,19 @@ void enqueue_chained(Ctx& c, Ctx::Inflight& f) {
         CK(cudaStreamSynchronize(c.stream));
     ensure_capacity(c, f.N, f.B, edge_guess(f.N));
     if (f.bytes > c.d_stage.bytes) ensure_stage(c, f.bytes);
-    CK(cudaMemcpyAsync(c.d_stage.p, f.blob, f.bytes, cudaMemcpyHostToDevice, c.stream));
+    // the upload runs on the copy stream while the previous step computes; the
+    // step's stream waits for it and moves the blob into the staging buffer (D2D)
+    if (!c.copy_stream) CK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+    if (!f.uploaded) CK(cudaEventCreateWithFlags(&f.uploaded, cudaEventDisableTiming));
+    if (f.inbox.bytes < f.bytes) {
+        if (f.inbox.p) CK(cudaFree(f.inbox.p));
+        CK(cudaMalloc(&f.inbox.p, f.cap));
+        f.inbox.bytes = f.cap;
+    }
+    CK(cudaMemcpyAsync(f.inbox.p, f.blob, f.bytes, cudaMemcpyHostToDevice, c.copy_stream));
+    CK(cudaEventRecord(f.uploaded, c.copy_stream));
+    CK(cudaStreamWaitEvent(c.stream, f.uploaded, 0));
+    CK(cudaMemcpyAsync(c.d_stage.p, f.inbox.p, f.bytes, cudaMemcpyDeviceToDevice, c.stream));
     launch_step(c);
     CK(cudaMemcpyAsync(f.result, c.d_stage.p, sizeof(StepHeader), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaEventRecord(f.done, c.stream));
