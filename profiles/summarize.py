@@ -157,7 +157,7 @@ def traffic(path, out, N, P, slot):
         n, t = acc.get(name, (0, 0.0))
         acc[name] = (n + 1, t + b)
     res = {"source": f"ncu --set full --clock-control none (cache flush before each replayed kernel), capture "
-                     f"{os.path.basename(path)}, profiles/r01_ncu_edge_kernels.md",
+                     f"{os.path.basename(path)}, profiles/r01_ncu_step_full.md",
            "step": {"N": N, "P": P, "slot": slot}, "kernels": {}}
     for name, (n, t) in acc.items():
         alg = bench.kernel_bytes(name, N, P)
