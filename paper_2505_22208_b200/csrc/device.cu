@@ -554,7 +554,7 @@ struct Model {
         int occ_e = 8, o = 0;
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_message<H, K, false>, kMsgGroups * H, smem_message()));
         occ_e = std::min(occ_e, o);
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_force<H, K>, kGroups * H, smem_force(c.D)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_force<H, K>, kForceGroups * H, smem_force(c.D)));
         occ_e = std::min(occ_e, o);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_head<H, K>, kGroups * H, smem_head(c.D)));
         occ_e = std::min(occ_e, o);
@@ -588,7 +588,7 @@ struct Model {
             launch(c, "update", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 0, act_map(c, d.mu[l]),
                    act_map(c, d.h[l + 1]), act_map(c, d.t[l + 1]));
         }
-        launch(c, "force", k_edge_force<H, K>, c.grid_edge, kGroups * H, smem_force(c.D), d);
+        launch(c, "force", k_edge_force<H, K>, c.grid_edge, kForceGroups * H, smem_force(c.D), d);
         launch(c, "force_out", k_force_out<H, K>, c.grid_warp, 256, 0, d, energy ? 0 : 1);
         if (energy) launch(c, "energy", k_energy, c.grid_small, 128, sizeof(double) * 128 * c.D, d);
     }

@@ -41,6 +41,8 @@ constexpr int kPartsPerCta = 12;
 // warps per SM, is slower than 4 x 64 - the per-chunk overhead doubles)
 constexpr int kMsgGroups = 4;
 constexpr int kMsgChunk = 64;
+// the force edges need no TMEM and fit 6 groups (768 threads, <= 85 registers)
+constexpr int kForceGroups = 6;
 
 // fcut*rbf of the edges for the tensor core: K-major canonical ("interleaved")
 // layout in blocks of 8 edges, element (e, k) at ((e/8)*(K/4) + k/4)*32 +
@@ -393,7 +395,7 @@ struct EdgeKernelSmem {
     static constexpr size_t one_cta = 120 * 1024;  // > half the SM: one CTA owns the 512 TMEM columns
     static size_t pad(size_t b) { return TC && b < one_cta ? one_cta : b; }
     static size_t message() { return pad(EdgeSmem<K, kMsgGroups, kMsgChunk>::extra_offset + filter); }
-    static size_t force(int) { return base; }
+    static size_t force(int) { return EdgeSmem<K, kForceGroups, kChunk>::extra_offset; }
     static size_t head(int D) { return base + 4 * kGroups * (3 * D * H + D * K); }
     static size_t bwd() { return pad(base + filter + 4 * kGroups * H * K); }
 };
@@ -507,8 +509,8 @@ struct ForceBody {
 };
 
 template <int H, int K>
-__global__ void __launch_bounds__(kGroups* H, 1) k_edge_force(Dev d) {
-    EdgeCta<H, K> c = edge_prologue<H, K>(d);
+__global__ void __launch_bounds__(kForceGroups* H, 1) k_edge_force(Dev d) {
+    EdgeCta<H, K, kForceGroups> c = edge_prologue<H, K, kForceGroups>(d);
     __syncthreads();
     const int kw = c.g % (H / 32);
     ForceBody<H, K> b{d, d.t[d.L], c.lt, d.L,
