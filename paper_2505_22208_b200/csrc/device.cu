@@ -171,6 +171,12 @@ namespace lamm_b200 {
 
 using Ctx = lamm_ctx;
 
+// Entry points that touch the device state refuse to run while pipelined steps
+// (lamm_train_step_submit) are in flight.
+void require_no_chain(const Ctx& c) {
+    require(c.oldest_ticket == c.next_ticket, "call while pipelined steps are in flight (lamm_train_step_wait first)");
+}
+
 Buf& buf(Ctx& c, const std::string& name) { return c.bufs[name]; }
 
 void ensure_buf(Ctx& c, const std::string& name, size_t bytes, bool& changed) {
@@ -1074,7 +1080,8 @@ LAMM_API int lamm_ctx_set_option(lamm_ctx* c, const char* name, int64_t value) {
         else if (n == "pdl") c->pdl = value != 0;
         else if (n == "export_fp64") {
             c->export64 = value != 0;
-            CK(cudaSetDevice(c->device));
+            require_no_chain(*c);
+        CK(cudaSetDevice(c->device));
             ensure_capacity(*c, 0, 0, 0);
             bool ch = false;
             if (c->export64) {
@@ -1090,6 +1097,7 @@ LAMM_API int lamm_ctx_set_option(lamm_ctx* c, const char* name, int64_t value) {
 LAMM_API int lamm_params_set(lamm_ctx* c, const double* flat, size_t n) {
     return lamm_guard([&] {
         require(c && flat && static_cast<int64_t>(n) == c->NP, "params_set: size mismatch");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         CK(cudaMemcpyAsync(c->p64.p, flat, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
         Dev d = make_dev(*c);
@@ -1104,6 +1112,7 @@ LAMM_API int lamm_params_set(lamm_ctx* c, const double* flat, size_t n) {
 LAMM_API int lamm_params_get(lamm_ctx* c, double* flat, size_t n) {
     return lamm_guard([&] {
         require(c && flat && static_cast<int64_t>(n) == c->NP, "params_get: size mismatch");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         CK(cudaMemcpyAsync(flat, c->p64.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -1113,6 +1122,7 @@ LAMM_API int lamm_params_get(lamm_ctx* c, double* flat, size_t n) {
 LAMM_API int lamm_rms_state_set(lamm_ctx* c, const double* flat, size_t n) {
     return lamm_guard([&] {
         require(c && flat && static_cast<int64_t>(n) == c->NP, "rms_state_set: size mismatch");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         CK(cudaMemcpyAsync(c->v64.p, flat, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -1122,6 +1132,7 @@ LAMM_API int lamm_rms_state_set(lamm_ctx* c, const double* flat, size_t n) {
 LAMM_API int lamm_rms_state_get(lamm_ctx* c, double* flat, size_t n) {
     return lamm_guard([&] {
         require(c && flat && static_cast<int64_t>(n) == c->NP, "rms_state_get: size mismatch");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         CK(cudaMemcpyAsync(flat, c->v64.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -1131,6 +1142,7 @@ LAMM_API int lamm_rms_state_get(lamm_ctx* c, double* flat, size_t n) {
 LAMM_API int lamm_ref_table_set(lamm_ctx* c, const lamm_ref_table* t) {
     return lamm_guard([&] {
         require(c != nullptr, "ref_table_set: null ctx");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         if (!t) {
             c->use_table = false;
@@ -1169,6 +1181,7 @@ LAMM_API int lamm_ref_table_set(lamm_ctx* c, const lamm_ref_table* t) {
 LAMM_API int lamm_batch_set(lamm_ctx* c, const lamm_batch_view* b) {
     return lamm_guard([&] {
         require(c != nullptr, "batch_set: null ctx");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         validate_batch(*c, b);
         const size_t bytes = pack_batch(*c, b, false, nullptr, 0, 0);
@@ -1186,6 +1199,7 @@ LAMM_API int lamm_labels_get(lamm_ctx* c, double* energy, double* forces) {
     return lamm_guard([&] {
         require(c != nullptr, "labels_get: null ctx");
         require_batch(*c);
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         if (energy) CK(cudaMemcpyAsync(energy, buf(*c, "En").p, 8 * c->B, cudaMemcpyDeviceToHost, c->stream));
         if (forces) CK(cudaMemcpyAsync(forces, buf(*c, "Fn").p, 24 * c->N, cudaMemcpyDeviceToHost, c->stream));
@@ -1197,6 +1211,7 @@ LAMM_API int lamm_neighbor_list(lamm_ctx* c, int64_t* n_pairs) {
     return lamm_guard([&] {
         require(c != nullptr, "neighbor_list: null ctx");
         require_batch(*c);
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         if (!c->nlist_valid) run_nlist(*c);
         const StepHeader h = read_header(*c);
@@ -1209,6 +1224,7 @@ LAMM_API int lamm_neighbor_list_copy(lamm_ctx* c, int64_t* sample_pair_ptr, int3
     return lamm_guard([&] {
         require(c != nullptr, "neighbor_list_copy: null ctx");
         require_batch(*c);
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         if (!c->nlist_valid) run_nlist(*c);
         const StepHeader h = read_header(*c);
@@ -1261,6 +1277,7 @@ void from_ref_layout(Ctx& c, const double* src, float* dst) {
 LAMM_API int lamm_forward(lamm_ctx* c, double* energy, double* forces) {
     return lamm_guard([&] {
         require(c != nullptr, "forward: null ctx");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         c->fwd_valid = false;
         ensure_forward(*c);
@@ -1278,6 +1295,7 @@ LAMM_API int lamm_forward(lamm_ctx* c, double* energy, double* forces) {
 LAMM_API int lamm_evaluate(lamm_ctx* c, const lamm_batch_view* b, lamm_eval_result* out) {
     return lamm_guard([&] {
         require(c && b && out, "evaluate: null argument");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         lamm_batch_view v = *b;
         v.denoise = nullptr;  // evaluate() takes the samples as given
@@ -1307,6 +1325,7 @@ LAMM_API int lamm_forward_cache_get(lamm_ctx* c, int which, int layer, double* o
         require(c && out, "forward_cache_get: null argument");
         require_batch(*c);
         require(c->fwd_valid, "forward_cache_get: run lamm_forward first");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         const int H = c->H;
         std::vector<float> v;
@@ -1332,6 +1351,7 @@ LAMM_API int lamm_loss_grad(lamm_ctx* c, const lamm_loss_config* cfg, lamm_loss_
                             double* g_forces) {
     return lamm_guard([&] {
         require(c != nullptr, "loss_grad: null ctx");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         const double le = cfg ? cfg->lambda_energy : 1.0, lf = cfg ? cfg->lambda_force : 1.0;
         require(le >= 0.0 && lf >= 0.0, "masked_loss: lambdas must be non-negative");
@@ -1367,6 +1387,7 @@ LAMM_API int lamm_loss_grad(lamm_ctx* c, const lamm_loss_config* cfg, lamm_loss_
 LAMM_API int lamm_backward(lamm_ctx* c, const double* up_energy, const double* up_forces, double* grads_accum) {
     return lamm_guard([&] {
         require(c != nullptr, "backward: null ctx");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         ensure_forward(*c);
         const bool general = up_energy || up_forces;
@@ -1394,6 +1415,7 @@ LAMM_API int lamm_backward(lamm_ctx* c, const double* up_energy, const double* u
 LAMM_API int lamm_grads_get(lamm_ctx* c, double* flat, size_t n) {
     return lamm_guard([&] {
         require(c && flat && static_cast<int64_t>(n) == c->NP, "grads_get: size mismatch");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         const auto g = d2h<float>(*c, c->grads.p, c->NP);
         for (int64_t k = 0; k < c->NP; ++k) flat[k] = g[k];
@@ -1414,6 +1436,7 @@ LAMM_API int lamm_comm_init(lamm_ctx* c, int nranks, int rank, const void* id128
     return lamm_guard([&] {
         require(c && id128, "comm_init: null argument");
         require(nranks >= 1 && rank >= 0 && rank < nranks, "comm_init: bad rank layout");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         if (nranks == 1) {
             c->nranks = 1, c->rank = 0;
@@ -1497,9 +1520,6 @@ void enqueue_chained(Ctx& c, Ctx::Inflight& f) {
     CK(cudaEventRecord(f.done, c.stream));
 }
 
-void require_no_chain(const Ctx& c) {
-    require(c.oldest_ticket == c.next_ticket, "synchronous step while pipelined steps are in flight (lamm_train_step_wait)");
-}
 }  // namespace lamm_b200
 
 LAMM_API int lamm_stage(lamm_ctx* c, const lamm_batch_view* b, const lamm_train_config* tc, int64_t step,
@@ -1507,6 +1527,7 @@ LAMM_API int lamm_stage(lamm_ctx* c, const lamm_batch_view* b, const lamm_train_
     return lamm_guard([&] {
         require(c && b && tc, "stage: null argument");
         require(slot >= 0 && slot < 1024, "stage: slot out of range");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         validate_batch(*c, b);
         apply_train_config(*c, tc, workers, rank);
@@ -1657,6 +1678,7 @@ LAMM_API int lamm_train_step_workers(lamm_ctx* c, const lamm_batch_view* batches
         require(c && batches && tc, "train_step_workers: null argument");
         require(workers >= 1, "train_step_workers: workers must be >= 1");
         require(c->nranks == 1, "train_step_workers: simulated workers need a context without a communicator");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         int64_t atoms = 0, edges = 0;
         for (int32_t g = 0; g < workers; ++g) {  // worker order, like S/trainer.cpp:262
@@ -1688,6 +1710,7 @@ LAMM_API int lamm_optimizer_step(lamm_ctx* c, const double* grad_sum, int32_t wo
     return lamm_guard([&] {
         require(c && grad_sum && tc, "optimizer_step: null argument");
         require(workers >= 1, "optimizer_step: workers must be >= 1");
+        require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         CK(cudaMemcpyAsync(c->g64.p, grad_sum, sizeof(double) * c->NP, cudaMemcpyHostToDevice, c->stream));
         Dev d = make_dev(*c);

@@ -449,6 +449,8 @@ def test_sync_step_refused_while_pipelined(pk):
     with pytest.raises(pk.InputError):
         dev.train_step(b, tc, step=1)
     with pytest.raises(pk.InputError):
+        dev.params()  # device state is not read mid-flight
+    with pytest.raises(pk.InputError):
         dev.train_step_wait(t + 1)
     assert np.isfinite(dev.train_step_wait(t).loss)
     dev.close()
