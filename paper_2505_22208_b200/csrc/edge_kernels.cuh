@@ -291,6 +291,7 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K, G, 
             const int ea = max(cb, e0) - cb, eb = min(cb + C, e1) - cb;
             const uint32_t trow = ft.tg + s * C + (quad * 32u << 16);
             const int blk0 = ea >> 3, blk1 = (eb + 7) >> 3;
+#pragma unroll(Body::kUnroll)
             for (int blk = blk0; blk < blk1; ++blk) {
                 typename Body::Reg r[8];
 #pragma unroll
@@ -410,6 +411,7 @@ struct MessageBody {
     static constexpr int kParts = TC ? 0 : kPartPlain;
     static constexpr bool kBlockHook = false;
     static constexpr bool kPrepare = false;
+    static constexpr int kUnroll = 2;  // block loop unroll (2: the r/rn register roles alternate)
     struct Reg {
         float t;
     };
@@ -466,6 +468,7 @@ struct ForceBody {
     static constexpr int kParts = kPartGeo | kPartPlain;
     static constexpr bool kBlockHook = false;
     static constexpr bool kPrepare = false;
+    static constexpr int kUnroll = 1;  // block loop unroll (2: the r/rn register roles alternate)
     static constexpr int kYW = 3 * H + 3 + 3 * K;  // per-atom feature floats
     struct Reg {
         float t;
@@ -666,6 +669,7 @@ struct HeadBody {
     static constexpr int kParts = kPartGeo | kPartPlain;
     static constexpr bool kBlockHook = false;
     static constexpr bool kPrepare = true;
+    static constexpr int kUnroll = 1;  // block loop unroll (2: the r/rn register roles alternate)
     struct Reg {
         float t;
     };
@@ -809,6 +813,7 @@ struct BwdBody {
     static constexpr int kParts = kPartPlain;
     static constexpr bool kBlockHook = true;
     static constexpr bool kPrepare = false;
+    static constexpr int kUnroll = 1;  // block loop unroll (2: the r/rn register roles alternate)
     struct Reg {
         float gm, t;
     };
