@@ -113,12 +113,14 @@ def triclinic_box(n=48, seed=0, cell=((11.5, 0.0, 0.0), (2.0, 11.0, 0.0), (1.0, 
     return np.array(pts), rng.choice(ORGANIC, n).astype(np.int32), cell
 
 
-def periodic_batch(lib, D=10, seed=3):
+def periodic_batch(lib, D=10, seed=3, large=False):
     """A mixed batch: two periodic crystals (diamond Si supercell, triclinic box) and
-    non-periodic molecules; labels from random values (parity only needs them finite)."""
+    non-periodic molecules; labels from random values (parity only needs them finite).
+    large: a 3x3x3 supercell (216 atoms) and a 150-atom triclinic box, i.e. samples
+    above kSmallAtoms that take the cell-list path."""
     mol = molecules(lib, 6, seed)
-    p1, z1, c1 = diamond_supercell(seed=seed)
-    p2, z2, c2 = triclinic_box(seed=seed + 1)
+    p1, z1, c1 = diamond_supercell(reps=3 if large else 2, seed=seed)
+    p2, z2, c2 = triclinic_box(n=150 if large else 48, seed=seed + 1)
     rng = np.random.default_rng(seed)
     extra = []
     for p, z in ((p1, z1), (p2, z2)):

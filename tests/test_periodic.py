@@ -91,9 +91,10 @@ def test_periodic_cell_list_bit_exact(pk, dev, oracle_port):
 
 
 @pytest.mark.gpu
-def test_periodic_train_step_matches_oracle(pk, oracle_port):
+@pytest.mark.parametrize("large", [False, True])
+def test_periodic_train_step_matches_oracle(pk, oracle_port, large):
     mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
-    b = cases.periodic_batch(pk, seed=5)
+    b = cases.periodic_batch(pk, seed=5, large=large)
     B = len(b["atom_ptr"]) - 1
     table = cases.random_table(cases.CFG[4], seed=4)
     params = oracle_port.init_params(cases.CFG, 8)
