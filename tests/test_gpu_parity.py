@@ -320,6 +320,7 @@ def test_nccl_allreduce_path_single_rank(pk):
         res = [dev.train_step(batch, _train_cfg(pk), step=s) for s in range(2)]
         dev.stage(batch, _train_cfg(pk), step=2, slot=0)
         res.append(dev.train_step_staged(0, sync=True))
+        res += dev.train_steps_pipelined([batch, batch], _train_cfg(pk), [3, 4])  # submit/wait with NCCL
         outs.append((dev.params(), dev.grads(), [r.loss for r in res]))
         dev.close()
     assert np.array_equal(outs[0][0], outs[1][0])
