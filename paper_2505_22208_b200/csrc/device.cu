@@ -591,7 +591,7 @@ struct Model {
         for (int l = 0; l < c.L; ++l) {
             launch(c, "message", l == 0 ? k_edge_message<H, K, true> : k_edge_message<H, K, false>, c.grid_edge,
                    kMsgGroups * H, smem_message(), d, l);
-            launch(c, "update", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 0, act_map(c, d.mu[l]),
+            launch(c, "update", k_node_gemm<H>, c.grid_upd, NodeGemmCfg<H>::NT, kGemmSmem, d, l, 0, act_map(c, d.mu[l]),
                    act_map(c, d.h[l + 1]), act_map(c, d.t[l + 1]));
         }
         launch(c, "force", k_edge_force<H, K>, c.grid_edge, kForceGroups * H, smem_force(c.D), d);
@@ -616,7 +616,7 @@ struct Model {
             if constexpr (kFusedBwd) {
                 launch(c, "bwd_gemm", k_bwd_gemm<H>, c.grid_upd, 256, BwdGemmSmem<H>::bytes, d, l, act_map(c, d.gh));
             } else {
-                launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, 256, kGemmSmem, d, l, 1, act_map(c, d.gh),
+                launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, NodeGemmCfg<H>::NT, kGemmSmem, d, l, 1, act_map(c, d.gh),
                        act_map(c, d.gm), act_map(c, d.gm));
                 launch(c, "dwu", k_dwu<H>, c.grid_gemm, 256, kDwuSmem, d, l);
             }

@@ -32,6 +32,7 @@ template <int H>
 struct NodeGemmCfg {
     static constexpr int NS = H == 128 ? 2 : 1;
     static constexpr int NC = H / NS;                       // output columns per CTA tile
+    static constexpr int NT = H == 32 ? 256 : 512;          // k_node_gemm threads (4 per TMEM lane)
     static constexpr size_t a_floats = 2 * kGemmM * H;      // activation tile hi | lo (full K)
     static constexpr size_t b_floats = 2 * NC * H;          // weight rows [NC][H] hi | lo
     static constexpr size_t bytes = 4 * (a_floats + b_floats) + 64 + 1024;  // + barriers, alignment slack
@@ -102,13 +103,13 @@ __global__ void __launch_bounds__(256) k_opt(Dev d, int G, double inv_g, double 
 // epilogue inputs (residual / mu) are prefetched while the tensor core runs.
 // Warps w and w+4 share TMEM lanes 32*(w%4).. and split the NC columns.
 template <int H>
-__global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, const __grid_constant__ CUtensorMap amap,
+__global__ void __launch_bounds__(NodeGemmCfg<H>::NT, 1) k_node_gemm(Dev d, int l, int mode, const __grid_constant__ CUtensorMap amap,
                                                       const __grid_constant__ CUtensorMap omap0,
                                                       const __grid_constant__ CUtensorMap omap1) {
     using Cfg = NodeGemmCfg<H>;
-    constexpr int NS = Cfg::NS, NC = Cfg::NC, CW = NC / 2;  // columns per thread
+    constexpr int NS = Cfg::NS, NC = Cfg::NC, NT = Cfg::NT, CW = NC / (NT / 128);  // columns per thread
     constexpr int KB = H / 32;                               // 32-column activation boxes (TMA, SWIZZLE_128B)
-    constexpr bool kTmaOut = CW == 32;  // epilogue through shared memory + TMA stores (one box per thread row)
+    constexpr bool kTmaOut = CW == 16 || CW == 32;  // epilogue through shared memory + TMA stores
     static_assert(CW % 16 == 0, "epilogue reads 16 columns at a time");
     extern __shared__ __align__(1024) unsigned char node_gemm_smem[];
     float* sm = reinterpret_cast<float*>(node_gemm_smem + ((1024u - (smem_u32(node_gemm_smem) & 1023u)) & 1023u));
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, co
     uint64_t* bar = reinterpret_cast<uint64_t*>(Bhi + Cfg::b_floats);
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2 + KB);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int quad = warp & 3, half = warp >> 2;
+    const int quad = warp & 3, part = warp >> 2;  // TMEM lane quarter, column part
     constexpr uint32_t kCols = NC < 32 ? 32 : NC;
     if (warp == 0) umma::tmem_alloc(tslot, kCols);
     if (tid == 0) {
@@ -167,10 +168,10 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, co
 #pragma unroll
         for (int kb = 0; kb < KB; ++kb) {
             mbar_wait(&bar[2 + kb], aphase);
-            constexpr int IT = kGemmM * 32 / 4 / 256;
+            constexpr int IT = kGemmM * 32 / 4 / NT;
 #pragma unroll
             for (int it = 0; it < IT; ++it) {
-                const int c = kb * kGemmM * 8 + tid + 256 * it;
+                const int c = kb * kGemmM * 8 + tid + NT * it;
                 const float4 x = *reinterpret_cast<const float4*>(Ahi + 4 * c);
                 *reinterpret_cast<float4*>(Alo + 4 * c) =
                     make_float4(umma::tf32_trunc_lo(x.x), umma::tf32_trunc_lo(x.y), umma::tf32_trunc_lo(x.z),
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, co
         aphase ^= 1u;
         if (w_pending) wphase ^= 1u, w_pending = false;
         // epilogue inputs for this thread's row/columns, fetched while the MMAs run
-        const int row = quad * 32 + lane, atom = base + row, c0 = np * NC + half * CW;
+        const int row = quad * 32 + lane, atom = base + row, c0 = np * NC + part * CW;
         const bool live = atom < N;
         float pre[CW];
 #pragma unroll
@@ -212,16 +213,18 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, co
         umma::fence_after();
         if constexpr (kTmaOut) {
             // outputs as SWIZZLE_128B boxes [128 rows][32 columns] in the (now free)
-            // activation tiles: box (array, half) = Ahi + (2 * array + half) * 4096;
-            // thread row r writes its 16-byte chunk q at chunk position q ^ (r % 8)
-            float* ob = Ahi + half * kGemmM * 32 + row * 32;
+            // activation tiles: box (array, b) = Ahi + (array * NC/32 + b) * 4096 holds tile
+            // columns [32 b, 32 b + 32); thread row r writes its 16-byte chunk q at chunk
+            // position q ^ (r % 8)
+            const int cb = part * CW;  // first tile column of this thread
+            float* ob = Ahi + (cb / 32) * kGemmM * 32 + row * 32;
 #pragma unroll
             for (int cc = 0; cc < CW; cc += 16) {
                 float v[16];
-                umma::ld16(tbase + (static_cast<uint32_t>(quad * 32) << 16) + half * CW + cc, v);
+                umma::ld16(tbase + (static_cast<uint32_t>(quad * 32) << 16) + cb + cc, v);
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
-                    const int q = cc / 4 + q4, pos = (q ^ (row & 7)) * 4;
+                    const int q = (cb % 32 + cc) / 4 + q4, pos = (q ^ (row & 7)) * 4;
                     float4 a, b;
                     if (mode == 0) {
                         float hn[4];
@@ -239,20 +242,20 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, co
                         a = b = make_float4(g[0], g[1], g[2], g[3]);
                     }
                     *reinterpret_cast<float4*>(ob + pos) = a;
-                    if (mode == 0) *reinterpret_cast<float4*>(ob + 2 * kGemmM * 32 + pos) = b;
+                    if (mode == 0) *reinterpret_cast<float4*>(ob + (NC / 32) * kGemmM * 32 + pos) = b;
                 }
             }
             umma::fence_proxy_async();  // generic-proxy writes -> visible to the TMA engine
             umma::fence_before();
             __syncthreads();
             if (tid == 0) {
-                const int nbox = mode == 0 ? 2 : 1;
-                for (int arr = 0; arr < nbox; ++arr)
-                    for (int hf = 0; hf < 2; ++hf)
+                const int narr = mode == 0 ? 2 : 1;
+                for (int arr = 0; arr < narr; ++arr)
+                    for (int hf = 0; hf < NC / 32; ++hf)
                         asm volatile(
                             "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                 reinterpret_cast<uint64_t>(arr == 0 ? &omap0 : &omap1)),
-                            "r"(np * NC + hf * CW), "r"(base), "r"(smem_u32(Ahi + (2 * arr + hf) * kGemmM * 32))
+                            "r"(np * NC + hf * 32), "r"(base), "r"(smem_u32(Ahi + (arr * (NC / 32) + hf) * kGemmM * 32))
                             : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(256, 1) k_node_gemm(Dev d, int l, int mode, co
 #pragma unroll
         for (int cc = 0; cc < CW; cc += 16) {
             float v[16];
-            umma::ld16(tbase + (static_cast<uint32_t>(quad * 32) << 16) + half * CW + cc, v);
+            umma::ld16(tbase + (static_cast<uint32_t>(quad * 32) << 16) + part * CW + cc, v);
             if (!live) continue;
             if (mode == 0) {
                 float hn[16], tn[16];
