@@ -194,6 +194,33 @@ def test_train_step_matches_oracle(pk, oracle_ref):
     dev.close()
 
 
+@pytest.mark.parametrize("cfg", [(64, 2, 16, 5.0, 3), (32, 1, 8, 4.0, 3)])
+def test_train_step_other_model_sizes(pk, oracle_ref, cfg):
+    """The other device instantiations (hidden 64 / rbf 16 and hidden 32 / rbf 8:
+    unfused update backward + split-K dW_u GEMM, FFMA filter) through a full step,
+    with samples above the cell-list threshold."""
+    mcfg = pk.ModelConfig(*cfg[:3], cutoff=cfg[3], heads=cfg[4])
+    dev = pk.Device(mcfg, seed=0)
+    params = oracle_ref.init_params(cfg, 21)
+    big = pk.synth_generate(2, 3, mode=300, sigma=0.01, min_atoms=290, max_atoms=310, elements=(6, 8))
+    batch = cases.with_heads(pk.concat([cases.mixed_batch(pk, D=cfg[4], seed=9, count=12), big]), cfg[4], seed=4)
+    batch["energy_mask"][:] = 1
+    B = len(batch["atom_ptr"]) - 1
+    table = cases.random_table(cfg[4], seed=2)
+    tc = _train_cfg(pk, clip_norm=1e9)
+    v0 = np.zeros_like(params)
+    ref = oracle_ref.train_step(cfg, 1, B, batch, table, params, v0, noise_sigma=tc.noise_sigma,
+                                noise_scheme=1, seed=tc.seed, step=1, clip=tc.clip_norm)
+    dev.set_params(params)
+    dev.set_rms_state(v0)
+    dev.set_reference_table(table)
+    res = dev.train_step(batch, tc, step=1, workers=1, rank=0)
+    assert abs(res.loss - ref["loss"]) <= TOL * abs(ref["loss"])
+    for name, t in tensors(cfg, dev.grads()).items():
+        assert_close(t, tensors(cfg, ref["grads"])[name], what=f"{cfg[0]}: step d/d{name}")
+    dev.close()
+
+
 def test_denoise_labels_match_reference(pk, oracle_ref):
     mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
     dev = pk.Device(mcfg, seed=0)
