@@ -118,6 +118,7 @@ struct lamm_ctx {
     int grid_edge = 0, grid_emb = 0;
     // graphs
     cudaGraphExec_t g_step = nullptr, g_opt = nullptr;
+    cudaGraphExec_t g_full = nullptr;  // step + optimizer in one graph (single rank: no allreduce between)
     bool graph_dirty = true;
     bool use_graph = true, profile = false, export64 = false, pdl = true;
     int denoise_scheme = 1;
@@ -484,11 +485,13 @@ void launch_coop(Ctx& c, const char* name, void (*kernel)(KArgs...), int grid, i
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = c.stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cudaLaunchAttribute attr2[2];
+    attr2[0].id = cudaLaunchAttributeCooperative;
+    attr2[0].val.cooperative = 1;
+    attr2[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr2[1].val.programmaticStreamSerializationAllowed = c.pdl ? 1 : 0;
+    cfg.attrs = attr2;
+    cfg.numAttrs = 2;
     CK(cudaLaunchKernelEx(&cfg, kernel, args...));
     if (slot) CK(cudaEventRecordWithFlags(slot->b, c.stream, cudaEventRecordExternal));
     ++c.launches;
@@ -857,7 +860,8 @@ void run_nlist(Ctx& c) {
 void destroy_graphs(Ctx& c) {
     if (c.g_step) cudaGraphExecDestroy(c.g_step);
     if (c.g_opt) cudaGraphExecDestroy(c.g_opt);
-    c.g_step = c.g_opt = nullptr;
+    if (c.g_full) cudaGraphExecDestroy(c.g_full);
+    c.g_step = c.g_opt = c.g_full = nullptr;
 }
 
 cudaGraphExec_t capture(Ctx& c, void (*body)(Ctx&)) {
@@ -892,8 +896,26 @@ void opt_body(Ctx& c) {
 // One train step from a staged blob (pinned host blob: H2D; resident slot:
 // D2D); returns the header after it, or a zeroed header when !sync.
 // The step after its upload: the step graph, the allreduce (G > 1), the optimizer graph.
+void full_body(Ctx& c) {
+    step_body(c);
+    opt_body(c);
+}
+
 void launch_step(Ctx& c) {
     const int64_t l0 = c.launches;
+    if (c.use_graph && c.nranks == 1 && !c.profile) {
+        // one graph: the optimizer's cooperative launch follows grad_reduce with
+        // programmatic serialization like every other kernel of the step
+        if (c.graph_dirty) destroy_graphs(c), c.graph_dirty = false;
+        if (!c.g_full) {
+            c.slot_cursor = 0;
+            c.g_full = capture(c, full_body);
+            c.graph_launches = c.launches - l0;
+        }
+        CK(cudaGraphLaunch(c.g_full, c.stream));
+        c.last_step_launches = c.graph_launches;
+        return;
+    }
     if (c.use_graph) {
         if (c.graph_dirty || !c.g_step) {
             destroy_graphs(c);
