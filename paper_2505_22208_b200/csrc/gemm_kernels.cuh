@@ -514,15 +514,16 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l, const __grid_
     }
     const int row = quad * 32 + lane;
     float* part = d.part_wu[l] + static_cast<int64_t>(blockIdx.x) * H * NC;
+    if (done > 0)  // CTAs without a tile write nothing (k_grad_reduce reads CTAs < ntiles only)
 #pragma unroll
-    for (int cc = 0; cc < CW; cc += 16) {
-        float v[16];
-        umma::ld16(tD2 + lane_off + half * CW + cc, v);
+        for (int cc = 0; cc < CW; cc += 16) {
+            float v[16];
+            umma::ld16(tD2 + lane_off + half * CW + cc, v);
 #pragma unroll
-        for (int k = 0; k < 16; k += 4)
-            *reinterpret_cast<float4*>(part + row * NC + half * CW + cc + k) =
-                done > 0 ? make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+            for (int k = 0; k < 16; k += 4)
+                *reinterpret_cast<float4*>(part + row * NC + half * CW + cc + k) =
+                    make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
+        }
     umma::fence_before();
     __syncthreads();
     if (warp == 0) umma::tmem_dealloc(tbase, 512);

@@ -1080,7 +1080,7 @@ __global__ void __launch_bounds__(256) k_grad_reduce(Dev d, SegTable tab) {
             const int64_t off = e - sg.dst;
             // this thread's partial stream: first CTA c0, CTA step cs, element base + c * stride
             const float* base = nullptr;
-            int c0 = g, cs = 8;
+            int c0 = g, cs = 8, ncta = sg.ncta;
             int64_t stride = sg.stride;
             if (sg.kind == 1) {
                 const int zrow = static_cast<int>(off / H), a = static_cast<int>(off % H);
@@ -1088,23 +1088,25 @@ __global__ void __launch_bounds__(256) k_grad_reduce(Dev d, SegTable tab) {
                 if (slot >= 0) base = sg.src + slot * H + a;
                 stride = static_cast<int64_t>(ns) * H;
             } else if (sg.kind == 2) {
-                // column-split partials: CTA c holds columns [np*nc, np*nc+nc), np = c % (H/nc)
+                // column-split partials: CTA c holds columns [np*nc, np*nc+nc), np = c % (H/nc);
+                // only the CTAs that had a 128-atom tile wrote one (c < ntiles)
                 const int nc = sg.stride / H, nsplit = H / nc;
                 const int b = static_cast<int>(off / H), a = static_cast<int>(off % H), np = a / nc;
                 base = sg.src + b * nc + (a - np * nc);
                 c0 = np + nsplit * g;
                 cs = 8 * nsplit;
+                ncta = min(ncta, (d.hdr->N + 127) / 128 * nsplit);
             } else {
                 base = sg.src + off;
             }
             if (base) {  // 4 loads in flight per step, summed in stream order
                 int c = c0;
-                for (; c + 3 * cs < sg.ncta; c += 4 * cs) {
+                for (; c + 3 * cs < ncta; c += 4 * cs) {
                     const float v0 = __ldcg(base + c * stride), v1 = __ldcg(base + (c + cs) * stride);
                     const float v2 = __ldcg(base + (c + 2 * cs) * stride), v3 = __ldcg(base + (c + 3 * cs) * stride);
                     acc = (((acc + v0) + v1) + v2) + v3;
                 }
-                for (; c < sg.ncta; c += cs) acc += __ldcg(base + c * stride);
+                for (; c < ncta; c += cs) acc += __ldcg(base + c * stride);
             }
         }
         red[g][k] = acc;
