@@ -378,6 +378,7 @@ __global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) 
     }
     __shared__ double mean[3];
     __shared__ double stage[4][128];
+    __shared__ double sp[3][kSmallAtoms];  // positions of a small sample
     __shared__ int scan_scratch[4];
     __shared__ bool last;
     for (int s = blockIdx.x; s < B; s += gridDim.x) {
@@ -473,6 +474,8 @@ __global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) 
                     d.Fn[3 * a + c] = d.use_table ? __dmul_rn(fs, lab) : lab;
                 }
                 d.x[a] = xyz[0], d.y[a] = xyz[1], d.z[a] = xyz[2];
+                if (hi - lo <= kSmallAtoms)  // the pair counts below read them from shared memory
+                    sp[0][a - lo] = xyz[0], sp[1][a - lo] = xyz[1], sp[2][a - lo] = xyz[2];
             }
         }
         __syncthreads();
@@ -483,21 +486,22 @@ __global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) 
             continue;
         }
         // neighbour counts of the sample (S/core.cpp:30-48), warp per atom, from the
-        // positions this block just wrote (plain loads: visible after the barrier)
+        // positions this block just staged in shared memory (visible after the barrier)
         const int lane = threadIdx.x & 31;
-        for (int64_t i = lo + (threadIdx.x >> 5); i < hi; i += blockDim.x >> 5) {
-            const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
+        const int n = static_cast<int>(hi - lo);
+        for (int il = threadIdx.x >> 5; il < n; il += blockDim.x >> 5) {
+            const double xi = sp[0][il], yi = sp[1][il], zi = sp[2][il];
             int cnt = 0;
-            for (int64_t j0 = lo; j0 < hi; j0 += 32) {
-                const int64_t j = j0 + lane;
+            for (int j0 = 0; j0 < n; j0 += 32) {
+                const int jl = j0 + lane;
                 bool in = false;
-                if (j < hi && j != i) {
+                if (jl < n && jl != il) {
                     double dx, dy, dz;
-                    in = pair_dist(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz, cell) < d.rc;
+                    in = pair_dist(xi, yi, zi, sp[0][jl], sp[1][jl], sp[2][jl], dx, dy, dz, cell) < d.rc;
                 }
                 cnt += __popc(__ballot_sync(0xffffffffu, in));
             }
-            if (lane == 0) d.cnt[i] = cnt;
+            if (lane == 0) d.cnt[lo + il] = cnt;
         }
         __syncthreads();
         int run = 0;  // the sample's row offsets, atoms in index order
