@@ -519,6 +519,33 @@ StepResult train_step(Device& dev, std::span<const Sample> samples, std::span<co
     return StepResult{r.loss, r.grad_norm, r.local, r.n_atoms, r.n_edges};
 }
 
+// Pipelined form of train_step (lamm_train_step_submit / lamm_train_step_wait):
+// submit_step packs and enqueues the step and returns its ticket without waiting,
+// so the host can pack step k+1 while the device runs step k; wait_step returns
+// the oldest outstanding step's result. At most two in flight, waited in order;
+// the results and parameters equal the synchronous sequence.
+template <class Sample, class TrainConfig>
+int64_t submit_step(Device& dev, std::span<const Sample> samples, std::span<const uint8_t> denoise,
+                    const TrainConfig& tcfg, int64_t step, int workers = 1, int rank = 0) {
+    if (!denoise.empty() && denoise.size() != samples.size())
+        throw InputError("submit_step: one denoise flag per sample");
+    PackedBatch b;
+    for (size_t s = 0; s < samples.size(); ++s) b.add_sample(samples[s], !denoise.empty() && denoise[s] != 0);
+    const lamm_batch_view v = b.view();
+    const lamm_train_config c = train_config_to_c(tcfg);
+    int64_t ticket = -1;
+    check(lamm_train_step_submit(dev.get(), &v, &c, step, workers, rank, &ticket));  // packed: b may go
+    return ticket;
+}
+
+inline StepResult wait_step(Device& dev, int64_t ticket) {
+    lamm_step_result r{};
+    const int st = lamm_train_step_wait(dev.get(), ticket, &r);
+    dev.params_changed_on_device();
+    check(st);
+    return StepResult{r.loss, r.grad_norm, r.local, r.n_atoms, r.n_edges};
+}
+
 // The step of S/trainer.cpp:258-327 for all G workers SIMULATED on this one
 // device, in worker order: `samples` is the whole MiniBatch (G*B, worker-major),
 // denoise[k] marks samples of denoising subsets (empty: none).

@@ -275,6 +275,23 @@ void check_train_step(const std::vector<lamm::Sample>& samples, const lamm::mode
            fmt(std::abs(r.grad_norm - gnorm) / gnorm));
     report(rel(dev.grads(), g) <= kTol, "train_step gradient", fmt(rel(dev.grads(), g)));
     report(rel(dev.rms_state(), v) <= 3 * kTol, "train_step RMS state", fmt(rel(dev.rms_state(), v)));
+
+    // the pipelined form (submit_step / wait_step, two steps in flight) reproduces two
+    // synchronous steps bit for bit
+    const auto r2 = lamm_b200::train_step(dev, std::span<const lamm::Sample>(samples),
+                                          std::span<const uint8_t>(denoise), tcfg, step + 1, 1, 0);
+    lamm_b200::Device dev2(cfg, 0);
+    dev2.set_params_from(params0);
+    dev2.set_rms_state(std::vector<double>(g.size(), 0.0));
+    dev2.set_reference_table(table);
+    const int64_t t0 = lamm_b200::submit_step(dev2, std::span<const lamm::Sample>(samples),
+                                              std::span<const uint8_t>(denoise), tcfg, step, 1, 0);
+    const int64_t t1 = lamm_b200::submit_step(dev2, std::span<const lamm::Sample>(samples),
+                                              std::span<const uint8_t>(denoise), tcfg, step + 1, 1, 0);
+    const auto p0 = lamm_b200::wait_step(dev2, t0);
+    const auto p1 = lamm_b200::wait_step(dev2, t1);
+    report(p0.loss == r.loss && p1.loss == r2.loss && dev2.params() == dev.params(),
+           "submit_step/wait_step == two train_step calls", fmt(std::abs(p1.loss - r2.loss)));
 }
 
 void check_evaluate(const std::vector<lamm::Sample>& samples, const lamm::model::ModelConfig& cfg,
