@@ -553,7 +553,7 @@ struct Model {
         set_smem((const void*)k_edge_bwd<H, K, true>, smem_bwd());
         set_smem((const void*)k_edge_bwd<H, K, false>, smem_bwd());
         set_smem((const void*)k_emb_grad, sizeof(float) * kMaxZ * H);
-        c.grid_emb = c.nsm;
+        c.grid_emb = 4 * c.nsm;  // ~13 atoms per CTA at cfg2: the gh loads of a CTA in flight together
         // one tcgen05 CTA per SM, persistent over 128-atom tiles; a multiple of the
         // column split so a CTA keeps one column block (k_bwd_gemm's dW_u partials)
         c.grid_upd = c.nsm / NodeGemmCfg<H>::NS * NodeGemmCfg<H>::NS;
