@@ -1103,12 +1103,14 @@ __global__ void __launch_bounds__(256) k_grad_reduce(Dev d, SegTable tab) {
             } else {
                 base = sg.src + off;
             }
-            if (base) {  // 4 loads in flight per step, summed in stream order
+            if (base) {  // 8 loads in flight per step, summed in stream order
                 int c = c0;
-                for (; c + 3 * cs < ncta; c += 4 * cs) {
-                    const float v0 = __ldcg(base + c * stride), v1 = __ldcg(base + (c + cs) * stride);
-                    const float v2 = __ldcg(base + (c + 2 * cs) * stride), v3 = __ldcg(base + (c + 3 * cs) * stride);
-                    acc = (((acc + v0) + v1) + v2) + v3;
+                for (; c + 7 * cs < ncta; c += 8 * cs) {
+                    float v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = __ldcg(base + (c + u * cs) * stride);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc += v[u];
                 }
                 for (; c < ncta; c += cs) acc += __ldcg(base + c * stride);
             }
