@@ -260,7 +260,7 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     }
     for (int l = 0; l < L; ++l) ensure_buf(c, "mu" + std::to_string(l), 4 * static_cast<size_t>(Nc) * H, changed);
     ensure_buf(c, "F", 12 * Nc * D, changed);
-    ensure_buf(c, "Yf", 4 * static_cast<size_t>(Nc) * (3 * H + 3 + 3 * K), changed);
+    ensure_buf(c, "Yf", 4 * static_cast<size_t>(Nc) * ((3 * H + 3 + 3 * K + 3) / 4 * 4), changed);  // ForceBody::kYW
     ensure_buf(c, "Epred", 8 * Bc * D, changed);
     ensure_buf(c, "gE", 4 * Bc * D, changed);
     ensure_buf(c, "gF", 12 * Nc * D, changed);

@@ -469,7 +469,7 @@ struct ForceBody {
     static constexpr bool kBlockHook = false;
     static constexpr bool kPrepare = false;
     static constexpr int kUnroll = 1;  // block loop unroll (2: the r/rn register roles alternate)
-    static constexpr int kYW = 3 * H + 3 + 3 * K;  // per-atom feature floats
+    static constexpr int kYW = (3 * H + 3 + 3 * K + 3) / 4 * 4;  // per-atom feature floats (16-byte rows)
     struct Reg {
         float t;
     };
@@ -588,11 +588,11 @@ __global__ void __launch_bounds__(256) k_force_out(Dev d, int own_head) {
         const int row = L > 0 ? i : __ldg(d.Z + i) - 1;
         float ti[C], yv[3][C];
         const VecF<C> tv = ldv<C>(T + static_cast<int64_t>(row) * H + lane * C);
+        const VecF<C> y0 = ldv<C>(y + lane * C), y1 = ldv<C>(y + H + lane * C), y2 = ldv<C>(y + 2 * H + lane * C);
 #pragma unroll
         for (int cc = 0; cc < C; ++cc) {
-            const int aa = lane * C + cc;
             ti[cc] = tv.v[cc];
-            yv[0][cc] = y[aa], yv[1][cc] = y[H + aa], yv[2][cc] = y[2 * H + aa];
+            yv[0][cc] = y0.v[cc], yv[1][cc] = y1.v[cc], yv[2][cc] = y2.v[cc];
         }
         const float u[3] = {y[3 * H], y[3 * H + 1], y[3 * H + 2]};
         float vk[3] = {0.f, 0.f, 0.f};
