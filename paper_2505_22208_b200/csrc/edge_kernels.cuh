@@ -119,9 +119,9 @@ enum StageParts : int { kPartGeo = 1, kPartPlain = 2, kPartCanon = 4 };
 
 // One TMA stage: edges [cb, cb + n), n = min(kChunk, e1 - cb) rounded up to a
 // whole 8-edge block (the tail reads into the CSR padding).
-template <int K, int C>
+template <int K, int C, int kB = 8>
 __device__ __forceinline__ void stage_chunk(const Dev& d, EdgeStage<K, C>& s, uint64_t* b, int cb, int e1, int parts) {
-    const int n = min(C, ((e1 - cb) + 7) & ~7);
+    const int n = min(C, ((e1 - cb) + kB - 1) & ~(kB - 1));
     uint32_t bytes = 8u * n + 32u;
     if (parts & kPartGeo) bytes += 16u * n;
     if (parts & kPartPlain) bytes += 4u * K * n;
@@ -242,11 +242,13 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K, G, 
     // four groups' leaders sit on different SM sub-partitions (warp id % 4)
     const bool lead = c.lt == 32 * (c.g % (H / 32));
     const uint32_t quad = (threadIdx.x >> 5) & 3;
-    const int base = e0 & ~7;  // chunks start on 8-edge blocks
+    constexpr int kB = Body::kBlock;  // edges per block (8 or 16)
+    constexpr unsigned kFull = (1u << kB) - 1u;
+    const int base = e0 & ~(kB - 1);  // chunks start on whole blocks
     const int nchunks = (e1 - base + C - 1) / C;
     if (lead && e1 > e0) {
-        stage_chunk<K, C>(d, c.st[0], &c.bar[0], base, e1, parts);
-        if (nchunks > 1) stage_chunk<K, C>(d, c.st[1], &c.bar[1], base + C, e1, parts);
+        stage_chunk<K, C, kB>(d, c.st[0], &c.bar[0], base, e1, parts);
+        if (nchunks > 1) stage_chunk<K, C, kB>(d, c.st[1], &c.bar[1], base + C, e1, parts);
         if constexpr (kF) {
             mbar_wait(&c.bar[0], 0);
             filter_mma<K, C>(ft.tg, ft, c.st[0]);
@@ -260,16 +262,19 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K, G, 
         // gathers of the next block are issued before the current block is
         // consumed, across chunk boundaries (the next chunk's stage is waited for
         // at the start of the current chunk)
-        typename Body::Reg rn[8];
+        typename Body::Reg rn[kB];
         auto load_block = [&](const EdgeStage<K, C>& sst, int blk) {
-            const int4 j0 = reinterpret_cast<const int4*>(sst.col)[2 * blk];
-            const int4 j1 = reinterpret_cast<const int4*>(sst.col)[2 * blk + 1];
-            const int jj[8] = {j0.x, j0.y, j0.z, j0.w, j1.x, j1.y, j1.z, j1.w};
 #pragma unroll
-            for (int u = 0; u < 8; ++u) body.load(sst, blk * 8 + u, jj[u], rn[u]);
+            for (int q = 0; q < kB / 4; ++q) {
+                const int4 j4 = reinterpret_cast<const int4*>(sst.col)[(kB / 4) * blk + q];
+                body.load(sst, blk * kB + 4 * q, j4.x, rn[4 * q]);
+                body.load(sst, blk * kB + 4 * q + 1, j4.y, rn[4 * q + 1]);
+                body.load(sst, blk * kB + 4 * q + 2, j4.z, rn[4 * q + 2]);
+                body.load(sst, blk * kB + 4 * q + 3, j4.w, rn[4 * q + 3]);
+            }
         };
         mbar_wait(&c.bar[0], 0);
-        load_block(c.st[0], (e0 - base) >> 3);
+        load_block(c.st[0], (e0 - base) / kB);
         for (int k = 0; k < nchunks; ++k) {
             const int s = k & 1;
             const bool more = k + 1 < nchunks;
@@ -290,40 +295,41 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K, G, 
             const int cb = base + k * C;
             const int ea = max(cb, e0) - cb, eb = min(cb + C, e1) - cb;
             const uint32_t trow = ft.tg + s * C + (quad * 32u << 16);
-            const int blk0 = ea >> 3, blk1 = (eb + 7) >> 3;
+            const int blk0 = ea / kB, blk1 = (eb + kB - 1) / kB;
 #pragma unroll(Body::kUnroll)
             for (int blk = blk0; blk < blk1; ++blk) {
-                typename Body::Reg r[8];
+                typename Body::Reg r[kB];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) r[u] = rn[u];
+                for (int u = 0; u < kB; ++u) r[u] = rn[u];
                 if (blk + 1 < blk1) load_block(st, blk + 1);
                 else if (more) load_block(c.st[s ^ 1], 0);  // first block of the next chunk
-                const int ulo = max(ea - blk * 8, 0), uhi = min(eb - blk * 8, 8);
-                if constexpr (Body::kPrepare) body.prepare(st, blk * 8);
-                float f[8];
+                const int ulo = max(ea - blk * kB, 0), uhi = min(eb - blk * kB, kB);
+                if constexpr (Body::kPrepare) body.prepare(st, blk * kB);
+                float f[kB];
                 if constexpr (kF) {
-                    umma::ld8(trow + blk * 8, f);
+                    if constexpr (kB == 16) umma::ld16(trow + blk * kB, f);
+                    else umma::ld8(trow + blk * kB, f);
                 } else {
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) f[u] = 0.f;
+                    for (int u = 0; u < kB; ++u) f[u] = 0.f;
                 }
                 // destination segments of the block: one flush call site per
                 // block (keeps end()/begin() inlined once), branch-free edges
                 const unsigned vm = ((1u << uhi) - 1u) & ~((1u << ulo) - 1u);
-                const int bp = cb - (((cb >> 5) & ~3) << 5) + blk * 8;  // bit of the block's first edge
-                unsigned seg = (((st.segw[bp >> 5] >> (bp & 31)) & 0xFFu) | (1u << ulo)) & vm;
-                if (seg == 1u && vm == 0xFFu && st.dst[blk * 8] == cur) {
-                    // the common block: 8 edges, all of the current destination (no
+                const int bp = cb - (((cb >> 5) & ~3) << 5) + blk * kB;  // bit of the block's first edge
+                unsigned seg = (((st.segw[bp >> 5] >> (bp & 31)) & kFull) | (1u << ulo)) & vm;
+                if (seg == 1u && vm == kFull && st.dst[blk * kB] == cur) {
+                    // the common block: all edges of the current destination (no
                     // segment start inside): the unpredicated body
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) body.edge(st, blk * 8 + u, r[u], f[u], 1u);
+                    for (int u = 0; u < kB; ++u) body.edge(st, blk * kB + u, r[u], f[u], 1u);
                     seg = 0u;
                 }
                 while (seg) {
                     const int u0 = __ffs(seg) - 1;
                     seg &= seg - 1u;
                     const int u1 = seg ? __ffs(seg) - 1 : uhi;
-                    const int i = st.dst[blk * 8 + u0];
+                    const int i = st.dst[blk * kB + u0];
                     if (i != cur) {
                         do {
                             body.end(cur);
@@ -333,13 +339,13 @@ __device__ __forceinline__ void walk_edges(const Dev& d, const EdgeCta<H, K, G, 
                     }
                     const unsigned on = ((1u << u1) - 1u) & ~((1u << u0) - 1u);  // this segment's edges
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) body.edge(st, blk * 8 + u, r[u], f[u], (on >> u) & 1u);
+                    for (int u = 0; u < kB; ++u) body.edge(st, blk * kB + u, r[u], f[u], (on >> u) & 1u);
                 }
-                if constexpr (Body::kBlockHook) body.block(st, blk * 8, r, ulo, uhi);
+                if constexpr (Body::kBlockHook) body.block(st, blk * kB, r, ulo, uhi);
             }
             if constexpr (kF) umma::fence_before();
             group_sync(c.g, H);  // every thread is done with this stage (smem + TMEM)
-            if (lead && k + 2 < nchunks) stage_chunk<K, C>(d, c.st[s], &c.bar[s], base + (k + 2) * C, e1, parts);
+            if (lead && k + 2 < nchunks) stage_chunk<K, C, kB>(d, c.st[s], &c.bar[s], base + (k + 2) * C, e1, parts);
         }
     }
     body.end(cur);
@@ -412,6 +418,7 @@ struct MessageBody {
     static constexpr bool kBlockHook = false;
     static constexpr bool kPrepare = false;
     static constexpr int kUnroll = 2;  // block loop unroll (2: the r/rn register roles alternate)
+    static constexpr int kBlock = 16;  // edges per block of the walk
     struct Reg {
         float t;
     };
@@ -469,6 +476,7 @@ struct ForceBody {
     static constexpr bool kBlockHook = false;
     static constexpr bool kPrepare = false;
     static constexpr int kUnroll = 1;  // block loop unroll (2: the r/rn register roles alternate)
+    static constexpr int kBlock = 8;  // edges per block of the walk
     static constexpr int kYW = (3 * H + 3 + 3 * K + 3) / 4 * 4;  // per-atom feature floats (16-byte rows)
     struct Reg {
         float t;
@@ -670,6 +678,7 @@ struct HeadBody {
     static constexpr bool kBlockHook = false;
     static constexpr bool kPrepare = true;
     static constexpr int kUnroll = 1;  // block loop unroll (2: the r/rn register roles alternate)
+    static constexpr int kBlock = 8;  // edges per block of the walk
     struct Reg {
         float t;
     };
@@ -814,6 +823,7 @@ struct BwdBody {
     static constexpr bool kBlockHook = true;
     static constexpr bool kPrepare = false;
     static constexpr int kUnroll = 1;  // block loop unroll (2: the r/rn register roles alternate)
+    static constexpr int kBlock = 8;  // edges per block of the walk
     struct Reg {
         float gm, t;
     };
