@@ -417,7 +417,7 @@ struct MessageBody {
     static constexpr int kParts = TC ? 0 : kPartPlain;
     static constexpr bool kBlockHook = false;
     static constexpr bool kPrepare = false;
-    static constexpr int kUnroll = 2;  // block loop unroll (2: the r/rn register roles alternate)
+    static constexpr int kUnroll = 1;  // block loop unroll (2: the r/rn register roles alternate)
     static constexpr int kBlock = 16;  // edges per block of the walk
     struct Reg {
         float t;
