@@ -617,7 +617,7 @@ struct Model {
                    q == 0 ? 1 : 0);
         for (int l = c.L - 1; l >= 0; --l) {
             if constexpr (kFusedBwd) {
-                launch(c, "bwd_gemm", k_bwd_gemm<H>, c.grid_upd, 256, BwdGemmSmem<H>::bytes, d, l, act_map(c, d.gh));
+                launch(c, "bwd_gemm", k_bwd_gemm<H>, c.grid_upd, 512, BwdGemmSmem<H>::bytes, d, l, act_map(c, d.gh));
             } else {
                 launch(c, "bwd_gemm", k_node_gemm<H>, c.grid_upd, NodeGemmCfg<H>::NT, kGemmSmem, d, l, 1, act_map(c, d.gh),
                        act_map(c, d.gm), act_map(c, d.gm));

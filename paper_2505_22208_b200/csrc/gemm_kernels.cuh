@@ -323,9 +323,10 @@ struct BwdGemmSmem {
 };
 
 template <int H>
-__global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l, const __grid_constant__ CUtensorMap ghmap) {
+__global__ void __launch_bounds__(512, 1) k_bwd_gemm(Dev d, int l, const __grid_constant__ CUtensorMap ghmap) {
     using Cfg = NodeGemmCfg<H>;
-    constexpr int NS = Cfg::NS, NC = Cfg::NC, CW = NC / 2, Q = H / 4;
+    constexpr int NT = 512, NP4 = NT / 128;  // threads; column parts per TMEM lane quarter
+    constexpr int NS = Cfg::NS, NC = Cfg::NC, CW = NC / NP4, Q = H / 4;
     static_assert(H == 128 && CW % 16 == 0, "fused update backward: H = 128");
     constexpr int MA = NC / 32;  // MN atoms of the mu tile
     extern __shared__ __align__(1024) unsigned char bwd_gemm_smem[];
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l, const __grid_
     uint64_t* bar = reinterpret_cast<uint64_t*>(Bhi + BwdGemmSmem<H>::b_floats);  // weights, MMA1, MMA2, gh TMA
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 4);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int quad = warp & 3, half = warp >> 2;
+    const int quad = warp & 3, part = warp >> 2;
     if (warp == 0) umma::tmem_alloc(tslot, 512);
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -373,7 +374,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l, const __grid_
         const int base = (tile / NS) * kGemmM;
         const int row = quad * 32 + lane, atom = base + row;
         const bool live = atom < N;
-        const int c0 = np * NC + half * CW;
+        const int c0 = np * NC + part * CW;
         if (done > 0) {  // MMA2 of the previous tile read TMEM A and the mu tile in B
             mbar_wait(&bar[2], dphase);
             dphase ^= 1u;
@@ -397,10 +398,10 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l, const __grid_
         mbar_wait(&bar[3], gphase);
         gphase ^= 1u;
         {  // MMA1's lo operand: x - trunc_tf32(x) at the same swizzled positions
-            constexpr int IT = kGemmM * Q / 256;
+            constexpr int IT = kGemmM * Q / NT;
 #pragma unroll
             for (int it = 0; it < IT; ++it) {
-                const int c = tid + 256 * it;
+                const int c = tid + NT * it;
                 const float4 x = *reinterpret_cast<const float4*>(Ahi + 4 * c);
                 *reinterpret_cast<float4*>(Alo + 4 * c) =
                     make_float4(umma::tf32_trunc_lo(x.x), umma::tf32_trunc_lo(x.y), umma::tf32_trunc_lo(x.z),
@@ -408,14 +409,14 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l, const __grid_
             }
         }
         // gh^T into TMEM from the staged tile: lane = channel b = row, columns = atoms
-        // [half*64, half*64+64); element (atom m, channel b) of the SW128 tile sits in
+        // [part*32, part*32+32); element (atom m, channel b) of the SW128 tile sits in
         // K block b/32, row m, 16-byte chunk ((b%32)/4) ^ (m%8) (a warp reads one 128 B row)
         {
             const float* blk = Ahi + (row >> 5) * kGemmM * 32;
             const int j = (row & 31) >> 2, w = row & 3;
 #pragma unroll
-            for (int cc = 0; cc < kGemmM / 2; cc += 16) {
-                const int a0 = half * (kGemmM / 2) + cc;
+            for (int cc = 0; cc < kGemmM / NP4; cc += 16) {
+                const int a0 = part * (kGemmM / NP4) + cc;
                 float hv[16], lv[16];
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
@@ -444,12 +445,12 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l, const __grid_
         wphase ^= 1u;
         // the mu tile for MMA2's B (N = this CTA's NC columns, K = atoms), MN-major
         // 128B_BASE32B, written chunk by chunk in storage order once MMA1 is done
-        constexpr int MIT = kGemmM * NC / 4 / 256;
+        constexpr int MIT = kGemmM * NC / 4 / NT;
         float4 vm[MIT];
         int mo[MIT];
 #pragma unroll
         for (int it = 0; it < MIT; ++it) {
-            const int c = tid + 256 * it;  // 16-byte chunk c of the tile in storage order
+            const int c = tid + NT * it;  // 16-byte chunk c of the tile in storage order
             const int mna = (c >> 5) % MA, kg = (c >> 5) / MA, kr = (c >> 3) & 3, x = (c >> 1) & 3, hl = c & 1;
             const int mn = mna * 32 + ((x ^ kr) << 3) + (hl << 2), k = kg * 4 + kr;  // column, atom
             vm[it] = base + k < N ? __ldg(reinterpret_cast<const float4*>(mu + static_cast<int64_t>(base + k) * H +
@@ -493,7 +494,7 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l, const __grid_
 #pragma unroll
         for (int cc = 0; cc < CW; cc += 16) {
             float v[16];
-            umma::ld16(tD1 + lane_off + half * CW + cc, v);
+            umma::ld16(tD1 + lane_off + part * CW + cc, v);
             if (!live) continue;
             float* go = d.gm + static_cast<int64_t>(atom) * H + c0 + cc;
 #pragma unroll
@@ -513,15 +514,15 @@ __global__ void __launch_bounds__(256, 1) k_bwd_gemm(Dev d, int l, const __grid_
         umma::fence_after();
     }
     const int row = quad * 32 + lane;
-    float* part = d.part_wu[l] + static_cast<int64_t>(blockIdx.x) * H * NC;
+    float* pout = d.part_wu[l] + static_cast<int64_t>(blockIdx.x) * H * NC;
     if (done > 0)  // CTAs without a tile write nothing (k_grad_reduce reads CTAs < ntiles only)
 #pragma unroll
         for (int cc = 0; cc < CW; cc += 16) {
             float v[16];
-            umma::ld16(tD2 + lane_off + half * CW + cc, v);
+            umma::ld16(tD2 + lane_off + part * CW + cc, v);
 #pragma unroll
             for (int k = 0; k < 16; k += 4)
-                *reinterpret_cast<float4*>(part + row * NC + half * CW + cc + k) =
+                *reinterpret_cast<float4*>(pout + row * NC + part * CW + cc + k) =
                     make_float4(v[k], v[k + 1], v[k + 2], v[k + 3]);
         }
     umma::fence_before();
