@@ -206,16 +206,12 @@ __device__ __forceinline__ int cell_walk_slot(const CellWalk& w, int t) {
 // atom's cell, a counting sort of the atoms by cell into cpos, and the cell
 // offsets. lptr holds the atom's rank inside its cell until k_cell_count
 // overwrites it with the row offset.
-__device__ void bin_sample(const Dev& d, int s, int64_t lo, int64_t hi, const double* cell) {
+// mn / mx: this thread's bounding box of the atoms it positioned (k_prep's loop).
+__device__ void bin_sample(const Dev& d, int s, int64_t lo, int64_t hi, const double* cell, double (&mn)[3],
+                           double (&mx)[3]) {
     __shared__ double red[4][6];
     __shared__ CellGrid sg;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int64_t a = lo + tid; a < hi; a += blockDim.x) {
-        const double p[3] = {d.x[a], d.y[a], d.z[a]};
-#pragma unroll
-        for (int k = 0; k < 3; ++k) mn[k] = fmin(mn[k], p[k]), mx[k] = fmax(mx[k], p[k]);
-    }
 #pragma unroll
     for (int k = 0; k < 3; ++k)
 #pragma unroll
@@ -436,6 +432,7 @@ __global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) 
         // the Eq. (5) weight of the atom's force term (S/loss.cpp:186-212): lambda_F / (sum m_F * n)
         const int mfs = hd.mf;
         const double fwa = fm[s] && mfs > 0 ? hd.lambda_f / (static_cast<double>(mfs) * static_cast<double>(hi - lo)) : 0.0;
+        double bmn[3] = {INFINITY, INFINITY, INFINITY}, bmx[3] = {-INFINITY, -INFINITY, -INFINITY};  // bounding box
         // 4 atoms per thread and round, every load issued before the first store
         // (large samples are latency-bound here: one block walks all their atoms)
         for (int64_t a0 = lo + threadIdx.x; a0 < hi; a0 += 4 * blockDim.x) {
@@ -474,6 +471,8 @@ __global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) 
                     d.Fn[3 * a + c] = d.use_table ? __dmul_rn(fs, lab) : lab;
                 }
                 d.x[a] = xyz[0], d.y[a] = xyz[1], d.z[a] = xyz[2];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) bmn[k] = fmin(bmn[k], xyz[k]), bmx[k] = fmax(bmx[k], xyz[k]);
                 if (hi - lo <= kSmallAtoms)  // the pair counts below read them from shared memory
                     sp[0][a - lo] = xyz[0], sp[1][a - lo] = xyz[1], sp[2][a - lo] = xyz[2];
             }
@@ -481,7 +480,7 @@ __global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) 
         __syncthreads();
         const double* cell = sample_cell(d, s);
         if (hi - lo > kSmallAtoms) {  // counted over its cell list by k_cell_count
-            bin_sample(d, s, lo, hi, cell);
+            bin_sample(d, s, lo, hi, cell, bmn, bmx);
             __syncthreads();
             continue;
         }
