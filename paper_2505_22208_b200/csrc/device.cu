@@ -247,6 +247,7 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     ensure_buf(c, "cstart", 4 * (4 * Nc + 65 * Bc + 1), changed);
     ensure_buf(c, "cpos", 32 * Nc, changed);
     ensure_buf(c, "sdone", 4 * Bc, changed);
+    ensure_buf(c, "cmask", 4 * kMaskWords * Nc, changed);
     ensure_buf(c, "eatom", 8 * Nc, changed);
     ensure_buf(c, "fterm", 8 * Nc, changed);
     ensure_buf(c, "fw", 8 * Nc, changed);
@@ -352,6 +353,7 @@ Dev make_dev(Ctx& c) {
     d.cstart = buf(c, "cstart").as<int32_t>();
     d.cpos = buf(c, "cpos").as<double4>();
     d.sdone = buf(c, "sdone").as<uint32_t>();
+    d.cmask = buf(c, "cmask").as<uint32_t>();
     d.eatom = buf(c, "eatom").as<double>();
     d.fterm = buf(c, "fterm").as<double>();
     d.fw = buf(c, "fw").as<double>();

@@ -36,6 +36,10 @@ constexpr int kMaxZ = 118;
 // counts, k_nbr_fill walks the 27 neighbour cells); smaller ones are swept
 // brute force by the sample's own block.
 constexpr int kSmallAtoms = 128;
+// Cell-list samples up to this size keep each row's hit bitmask (kMaskAtoms / 32
+// words) between k_cell_count and k_nbr_fill.
+constexpr int kMaskAtoms = 2048;
+constexpr int kMaskWords = kMaskAtoms / 32;
 
 // Uniform grid over one sample: non-periodic — the bounding box cut into cells of
 // width >= rc (1 + 1e-9); periodic — n[k] slabs of fractional coordinate k, each
@@ -103,6 +107,7 @@ struct Dev {
     int32_t* cstart;           // [4 N + 65 B + 1] per-sample cell offsets (region 4 lo + 65 s)
     double4* cpos;             // [N]  the sample's atoms ordered by cell: x, y, z, j (bits)
     uint32_t* sdone;           // [B]  atoms of the sample counted (k_cell_count)
+    uint32_t* cmask;           // [N][kMaskWords] hit bitmask of a row of a sample <= kMaskAtoms
     float4* geo;
     float* rbf;                // [P][K] fcut * Gaussians, canonical tcgen05 layout, tf32 hi part
     float* rbfl;               //        ... and the fp32 lo remainder

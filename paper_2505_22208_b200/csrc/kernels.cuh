@@ -531,6 +531,7 @@ __global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) 
 // neighbour cells. The warp that counts a sample's last atom scans the sample's
 // row offsets; the one that finishes the last such sample runs finalize_csr_warp.
 __global__ void __launch_bounds__(256) k_cell_count(Dev d, int Q) {
+    __shared__ uint32_t wbits[8][kMaskWords];
     pdl_enter();
     const StepHeader& hd = *d.hdr;
     const int n_large = hd.n_large;
@@ -546,17 +547,32 @@ __global__ void __launch_bounds__(256) k_cell_count(Dev d, int Q) {
         const double* cell = sample_cell(d, s);
         const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
         int cnt = 0;
+        // samples of <= 1024 atoms (one window of k_nbr_fill): the hits as a bitmask over
+        // the sample's atoms, kept for the fill (no second pass of pair tests)
+        const bool keep = hi - lo <= kMaskAtoms;
+        uint32_t* bits = wbits[threadIdx.x >> 5];
+#pragma unroll
+        for (int q = 0; q < kMaskWords / 32; ++q) bits[32 * q + lane] = 0u;
+        __syncwarp();
         const CellWalk w = cell_walk_setup(d, g, d.acell[i]);
         for (int t0 = 0; t0 < w.total; t0 += 32) {
             const int k = cell_walk_slot(w, t0 + lane);
             bool in = false;
+            int j = 0;
             if (t0 + lane < w.total) {
                 const double4 p = d.cpos[lo + k];
                 double dx, dy, dz;
-                in = __double_as_longlong(p.w) != i && pair_dist(xi, yi, zi, p.x, p.y, p.z, dx, dy, dz, cell) < d.rc;
+                j = static_cast<int>(__double_as_longlong(p.w));
+                in = j != i && pair_dist(xi, yi, zi, p.x, p.y, p.z, dx, dy, dz, cell) < d.rc;
             }
+            if (keep && in) atomicOr(bits + ((j - lo) >> 5), 1u << ((j - lo) & 31));
             cnt += __popc(__ballot_sync(0xffffffffu, in));
         }
+        __syncwarp();
+        if (keep)
+#pragma unroll
+            for (int q = 0; q < kMaskWords / 32; ++q)
+                d.cmask[static_cast<int64_t>(i) * kMaskWords + 32 * q + lane] = bits[32 * q + lane];
         unsigned last = 0;
         if (lane == 0) {
             d.cnt[i] = cnt;
@@ -687,13 +703,14 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d, int Q) {
             continue;
         }
         const CellGrid g = d.cgrid[s];
-        const CellWalk cw = cell_walk_setup(d, g, d.acell[i]);
+        const bool kept = hi - lo <= kMaskAtoms;  // k_cell_count left the row's bitmask
+        const CellWalk cw = kept ? CellWalk{} : cell_walk_setup(d, g, d.acell[i]);
         uint32_t* bits = wbits[wib];
         int* list = wlist[wib];
         for (int w0 = lo; w0 < hi; w0 += kWin) {
-            bits[lane] = 0u;
+            bits[lane] = kept ? __ldcg(d.cmask + static_cast<int64_t>(i) * kMaskWords + (w0 - lo) / 32 + lane) : 0u;
             __syncwarp();
-            for (int t0 = 0; t0 < cw.total; t0 += 32) {
+            for (int t0 = 0; !kept && t0 < cw.total; t0 += 32) {
                 const int k = cell_walk_slot(cw, t0 + lane);
                 if (t0 + lane < cw.total) {
                     const double4 p = d.cpos[lo + k];
