@@ -238,6 +238,7 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     ensure_buf(c, "dst", 4 * Pp, changed);
     ensure_buf(c, "segw", 4 * (Pp / 32 + 32), changed);
     ensure_buf(c, "geo", 16 * Pp, changed);
+    ensure_buf(c, "sij", 8 * Pp, changed);
     ensure_buf(c, "rbf", 4 * static_cast<size_t>(Pp) * K, changed);
     ensure_buf(c, "rbfl", 4 * static_cast<size_t>(Pp) * K, changed);
     ensure_buf(c, "rbfp", 4 * static_cast<size_t>(Pp) * K, changed);
@@ -358,6 +359,7 @@ Dev make_dev(Ctx& c) {
     d.fterm = buf(c, "fterm").as<double>();
     d.fw = buf(c, "fw").as<double>();
     d.geo = buf(c, "geo").as<float4>();
+    d.sij = buf(c, "sij").as<float2>();
     d.rbf = buf(c, "rbf").as<float>();
     d.rbfl = buf(c, "rbfl").as<float>();
     d.rbfp = buf(c, "rbfp").as<float>();
@@ -551,7 +553,8 @@ struct Model {
             throw InputErr("model: too many heads for the device path at this hidden size");
         // embedding-gradient slots (distinct Z per device-batch) that fit next to the staging
         set_smem((const void*)k_edge_force<H, K>, smem_force(c.D));
-        set_smem((const void*)k_edge_head<H, K>, smem_head(c.D));
+        set_smem((const void*)k_edge_head<H, K, false>, smem_head(c.D));
+        set_smem((const void*)k_edge_head<H, K, true>, smem_head(c.D));
         set_smem((const void*)k_edge_bwd<H, K, true>, smem_bwd());
         set_smem((const void*)k_edge_bwd<H, K, false>, smem_bwd());
         set_smem((const void*)k_emb_grad, sizeof(float) * kMaxZ * H);
@@ -567,7 +570,7 @@ struct Model {
         occ_e = std::min(occ_e, o);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_force<H, K>, kForceGroups * H, smem_force(c.D)));
         occ_e = std::min(occ_e, o);
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_head<H, K>, kGroups * H, smem_head(c.D)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_head<H, K, false>, kGroups * H, smem_head(c.D)));
         occ_e = std::min(occ_e, o);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_edge_bwd<H, K, false>, kGroups * H, smem_bwd()));
         occ_e = std::min(occ_e, o);
@@ -615,7 +618,8 @@ struct Model {
         const Dev d = make_dev(c);
         const int passes = general ? c.D : 1;
         for (int q = 0; q < passes; ++q)
-            launch(c, "head_bwd", k_edge_head<H, K>, c.grid_edge, kGroups * H, smem_head(c.D), d, general ? q : -1,
+            launch(c, "head_bwd", general ? k_edge_head<H, K, false> : k_edge_head<H, K, true>, c.grid_edge,
+                   kGroups * H, smem_head(c.D), d, general ? q : -1,
                    q == 0 ? 1 : 0);
         for (int l = c.L - 1; l >= 0; --l) {
             if constexpr (kFusedBwd) {

@@ -109,6 +109,7 @@ struct Dev {
     uint32_t* sdone;           // [B]  atoms of the sample counted (k_cell_count)
     uint32_t* cmask;           // [N][kMaskWords] hit bitmask of a row of a sample <= kMaskAtoms
     float4* geo;
+    float2* sij;               // [P] train step: fcut (gF_i - gF_j).u_ij and gF_i.u_ij (k_loss, for k_edge_head)
     float* rbf;                // [P][K] fcut * Gaussians, canonical tcgen05 layout, tf32 hi part
     float* rbfl;               //        ... and the fp32 lo remainder
     float* rbfp;               // [P][K] fcut * Gaussians, edge-major (FFMA consumers)

@@ -62,6 +62,7 @@ struct EdgeStage {
     float fcp[C * K];  // fcut*rbf, edge-major
     float fch[C * K];  // fcut*rbf, canonical tf32 hi (tensor-core filter)
     float fcl[C * K];  // fcut*rbf, canonical lo
+    float2 sij[C];     // train-step head backward: s_ij and gF_i.u_ij (k_loss)
 };
 
 // --------------------------------------------------------------- PTX glue --
@@ -115,7 +116,7 @@ __device__ __forceinline__ void group_sync(int g, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(nthreads) : "memory");
 }
 
-enum StageParts : int { kPartGeo = 1, kPartPlain = 2, kPartCanon = 4 };
+enum StageParts : int { kPartGeo = 1, kPartPlain = 2, kPartCanon = 4, kPartSij = 8 };
 
 // One TMA stage: edges [cb, cb + n), n = min(kChunk, e1 - cb) rounded up to a
 // whole 8-edge block (the tail reads into the CSR padding).
@@ -126,6 +127,7 @@ __device__ __forceinline__ void stage_chunk(const Dev& d, EdgeStage<K, C>& s, ui
     if (parts & kPartGeo) bytes += 16u * n;
     if (parts & kPartPlain) bytes += 4u * K * n;
     if (parts & kPartCanon) bytes += 8u * K * n;
+    if (parts & kPartSij) bytes += 8u * n;
     mbar_expect_tx(b, bytes);
     bulk_g2s(s.col, d.col + cb, 4 * n, b);
     bulk_g2s(s.dst, d.dst + cb, 4 * n, b);
@@ -136,6 +138,7 @@ __device__ __forceinline__ void stage_chunk(const Dev& d, EdgeStage<K, C>& s, ui
         bulk_g2s(s.fch, d.rbf + static_cast<int64_t>(cb) * K, 4 * K * n, b);
         bulk_g2s(s.fcl, d.rbfl + static_cast<int64_t>(cb) * K, 4 * K * n, b);
     }
+    if (parts & kPartSij) bulk_g2s(s.sij, d.sij + cb, 8u * n, b);
 }
 
 // Shared-memory layout common to the edge kernels: per group kStages staged
@@ -671,12 +674,13 @@ __global__ void __launch_bounds__(256) k_force_out(Dev d, int own_head) {
 //   gh_i = We gE_s + gT_i (.) (1 - T_i^2)
 //   dWa[:,ch] += S_i T_i, dWb[:,ch] += T_i (.) W_i / 2, dWc[k,ch] += sum_j (gF_i.u_ij) fcut rbf_ijk,
 //   dWe[:,d] += h^L_i gE_s[d]      (per-CTA partials, thread-owned columns)
-template <int H, int K>
+template <int H, int K, bool kTrain>
 struct HeadBody {
     static constexpr bool kFilter = false;
-    static constexpr int kParts = kPartGeo | kPartPlain;
+    // train step: s_ij and gF_i.u_ij per edge come staged (k_loss computed them)
+    static constexpr int kParts = kTrain ? (kPartPlain | kPartSij) : (kPartGeo | kPartPlain);
     static constexpr bool kBlockHook = false;
-    static constexpr bool kPrepare = true;
+    static constexpr bool kPrepare = !kTrain;
     static constexpr int kUnroll = 1;  // block loop unroll (2: the r/rn register roles alternate)
     static constexpr int kBlock = 8;  // edges per block of the walk
     struct Reg {
@@ -723,10 +727,17 @@ struct HeadBody {
         }
     }
     __device__ void edge(const EdgeStage<K>& st, int e, const Reg& r, float, unsigned on) {
-        const float sij = on ? es[e & 7] : 0.f;
+        float sv, dv;
+        if constexpr (kTrain) {
+            const float2 q = st.sij[e];
+            sv = q.x, dv = q.y;
+        } else {
+            sv = es[e & 7], dv = ed[e & 7];
+        }
+        const float sij = on ? sv : 0.f;
         S += sij;
         W = fmaf(sij, r.t, W);
-        if (kv) R = fmaf(on ? ed[e & 7] : 0.f, st.fcp[e * K + k], R);
+        if (kv) R = fmaf(on ? dv : 0.f, st.fcp[e * K + k], R);
     }
     // per-atom operands are loaded when the atom begins and used at its end, so
     // their latency hides behind the atom's edges
@@ -774,7 +785,7 @@ struct HeadBody {
     }
 };
 
-template <int H, int K>
+template <int H, int K, bool kTrain>
 __global__ void __launch_bounds__(kGroups* H, 1) k_edge_head(Dev d, int pass_ch, int first) {
     EdgeCta<H, K> c = edge_prologue<H, K>(d);
     const int D = d.D;
@@ -784,7 +795,7 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_head(Dev d, int pass_ch,
     for (int e = c.lt; e < AW; e += H) acc[e] = 0.f;
     __syncthreads();
     const int kw = c.g % (H / 32);
-    HeadBody<H, K> b{d, d.t[d.L], d.h[d.L], acc, c.lt, D, d.L, pass_ch,
+    HeadBody<H, K, kTrain> b{d, d.t[d.L], d.h[d.L], acc, c.lt, D, d.L, pass_ch,
                      first, d.hdr->N, (c.lt >> 5) == kw && (c.lt & 31) < K, c.lt & 31};
     walk_edges<H, K>(d, c, b, FilterTc{});
     __syncthreads();

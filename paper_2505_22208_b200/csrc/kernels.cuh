@@ -844,6 +844,17 @@ __global__ void __launch_bounds__(128) k_energy(Dev d) {
 // as an fp32 hi/lo pair, into the allreduce payload after the gradients.
 __global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy, int full_gF) {
     pdl_enter();
+    if (with_energy == 2 && !d.hdr->overflow) {  // train step: the head backward's per-edge scalars
+        const int P = d.hdr->P;                     // (S/model.cpp:318-340); on overflow P > capacity
+        for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+            const int i = d.dst[p], j = d.col[p];
+            const float4 gv = d.geo[p];
+            const float4 gi = d.gFc[i], gj = d.gFc[j];
+            const float di = gi.x * gv.x + gi.y * gv.y + gi.z * gv.z;
+            const float dj = gj.x * gv.x + gj.y * gv.y + gj.z * gv.z;
+            d.sij[p] = make_float2(gv.w * (di - dj), di);
+        }
+    }
     double* ered = dyn_smem<double>();  // [D][128] when with_energy
     __shared__ double red[128], red2[128];
     __shared__ bool last;
