@@ -236,6 +236,7 @@ void ensure_capacity(Ctx& c, int64_t N, int64_t B, int64_t P) {
     const int64_t Pp = ((Pc + kChunk + 16 + 7) / 8) * 8;  // CSR padding for the chunk staging
     ensure_buf(c, "col", 4 * Pp, changed);
     ensure_buf(c, "dst", 4 * Pp, changed);
+    ensure_buf(c, "colz", 4 * Pp, changed);
     ensure_buf(c, "segw", 4 * (Pp / 32 + 32), changed);
     ensure_buf(c, "geo", 16 * Pp, changed);
     ensure_buf(c, "sij", 8 * Pp, changed);
@@ -348,6 +349,7 @@ Dev make_dev(Ctx& c) {
     d.segw = buf(c, "segw").as<uint32_t>();
     d.col = buf(c, "col").as<int32_t>();
     d.dst = buf(c, "dst").as<int32_t>();
+    d.colz = buf(c, "colz").as<int32_t>();
     d.part_lo = buf(c, "part_lo").as<int32_t>();
     d.cgrid = buf(c, "cgrid").as<CellGrid>();
     d.acell = buf(c, "acell").as<int32_t>();

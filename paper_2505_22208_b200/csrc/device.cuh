@@ -98,6 +98,7 @@ struct Dev {
     const uint8_t* thas;
     // edges
     int32_t *cnt, *row_ptr, *col, *dst;
+    int32_t* colz;             // [P] Z_j - 1 of each edge's source (layer-0 message rows)
     int32_t *lptr, *stot, *soff;  // per-atom row offset inside its sample, per-sample edge totals / offsets
     uint32_t* segw;            // bit p set: edge p is the first of its destination atom
     int32_t* part_lo;          // [Q+1] edge-balanced atom partitions (edge kernels)

@@ -116,7 +116,7 @@ __device__ __forceinline__ void group_sync(int g, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(nthreads) : "memory");
 }
 
-enum StageParts : int { kPartGeo = 1, kPartPlain = 2, kPartCanon = 4, kPartSij = 8 };
+enum StageParts : int { kPartGeo = 1, kPartPlain = 2, kPartCanon = 4, kPartSij = 8, kPartColZ = 16 };
 
 // One TMA stage: edges [cb, cb + n), n = min(kChunk, e1 - cb) rounded up to a
 // whole 8-edge block (the tail reads into the CSR padding).
@@ -129,7 +129,7 @@ __device__ __forceinline__ void stage_chunk(const Dev& d, EdgeStage<K, C>& s, ui
     if (parts & kPartCanon) bytes += 8u * K * n;
     if (parts & kPartSij) bytes += 8u * n;
     mbar_expect_tx(b, bytes);
-    bulk_g2s(s.col, d.col + cb, 4 * n, b);
+    bulk_g2s(s.col, ((parts & kPartColZ) ? d.colz : d.col) + cb, 4 * n, b);  // kPartColZ: source rows Z_j - 1
     bulk_g2s(s.dst, d.dst + cb, 4 * n, b);
     bulk_g2s(s.segw, d.segw + ((cb >> 5) & ~3), 32, b);
     if (parts & kPartGeo) bulk_g2s(s.geo, d.geo + cb, 16 * n, b);
@@ -417,7 +417,8 @@ struct EdgeKernelSmem {
 template <int H, int K, bool TC, bool kZ, int C = kChunk>
 struct MessageBody {
     static constexpr bool kFilter = TC;
-    static constexpr int kParts = TC ? 0 : kPartPlain;
+    // layer 0 stages Z_j - 1 (k_nbr_fill) in place of j: no dependent Z load per edge
+    static constexpr int kParts = (TC ? 0 : kPartPlain) | (kZ ? kPartColZ : 0);
     static constexpr bool kBlockHook = false;
     static constexpr bool kPrepare = false;
     static constexpr int kUnroll = 1;  // block loop unroll (2: the r/rn register roles alternate)
@@ -432,8 +433,7 @@ struct MessageBody {
     float w[K];
     float m;
     __device__ void load(const EdgeStage<K, C>&, int, int j, Reg& r) const {
-        const int row = kZ ? __ldg(d.Z + j) - 1 : j;
-        r.t = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
+        r.t = __ldg(tsrc + static_cast<int64_t>(j) * H + a);  // j = Z_j - 1 at layer 0 (kPartColZ)
     }
     __device__ void edge(const EdgeStage<K, C>& s, int e, const Reg& r, float f, unsigned on) {
         if constexpr (!TC) f = filter_ffma<K>(w, s, e);

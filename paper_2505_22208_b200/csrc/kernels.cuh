@@ -336,7 +336,7 @@ __device__ void finalize_csr_warp(const Dev& d, int Q) {
         for (int q = lane; q < Q; q += 32) d.part_lo[q] = 0;
     if (lane == 0) d.part_lo[Q] = over ? 0 : N;
     if (!over)  // CSR padding read by the edge kernels' block staging: valid source atom 0
-        for (int x = lane; x < kChunk + 8; x += 32) d.col[run + x] = 0, d.dst[run + x] = N;
+        for (int x = lane; x < kChunk + 8; x += 32) d.col[run + x] = 0, d.colz[run + x] = 0, d.dst[run + x] = N;
 }
 
 
@@ -602,6 +602,7 @@ template <int K>
 __device__ __forceinline__ void emit_pair(const Dev& d, int p, int i, int j, double r, double dx, double dy, double dz,
                                           float wf, float invf, float rc_inv) {
     d.col[p] = j;
+    d.colz[p] = d.Z[j] - 1;
     d.dst[p] = i;
     const double sc = __ddiv_rn(1.0, r);
     const double ux = __dmul_rn(sc, dx), uy = __dmul_rn(sc, dy), uz = __dmul_rn(sc, dz);
