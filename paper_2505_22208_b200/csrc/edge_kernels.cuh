@@ -63,6 +63,7 @@ struct EdgeStage {
     float fch[C * K];  // fcut*rbf, canonical tf32 hi (tensor-core filter)
     float fcl[C * K];  // fcut*rbf, canonical lo
     float2 sij[C];     // train-step head backward: s_ij and gF_i.u_ij (k_loss)
+    int32_t colz[C];   // Z_j - 1 (layer-0 layer backward)
 };
 
 // --------------------------------------------------------------- PTX glue --
@@ -116,7 +117,7 @@ __device__ __forceinline__ void group_sync(int g, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(nthreads) : "memory");
 }
 
-enum StageParts : int { kPartGeo = 1, kPartPlain = 2, kPartCanon = 4, kPartSij = 8, kPartColZ = 16 };
+enum StageParts : int { kPartGeo = 1, kPartPlain = 2, kPartCanon = 4, kPartSij = 8, kPartColZ = 16, kPartZRow = 32 };
 
 // One TMA stage: edges [cb, cb + n), n = min(kChunk, e1 - cb) rounded up to a
 // whole 8-edge block (the tail reads into the CSR padding).
@@ -128,6 +129,7 @@ __device__ __forceinline__ void stage_chunk(const Dev& d, EdgeStage<K, C>& s, ui
     if (parts & kPartPlain) bytes += 4u * K * n;
     if (parts & kPartCanon) bytes += 8u * K * n;
     if (parts & kPartSij) bytes += 8u * n;
+    if (parts & kPartZRow) bytes += 4u * n;
     mbar_expect_tx(b, bytes);
     bulk_g2s(s.col, ((parts & kPartColZ) ? d.colz : d.col) + cb, 4 * n, b);  // kPartColZ: source rows Z_j - 1
     bulk_g2s(s.dst, d.dst + cb, 4 * n, b);
@@ -139,6 +141,7 @@ __device__ __forceinline__ void stage_chunk(const Dev& d, EdgeStage<K, C>& s, ui
         bulk_g2s(s.fcl, d.rbfl + static_cast<int64_t>(cb) * K, 4 * K * n, b);
     }
     if (parts & kPartSij) bulk_g2s(s.sij, d.sij + cb, 8u * n, b);
+    if (parts & kPartZRow) bulk_g2s(s.colz, d.colz + cb, 4u * n, b);
 }
 
 // Shared-memory layout common to the edge kernels: per group kStages staged
@@ -830,7 +833,7 @@ __global__ void __launch_bounds__(kGroups* H, 1) k_edge_head(Dev d, int pass_ch,
 template <int H, int K, bool TC, bool kZ>
 struct BwdBody {
     static constexpr bool kFilter = TC;
-    static constexpr int kParts = kPartPlain;
+    static constexpr int kParts = kPartPlain | (kZ ? kPartZRow : 0);  // layer 0: Z_j - 1 staged
     static constexpr bool kBlockHook = true;
     static constexpr bool kPrepare = false;
     static constexpr int kUnroll = 1;  // block loop unroll (2: the r/rn register roles alternate)
@@ -845,9 +848,9 @@ struct BwdBody {
     uint64_t dw2[K / 2];  // dW_f accumulators as packed fp32 pairs (k, k+1)
     float gmi, gt;
     float gi[8];  // gm of the destination of each edge of the block (0: masked)
-    __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
+    __device__ void load(const EdgeStage<K>& st, int e, int j, Reg& r) const {
         r.gm = __ldg(d.gm + static_cast<int64_t>(j) * H + a);
-        const int row = kZ ? __ldg(d.Z + j) - 1 : j;
+        const int row = kZ ? st.colz[e] : j;
         r.t = __ldg(tsrc + static_cast<int64_t>(row) * H + a);
     }
     __device__ void edge(const EdgeStage<K>& s, int e, const Reg& r, float f, unsigned on) {
