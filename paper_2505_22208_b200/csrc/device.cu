@@ -605,7 +605,7 @@ struct Model {
                    act_map(c, d.h[l + 1]), act_map(c, d.t[l + 1]));
         }
         launch(c, "force", k_edge_force<H, K>, c.grid_edge, kForceGroups * H, smem_force(c.D), d);
-        launch(c, "force_out", k_force_out<H, K>, c.grid_warp, 256, 0, d, energy ? 0 : 1);
+        launch(c, "force_out", k_force_out<H, K>, 2 * c.nsm, 256, 0, d, energy ? 0 : 1);  // fewer CTAs: each stages the head weights
         if (energy) launch(c, "energy", k_energy, c.grid_small, 128, sizeof(double) * 128 * c.D, d);
     }
 
