@@ -374,12 +374,17 @@ def test_evaluate_matches_reference(pk, oracle_ref):
         assert abs(got[k] - want[k]) <= TOL * abs(want[k]), (k, got[k], want[k])
 
 
-def test_train_step_large_structures(pk, oracle_ref):
+@pytest.mark.parametrize("denoise", [False, True])
+def test_train_step_large_structures(pk, oracle_ref, denoise):
     """cfg4-like: two 500-700 atom clusters (dense lists, ~30+ edges per atom,
-    partitions cutting through one atom's row run) through the full step."""
+    partitions cutting through one atom's row run) through the full step; with
+    denoise, the second cluster is a coordinate-denoising sample (its centered
+    noise mean staged through shared memory, cell lists over the noisy positions)."""
     mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
     batch = cases.synth(pk, 2, 77, mode=600, sigma=0.1, min_atoms=500, max_atoms=700, elements=cases.ORGANIC)
     batch = cases.with_heads(batch, cases.CFG[4], seed=3)
+    if denoise:
+        batch["denoise"][1] = 1
     table = cases.random_table(cases.CFG[4], seed=12)
     params = oracle_ref.init_params(cases.CFG, 31)
     tc = _train_cfg(pk, clip_norm=1e9)
