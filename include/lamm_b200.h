@@ -143,7 +143,10 @@ void lamm_ctx_destroy(lamm_ctx* ctx);
 /* Options: "graph" (CUDA-graph capture of the step, default 1),
  * "profile" (per-kernel CUDA events inside the step, default 0),
  * "export_fp64" (keep fp64 pair distance/unit for lamm_neighbor_list_copy),
- * "pdl" (programmatic dependent launch between the step's kernels, default 1). */
+ * "pdl" (programmatic dependent launch between the step's kernels, default 1),
+ * "rank_local" (default 0: a train step with workers > 1 on a context without
+ * a communicator is refused; 1: run and apply this rank's share alone, for
+ * per-rank timing and per-rank gradient checks). */
 int lamm_ctx_set_option(lamm_ctx* ctx, const char* name, int64_t value);
 
 /* ---------------------------------------------------------- parameters --- */
@@ -285,6 +288,12 @@ int lamm_kernel_times_reset(lamm_ctx* ctx);
 int lamm_step_times(lamm_ctx* ctx, double* total_ms, int64_t* steps);
 /* Number of this library's kernel launches issued by the last train step. */
 int64_t lamm_last_step_launches(lamm_ctx* ctx);
+/* Launch geometry of the context, for tests and benchmarks: "grid_edge" (CTAs of
+ * the edge kernels), "parts_per_cta" (edge partitions per CTA), "chunk_edges"
+ * (edges per TMA-staged chunk), "message_groups" / "edge_groups" / "force_groups"
+ * (edge streams per CTA), "message_block" / "edge_block" (edges per walk block),
+ * "sm_count", "edge_capacity". Unknown names are LAMM_EINPUT. */
+int lamm_ctx_get_info(lamm_ctx* ctx, const char* name, int64_t* value);
 
 /* -------------------------------------------------- host: scheduling --- */
 /* lamm::scheduler::greedy_assign, H/scheduler.hpp:66-67 / S/scheduler.cpp:62-89. */
@@ -338,11 +347,13 @@ int lamm_rms_state_load(const char* path, lamm_model_config* cfg, double* v, siz
 /* LAMMDS1 catalog subsets (S/dataset.cpp:273-330) read straight into the packed
  * batch layout of lamm_batch_view: info gives the sample and atom counts to size
  * the arrays (atom_ptr[count+1], positions[3N], Z[N], per-sample masks/energy,
- * forces[3N]); dataset_index is set to head_index (read_catalog). */
+ * forces[3N]); dataset_index is set to head_index (read_catalog). info reads
+ * through the records (a truncated file is LAMM_EINPUT); read refuses files with
+ * more than sample_cap samples or atom_cap atoms (the sizes of the arrays). */
 int lamm_subset_info(const char* path, int64_t* count, int64_t* total_atoms);
-int lamm_subset_read(const char* path, int32_t head_index, int64_t* atom_ptr, double* positions,
-                     int32_t* atomic_numbers, int32_t* dataset_index, uint8_t* energy_mask, uint8_t* force_mask,
-                     double* energy, double* forces);
+int lamm_subset_read(const char* path, int32_t head_index, int64_t sample_cap, int64_t atom_cap,
+                     int64_t* atom_ptr, double* positions, int32_t* atomic_numbers, int32_t* dataset_index,
+                     uint8_t* energy_mask, uint8_t* force_mask, double* energy, double* forces);
 
 /* Inverse of a 3x3 cell (row-major, rows = lattice vectors) by cofactors: the
  * exact bits the minimum-image test uses. Returns LAMM_EINPUT if singular. */

@@ -143,6 +143,7 @@ struct PackedBatch {
     std::vector<int32_t> Z, dataset_index;
     std::vector<uint8_t> energy_mask, force_mask, denoise;
     std::vector<double> cell;  // [B][9] periodic cells, empty if none was given (extension; see lamm_b200.h)
+    bool has_cell = false;     // some system carried a cell (then cell holds a row per system)
 
     int32_t size() const { return static_cast<int32_t>(atom_ptr.size() - 1); }
     int64_t atoms() const { return atom_ptr.back(); }
@@ -151,8 +152,13 @@ struct PackedBatch {
     // reference's AtomicSystem has none
     template <class System>
     void add_system(const System& s, const double* cell9 = nullptr) {
-        if (cell9 != nullptr && cell.empty()) cell.assign(9 * static_cast<size_t>(size()), 0.0);
-        if (!cell.empty()) {
+        // once any system has a cell, every system has a [9] row (all zero:
+        // non-periodic); the rows of the systems added before it are zero-filled
+        if (cell9 != nullptr && !has_cell) {
+            cell.assign(9 * static_cast<size_t>(size()), 0.0);
+            has_cell = true;
+        }
+        if (has_cell) {
             for (int k = 0; k < 9; ++k) cell.push_back(cell9 ? cell9[k] : 0.0);
         }
         const size_t n = s.positions.size();
@@ -204,7 +210,7 @@ struct PackedBatch {
         v.energy = energy.data();
         v.forces = forces.data();
         v.denoise = denoise.data();
-        v.cell = cell.empty() ? nullptr : cell.data();
+        v.cell = has_cell ? cell.data() : nullptr;
         return v;
     }
 };
@@ -515,6 +521,7 @@ StepResult train_step(Device& dev, std::span<const Sample> samples, std::span<co
     lamm_step_result r{};
     const int st = lamm_train_step(dev.get(), &v, &c, step, workers, rank, &r);
     dev.params_changed_on_device();
+    dev.batch_replaced(b.atom_ptr);  // earlier DeviceCaches are stale now
     check(st);
     return StepResult{r.loss, r.grad_norm, r.local, r.n_atoms, r.n_edges};
 }
@@ -534,7 +541,9 @@ int64_t submit_step(Device& dev, std::span<const Sample> samples, std::span<cons
     const lamm_batch_view v = b.view();
     const lamm_train_config c = train_config_to_c(tcfg);
     int64_t ticket = -1;
-    check(lamm_train_step_submit(dev.get(), &v, &c, step, workers, rank, &ticket));  // packed: b may go
+    const int st = lamm_train_step_submit(dev.get(), &v, &c, step, workers, rank, &ticket);  // packed: b may go
+    dev.batch_replaced(b.atom_ptr);  // the device batch is this step's from now on
+    check(st);
     return ticket;
 }
 

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("LAMM_B200_LIB") or os.path.join(_HERE, "liblamm_b200.so")  # override: A/B timing builds
+LIB_PATH = os.path.join(_HERE, "liblamm_b200.so")
 
 
 class LammError(RuntimeError):
@@ -84,7 +84,7 @@ EXPORTS = [
     "lamm_train_step_submit", "lamm_train_step_wait",
     "lamm_flush_l2", "lamm_step_times", "lamm_evaluate", "lamm_cell_inverse",
     "lamm_checkpoint_save", "lamm_checkpoint_load", "lamm_rms_state_save", "lamm_rms_state_load",
-    "lamm_subset_info", "lamm_subset_read", "lamm_train_step_workers",
+    "lamm_subset_info", "lamm_subset_read", "lamm_train_step_workers", "lamm_ctx_get_info",
 ]
 
 _lib = None

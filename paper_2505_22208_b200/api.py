@@ -413,6 +413,12 @@ class Device:
     def kernel_times_reset(self):
         check(lib().lamm_kernel_times_reset(self._h))
 
+    def info(self, name: str) -> int:
+        """Launch geometry (lamm_ctx_get_info): grid_edge, parts_per_cta, chunk_edges, ..."""
+        v = C.c_int64()
+        check(lib().lamm_ctx_get_info(self._h, name.encode(), C.byref(v)))
+        return v.value
+
     def last_step_launches(self) -> int:
         return int(lib().lamm_last_step_launches(self._h))
 

@@ -121,6 +121,7 @@ struct lamm_ctx {
     cudaGraphExec_t g_full = nullptr;  // step + optimizer in one graph (single rank: no allreduce between)
     bool graph_dirty = true;
     bool use_graph = true, profile = false, export64 = false, pdl = true;
+    bool rank_local = false;  // option "rank_local": workers > 1 without a communicator (one rank's share only)
     int denoise_scheme = 1;
     double opt_inv_g = 1.0, opt_lr = 0, opt_decay = 0, opt_eps = 0, opt_clip = 0;
     int opt_G = 1;
@@ -428,12 +429,17 @@ BatchArrays make_batch_arrays(Ctx& c) {
 }
 
 // ------------------------------------------------------------- launches ---
-// Timing experiments only: LAMM_SKIP_KERNEL=<name> leaves that kernel out of the
-// step (results are then wrong; used to measure a kernel's marginal cost).
+// Timing experiments only, compiled in with -DLAMM_TIMING_KNOBS (never in the
+// shipped build): LAMM_SKIP_KERNEL=<name> leaves that kernel out of the step
+// (results are then wrong; used to measure a kernel's marginal cost).
+#ifdef LAMM_TIMING_KNOBS
 inline bool skipped(const char* name) {
     const char* s = std::getenv("LAMM_SKIP_KERNEL");
     return s != nullptr && std::strcmp(s, name) == 0;
 }
+#else
+constexpr bool skipped(const char*) { return false; }
+#endif
 
 template <class Kern, class... Args>
 void launch(Ctx& c, const char* name, Kern kernel, int grid, int block, size_t smem, Args... args) {
@@ -963,7 +969,10 @@ StepHeader run_train_step(Ctx& c, const void* src, size_t bytes, cudaMemcpyKind 
         if (!sync) return StepHeader{};
         const StepHeader h = read_header(c);
         if (h.status != 2) {
-            c.batch_valid = c.nlist_valid = c.fwd_valid = c.loss_valid = true;
+            // the optimizer in the step graph already rewrote the parameters: the
+            // forward cache and the loss gradient belong to the old ones
+            c.batch_valid = c.nlist_valid = true;
+            c.fwd_valid = c.loss_valid = false;
             return h;
         }
         require(attempt < 4, "edge capacity regrowth did not converge");
@@ -1108,6 +1117,7 @@ LAMM_API int lamm_ctx_set_option(lamm_ctx* c, const char* name, int64_t value) {
         if (n == "graph") c->use_graph = value != 0;
         else if (n == "profile") c->profile = value != 0;
         else if (n == "pdl") c->pdl = value != 0;
+        else if (n == "rank_local") c->rank_local = value != 0;
         else if (n == "export_fp64") {
             c->export64 = value != 0;
             require_no_chain(*c);
@@ -1483,8 +1493,15 @@ LAMM_API int lamm_comm_init(lamm_ctx* c, int nranks, int rank, const void* id128
 namespace lamm_b200 {
 void apply_train_config(Ctx& c, const lamm_train_config* tc, int32_t workers, int32_t rank) {
     require(workers >= 1 && rank >= 0 && rank < workers, "train_step: bad worker layout");
-    require(workers == c.nranks || c.nranks == 1,
-            "train_step: workers must equal the communicator size (or 1 rank simulating)");
+    if (c.nranks > 1) {
+        require(workers == c.nranks && rank == c.rank, "train_step: workers/rank must match the communicator");
+    } else if (workers > 1) {
+        // without a communicator a workers > 1 step would apply this rank's gradient
+        // alone (scaled 1/G) - not the reference step (S/trainer.cpp:319-326)
+        require(c.rank_local,
+                "train_step: workers > 1 needs a communicator (lamm_comm_init) or lamm_train_step_workers; "
+                "set option rank_local to run one rank's share on its own");
+    }
     require(tc->learning_rate > 0.0, "train: learning_rate must be positive");
     require(tc->clip_norm >= 0.0, "train: clip_norm must be >= 0");
     require(tc->rms_decay >= 0.0 && tc->rms_decay < 1.0, "train: rms_decay must be in [0, 1)");
@@ -1811,6 +1828,24 @@ LAMM_API int lamm_step_times(lamm_ctx* c, double* total_ms, int64_t* steps) {
 }
 
 LAMM_API int64_t lamm_last_step_launches(lamm_ctx* c) { return c ? c->last_step_launches : -1; }
+
+LAMM_API int lamm_ctx_get_info(lamm_ctx* c, const char* name, int64_t* value) {
+    return lamm_guard([&] {
+        require(c && name && value, "get_info: null argument");
+        const std::string n(name);
+        if (n == "grid_edge") *value = c->grid_edge;
+        else if (n == "parts_per_cta") *value = kPartsPerCta;
+        else if (n == "chunk_edges") *value = kChunk;
+        else if (n == "message_groups") *value = kMsgGroups;
+        else if (n == "message_block") *value = MessageBody<128, 16, true, false>::kBlock;
+        else if (n == "edge_groups") *value = kGroups;
+        else if (n == "edge_block") *value = BwdBody<128, 16, true, false>::kBlock;
+        else if (n == "force_groups") *value = kForceGroups;
+        else if (n == "sm_count") *value = c->nsm;
+        else if (n == "edge_capacity") *value = c->Pcap;
+        else throw InputErr("get_info: unknown name " + n);
+    });
+}
 
 LAMM_API int lamm_cell_inverse(const double* cell, double* out) {
     return lamm_guard([&] {

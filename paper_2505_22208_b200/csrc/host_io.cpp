@@ -16,6 +16,7 @@
 //                            paper_2505_22208_b200/io.py reads it).
 #include <cmath>
 #include <cstdint>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -207,15 +208,24 @@ LAMM_API int lamm_subset_info(const char* path, int64_t* count, int64_t* total_a
     return lamm_guard([&] {
         require(path != nullptr, "subset_info: null path");
         File f(path, "rb");
+        require(std::fseek(f.f, 0, SEEK_END) == 0, "subset_info: cannot seek");
+        const long size = std::ftell(f.f);
+        require(size >= 0 && std::fseek(f.f, 0, SEEK_SET) == 0, "subset_info: cannot seek");
         f.magic(kDsMagic, 7);
         const uint64_t cnt = f.ru64();
         int64_t atoms = 0;
-        for (uint64_t s = 0; s < cnt; ++s) {  // skip through the records
+        // skip through the records; fseek succeeds past the end of the file, so
+        // every skip is checked against the file size (a truncated file is an error)
+        auto skip = [&](long bytes) {
+            const long at = std::ftell(f.f);
+            if (at < 0 || bytes > size - at || std::fseek(f.f, bytes, SEEK_CUR) != 0)
+                throw InputErr("unexpected end of file");
+        };
+        for (uint64_t s = 0; s < cnt; ++s) {
             const uint32_t n = f.ru32();
-            if (std::fseek(f.f, 24L * n + n, SEEK_CUR) != 0) throw InputErr("unexpected end of file");
+            skip(24L * n + n);
             const uint8_t mask = f.ru8();
-            long skip = ((mask & 1) ? 8L : 0L) + ((mask & 2) ? 24L * n : 0L);
-            if (skip && std::fseek(f.f, skip, SEEK_CUR) != 0) throw InputErr("unexpected end of file");
+            skip(((mask & 1) ? 8L : 0L) + ((mask & 2) ? 24L * n : 0L));
             atoms += n;
         }
         if (count) *count = static_cast<int64_t>(cnt);
@@ -223,19 +233,23 @@ LAMM_API int lamm_subset_info(const char* path, int64_t* count, int64_t* total_a
     });
 }
 
-LAMM_API int lamm_subset_read(const char* path, int32_t head_index, int64_t* atom_ptr, double* positions,
-                              int32_t* atomic_numbers, int32_t* dataset_index, uint8_t* energy_mask,
-                              uint8_t* force_mask, double* energy, double* forces) {
+LAMM_API int lamm_subset_read(const char* path, int32_t head_index, int64_t sample_cap, int64_t atom_cap,
+                              int64_t* atom_ptr, double* positions, int32_t* atomic_numbers, int32_t* dataset_index,
+                              uint8_t* energy_mask, uint8_t* force_mask, double* energy, double* forces) {
     return lamm_guard([&] {
         require(path && atom_ptr && positions && atomic_numbers, "subset_read: null argument");
         File f(path, "rb");
         f.magic(kDsMagic, 7);
         const uint64_t cnt = f.ru64();
+        require(cnt <= static_cast<uint64_t>(std::max<int64_t>(sample_cap, 0)),
+                "subset_read: more samples than sample_cap (size the arrays with lamm_subset_info)");
         atom_ptr[0] = 0;
         for (uint64_t s = 0; s < cnt; ++s) {
             const uint32_t n = f.ru32();
             require(n >= 1, "system has no atoms");  // validate_system (S/core.cpp:10-20)
             const int64_t a0 = atom_ptr[s];
+            require(static_cast<int64_t>(n) <= atom_cap - a0,
+                    "subset_read: more atoms than atom_cap (size the arrays with lamm_subset_info)");
             atom_ptr[s + 1] = a0 + n;
             for (uint32_t a = 0; a < n; ++a)
                 for (int c = 0; c < 3; ++c) {

@@ -55,7 +55,7 @@ def read_subset(path: str, head_index: int = 0) -> dict:
     b = dict(atom_ptr=np.empty(B + 1, np.int64), pos=np.empty((N, 3)), Z=np.empty(N, np.int32),
              dataset_index=np.empty(B, np.int32), energy_mask=np.empty(B, np.uint8), force_mask=np.empty(B, np.uint8),
              energy=np.empty(B), forces=np.empty((N, 3)), denoise=np.zeros(B, np.uint8))
-    check(lib().lamm_subset_read(os.fsencode(path), head_index, _p(b["atom_ptr"]), _p(b["pos"]), _p(b["Z"]),
+    check(lib().lamm_subset_read(os.fsencode(path), head_index, C.c_int64(B), C.c_int64(N), _p(b["atom_ptr"]), _p(b["pos"]), _p(b["Z"]),
                                  _p(b["dataset_index"]), _p(b["energy_mask"]), _p(b["force_mask"]), _p(b["energy"]),
                                  _p(b["forces"])))
     return b

@@ -320,6 +320,35 @@ void check_checkpoint(const lamm::model::ModelConfig& cfg, const lamm::model::Mo
 
 }  // namespace
 
+// PackedBatch::add_system keeps the cell of the FIRST system too (a one-sample
+// periodic batch), zero rows for systems without one; the device then applies the
+// minimum image: two atoms 9.5 A apart along x in a 10 A cubic cell are 0.5 A
+// apart periodically (2 directed pairs), none without the cell.
+void check_periodic_pack(lamm_b200::Device& dev, const lamm::model::ModelConfig& cfg) {
+    lamm::AtomicSystem sys;
+    sys.positions = {{0.25, 0.0, 0.0}, {9.75, 0.0, 0.0}};
+    sys.atomic_numbers = {6, 8};
+    const double cell[9] = {10.5, 0, 0, 0, 10.5, 0, 0, 0, 10.5};
+    lamm_b200::PackedBatch one;
+    one.add_system(sys, cell);
+    const lamm_batch_view v = one.view();
+    bool ok = v.cell != nullptr && one.cell.size() == 9 && one.cell[0] == 10.5 && one.cell[8] == 10.5;
+    lamm_b200::PackedBatch two;
+    two.add_system(sys);
+    two.add_system(sys, cell);
+    ok = ok && two.cell.size() == 18 && two.cell[0] == 0.0 && two.cell[9] == 10.5 && two.view().cell != nullptr;
+    lamm_b200::PackedBatch none;
+    none.add_system(sys);
+    ok = ok && none.view().cell == nullptr;
+    dev.set_batch(two);
+    int64_t npairs = 0;
+    lamm_b200::check(lamm_neighbor_list(dev.get(), &npairs));
+    std::vector<int64_t> ptr(3);
+    lamm_b200::check(lamm_neighbor_list_copy(dev.get(), ptr.data(), nullptr, nullptr, nullptr, nullptr));
+    ok = ok && npairs == 2 && ptr[1] - ptr[0] == 0 && ptr[2] - ptr[1] == 2;
+    report(ok, "PackedBatch: first system's cell kept, periodic pairs under the minimum image");
+}
+
 int main() {
     try {
         const lamm::model::ModelConfig cfg{128, 3, 16, 5.0, 4};
@@ -336,6 +365,7 @@ int main() {
         check_train_step(samples, cfg, params, table);
         check_evaluate(samples, cfg, params, table);
         check_checkpoint(cfg, params);
+        check_periodic_pack(dev, cfg);
         bool threw = false;
         try {
             lamm::model::ModelConfig bad = cfg;

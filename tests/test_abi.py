@@ -29,6 +29,16 @@ def test_exports_every_declared_symbol():
     assert all(s.startswith("lamm_") for s in exported)
 
 
+def test_no_timing_knobs_in_shipped_library():
+    """Timing-experiment knobs (LAMM_SKIP_KERNEL drops a kernel from the step) are
+    compiled in only with -DLAMM_TIMING_KNOBS; the shipped build has none, and the
+    Python loader takes no library-override environment variable."""
+    from paper_2505_22208_b200 import _lib
+    blob = open(_lib.LIB_PATH, "rb").read()
+    assert b"LAMM_SKIP_KERNEL" not in blob
+    assert "LAMM_B200_LIB" not in open(_lib.__file__).read()
+
+
 def test_library_is_sm100a_only():
     from paper_2505_22208_b200._lib import LIB_PATH
     out = subprocess.run(["cuobjdump", "--list-elf", LIB_PATH], capture_output=True, text=True).stdout

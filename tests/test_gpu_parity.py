@@ -229,6 +229,7 @@ def test_denoise_labels_match_reference(pk, oracle_ref):
     dev.set_reference_table(table)
     tc = _train_cfg(pk)
     B, G, rank, step = 12, 3, 2, 5
+    dev.set_option("rank_local", 1)  # one rank's share without a communicator
     dev.train_step(batch, tc, step=step, workers=G, rank=rank)
     # worker-major position of sample b on rank r is r*B + b (S/trainer.cpp:268)
     e_dev, f_dev = dev.labels()
@@ -288,6 +289,7 @@ def test_multi_worker_sum_semantics(pk, oracle_ref):
         dev = pk.Device(mcfg, seed=0)
         dev.set_params(params)
         dev.set_reference_table(table)
+        dev.set_option("rank_local", 1)
         shard = pk.select(batch, np.arange(r * B, (r + 1) * B))
         res = dev.train_step(shard, tc, step=1, workers=G, rank=r)
         gsum += dev.grads()

@@ -62,3 +62,28 @@ def test_catalog_reader_matches_reference(tmp_path, io, oracle_ref):
         assert np.array_equal(ours[k].view(np.uint64), ref[k].view(np.uint64)), k
     assert [s["task"] for s in cat["subsets"]] == ["energy_and_forces", "energy_only", "denoising"]
     assert cat["subsets"][2]["batch"]["denoise"].all()
+
+
+def test_subset_truncated_and_capacity(tmp_path, io, oracle_ref):
+    """A truncated LAMMDS1 file fails in info (not a silent short count), and read
+    refuses arrays smaller than the file declares."""
+    import ctypes as C
+    import paper_2505_22208_b200 as pk
+    from paper_2505_22208_b200._lib import lib
+    d = str(tmp_path / "cat")
+    oracle_ref.write_demo_catalog(d, 6, 3)
+    f = sorted(x for x in os.listdir(d) if x.endswith(".bin"))[0]
+    path = os.path.join(d, f)
+    full = open(path, "rb").read()
+    b = io.read_subset(path)
+    trunc = str(tmp_path / "trunc.bin")
+    open(trunc, "wb").write(full[:-5])
+    with pytest.raises(pk.InputError):
+        io.read_subset(trunc)
+    B, N = len(b["atom_ptr"]) - 1, int(b["atom_ptr"][-1])
+    ap, pos, Z = np.empty(B + 1, np.int64), np.empty(3 * N), np.empty(N, np.int32)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    for scap, acap in ((B - 1, N), (B, N - 1)):
+        st = lib().lamm_subset_read(os.fsencode(path), 0, C.c_int64(scap), C.c_int64(acap), p(ap), p(pos), p(Z),
+                                    None, None, None, None, None)
+        assert st == 1
