@@ -113,6 +113,7 @@ struct lamm_ctx {
     std::vector<uint8_t> h_emask, h_fmask;
     int me = 0, mf = 0;
     bool batch_valid = false, nlist_valid = false, fwd_valid = false, loss_valid = false;
+    bool grads_in_acc = false;  // the last step was lamm_train_step_workers: its worker sum is in g64
     // launch geometry
     int grid_warp = 0, grid_gemm = 0, grid_upd = 0, grid_small = 0, grid_opt = 0, ncta_red = 0, grid_reduce = 0;
     int grid_edge = 0, grid_emb = 0;
@@ -957,6 +958,7 @@ void launch_step(Ctx& c) {
 // the in-flight poison cleared (an overflowing attempt sets it again).
 StepHeader run_train_step(Ctx& c, const void* src, size_t bytes, cudaMemcpyKind kind, bool sync = true,
                           bool clear_poison = false) {
+    c.grads_in_acc = false;
     for (int attempt = 0;; ++attempt) {
         ensure_capacity(c, c.N, c.B, edge_guess(c.N));
         if (bytes > c.d_stage.bytes) ensure_stage(c, bytes);
@@ -983,6 +985,7 @@ StepHeader run_train_step(Ctx& c, const void* src, size_t bytes, cudaMemcpyKind 
 // Upload + step graph without the optimizer (one simulated worker); regrows
 // the edge capacity and reruns on overflow. Returns the header after the pass.
 StepHeader run_pass(Ctx& c, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    c.grads_in_acc = false;
     for (int attempt = 0;; ++attempt) {
         ensure_capacity(c, c.N, c.B, edge_guess(c.N));
         if (bytes > c.d_stage.bytes) ensure_stage(c, bytes);
@@ -1427,6 +1430,7 @@ LAMM_API int lamm_loss_grad(lamm_ctx* c, const lamm_loss_config* cfg, lamm_loss_
 LAMM_API int lamm_backward(lamm_ctx* c, const double* up_energy, const double* up_forces, double* grads_accum) {
     return lamm_guard([&] {
         require(c != nullptr, "backward: null ctx");
+        c->grads_in_acc = false;
         require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         ensure_forward(*c);
@@ -1457,6 +1461,11 @@ LAMM_API int lamm_grads_get(lamm_ctx* c, double* flat, size_t n) {
         require(c && flat && static_cast<int64_t>(n) == c->NP, "grads_get: size mismatch");
         require_no_chain(*c);
         CK(cudaSetDevice(c->device));
+        if (c->grads_in_acc) {  // simulated workers: the fp64 worker sum the optimizer consumed
+            CK(cudaMemcpyAsync(flat, c->g64.p, sizeof(double) * c->NP, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            return;
+        }
         const auto g = d2h<float>(*c, c->grads.p, c->NP);
         for (int64_t k = 0; k < c->NP; ++k) flat[k] = g[k];
     });
@@ -1491,11 +1500,12 @@ LAMM_API int lamm_comm_init(lamm_ctx* c, int nranks, int rank, const void* id128
 }
 
 namespace lamm_b200 {
-void apply_train_config(Ctx& c, const lamm_train_config* tc, int32_t workers, int32_t rank) {
+// simulated: lamm_train_step_workers runs every worker on this ctx and sums them itself
+void apply_train_config(Ctx& c, const lamm_train_config* tc, int32_t workers, int32_t rank, bool simulated = false) {
     require(workers >= 1 && rank >= 0 && rank < workers, "train_step: bad worker layout");
     if (c.nranks > 1) {
         require(workers == c.nranks && rank == c.rank, "train_step: workers/rank must match the communicator");
-    } else if (workers > 1) {
+    } else if (workers > 1 && !simulated) {
         // without a communicator a workers > 1 step would apply this rank's gradient
         // alone (scaled 1/G) - not the reference step (S/trainer.cpp:319-326)
         require(c.rank_local,
@@ -1730,7 +1740,7 @@ LAMM_API int lamm_train_step_workers(lamm_ctx* c, const lamm_batch_view* batches
         int64_t atoms = 0, edges = 0;
         for (int32_t g = 0; g < workers; ++g) {  // worker order, like S/trainer.cpp:262
             validate_batch(*c, &batches[g]);
-            apply_train_config(*c, tc, workers, g);
+            apply_train_config(*c, tc, workers, g, true);
             const size_t bytes = pack_batch(*c, &batches[g], true, tc, step, g);
             const StepHeader h = run_pass(*c, c->h_stage, bytes, cudaMemcpyHostToDevice);
             atoms += c->N, edges += h.P;
@@ -1744,6 +1754,7 @@ LAMM_API int lamm_train_step_workers(lamm_ctx* c, const lamm_batch_view* batches
         const StepHeader h = read_header(*c);
         c->batch_valid = c->nlist_valid = true;  // the last worker's batch stays current
         c->fwd_valid = c->loss_valid = false;    // its parameters changed
+        c->grads_in_acc = true;
         c->last_h2d = 0;
         fill_result(*c, h, res);
         if (res) res->n_atoms = atoms, res->n_edges = edges;
@@ -1757,6 +1768,7 @@ LAMM_API int lamm_optimizer_step(lamm_ctx* c, const double* grad_sum, int32_t wo
     return lamm_guard([&] {
         require(c && grad_sum && tc, "optimizer_step: null argument");
         require(workers >= 1, "optimizer_step: workers must be >= 1");
+        c->grads_in_acc = false;
         require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         CK(cudaMemcpyAsync(c->g64.p, grad_sum, sizeof(double) * c->NP, cudaMemcpyHostToDevice, c->stream));

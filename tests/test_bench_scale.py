@@ -109,8 +109,9 @@ def test_cfg2_bench_slots_match_reference(pk, oracle_ref):
     for s in picks:
         b = shards[s]
         rp = row_ptr_of(dev, b)
-        assert len(b["atom_ptr"]) - 1 == 256 and atoms[s] > 5000
+        assert len(b["atom_ptr"]) - 1 == 256
         if s == picks[0]:  # the steady-state restage path (k + 2 < nchunks) runs
+            assert atoms[s] > 5000
             for g, blk in ((geo["message_groups"], geo["message_block"]), (geo["edge_groups"], geo["edge_block"])):
                 nch = max_chunks_per_group(rp, Q, g, geo["parts_per_cta"], blk, geo["chunk_edges"])
                 assert nch >= 3, (g, blk, nch)
@@ -190,7 +191,8 @@ def test_cfg3_semisupervised_mix_g8_b32(pk, oracle_ref):
     dev.set_reference_table(table)
     res = dev.train_step_workers([pk.select(batch, np.arange(g * B, (g + 1) * B)) for g in range(G)], tc, step=2)
     assert res.n_atoms == int(batch["atom_ptr"][-1])
-    _check_step(res, dev.grads(), dev.rms_state(), ref, cases.CFG, "cfg3 G=8 B=32")
+    # grads_get after simulated workers: the fp64 worker sum the optimizer consumed (before /G)
+    _check_step(res, dev.grads() / G, dev.rms_state(), ref, cases.CFG, "cfg3 G=8 B=32")
     dev.close()
 
 

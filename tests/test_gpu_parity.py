@@ -323,6 +323,7 @@ def test_simulated_workers_step_matches_reference(pk, oracle_ref):
     assert abs(res.loss - ref["loss"]) <= TOL * abs(ref["loss"])
     assert abs(res.grad_norm - ref["grad_norm"]) <= TOL * ref["grad_norm"]
     assert_close(dev.rms_state(), ref["rms_v"], tol=3 * TOL, what="rms v after the G-worker step")
+    assert_close(dev.grads() / G, ref["grads"], what="worker-summed gradient / G")
     # a second step continues from the device state (graph reuse, accumulator reset)
     ref2 = oracle_ref.train_step(cases.CFG, G, B, batch, table, ref["params"], ref["rms_v"], seed=tc.seed, step=5,
                                  clip=tc.clip_norm)
