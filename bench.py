@@ -144,27 +144,50 @@ class ClockSampler:
 
 # ------------------------------------------------------------ roofline
 def kernel_bytes(name, N, P, H=128, K=16, D=10):
-    """Algorithmic (compulsory, gather-inclusive) HBM-side bytes per launch, fp32
-    storage, from the data each kernel must touch."""
+    """Algorithmic bytes per launch, SURVEY.md §8(d)'s model verbatim: fp32
+    storage, gather-inclusive (every edge pays its source-row read):
+      message   P (4 + 4 + 4H) + N 8H          bwd_edge  P (8 + 8H) + N 12H
+      force     P (20 + 4H) + N (4H + 12D)     head_bwd  P (20 + 4H + 12D) + N (8H + 12D)
+    (node GEMMs: activations in + out + weights)."""
     e = {
-        "message": P * (4 + 4 + 4 * K + 4 * H) + N * (8 + 4 * H),
-        "bwd_edge": P * (4 + 4 + 4 * K + 8 * H) + N * (8 + 16 * H),
-        "force": P * (4 + 16 + 4 * K + 4 * H + 4 * D) + N * (8 + 4 * H + 4 * D + 12 * D),
-        "head_bwd": P * (4 + 16 + 12 + 4 * H + 4 * K) + N * (8 + 4 * H + 12 + 8 * H + 4 * (H + K + 4)),
+        "message": P * (4 + 4 + 4 * H) + N * 8 * H,
+        "bwd_edge": P * (8 + 8 * H) + N * 12 * H,
+        "force": P * (20 + 4 * H) + N * (4 * H + 12 * D),
+        "head_bwd": P * (20 + 4 * H + 12 * D) + N * (8 * H + 12 * D),
         "update": N * (4 * H + 4 * H + 8 * H) + 4 * H * H,
         "bwd_gemm": N * (8 * H + 4 * H) + 4 * H * H,
     }
     return e.get(name)
 
 
-def ncu_traffic(name, algorithmic_bytes):
+def kernel_bytes_unique(name, N, P, H=128, K=16, D=10):
+    """Compulsory (unique) bytes per launch: every array the kernel touches read or
+    written once (per-edge metadata as stored: col, dst, {r, fcut}, segment bits;
+    per-atom rows once). The gap to the gather-inclusive bytes is L1/L2 reuse of
+    the gathered source rows."""
+    e = {
+        "message": P * (4 + 4 + 8 + 0.125) + N * (4 * H + 4 * H + 4),
+        "bwd_edge": P * (4 + 4 + 8 + 0.125) + N * (4 * H + 4 * H + 8 * H + 4),
+        "force": P * (4 + 4 + 16 + 8 + 0.125) + N * (4 * H + 4 * (3 * H + 3 + 3 * K) + 4),
+        "head_bwd": P * (4 + 4 + 8 + 8 + 0.125) + N * (4 * H + 4 * H + 4 * H + 16 + 4),
+        "update": N * (4 * H + 4 * H + 8 * H) + 4 * H * H,
+        "bwd_gemm": N * (8 * H + 4 * H) + 4 * H * H,
+    }
+    return e.get(name)
+
+
+TRAFFIC_JSON = "r02_ncu_traffic.json"
+
+
+def ncu_traffic(name, algorithmic_bytes, which="cfg2"):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the
-    kernel from the committed ncu --set full capture (profiles/r01_ncu_traffic.json),
-    scaled from the captured step to this workload by the algorithmic bytes."""
+    kernel from the committed ncu --set full capture (profiles/r02_ncu_traffic.json,
+    section `which`), scaled from the captured step to this workload by the
+    algorithmic bytes."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
-            k = json.load(f)["kernels"][name]
-        return k["ratio"] * algorithmic_bytes
+        with open(os.path.join(ROOT, "profiles", TRAFFIC_JSON)) as f:
+            k = json.load(f)[which]["kernels"][name]
+        return k["dram_bytes"] / k["algorithmic_bytes"] * algorithmic_bytes
     except Exception:
         return None
 
@@ -277,15 +300,18 @@ def run_ours(args, dist):
     launches_per_step = tcount / steps_done
     byts = kernel_bytes(tname, N_mean, P_mean)
     roof = {"kernel": tname, "bound": "hbm", "unit": "GB/s", "peak": hbm, "peak_source": src,
-            "traffic_source": "profiles/r01_ncu_traffic.json (ncu --set full, DRAM bytes / algorithmic bytes of the "
-                              "captured step, times this workload's algorithmic bytes)",
+            "bytes_model": "SURVEY.md §8(d) (gather-inclusive, fp32 storage)",
+            "traffic_source": f"profiles/{TRAFFIC_JSON} (ncu --set full, DRAM bytes / algorithmic bytes of the "
+                              "captured cfg2 step, times this workload's algorithmic bytes)",
             "share_of_step": tms / tot_ms if tot_ms else None, "avg_launch_us": per_launch_ms * 1e3,
             "launches_per_step": launches_per_step,
             "timing": "CUDA event pair around each launch on the ctx stream, second pass over the same K steps "
                       "(profiled step %.3f ms vs %.3f ms unprofiled)" % (prof_ms / K, dev_ms / K)}
     if byts is not None:
         ach = byts / (per_launch_ms / 1e3) / 1e9
-        roof.update(achieved=ach, frac=ach / hbm, traffic=ncu_traffic(tname, byts), algorithmic_bytes_per_launch=byts)
+        ub = kernel_bytes_unique(tname, N_mean, P_mean)
+        roof.update(achieved=ach, frac=ach / hbm, traffic=ncu_traffic(tname, byts), algorithmic_bytes_per_launch=byts,
+                    compulsory_bytes_per_launch=ub, compulsory_frac=ub / (per_launch_ms / 1e3) / 1e9 / hbm)
     fl = kernel_flops(tname, N_mean, P_mean)
     if fl is not None:
         roof["fp32_flops_per_launch"] = fl
@@ -320,6 +346,8 @@ def run_ours(args, dist):
         out["periodic_cfg1"] = periodic_cfg1(pk, mcfg, tc)
         out["semisup_cfg3"] = semisup_cfg3(pk, mcfg, tc)
         out["supercells_cfg4"] = supercells_cfg4(pk, mcfg, tc)
+    if dist.rank == 0 and dist.world == 1 and not args.no_large:
+        out["roofline_large"] = roofline_large(pk, mcfg, tc)
     dev.close()
     return out
 
@@ -616,6 +644,83 @@ def supercells_cfg4(pk, mcfg, tc, Gs=(2, 4, 8), B=4, steps=6):
     return out
 
 
+LARGE_B = 48  # 1,000-atom supercells per step: N = 48,000, P = 1.344 M (working set >> the 126 MB L2)
+
+
+def large_batch(pk, B=LARGE_B, reps=5, seed=2000):
+    """B periodic diamond-Si supercells of reps^3 cubic cells (1,000 atoms at reps
+    5, 28 neighbours each within 5 A), random labels: one device-batch whose
+    per-layer features alone (h, t, mu: 3 x N x 512 B) exceed the L2."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import cases
+    rng = np.random.default_rng(seed)
+    parts = []
+    for s in range(B):
+        pos, Z, cell = cases.diamond_supercell(reps=reps, seed=seed + s)
+        n = len(Z)
+        parts.append(dict(atom_ptr=np.array([0, n], np.int64), pos=pos, Z=Z,
+                          forces=rng.normal(0, 0.1, (n, 3)), dataset_index=np.array([s % CFG["heads"]], np.int32),
+                          energy_mask=np.ones(1, np.uint8), force_mask=np.ones(1, np.uint8),
+                          energy=np.array([-4.6 * n + rng.normal()]), denoise=np.zeros(1, np.uint8),
+                          cell=cell[None]))
+    return pk.concat(parts)
+
+
+def roofline_large(pk, mcfg, tc, steps=5):
+    """the edge kernels' roofline on a device-batch larger
+    than L2 (LARGE_B x 1,000-atom supercells), where the HBM bound is meaningful.
+    Per kernel: event-timed launch duration (profiled pass), SURVEY §8(d)
+    gather-inclusive bytes and compulsory (unique) bytes as fractions of the
+    measured HBM peak, and the ncu DRAM bytes per launch of the committed capture
+    (profiles/r02_ncu_traffic.json, section "large") when present."""
+    hbm, _, src = peaks()
+    batch = large_batch(pk)
+    N = int(batch["atom_ptr"][-1])
+    dev = pk.Device(mcfg, seed=7)
+    dev.set_reference_table(fit_table(batch, CFG["heads"]))
+    dev.stage(batch, tc, step=0, slot=0)
+    for _ in range(3):
+        r = dev.train_step_staged(0, sync=True)
+    P = r.n_edges
+    ms = []
+    for _ in range(steps):
+        dev.flush_l2(L2_FLUSH)
+        dev.event_record(0)
+        dev.train_step_staged(0, sync=False)
+        dev.event_record(1)
+        ms.append(dev.event_elapsed_ms(0, 1))
+    dev.set_option("profile", 1)
+    dev.train_step_staged(0, sync=True)
+    dev.kernel_times_reset()
+    for _ in range(steps):
+        dev.flush_l2(L2_FLUSH)
+        dev.train_step_staged(0, sync=True)
+    kt = dev.kernel_times()
+    dev.set_option("profile", 0)
+    dev.close()
+    step_ms = float(np.median(ms))
+    kern = {}
+    for name in ("bwd_edge", "message", "head_bwd", "force", "update", "bwd_gemm"):
+        if name not in kt:
+            continue
+        tot, cnt = kt[name]
+        us = tot / cnt * 1e3
+        b8, bu = kernel_bytes(name, N, P), kernel_bytes_unique(name, N, P)
+        row = {"launches_per_step": cnt / steps, "avg_launch_us": us,
+               "s8d_bytes": b8, "s8d_GBs": b8 / us / 1e3, "s8d_frac": b8 / us / 1e3 / hbm,
+               "compulsory_bytes": bu, "compulsory_GBs": bu / us / 1e3, "compulsory_frac": bu / us / 1e3 / hbm,
+               "share_of_step": tot / sum(v[0] for v in kt.values())}
+        tr = ncu_traffic(name, b8, which="large")
+        if tr is not None:
+            row["ncu_dram_bytes"] = tr
+            row["ncu_dram_over_compulsory"] = tr / bu
+        kern[name] = row
+    return {"workload": f"{LARGE_B} periodic diamond-Si supercells of 1,000 atoms (5x5x5 cubic cells), one "
+                        "device-batch per step, L2 flushed between steps", "atoms": N, "edges": P,
+            "ms_per_step": step_ms, "atoms_per_s": N / step_ms * 1e3, "peak_GBs": hbm, "peak_source": src,
+            "kernels": kern}
+
+
 def semisup_cfg3(pk, mcfg, tc, G=8, B=32, steps=6):
     """BASELINE configs[2] (non-periodic twin): three subsets of
     reference-generator structures clamped to 8-200 atoms — E+F labeled (mode 15),
@@ -702,6 +807,8 @@ def main():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-imbalance", action="store_true")
+    ap.add_argument("--no-large", action="store_true", help="skip the larger-than-L2 roofline section")
+    ap.add_argument("--only-large", action="store_true", help="run only the larger-than-L2 roofline section")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -713,6 +820,10 @@ def main():
         assert "paper_2505_22208_b200" not in sys.modules, "the reference arm imported the product"
         out["product_imported"] = False
         print(json.dumps(out), flush=True)
+        return
+    if args.only_large:
+        import paper_2505_22208_b200 as pk
+        print(json.dumps(roofline_large(pk, pk.ModelConfig(**CFG), pk.TrainConfig(seed=11))), flush=True)
         return
     from paper_2505_22208_b200.dist import Dist
     dist = Dist("gloo")
