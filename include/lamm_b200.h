@@ -76,9 +76,17 @@ typedef struct {
     /* Periodic cells (extension; the reference has none): [n_samples][3][3], row k =
      * lattice vector k (Angstrom); an all-zero cell marks a non-periodic sample.
      * NULL: every sample is non-periodic (the reference's behaviour, bit-exact).
-     * Periodic samples use the minimum image, which requires every perpendicular
-     * cell width >= 2 * cutoff (else LAMM_EINPUT). */
+     * A periodic sample's pairs are (i, j, n): every image of j within the cutoff,
+     * n the integer shift relative to j's minimum image (cells at least 2 * cutoff
+     * wide on every periodic axis: exactly the minimum image; narrower cells:
+     * several images per pair and self-images (i, i, n != 0)); order i-major, j
+     * ascending, n lexicographic (oracle/lamm_oracle.c states the fp64 sequence).
+     * More than 4096 images per pair (cells far below the cutoff) is LAMM_EINPUT. */
     const double* cell;
+    /* Per-axis periodicity of the cells, [n_samples][3] (1 periodic, 0 open: no
+     * wrapping along lattice vector k, e.g. slabs {1, 1, 0}). NULL: all periodic.
+     * Ignored for non-periodic samples. */
+    const uint8_t* pbc;
 } lamm_batch_view;
 
 /* lamm::loss::ReferenceTable / DatasetNormalizer, H/loss.hpp:31-44. rho and

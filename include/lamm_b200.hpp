@@ -143,23 +143,27 @@ struct PackedBatch {
     std::vector<int32_t> Z, dataset_index;
     std::vector<uint8_t> energy_mask, force_mask, denoise;
     std::vector<double> cell;  // [B][9] periodic cells, empty if none was given (extension; see lamm_b200.h)
+    std::vector<uint8_t> pbc;  // [B][3] per-axis periodicity of the cells (1 on all axes unless given)
     bool has_cell = false;     // some system carried a cell (then cell holds a row per system)
 
     int32_t size() const { return static_cast<int32_t>(atom_ptr.size() - 1); }
     int64_t atoms() const { return atom_ptr.back(); }
 
-    // cell9: optional periodic cell of this system (rows = lattice vectors); the
-    // reference's AtomicSystem has none
+    // cell9: optional periodic cell of this system (rows = lattice vectors); pbc3:
+    // optional per-axis periodicity of that cell (nullptr: periodic on all three
+    // axes, e.g. {1, 1, 0} for a slab); the reference's AtomicSystem has neither
     template <class System>
-    void add_system(const System& s, const double* cell9 = nullptr) {
+    void add_system(const System& s, const double* cell9 = nullptr, const uint8_t* pbc3 = nullptr) {
         // once any system has a cell, every system has a [9] row (all zero:
         // non-periodic); the rows of the systems added before it are zero-filled
         if (cell9 != nullptr && !has_cell) {
             cell.assign(9 * static_cast<size_t>(size()), 0.0);
+            pbc.assign(3 * static_cast<size_t>(size()), 1);
             has_cell = true;
         }
         if (has_cell) {
             for (int k = 0; k < 9; ++k) cell.push_back(cell9 ? cell9[k] : 0.0);
+            for (int k = 0; k < 3; ++k) pbc.push_back(pbc3 ? (pbc3[k] ? 1 : 0) : 1);
         }
         const size_t n = s.positions.size();
         if (s.atomic_numbers.size() != n) throw InputError("system: positions / atomic_numbers size mismatch");
@@ -211,6 +215,7 @@ struct PackedBatch {
         v.forces = forces.data();
         v.denoise = denoise.data();
         v.cell = has_cell ? cell.data() : nullptr;
+        v.pbc = has_cell ? pbc.data() : nullptr;
         return v;
     }
 };

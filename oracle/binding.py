@@ -77,9 +77,10 @@ class OracleLib:
         return out
 
     @contextlib.contextmanager
-    def periodic(self, cells):
-        """Port only: batch calls inside use these cells ([B, 3, 3], all-zero = non-periodic),
-        minimum image (parity-unpinned extension: the reference has no cells)."""
+    def periodic(self, cells, pbc=None):
+        """Port only: batch calls inside use these cells ([B, 3, 3], all-zero = non-periodic)
+        and per-axis periodicity pbc ([B, 3], None = all periodic): every image within the
+        cutoff (parity-unpinned extension: the reference has no cells)."""
         if self.kind != "port":
             raise NotImplementedError("the reference has no periodic cells")
         cells = _c(np.asarray(cells).reshape(-1, 9), np.float64)
@@ -87,11 +88,14 @@ class OracleLib:
         for s in range(len(cells)):
             if np.any(cells[s] != 0.0):
                 inv[s] = self.cell_inverse(cells[s])
+        flags = None if pbc is None else _c(np.asarray(pbc).reshape(-1, 3), np.uint8)
         self.lib.lor_set_cells(_p(cells), _p(inv))
+        self.lib.lor_set_pbc(_p(flags) if flags is not None else None)
         try:
             yield
         finally:
             self.lib.lor_set_cells(None, None)
+            self.lib.lor_set_pbc(None)
 
     def _samples_from_handle(self, h):
         cnt, tot = _i64(), _i64()
@@ -172,13 +176,16 @@ class OracleLib:
         Z = _c(Z, np.int32)
         n = len(Z)
         cap = max(1, n * (n - 1))
-        oi, oj = np.empty(cap, np.int32), np.empty(cap, np.int32)
-        od, ou = np.empty(cap, np.float64), np.empty((cap, 3), np.float64)
-        cnt = self._f("neighbor_list")(_i32(n), _p(pos), _p(Z), _f64(cutoff), _i64(cap), _p(oi), _p(oj), _p(od),
-                                       _p(ou))
-        if cnt < 0:
-            raise OracleError(self._f("last_error")().decode())
-        return oi[:cnt], oj[:cnt], od[:cnt], ou[:cnt]
+        while True:  # periodic images can give more than n (n - 1) pairs: grow and retry
+            oi, oj = np.empty(cap, np.int32), np.empty(cap, np.int32)
+            od, ou = np.empty(cap, np.float64), np.empty((cap, 3), np.float64)
+            cnt = self._f("neighbor_list")(_i32(n), _p(pos), _p(Z), _f64(cutoff), _i64(cap), _p(oi), _p(oj),
+                                           _p(od), _p(ou))
+            if cnt < 0:
+                raise OracleError(self._f("last_error")().decode())
+            if cnt <= cap:
+                return oi[:cnt], oj[:cnt], od[:cnt], ou[:cnt]
+            cap = cnt
 
     # -------------------------------------------------------------- model
     def param_count(self, cfg):

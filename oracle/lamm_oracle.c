@@ -157,13 +157,20 @@ static int validate_system(int32_t n, const double* pos, const int32_t* Z) { /* 
 
 /* Periodic cells (SURVEY.md §8(f) extension; the reference has none, so this is
  * parity-unpinned): sample s is periodic when g_cells holds a nonzero 3x3 cell
- * (rows = lattice vectors) for it; pairs then use the minimum image,
- *   f_k = sum_c d_c cinv[c][k], f_k -= rint(f_k), d_c = sum_k f_k cell[k][c],
- * evaluated left to right without contraction (the device kernels use the same
- * sequence with __dmul_rn/__dadd_rn), which is exact for cells whose
- * perpendicular widths are at least 2 * cutoff. */
+ * (rows = lattice vectors) for it, with per-axis periodicity g_pbc[s][k] (NULL:
+ * all three axes periodic). A pair is (i, j, n): atom j's image shifted by the
+ * integer vector n relative to its minimum image,
+ *   f_k = sum_c d_c cinv[c][k];  f_k -= rint(f_k) on periodic axes;
+ *   g_k = f_k - n_k;  d_c = sum_k g_k cell[k][c]         (d = p_i - p_j, left to right,
+ * no contraction; the device kernels use the same sequence with __d*_rn), with
+ * n_k in [-m_k, m_k], m_k = floor(0.5 + cutoff * b_k (1 + 1e-9)) on periodic axes
+ * (b_k = |column k of cinv| = 1 / perpendicular width k) and 0 otherwise: every
+ * image within the cutoff (|f_k| < cutoff b_k for |d| < cutoff, |f_k - rint| <= 1/2).
+ * Order: i-major, j ascending, then n lexicographic; (i, i, 0) excluded. Cells at
+ * least 2 * cutoff wide on every periodic axis give m = 0: the minimum image. */
 static _Thread_local const double* g_cells = NULL;
 static _Thread_local const double* g_cellinv = NULL;
+static _Thread_local const uint8_t* g_pbc = NULL;
 
 /* 3x3 inverse by cofactors (rows = lattice vectors), the same expression
  * sequence as the device library's cell_inverse (device.cuh); 1 if singular. */
@@ -183,6 +190,20 @@ void lor_set_cells(const double* cells, const double* cellinv) {
     g_cellinv = cellinv;
 }
 
+void lor_set_pbc(const uint8_t* pbc) { g_pbc = pbc; }
+
+/* Image range per axis (-1: non-periodic axis of a periodic sample). */
+void lor_image_range(const double* ci, const uint8_t* pbc, double cutoff, int* m) {
+    for (int k = 0; k < 3; ++k) {
+        if (pbc && !pbc[k]) {
+            m[k] = -1;
+            continue;
+        }
+        const double b = sqrt((ci[k] * ci[k] + ci[3 + k] * ci[3 + k]) + ci[6 + k] * ci[6 + k]);
+        m[k] = (int)floor(0.5 + cutoff * b * (1.0 + 1e-9));
+    }
+}
+
 static const double* cell_of(int64_t s) {
     if (!g_cells) return NULL;
     const double* c = g_cells + 9 * s;
@@ -191,12 +212,14 @@ static const double* cell_of(int64_t s) {
     return NULL;
 }
 
-static void min_image(const double* cell, const double* ci, double* d0, double* d1, double* d2) {
+static void image_disp(const double* cell, const double* ci, const int* m, const int* n, double* d0, double* d1,
+                       double* d2) {
     double f[3];
     for (int k = 0; k < 3; ++k) {
         const double a = *d0 * ci[k], b = *d1 * ci[3 + k], c = *d2 * ci[6 + k];
         f[k] = (a + b) + c;
-        f[k] = f[k] - rint(f[k]);
+        if (m[k] >= 0) f[k] = f[k] - rint(f[k]);
+        f[k] = f[k] - (double)n[k];
     }
     double o[3];
     for (int c = 0; c < 3; ++c) {
@@ -207,11 +230,12 @@ static void min_image(const double* cell, const double* ci, double* d0, double* 
 }
 
 /* S/core.cpp:30-48: all ordered pairs, r < cutoff strictly, i-major, j-ascending.
- * cell/ci non-NULL: minimum-image pairs of a periodic sample. */
+ * cell/ci non-NULL: the image pairs of a periodic sample (pbc: its per-axis flags,
+ * NULL = all periodic), see above. */
 static int build_pairs_cell(int32_t n, const double* pos, const int32_t* Z, double cutoff, const double* cell,
-                            const double* ci, Pairs* out);
+                            const double* ci, const uint8_t* pbc, Pairs* out);
 static int build_pairs_cell(int32_t n, const double* pos, const int32_t* Z, double cutoff, const double* cell,
-                            const double* ci, Pairs* out) {
+                            const double* ci, const uint8_t* pbc, Pairs* out) {
     if (validate_system(n, pos, Z)) return 1;
     if (!(cutoff > 0.0)) return set_err("cutoff must be positive"), 1;
     int64_t cap = 64, cnt = 0;
@@ -219,11 +243,17 @@ static int build_pairs_cell(int32_t n, const double* pos, const int32_t* Z, doub
     out->j = malloc(sizeof(int32_t) * cap);
     out->dist = malloc(sizeof(double) * cap);
     out->unit = malloc(sizeof(double) * 3 * cap);
+    int m[3] = {0, 0, 0};
+    if (cell) lor_image_range(ci, pbc, cutoff, m);
+    const int w0 = 2 * (m[0] > 0 ? m[0] : 0) + 1, w1 = 2 * (m[1] > 0 ? m[1] : 0) + 1,
+              w2 = 2 * (m[2] > 0 ? m[2] : 0) + 1;
+    const int nimg = w0 * w1 * w2;
     for (int32_t i = 0; i < n; ++i) {
-        for (int32_t j = 0; j < n; ++j) {
-            if (j == i) continue;
+        for (int32_t j = 0; j < n; ++j) for (int img = 0; img < nimg; ++img) {
+            const int sh[3] = {img / (w1 * w2) - (w0 - 1) / 2, (img / w2) % w1 - (w1 - 1) / 2, img % w2 - (w2 - 1) / 2};
+            if (j == i && sh[0] == 0 && sh[1] == 0 && sh[2] == 0) continue;
             double d0 = pos[3 * i] - pos[3 * j], d1 = pos[3 * i + 1] - pos[3 * j + 1], d2 = pos[3 * i + 2] - pos[3 * j + 2];
-            if (cell) min_image(cell, ci, &d0, &d1, &d2);
+            if (cell) image_disp(cell, ci, m, sh, &d0, &d1, &d2);
             const double r = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
             if (r < cutoff) {
                 if (cnt == cap) {
@@ -259,7 +289,7 @@ int64_t lor_neighbor_list(int32_t n, const double* pos, const int32_t* Z, double
                           int32_t* oj, double* odist, double* ounit) {
     Pairs p;
     const double* cell = cell_of(0);
-    if (build_pairs_cell(n, pos, Z, cutoff, cell, cell ? g_cellinv : NULL, &p)) return -1;
+    if (build_pairs_cell(n, pos, Z, cutoff, cell, cell ? g_cellinv : NULL, g_pbc, &p)) return -1;
     for (int64_t k = 0; k < p.n && k < cap; ++k) {
         oi[k] = p.i[k];
         oj[k] = p.j[k];
@@ -353,7 +383,9 @@ static int run_encoder_s(const Params* p, int32_t n, const double* pos, const in
     /* S/model.cpp:37-110 */
     const int H = p->H, K = p->K, L = p->L;
     const double* cell = cell_of(s);
-    if (build_pairs_cell(n, pos, Z, p->rc, cell, cell ? g_cellinv + 9 * s : NULL, &c->pr)) return 1;
+    if (build_pairs_cell(n, pos, Z, p->rc, cell, cell ? g_cellinv + 9 * s : NULL, g_pbc ? g_pbc + 3 * s : NULL,
+                         &c->pr))
+        return 1;
     const int64_t P = c->pr.n;
     c->n = n;
     c->Z = Z;

@@ -27,6 +27,10 @@ void lor_rng_permutation(uint64_t seed, int64_t n, int64_t* out);
  * vectors, all-zero rows block = non-periodic sample; cellinv its inverse), or
  * NULL. Minimum image; parity-unpinned extension (the reference has no cells). */
 void lor_set_cells(const double* cells, const double* cellinv);
+/* Per-axis periodicity [B][3] of the cells above (NULL: all periodic). */
+void lor_set_pbc(const uint8_t* pbc);
+/* Image range m[k] of a cell (see lamm_oracle.c; -1 = non-periodic axis). */
+void lor_image_range(const double* cellinv, const uint8_t* pbc, double cutoff, int* m);
 int lor_cell_inverse(const double* cell, double* out);
 int64_t lor_neighbor_list(int32_t n, const double* pos, const int32_t* Z, double cutoff, int64_t cap,
                           int32_t* oi, int32_t* oj, double* odist, double* ounit);

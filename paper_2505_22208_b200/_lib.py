@@ -34,7 +34,7 @@ class BatchViewC(C.Structure):
     _fields_ = [("n_samples", C.c_int32), ("n_atoms", C.c_int64), ("atom_ptr", C.c_void_p),
                 ("positions", C.c_void_p), ("atomic_numbers", C.c_void_p), ("dataset_index", C.c_void_p),
                 ("energy_mask", C.c_void_p), ("force_mask", C.c_void_p), ("energy", C.c_void_p),
-                ("forces", C.c_void_p), ("denoise", C.c_void_p), ("cell", C.c_void_p)]
+                ("forces", C.c_void_p), ("denoise", C.c_void_p), ("cell", C.c_void_p), ("pbc", C.c_void_p)]
 
 
 class RefTableC(C.Structure):

@@ -111,12 +111,15 @@ def _batch_view(b: dict):
     }
     if b.get("cell") is not None:  # periodic cells [B, 3, 3] (all-zero: non-periodic sample)
         keep["cell"] = _c(np.asarray(b["cell"]).reshape(B, 9), np.float64)
+        if b.get("pbc") is not None:  # per-axis periodicity [B, 3] (absent: all periodic)
+            keep["pbc"] = _c(np.asarray(b["pbc"]).reshape(B, 3), np.uint8)
+
     def addr(k):  # c_void_p structure fields take the integer address directly
         return keep[k].__array_interface__["data"][0]
 
     v = BatchViewC(B, int(ap[-1]), addr("atom_ptr"), addr("pos"), addr("Z"), addr("dataset_index"),
                    addr("energy_mask"), addr("force_mask"), addr("energy"), addr("forces"), addr("denoise"),
-                   addr("cell") if "cell" in keep else None)
+                   addr("cell") if "cell" in keep else None, addr("pbc") if "pbc" in keep else None)
     return v, keep
 
 
@@ -549,6 +552,8 @@ def select(batch: dict, ids) -> dict:
         out[k] = np.ascontiguousarray(batch[k][ids])
     if batch.get("cell") is not None:
         out["cell"] = np.ascontiguousarray(np.asarray(batch["cell"]).reshape(-1, 3, 3)[ids])
+        if batch.get("pbc") is not None:
+            out["pbc"] = np.ascontiguousarray(np.asarray(batch["pbc"]).reshape(-1, 3)[ids])
     return out
 
 
@@ -563,4 +568,7 @@ def concat(batches) -> dict:
     if any(b.get("cell") is not None for b in batches):  # non-periodic parts get all-zero cells
         out["cell"] = np.concatenate([np.asarray(b["cell"]).reshape(-1, 3, 3) if b.get("cell") is not None
                                       else np.zeros((len(b["atom_ptr"]) - 1, 3, 3)) for b in batches])
+        if any(b.get("pbc") is not None for b in batches):  # parts without flags: all periodic
+            out["pbc"] = np.concatenate([np.asarray(b["pbc"], np.uint8).reshape(-1, 3) if b.get("pbc") is not None
+                                         else np.ones((len(b["atom_ptr"]) - 1, 3), np.uint8) for b in batches])
     return out

@@ -782,7 +782,8 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
     }
     if (b->forces) std::memcpy(F, b->forces, 24 * N);
     else std::memset(F, 0, 24 * N);
-    if (b->cell) {  // {flag, cell, cell^-1} per sample; minimum image needs widths >= 2 rc
+    std::vector<uint8_t> brute(B, 0);  // samples swept brute force over (j, image) whatever their size
+    if (b->cell) {  // {flag, cell, cell^-1, m[3], nimg} per sample (device.cuh: kCellDoubles)
         double* cs = reinterpret_cast<double*>(base + h.off_cell);
         for (int32_t s = 0; s < B; ++s) {
             const double* m = b->cell + 9 * static_cast<int64_t>(s);
@@ -793,17 +794,29 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
             if (!periodic) continue;
             for (int k = 0; k < 9; ++k) require(std::isfinite(m[k]), "cell: non-finite entry");
             require(cell_inverse(m, o + 10), "cell: singular");
-            const double det = std::fabs((m[0] * (m[4] * m[8] - m[5] * m[7]) + m[1] * (m[5] * m[6] - m[3] * m[8])) +
-                                         m[2] * (m[3] * m[7] - m[4] * m[6]));
-            for (int k = 0; k < 3; ++k) {  // perpendicular width along lattice vector k
-                const double* u = m + 3 * ((k + 1) % 3);
-                const double* v = m + 3 * ((k + 2) % 3);
-                const double cx = u[1] * v[2] - u[2] * v[1], cy = u[2] * v[0] - u[0] * v[2], cz = u[0] * v[1] - u[1] * v[0];
-                const double width = det / std::sqrt(cx * cx + cy * cy + cz * cz);
-                require(width >= 2.0 * c.cfg.cutoff,
-                        "cell: perpendicular width below 2 * cutoff (minimum image); replicate the cell");
+            // images per axis: m_k = floor(1/2 + rc b_k (1 + 1e-9)), b_k = |column k of
+            // cell^-1| = 1 / perpendicular width k (oracle/lamm_oracle.c:lor_image_range);
+            // -1 on an open axis (pbc[k] = 0)
+            const double* ci = o + 10;
+            int nimg = 1;
+            bool multi = false;
+            for (int k = 0; k < 3; ++k) {
+                const uint8_t* pb = b->pbc ? b->pbc + 3 * static_cast<int64_t>(s) : nullptr;
+                int mk = -1;
+                if (!pb || pb[k]) {
+                    const double bk = std::sqrt((ci[k] * ci[k] + ci[3 + k] * ci[3 + k]) + ci[6 + k] * ci[6 + k]);
+                    const double mm = std::floor(0.5 + c.cfg.cutoff * bk * (1.0 + 1e-9));
+                    require(mm <= kMaxImages, "cell: far narrower than the cutoff (too many images)");
+                    mk = static_cast<int>(mm);
+                }
+                o[19 + k] = static_cast<double>(mk);
+                multi |= mk != 0;
+                nimg *= 2 * std::max(mk, 0) + 1;
+                require(nimg <= kMaxImages, "cell: more than 4096 images per pair (cell far narrower than the cutoff)");
             }
-            o[0] = 1.0;
+            o[22] = static_cast<double>(nimg);
+            o[0] = multi ? 2.0 : 1.0;
+            brute[s] = multi ? 1 : 0;
             std::memcpy(o + 1, m, sizeof(double) * 9);
         }
     }
@@ -829,7 +842,8 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
     h.lambda_f = tc ? tc->lambda_force : 1.0;
     h.workers = 1;
     h.n_large = 0;
-    for (int32_t s = 0; s < B; ++s) h.n_large += b->atom_ptr[s + 1] - b->atom_ptr[s] > kSmallAtoms ? 1 : 0;
+    for (int32_t s = 0; s < B; ++s)  // cell-list samples (k_cell_count)
+        h.n_large += (b->atom_ptr[s + 1] - b->atom_ptr[s] > kSmallAtoms && !brute[s]) ? 1 : 0;
     std::memcpy(base, &h, sizeof(StepHeader));
     // host mirror
     c.B = B, c.N = N, c.me = me, c.mf = mf;

@@ -171,11 +171,17 @@ __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Periodic cells: per sample 19 doubles {flag, cell[9] (rows = lattice vectors),
-// cell^-1[9]} in the staged blob. The minimum image uses
-//   f_k = sum_c d_c cinv[c][k] - rint(.),  d_c = sum_k f_k cell[k][c],
-// left to right, correctly rounded (oracle/lamm_oracle.c:min_image is the same).
-constexpr int kCellDoubles = 19;
+// Periodic cells: per sample 24 doubles {flag, cell[9] (rows = lattice vectors),
+// cell^-1[9], m[3], nimg, 0} in the staged blob. flag 1: every periodic width is
+// at least 2 rc (m = 0): the minimum image, cell lists above kSmallAtoms; flag 2:
+// several images per pair (m_k >= 1) or an open axis (m_k = -1): brute force over
+// (j, image). The image n of a pair uses
+//   f_k = sum_c d_c cinv[c][k];  f_k -= rint(f_k) (periodic axes);  f_k -= n_k;
+//   d_c = sum_k f_k cell[k][c]
+// left to right, correctly rounded (oracle/lamm_oracle.c:image_disp is the same;
+// n = 0 gives min_image below bit for bit).
+constexpr int kCellDoubles = 24;
+constexpr int kMaxImages = 4096;
 
 __host__ __device__ inline bool cell_inverse(const double* m, double* inv) {
     const double c00 = m[4] * m[8] - m[5] * m[7], c01 = m[5] * m[6] - m[3] * m[8], c02 = m[3] * m[7] - m[4] * m[6];
@@ -195,6 +201,29 @@ __device__ __forceinline__ void min_image(const double* cell, const double* ci, 
         const double a = __dmul_rn(d0, ci[k]), b = __dmul_rn(d1, ci[3 + k]), c = __dmul_rn(d2, ci[6 + k]);
         f[k] = __dadd_rn(__dadd_rn(a, b), c);
         f[k] = __dsub_rn(f[k], rint(f[k]));
+    }
+    double o[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const double a = __dmul_rn(f[0], cell[c]), b = __dmul_rn(f[1], cell[3 + c]), e = __dmul_rn(f[2], cell[6 + c]);
+        o[c] = __dadd_rn(__dadd_rn(a, b), e);
+    }
+    d0 = o[0], d1 = o[1], d2 = o[2];
+}
+
+// Image n = (n0, n1, n2) of a flag-2 sample (cell + 18 holds m[3]).
+__device__ __forceinline__ void image_disp(const double* cell, int n0, int n1, int n2, double& d0, double& d1,
+                                           double& d2) {
+    const double* ci = cell + 9;
+    const double* m = cell + 18;
+    const int n[3] = {n0, n1, n2};
+    double f[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double a = __dmul_rn(d0, ci[k]), b = __dmul_rn(d1, ci[3 + k]), c = __dmul_rn(d2, ci[6 + k]);
+        f[k] = __dadd_rn(__dadd_rn(a, b), c);
+        if (m[k] >= 0.0) f[k] = __dsub_rn(f[k], rint(f[k]));
+        f[k] = __dsub_rn(f[k], static_cast<double>(n[k]));
     }
     double o[3];
 #pragma unroll

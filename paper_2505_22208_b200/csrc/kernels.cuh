@@ -62,13 +62,47 @@ __device__ __forceinline__ double pair_dist(double xi, double yi, double zi, dou
     return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
 }
 
-// The sample's periodic cell in the staged blob, or nullptr.
+// The sample's periodic cell in the staged blob ({cell, cinv, m, nimg}), or nullptr.
 __device__ __forceinline__ const double* sample_cell(const Dev& d, int s) {
     const StepHeader& hd = *d.hdr;
     if (hd.off_cell == 0) return nullptr;
     const double* c = reinterpret_cast<const double*>(reinterpret_cast<const char*>(d.hdr) + hd.off_cell) +
                       static_cast<int64_t>(kCellDoubles) * s;
     return c[0] != 0.0 ? c + 1 : nullptr;
+}
+
+// Candidate images of one sample's pairs: brute-force samples sweep the flattened
+// (j, image) index c = j * nimg + img (image order lexicographic in n, the
+// reference order i-major / j ascending kept), skipping (i, i, 0). Samples of
+// more than kSmallAtoms atoms take the cell lists unless they need images.
+struct Images {
+    int nimg, w1, w2, m0, m1, m2;
+    bool multi;  // flag 2: image shifts / open axes (image_disp), else the minimum image (or none)
+};
+__device__ __forceinline__ Images sample_images(const double* cell) {
+    Images im{1, 1, 1, 0, 0, 0, false};
+    if (cell && cell[-1] == 2.0) {
+        im.multi = true;
+        im.m0 = max(0, static_cast<int>(cell[18])), im.m1 = max(0, static_cast<int>(cell[19]));
+        im.m2 = max(0, static_cast<int>(cell[20]));
+        im.w1 = 2 * im.m1 + 1, im.w2 = 2 * im.m2 + 1;
+        im.nimg = (2 * im.m0 + 1) * im.w1 * im.w2;
+    }
+    return im;
+}
+__device__ __forceinline__ bool sample_brute(const double* cell, int n) {
+    return n <= kSmallAtoms || (cell && cell[-1] == 2.0);
+}
+// Candidate c of a brute-force sweep: source atom offset jl, its image test.
+__device__ __forceinline__ double pair_dist_c(const Images& im, const double* cell, double xi, double yi, double zi,
+                                              double xj, double yj, double zj, int img, double& dx, double& dy,
+                                              double& dz) {
+    if (!im.multi) return pair_dist(xi, yi, zi, xj, yj, zj, dx, dy, dz, cell);
+    dx = __dsub_rn(xi, xj);
+    dy = __dsub_rn(yi, yj);
+    dz = __dsub_rn(zi, zj);
+    image_disp(cell, img / (im.w1 * im.w2) - im.m0, (img / im.w2) % im.w1 - im.m1, img % im.w2 - im.m2, dx, dy, dz);
+    return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
 }
 
 
@@ -479,24 +513,33 @@ __global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) 
         }
         __syncthreads();
         const double* cell = sample_cell(d, s);
-        if (hi - lo > kSmallAtoms) {  // counted over its cell list by k_cell_count
+        const int n = static_cast<int>(hi - lo);
+        if (!sample_brute(cell, n)) {  // counted over its cell list by k_cell_count
             bin_sample(d, s, lo, hi, cell, bmn, bmx);
             __syncthreads();
             continue;
         }
-        // neighbour counts of the sample (S/core.cpp:30-48), warp per atom, from the
-        // positions this block just staged in shared memory (visible after the barrier)
+        // neighbour counts of the sample (S/core.cpp:30-48), warp per atom over the
+        // (j, image) candidates, from the positions this block just staged in shared
+        // memory (samples of more than kSmallAtoms atoms that need images: from
+        // global memory, written by this block; visible after the barrier)
         const int lane = threadIdx.x & 31;
-        const int n = static_cast<int>(hi - lo);
+        const Images im = sample_images(cell);
+        const int ncand = n * im.nimg, self = (im.nimg - 1) / 2;
+        const bool smem = n <= kSmallAtoms;
         for (int il = threadIdx.x >> 5; il < n; il += blockDim.x >> 5) {
-            const double xi = sp[0][il], yi = sp[1][il], zi = sp[2][il];
+            const double xi = smem ? sp[0][il] : d.x[lo + il], yi = smem ? sp[1][il] : d.y[lo + il],
+                         zi = smem ? sp[2][il] : d.z[lo + il];
             int cnt = 0;
-            for (int j0 = 0; j0 < n; j0 += 32) {
-                const int jl = j0 + lane;
+            for (int c0 = 0; c0 < ncand; c0 += 32) {
+                const int c = c0 + lane;
+                const int jl = im.nimg == 1 ? c : c / im.nimg, img = im.nimg == 1 ? 0 : c - jl * im.nimg;
                 bool in = false;
-                if (jl < n && jl != il) {
+                if (c < ncand && (jl != il || img != self)) {
                     double dx, dy, dz;
-                    in = pair_dist(xi, yi, zi, sp[0][jl], sp[1][jl], sp[2][jl], dx, dy, dz, cell) < d.rc;
+                    const double xj = smem ? sp[0][jl] : d.x[lo + jl], yj = smem ? sp[1][jl] : d.y[lo + jl],
+                                 zj = smem ? sp[2][jl] : d.z[lo + jl];
+                    in = pair_dist_c(im, cell, xi, yi, zi, xj, yj, zj, img, dx, dy, dz) < d.rc;
                 }
                 cnt += __popc(__ballot_sync(0xffffffffu, in));
             }
@@ -542,9 +585,9 @@ __global__ void __launch_bounds__(256) k_cell_count(Dev d, int Q) {
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
         const int s = d.sample_of[i];
         const int lo = static_cast<int>(d.atom_ptr[s]), hi = static_cast<int>(d.atom_ptr[s + 1]);
-        if (hi - lo <= kSmallAtoms) continue;
-        const CellGrid g = d.cgrid[s];
         const double* cell = sample_cell(d, s);
+        if (sample_brute(cell, hi - lo)) continue;
+        const CellGrid g = d.cgrid[s];
         const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
         int cnt = 0;
         // samples of <= 1024 atoms (one window of k_nbr_fill): the hits as a bitmask over
@@ -688,13 +731,17 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d, int Q) {
                     for (int64_t q = ((static_cast<int64_t>(base) + 1) * Q + P - 1) / P; q < Q; ++q) d.part_lo[q] = N;
             }
         }
-        if (hi - lo <= kSmallAtoms) {
-            for (int j0 = lo; j0 < hi; j0 += 32) {
-                const int j = j0 + lane;
+        if (sample_brute(cell, hi - lo)) {
+            const Images im = sample_images(cell);
+            const int ncand = (hi - lo) * im.nimg, self = (im.nimg - 1) / 2, il = i - lo;
+            for (int c0 = 0; c0 < ncand; c0 += 32) {
+                const int c = c0 + lane;
+                const int jl = im.nimg == 1 ? c : c / im.nimg, img = im.nimg == 1 ? 0 : c - jl * im.nimg;
+                const int j = lo + jl;
                 bool in = false;
                 double dx = 0, dy = 0, dz = 0, r = 0;
-                if (j < hi && j != i) {
-                    r = pair_dist(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz, cell);
+                if (c < ncand && (jl != il || img != self)) {
+                    r = pair_dist_c(im, cell, xi, yi, zi, d.x[j], d.y[j], d.z[j], img, dx, dy, dz);
                     in = r < d.rc;
                 }
                 const unsigned mask = __ballot_sync(0xffffffffu, in);
