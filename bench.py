@@ -345,6 +345,8 @@ def run_ours(args, dist):
         out["rank_imbalance_heavy_tail"] = rank_imbalance_heavy(pk, dev, tc)
         out["periodic_cfg1"] = periodic_cfg1(pk, mcfg, tc)
         out["semisup_cfg3"] = semisup_cfg3(pk, mcfg, tc)
+        out["semisup_cfg3_periodic"] = semisup_cfg3(pk, mcfg, tc, periodic=True)
+        out["cost_balancing"] = cost_balancing(pk, mcfg, tc)
         out["supercells_cfg4"] = supercells_cfg4(pk, mcfg, tc)
     if dist.rank == 0 and dist.world == 1 and not args.no_large:
         out["roofline_large"] = roofline_large(pk, mcfg, tc)
@@ -571,6 +573,80 @@ def rank_imbalance_heavy(pk, dev, tc, G=8, B=4, S=64, steps=8):
     return out
 
 
+def pair_counts(pk, dev, pool, chunk=512):
+    """Directed pair count per sample, from the device neighbour list (bit-exact
+    with the reference's build_neighbor_list), chunk samples at a time."""
+    B = len(pool["atom_ptr"]) - 1
+    out = np.zeros(B, np.int64)
+    for s0 in range(0, B, chunk):
+        sub = pk.select(pool, np.arange(s0, min(B, s0 + chunk)))
+        dev.set_batch(sub)
+        ptr = dev.build_neighbor_list(fp64=False)[0]
+        out[s0:s0 + len(ptr) - 1] = np.diff(ptr)
+    return out
+
+
+def cost_balancing(pk, mcfg, tc, G=8, B=48, steps=6):
+    """North star: "assigns samples to ranks by predicted atom/edge cost". A mixed
+    pool where atoms alone mispredict the work: cfg2-like molecules (~17 pairs per
+    atom), periodic crystals (~40, with images) and Si supercells (28). (1) the
+    reference's atom-balanced plan, every rank slice timed; (2) the step-time model
+    t = t0 + per_atom * atoms + per_edge * edges fitted to those times
+    (pk.fit_cost_model); (3) a fresh schedule seed planned by atoms and by the
+    fitted cost (lamm_plan_cost), both timed: max/mean per-rank time per step."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import cases
+    rng = np.random.default_rng(17)
+    mol = pk.synth_generate(2400, 31, threads=os.cpu_count() or 8, mode=30.0, sigma=0.6, min_atoms=5, max_atoms=200,
+                            elements=(1, 6, 7, 8))
+    mol["denoise"] = np.zeros(len(mol["atom_ptr"]) - 1, np.uint8)
+    cry = crystal_pool(pk, 1000, 33, "energy_and_forces", 40.0, sigma=0.6)
+    sc = []
+    for k in range(200):
+        pos, Z, cell = cases.diamond_supercell(reps=tuple(rng.integers(2, 4, 3)), seed=3000 + k)
+        n = len(Z)
+        sc.append(dict(atom_ptr=np.array([0, n], np.int64), pos=pos, Z=Z, forces=rng.normal(0, 0.1, (n, 3)),
+                       dataset_index=np.zeros(1, np.int32), energy_mask=np.ones(1, np.uint8),
+                       force_mask=np.ones(1, np.uint8), energy=np.array([-4.6 * n]), denoise=np.zeros(1, np.uint8),
+                       cell=cell[None]))
+    pool = pk.concat([mol, cry] + sc)
+    pool = pk.select(pool, rng.permutation(len(pool["atom_ptr"]) - 1))
+    atoms = np.diff(pool["atom_ptr"])
+    dev = pk.Device(mcfg, seed=7)
+    edges = pair_counts(pk, dev, pool)
+    dev.set_option("rank_local", 1)
+    dev.set_reference_table(fit_table(mol, CFG["heads"]))
+
+    def timed(sched):
+        rows = time_rank_slices(pk, dev, pool, sched, G, B, tc, steps, slot0=900)
+        per = G * B
+        a, e, t, r = [], [], [], []
+        for s, (ra, rt) in enumerate(rows):
+            ids = sched["sample"][s * per:(s + 1) * per]
+            re = [int(edges[ids[g * B:(g + 1) * B]].sum()) for g in range(G)]
+            a += ra.tolist()
+            e += re
+            t += rt.tolist()
+            r.append(rt.max() / rt.mean())
+        return a, e, t, r
+
+    fa, fe, ft, fr = timed(pk.plan(atoms, G, B, 8, seed=5, mode="balanced"))
+    cm, t0, r2 = pk.fit_cost_model(fa, fe, ft)
+    _, _, _, ra = timed(pk.plan(atoms, G, B, 8, seed=6, mode="balanced"))
+    pc = pk.plan_cost(atoms, edges, cm, G, B, 8, seed=6, mode="balanced")
+    _, _, _, rc = timed(pc)
+    return {"pool": "2400 molecules (5-200 atoms) + 1000 periodic crystals (8-200) + 200 Si supercells (64-216), "
+                    "shuffled", "G": G, "batch_per_rank": B, "pool_atoms_mean": float(atoms.mean()),
+            "pool_edges_per_atom": float(edges.sum() / atoms.sum()),
+            "fit": {"t0_ms": t0, "per_atom_us": cm.per_atom * 1e3, "per_edge_us": cm.per_edge * 1e3, "r2": r2,
+                    "on": f"{len(ft)} rank steps of the atom-balanced plan, schedule seed 5"},
+            "atoms_balanced": {"time_imbalance_mean": float(np.mean(ra)), "time_imbalance_p95": float(np.percentile(ra, 95)),
+                               "steps": len(ra)},
+            "cost_balanced": {"time_imbalance_mean": float(np.mean(rc)), "time_imbalance_p95": float(np.percentile(rc, 95)),
+                              "predicted_cost_imbalance_mean": pc["cost_imbalance_mean"], "steps": len(rc)},
+            "evaluated_on": "schedule seed 6 (not the fit's)"}
+
+
 def time_rank_slices(pk, dev, pool, sched, G, B, tc, steps, slot0=970):
     """Per scheduled mini-batch, each of the G ranks' B-sample slices staged and
     timed as its own device step on this GPU (min of 3, CUDA events on the ctx
@@ -721,7 +797,36 @@ def roofline_large(pk, mcfg, tc, steps=5):
             "kernels": kern}
 
 
-def semisup_cfg3(pk, mcfg, tc, G=8, B=32, steps=6):
+def crystal_pool(pk, count, seed, task, mode, sigma=0.5, lo=8, hi=200, dataset_index=0):
+    """Periodic crystals for the literal cfg3: n ~ lognormal(mode, sigma) clamped to
+    [lo, hi] atoms on randomly chosen sites of a k^3 simple-cubic grid (k^3 >= n,
+    spacing 2.3 A, 0.08 A jitter) in a sheared cell of k * 2.3 A: small crystals
+    (4.6-9.2 A cells) need several images per pair, large ones take the minimum
+    image and cell lists. Elements Si/O; Morse-like random labels (parity only needs
+    them finite); task as the reference's subset tasks."""
+    rng = np.random.default_rng(seed)
+    mu = np.log(mode) + sigma * sigma
+    parts = []
+    for _ in range(count):
+        n = int(np.clip(np.rint(rng.lognormal(mu, sigma)), lo, hi))
+        k = int(np.ceil(n ** (1 / 3) - 1e-9))
+        a = 2.3
+        sites = rng.choice(k ** 3, n, replace=False)
+        grid = np.stack(np.unravel_index(sites, (k, k, k)), 1).astype(float)
+        cell = np.eye(3) * k * a
+        cell[1, 0] = rng.uniform(-0.2, 0.2) * k * a  # shear: triclinic
+        pos = (grid + 0.25) / k @ cell + rng.normal(0, 0.08, (n, 3))
+        Z = rng.choice(np.array([8, 14], np.int32), n)
+        parts.append(dict(atom_ptr=np.array([0, n], np.int64), pos=pos, Z=Z, forces=rng.normal(0, 0.3, (n, 3)),
+                          dataset_index=np.array([dataset_index], np.int32),
+                          energy_mask=np.array([task != "denoising"], np.uint8),
+                          force_mask=np.array([task == "energy_and_forces"], np.uint8),
+                          energy=np.array([-5.0 * n + rng.normal()]),
+                          denoise=np.array([task == "denoising"], np.uint8), cell=cell[None]))
+    return pk.concat(parts)
+
+
+def semisup_cfg3(pk, mcfg, tc, G=8, B=32, steps=6, periodic=False):
     """BASELINE configs[2] (non-periodic twin): three subsets of
     reference-generator structures clamped to 8-200 atoms — E+F labeled (mode 15),
     energy-only (mode 60), coordinate-denoising (mode 30, sigma 0.3 A, centered) —
@@ -731,8 +836,11 @@ def semisup_cfg3(pk, mcfg, tc, G=8, B=32, steps=6):
     subs = []
     for k, (task, mode, n) in enumerate((("energy_and_forces", 15.0, 3000), ("energy_only", 60.0, 600),
                                          ("denoising", 30.0, 1500))):
-        b = pk.synth_generate(n, 21 + k, task=task, mode=mode, sigma=0.5, min_atoms=8, max_atoms=200,
-                              elements=(1, 6, 7, 8), threads=os.cpu_count() or 8, dataset_index=k)
+        if periodic:
+            b = crystal_pool(pk, n, 21 + k, task, mode, dataset_index=k)
+        else:
+            b = pk.synth_generate(n, 21 + k, task=task, mode=mode, sigma=0.5, min_atoms=8, max_atoms=200,
+                                  elements=(1, 6, 7, 8), threads=os.cpu_count() or 8, dataset_index=k)
         subs.append(b)
     sizes = [len(b["atom_ptr"]) - 1 for b in subs]
     rep = pk.temperature_counts(sizes, 2.0)
@@ -752,8 +860,10 @@ def semisup_cfg3(pk, mcfg, tc, G=8, B=32, steps=6):
     dev = pk.Device(mcfg, seed=7)
     dev.set_option("rank_local", 1)
     dev.set_reference_table(table)
-    out = {"workload": "cfg3: E+F / energy-only / denoising subsets (8-200 atoms, non-periodic twin), "
-                       "T = 2 mix, G = 8, B = 32",
+    out = {"workload": ("cfg3: E+F / energy-only / denoising subsets of periodic crystals (8-200 atoms; "
+                        "cells of 4.6-14 A: image pairs below 2 rc, minimum image above)" if periodic else
+                        "cfg3: E+F / energy-only / denoising subsets (8-200 atoms, non-periodic twin)") +
+                       ", T = 2 mix, G = 8, B = 32",
            "epoch_samples": int(len(ids)), "subset_share": [float(np.mean(osub == k)) for k in range(3)],
            "pool_atoms_mean": float(atoms.mean())}
     for mode in ("balanced", "naive"):
@@ -809,6 +919,7 @@ def main():
     ap.add_argument("--no-imbalance", action="store_true")
     ap.add_argument("--no-large", action="store_true", help="skip the larger-than-L2 roofline section")
     ap.add_argument("--only-large", action="store_true", help="run only the larger-than-L2 roofline section")
+    ap.add_argument("--only-cost", action="store_true", help="run only the cost-model balancing section")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -820,6 +931,10 @@ def main():
         assert "paper_2505_22208_b200" not in sys.modules, "the reference arm imported the product"
         out["product_imported"] = False
         print(json.dumps(out), flush=True)
+        return
+    if args.only_cost:
+        import paper_2505_22208_b200 as pk
+        print(json.dumps(cost_balancing(pk, pk.ModelConfig(**CFG), pk.TrainConfig(seed=11))), flush=True)
         return
     if args.only_large:
         import paper_2505_22208_b200 as pk

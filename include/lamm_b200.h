@@ -315,6 +315,29 @@ int lamm_greedy_assign(const int64_t* atoms, int64_t n, int32_t workers, int32_t
 int lamm_plan(const int64_t* atoms, int64_t n, int32_t workers, int32_t batch_per_worker, int32_t num_splits,
               uint64_t seed, int32_t mode, int64_t* sample, int32_t* worker, int64_t* atoms_out, int64_t* split,
               int64_t* chunk_rank, int64_t* worker_atoms, int64_t* n_batches, int64_t* dropped);
+/* Cost-model balancing (north_star "predicted atom/edge cost"; the reference
+ * balances on atoms only, S/scheduler.cpp:62-158, and keeps a cost model only in
+ * its simulator, H/simulator.hpp:22-27). Predicted per-sample cost
+ *   cost = (per_sample + per_atom * atoms) + per_edge * edges
+ * (edges: the sample's directed pair count, e.g. from lamm_neighbor_list_copy). */
+typedef struct {
+    double per_sample;
+    double per_atom;
+    double per_edge;
+} lamm_cost_model;
+/* cost[n] of each sample (edges nullable when per_edge == 0); LAMM_EINPUT on a
+ * non-positive or non-finite cost. */
+int lamm_sample_cost(const int64_t* atoms, const int64_t* edges, int64_t n, const lamm_cost_model* model,
+                     double* cost);
+/* lamm_plan with the balancing key = the predicted cost instead of the atom count:
+ * the same shuffle, splits sorted by key, transpose chunk stream and greedy
+ * least-loaded assignment (S/scheduler.cpp:91-158). With {0, 1, 0} it is
+ * lamm_plan bit for bit. worker_cost [n_batches][workers] (nullable): predicted
+ * per-worker cost of every mini-batch; the other outputs as lamm_plan. */
+int lamm_plan_cost(const int64_t* atoms, const int64_t* edges, int64_t n, const lamm_cost_model* model,
+                   int32_t workers, int32_t batch_per_worker, int32_t num_splits, uint64_t seed, int32_t mode,
+                   int64_t* sample, int32_t* worker, int64_t* atoms_out, int64_t* split, int64_t* chunk_rank,
+                   int64_t* worker_atoms, double* worker_cost, int64_t* n_batches, int64_t* dropped);
 /* lamm::scheduler::schedule_metrics (S/scheduler.cpp:205-251). */
 int lamm_schedule_metrics(int64_t n_batches, int32_t workers, int32_t batch_per_worker, const int32_t* worker,
                           const int64_t* atoms, const int64_t* split, const int64_t* chunk_rank,

@@ -37,6 +37,10 @@ class BatchViewC(C.Structure):
                 ("forces", C.c_void_p), ("denoise", C.c_void_p), ("cell", C.c_void_p), ("pbc", C.c_void_p)]
 
 
+class CostModelC(C.Structure):
+    _fields_ = [("per_sample", C.c_double), ("per_atom", C.c_double), ("per_edge", C.c_double)]
+
+
 class RefTableC(C.Structure):
     _fields_ = [("n_tables", C.c_int32), ("rho", C.c_void_p), ("rho_has", C.c_void_p),
                 ("energy_mean", C.c_void_p), ("energy_std", C.c_void_p), ("force_std", C.c_void_p),
@@ -85,6 +89,7 @@ EXPORTS = [
     "lamm_flush_l2", "lamm_step_times", "lamm_evaluate", "lamm_cell_inverse",
     "lamm_checkpoint_save", "lamm_checkpoint_load", "lamm_rms_state_save", "lamm_rms_state_load",
     "lamm_subset_info", "lamm_subset_read", "lamm_train_step_workers", "lamm_ctx_get_info",
+    "lamm_sample_cost", "lamm_plan_cost",
 ]
 
 _lib = None

@@ -26,7 +26,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import (BatchViewC, EvalResultC, InputError, LossBreakdownC, LossConfigC, ModelConfigC, NonFiniteError,  # noqa: F401
+from ._lib import (BatchViewC, CostModelC, EvalResultC, InputError, LossBreakdownC, LossConfigC, ModelConfigC, NonFiniteError,  # noqa: F401
                    RefTableC, StepResultC, TrainConfigC, check, lib)
 
 
@@ -468,6 +468,79 @@ def plan(atoms, workers: int, batch_per_worker: int, num_splits: int = 100, seed
     out.update(n_batches=nb, dropped=dr, max_imbalance=mx.value, mean_imbalance=mean.value,
                monotonicity_violations=mono.value, growth_events=grow.value)
     return out
+
+
+@dataclass
+class CostModel:
+    """Predicted per-sample step cost (lamm_cost_model): (per_sample + per_atom *
+    atoms) + per_edge * edges. CostModel(0, 1, 0) is the reference's atom count."""
+    per_sample: float = 0.0
+    per_atom: float = 1.0
+    per_edge: float = 0.0
+
+    def c(self):
+        return CostModelC(self.per_sample, self.per_atom, self.per_edge)
+
+
+def sample_cost(atoms, edges, model: CostModel) -> np.ndarray:
+    a = _c(atoms, np.int64)
+    e = None if edges is None else _c(edges, np.int64)
+    out = np.empty(len(a), np.float64)
+    cm = model.c()
+    check(lib().lamm_sample_cost(_p(a), _p(e) if e is not None else None, C.c_int64(len(a)), C.byref(cm), _p(out)))
+    return out
+
+
+def plan_cost(atoms, edges, model: CostModel, workers: int, batch_per_worker: int, num_splits: int = 100,
+              seed: int = 0, mode: str = "balanced") -> dict:
+    """lamm_plan_cost: the reference's plan with the predicted cost as the balancing
+    key (north_star "predicted atom/edge cost"); adds worker_cost [n_batches][G]."""
+    a = _c(atoms, np.int64)
+    e = None if edges is None else _c(edges, np.int64)
+    n = len(a)
+    cap = max(n, 1)
+    out = dict(sample=np.empty(cap, np.int64), worker=np.empty(cap, np.int32), atoms=np.empty(cap, np.int64),
+               split=np.empty(cap, np.int64), chunk_rank=np.empty(cap, np.int64),
+               worker_atoms=np.empty(cap, np.int64), worker_cost=np.empty(cap, np.float64))
+    nb, dr = C.c_int64(), C.c_int64()
+    cm = model.c()
+    check(lib().lamm_plan_cost(_p(a), _p(e) if e is not None else None, C.c_int64(n), C.byref(cm), workers,
+                               batch_per_worker, num_splits, C.c_uint64(seed), MODES[mode], _p(out["sample"]),
+                               _p(out["worker"]), _p(out["atoms"]), _p(out["split"]), _p(out["chunk_rank"]),
+                               _p(out["worker_atoms"]), _p(out["worker_cost"]), C.byref(nb), C.byref(dr)))
+    nb, dr = nb.value, dr.value
+    tot = nb * workers * batch_per_worker
+    for k in ("sample", "worker", "atoms", "split", "chunk_rank"):
+        out[k] = out[k][:tot]
+    out["worker_atoms"] = out["worker_atoms"][:nb * workers]
+    out["worker_cost"] = out["worker_cost"][:nb * workers]
+    wc = out["worker_cost"].reshape(nb, workers) if nb else np.ones((1, workers))
+    out.update(n_batches=nb, dropped=dr,
+               cost_imbalance_mean=float(np.mean(wc.max(1) / wc.mean(1))) if nb else 1.0)
+    return out
+
+
+def fit_cost_model(atoms, edges, times, samples=None) -> tuple:
+    """Non-negative least-squares step-time model t = t0 + per_atom * atoms +
+    per_edge * edges (+ per_sample * samples when given) over measured per-rank steps; returns
+    (CostModel, t0, r2). t0 (the per-step fixed cost) is the same on every rank and
+    does not enter the balancing."""
+    cols = [np.ones(len(times)), np.asarray(atoms, float), np.asarray(edges, float)]
+    if samples is not None:
+        cols.append(np.asarray(samples, float))
+    A = np.stack(cols, 1)
+    y = np.asarray(times, float)
+    # non-negative least squares (a cost cannot fall with atoms or edges; atoms and
+    # edges are strongly correlated, so an unconstrained fit can trade them off)
+    from scipy.optimize import nnls
+    scale = np.maximum(np.abs(A).max(0), 1e-300)
+    coef, _ = nnls(A / scale, y)
+    coef = coef / scale
+    pred = A @ coef
+    r2 = 1.0 - float(np.sum((y - pred) ** 2) / max(np.sum((y - y.mean()) ** 2), 1e-300))
+    cm = CostModel(per_sample=float(coef[3]) if samples is not None else 0.0, per_atom=float(coef[1]),
+                   per_edge=float(coef[2]))
+    return cm, float(coef[0]), r2
 
 
 TRACE_KINDS = {"constant": 0, "uniform": 1, "lognormal": 2, "bimodal": 3}

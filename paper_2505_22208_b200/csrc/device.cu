@@ -782,7 +782,6 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
     }
     if (b->forces) std::memcpy(F, b->forces, 24 * N);
     else std::memset(F, 0, 24 * N);
-    std::vector<uint8_t> brute(B, 0);  // samples swept brute force over (j, image) whatever their size
     if (b->cell) {  // {flag, cell, cell^-1, m[3], nimg} per sample (device.cuh: kCellDoubles)
         double* cs = reinterpret_cast<double*>(base + h.off_cell);
         for (int32_t s = 0; s < B; ++s) {
@@ -816,7 +815,6 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
             }
             o[22] = static_cast<double>(nimg);
             o[0] = multi ? 2.0 : 1.0;
-            brute[s] = multi ? 1 : 0;
             std::memcpy(o + 1, m, sizeof(double) * 9);
         }
     }
@@ -842,8 +840,12 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
     h.lambda_f = tc ? tc->lambda_force : 1.0;
     h.workers = 1;
     h.n_large = 0;
-    for (int32_t s = 0; s < B; ++s)  // cell-list samples (k_cell_count)
-        h.n_large += (b->atom_ptr[s + 1] - b->atom_ptr[s] > kSmallAtoms && !brute[s]) ? 1 : 0;
+    for (int32_t s = 0; s < B; ++s) {  // samples counted by k_cell_count: all but the small non-periodic ones
+        bool periodic = false;
+        if (b->cell)
+            for (int k = 0; k < 9; ++k) periodic |= b->cell[9 * static_cast<int64_t>(s) + k] != 0.0;
+        h.n_large += (b->atom_ptr[s + 1] - b->atom_ptr[s] > kSmallAtoms || periodic) ? 1 : 0;
+    }
     std::memcpy(base, &h, sizeof(StepHeader));
     // host mirror
     c.B = B, c.N = N, c.me = me, c.mf = mf;

@@ -56,7 +56,7 @@ struct StepHeader {
     int32_t B, N, P, overflow;   // P written by k_prep; overflow if P > capacity
     int32_t me, mf;              // this rank's sum m_E, sum m_F (after denoise relabelling)
     int32_t nslots, status;      // distinct atomic numbers; non-finite flag
-    int32_t workers, n_large;    // n_large: samples above kSmallAtoms (cell-list neighbour search)
+    int32_t workers, n_large;    // n_large: samples k_cell_count counts (above kSmallAtoms or periodic)
     int32_t chain, pad2;         // chain: submitted by lamm_train_step_submit (in-flight poison applies)
     double lambda_e, lambda_f;
     double loss_energy, loss_force, loss_total;  // this rank's Eq. (5) breakdown
@@ -211,27 +211,31 @@ __device__ __forceinline__ void min_image(const double* cell, const double* ci, 
     d0 = o[0], d1 = o[1], d2 = o[2];
 }
 
-// Image n = (n0, n1, n2) of a flag-2 sample (cell + 18 holds m[3]).
-__device__ __forceinline__ void image_disp(const double* cell, int n0, int n1, int n2, double& d0, double& d1,
-                                           double& d2) {
+// Images of a flag-2 sample (cell + 18 holds m[3]) in two parts: the pair's
+// fractional minimum-image displacement (once per (i, j)), then image n of it
+// with the rounded squared distance (once per image).
+__device__ __forceinline__ void image_frac(const double* cell, double d0, double d1, double d2, double (&f)[3]) {
     const double* ci = cell + 9;
     const double* m = cell + 18;
-    const int n[3] = {n0, n1, n2};
-    double f[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const double a = __dmul_rn(d0, ci[k]), b = __dmul_rn(d1, ci[3 + k]), c = __dmul_rn(d2, ci[6 + k]);
         f[k] = __dadd_rn(__dadd_rn(a, b), c);
         if (m[k] >= 0.0) f[k] = __dsub_rn(f[k], rint(f[k]));
-        f[k] = __dsub_rn(f[k], static_cast<double>(n[k]));
     }
+}
+__device__ __forceinline__ double image_sq(const double* cell, const double (&f)[3], int n0, int n1, int n2,
+                                           double& d0, double& d1, double& d2) {
+    const double g0 = __dsub_rn(f[0], static_cast<double>(n0)), g1 = __dsub_rn(f[1], static_cast<double>(n1)),
+                 g2 = __dsub_rn(f[2], static_cast<double>(n2));
     double o[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        const double a = __dmul_rn(f[0], cell[c]), b = __dmul_rn(f[1], cell[3 + c]), e = __dmul_rn(f[2], cell[6 + c]);
+        const double a = __dmul_rn(g0, cell[c]), b = __dmul_rn(g1, cell[3 + c]), e = __dmul_rn(g2, cell[6 + c]);
         o[c] = __dadd_rn(__dadd_rn(a, b), e);
     }
     d0 = o[0], d1 = o[1], d2 = o[2];
+    return __dadd_rn(__dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1)), __dmul_rn(d2, d2));
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

@@ -33,22 +33,24 @@ struct Slot {
 };
 
 // Worker for each of the G*B entries of one mini-batch: entries visited by
-// descending atom count (ties by position: a stable sort), each given to the
+// descending key (ties by position: a stable sort), each given to the
 // least-loaded worker that still has room; load ties go to the lower worker.
-void balance_minibatch(const std::int64_t* atoms, std::int64_t count, int G, int B, std::int32_t* worker) {
+// Key = the atom count (the reference's balancer) or a predicted cost (double).
+template <class Key>
+void balance_minibatch(const Key* key, std::int64_t count, int G, int B, std::int32_t* worker) {
     std::vector<std::int64_t> order(static_cast<std::size_t>(count));
     std::iota(order.begin(), order.end(), 0);
     std::sort(order.begin(), order.end(), [&](std::int64_t a, std::int64_t b) {
-        return atoms[a] != atoms[b] ? atoms[a] > atoms[b] : a < b;
+        return key[a] != key[b] ? key[a] > key[b] : a < b;
     });
-    std::vector<std::int64_t> load(static_cast<std::size_t>(G), 0);
+    std::vector<Key> load(static_cast<std::size_t>(G), Key(0));
     std::vector<int> filled(static_cast<std::size_t>(G), 0);
     for (const std::int64_t e : order) {
         int pick = -1;
         for (int g = 0; g < G; ++g)
             if (filled[g] < B && (pick < 0 || load[g] < load[pick])) pick = g;
         worker[e] = pick;
-        load[pick] += atoms[e];
+        load[pick] += key[e];
         ++filled[pick];
     }
 }
@@ -60,6 +62,8 @@ struct PlanOut {
     std::int64_t* split;
     std::int64_t* chunk_rank;
     std::int64_t* worker_atoms;
+    double* worker_cost = nullptr;  // cost plans: predicted per-worker cost [batch][G] (nullable)
+    const double* cost = nullptr;
     std::int64_t written = 0;
     std::int64_t batches = 0;
 };
@@ -68,8 +72,10 @@ struct PlanOut {
 // preserved inside each worker.
 void emit_minibatch(const std::vector<Slot>& mb, const std::vector<std::int32_t>& assign, int G, PlanOut& out) {
     std::int64_t* wa = out.worker_atoms + out.batches * G;
+    double* wc = out.worker_cost ? out.worker_cost + out.batches * G : nullptr;
     for (int g = 0; g < G; ++g) {
         wa[g] = 0;
+        if (wc) wc[g] = 0.0;
         for (std::size_t e = 0; e < mb.size(); ++e) {
             if (assign[e] != g) continue;
             const std::int64_t w = out.written++;
@@ -79,6 +85,7 @@ void emit_minibatch(const std::vector<Slot>& mb, const std::vector<std::int32_t>
             out.split[w] = mb[e].split;
             out.chunk_rank[w] = mb[e].chunk_rank;
             wa[g] += mb[e].atoms;
+            if (wc) wc[g] += out.cost[mb[e].sample];
         }
     }
     ++out.batches;
@@ -121,77 +128,117 @@ LAMM_API int lamm_greedy_assign(const int64_t* atoms, int64_t n, int32_t workers
     });
 }
 
+namespace lamm_b200 {
+namespace {
+// plan() of S/scheduler.cpp:91-203 with the balancing key `key` (atoms: the
+// reference's plan, bit-exact; a predicted per-sample cost: the cost plan).
+template <class Key>
+void plan_impl(const Key* key, const int64_t* atoms, int64_t n, int32_t G, int32_t B, int32_t S, uint64_t seed,
+               int32_t mode, PlanOut& out, int64_t* n_batches, int64_t* dropped) {
+    require(G >= 1, "schedule: workers must be >= 1");
+    require(B >= 1, "schedule: batch_per_worker must be >= 1");
+    require(S >= 1, "schedule: num_splits must be >= 1");
+    require(mode >= 0 && mode <= 2, "schedule: unknown mode");
+    for (int64_t k = 0; k < n; ++k) require(atoms[k] >= 1, "schedule: atom counts must be >= 1");
+    const int64_t per_batch = static_cast<int64_t>(G) * B;
+    const auto ids = shuffled_ids(n, seed);
+    std::vector<Slot> mb;
+    std::vector<Key> mb_key(static_cast<std::size_t>(per_batch));
+    std::vector<std::int32_t> assign(static_cast<std::size_t>(per_batch));
+    int64_t lost = 0;
+    auto flush = [&] {
+        for (std::size_t e = 0; e < mb.size(); ++e) mb_key[e] = key[mb[e].sample];
+        if (mode == 2) {
+            for (int64_t e = 0; e < per_batch; ++e) assign[static_cast<std::size_t>(e)] = static_cast<int32_t>(e / B);
+        } else {
+            balance_minibatch(mb_key.data(), per_batch, G, B, assign.data());
+        }
+        emit_minibatch(mb, assign, G, out);
+        mb.clear();
+    };
+    if (mode == 0) {
+        // (1) near-equal contiguous splits of the shuffled ids, each sorted
+        //     by key descending (ties: lower id first).
+        std::vector<int64_t> bounds(static_cast<std::size_t>(S) + 1, 0);
+        for (int64_t s = 0; s < S; ++s) bounds[s + 1] = bounds[s] + n / S + (s < n % S ? 1 : 0);
+        std::vector<std::int64_t> sorted = ids;
+        int64_t ranks_max = 0;
+        for (int64_t s = 0; s < S; ++s) {
+            std::sort(sorted.begin() + bounds[s], sorted.begin() + bounds[s + 1], [&](std::int64_t a, std::int64_t b) {
+                return key[a] != key[b] ? key[a] > key[b] : a < b;
+            });
+            const int64_t len = bounds[s + 1] - bounds[s];
+            lost += len % G;
+            ranks_max = std::max<int64_t>(ranks_max, len / G);
+        }
+        // (2) G-sized chunks consumed in transpose order (rank-major over
+        // splits); (3) every B consecutive chunks form one mini-batch.
+        for (int64_t r = 0; r < ranks_max; ++r)
+            for (int64_t s = 0; s < S; ++s) {
+                if ((r + 1) * G > bounds[s + 1] - bounds[s]) continue;
+                for (int64_t k = r * G; k < (r + 1) * G; ++k) {
+                    const std::int64_t id = sorted[static_cast<std::size_t>(bounds[s] + k)];
+                    mb.push_back({id, atoms[id], s, r});
+                }
+                if (static_cast<int64_t>(mb.size()) == per_batch) flush();
+            }
+        lost += static_cast<int64_t>(mb.size());
+        mb.clear();
+    } else {
+        const int64_t full = n / per_batch;
+        lost = n - full * per_batch;
+        for (int64_t b = 0; b < full; ++b) {
+            for (int64_t e = 0; e < per_batch; ++e) {
+                const std::int64_t id = ids[static_cast<std::size_t>(b * per_batch + e)];
+                mb.push_back({id, atoms[id], 0, (b * per_batch + e) / G});
+            }
+            flush();
+        }
+    }
+    *n_batches = out.batches;
+    *dropped = lost;
+}
+}  // namespace
+}  // namespace lamm_b200
+
 LAMM_API int lamm_plan(const int64_t* atoms, int64_t n, int32_t G, int32_t B, int32_t S, uint64_t seed, int32_t mode,
                        int64_t* sample, int32_t* worker, int64_t* atoms_out, int64_t* split, int64_t* chunk_rank,
                        int64_t* worker_atoms, int64_t* n_batches, int64_t* dropped) {
     return lamm_guard([&] {
-        require(G >= 1, "schedule: workers must be >= 1");
-        require(B >= 1, "schedule: batch_per_worker must be >= 1");
-        require(S >= 1, "schedule: num_splits must be >= 1");
-        require(mode >= 0 && mode <= 2, "schedule: unknown mode");
-        for (int64_t k = 0; k < n; ++k) require(atoms[k] >= 1, "schedule: atom counts must be >= 1");
         PlanOut out{sample, worker, atoms_out, split, chunk_rank, worker_atoms};
-        const int64_t per_batch = static_cast<int64_t>(G) * B;
-        const auto ids = shuffled_ids(n, seed);
-        std::vector<Slot> mb;
-        std::vector<std::int64_t> mb_atoms(static_cast<std::size_t>(per_batch));
-        std::vector<std::int32_t> assign(static_cast<std::size_t>(per_batch));
-        int64_t lost = 0;
-        auto flush = [&] {
-            for (std::size_t e = 0; e < mb.size(); ++e) mb_atoms[e] = mb[e].atoms;
-            if (mode == 2) {
-                for (int64_t e = 0; e < per_batch; ++e) assign[static_cast<std::size_t>(e)] = static_cast<int32_t>(e / B);
-            } else {
-                balance_minibatch(mb_atoms.data(), per_batch, G, B, assign.data());
-            }
-            emit_minibatch(mb, assign, G, out);
-            mb.clear();
-        };
-        if (mode == 0) {
-            // (1) near-equal contiguous splits of the shuffled ids, each sorted
-            //     by atoms descending (ties: lower id first).
-            std::vector<int64_t> bounds(static_cast<std::size_t>(S) + 1, 0);
-            for (int64_t s = 0; s < S; ++s) bounds[s + 1] = bounds[s] + n / S + (s < n % S ? 1 : 0);
-            std::vector<std::int64_t> sorted = ids;
-            int64_t ranks_max = 0;
-            for (int64_t s = 0; s < S; ++s) {
-                std::sort(sorted.begin() + bounds[s], sorted.begin() + bounds[s + 1],
-                          [&](std::int64_t a, std::int64_t b) {
-                              return atoms[a] != atoms[b] ? atoms[a] > atoms[b] : a < b;
-                          });
-                const int64_t len = bounds[s + 1] - bounds[s];
-                lost += len % G;
-                ranks_max = std::max<int64_t>(ranks_max, len / G);
-            }
-            // (2) G-sized chunks consumed in transpose order (rank-major over
-            // splits); (3) every B consecutive chunks form one mini-batch.
-            int64_t streamed = 0;
-            for (int64_t r = 0; r < ranks_max; ++r)
-                for (int64_t s = 0; s < S; ++s) {
-                    if ((r + 1) * G > bounds[s + 1] - bounds[s]) continue;
-                    for (int64_t k = r * G; k < (r + 1) * G; ++k) {
-                        const std::int64_t id = sorted[static_cast<std::size_t>(bounds[s] + k)];
-                        mb.push_back({id, atoms[id], s, r});
-                    }
-                    streamed += G;
-                    if (static_cast<int64_t>(mb.size()) == per_batch) flush();
-                }
-            lost += static_cast<int64_t>(mb.size());
-            mb.clear();
-            (void)streamed;
-        } else {
-            const int64_t full = n / per_batch;
-            lost = n - full * per_batch;
-            for (int64_t b = 0; b < full; ++b) {
-                for (int64_t e = 0; e < per_batch; ++e) {
-                    const std::int64_t id = ids[static_cast<std::size_t>(b * per_batch + e)];
-                    mb.push_back({id, atoms[id], 0, (b * per_batch + e) / G});
-                }
-                flush();
-            }
+        plan_impl(atoms, atoms, n, G, B, S, seed, mode, out, n_batches, dropped);
+    });
+}
+
+LAMM_API int lamm_sample_cost(const int64_t* atoms, const int64_t* edges, int64_t n, const lamm_cost_model* cm,
+                              double* cost) {
+    return lamm_guard([&] {
+        require(atoms && cm && cost, "sample_cost: null argument");
+        require(std::isfinite(cm->per_sample) && std::isfinite(cm->per_atom) && std::isfinite(cm->per_edge),
+                "cost model: non-finite coefficient");
+        require(cm->per_edge == 0.0 || edges != nullptr, "cost model: per_edge set but no edge counts");
+        for (int64_t k = 0; k < n; ++k) {
+            // fixed order: ((per_sample + per_atom * atoms) + per_edge * edges)
+            double c = cm->per_sample + cm->per_atom * static_cast<double>(atoms[k]);
+            if (edges) c += cm->per_edge * static_cast<double>(edges[k]);
+            require(c > 0.0, "cost model: predicted sample cost must be positive");
+            cost[k] = c;
         }
-        *n_batches = out.batches;
-        *dropped = lost;
+    });
+}
+
+LAMM_API int lamm_plan_cost(const int64_t* atoms, const int64_t* edges, int64_t n, const lamm_cost_model* cm,
+                            int32_t G, int32_t B, int32_t S, uint64_t seed, int32_t mode, int64_t* sample,
+                            int32_t* worker, int64_t* atoms_out, int64_t* split, int64_t* chunk_rank,
+                            int64_t* worker_atoms, double* worker_cost, int64_t* n_batches, int64_t* dropped) {
+    return lamm_guard([&] {
+        std::vector<double> cost(static_cast<std::size_t>(std::max<int64_t>(n, 1)));
+        const int st = lamm_sample_cost(atoms, edges, n, cm, cost.data());
+        if (st != 0) throw InputErr(last_error_cstr());
+        PlanOut out{sample, worker, atoms_out, split, chunk_rank, worker_atoms};
+        out.worker_cost = worker_cost;
+        out.cost = cost.data();
+        plan_impl(cost.data(), atoms, n, G, B, S, seed, mode, out, n_batches, dropped);
     });
 }
 

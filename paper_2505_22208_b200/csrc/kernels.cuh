@@ -53,13 +53,29 @@ struct BatchArrays {
 // Bit-exact with S/core.cpp:40-43: d = p_i - p_j, r = sqrt((dx*dx + dy*dy) + dz*dz)
 // with every operation individually rounded (no FMA contraction), r < cutoff.
 // cell: nullptr, or {cell[9], cell^-1[9]} of a periodic sample (minimum image)
-__device__ __forceinline__ double pair_dist(double xi, double yi, double zi, double xj, double yj, double zj,
-                                            double& dx, double& dy, double& dz, const double* cell = nullptr) {
+// pair_sq: the rounded (dx*dx + dy*dy) + dz*dz that r = sqrt(.) rounds from.
+__device__ __forceinline__ double pair_sq(double xi, double yi, double zi, double xj, double yj, double zj,
+                                          double& dx, double& dy, double& dz, const double* cell = nullptr) {
     dx = __dsub_rn(xi, xj);
     dy = __dsub_rn(yi, yj);
     dz = __dsub_rn(zi, zj);
     if (cell) min_image(cell, cell + 9, dx, dy, dz);
-    return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+__device__ __forceinline__ double pair_dist(double xi, double yi, double zi, double xj, double yj, double zj,
+                                            double& dx, double& dy, double& dz, const double* cell = nullptr) {
+    return __dsqrt_rn(pair_sq(xi, yi, zi, xj, yj, zj, dx, dy, dz, cell));
+}
+// The test sqrt_rn(s) < rc without the square root away from the boundary: s below
+// rc^2 (1 - 1e-12) is inside and s at or above rc^2 (1 + 1e-12) outside whatever
+// the roundings (relative 1e-16 each); only the thin shell between takes the sqrt.
+// The decision is the reference's r < cutoff bit for bit.
+struct Cut {
+    double rc, lo2, hi2;
+};
+__device__ __forceinline__ Cut make_cut(double rc) { return Cut{rc, rc * rc * (1.0 - 1e-12), rc * rc * (1.0 + 1e-12)}; }
+__device__ __forceinline__ bool inside(double s, const Cut& q) {
+    return s < q.lo2 || (s < q.hi2 && __dsqrt_rn(s) < q.rc);
 }
 
 // The sample's periodic cell in the staged blob ({cell, cinv, m, nimg}), or nullptr.
@@ -90,19 +106,28 @@ __device__ __forceinline__ Images sample_images(const double* cell) {
     }
     return im;
 }
-__device__ __forceinline__ bool sample_brute(const double* cell, int n) {
-    return n <= kSmallAtoms || (cell && cell[-1] == 2.0);
+// Who counts a sample's pairs: k_prep's block (small non-periodic samples: the
+// reference's molecules), k_cell_count's warp per atom otherwise — over the cell
+// lists (large samples without images) or brute force over j (and images).
+__device__ __forceinline__ bool counted_in_prep(const double* cell, int n) { return n <= kSmallAtoms && !cell; }
+__device__ __forceinline__ bool uses_cells(const double* cell, int n) {
+    return n > kSmallAtoms && !(cell && cell[-1] == 2.0);
 }
-// Candidate c of a brute-force sweep: source atom offset jl, its image test.
-__device__ __forceinline__ double pair_dist_c(const Images& im, const double* cell, double xi, double yi, double zi,
-                                              double xj, double yj, double zj, int img, double& dx, double& dy,
-                                              double& dz) {
-    if (!im.multi) return pair_dist(xi, yi, zi, xj, yj, zj, dx, dy, dz, cell);
-    dx = __dsub_rn(xi, xj);
-    dy = __dsub_rn(yi, yj);
-    dz = __dsub_rn(zi, zj);
-    image_disp(cell, img / (im.w1 * im.w2) - im.m0, (img / im.w2) % im.w1 - im.m1, img % im.w2 - im.m2, dx, dy, dz);
-    return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+// The images of (i, j) within the cutoff, in image order (n lexicographic), for
+// one lane: f(n, dx, dy, dz, sq) is called for each; (i, i, 0) skipped.
+template <class F>
+__device__ __forceinline__ void for_images(const Images& im, const double* cell, double xi, double yi, double zi,
+                                           double xj, double yj, double zj, bool self, const Cut& cut, F&& f) {
+    double fr[3];
+    image_frac(cell, __dsub_rn(xi, xj), __dsub_rn(yi, yj), __dsub_rn(zi, zj), fr);
+    for (int n0 = -im.m0; n0 <= im.m0; ++n0)
+        for (int n1 = -im.m1; n1 <= im.m1; ++n1)
+            for (int n2 = -im.m2; n2 <= im.m2; ++n2) {
+                if (self && n0 == 0 && n1 == 0 && n2 == 0) continue;
+                double dx, dy, dz;
+                const double sq = image_sq(cell, fr, n0, n1, n2, dx, dy, dz);
+                if (inside(sq, cut)) f(dx, dy, dz, sq);
+            }
 }
 
 
@@ -514,32 +539,28 @@ __global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) 
         __syncthreads();
         const double* cell = sample_cell(d, s);
         const int n = static_cast<int>(hi - lo);
-        if (!sample_brute(cell, n)) {  // counted over its cell list by k_cell_count
-            bin_sample(d, s, lo, hi, cell, bmn, bmx);
-            __syncthreads();
+        if (!counted_in_prep(cell, n)) {  // counted by k_cell_count (warp per atom)
+            if (uses_cells(cell, n)) {
+                bin_sample(d, s, lo, hi, cell, bmn, bmx);
+                __syncthreads();
+            } else if (threadIdx.x == 0) {
+                d.sdone[s] = 0u;
+            }
             continue;
         }
-        // neighbour counts of the sample (S/core.cpp:30-48), warp per atom over the
-        // (j, image) candidates, from the positions this block just staged in shared
-        // memory (samples of more than kSmallAtoms atoms that need images: from
-        // global memory, written by this block; visible after the barrier)
+        // neighbour counts of the sample (S/core.cpp:30-48), warp per atom, from the
+        // positions this block just staged in shared memory (visible after the barrier)
         const int lane = threadIdx.x & 31;
-        const Images im = sample_images(cell);
-        const int ncand = n * im.nimg, self = (im.nimg - 1) / 2;
-        const bool smem = n <= kSmallAtoms;
+        const Cut cut = make_cut(d.rc);
         for (int il = threadIdx.x >> 5; il < n; il += blockDim.x >> 5) {
-            const double xi = smem ? sp[0][il] : d.x[lo + il], yi = smem ? sp[1][il] : d.y[lo + il],
-                         zi = smem ? sp[2][il] : d.z[lo + il];
+            const double xi = sp[0][il], yi = sp[1][il], zi = sp[2][il];
             int cnt = 0;
-            for (int c0 = 0; c0 < ncand; c0 += 32) {
-                const int c = c0 + lane;
-                const int jl = im.nimg == 1 ? c : c / im.nimg, img = im.nimg == 1 ? 0 : c - jl * im.nimg;
+            for (int j0 = 0; j0 < n; j0 += 32) {
+                const int jl = j0 + lane;
                 bool in = false;
-                if (c < ncand && (jl != il || img != self)) {
+                if (jl < n && jl != il) {
                     double dx, dy, dz;
-                    const double xj = smem ? sp[0][jl] : d.x[lo + jl], yj = smem ? sp[1][jl] : d.y[lo + jl],
-                                 zj = smem ? sp[2][jl] : d.z[lo + jl];
-                    in = pair_dist_c(im, cell, xi, yi, zi, xj, yj, zj, img, dx, dy, dz) < d.rc;
+                    in = inside(pair_sq(xi, yi, zi, sp[0][jl], sp[1][jl], sp[2][jl], dx, dy, dz, cell), cut);
                 }
                 cnt += __popc(__ballot_sync(0xffffffffu, in));
             }
@@ -582,14 +603,30 @@ __global__ void __launch_bounds__(256) k_cell_count(Dev d, int Q) {
     const int N = hd.N;
     const int lane = threadIdx.x & 31;
     const int nw = (gridDim.x * blockDim.x) >> 5;
+    const Cut cut = make_cut(d.rc);
     for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
         const int s = d.sample_of[i];
         const int lo = static_cast<int>(d.atom_ptr[s]), hi = static_cast<int>(d.atom_ptr[s + 1]);
         const double* cell = sample_cell(d, s);
-        if (sample_brute(cell, hi - lo)) continue;
-        const CellGrid g = d.cgrid[s];
+        if (counted_in_prep(cell, hi - lo)) continue;
+        const Images im = sample_images(cell);
         const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
         int cnt = 0;
+        if (im.multi) {  // image sample: lane per source atom j, its images in a loop
+            int own = 0;
+            for (int j = lo + lane; j < hi; j += 32)
+                for_images(im, cell, xi, yi, zi, d.x[j], d.y[j], d.z[j], j == i, cut,
+                           [&](double, double, double, double) { ++own; });
+            cnt = __reduce_add_sync(0xffffffffu, own);
+        } else if (!uses_cells(cell, hi - lo)) {  // small periodic sample: minimum image, lane per j
+            int own = 0;
+            for (int j = lo + lane; j < hi; j += 32) {
+                double dx, dy, dz;
+                own += (j != i && inside(pair_sq(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz, cell), cut)) ? 1 : 0;
+            }
+            cnt = __reduce_add_sync(0xffffffffu, own);
+        } else {
+        const CellGrid g = d.cgrid[s];
         // samples of <= 1024 atoms (one window of k_nbr_fill): the hits as a bitmask over
         // the sample's atoms, kept for the fill (no second pass of pair tests)
         const bool keep = hi - lo <= kMaskAtoms;
@@ -606,7 +643,7 @@ __global__ void __launch_bounds__(256) k_cell_count(Dev d, int Q) {
                 const double4 p = d.cpos[lo + k];
                 double dx, dy, dz;
                 j = static_cast<int>(__double_as_longlong(p.w));
-                in = j != i && pair_dist(xi, yi, zi, p.x, p.y, p.z, dx, dy, dz, cell) < d.rc;
+                in = j != i && inside(pair_sq(xi, yi, zi, p.x, p.y, p.z, dx, dy, dz, cell), cut);
             }
             if (keep && in) atomicOr(bits + ((j - lo) >> 5), 1u << ((j - lo) & 31));
             cnt += __popc(__ballot_sync(0xffffffffu, in));
@@ -616,6 +653,7 @@ __global__ void __launch_bounds__(256) k_cell_count(Dev d, int Q) {
 #pragma unroll
             for (int q = 0; q < kMaskWords / 32; ++q)
                 d.cmask[static_cast<int64_t>(i) * kMaskWords + 32 * q + lane] = bits[32 * q + lane];
+        }
         unsigned last = 0;
         if (lane == 0) {
             d.cnt[i] = cnt;
@@ -688,7 +726,7 @@ __device__ __forceinline__ void emit_pair(const Dev& d, int p, int i, int j, dou
 // shared-memory mask, the set bits are listed in ascending j (one mask word per
 // lane, warp scan of the popcounts) and the lanes emit the listed pairs.
 template <int K>
-__global__ void __launch_bounds__(256) k_nbr_fill(Dev d, int Q) {
+__global__ void __launch_bounds__(256, 4) k_nbr_fill(Dev d, int Q) {
     constexpr int kWin = 1024;
     __shared__ uint32_t wbits[8][kWin / 32];
     __shared__ int wlist[8][kWin];
@@ -701,6 +739,7 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d, int Q) {
     const double width = d.rc / static_cast<double>(K - 1);
     const float wf = static_cast<float>(width), invf = static_cast<float>(1.0 / (2.0 * width * width));
     const float rc_inv = static_cast<float>(1.0 / d.rc);
+    const Cut cut = make_cut(d.rc);
     if (blockIdx.x == 0)  // the CSR padding's geometry: finite zeros (masked edges must not carry stale NaN)
         for (int x = threadIdx.x; x < (kChunk + 8) * K; x += blockDim.x) {
             const int64_t p = P + x / K;
@@ -731,17 +770,32 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d, int Q) {
                     for (int64_t q = ((static_cast<int64_t>(base) + 1) * Q + P - 1) / P; q < Q; ++q) d.part_lo[q] = N;
             }
         }
-        if (sample_brute(cell, hi - lo)) {
-            const Images im = sample_images(cell);
-            const int ncand = (hi - lo) * im.nimg, self = (im.nimg - 1) / 2, il = i - lo;
-            for (int c0 = 0; c0 < ncand; c0 += 32) {
-                const int c = c0 + lane;
-                const int jl = im.nimg == 1 ? c : c / im.nimg, img = im.nimg == 1 ? 0 : c - jl * im.nimg;
-                const int j = lo + jl;
+        const Images im = sample_images(cell);
+        if (im.multi) {  // image sample: lane per source atom j (ascending), its hits in image order
+            for (int j0 = lo; j0 < hi; j0 += 32) {
+                const int j = j0 + lane;
+                int own = 0;
+                if (j < hi)
+                    for_images(im, cell, xi, yi, zi, d.x[j], d.y[j], d.z[j], j == i, cut,
+                               [&](double, double, double, double) { ++own; });
+                const int incl = warp_incl_scan(own);
+                int at = base + incl - own;
+                if (j < hi)
+                    for_images(im, cell, xi, yi, zi, d.x[j], d.y[j], d.z[j], j == i, cut,
+                               [&](double dx, double dy, double dz, double sq) {
+                                   emit_pair<K>(d, at++, i, j, __dsqrt_rn(sq), dx, dy, dz, wf, invf, rc_inv);
+                               });
+                base += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            continue;
+        }
+        if (!uses_cells(cell, hi - lo)) {
+            for (int j0 = lo; j0 < hi; j0 += 32) {
+                const int j = j0 + lane;
                 bool in = false;
                 double dx = 0, dy = 0, dz = 0, r = 0;
-                if (c < ncand && (jl != il || img != self)) {
-                    r = pair_dist_c(im, cell, xi, yi, zi, d.x[j], d.y[j], d.z[j], img, dx, dy, dz);
+                if (j < hi && j != i) {
+                    r = pair_dist(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz, cell);
                     in = r < d.rc;
                 }
                 const unsigned mask = __ballot_sync(0xffffffffu, in);
@@ -764,7 +818,7 @@ __global__ void __launch_bounds__(256) k_nbr_fill(Dev d, int Q) {
                     const double4 p = d.cpos[lo + k];
                     const int j = static_cast<int>(__double_as_longlong(p.w));
                     double dx, dy, dz;
-                    if (j >= w0 && j < w0 + kWin && j != i && pair_dist(xi, yi, zi, p.x, p.y, p.z, dx, dy, dz, cell) < d.rc)
+                    if (j >= w0 && j < w0 + kWin && j != i && inside(pair_sq(xi, yi, zi, p.x, p.y, p.z, dx, dy, dz, cell), cut))
                         atomicOr(bits + ((j - w0) >> 5), 1u << ((j - w0) & 31));
                 }
             }
