@@ -344,6 +344,45 @@ int lamm_schedule_metrics(int64_t n_batches, int32_t workers, int32_t batch_per_
                           double* max_imbalance, double* mean_imbalance, int64_t* monotonicity_violations,
                           int64_t* growth_events);
 
+/* ------------------------------------------------- host: data layer --- */
+/* The orchestration's data layer (S/trainer.cpp:64-125), host C++ in this library:
+ * dataset::filter_max_atoms (S/dataset.cpp:85-96): indices of the samples with at
+ * most `limit` atoms, in order. */
+int lamm_filter_max_atoms(const int64_t* atom_ptr, int64_t n_samples, int64_t limit, int64_t* kept,
+                          int64_t* n_kept);
+/* dataset::split_train_val (S/dataset.cpp:98-111): Rng(seed).permutation(n), the
+ * first llround(val_fraction * n) ids are validation; both sorted. */
+int lamm_split_train_val(int64_t n, double val_fraction, uint64_t seed, int64_t* train, int64_t* n_train,
+                         int64_t* val, int64_t* n_val);
+/* denoise::apply_noise (S/denoise.cpp:7-40) of one system: noisy positions and
+ * pseudo-force labels (either output nullable); scheme 1 centered, 0 baseline. */
+int lamm_apply_noise(const double* positions, int64_t n_atoms, double sigma, int32_t scheme, uint64_t seed,
+                     double* noisy, double* pseudo_forces);
+/* estimate_pseudo_force_std (S/trainer.cpp:82-100): std of the pseudo-forces of the
+ * first min(n_ids, 256) samples ids[v] (NULL: v) under seeds mix_seed(seed,
+ * 0x50535444 + v). */
+int lamm_pseudo_force_std(const int64_t* atom_ptr, const double* positions, const int64_t* ids, int64_t n_ids,
+                          double sigma, int32_t scheme, uint64_t seed, double* out);
+/* loss::DatasetNormalizer (H/loss.hpp:32-38): rho indexed by Z. */
+typedef struct {
+    double rho[119];
+    uint8_t rho_has[119];
+    double energy_mean;
+    double energy_std;
+    double force_std;
+    uint8_t has_energy_stats;
+} lamm_normalizer;
+/* loss::fit_normalizer (S/loss.cpp:64-111) over the view's samples (masks and
+ * labels as in lamm_batch_view; positions unused): per-element reference energies
+ * by a minimum-norm least-squares solve (fit_reference, S/loss.cpp:17-48; complete
+ * orthogonal decomposition, host_data.cpp), residual mean/std, force std (else
+ * pseudo_force_std when > 0). */
+int lamm_fit_normalizer(const lamm_batch_view* samples, double pseudo_force_std, lamm_normalizer* out);
+/* model::reset_heads / init_heads (S/model.cpp:167-202): fresh energy head [H][heads]
+ * and force head [2H+K][heads] from Rng(seed), bit-exact. */
+int lamm_init_heads(const lamm_model_config* cfg, int32_t heads, uint64_t seed, double* energy_head,
+                    double* force_head);
+
 /* ----------------------------------------------- host: data generation --- */
 /* lamm::trace::make_trace (S/trace.cpp:50-76). kind: 0 constant, 1 uniform,
  * 2 lognormal, 3 bimodal. */

@@ -9,11 +9,15 @@
 // result types, same seed streams, sinks, metric points and cadences. What runs
 // where:
 //
-//   data layer (filter/split, mix plan, normalizer fit, noise, reset_heads)
-//        the caller's reference library - this header is for integrators who
-//        link it (include <lamm/trainer.hpp> first); only the file-local glue of
-//        S/trainer.cpp (make_view, build_refs, build_val_samples) is restated
-//        here over those public functions
+//   data layer (filter/split, mix plan, normalizer fit, noise, reset_heads,
+//   config validation)
+//        this library's native host code (csrc/host_data.cpp, host_sched.cpp):
+//        lamm_filter_max_atoms, lamm_split_train_val, lamm_pseudo_force_std,
+//        lamm_fit_normalizer, lamm_apply_noise, lamm_temperature_counts,
+//        lamm_init_heads; the file-local glue of S/trainer.cpp (make_view,
+//        build_refs, build_val_samples) is restated here over them. Only the
+//        caller's value types (Catalog, Subset, Sample, TrainConfig, ...) come
+//        from <lamm/...> headers: no reference function runs in this header
 //   seed streams (mix_seed), epoch index, balanced schedule, init_params
 //        this library's native host code (bit-exact with the reference)
 //   step body (S/trainer.cpp:258-327): denoise -> normalize -> neighbour list
@@ -59,6 +63,70 @@ namespace detail {
 
 using Nan = std::numeric_limits<double>;
 
+// lamm::trainer::validate_train_config (S/trainer.cpp:347-364) and
+// lamm::model::validate_config (S/model.cpp:114-120), restated: the same checks and messages.
+inline void check_train_config(const lamm::trainer::TrainConfig& cfg) {
+    auto need = [](bool ok, const char* msg) {
+        if (!ok) throw lamm::InputError(msg);
+    };
+    need(cfg.max_steps >= 1, "train: max_steps must be >= 1");
+    need(cfg.learning_rate > 0.0, "train: learning_rate must be positive");
+    need(cfg.clip_norm >= 0.0, "train: clip_norm must be >= 0");
+    need(cfg.val_every >= 1, "train: val_every must be >= 1");
+    need(cfg.checkpoint_every >= 0, "train: checkpoint_every must be >= 0");
+    need(cfg.lambda_energy >= 0.0 && cfg.lambda_force >= 0.0, "train: lambdas must be >= 0");
+    need(cfg.val_fraction >= 0.0 && cfg.val_fraction < 1.0, "train: val_fraction must be in [0, 1)");
+    need(cfg.max_atoms >= 1, "train: max_atoms must be >= 1");
+    need(cfg.noise_sigma > 0.0, "train: noise_sigma must be positive");
+    need(cfg.energy_threshold >= 0.0 && cfg.force_threshold >= 0.0, "train: thresholds must be >= 0");
+    need(cfg.rms_decay >= 0.0 && cfg.rms_decay < 1.0, "train: rms_decay must be in [0, 1)");
+    need(cfg.rms_epsilon > 0.0, "train: rms_epsilon must be positive");
+}
+inline void check_model_config(const lamm::model::ModelConfig& c) {
+    if (c.hidden < 1) throw lamm::InputError("model: hidden must be >= 1");
+    if (c.layers < 0) throw lamm::InputError("model: layers must be >= 0");
+    if (c.rbf < 2) throw lamm::InputError("model: rbf must be >= 2");
+    if (!(c.cutoff > 0.0)) throw lamm::InputError("model: cutoff must be positive");
+    if (c.heads < 1) throw lamm::InputError("model: heads must be >= 1");
+}
+
+// Packed (CSR) views of a subset's samples for the native data-layer calls.
+template <class Samples>
+inline PackedBatch pack_samples(const Samples& samples, const std::vector<int64_t>* ids = nullptr) {
+    PackedBatch p;
+    const size_t n = ids ? ids->size() : samples.size();
+    for (size_t k = 0; k < n; ++k) p.add_sample(samples[ids ? static_cast<size_t>((*ids)[k]) : k]);
+    return p;
+}
+
+inline int scheme_of(const lamm::trainer::TrainConfig& cfg) {
+    return cfg.noise_scheme == lamm::denoise::Scheme::centered ? 1 : 0;
+}
+
+// make_denoising_sample (S/denoise.cpp:42-53) through the native apply_noise.
+inline lamm::Sample denoising_copy(const lamm::Sample& src, const lamm::trainer::TrainConfig& cfg, uint64_t seed,
+                                   int dataset_index, int subset_id) {
+    const size_t n = src.system.positions.size();
+    std::vector<double> pos(3 * n), noisy(3 * n), pf(3 * n);
+    for (size_t a = 0; a < n; ++a)
+        for (int c = 0; c < 3; ++c) pos[3 * a + c] = src.system.positions[a][c];
+    check(lamm_apply_noise(pos.data(), static_cast<int64_t>(n), cfg.noise_sigma, scheme_of(cfg), seed, noisy.data(),
+                           pf.data()));
+    lamm::Sample out;
+    out.system = src.system;
+    out.labels.forces.resize(n);
+    for (size_t a = 0; a < n; ++a)
+        for (int c = 0; c < 3; ++c) {
+            out.system.positions[a][c] = noisy[3 * a + c];
+            out.labels.forces[a][c] = pf[3 * a + c];
+        }
+    out.labels.force_mask = true;
+    out.labels.energy_mask = false;
+    out.labels.dataset_index = dataset_index;
+    out.subset_id = subset_id;
+    return out;
+}
+
 // A subset resolved for training: kept sample ids split into train / val.
 struct Split {
     const lamm::dataset::Subset* subset = nullptr;
@@ -71,12 +139,19 @@ inline Split split_subset(const lamm::dataset::Subset& subset, const lamm::train
     Split s;
     s.subset = &subset;
     s.denoising = subset.meta.task == lamm::dataset::TaskKind::denoising;
-    const auto kept = lamm::dataset::filter_max_atoms(subset.samples, cfg.max_atoms).first;
-    if (kept.empty()) throw lamm::InputError("subset \"" + subset.meta.name + "\": no samples under the atom limit");
-    const auto tv = lamm::dataset::split_train_val(kept.size(), cfg.val_fraction, seed);
-    s.train.reserve(tv.train.size());
-    for (const auto k : tv.train) s.train.push_back(kept[static_cast<size_t>(k)]);
-    for (const auto k : tv.val) s.val.push_back(kept[static_cast<size_t>(k)]);
+    std::vector<int64_t> ptr{0};
+    for (const auto& smp : subset.samples) ptr.push_back(ptr.back() + static_cast<int64_t>(smp.system.size()));
+    const int64_t ns = static_cast<int64_t>(subset.samples.size());
+    std::vector<int64_t> kept(static_cast<size_t>(std::max<int64_t>(ns, 1)));
+    int64_t nk = 0;
+    check(lamm_filter_max_atoms(ptr.data(), ns, cfg.max_atoms, kept.data(), &nk));
+    if (nk == 0) throw lamm::InputError("subset \"" + subset.meta.name + "\": no samples under the atom limit");
+    std::vector<int64_t> tr(static_cast<size_t>(nk)), va(static_cast<size_t>(nk));
+    int64_t nt = 0, nv = 0;
+    check(lamm_split_train_val(nk, cfg.val_fraction, seed, tr.data(), &nt, va.data(), &nv));
+    s.train.reserve(static_cast<size_t>(nt));
+    for (int64_t k = 0; k < nt; ++k) s.train.push_back(kept[static_cast<size_t>(tr[static_cast<size_t>(k)])]);
+    for (int64_t k = 0; k < nv; ++k) s.val.push_back(kept[static_cast<size_t>(va[static_cast<size_t>(k)])]);
     if (s.train.empty()) throw lamm::InputError("subset \"" + subset.meta.name + "\": empty training split");
     return s;
 }
@@ -88,19 +163,24 @@ inline const lamm::Sample& sample_of(const Split& s, int64_t train_pos) {
 // Pseudo-force scale of a denoising subset: std of the noise labels over a
 // fixed probe of up to 256 training structures (S/trainer.cpp:85-105).
 inline double pseudo_force_scale(const Split& s, const lamm::trainer::TrainConfig& cfg) {
-    const size_t probe = std::min<size_t>(s.train.size(), 256);
-    double sum = 0.0, sq = 0.0;
-    size_t n = 0;
-    for (size_t v = 0; v < probe; ++v) {
-        const lamm::denoise::NoiseConfig nc{cfg.noise_sigma, cfg.noise_scheme,
-                                            lamm_mix_seed(cfg.seed, kProbeStream + v)};
-        const auto noise = lamm::denoise::apply_noise(sample_of(s, static_cast<int64_t>(v)).system, nc);
-        for (const auto& f : noise.pseudo_forces)
-            for (const double c : f) sum += c, sq += c * c, ++n;
-    }
-    if (n == 0) return cfg.noise_sigma;
-    const double mean = sum / static_cast<double>(n);
-    return std::max(std::sqrt(std::max(sq / static_cast<double>(n) - mean * mean, 0.0)), 1e-8);
+    const std::vector<int64_t> probe(s.train.begin(), s.train.begin() + std::min<size_t>(s.train.size(), 256));
+    const PackedBatch p = pack_samples(s.subset->samples, &probe);
+    double out = 0.0;
+    check(lamm_pseudo_force_std(p.atom_ptr.data(), p.positions.data(), nullptr, static_cast<int64_t>(probe.size()),
+                                cfg.noise_sigma, scheme_of(cfg), cfg.seed, &out));
+    return out;
+}
+
+// loss::DatasetNormalizer from the native fit (rho by Z -> the reference's map).
+inline lamm::loss::DatasetNormalizer normalizer_of(const lamm_normalizer& n) {
+    lamm::loss::DatasetNormalizer d;
+    for (int z = 0; z < 119; ++z)
+        if (n.rho_has[z]) d.reference_energies[z] = n.rho[z];
+    d.energy_mean = n.energy_mean;
+    d.energy_std = n.energy_std;
+    d.force_std = n.force_std;
+    d.has_energy_stats = n.has_energy_stats != 0;
+    return d;
 }
 
 // One normalizer per prediction channel over the pooled training samples of
@@ -110,17 +190,22 @@ inline lamm::loss::ReferenceTable fit_channels(const std::vector<Split>& splits,
     lamm::loss::ReferenceTable t;
     t.per_dataset.resize(static_cast<size_t>(heads));
     for (int d = 0; d < heads; ++d) {
-        std::vector<lamm::Sample> pool;
+        PackedBatch pool;
         double pseudo = 0.0;
         for (const auto& s : splits) {
             if (s.subset->meta.head_index != d) continue;
             if (s.denoising) {
                 pseudo = std::max(pseudo, pseudo_force_scale(s, cfg));
             } else {
-                for (const auto id : s.train) pool.push_back(s.subset->samples[static_cast<size_t>(id)]);
+                for (const auto id : s.train) pool.add_sample(s.subset->samples[static_cast<size_t>(id)]);
             }
         }
-        if (!pool.empty() || pseudo > 0.0) t.per_dataset[static_cast<size_t>(d)] = lamm::loss::fit_normalizer(pool, pseudo);
+        if (pool.size() > 0 || pseudo > 0.0) {
+            lamm_normalizer n{};
+            const lamm_batch_view v = pool.view();
+            check(lamm_fit_normalizer(&v, pseudo, &n));
+            t.per_dataset[static_cast<size_t>(d)] = normalizer_of(n);
+        }
     }
     return t;
 }
@@ -137,10 +222,8 @@ inline std::vector<lamm::Sample> held_out(const std::vector<Split>& splits, cons
             if (!s.denoising) {
                 out.push_back(raw);
             } else if (with_denoising) {
-                const lamm::denoise::NoiseConfig nc{cfg.noise_sigma, cfg.noise_scheme,
-                                                    lamm_mix_seed(cfg.seed, kValNoiseStream + ordinal)};
-                out.push_back(lamm::denoise::make_denoising_sample(raw.system, nc, s.subset->meta.head_index,
-                                                                   raw.subset_id));
+                out.push_back(denoising_copy(raw, cfg, lamm_mix_seed(cfg.seed, kValNoiseStream + ordinal),
+                                             s.subset->meta.head_index, raw.subset_id));
             }
             ++ordinal;
         }
@@ -182,8 +265,8 @@ inline lamm::trainer::RunMetrics run(const Run& r, lamm::model::ModelParams& par
                                      const lamm::trainer::CheckpointSink& on_checkpoint,
                                      const lamm::trainer::PointSink& on_point) {
     const auto& cfg = r.cfg;
-    lamm::trainer::validate_train_config(cfg);
-    lamm::model::validate_config(r.mcfg);
+    check_train_config(cfg);
+    check_model_config(r.mcfg);
     for (const auto& s : r.splits)
         if (s.subset->meta.head_index < 0 || s.subset->meta.head_index >= r.mcfg.heads)
             throw lamm::InputError("subset \"" + s.subset->meta.name + "\" trains head " +
@@ -250,13 +333,13 @@ inline lamm::trainer::RunMetrics run(const Run& r, lamm::model::ModelParams& par
                 std::vector<lamm::Sample> phys = batch;
                 for (int k = 0; k < G * B; ++k) {
                     if (!noisy[static_cast<size_t>(k)]) continue;
+                    // the draws the device step makes for worker slot k (S/trainer.cpp:276-277)
                     const auto& src = batch[static_cast<size_t>(k)];
-                    const lamm::denoise::NoiseConfig nc{
-                        cfg.noise_sigma, cfg.noise_scheme,
+                    phys[static_cast<size_t>(k)] = denoising_copy(
+                        src, cfg,
                         lamm_mix_seed(lamm_mix_seed(cfg.seed, kNoiseStream + static_cast<uint64_t>(step)),
-                                       static_cast<uint64_t>(k))};
-                    phys[static_cast<size_t>(k)] = lamm::denoise::make_denoising_sample(
-                        src.system, nc, src.labels.dataset_index, src.subset_id);
+                                      static_cast<uint64_t>(k)),
+                        src.labels.dataset_index, src.subset_id);
                 }
                 stats = evaluate<lamm::trainer::EvalResult>(dev, std::span<const lamm::Sample>(phys));
             }
@@ -320,7 +403,10 @@ inline lamm::trainer::PretrainResult pretrain(const lamm::dataset::Catalog& cata
     if (mix.repeats.empty()) {
         std::vector<double> sizes;
         for (const auto& s : r.splits) sizes.push_back(static_cast<double>(s.train.size()));
-        r.mix = lamm::dataset::make_mix_plan(sizes, mix.temperature);
+        r.mix.temperature = mix.temperature;  // dataset::make_mix_plan (S/dataset.cpp:54-59)
+        r.mix.repeats.assign(sizes.size(), 0.0);
+        check(lamm_temperature_counts(sizes.data(), static_cast<int32_t>(sizes.size()), mix.temperature,
+                                      r.mix.repeats.data()));
     } else {
         r.mix = mix;
     }
@@ -342,7 +428,7 @@ inline lamm::trainer::FinetuneResult finetune(const lamm::model::Checkpoint& sta
                                               const lamm::trainer::TrainConfig& cfg,
                                               const lamm::trainer::CheckpointSink& on_checkpoint = {},
                                               const lamm::trainer::PointSink& on_point = {}, int device = 0) {
-    lamm::model::validate_config(start.config);
+    detail::check_model_config(start.config);
     lamm::dataset::Subset local = target;
     local.meta.head_index = 0;
     for (auto& s : local.samples) s.labels.dataset_index = 0;
@@ -359,7 +445,15 @@ inline lamm::trainer::FinetuneResult finetune(const lamm::model::Checkpoint& sta
 
     lamm::trainer::FinetuneResult out;
     out.config = r.mcfg;
-    out.params = lamm::model::reset_heads(start.params, start.config, 1, lamm_mix_seed(cfg.seed, kHeadStream));
+    out.params = start.params;  // model::reset_heads (S/model.cpp:195-202): one fresh head, natively drawn
+    {
+        const auto H = static_cast<size_t>(start.config.hidden), K = static_cast<size_t>(start.config.rbf);
+        lamm_model_config mc{start.config.hidden, start.config.layers, start.config.rbf, 1, start.config.cutoff};
+        out.params.energy_head = lamm::Matrix(H, 1);
+        out.params.force_head = lamm::Matrix(2 * H + K, 1);
+        check(lamm_init_heads(&mc, 1, lamm_mix_seed(cfg.seed, kHeadStream), out.params.energy_head.data(),
+                              out.params.force_head.data()));
+    }
     out.refs = r.refs;
     out.metrics = detail::run(r, out.params, device, on_checkpoint, on_point);
     return out;

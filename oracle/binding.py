@@ -170,6 +170,37 @@ class OracleLib:
         self._f("rng_permutation")(_u64(seed), _i64(n), _p(o))
         return o
 
+    # ------------------------------------------------------- data layer (ref)
+    def split_train_val(self, n, val_fraction, seed):
+        tr, va = np.empty(max(n, 1), np.int64), np.empty(max(n, 1), np.int64)
+        nt, nv = _i64(), _i64()
+        self._check(self.lib.lref_split_train_val(_i64(n), _f64(val_fraction), _u64(seed), _p(tr), C.byref(nt),
+                                                  _p(va), C.byref(nv)))
+        return tr[:nt.value], va[:nv.value]
+
+    def fit_normalizer(self, b, pseudo_std=0.0):
+        B = len(b["atom_ptr"]) - 1
+        rho, has, st = np.zeros(119), np.zeros(119, np.uint8), np.zeros(4)
+        self._check(self.lib.lref_fit_normalizer(
+            B, _p(_c(b["atom_ptr"], np.int64)), _p(_c(b["pos"], np.float64)), _p(_c(b["Z"], np.int32)),
+            _p(_c(b["energy_mask"], np.uint8)), _p(_c(b["force_mask"], np.uint8)), _p(_c(b["energy"], np.float64)),
+            _p(_c(b["forces"], np.float64)), _f64(pseudo_std), _p(rho), _p(has), _p(st)))
+        return dict(rho=rho, rho_has=has, mean=st[0], std=st[1], fstd=st[2], has=int(st[3]))
+
+    def pseudo_force_std(self, b, sigma, scheme, seed):
+        out = C.c_double()
+        self._check(self.lib.lref_pseudo_force_std(len(b["atom_ptr"]) - 1, _p(_c(b["atom_ptr"], np.int64)),
+                                                   _p(_c(b["pos"], np.float64)), _p(_c(b["Z"], np.int32)),
+                                                   _f64(sigma), scheme, _u64(seed), C.byref(out)))
+        return out.value
+
+    def reset_heads(self, cfg, params, heads, seed):
+        H, L, K, rc, D = cfg
+        e, f = np.empty(H * heads), np.empty((2 * H + K) * heads)
+        self._check(self.lib.lref_reset_heads(H, L, K, _f64(rc), D, _p(_c(params, np.float64)), heads, _u64(seed),
+                                              _p(e), _p(f)))
+        return e.reshape(H, heads), f.reshape(2 * H + K, heads)
+
     # ----------------------------------------------------------- geometry
     def neighbor_list(self, pos, Z, cutoff):
         pos = _c(pos, np.float64).reshape(-1, 3)

@@ -714,3 +714,70 @@ LREF_API int lref_checkpoint_load(const char* path, int32_t* cfg_out, double* rc
         params_to_flat(ck.params, params);
     });
 }
+
+// ---- data layer (S/dataset.cpp:85-111, S/loss.cpp:17-111, S/trainer.cpp:82-100,
+// S/model.cpp:195-202): checkers for paper_2505_22208_b200/csrc/host_data.cpp ----
+LREF_API int lref_split_train_val(int64_t n, double val_fraction, uint64_t seed, int64_t* train, int64_t* n_train,
+                                  int64_t* val, int64_t* n_val) {
+    return guarded([&] {
+        const auto s = lamm::dataset::split_train_val(static_cast<std::size_t>(n), val_fraction, seed);
+        for (std::size_t k = 0; k < s.train.size(); ++k) train[k] = static_cast<int64_t>(s.train[k]);
+        for (std::size_t k = 0; k < s.val.size(); ++k) val[k] = static_cast<int64_t>(s.val[k]);
+        *n_train = static_cast<int64_t>(s.train.size());
+        *n_val = static_cast<int64_t>(s.val.size());
+    });
+}
+
+/// fit_normalizer over the batch's samples (this build's Eigen is oracle/shim:
+/// its minimum-norm solve is a Jacobi pseudo-inverse, parity-unpinned).
+LREF_API int lref_fit_normalizer(int32_t B, const int64_t* atom_ptr, const double* pos, const int32_t* Z,
+                                 const uint8_t* emask, const uint8_t* fmask, const double* energy,
+                                 const double* forces, double pseudo_std, double* rho, uint8_t* rho_has,
+                                 double* stats /* mean, std, fstd, has */) {
+    return guarded([&] {
+        std::vector<lamm::Sample> pool;
+        for (int s = 0; s < B; ++s) pool.push_back(sample_at(atom_ptr, pos, Z, nullptr, emask, fmask, energy, forces, s));
+        const auto n = lamm::loss::fit_normalizer(pool, pseudo_std);
+        for (int z = 0; z < 119; ++z) rho[z] = 0.0, rho_has[z] = 0;
+        for (const auto& [z, v] : n.reference_energies) rho[z] = v, rho_has[z] = 1;
+        stats[0] = n.energy_mean, stats[1] = n.energy_std, stats[2] = n.force_std;
+        stats[3] = n.has_energy_stats ? 1.0 : 0.0;
+    });
+}
+
+/// estimate_pseudo_force_std (S/trainer.cpp:82-100, file-local there): restated over
+/// the reference's own apply_noise with the reference's probe seeds.
+LREF_API int lref_pseudo_force_std(int32_t B, const int64_t* atom_ptr, const double* pos, const int32_t* Z,
+                                   double sigma, int scheme, uint64_t seed, double* out) {
+    return guarded([&] {
+        constexpr uint64_t kProbeTag = 0x50535444;
+        const int64_t probe = std::min<int64_t>(B, 256);
+        double sum = 0.0, sq = 0.0;
+        std::size_t count = 0;
+        for (int64_t v = 0; v < probe; ++v) {
+            lamm::denoise::NoiseConfig nc;
+            nc.sigma = sigma;
+            nc.scheme = scheme ? lamm::denoise::Scheme::centered : lamm::denoise::Scheme::baseline;
+            nc.seed = lamm::mix_seed(seed, kProbeTag + static_cast<uint64_t>(v));
+            const auto r = lamm::denoise::apply_noise(system_at(atom_ptr, pos, Z, static_cast<int>(v)), nc);
+            for (const auto& f : r.pseudo_forces)
+                for (double c : f) sum += c, sq += c * c, ++count;
+        }
+        if (count == 0) {
+            *out = sigma;
+            return;
+        }
+        const double mean = sum / static_cast<double>(count);
+        *out = std::max(std::sqrt(std::max(sq / static_cast<double>(count) - mean * mean, 0.0)), 1e-8);
+    });
+}
+
+LREF_API int lref_reset_heads(int H, int L, int K, double rc, int D, const double* params, int new_heads,
+                              uint64_t seed, double* energy_head, double* force_head) {
+    return guarded([&] {
+        const auto cfg = make_cfg(H, L, K, rc, D);
+        const auto p = lamm::model::reset_heads(params_from_flat(cfg, params), cfg, new_heads, seed);
+        std::copy(p.energy_head.data(), p.energy_head.data() + p.energy_head.size(), energy_head);
+        std::copy(p.force_head.data(), p.force_head.data() + p.force_head.size(), force_head);
+    });
+}

@@ -37,6 +37,11 @@ class BatchViewC(C.Structure):
                 ("forces", C.c_void_p), ("denoise", C.c_void_p), ("cell", C.c_void_p), ("pbc", C.c_void_p)]
 
 
+class NormalizerC(C.Structure):
+    _fields_ = [("rho", C.c_double * 119), ("rho_has", C.c_uint8 * 119), ("energy_mean", C.c_double),
+                ("energy_std", C.c_double), ("force_std", C.c_double), ("has_energy_stats", C.c_uint8)]
+
+
 class CostModelC(C.Structure):
     _fields_ = [("per_sample", C.c_double), ("per_atom", C.c_double), ("per_edge", C.c_double)]
 
@@ -89,7 +94,8 @@ EXPORTS = [
     "lamm_flush_l2", "lamm_step_times", "lamm_evaluate", "lamm_cell_inverse",
     "lamm_checkpoint_save", "lamm_checkpoint_load", "lamm_rms_state_save", "lamm_rms_state_load",
     "lamm_subset_info", "lamm_subset_read", "lamm_train_step_workers", "lamm_ctx_get_info",
-    "lamm_sample_cost", "lamm_plan_cost",
+    "lamm_sample_cost", "lamm_plan_cost", "lamm_filter_max_atoms", "lamm_split_train_val", "lamm_apply_noise",
+    "lamm_pseudo_force_std", "lamm_fit_normalizer", "lamm_init_heads",
 ]
 
 _lib = None

@@ -26,7 +26,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import (BatchViewC, CostModelC, EvalResultC, InputError, LossBreakdownC, LossConfigC, ModelConfigC, NonFiniteError,  # noqa: F401
+from ._lib import (BatchViewC, CostModelC, NormalizerC, EvalResultC, InputError, LossBreakdownC, LossConfigC, ModelConfigC, NonFiniteError,  # noqa: F401
                    RefTableC, StepResultC, TrainConfigC, check, lib)
 
 
@@ -541,6 +541,66 @@ def fit_cost_model(atoms, edges, times, samples=None) -> tuple:
     cm = CostModel(per_sample=float(coef[3]) if samples is not None else 0.0, per_atom=float(coef[1]),
                    per_edge=float(coef[2]))
     return cm, float(coef[0]), r2
+
+
+# ------------------------------------------------------- data layer (host C++)
+def filter_max_atoms(atom_ptr, limit: int) -> np.ndarray:
+    """dataset::filter_max_atoms (S/dataset.cpp:85-96): kept sample indices."""
+    ap = _c(atom_ptr, np.int64)
+    out = np.empty(max(len(ap) - 1, 1), np.int64)
+    n = C.c_int64()
+    check(lib().lamm_filter_max_atoms(_p(ap), C.c_int64(len(ap) - 1), C.c_int64(limit), _p(out), C.byref(n)))
+    return out[:n.value]
+
+
+def split_train_val(n: int, val_fraction: float, seed: int):
+    """dataset::split_train_val (S/dataset.cpp:98-111): (train ids, val ids)."""
+    tr, va = np.empty(max(n, 1), np.int64), np.empty(max(n, 1), np.int64)
+    nt, nv = C.c_int64(), C.c_int64()
+    check(lib().lamm_split_train_val(C.c_int64(n), C.c_double(val_fraction), C.c_uint64(seed), _p(tr),
+                                     C.byref(nt), _p(va), C.byref(nv)))
+    return tr[:nt.value], va[:nv.value]
+
+
+def apply_noise(positions, sigma: float, scheme: int, seed: int):
+    """denoise::apply_noise (S/denoise.cpp:7-40): (noisy positions, pseudo-forces)."""
+    pos = _c(positions, np.float64).reshape(-1, 3)
+    noisy, pf = np.empty_like(pos), np.empty_like(pos)
+    check(lib().lamm_apply_noise(_p(pos), C.c_int64(len(pos)), C.c_double(sigma), scheme, C.c_uint64(seed),
+                                 _p(noisy), _p(pf)))
+    return noisy, pf
+
+
+def pseudo_force_std(batch: dict, sigma: float, scheme: int, seed: int, ids=None) -> float:
+    """estimate_pseudo_force_std (S/trainer.cpp:82-100) over ids (default: all samples)."""
+    ap = _c(batch["atom_ptr"], np.int64)
+    pos = _c(batch["pos"], np.float64)
+    idv = None if ids is None else _c(ids, np.int64)
+    n = len(ap) - 1 if ids is None else len(idv)
+    out = C.c_double()
+    check(lib().lamm_pseudo_force_std(_p(ap), _p(pos), _p(idv) if idv is not None else None, C.c_int64(n),
+                                      C.c_double(sigma), scheme, C.c_uint64(seed), C.byref(out)))
+    return out.value
+
+
+def fit_normalizer(batch: dict, pseudo_force_std: float = 0.0) -> dict:
+    """loss::fit_normalizer (S/loss.cpp:64-111): rho [119] (by Z), rho_has, mean, std,
+    fstd, has (one row of a reference table)."""
+    v, keep = _batch_view(batch)
+    out = NormalizerC()
+    check(lib().lamm_fit_normalizer(C.byref(v), C.c_double(pseudo_force_std), C.byref(out)))
+    return dict(rho=np.array(out.rho[:]), rho_has=np.array(out.rho_has[:], np.uint8), mean=out.energy_mean,
+                std=out.energy_std, fstd=out.force_std, has=int(out.has_energy_stats))
+
+
+def init_heads(cfg: ModelConfig, heads: int, seed: int):
+    """model::reset_heads' fresh heads (S/model.cpp:167-202): (energy_head [H, heads],
+    force_head [2H+K, heads])."""
+    H, K = cfg.hidden, cfg.rbf
+    e, f = np.empty(H * heads), np.empty((2 * H + K) * heads)
+    mc = cfg.c()
+    check(lib().lamm_init_heads(C.byref(mc), heads, C.c_uint64(seed), _p(e), _p(f)))
+    return e.reshape(H, heads), f.reshape(2 * H + K, heads)
 
 
 TRACE_KINDS = {"constant": 0, "uniform": 1, "lognormal": 2, "bimodal": 3}

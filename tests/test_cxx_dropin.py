@@ -25,6 +25,38 @@ def test_header_compiles_standalone(tmp_path):
     assert r.returncode == 0, r.stderr
 
 
+REF_INCLUDE = "/root/reference/proj/core/include"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_INCLUDE), reason="needs the reference headers (value types only)")
+def test_trainer_header_calls_no_reference_function(tmp_path):
+    """include/lamm_b200_trainer.hpp instantiated over the reference's value types
+    (Catalog, Subset, Sample, TrainConfig, ...) and compiled WITHOUT the reference's
+    sources: the object's undefined symbols name this library's C ABI and the C++
+    runtime only - the data layer (filter/split, normalizer fit, noise, reset_heads,
+    config validation) is native, no lamm:: function is needed to link it."""
+    src = tmp_path / "tu.cpp"
+    src.write_text(
+        "#include <lamm/trainer.hpp>\n#include \"lamm_b200_trainer.hpp\"\n"
+        "void use(const lamm::dataset::Catalog& c, const lamm::dataset::MixPlan& m,\n"
+        "         const lamm::scheduler::ScheduleConfig& s, const lamm::model::ModelConfig& mc,\n"
+        "         const lamm::trainer::TrainConfig& t, const lamm::model::Checkpoint& ck,\n"
+        "         const lamm::dataset::Subset& sub) {\n"
+        "  (void)lamm_b200::trainer::pretrain(c, m, s, mc, t);\n"
+        "  (void)lamm_b200::trainer::finetune(ck, sub, s, t);\n"
+        "  (void)lamm_b200::trainer::denoise_bench(sub, s, mc, t, 0.1);\n}\n")
+    obj = tmp_path / "tu.o"
+    r = subprocess.run(["g++", "-std=gnu++20", "-O1", "-c", "-I", REF_INCLUDE, "-I", os.path.join(ROOT, "include"),
+                        "-I", os.path.join(ROOT, "oracle", "shim"), "-o", str(obj), str(src)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    nm = subprocess.run(["nm", "-C", "--undefined-only", str(obj)], capture_output=True, text=True).stdout
+    undefined = [ln.split(None, 1)[1] for ln in nm.splitlines() if ln.strip().startswith("U ")]
+    reference = [u for u in undefined if "lamm::" in u and "lamm_b200::" not in u]
+    assert not reference, reference
+    assert any(u.startswith("lamm_fit_normalizer") for u in undefined)
+
+
 @pytest.mark.gpu
 def test_cxx_dropin_with_reference_types():
     if not os.path.exists(BIN):
