@@ -209,6 +209,9 @@ def run_ours(args, dist):
     mcfg = pk.ModelConfig(**CFG)
     dev = pk.Device(mcfg, device=gpu, seed=7)
     if dist.world > 1:
+        # NCCL's INIT lines on stderr (nranks / rank / device of every communicator)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         uid = dist.bcast_bytes(pk.comm_unique_id() if dist.rank == 0 else None)
         dev.comm_init(dist.world, dist.rank, uid)
     dev.set_reference_table(table)
@@ -229,21 +232,33 @@ def run_ours(args, dist):
         header read-back sit outside the brackets. Returns (device ms, atoms)."""
         dev.kernel_times_reset()  # also resets the step-time accumulator
         atoms = 0
+        comp.clear()
         dist.barrier()
         dev.sync()
         for k in range(K):
             dev.flush_l2(L2_FLUSH)
             r = dev.train_step_staged(k % n_steps, sync=True)
             atoms += r.n_atoms
+            if dist.world > 1:  # this rank's upload -> allreduce time (its own work)
+                comp.append(dev.last_step_compute_ms())
         dist.barrier()
         ms, nsteps = dev.step_times()
         assert nsteps == K, (nsteps, K)
         return ms, atoms
 
     # ---- timed region (device-resident inputs, no per-kernel events)
+    comp = []
     clk = ClockSampler(gpu).start()
     dev_ms, atoms_local = timed_region()
     clk.stop()
+    live_imb = None
+    if dist.world > 1:  # the north star's max/mean per-rank step time, from the concurrent ranks themselves
+        c = np.asarray(comp, np.float64)
+        cmax, csum = dist.allreduce_array(c, "max"), dist.allreduce_array(c, "sum")
+        r = cmax / (csum / dist.world)
+        live_imb = {"time_mean": float(r.mean()), "time_p95": float(np.percentile(r, 95)), "steps": int(len(r)),
+                    "per_rank_time": "device time from the step's upload to its gradient allreduce (event inside "
+                                     "the step graph), each rank; max / mean over ranks per step"}
     launches = dev.last_step_launches() * K
     ms_max = dist.allreduce(dev_ms, "max")
     atoms_all = dist.allreduce(float(atoms_local), "sum")
@@ -335,6 +350,7 @@ def run_ours(args, dist):
                           "between steps is inside the timed region)"},
         "gpu_launches": launches,
         "roofline": roof,
+        "rank_imbalance_live": live_imb,
         "kernels": kern,
         "clocks": clk.summary(),
     }

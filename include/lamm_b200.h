@@ -278,6 +278,10 @@ int lamm_flush_l2(lamm_ctx* ctx, int64_t bytes);
  * (S/trainer.cpp:319-326) applied to a host fp64 worker-summed gradient. */
 int lamm_optimizer_step(lamm_ctx* ctx, const double* grad_sum, int32_t workers, const lamm_train_config* cfg,
                         double* grad_norm);
+/* With a communicator: device time of the last synced step from its upload to the
+ * gradient allreduce (this rank's own work; max/mean over ranks = the per-rank
+ * step-time imbalance). */
+int lamm_last_step_compute_ms(lamm_ctx* ctx, double* ms);
 /* Device gradient of the last step (sum over ranks - or over the simulated workers of
  * lamm_train_step_workers, fp64 - before /G), fp64 copy. */
 int lamm_grads_get(lamm_ctx* ctx, double* flat, size_t n);

@@ -95,7 +95,7 @@ EXPORTS = [
     "lamm_checkpoint_save", "lamm_checkpoint_load", "lamm_rms_state_save", "lamm_rms_state_load",
     "lamm_subset_info", "lamm_subset_read", "lamm_train_step_workers", "lamm_ctx_get_info",
     "lamm_sample_cost", "lamm_plan_cost", "lamm_filter_max_atoms", "lamm_split_train_val", "lamm_apply_noise",
-    "lamm_pseudo_force_std", "lamm_fit_normalizer", "lamm_init_heads",
+    "lamm_pseudo_force_std", "lamm_fit_normalizer", "lamm_init_heads", "lamm_last_step_compute_ms",
 ]
 
 _lib = None

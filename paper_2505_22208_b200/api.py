@@ -290,6 +290,12 @@ class Device:
         return out
 
     # ----------------------------------------------------------- training
+    def last_step_compute_ms(self) -> float:
+        """Upload -> allreduce device time of the last synced step (communicator only)."""
+        ms = C.c_double()
+        check(lib().lamm_last_step_compute_ms(self._h, C.byref(ms)))
+        return ms.value
+
     def comm_init(self, nranks: int, rank: int, unique_id: bytes):
         buf = C.create_string_buffer(bytes(unique_id), 128)
         check(lib().lamm_comm_init(self._h, nranks, rank, buf))

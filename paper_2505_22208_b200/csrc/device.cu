@@ -164,6 +164,8 @@ struct lamm_ctx {
     int64_t launches = 0, last_step_launches = 0, graph_launches = 0;
     int flush_flip = 0;
     cudaEvent_t step_ev[2] = {};
+    cudaEvent_t coll_ev = nullptr;  // recorded inside the step just before the gradient allreduce
+    double compute_ms_last = -1.0;  // upload -> allreduce of the last synced step (communicator only)
     double step_ms_total = 0.0;
     int64_t step_count = 0;
     bool step_ev_pending = false;
@@ -865,6 +867,11 @@ StepHeader read_header(Ctx& c) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, c.step_ev[0], c.step_ev[1]));
         c.step_ms_total += ms;
+        if (c.comm) {  // this rank's own work before the allreduce (the per-rank time of the imbalance)
+            float cm = 0.f;
+            CK(cudaEventElapsedTime(&cm, c.step_ev[0], c.coll_ev));
+            c.compute_ms_last = cm;
+        }
         ++c.step_count;
         c.step_ev_pending = false;
     }
@@ -924,19 +931,33 @@ void opt_body(Ctx& c) {
     c.ops->opt(c, make_dev(c), c.opt_G, c.opt_inv_g, c.opt_clip, c.opt_lr, c.opt_decay, c.opt_eps);
 }
 
-// One train step from a staged blob (pinned host blob: H2D; resident slot:
-// D2D); returns the header after it, or a zeroed header when !sync.
-// The step after its upload: the step graph, the allreduce (G > 1), the optimizer graph.
+// The gradient allreduce over the ranks (S/trainer.cpp:319: the worker sum),
+// in place on the packed fp32 payload [grads | loss hi/lo | overflow | count].
+void allreduce_body(Ctx& c) {
+    // external: inside a capture a plain record only orders streams; this one is a
+    // real event-record node of the graph (timed against step_ev[0])
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(c.stream, &cs));
+    if (cs == cudaStreamCaptureStatusActive) CK(cudaEventRecordWithFlags(c.coll_ev, c.stream, cudaEventRecordExternal));
+    else CK(cudaEventRecord(c.coll_ev, c.stream));
+    nccl_check(nccl().all_reduce(c.grads.p, c.grads.p, static_cast<size_t>(c.NP + 4), ncclFloat32, ncclSum, c.comm,
+                                 c.stream),
+               "ncclAllReduce");
+}
+
+// The whole step after its upload as ONE graph: step -> (communicator: event +
+// ncclAllReduce, captured) -> optimizer.
 void full_body(Ctx& c) {
     step_body(c);
+    if (c.comm) allreduce_body(c);
     opt_body(c);
 }
 
 void launch_step(Ctx& c) {
     const int64_t l0 = c.launches;
-    if (c.use_graph && c.nranks == 1 && !c.profile) {
-        // one graph: the optimizer's cooperative launch follows grad_reduce with
-        // programmatic serialization like every other kernel of the step
+    if (c.use_graph && !c.profile) {
+        // one graph: the optimizer's cooperative launch follows grad_reduce (or the
+        // captured allreduce) with programmatic serialization like every other kernel
         if (c.graph_dirty) destroy_graphs(c), c.graph_dirty = false;
         if (!c.g_full) {
             c.slot_cursor = 0;
@@ -961,10 +982,7 @@ void launch_step(Ctx& c) {
         c.slot_cursor = 0;
         step_body(c);
     }
-    if (c.nranks > 1)
-        nccl_check(nccl().all_reduce(c.grads.p, c.grads.p, static_cast<size_t>(c.NP + 4), ncclFloat32, ncclSum,
-                                     c.comm, c.stream),
-                   "ncclAllReduce");
+    if (c.comm) allreduce_body(c);  // profiling pass: between the two graphs
     if (c.use_graph) CK(cudaGraphLaunch(c.g_opt, c.stream));
     else opt_body(c);
     c.last_step_launches = c.use_graph ? c.graph_launches : c.launches - l0;
@@ -1082,6 +1100,7 @@ LAMM_API int lamm_ctx_create(int device, const lamm_model_config* cfg, lamm_ctx*
             ensure_stage(*c, 1 << 20);
             for (auto& e : c->ev) CK(cudaEventCreate(&e));
             for (auto& e : c->step_ev) CK(cudaEventCreate(&e));
+            CK(cudaEventCreate(&c->coll_ev));
             ensure_capacity(*c, 1024, 64, 4096);
             // empty reference table buffers so the device pointers are valid
             bool ch = false;
@@ -1121,6 +1140,7 @@ LAMM_API void lamm_ctx_destroy(lamm_ctx* c) {
         if (e) cudaEventDestroy(e);
     for (auto& e : c->step_ev)
         if (e) cudaEventDestroy(e);
+    if (c->coll_ev) cudaEventDestroy(c->coll_ev);
     for (auto& s : c->slots) {
         if (s.a) cudaEventDestroy(s.a);
         if (s.b) cudaEventDestroy(s.b);
@@ -1503,15 +1523,15 @@ LAMM_API int lamm_comm_init(lamm_ctx* c, int nranks, int rank, const void* id128
         require(nranks >= 1 && rank >= 0 && rank < nranks, "comm_init: bad rank layout");
         require_no_chain(*c);
         CK(cudaSetDevice(c->device));
-        if (nranks == 1) {
-            c->nranks = 1, c->rank = 0;
-            return;
-        }
+        require(c->comm == nullptr, "comm_init: the context already has a communicator");
+        // a real communicator even for one rank: the step then runs the same
+        // captured allreduce as every rank of a multi-GPU job
         if (!nccl().ok) throw NcclErr("libnccl.so.2 could not be loaded");
         ncclUniqueId id;
         std::memcpy(&id, id128, sizeof(id));
         nccl_check(nccl().comm_init_rank(&c->comm, nranks, id, rank), "ncclCommInitRank");
         c->nranks = nranks, c->rank = rank;
+        c->graph_dirty = true;
     });
 }
 
@@ -1519,7 +1539,7 @@ namespace lamm_b200 {
 // simulated: lamm_train_step_workers runs every worker on this ctx and sums them itself
 void apply_train_config(Ctx& c, const lamm_train_config* tc, int32_t workers, int32_t rank, bool simulated = false) {
     require(workers >= 1 && rank >= 0 && rank < workers, "train_step: bad worker layout");
-    if (c.nranks > 1) {
+    if (c.comm) {
         require(workers == c.nranks && rank == c.rank, "train_step: workers/rank must match the communicator");
     } else if (workers > 1 && !simulated) {
         // without a communicator a workers > 1 step would apply this rank's gradient
@@ -1750,7 +1770,7 @@ LAMM_API int lamm_train_step_workers(lamm_ctx* c, const lamm_batch_view* batches
     return lamm_guard([&] {
         require(c && batches && tc, "train_step_workers: null argument");
         require(workers >= 1, "train_step_workers: workers must be >= 1");
-        require(c->nranks == 1, "train_step_workers: simulated workers need a context without a communicator");
+        require(c->comm == nullptr, "train_step_workers: simulated workers need a context without a communicator");
         require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         int64_t atoms = 0, edges = 0;
@@ -1856,6 +1876,14 @@ LAMM_API int lamm_step_times(lamm_ctx* c, double* total_ms, int64_t* steps) {
 }
 
 LAMM_API int64_t lamm_last_step_launches(lamm_ctx* c) { return c ? c->last_step_launches : -1; }
+
+LAMM_API int lamm_last_step_compute_ms(lamm_ctx* c, double* ms) {
+    return lamm_guard([&] {
+        require(c && ms, "last_step_compute_ms: null argument");
+        require(c->comm != nullptr, "last_step_compute_ms: needs a communicator (lamm_comm_init)");
+        *ms = c->compute_ms_last;
+    });
+}
 
 LAMM_API int lamm_ctx_get_info(lamm_ctx* c, const char* name, int64_t* value) {
     return lamm_guard([&] {

@@ -336,8 +336,9 @@ def test_simulated_workers_step_matches_reference(pk, oracle_ref):
 
 
 def test_nccl_allreduce_path_single_rank(pk):
-    """The data-parallel path (NCCL communicator, allreduce between the two graph
-    halves) on one rank: identical to the communicator-free step, bit for bit."""
+    """The data-parallel path on one rank: a real one-rank NCCL communicator, the
+    ncclAllReduce captured inside the single step graph (and issued between the two
+    graphs of the profiling pass): identical to the communicator-free step, bit for bit."""
     mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
     batch = cases.mixed_batch(pk, D=cases.CFG[4], seed=17, count=16)
     table = cases.random_table(cases.CFG[4], seed=6)
@@ -351,6 +352,16 @@ def test_nccl_allreduce_path_single_rank(pk):
         dev.stage(batch, _train_cfg(pk), step=2, slot=0)
         res.append(dev.train_step_staged(0, sync=True))
         res += dev.train_steps_pipelined([batch, batch], _train_cfg(pk), [3, 4])  # submit/wait with NCCL
+        dev.set_option("profile", 1)  # the per-kernel-event pass: two graphs, the allreduce between them
+        res.append(dev.train_step(batch, _train_cfg(pk), step=5))
+        dev.set_option("profile", 0)
+        if use_comm:  # the captured allreduce ran: this rank's pre-allreduce time is recorded
+            res.append(dev.train_step(batch, _train_cfg(pk), step=6))
+            assert 0.0 < dev.last_step_compute_ms() < 1e3
+        else:
+            res.append(dev.train_step(batch, _train_cfg(pk), step=6))
+            with pytest.raises(pk.InputError):
+                dev.last_step_compute_ms()
         outs.append((dev.params(), dev.grads(), [r.loss for r in res]))
         dev.close()
     assert np.array_equal(outs[0][0], outs[1][0])
