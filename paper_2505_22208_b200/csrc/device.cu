@@ -108,6 +108,8 @@ struct lamm_ctx {
     // host mirror of the current batch
     int32_t B = 0;
     int64_t N = 0;
+    int n_large = 0;  // samples of the current batch counted by k_cell_count
+    bool omit_cell_count = false;  // set while capturing g_full[0] (batches with n_large == 0)
     std::vector<int64_t> h_atom_ptr;
     std::vector<int32_t> h_Z, h_dsidx;
     std::vector<uint8_t> h_emask, h_fmask;
@@ -119,7 +121,9 @@ struct lamm_ctx {
     int grid_edge = 0, grid_emb = 0;
     // graphs
     cudaGraphExec_t g_step = nullptr, g_opt = nullptr;
-    cudaGraphExec_t g_full = nullptr;  // step + optimizer in one graph (single rank: no allreduce between)
+    // step (+ allreduce) + optimizer in one graph; [1]: with k_cell_count (batches with
+    // samples above kSmallAtoms or periodic ones), [0]: without
+    cudaGraphExec_t g_full[2] = {nullptr, nullptr};
     bool graph_dirty = true;
     bool use_graph = true, profile = false, export64 = false, pdl = true;
     bool rank_local = false;  // option "rank_local": workers > 1 without a communicator (one rank's share only)
@@ -132,7 +136,7 @@ struct lamm_ctx {
         size_t bytes = 0;
         int32_t B = 0;
         int64_t N = 0;
-        int me = 0, mf = 0;
+        int me = 0, mf = 0, n_large = 0;
     };
     std::vector<Slot> staged;
     // pipelined steps (lamm_train_step_submit / _wait): at most two in flight,
@@ -146,7 +150,7 @@ struct lamm_ctx {
         cudaEvent_t done = nullptr;
         int32_t B = 0, workers = 1, rank = 0;
         int64_t N = 0, step = 0;
-        int me = 0, mf = 0;
+        int me = 0, mf = 0, n_large = 0;
         lamm_train_config tc{};
     };
     Inflight ring[2];
@@ -599,7 +603,8 @@ struct Model {
 
     static void nlist(Ctx& c) {
         const Dev d = make_dev(c);
-        launch(c, "cell_count", k_cell_count, c.grid_warp, 256, 0, d, c.grid_edge * kPartsPerCta);
+        if (!c.omit_cell_count)  // (k_prep finalizes the CSR itself when no sample needs k_cell_count)
+            launch(c, "cell_count", k_cell_count, c.grid_warp, 256, 0, d, c.grid_edge * kPartsPerCta);
         launch(c, "nbr_fill", k_nbr_fill<K>, c.grid_warp, 256, 0, d, c.grid_edge * kPartsPerCta);
     }
 
@@ -850,7 +855,7 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
     }
     std::memcpy(base, &h, sizeof(StepHeader));
     // host mirror
-    c.B = B, c.N = N, c.me = me, c.mf = mf;
+    c.B = B, c.N = N, c.me = me, c.mf = mf, c.n_large = h.n_large;
     c.h_atom_ptr.assign(b->atom_ptr, b->atom_ptr + B + 1);
     c.h_Z.assign(b->atomic_numbers, b->atomic_numbers + N);
     c.h_dsidx.assign(ds, ds + B);
@@ -898,8 +903,9 @@ void run_nlist(Ctx& c) {
 void destroy_graphs(Ctx& c) {
     if (c.g_step) cudaGraphExecDestroy(c.g_step);
     if (c.g_opt) cudaGraphExecDestroy(c.g_opt);
-    if (c.g_full) cudaGraphExecDestroy(c.g_full);
-    c.g_step = c.g_opt = c.g_full = nullptr;
+    for (auto& g : c.g_full)
+        if (g) cudaGraphExecDestroy(g), g = nullptr;
+    c.g_step = c.g_opt = nullptr;
 }
 
 cudaGraphExec_t capture(Ctx& c, void (*body)(Ctx&)) {
@@ -959,12 +965,21 @@ void launch_step(Ctx& c) {
         // one graph: the optimizer's cooperative launch follows grad_reduce (or the
         // captured allreduce) with programmatic serialization like every other kernel
         if (c.graph_dirty) destroy_graphs(c), c.graph_dirty = false;
-        if (!c.g_full) {
+        const int variant = c.n_large > 0 ? 1 : 0;
+        cudaGraphExec_t& g = c.g_full[variant];
+        if (!g) {
             c.slot_cursor = 0;
-            c.g_full = capture(c, full_body);
+            c.omit_cell_count = variant == 0;
+            try {
+                g = capture(c, full_body);
+            } catch (...) {
+                c.omit_cell_count = false;
+                throw;
+            }
+            c.omit_cell_count = false;
             c.graph_launches = c.launches - l0;
         }
-        CK(cudaGraphLaunch(c.g_full, c.stream));
+        CK(cudaGraphLaunch(g, c.stream));
         c.last_step_launches = c.graph_launches;
         return;
     }
@@ -1589,7 +1604,7 @@ void fill_result(Ctx& c, const StepHeader& h, lamm_step_result* res) {
 // result, then the slot's completion event. Capacity growth or a graph
 // recapture first drains the stream (nothing in flight is reallocated).
 void enqueue_chained(Ctx& c, Ctx::Inflight& f) {
-    c.B = f.B, c.N = f.N, c.me = f.me, c.mf = f.mf;
+    c.B = f.B, c.N = f.N, c.me = f.me, c.mf = f.mf, c.n_large = f.n_large;
     apply_train_config(c, &f.tc, f.workers, f.rank);
     if (c.graph_dirty || f.N > c.Ncap || f.B > c.Bcap || edge_guess(f.N) > c.Pcap || f.bytes > c.d_stage.bytes)
         CK(cudaStreamSynchronize(c.stream));
@@ -1634,7 +1649,7 @@ LAMM_API int lamm_stage(lamm_ctx* c, const lamm_batch_view* b, const lamm_train_
         }
         CK(cudaMemcpyAsync(s.blob.p, c->h_stage, bytes, cudaMemcpyHostToDevice, c->stream));
         CK(cudaStreamSynchronize(c->stream));
-        s.bytes = bytes, s.B = c->B, s.N = c->N, s.me = c->me, s.mf = c->mf;
+        s.bytes = bytes, s.B = c->B, s.N = c->N, s.me = c->me, s.mf = c->mf, s.n_large = c->n_large;
         ensure_capacity(*c, c->N, c->B, edge_guess(c->N));
     });
 }
@@ -1647,7 +1662,7 @@ LAMM_API int lamm_train_step_staged(lamm_ctx* c, int32_t slot, int32_t sync, lam
         require_no_chain(*c);
         CK(cudaSetDevice(c->device));
         auto& s = c->staged[slot];
-        c->B = s.B, c->N = s.N, c->me = s.me, c->mf = s.mf;
+        c->B = s.B, c->N = s.N, c->me = s.me, c->mf = s.mf, c->n_large = s.n_large;
         c->batch_valid = false;  // the host mirror of per-atom arrays is not kept for staged batches
         const StepHeader h = run_train_step(*c, s.blob.p, s.bytes, cudaMemcpyDeviceToDevice, sync != 0);
         c->last_h2d = 0;
@@ -1722,7 +1737,7 @@ LAMM_API int lamm_train_step_submit(lamm_ctx* c, const lamm_batch_view* b, const
         std::swap(c->h_stage, f.blob);
         std::swap(c->h_stage_cap, f.cap);
         reinterpret_cast<StepHeader*>(f.blob)->chain = 1;
-        f.bytes = bytes, f.B = c->B, f.N = c->N, f.me = c->me, f.mf = c->mf;
+        f.bytes = bytes, f.B = c->B, f.N = c->N, f.me = c->me, f.mf = c->mf, f.n_large = c->n_large;
         f.step = step, f.workers = workers, f.rank = rank, f.tc = *tc;
         c->batch_valid = c->nlist_valid = c->fwd_valid = c->loss_valid = false;
         enqueue_chained(*c, f);
@@ -1745,7 +1760,7 @@ LAMM_API int lamm_train_step_wait(lamm_ctx* c, int64_t ticket, lamm_step_result*
             CK(cudaMemsetAsync(c->anomaly.as<unsigned int>() + 8, 0, sizeof(unsigned int), c->stream));
             for (int64_t t = ticket; t < c->next_ticket; ++t) {
                 auto& g = c->ring[t & 1];
-                c->B = g.B, c->N = g.N, c->me = g.me, c->mf = g.mf;
+                c->B = g.B, c->N = g.N, c->me = g.me, c->mf = g.mf, c->n_large = g.n_large;
                 apply_train_config(*c, &g.tc, g.workers, g.rank);
                 *g.result = run_train_step(*c, g.blob, g.bytes, cudaMemcpyHostToDevice, true, true);
                 if (g.result->status == 1) {  // later ones stay "skipped" and rerun at their wait
@@ -1758,7 +1773,7 @@ LAMM_API int lamm_train_step_wait(lamm_ctx* c, int64_t ticket, lamm_step_result*
         c->oldest_ticket = ticket + 1;
         if (h.status == 1 && c->oldest_ticket == c->next_ticket)  // nothing behind it: clear the poison now
             CK(cudaMemsetAsync(c->anomaly.as<unsigned int>() + 8, 0, sizeof(unsigned int), c->stream));
-        c->B = f.B, c->N = f.N, c->me = f.me, c->mf = f.mf;
+        c->B = f.B, c->N = f.N, c->me = f.me, c->mf = f.mf, c->n_large = f.n_large;
         c->last_h2d = static_cast<int64_t>(f.bytes);
         fill_result(*c, h, res);
         if (h.status == 1) throw NonFinite("non-finite loss or gradient at step " + std::to_string(f.step));
