@@ -1,4 +1,5 @@
-"""Runs a few train steps of one workload for ncu: cfg2 (default) or 'si' (4 x 1000-atom Si supercells)."""
+"""Runs a few train steps of one workload for ncu: cfg2 (default), 'si' (4 x 1000-atom
+Si supercells) or 'large' (bench.large_batch: 48 x 1000-atom supercells, > L2)."""
 import sys, os, numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -17,6 +18,9 @@ if which == "si":
                           denoise=np.zeros(1, np.uint8), cell=cell[None]))
     batch = pk.concat(parts)
     table = None
+elif which == "large":
+    batch = bench.large_batch(pk)
+    table = bench.fit_table(batch, bench.CFG["heads"])
 else:
     pool, table, sched = bench.make_workload(pk, 1)
     from paper_2505_22208_b200.dist import shard

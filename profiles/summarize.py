@@ -11,9 +11,10 @@
         utilisation and pipe activity of every kernel in an `ncu --set full`
         capture; with the step's atoms N and edges P, the algorithmic bytes of
         the edge kernels (bench.kernel_bytes) next to the measured DRAM bytes.
-    python profiles/summarize.py traffic <capture.ncu-rep> <out.json> N P slot
-        DRAM bytes per launch of each edge kernel in the capture and their ratio
-        to the algorithmic bytes (bench.py reads roofline.traffic from it).
+    python profiles/summarize.py traffic <capture.ncu-rep> <out.json> N P section
+        DRAM bytes per launch of each edge / GEMM kernel of the capture's last step
+        next to the algorithmic and compulsory bytes, merged into out.json under
+        `section` (bench.py reads roofline.traffic from it).
 """
 import collections
 import csv
@@ -137,38 +138,78 @@ def full(path, out, N=None, P=None):
     open(out, "w").write("\n".join(lines) + "\n")
 
 
-def traffic(path, out, N, P, slot):
+SHORT = {"k_edge_message": "message", "k_edge_force": "force", "k_edge_head": "head_bwd", "k_edge_bwd": "bwd_edge",
+         "k_node_gemm": "update", "k_bwd_gemm": "bwd_gemm"}
+
+
+def _merge(out, section, path, N, P, acc):
     import json
     import bench
-    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--metrics",
-                          "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True,
-                         check=True).stdout
+    doc = json.load(open(out)) if os.path.exists(out) else {}
+    res = {"source": f"ncu --set full --clock-control none (cache flush before each replayed kernel), "
+                     f"{os.path.basename(path)}; the last step's launches", "N": N, "P": P, "kernels": {}}
+    for name, (n, t, d) in acc.items():
+        alg, uniq = bench.kernel_bytes(name, N, P), bench.kernel_bytes_unique(name, N, P)
+        res["kernels"][name] = {"launches": n, "dram_bytes": t / n, "us_cold": d / n, "algorithmic_bytes": alg,
+                                "compulsory_bytes": uniq, "dram_over_algorithmic": t / n / alg,
+                                "dram_over_compulsory": t / n / uniq}
+    doc[section] = res
+    json.dump(doc, open(out, "w"), indent=1)
+
+
+def traffic_md(path, out, N, P, section):
+    rows = [ln.split("|")[1:-1] for ln in open(path) if ln.startswith("| k_")]
+    start = max(i for i, r in enumerate(rows) if r[0].strip() == "k_prep")
+    acc = collections.OrderedDict()
+    for r in rows[start:]:
+        name = SHORT.get(r[0].strip().split("<")[0])
+        if name is None:
+            continue
+        us, rd, wr = float(r[1]), float(r[2]) * 1e6, float(r[3]) * 1e6
+        n, t, d = acc.get(name, (0, 0.0, 0.0))
+        acc[name] = (n + 1, t + rd + wr, d + us)
+    _merge(out, section, path, N, P, acc)
+
+
+def traffic(path, out, N, P, section):
+    """Per edge/GEMM kernel of the LAST step in the capture: DRAM bytes per launch
+    next to SURVEY §8(d)'s algorithmic (gather-inclusive) bytes and the compulsory
+    bytes (bench.kernel_bytes / kernel_bytes_unique); merged into `out` under
+    `section` (bench.py reads roofline.traffic from it)."""
+    import json
+    import bench
+    if path.endswith(".md"):  # a `full` summary table (the capture itself stayed on the GPU box)
+        return traffic_md(path, out, N, P, section)
+    if path.endswith(".csv"):  # `ncu -i <rep> --page raw --csv` output
+        txt = open(path).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--metrics",
+                              "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
+                             capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     kn, rd, wr = hdr.index("Kernel Name"), hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-    short = {"k_edge_message": "message", "k_edge_force": "force", "k_edge_head": "head_bwd", "k_edge_bwd": "bwd_edge"}
+    du = hdr.index("gpu__time_duration.sum")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3,
+             "ns": 1e-3, "us": 1.0, "ms": 1e3}
+    short = SHORT
+    # the last step: from the last k_prep on
+    start = max(i for i, r in enumerate(data) if "k_prep" in r[kn])
     acc = collections.OrderedDict()
-    for r in data:
+    for r in data[start:]:
         name = short.get(r[kn].split("<")[0].split("(")[0].strip().split(" ")[-1])
         if name is None:
             continue
         b = float(r[rd].replace(",", "")) * scale[units[rd]] + float(r[wr].replace(",", "")) * scale[units[wr]]
-        n, t = acc.get(name, (0, 0.0))
-        acc[name] = (n + 1, t + b)
-    res = {"source": f"ncu --set full --clock-control none (cache flush before each replayed kernel), capture "
-                     f"{os.path.basename(path)}, profiles/r01_ncu_step_full.md",
-           "step": {"N": N, "P": P, "slot": slot}, "kernels": {}}
-    for name, (n, t) in acc.items():
-        alg = bench.kernel_bytes(name, N, P)
-        res["kernels"][name] = {"launches": n, "dram_bytes_per_launch": t / n, "algorithmic_bytes_per_launch": alg,
-                                "ratio": t / n / alg}
-    json.dump(res, open(out, "w"), indent=1)
+        us = float(r[du].replace(",", "")) * scale[units[du]]
+        n, t, d = acc.get(name, (0, 0.0, 0.0))
+        acc[name] = (n + 1, t + b, d + us)
+    _merge(out, section, path, N, P, acc)
 
 
 if __name__ == "__main__":
     if sys.argv[1] == "traffic":
-        traffic(sys.argv[2], sys.argv[3], int(sys.argv[4]), int(sys.argv[5]), int(sys.argv[6]))
+        traffic(sys.argv[2], sys.argv[3], int(sys.argv[4]), int(sys.argv[5]), sys.argv[6])
     elif sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
