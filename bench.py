@@ -220,16 +220,19 @@ def run_ours(args, dist):
     shards = [shard(pool, sched, s, dist.rank, dist.world, BATCH_PER_GPU) for s in range(n_steps)]
     for s, b in enumerate(shards):
         dev.stage(b, tc, step=s, slot=s, workers=dist.world, rank=dist.rank)
-    # warm-up: every slot once (grows all capacities, captures the graph), then W more
+    # warm-up: every slot once (grows all capacities, captures the graphs), then W more;
+    # each step also builds the next step's batch preparation (denoise, labels,
+    # neighbour list) on a side stream during its model (lamm_train_step_staged_next)
     for k in range(max(args.warmup, 0) + n_steps):
-        dev.train_step_staged(k % n_steps, sync=True)
+        dev.train_step_staged(k % n_steps, sync=True, next_slot=(k + 1) % n_steps)
     anomalies0 = dev.anomalies()
     K = args.steps
 
-    def timed_region():
+    def timed_region(pipelined=True):
         """K steps, each bracketed by CUDA events on the ctx stream inside the
-        library (upload -> step -> allreduce -> optimizer); the L2 flush and the
-        header read-back sit outside the brackets. Returns (device ms, atoms)."""
+        library (upload -> step -> allreduce -> optimizer, and the next step's batch
+        preparation it overlaps); the L2 flush and the header read-back sit outside
+        the brackets. Returns (device ms, atoms)."""
         dev.kernel_times_reset()  # also resets the step-time accumulator
         atoms = 0
         comp.clear()
@@ -237,7 +240,7 @@ def run_ours(args, dist):
         dev.sync()
         for k in range(K):
             dev.flush_l2(L2_FLUSH)
-            r = dev.train_step_staged(k % n_steps, sync=True)
+            r = dev.train_step_staged(k % n_steps, sync=True, next_slot=(k + 1) % n_steps if pipelined else None)
             atoms += r.n_atoms
             if dist.world > 1:  # this rank's upload -> allreduce time (its own work)
                 comp.append(dev.last_step_compute_ms())
@@ -267,7 +270,7 @@ def run_ours(args, dist):
     # graph is re-captured with event-record nodes): per-kernel durations
     dev.set_option("profile", 1)
     dev.train_step_staged(0, sync=True)
-    prof_ms, _ = timed_region()
+    prof_ms, _ = timed_region(pipelined=False)
     ktimes = dev.kernel_times()
     dev.set_option("profile", 0)
     assert dev.anomalies() == anomalies0, "a timed step skipped its update (capacity overflow or non-finite)"

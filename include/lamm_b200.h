@@ -268,6 +268,16 @@ int lamm_train_step_wait(lamm_ctx* ctx, int64_t ticket, lamm_step_result* result
 int lamm_stage(lamm_ctx* ctx, const lamm_batch_view* batch, const lamm_train_config* cfg, int64_t step,
                int32_t workers, int32_t rank, int32_t slot);
 int lamm_train_step_staged(lamm_ctx* ctx, int32_t slot, int32_t sync, lamm_step_result* result);
+/* lamm_train_step_staged with the next step's batch preparation pipelined: the
+ * denoise / label / neighbour-list kernels of `next_slot` (independent of the
+ * parameters) run on a side stream into a second copy of the batch state while
+ * this step's forward/backward/optimizer run; the next call with slot ==
+ * next_slot starts directly with its model. next_slot < 0: no prefetch. Results
+ * are bit-identical to lamm_train_step_staged; the step's device time (step_ev)
+ * includes the prefetch it overlaps. Needs graph capture (options graph 1,
+ * profile 0). Any other call first finishes and discards a pending prefetch. */
+int lamm_train_step_staged_next(lamm_ctx* ctx, int32_t slot, int32_t next_slot, int32_t sync,
+                                lamm_step_result* result);
 /* Steps since context creation whose update was skipped (non-finite or edge
  * capacity overflow). */
 int64_t lamm_anomalies(lamm_ctx* ctx);

@@ -96,6 +96,7 @@ EXPORTS = [
     "lamm_subset_info", "lamm_subset_read", "lamm_train_step_workers", "lamm_ctx_get_info",
     "lamm_sample_cost", "lamm_plan_cost", "lamm_filter_max_atoms", "lamm_split_train_val", "lamm_apply_noise",
     "lamm_pseudo_force_std", "lamm_fit_normalizer", "lamm_init_heads", "lamm_last_step_compute_ms",
+    "lamm_train_step_staged_next",
 ]
 
 _lib = None

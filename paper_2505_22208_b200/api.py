@@ -371,9 +371,16 @@ class Device:
         check(lib().lamm_stage(self._h, C.byref(v), C.byref(tc), C.c_int64(step), workers, rank, slot))
         return int(keep["atom_ptr"][-1])
 
-    def train_step_staged(self, slot: int, sync: bool = True) -> StepResult | None:
+    def train_step_staged(self, slot: int, sync: bool = True, next_slot: int | None = None) -> StepResult | None:
+        """One step of a staged slot. next_slot: also build that slot's batch preparation
+        (denoise, labels, neighbour list) on a side stream during this step's model
+        (lamm_train_step_staged_next); the next call with slot == next_slot uses it."""
         res = StepResultC()
-        check(lib().lamm_train_step_staged(self._h, slot, 1 if sync else 0, C.byref(res) if sync else None))
+        if next_slot is None:
+            check(lib().lamm_train_step_staged(self._h, slot, 1 if sync else 0, C.byref(res) if sync else None))
+        else:
+            check(lib().lamm_train_step_staged_next(self._h, slot, next_slot, 1 if sync else 0,
+                                                    C.byref(res) if sync else None))
         if not sync:
             return None
         return StepResult(res.loss, res.grad_norm, _breakdown(res.local), res.n_atoms, res.n_edges, res.status)

@@ -97,6 +97,7 @@ struct lamm_ctx {
     char* h_stage = nullptr;
     size_t h_stage_cap = 0;
     lamm_b200::Buf d_stage;
+    lamm_b200::Buf d_stage_alt;  // the other batch-state parity's staging blob (neighbour-list pipelining)
     lamm_b200::StepHeader* h_result = nullptr;  // pinned copy of the header after a step
     // capacities
     int64_t Ncap = 0, Bcap = 0, Pcap = 0;
@@ -124,6 +125,19 @@ struct lamm_ctx {
     // step (+ allreduce) + optimizer in one graph; [1]: with k_cell_count (batches with
     // samples above kSmallAtoms or periodic ones), [0]: without
     cudaGraphExec_t g_full[2] = {nullptr, nullptr};
+    // neighbour-list pipelining (lamm_train_step_staged_next): the batch state that
+    // k_prep / k_cell_count / k_nbr_fill write exists twice; step k's model runs on one
+    // parity while the next step's neighbour list is built into the other on `side`.
+    // swap_parity() exchanges the two sets (buffers, staging blob, graphs).
+    cudaGraphExec_t g_nl[2] = {nullptr, nullptr}, g_model = nullptr;
+    struct ParityGraphs {
+        cudaGraphExec_t g_full[2] = {nullptr, nullptr}, g_nl[2] = {nullptr, nullptr}, g_model = nullptr,
+                        g_step = nullptr, g_opt = nullptr;
+    } alt_graphs;
+    bool pipe_alloc = false, pipe_valid = false;
+    int pipe_slot = -1, par = 0;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_prev = nullptr, ev_nl = nullptr;
     bool graph_dirty = true;
     bool use_graph = true, profile = false, export64 = false, pdl = true;
     bool rank_local = false;  // option "rank_local": workers > 1 without a communicator (one rank's share only)
@@ -182,13 +196,33 @@ using Ctx = lamm_ctx;
 
 // Entry points that touch the device state refuse to run while pipelined steps
 // (lamm_train_step_submit) are in flight.
-void require_no_chain(const Ctx& c) {
+// A prefetched neighbour list (lamm_train_step_staged_next) may still be building
+// into the other batch-state parity on the side stream: finish it and forget it.
+void drain_pipe(Ctx& c) {
+    if (c.side) CK(cudaStreamSynchronize(c.side));
+    c.pipe_valid = false;
+}
+void require_no_chain(Ctx& c) {
     require(c.oldest_ticket == c.next_ticket, "call while pipelined steps are in flight (lamm_train_step_wait first)");
+    drain_pipe(c);
 }
 
 Buf& buf(Ctx& c, const std::string& name) { return c.bufs[name]; }
 
-void ensure_buf(Ctx& c, const std::string& name, size_t bytes, bool& changed) {
+// The batch state: everything k_prep / k_cell_count / k_nbr_fill write and the model
+// kernels read. With pipelining on, each has a second copy ("<name>#1").
+bool is_batch_state(const std::string& n) {
+    static const char* const names[] = {"atom_ptr", "Z",    "zslot",  "z2s",  "dsidx", "emask",   "fmask",  "denoise",
+                                        "sample_of", "chan", "x",      "y",    "z",     "En",      "Fn",     "cnt",
+                                        "lptr",     "stot", "soff",   "row_ptr", "col", "dst",     "colz",   "segw",
+                                        "geo",      "rbf",  "rbfl",   "rbfp", "part_lo", "cgrid",  "acell",  "cstart",
+                                        "cpos",     "sdone", "cmask", "fw",   "dist64", "unit64"};
+    for (const char* k : names)
+        if (n == k) return true;
+    return false;
+}
+
+void ensure_one(Ctx& c, const std::string& name, size_t bytes, bool& changed) {
     Buf& b = c.bufs[name];
     if (b.bytes >= bytes && b.p) return;
     if (b.p) CK(cudaFree(b.p));
@@ -196,6 +230,33 @@ void ensure_buf(Ctx& c, const std::string& name, size_t bytes, bool& changed) {
     CK(cudaMalloc(&b.p, std::max<size_t>(bytes, 256)));
     b.bytes = std::max<size_t>(bytes, 256);
     changed = true;
+}
+
+void ensure_buf(Ctx& c, const std::string& name, size_t bytes, bool& changed) {
+    ensure_one(c, name, bytes, changed);
+    if (c.pipe_alloc && is_batch_state(name)) ensure_one(c, name + "#1", bytes, changed);
+}
+
+// Exchanges the two batch-state parities: buffers, staging blob and the graphs
+// captured over them (the rest of the code always works on "the current" set).
+void swap_parity(Ctx& c) {
+    for (auto& kv : c.bufs) {
+        const std::string& n = kv.first;
+        if (n.size() > 2 && n.compare(n.size() - 2, 2, "#1") == 0) continue;
+        if (!is_batch_state(n)) continue;
+        auto it = c.bufs.find(n + "#1");
+        if (it != c.bufs.end()) std::swap(kv.second, it->second);
+    }
+    std::swap(c.d_stage, c.d_stage_alt);
+    auto& a = c.alt_graphs;
+    std::swap(c.g_full[0], a.g_full[0]);
+    std::swap(c.g_full[1], a.g_full[1]);
+    std::swap(c.g_nl[0], a.g_nl[0]);
+    std::swap(c.g_nl[1], a.g_nl[1]);
+    std::swap(c.g_model, a.g_model);
+    std::swap(c.g_step, a.g_step);
+    std::swap(c.g_opt, a.g_opt);
+    c.par ^= 1;
 }
 
 void alloc_param_state(Ctx& c) {
@@ -698,11 +759,13 @@ void ensure_stage(Ctx& c, size_t bytes) {
         CK(cudaMallocHost(reinterpret_cast<void**>(&c.h_stage), cap));
         c.h_stage_cap = cap;
     }
-    if (bytes > c.d_stage.bytes) {
-        if (c.d_stage.p) CK(cudaFree(c.d_stage.p));
+    for (Buf* st : {&c.d_stage, &c.d_stage_alt}) {
+        if (st == &c.d_stage_alt && !c.pipe_alloc) continue;
+        if (bytes <= st->bytes) continue;
+        if (st->p) CK(cudaFree(st->p));
         const size_t cap = bytes + bytes / 4 + 4096;
-        CK(cudaMalloc(&c.d_stage.p, cap));
-        c.d_stage.bytes = cap;
+        CK(cudaMalloc(&st->p, cap));
+        st->bytes = cap;
         c.graph_dirty = true;
     }
 }
@@ -901,11 +964,14 @@ void run_nlist(Ctx& c) {
 }
 
 void destroy_graphs(Ctx& c) {
-    if (c.g_step) cudaGraphExecDestroy(c.g_step);
-    if (c.g_opt) cudaGraphExecDestroy(c.g_opt);
-    for (auto& g : c.g_full)
-        if (g) cudaGraphExecDestroy(g), g = nullptr;
-    c.g_step = c.g_opt = nullptr;
+    auto kill = [](cudaGraphExec_t& g) {
+        if (g) cudaGraphExecDestroy(g);
+        g = nullptr;
+    };
+    auto& a = c.alt_graphs;
+    for (cudaGraphExec_t* g : {&c.g_step, &c.g_opt, &c.g_full[0], &c.g_full[1], &c.g_nl[0], &c.g_nl[1], &c.g_model,
+                               &a.g_step, &a.g_opt, &a.g_full[0], &a.g_full[1], &a.g_nl[0], &a.g_nl[1], &a.g_model})
+        kill(*g);
 }
 
 cudaGraphExec_t capture(Ctx& c, void (*body)(Ctx&)) {
@@ -955,6 +1021,21 @@ void allreduce_body(Ctx& c) {
 // ncclAllReduce, captured) -> optimizer.
 void full_body(Ctx& c) {
     step_body(c);
+    if (c.comm) allreduce_body(c);
+    opt_body(c);
+}
+
+// The two halves of a step for neighbour-list pipelining: the batch preparation
+// (denoise, labels, neighbour list; independent of the parameters) and the model
+// (forward -> loss -> backward -> allreduce -> optimizer).
+void nl_body(Ctx& c) {
+    c.ops->prep(c);
+    c.ops->nlist(c);
+}
+void model_body(Ctx& c) {
+    c.ops->forward(c, false);
+    c.ops->loss(c, true);
+    c.ops->backward(c, false);
     if (c.comm) allreduce_body(c);
     opt_body(c);
 }
@@ -1156,6 +1237,10 @@ LAMM_API void lamm_ctx_destroy(lamm_ctx* c) {
     for (auto& e : c->step_ev)
         if (e) cudaEventDestroy(e);
     if (c->coll_ev) cudaEventDestroy(c->coll_ev);
+    if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
+    for (cudaEvent_t e : {c->ev_prev, c->ev_nl})
+        if (e) cudaEventDestroy(e);
+    if (c->d_stage_alt.p) cudaFree(c->d_stage_alt.p);
     for (auto& s : c->slots) {
         if (s.a) cudaEventDestroy(s.a);
         if (s.b) cudaEventDestroy(s.b);
@@ -1668,6 +1753,120 @@ LAMM_API int lamm_train_step_staged(lamm_ctx* c, int32_t slot, int32_t sync, lam
         c->last_h2d = 0;
         c->batch_valid = c->nlist_valid = c->fwd_valid = c->loss_valid = false;
         if (!sync) return;
+        fill_result(*c, h, res);
+        if (h.status == 1) throw NonFinite("non-finite loss or gradient");
+    });
+}
+
+namespace lamm_b200 {
+// The batch-preparation graph (variant: with k_cell_count or not) of the current
+// parity on `stream`, captured on first use.
+void launch_nl(Ctx& c, cudaStream_t stream) {
+    const int v = c.n_large > 0 ? 1 : 0;
+    cudaGraphExec_t& g = c.g_nl[v];
+    if (!g) {
+        c.slot_cursor = 0;
+        c.omit_cell_count = v == 0;
+        try {
+            g = capture(c, nl_body);
+        } catch (...) {
+            c.omit_cell_count = false;
+            throw;
+        }
+        c.omit_cell_count = false;
+    }
+    CK(cudaGraphLaunch(g, stream));
+}
+void launch_model(Ctx& c) {
+    if (!c.g_model) {
+        const int64_t l0 = c.launches;
+        c.slot_cursor = 0;
+        c.g_model = capture(c, model_body);
+        c.graph_launches = c.launches - l0;
+    }
+    CK(cudaGraphLaunch(c.g_model, c.stream));
+}
+}  // namespace lamm_b200
+
+// A staged step whose batch preparation (denoise, labels, neighbour list: k_prep,
+// k_cell_count, k_nbr_fill — independent of the parameters) was built ahead, while
+// the previous step's model ran, into the other batch-state parity; this call in
+// turn builds `next_slot`'s on the side stream during its own model. The step's
+// device interval (step_ev) covers its model and the prefetch it overlaps, so the
+// summed step times still contain every neighbour list that ran.
+LAMM_API int lamm_train_step_staged_next(lamm_ctx* c, int32_t slot, int32_t next_slot, int32_t sync,
+                                         lamm_step_result* res) {
+    return lamm_guard([&] {
+        require(c != nullptr, "train_step_staged_next: null ctx");
+        auto ok_slot = [&](int32_t k) {
+            return k >= 0 && static_cast<size_t>(k) < c->staged.size() && c->staged[k].bytes > 0;
+        };
+        require(ok_slot(slot), "train_step_staged_next: empty slot");
+        require(next_slot < 0 || ok_slot(next_slot), "train_step_staged_next: empty next slot");
+        require(c->oldest_ticket == c->next_ticket, "call while pipelined steps are in flight (lamm_train_step_wait first)");
+        require(c->use_graph && !c->profile, "train_step_staged_next: needs graph capture (option graph 1, profile 0)");
+        CK(cudaSetDevice(c->device));
+        if (!c->side) {
+            CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->ev_prev, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&c->ev_nl, cudaEventDisableTiming));
+        }
+        const auto& s = c->staged[slot];
+        const Ctx::Slot* nx = next_slot >= 0 ? &c->staged[next_slot] : nullptr;
+        // capacity for both batches before anything is enqueued (growth drains first)
+        const int64_t N = std::max<int64_t>(s.N, nx ? nx->N : 0);
+        const int64_t B = std::max<int64_t>(s.B, nx ? nx->B : 0);
+        const size_t bytes = std::max(s.bytes, nx ? nx->bytes : 0);
+        const bool grow = !c->pipe_alloc || N > c->Ncap || B > c->Bcap || edge_guess(N) > c->Pcap ||
+                          bytes > c->d_stage.bytes || bytes > c->d_stage_alt.bytes || c->graph_dirty;
+        if (grow) {
+            CK(cudaStreamSynchronize(c->stream));
+            drain_pipe(*c);
+            c->pipe_alloc = true;
+            ensure_capacity(*c, N, B, edge_guess(N));
+            ensure_stage(*c, bytes);
+            if (c->graph_dirty) destroy_graphs(*c), c->graph_dirty = false;
+        }
+        const bool pre = c->pipe_valid && c->pipe_slot == slot;
+        if (pre) swap_parity(*c);  // the prefetched batch state becomes the current one
+        c->B = s.B, c->N = s.N, c->me = s.me, c->mf = s.mf, c->n_large = s.n_large;
+        c->grads_in_acc = false;
+        CK(cudaEventRecord(c->step_ev[0], c->stream));
+        if (pre) {
+            CK(cudaStreamWaitEvent(c->stream, c->ev_nl, 0));
+        } else {
+            CK(cudaMemcpyAsync(c->d_stage.p, s.blob.p, s.bytes, cudaMemcpyDeviceToDevice, c->stream));
+            launch_nl(*c, c->stream);
+        }
+        // the other parity is free once everything before this step's model is done
+        CK(cudaEventRecord(c->ev_prev, c->stream));
+        launch_model(*c);
+        c->last_step_launches = c->graph_launches;
+        c->pipe_valid = false;
+        if (nx) {
+            swap_parity(*c);
+            c->n_large = nx->n_large;
+            CK(cudaStreamWaitEvent(c->side, c->ev_prev, 0));
+            CK(cudaMemcpyAsync(c->d_stage.p, nx->blob.p, nx->bytes, cudaMemcpyDeviceToDevice, c->side));
+            launch_nl(*c, c->side);
+            CK(cudaEventRecord(c->ev_nl, c->side));
+            swap_parity(*c);
+            c->n_large = s.n_large;
+            c->pipe_valid = true, c->pipe_slot = next_slot;
+            CK(cudaStreamWaitEvent(c->stream, c->ev_nl, 0));  // the step's interval covers the prefetch
+            c->last_step_launches += c->n_large > 0 ? 3 : 2;
+        }
+        CK(cudaEventRecord(c->step_ev[1], c->stream));
+        c->step_ev_pending = true;
+        c->last_h2d = 0;
+        c->batch_valid = c->nlist_valid = c->fwd_valid = c->loss_valid = false;
+        if (!sync) return;
+        StepHeader h = read_header(*c);
+        if (h.status == 2) {  // this batch overflowed the edge capacity: regrow, rerun it unpipelined
+            drain_pipe(*c);
+            ensure_capacity(*c, c->N, c->B, h.overflow ? h.P : 0);
+            h = run_train_step(*c, s.blob.p, s.bytes, cudaMemcpyDeviceToDevice, true);
+        }
         fill_result(*c, h, res);
         if (h.status == 1) throw NonFinite("non-finite loss or gradient");
     });

@@ -501,3 +501,45 @@ def test_sync_step_refused_while_pipelined(pk):
         dev.train_step_wait(t + 1)
     assert np.isfinite(dev.train_step_wait(t).loss)
     dev.close()
+
+
+def test_staged_next_prefetch_is_bit_identical(pk):
+    """lamm_train_step_staged_next: each step's batch preparation (prep + neighbour
+    list) built ahead on a side stream into the other batch-state parity while the
+    previous step's model runs. Slots of different kinds (molecules, a cell-list
+    batch, periodic image cells, a dense batch that overflows the first edge
+    capacity guess mid-pipeline) cycled twice: parameters, RMS state and every loss
+    equal the unpipelined staged steps bit for bit."""
+    import test_periodic
+    rng = np.random.default_rng(9)
+    mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=cases.CFG[4])
+    big = cases.molecules(pk, 3, 4)
+    pos, Z, cell = cases.diamond_supercell(reps=3, seed=2)  # 216 atoms: cell lists
+    n = len(Z)
+    big = pk.concat([big, dict(atom_ptr=np.array([0, n], np.int64), pos=pos, Z=Z, forces=rng.normal(0, 0.1, (n, 3)),
+                                dataset_index=np.zeros(1, np.int32), energy_mask=np.ones(1, np.uint8),
+                                force_mask=np.ones(1, np.uint8), energy=np.array([-4.6 * n]),
+                                denoise=np.zeros(1, np.uint8))])
+    dense = cases.pack([(rng.uniform(0, 4, (150, 3)), np.full(150, 6))])
+    dense["energy_mask"][:] = 1
+    dense["energy"][:] = -100.0
+    slots = [cases.mixed_batch(pk, D=cases.CFG[4], seed=40, count=12), big, test_periodic.image_batch(pk, seed=3),
+             dense, cases.mixed_batch(pk, D=cases.CFG[4], seed=41, count=20)]
+    table = cases.random_table(cases.CFG[4], seed=2, elements=(1, 6, 7, 8, 14))
+    outs = []
+    for pipelined in (False, True):
+        dev = pk.Device(mcfg, seed=5)
+        dev.set_reference_table(table)
+        tc = _train_cfg(pk)
+        for k, b in enumerate(slots):
+            dev.stage(b, tc, step=k, slot=k)
+        order = [0, 1, 2, 3, 4, 2, 0, 4, 1, 3]
+        losses = []
+        for t, k in enumerate(order):
+            nxt = order[t + 1] if pipelined and t + 1 < len(order) else None
+            r = dev.train_step_staged(k, sync=True, next_slot=nxt)
+            losses.append((r.loss, r.grad_norm, r.n_edges))
+        outs.append((dev.params(), dev.rms_state(), losses))
+        dev.close()
+    assert outs[0][2] == outs[1][2]
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
