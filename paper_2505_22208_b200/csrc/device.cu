@@ -162,6 +162,7 @@ struct lamm_ctx {
         cudaEvent_t uploaded = nullptr;
         lamm_b200::StepHeader* result = nullptr;
         cudaEvent_t done = nullptr;
+        cudaEvent_t nl_done = nullptr;  // its batch preparation finished (side stream)
         int32_t B = 0, workers = 1, rank = 0;
         int64_t N = 0, step = 0;
         int me = 0, mf = 0, n_large = 0;
@@ -1231,6 +1232,7 @@ LAMM_API void lamm_ctx_destroy(lamm_ctx* c) {
         if (f.blob) cudaFreeHost(f.blob);
         if (f.result) cudaFreeHost(f.result);
         if (f.done) cudaEventDestroy(f.done);
+        if (f.nl_done) cudaEventDestroy(f.nl_done);
     }
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
@@ -1688,13 +1690,29 @@ void fill_result(Ctx& c, const StepHeader& h, lamm_step_result* res) {
 // optimizer graphs, and the read-back of its header into the slot's pinned
 // result, then the slot's completion event. Capacity growth or a graph
 // recapture first drains the stream (nothing in flight is reallocated).
+void launch_nl(Ctx& c, cudaStream_t stream);
+void launch_model(Ctx& c);
+
 void enqueue_chained(Ctx& c, Ctx::Inflight& f) {
     c.B = f.B, c.N = f.N, c.me = f.me, c.mf = f.mf, c.n_large = f.n_large;
     apply_train_config(c, &f.tc, f.workers, f.rank);
-    if (c.graph_dirty || f.N > c.Ncap || f.B > c.Bcap || edge_guess(f.N) > c.Pcap || f.bytes > c.d_stage.bytes)
+    // graphs on: the step's batch preparation runs on the side stream into the batch-
+    // state parity the in-flight step does not use, overlapping that step's model
+    const bool pipe = c.use_graph && !c.profile;
+    if (pipe && !c.side) {
+        CK(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c.ev_prev, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c.ev_nl, cudaEventDisableTiming));
+    }
+    if (c.graph_dirty || f.N > c.Ncap || f.B > c.Bcap || edge_guess(f.N) > c.Pcap || f.bytes > c.d_stage.bytes ||
+        (pipe && (!c.pipe_alloc || f.bytes > c.d_stage_alt.bytes))) {
         CK(cudaStreamSynchronize(c.stream));
+        if (c.side) CK(cudaStreamSynchronize(c.side));
+    }
+    c.pipe_valid = false;
+    if (pipe) c.pipe_alloc = true;
     ensure_capacity(c, f.N, f.B, edge_guess(f.N));
-    if (f.bytes > c.d_stage.bytes) ensure_stage(c, f.bytes);
+    ensure_stage(c, f.bytes);
     // the upload runs on the copy stream while the previous step computes; the
     // step's stream waits for it and moves the blob into the staging buffer (D2D)
     if (!c.copy_stream) CK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
@@ -1706,9 +1724,25 @@ void enqueue_chained(Ctx& c, Ctx::Inflight& f) {
     }
     CK(cudaMemcpyAsync(f.inbox.p, f.blob, f.bytes, cudaMemcpyHostToDevice, c.copy_stream));
     CK(cudaEventRecord(f.uploaded, c.copy_stream));
-    CK(cudaStreamWaitEvent(c.stream, f.uploaded, 0));
-    CK(cudaMemcpyAsync(c.d_stage.p, f.inbox.p, f.bytes, cudaMemcpyDeviceToDevice, c.stream));
-    launch_step(c);
+    if (!pipe) {
+        CK(cudaStreamWaitEvent(c.stream, f.uploaded, 0));
+        CK(cudaMemcpyAsync(c.d_stage.p, f.inbox.p, f.bytes, cudaMemcpyDeviceToDevice, c.stream));
+        launch_step(c);
+    } else {
+        if (c.graph_dirty) destroy_graphs(c), c.graph_dirty = false;
+        if (!f.nl_done) CK(cudaEventCreateWithFlags(&f.nl_done, cudaEventDisableTiming));
+        // the other parity's last user is the step before the in-flight one, already
+        // waited for (at most two in flight); the side stream keeps the order of the
+        // batch preparations
+        swap_parity(c);
+        CK(cudaStreamWaitEvent(c.side, f.uploaded, 0));
+        CK(cudaMemcpyAsync(c.d_stage.p, f.inbox.p, f.bytes, cudaMemcpyDeviceToDevice, c.side));
+        launch_nl(c, c.side);
+        CK(cudaEventRecord(f.nl_done, c.side));
+        CK(cudaStreamWaitEvent(c.stream, f.nl_done, 0));
+        launch_model(c);
+        c.last_step_launches = c.graph_launches + (c.n_large > 0 ? 3 : 2);
+    }
     CK(cudaMemcpyAsync(f.result, c.d_stage.p, sizeof(StepHeader), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaEventRecord(f.done, c.stream));
 }
@@ -1956,6 +1990,7 @@ LAMM_API int lamm_train_step_wait(lamm_ctx* c, int64_t ticket, lamm_step_result*
             // the poison, rerun this step and the later in-flight ones in order
             // (run_train_step regrows capacity until the step fits)
             CK(cudaStreamSynchronize(c->stream));
+            if (c->side) CK(cudaStreamSynchronize(c->side));
             CK(cudaMemsetAsync(c->anomaly.as<unsigned int>() + 8, 0, sizeof(unsigned int), c->stream));
             for (int64_t t = ticket; t < c->next_ticket; ++t) {
                 auto& g = c->ring[t & 1];
