@@ -250,3 +250,40 @@ def test_cfg4_periodic_supercells_vs_port(pk, oracle_port):
     assert res.n_edges == 28 * res.n_atoms  # every Si has its 4 + 12 + 12 neighbours within 5 A
     _check_step(res, dev.grads(), dev.rms_state(), ref, cases.CFG, "cfg4 periodic")
     dev.close()
+
+
+def test_cfg3_periodic_crystals_g8_b32_vs_port(pk, oracle_port):
+    """The literal cfg3 (BASELINE configs[2]): periodic crystals of 8-200 atoms (4.6-14 A
+    cells: the small ones need several images per pair), E+F / energy-only / denoising
+    subsets mixed at T = 2, one balanced mini-batch at G = 8, B = 32 through the
+    simulated-worker step vs the C port's G-worker step under the same cells
+    (parity-unpinned extension; the port's images are checked in test_periodic)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    subs = [bench.crystal_pool(pk, n, 21 + k, task, mode, dataset_index=k)
+            for k, (task, mode, n) in enumerate((("energy_and_forces", 15.0, 400), ("energy_only", 60.0, 80),
+                                                 ("denoising", 30.0, 200)))]
+    sizes = [len(b["atom_ptr"]) - 1 for b in subs]
+    osub, osam = pk.build_epoch_index(pk.temperature_counts(sizes, 2.0), sizes, seed=5)
+    offs = np.concatenate([[0], np.cumsum(sizes)])
+    pool = pk.select(pk.concat(subs), offs[osub] + osam)
+    G, B = 8, 32
+    sched = pk.plan(np.diff(pool["atom_ptr"]), G, B, 4, seed=3, mode="balanced")
+    batch = pk.select(pool, sched["sample"][:G * B])
+    assert batch["denoise"].sum() > 20 and np.diff(batch["atom_ptr"]).min() >= 8
+    D = cases.CFG[4]
+    table = cases.random_table(D, seed=8, elements=(8, 14))
+    params = oracle_port.init_params(cases.CFG, 3)
+    v0 = np.zeros_like(params)
+    tc = pk.TrainConfig(seed=19, clip_norm=1e9)
+    with oracle_port.periodic(batch["cell"]):
+        ref = oracle_port.train_step(cases.CFG, G, B, batch, table, params, v0, seed=tc.seed, step=2,
+                                     clip=tc.clip_norm)
+    mcfg = pk.ModelConfig(*cases.CFG[:3], cutoff=cases.CFG[3], heads=D)
+    dev = pk.Device(mcfg, seed=0)
+    dev.set_params(params)
+    dev.set_rms_state(v0)
+    dev.set_reference_table(table)
+    res = dev.train_step_workers([pk.select(batch, np.arange(g * B, (g + 1) * B)) for g in range(G)], tc, step=2)
+    _check_step(res, dev.grads() / G, dev.rms_state(), ref, cases.CFG, "cfg3 periodic G=8 B=32")
+    dev.close()
