@@ -609,6 +609,7 @@ struct Model {
     static constexpr size_t kGemmSmem = NodeGemmSmem<H>::bytes;
     static constexpr size_t kDwuSmem = DwuSmem<H>::bytes;
     static constexpr bool kFusedBwd = H == 128;  // k_bwd_gemm: update backward + dW_u in one kernel
+    static constexpr bool kFusedUpd = H == 128;  // k_message_update: message walk + the CTA's own update GEMM
     static size_t smem_message() { return ES::message(); }
     static size_t smem_force(int D) { return ES::force(D); }
     static size_t smem_head(int D) { return ES::head(D); }
@@ -624,6 +625,10 @@ struct Model {
         if constexpr (kFusedBwd) set_smem((const void*)k_bwd_gemm<H>, BwdGemmSmem<H>::bytes);
         set_smem((const void*)k_edge_message<H, K, true>, smem_message());
         set_smem((const void*)k_edge_message<H, K, false>, smem_message());
+        if constexpr (kFusedUpd) {
+            set_smem((const void*)k_message_update<K, true>, MsgUpdSmem<K>::bytes);
+            set_smem((const void*)k_message_update<K, false>, MsgUpdSmem<K>::bytes);
+        }
         int smem_max = 0;
         CK(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
         if (smem_head(c.D) > static_cast<size_t>(smem_max) || 3 * c.D > H)
@@ -675,6 +680,11 @@ struct Model {
         const Dev d = make_dev(c);
         if (c.L == 0) throw InputErr("model: layers == 0 is not supported by the device path");
         for (int l = 0; l < c.L; ++l) {
+            if constexpr (kFusedUpd) {  // one kernel per layer: message walk + the CTA's own update GEMM
+                launch(c, "message", l == 0 ? k_message_update<K, true> : k_message_update<K, false>, c.grid_edge,
+                       kMsgGroups * H, MsgUpdSmem<K>::bytes, d, l);
+                continue;
+            }
             launch(c, "message", l == 0 ? k_edge_message<H, K, true> : k_edge_message<H, K, false>, c.grid_edge,
                    kMsgGroups * H, smem_message(), d, l);
             launch(c, "update", k_node_gemm<H>, c.grid_upd, NodeGemmCfg<H>::NT, kGemmSmem, d, l, 0, act_map(c, d.mu[l]),

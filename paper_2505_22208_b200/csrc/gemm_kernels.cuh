@@ -300,6 +300,161 @@ __global__ void __launch_bounds__(NodeGemmCfg<H>::NT, 1) k_node_gemm(Dev d, int 
     if (warp == 0) umma::tmem_dealloc(tbase, kCols);
 }
 
+// ------------------------------------------------- message + update, fused --
+// One encoder layer in ONE kernel (H = 128, S/model.cpp:78-102): the message walk
+// of k_edge_message over the CTA's 12 edge partitions, then the update GEMM
+//   h_{l+1} = h_l + mu W_u^T,  t_{l+1} = tanh(h_{l+1})
+// for the CTA's OWN atoms - the rows its partitions cover, [a0, a1), contiguous
+// and disjoint between CTAs - on tcgen05 (3xTF32, TMEM accumulator). No grid-wide
+// dependency separates the two phases: every mu row the GEMM reads was written by
+// this CTA's walk (visible after the CTA barrier), so the update needs neither its
+// own launch nor a round trip through a dependency wait. Per 128-row tile:
+//   A = the mu rows as a SWIZZLE_128B K-major tile (raw fp32 = the tf32 hi operand,
+//       lo = x - trunc_tf32(x)) written by the threads into the walk's (dead) stage
+//       region; B = a 64-column block of W_u (hi | lo, k_pack_weights' layout) by
+//       one bulk copy - block 0 prefetched before the walk, block 1 once MMA 0 has
+//       read block 0; accumulators in TMEM columns [0, 64) and [64, 128) of the
+//       walk's allocation; epilogue: thread = (TMEM lane quarter, 16-column part).
+template <int K>
+struct MsgUpdSmem {
+    static constexpr size_t a_bytes = 4 * 2 * kGemmM * 128;      // A hi | lo
+    static constexpr size_t b_bytes = 4 * 2 * 64 * 128;          // one 64-column W_u block, hi | lo
+    static constexpr size_t walk = EdgeSmem<K, kMsgGroups, kMsgChunk>::extra_offset + 4 * 2 * 128 * K;  // + W_f tiles
+    static constexpr size_t b_off = ((walk > a_bytes + 1024 ? walk : a_bytes + 1024) + 127) / 128 * 128;
+    static constexpr size_t bar_off = b_off + b_bytes;
+    static constexpr size_t bytes = bar_off + 64;
+};
+
+template <int K, bool kZ>
+__global__ void __launch_bounds__(kMsgGroups * 128, 1) k_message_update(Dev d, int l) {
+    constexpr int H = 128, NC = 64;
+    extern __shared__ __align__(128) unsigned char lamm_edge_smem[];
+    EdgeCta<H, K, kMsgGroups, kMsgChunk> c = edge_prologue<H, K, kMsgGroups, kMsgChunk>(d, kZ);
+    using Sm = MsgUpdSmem<K>;
+    float* Bw = reinterpret_cast<float*>(lamm_edge_smem + Sm::b_off);
+    uint64_t* gb = reinterpret_cast<uint64_t*>(lamm_edge_smem + Sm::bar_off);  // [0] weights, [1..2] MMA
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int b = 0; b < 3; ++b) mbar_init(&gb[b], 1);
+        mbar_fence_init();
+    }
+    float* Wh = reinterpret_cast<float*>(c.extra);
+    const FilterTc ft = filter_setup<H, K>(d, c, l, Wh, Wh + H * K);  // TMEM: 512 columns; barrier inside
+    constexpr uint32_t kBBytes = static_cast<uint32_t>(Sm::b_bytes);
+    const float* wsrc = d.wpack + static_cast<int64_t>(4 * l) * H * H;  // the update operand blocks of layer l
+    // W_u block 0: packed by the last optimizer step (at least two kernels back, or a
+    // previous graph) - fetched before the dependency wait, overlapping the walk
+    if (tid == 0) {
+        mbar_expect_tx(&gb[0], kBBytes);
+        bulk_g2s(Bw, wsrc, kBBytes, &gb[0]);
+    }
+    MessageBody<H, K, true, kZ, kMsgChunk> b{d, kZ ? d.tanh_emb : d.t[l], d.mu[l], l, c.lt};
+    walk_edges<H, K>(d, c, b, ft);
+
+    // ---- update GEMM over this CTA's atoms
+    const int a0 = d.part_lo[blockIdx.x * kPartsPerCta], a1 = d.part_lo[(blockIdx.x + 1) * kPartsPerCta];
+    umma::fence_before();
+    __syncthreads();  // the walk's mu rows written (global), its TMEM columns and stages free
+    umma::fence_after();
+    const uint32_t tbase = *c.tslot;  // (the A tile below overwrites the walk region, slot included)
+    if (tid < 2 * kMsgGroups * kStages) {  // the walk's TMA / MMA barriers: retired before the memory is reused
+        uint64_t* wb = reinterpret_cast<uint64_t*>(lamm_edge_smem + EdgeSmem<K, kMsgGroups, kMsgChunk>::stage_bytes);
+        asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(wb + tid)) : "memory");
+    }
+    __syncthreads();
+    float* Ahi = reinterpret_cast<float*>(lamm_edge_smem +
+                                          ((1024u - (smem_u32(lamm_edge_smem) & 1023u)) & 1023u));
+    float* Alo = Ahi + kGemmM * H;
+    const int warp = tid >> 5, lane = tid & 31, quad = warp & 3, part = warp >> 2;
+    const uint32_t idesc = umma::idesc_tf32(kGemmM, NC);
+    int have = 0;                   // W_u block resident in Bw (tid 0's view)
+    uint32_t wpar = 0;              // parity of the next weights-barrier completion (tid 0)
+    bool wpend = true;              // a weights load not yet waited for (tid 0)
+    uint32_t tpar = 0;              // per-tile parity of the two MMA barriers
+    for (int r0 = a0; r0 < a1; r0 += kGemmM) {
+        const int nrows = min(kGemmM, a1 - r0);
+        // A: mu rows [r0, r0 + nrows) into the SW128 K-major tile (16 KB per 32-column block)
+#pragma unroll
+        for (int it = 0; it < kGemmM * H / 4 / (kMsgGroups * H); ++it) {
+            const int f = tid + kMsgGroups * H * it, row = f >> 5, c4 = f & 31;
+            float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (row < nrows) x = *reinterpret_cast<const float4*>(d.mu[l] + static_cast<int64_t>(r0 + row) * H + 4 * c4);
+            const int off = (c4 >> 3) * kGemmM * 32 + row * 32 + (((c4 & 7) ^ (row & 7)) << 2);
+            *reinterpret_cast<float4*>(Ahi + off) = x;
+            *reinterpret_cast<float4*>(Alo + off) = make_float4(umma::tf32_trunc_lo(x.x), umma::tf32_trunc_lo(x.y),
+                                                                umma::tf32_trunc_lo(x.z), umma::tf32_trunc_lo(x.w));
+        }
+        umma::fence_proxy_async();
+        __syncthreads();
+        if (tid == 0) {
+            for (int np = 0; np < 2; ++np) {
+                if (have != np) {
+                    // the block in Bw was read by the previous MMA group: wait for it, then reload
+                    mbar_wait(&gb[1 + have], np == 1 ? tpar : tpar ^ 1u);
+                    mbar_expect_tx(&gb[0], kBBytes);
+                    bulk_g2s(Bw, wsrc + static_cast<int64_t>(np) * 2 * NC * H, kBBytes, &gb[0]);
+                    have = np;
+                    wpend = true;
+                }
+                if (wpend) {
+                    mbar_wait(&gb[0], wpar);
+                    wpar ^= 1u;
+                    wpend = false;
+                }
+                umma::fence_after();
+                const float* Blo = Bw + NC * H;
+#pragma unroll
+                for (int s = 0; s < H / 8; ++s)
+                    umma::mma3(tbase + np * NC, umma::sw128_kdesc(Ahi, s, kGemmM), umma::sw128_kdesc(Alo, s, kGemmM),
+                               umma::kdesc(Bw, s, H), umma::kdesc(Blo, s, H), idesc, s ? 1u : 0u);
+                umma::commit(&gb[1 + np]);
+            }
+        }
+        // epilogue per column block as its MMAs land: residual h_l (layer 0: E[Z]) + D
+        const int row = quad * 32 + lane, atom = r0 + row;
+        const bool live = row < nrows;
+#pragma unroll
+        for (int np = 0; np < 2; ++np) {
+            const int c0 = np * NC + part * 16;
+            float pre[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) pre[q] = 0.f;
+            if (live) {
+                const float* p = kZ ? d.emb + static_cast<int64_t>(__ldg(d.Z + atom) - 1) * H
+                                    : d.h[l] + static_cast<int64_t>(atom) * H;
+#pragma unroll
+                for (int q = 0; q < 16; q += 4) {
+                    const float4 x = __ldg(reinterpret_cast<const float4*>(p + c0 + q));
+                    pre[q] = x.x, pre[q + 1] = x.y, pre[q + 2] = x.z, pre[q + 3] = x.w;
+                }
+            }
+            mbar_wait(&gb[1 + np], tpar);
+            umma::fence_after();
+            float v[16];
+            umma::ld16(tbase + (static_cast<uint32_t>(quad * 32) << 16) + np * NC + part * 16, v);
+            if (live) {
+                float* ho = d.h[l + 1] + static_cast<int64_t>(atom) * H + c0;
+                float* to = d.t[l + 1] + static_cast<int64_t>(atom) * H + c0;
+#pragma unroll
+                for (int q = 0; q < 16; q += 4) {
+                    const float h0 = pre[q] + v[q], h1 = pre[q + 1] + v[q + 1], h2 = pre[q + 2] + v[q + 2],
+                                h3 = pre[q + 3] + v[q + 3];
+                    *reinterpret_cast<float4*>(ho + q) = make_float4(h0, h1, h2, h3);
+                    *reinterpret_cast<float4*>(to + q) = make_float4(tanhf(h0), tanhf(h1), tanhf(h2), tanhf(h3));
+                }
+            }
+        }
+        tpar ^= 1u;
+        umma::fence_before();
+        __syncthreads();  // the tile's MMAs and TMEM reads done before A / TMEM are reused
+        umma::fence_after();
+    }
+    if (tid == 0 && wpend) mbar_wait(&gb[0], wpar);  // no tile: the prefetch still lands before exit
+    umma::fence_before();
+    __syncthreads();
+    if (tid < 32) umma::tmem_dealloc(tbase, 512);
+}
+
 // Backward of the update GEMM fused with its weight gradient (H = 128):
 //   gm = (gh W_u) (.) (1 - mu^2)        MMA1: A = the gh tile (shared, K-major canonical),
 //                                       B = W_u block (K-major, TMA)       (S/model.cpp:380-390)
