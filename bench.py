@@ -147,10 +147,13 @@ def kernel_bytes(name, N, P, H=128, K=16, D=10):
     """Algorithmic bytes per launch, SURVEY.md §8(d)'s model verbatim: fp32
     storage, gather-inclusive (every edge pays its source-row read):
       message   P (4 + 4 + 4H) + N 8H          bwd_edge  P (8 + 8H) + N 12H
+                (fused with the update GEMM at H = 128: + N 16H + 4H^2)
       force     P (20 + 4H) + N (4H + 12D)     head_bwd  P (20 + 4H + 12D) + N (8H + 12D)
     (node GEMMs: activations in + out + weights)."""
     e = {
-        "message": P * (4 + 4 + 4 * H) + N * 8 * H,
+        # k_message_update (H = 128) also runs the layer's update GEMM: + its activations
+        # (mu in, h in, h and t out) and W_u
+        "message": P * (4 + 4 + 4 * H) + N * 8 * H + N * 16 * H + 4 * H * H,
         "bwd_edge": P * (8 + 8 * H) + N * 12 * H,
         "force": P * (20 + 4 * H) + N * (4 * H + 12 * D),
         "head_bwd": P * (20 + 4 * H + 12 * D) + N * (8 * H + 12 * D),
@@ -166,7 +169,7 @@ def kernel_bytes_unique(name, N, P, H=128, K=16, D=10):
     per-atom rows once). The gap to the gather-inclusive bytes is L1/L2 reuse of
     the gathered source rows."""
     e = {
-        "message": P * (4 + 4 + 8 + 0.125) + N * (4 * H + 4 * H + 4),
+        "message": P * (4 + 4 + 8 + 0.125) + N * (4 * H + 4 * H + 4) + N * 16 * H + 4 * H * H,
         "bwd_edge": P * (4 + 4 + 8 + 0.125) + N * (4 * H + 4 * H + 8 * H + 4),
         "force": P * (4 + 4 + 16 + 8 + 0.125) + N * (4 * H + 4 * (3 * H + 3 + 3 * K) + 4),
         "head_bwd": P * (4 + 4 + 8 + 8 + 0.125) + N * (4 * H + 4 * H + 4 * H + 16 + 4),
@@ -775,15 +778,14 @@ def roofline_large(pk, mcfg, tc, steps=5):
     dev.set_reference_table(fit_table(batch, CFG["heads"]))
     dev.stage(batch, tc, step=0, slot=0)
     for _ in range(3):
-        r = dev.train_step_staged(0, sync=True)
+        r = dev.train_step_staged(0, sync=True, next_slot=0)
     P = r.n_edges
-    ms = []
-    for _ in range(steps):
+    dev.kernel_times_reset()
+    for _ in range(steps):  # the next step's batch preparation overlaps each step (as in the headline)
         dev.flush_l2(L2_FLUSH)
-        dev.event_record(0)
-        dev.train_step_staged(0, sync=False)
-        dev.event_record(1)
-        ms.append(dev.event_elapsed_ms(0, 1))
+        dev.train_step_staged(0, sync=True, next_slot=0)
+    tot_ms, nst = dev.step_times()
+    ms = [tot_ms / nst]
     dev.set_option("profile", 1)
     dev.train_step_staged(0, sync=True)
     dev.kernel_times_reset()
