@@ -1744,7 +1744,7 @@ void enqueue_chained(Ctx& c, Ctx::Inflight& f) {
         // the other parity's last user is the step before the in-flight one, already
         // waited for (at most two in flight); the side stream keeps the order of the
         // batch preparations
-        swap_parity(c);
+        swap_parity(c);  // (the ring alternates parities; a failure below leaves it swapped: still consistent)
         CK(cudaStreamWaitEvent(c.side, f.uploaded, 0));
         CK(cudaMemcpyAsync(c.d_stage.p, f.inbox.p, f.bytes, cudaMemcpyDeviceToDevice, c.side));
         launch_nl(c, c.side);
@@ -1890,10 +1890,16 @@ LAMM_API int lamm_train_step_staged_next(lamm_ctx* c, int32_t slot, int32_t next
         if (nx) {
             swap_parity(*c);
             c->n_large = nx->n_large;
-            CK(cudaStreamWaitEvent(c->side, c->ev_prev, 0));
-            CK(cudaMemcpyAsync(c->d_stage.p, nx->blob.p, nx->bytes, cudaMemcpyDeviceToDevice, c->side));
-            launch_nl(*c, c->side);
-            CK(cudaEventRecord(c->ev_nl, c->side));
+            try {
+                CK(cudaStreamWaitEvent(c->side, c->ev_prev, 0));
+                CK(cudaMemcpyAsync(c->d_stage.p, nx->blob.p, nx->bytes, cudaMemcpyDeviceToDevice, c->side));
+                launch_nl(*c, c->side);
+                CK(cudaEventRecord(c->ev_nl, c->side));
+            } catch (...) {  // keep the current step's parity current
+                swap_parity(*c);
+                c->n_large = s.n_large;
+                throw;
+            }
             swap_parity(*c);
             c->n_large = s.n_large;
             c->pipe_valid = true, c->pipe_slot = next_slot;
