@@ -138,7 +138,7 @@ def full(path, out, N=None, P=None):
     open(out, "w").write("\n".join(lines) + "\n")
 
 
-SHORT = {"k_edge_message": "message", "k_edge_force": "force", "k_edge_head": "head_bwd", "k_edge_bwd": "bwd_edge",
+SHORT = {"k_edge_message": "message", "k_message_update": "message", "k_edge_force": "force", "k_edge_head": "head_bwd", "k_edge_bwd": "bwd_edge",
          "k_node_gemm": "update", "k_bwd_gemm": "bwd_gemm"}
 
 
