@@ -579,8 +579,18 @@ def rank_imbalance_heavy(pk, dev, tc, G=8, B=4, S=64, steps=8):
     sim = {"alpha_ms": float(alpha), "beta_us_per_atom": float(beta * 1e3),
            "fit_r2": float(1 - np.sum((t - alpha - beta * a) ** 2) / np.sum((t - t.mean()) ** 2))}
     for mode in ("balanced", "naive"):
-        p = [(alpha + beta * wa).max() / (alpha + beta * wa).mean() for wa in out[mode].pop("_worker_atoms")]
-        sim[mode] = {"predicted_time_mean": float(np.mean(p)), "measured_time_mean": out[mode]["time_mean"]}
+        # the native simulator (lamm_simulate, bit-exact with S/simulator.cpp:19-59) on
+        # the timed steps' worker atoms with the fitted alpha / beta (one GPU: gamma,
+        # delta = 0): per step the slowest worker and the summed idle give max / mean
+        wa = np.concatenate(out[mode].pop("_worker_atoms"))
+        nb = len(wa) // G
+        sr = pk.simulate({"n_batches": nb, "worker_atoms": wa, "sample": np.zeros(nb * G * B, np.int64)},
+                         alpha_s=max(alpha, 0.0) * 1e-3, beta_s_per_atom=max(beta, 1e-12) * 1e-3, gamma_s=0.0,
+                         delta_s=0.0)
+        slow = sr["step_time"]
+        p = slow / (slow - sr["step_idle"] / G)
+        sim[mode] = {"predicted_time_mean": float(np.mean(p)), "measured_time_mean": out[mode]["time_mean"],
+                     "predicted_by": "lamm_simulate"}
     out["simulator_cross_check"] = sim
     trace = pk.make_trace("lognormal", count=1_000_000, min_atoms=2, max_atoms=2000, mode=20.0, sigma=1.0, seed=3)
     sched_1m = {}

@@ -397,6 +397,28 @@ int lamm_fit_normalizer(const lamm_batch_view* samples, double pseudo_force_std,
 int lamm_init_heads(const lamm_model_config* cfg, int32_t heads, uint64_t seed, double* energy_head,
                     double* force_head);
 
+/* simulator::CostModel (H/simulator.hpp:22-27) and SimResult totals. */
+typedef struct {
+    double alpha_s;          /* per-worker fixed compute */
+    double beta_s_per_atom;  /* compute per atom */
+    double gamma_s;          /* allreduce constant */
+    double delta_s;          /* penalty per high-water growth event */
+} lamm_sim_cost;
+typedef struct {
+    double total_s;
+    double throughput_samples_per_s;
+    int64_t realloc_events;
+    int64_t samples;
+} lamm_sim_totals;
+/* simulator::simulate (S/simulator.cpp:19-59) over a schedule's worker_atoms
+ * [n_batches][workers] (lamm_plan output): per-step time, idle, realloc events and
+ * max worker atoms (each output nullable), per-worker idle, totals; bit-exact with
+ * the reference. worker_cost (nullable, extension): per-worker predicted seconds
+ * [n_batches][workers] used in place of alpha + beta * atoms. */
+int lamm_simulate(const int64_t* worker_atoms, const double* worker_cost, int64_t n_batches, int32_t workers,
+                  int64_t samples_per_batch, const lamm_sim_cost* cost, double* step_time, double* step_idle,
+                  int32_t* step_realloc, int64_t* step_max_atoms, double* worker_idle, lamm_sim_totals* totals);
+
 /* ----------------------------------------------- host: data generation --- */
 /* lamm::trace::make_trace (S/trace.cpp:50-76). kind: 0 constant, 1 uniform,
  * 2 lognormal, 3 bimodal. */

@@ -194,6 +194,19 @@ class OracleLib:
                                                    _f64(sigma), scheme, _u64(seed), C.byref(out)))
         return out.value
 
+    def simulate(self, worker_atoms, n_batches, G, samples_per_batch, cost4):
+        nb = n_batches
+        o = dict(step_time=np.empty(max(nb, 1)), step_idle=np.empty(max(nb, 1)),
+                 step_realloc=np.empty(max(nb, 1), np.int32), step_max_atoms=np.empty(max(nb, 1), np.int64),
+                 worker_idle=np.empty(G), totals=np.empty(4))
+        self._check(self.lib.lref_simulate(_p(_c(worker_atoms, np.int64)), _i64(nb), G, _i64(samples_per_batch),
+                                           _p(_c(cost4, np.float64)), _p(o["step_time"]), _p(o["step_idle"]),
+                                           _p(o["step_realloc"]), _p(o["step_max_atoms"]), _p(o["worker_idle"]),
+                                           _p(o["totals"])))
+        for k in ("step_time", "step_idle", "step_realloc", "step_max_atoms"):
+            o[k] = o[k][:nb]
+        return o
+
     def reset_heads(self, cfg, params, heads, seed):
         H, L, K, rc, D = cfg
         e, f = np.empty(H * heads), np.empty((2 * H + K) * heads)

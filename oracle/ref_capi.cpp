@@ -34,6 +34,7 @@
 #include "lamm/model.hpp"
 #include "lamm/rng.hpp"
 #include "lamm/scheduler.hpp"
+#include "lamm/simulator.hpp"
 #include "lamm/trace.hpp"
 #include "lamm/trainer.hpp"
 
@@ -779,5 +780,33 @@ LREF_API int lref_reset_heads(int H, int L, int K, double rc, int D, const doubl
         const auto p = lamm::model::reset_heads(params_from_flat(cfg, params), cfg, new_heads, seed);
         std::copy(p.energy_head.data(), p.energy_head.data() + p.energy_head.size(), energy_head);
         std::copy(p.force_head.data(), p.force_head.data() + p.force_head.size(), force_head);
+    });
+}
+
+// ---- simulator (S/simulator.cpp:19-59): checker for lamm_simulate ----
+LREF_API int lref_simulate(const int64_t* worker_atoms, int64_t n_batches, int G, int64_t samples_per_batch,
+                           const double* cost4, double* step_time, double* step_idle, int32_t* step_realloc,
+                           int64_t* step_max_atoms, double* worker_idle, double* totals4) {
+    return guarded([&] {
+        lamm::scheduler::MiniBatchSchedule sch;
+        sch.workers = G;
+        for (int64_t b = 0; b < n_batches; ++b) {
+            lamm::scheduler::MiniBatch mb;
+            mb.samples.resize(static_cast<std::size_t>(samples_per_batch));
+            mb.worker_atoms.assign(worker_atoms + b * G, worker_atoms + (b + 1) * G);
+            sch.batches.push_back(std::move(mb));
+        }
+        lamm::simulator::CostModel cm;
+        cm.alpha_s = cost4[0], cm.beta_s_per_atom = cost4[1], cm.gamma_s = cost4[2], cm.delta_s = cost4[3];
+        const auto r = lamm::simulator::simulate(sch, cm);
+        for (std::size_t b = 0; b < r.steps.size(); ++b) {
+            step_time[b] = r.steps[b].time_s;
+            step_idle[b] = r.steps[b].idle_s;
+            step_realloc[b] = r.steps[b].realloc_events;
+            step_max_atoms[b] = r.steps[b].max_worker_atoms;
+        }
+        for (int g = 0; g < G; ++g) worker_idle[g] = r.worker_idle_s[static_cast<std::size_t>(g)];
+        totals4[0] = r.total_s, totals4[1] = r.throughput_samples_per_s;
+        totals4[2] = static_cast<double>(r.realloc_events), totals4[3] = static_cast<double>(r.samples);
     });
 }

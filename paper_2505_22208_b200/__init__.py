@@ -10,5 +10,5 @@ from .api import (Device, LossConfig, ModelConfig, TrainConfig, build_epoch_inde
                   concat, empty_table, greedy_assign, init_params, make_trace, mix_seed, param_count, plan,
                   rng_normals, select, synth_generate, temperature_counts, CostModel, sample_cost, plan_cost,
                   fit_cost_model, filter_max_atoms, split_train_val, apply_noise, pseudo_force_std,
-                  fit_normalizer, init_heads)
+                  fit_normalizer, init_heads, simulate)
 from ._lib import InputError, LammError, NonFiniteError, LIB_PATH  # noqa: F401

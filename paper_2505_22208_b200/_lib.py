@@ -42,6 +42,16 @@ class NormalizerC(C.Structure):
                 ("energy_std", C.c_double), ("force_std", C.c_double), ("has_energy_stats", C.c_uint8)]
 
 
+class SimCostC(C.Structure):
+    _fields_ = [("alpha_s", C.c_double), ("beta_s_per_atom", C.c_double), ("gamma_s", C.c_double),
+                ("delta_s", C.c_double)]
+
+
+class SimTotalsC(C.Structure):
+    _fields_ = [("total_s", C.c_double), ("throughput_samples_per_s", C.c_double), ("realloc_events", C.c_int64),
+                ("samples", C.c_int64)]
+
+
 class CostModelC(C.Structure):
     _fields_ = [("per_sample", C.c_double), ("per_atom", C.c_double), ("per_edge", C.c_double)]
 
@@ -96,7 +106,7 @@ EXPORTS = [
     "lamm_subset_info", "lamm_subset_read", "lamm_train_step_workers", "lamm_ctx_get_info",
     "lamm_sample_cost", "lamm_plan_cost", "lamm_filter_max_atoms", "lamm_split_train_val", "lamm_apply_noise",
     "lamm_pseudo_force_std", "lamm_fit_normalizer", "lamm_init_heads", "lamm_last_step_compute_ms",
-    "lamm_train_step_staged_next",
+    "lamm_train_step_staged_next", "lamm_simulate",
 ]
 
 _lib = None

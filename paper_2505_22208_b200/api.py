@@ -26,7 +26,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import (BatchViewC, CostModelC, NormalizerC, EvalResultC, InputError, LossBreakdownC, LossConfigC, ModelConfigC, NonFiniteError,  # noqa: F401
+from ._lib import (BatchViewC, CostModelC, NormalizerC, SimCostC, SimTotalsC, EvalResultC, InputError, LossBreakdownC, LossConfigC, ModelConfigC, NonFiniteError,  # noqa: F401
                    RefTableC, StepResultC, TrainConfigC, check, lib)
 
 
@@ -614,6 +614,31 @@ def init_heads(cfg: ModelConfig, heads: int, seed: int):
     mc = cfg.c()
     check(lib().lamm_init_heads(C.byref(mc), heads, C.c_uint64(seed), _p(e), _p(f)))
     return e.reshape(H, heads), f.reshape(2 * H + K, heads)
+
+
+def simulate(schedule: dict, alpha_s=0.005, beta_s_per_atom=1e-5, gamma_s=0.010, delta_s=0.050,
+             worker_cost=None) -> dict:
+    """simulator::simulate (S/simulator.cpp:19-59) of a plan() / plan_cost() schedule:
+    per-step time (slowest worker + gamma), idle, realloc events, max worker atoms,
+    per-worker idle and totals. worker_cost [n_batches, G] (seconds, optional): the
+    cost model's own per-worker prediction in place of alpha + beta * atoms."""
+    nb = int(schedule["n_batches"])
+    G = len(schedule["worker_atoms"]) // max(nb, 1) if nb else 1
+    wa = _c(schedule["worker_atoms"], np.int64)
+    per = len(schedule["sample"]) // max(nb, 1) if nb else 0
+    wc = None if worker_cost is None else _c(worker_cost, np.float64)
+    out = dict(step_time=np.empty(max(nb, 1)), step_idle=np.empty(max(nb, 1)),
+               step_realloc=np.empty(max(nb, 1), np.int32), step_max_atoms=np.empty(max(nb, 1), np.int64),
+               worker_idle=np.empty(G))
+    cost, tot = SimCostC(alpha_s, beta_s_per_atom, gamma_s, delta_s), SimTotalsC()
+    check(lib().lamm_simulate(_p(wa), _p(wc) if wc is not None else None, C.c_int64(nb), G, C.c_int64(per),
+                              C.byref(cost), _p(out["step_time"]), _p(out["step_idle"]), _p(out["step_realloc"]),
+                              _p(out["step_max_atoms"]), _p(out["worker_idle"]), C.byref(tot)))
+    for k in ("step_time", "step_idle", "step_realloc", "step_max_atoms"):
+        out[k] = out[k][:nb]
+    out.update(total_s=tot.total_s, throughput_samples_per_s=tot.throughput_samples_per_s,
+               realloc_events=tot.realloc_events, samples=tot.samples)
+    return out
 
 
 TRACE_KINDS = {"constant": 0, "uniform": 1, "lognormal": 2, "bimodal": 3}

@@ -553,3 +553,63 @@ LAMM_API int lamm_init_params(const lamm_model_config* c, uint64_t seed, double*
         fill((2 * H + K) * D, 1.0 / std::sqrt(static_cast<double>(2 * H + K)));
     });
 }
+
+// simulator::simulate (S/simulator.cpp:19-59): per step and worker compute =
+// alpha + beta * atoms, + delta when the worker's atoms exceed its running high
+// water; step = slowest worker + gamma. Bit-exact with the reference (the same
+// operations in the same order). worker_cost (nullable): a predicted per-worker
+// cost [n_batches][G] in seconds (lamm_plan_cost's worker_cost scaled) used in
+// place of alpha + beta * atoms (extension: the cost model's own prediction).
+LAMM_API int lamm_simulate(const int64_t* worker_atoms, const double* worker_cost, int64_t n_batches, int32_t G,
+                           int64_t samples_per_batch, const lamm_sim_cost* cost, double* step_time,
+                           double* step_idle, int32_t* step_realloc, int64_t* step_max_atoms, double* worker_idle,
+                           lamm_sim_totals* totals) {
+    return lamm_guard([&] {
+        require(worker_atoms && cost && totals, "simulate: null argument");
+        const double v[] = {cost->alpha_s, cost->beta_s_per_atom, cost->gamma_s, cost->delta_s};
+        for (double x : v)
+            require(x >= 0.0 && std::isfinite(x), "cost model: coefficients must be finite and non-negative");
+        require(cost->alpha_s + cost->beta_s_per_atom > 0.0, "cost model: compute cost must be positive");
+        require(G >= 1, "simulate: schedule has no workers");
+        std::vector<int64_t> peak(static_cast<std::size_t>(G), 0);
+        std::vector<double> busy(static_cast<std::size_t>(G)), idle_acc(static_cast<std::size_t>(G), 0.0);
+        double total = 0.0;
+        int64_t reallocs = 0, samples = 0;
+        for (int64_t b = 0; b < n_batches; ++b) {
+            double slowest = 0.0, idle = 0.0;
+            int32_t rec_realloc = 0;
+            int64_t max_atoms = 0;
+            for (int g = 0; g < G; ++g) {
+                const int64_t atoms = worker_atoms[b * G + g];
+                double t = worker_cost ? worker_cost[b * G + g]
+                                       : cost->alpha_s + cost->beta_s_per_atom * static_cast<double>(atoms);
+                if (atoms > peak[g]) {
+                    t += cost->delta_s;
+                    peak[g] = atoms;
+                    ++rec_realloc;
+                }
+                busy[g] = t;
+                slowest = std::max(slowest, t);
+                max_atoms = std::max(max_atoms, atoms);
+            }
+            const double st = slowest + cost->gamma_s;
+            for (int g = 0; g < G; ++g) {
+                const double i = slowest - busy[g];
+                idle_acc[g] += i;
+                idle += i;
+            }
+            reallocs += rec_realloc;
+            total += st;
+            samples += samples_per_batch;
+            if (step_time) step_time[b] = st;
+            if (step_idle) step_idle[b] = idle;
+            if (step_realloc) step_realloc[b] = rec_realloc;
+            if (step_max_atoms) step_max_atoms[b] = max_atoms;
+        }
+        if (worker_idle) std::copy(idle_acc.begin(), idle_acc.end(), worker_idle);
+        totals->total_s = total;
+        totals->realloc_events = reallocs;
+        totals->samples = samples;
+        totals->throughput_samples_per_s = total > 0.0 ? static_cast<double>(samples) / total : 0.0;
+    });
+}

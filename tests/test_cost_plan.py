@@ -88,3 +88,36 @@ def test_fit_recovers_linear_model(pk):
     cm, t0, r2 = pk.fit_cost_model(atoms, edges, t)
     assert t0 == pytest.approx(0.12, rel=1e-6) and cm.per_atom == pytest.approx(2e-5, rel=1e-6)
     assert cm.per_edge == pytest.approx(3e-6, rel=1e-6) and r2 > 0.999999
+
+
+@pytest.mark.parametrize("mode", ["balanced", "naive"])
+def test_simulate_bit_exact_with_reference(pk, mode):
+    """simulator::simulate (S/simulator.cpp:19-59) natively: step times, idle,
+    realloc events, per-worker idle and totals equal the reference's, bit for bit."""
+    if not ref_available():
+        pytest.skip("oracle/_ref not built")
+    from oracle import ref
+    atoms = pk.make_trace("lognormal", 20000, 2, 2000, mode=20.0, sigma=1.0, seed=7)
+    sch = pk.plan(atoms, 8, 4, 100, seed=3, mode=mode)
+    cost = (0.004, 2e-5, 0.003, 0.05)
+    got = pk.simulate(sch, *cost)
+    G, nb = 8, sch["n_batches"]
+    want = ref().simulate(sch["worker_atoms"], nb, G, 32, cost)
+    for k in ("step_time", "step_idle", "step_max_atoms", "worker_idle"):
+        assert np.array_equal(np.asarray(got[k]).view(np.uint64) if got[k].dtype == np.float64 else got[k],
+                              np.asarray(want[k]).view(np.uint64) if want[k].dtype == np.float64 else want[k]), k
+    assert np.array_equal(got["step_realloc"], want["step_realloc"])
+    assert got["total_s"] == want["totals"][0] and got["throughput_samples_per_s"] == want["totals"][1]
+    assert got["realloc_events"] == want["totals"][2] and got["samples"] == want["totals"][3]
+
+
+def test_simulate_with_predicted_worker_cost(pk):
+    rng = np.random.default_rng(1)
+    atoms = rng.integers(10, 400, 2048)
+    edges = atoms * rng.integers(10, 40, 2048)
+    cm = pk.CostModel(0.0, 1e-6, 2e-7)
+    p = pk.plan_cost(atoms, edges, cm, 4, 8, 8, seed=2, mode="balanced")
+    s = pk.simulate(p, alpha_s=0.0, beta_s_per_atom=1e-9, gamma_s=0.0, delta_s=0.0, worker_cost=p["worker_cost"])
+    wc = p["worker_cost"].reshape(-1, 4)
+    assert np.allclose(s["step_time"], wc.max(1), rtol=0, atol=0)
+    assert s["step_idle"] == pytest.approx((wc.max(1, keepdims=True) - wc).sum(1))
