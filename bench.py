@@ -231,11 +231,14 @@ def run_ours(args, dist):
     anomalies0 = dev.anomalies()
     K = args.steps
 
-    def timed_region(pipelined=True):
+    slot_atoms = [int(b["atom_ptr"][-1]) for b in shards]
+
+    def timed_region(pipelined=True, per_step_sync=True):
         """K steps, each bracketed by CUDA events on the ctx stream inside the
         library (upload -> step -> allreduce -> optimizer, and the next step's batch
-        preparation it overlaps); the L2 flush and the header read-back sit outside
-        the brackets. Returns (device ms, atoms)."""
+        preparation it overlaps); the L2 flush and the result read-back sit outside
+        the brackets (every step's result is read before the next, like the
+        reference's per-step loss check). Returns (device ms, atoms)."""
         dev.kernel_times_reset()  # also resets the step-time accumulator
         atoms = 0
         comp.clear()
@@ -243,10 +246,12 @@ def run_ours(args, dist):
         dev.sync()
         for k in range(K):
             dev.flush_l2(L2_FLUSH)
-            r = dev.train_step_staged(k % n_steps, sync=True, next_slot=(k + 1) % n_steps if pipelined else None)
-            atoms += r.n_atoms
-            if dist.world > 1:  # this rank's upload -> allreduce time (its own work)
+            dev.train_step_staged(k % n_steps, sync=per_step_sync,
+                                  next_slot=(k + 1) % n_steps if pipelined else None)
+            atoms += slot_atoms[k % n_steps]
+            if per_step_sync and dist.world > 1:  # this rank's upload -> allreduce time (its own work)
                 comp.append(dev.last_step_compute_ms())
+        dev.sync()
         dist.barrier()
         ms, nsteps = dev.step_times()
         assert nsteps == K, (nsteps, K)

@@ -182,12 +182,16 @@ struct lamm_ctx {
     std::map<std::string, std::pair<double, int64_t>> ktimes;
     int64_t launches = 0, last_step_launches = 0, graph_launches = 0;
     int flush_flip = 0;
-    cudaEvent_t step_ev[2] = {};
+    // per-step device intervals (upload -> optimizer): a ring of event pairs, so steps
+    // submitted without a sync are timed too; collected in order once complete
+    static constexpr int kStepRing = 64;
+    cudaEvent_t step_ev[kStepRing][2] = {};
+    int ring_next = 0, last_slot = -1;
+    std::vector<int> ring_pending;
     cudaEvent_t coll_ev = nullptr;  // recorded inside the step just before the gradient allreduce
     double compute_ms_last = -1.0;  // upload -> allreduce of the last synced step (communicator only)
     double step_ms_total = 0.0;
     int64_t step_count = 0;
-    bool step_ev_pending = false;
     int64_t last_h2d = 0;
 };
 
@@ -938,22 +942,51 @@ size_t pack_batch(Ctx& c, const lamm_batch_view* b, bool apply_denoise, const la
     return off;
 }
 
+void collect_step_times(Ctx& c, bool wait_all);
+// Step timing: begin / end record a ring slot's event pair on the ctx stream;
+// collect_step_times adds the completed intervals in submission order.
+int begin_step_events(Ctx& c) {
+    if (static_cast<int>(c.ring_pending.size()) == Ctx::kStepRing) {  // ring full: drain the oldest
+        CK(cudaEventSynchronize(c.step_ev[c.ring_pending.front()][1]));
+        collect_step_times(c, false);
+    }
+    const int slot = c.ring_next;
+    c.ring_next = (c.ring_next + 1) % Ctx::kStepRing;
+    CK(cudaEventRecord(c.step_ev[slot][0], c.stream));
+    return slot;
+}
+void end_step_events(Ctx& c, int slot) {
+    CK(cudaEventRecord(c.step_ev[slot][1], c.stream));
+    c.ring_pending.push_back(slot);
+    c.last_slot = slot;
+}
+void collect_step_times(Ctx& c, bool wait_all) {
+    size_t k = 0;
+    for (; k < c.ring_pending.size(); ++k) {
+        const int slot = c.ring_pending[k];
+        if (wait_all) CK(cudaEventSynchronize(c.step_ev[slot][1]));
+        else if (cudaEventQuery(c.step_ev[slot][1]) != cudaSuccess) break;
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c.step_ev[slot][0], c.step_ev[slot][1]));
+        c.step_ms_total += ms;
+        ++c.step_count;
+        if (c.comm && slot == c.last_slot && c.ring_pending.size() == k + 1) {
+            // this rank's own work before the allreduce of the last step (coll_ev is one
+            // event recorded by every step's graph: valid for the newest step only)
+            float cm = 0.f;
+            CK(cudaEventElapsedTime(&cm, c.step_ev[slot][0], c.coll_ev));
+            c.compute_ms_last = cm;
+        }
+    }
+    c.ring_pending.erase(c.ring_pending.begin(), c.ring_pending.begin() + static_cast<std::ptrdiff_t>(k));
+    (void)cudaGetLastError();  // a cudaEventQuery "not ready" is not an error
+}
+
 StepHeader read_header(Ctx& c) {
     CK(cudaMemcpyAsync(c.h_result, c.d_stage.p, sizeof(StepHeader), cudaMemcpyDeviceToHost, c.stream));
     CK(cudaStreamSynchronize(c.stream));
     collect_kernel_times(c);
-    if (c.step_ev_pending) {  // device time of the last step: upload -> optimizer, before the result D2H
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, c.step_ev[0], c.step_ev[1]));
-        c.step_ms_total += ms;
-        if (c.comm) {  // this rank's own work before the allreduce (the per-rank time of the imbalance)
-            float cm = 0.f;
-            CK(cudaEventElapsedTime(&cm, c.step_ev[0], c.coll_ev));
-            c.compute_ms_last = cm;
-        }
-        ++c.step_count;
-        c.step_ev_pending = false;
-    }
+    collect_step_times(c, true);  // device time of the steps so far: upload -> optimizer
     return *c.h_result;
 }
 
@@ -1104,11 +1137,10 @@ StepHeader run_train_step(Ctx& c, const void* src, size_t bytes, cudaMemcpyKind 
         ensure_capacity(c, c.N, c.B, edge_guess(c.N));
         if (bytes > c.d_stage.bytes) ensure_stage(c, bytes);
         if (clear_poison) CK(cudaMemsetAsync(c.anomaly.as<unsigned int>() + 8, 0, sizeof(unsigned int), c.stream));
-        CK(cudaEventRecord(c.step_ev[0], c.stream));
+        const int ts = begin_step_events(c);
         CK(cudaMemcpyAsync(c.d_stage.p, src, bytes, kind, c.stream));
         launch_step(c);
-        CK(cudaEventRecord(c.step_ev[1], c.stream));
-        c.step_ev_pending = true;
+        end_step_events(c, ts);
         if (!sync) return StepHeader{};
         const StepHeader h = read_header(c);
         if (h.status != 2) {
@@ -1206,7 +1238,8 @@ LAMM_API int lamm_ctx_create(int device, const lamm_model_config* cfg, lamm_ctx*
             CK(cudaMallocHost(reinterpret_cast<void**>(&c->h_result), sizeof(StepHeader)));
             ensure_stage(*c, 1 << 20);
             for (auto& e : c->ev) CK(cudaEventCreate(&e));
-            for (auto& e : c->step_ev) CK(cudaEventCreate(&e));
+            for (auto& pr : c->step_ev)
+                for (auto& e : pr) CK(cudaEventCreate(&e));
             CK(cudaEventCreate(&c->coll_ev));
             ensure_capacity(*c, 1024, 64, 4096);
             // empty reference table buffers so the device pointers are valid
@@ -1246,8 +1279,9 @@ LAMM_API void lamm_ctx_destroy(lamm_ctx* c) {
     }
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
-    for (auto& e : c->step_ev)
-        if (e) cudaEventDestroy(e);
+    for (auto& pr : c->step_ev)
+        for (auto& e : pr)
+            if (e) cudaEventDestroy(e);
     if (c->coll_ev) cudaEventDestroy(c->coll_ev);
     if (c->side) cudaStreamSynchronize(c->side), cudaStreamDestroy(c->side);
     for (cudaEvent_t e : {c->ev_prev, c->ev_nl})
@@ -1884,7 +1918,7 @@ LAMM_API int lamm_train_step_staged_next(lamm_ctx* c, int32_t slot, int32_t next
         if (pre) swap_parity(*c);  // the prefetched batch state becomes the current one
         c->B = s.B, c->N = s.N, c->me = s.me, c->mf = s.mf, c->n_large = s.n_large;
         c->grads_in_acc = false;
-        CK(cudaEventRecord(c->step_ev[0], c->stream));
+        const int ts = begin_step_events(*c);
         if (pre) {
             CK(cudaStreamWaitEvent(c->stream, c->ev_nl, 0));
         } else {
@@ -1915,8 +1949,7 @@ LAMM_API int lamm_train_step_staged_next(lamm_ctx* c, int32_t slot, int32_t next
             CK(cudaStreamWaitEvent(c->stream, c->ev_nl, 0));  // the step's interval covers the prefetch
             c->last_step_launches += c->n_large > 0 ? 3 : 2;
         }
-        CK(cudaEventRecord(c->step_ev[1], c->stream));
-        c->step_ev_pending = true;
+        end_step_events(*c, ts);
         c->last_h2d = 0;
         c->batch_valid = c->nlist_valid = c->fwd_valid = c->loss_valid = false;
         if (!sync) return;
@@ -2136,6 +2169,7 @@ LAMM_API int lamm_kernel_times_reset(lamm_ctx* c) {
     return lamm_guard([&] {
         require(c != nullptr, "kernel_times_reset: null ctx");
         c->ktimes.clear();
+        c->ring_pending.clear();  // intervals not yet collected belong to the old window
         c->step_ms_total = 0.0;
         c->step_count = 0;
     });
@@ -2144,6 +2178,7 @@ LAMM_API int lamm_kernel_times_reset(lamm_ctx* c) {
 LAMM_API int lamm_step_times(lamm_ctx* c, double* total_ms, int64_t* steps) {
     return lamm_guard([&] {
         require(c != nullptr, "step_times: null ctx");
+        collect_step_times(*c, true);  // steps submitted without a sync included
         if (total_ms) *total_ms = c->step_ms_total;
         if (steps) *steps = c->step_count;
     });
