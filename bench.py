@@ -560,11 +560,11 @@ def rank_imbalance_heavy(pk, dev, tc, G=8, B=4, S=64, steps=8):
             for g in range(G):
                 sub = pk.select(pool, ids[g * B:(g + 1) * B])
                 dev.stage(sub, tc, step=s, slot=950 + g, workers=G, rank=g)
-                dev.train_step_staged(950 + g, sync=True)
+                dev.train_step_staged(950 + g, sync=True, next_slot=950 + g)
                 ms = []
                 for rep in range(3):
                     dev.event_record(0)
-                    dev.train_step_staged(950 + g, sync=False)
+                    dev.train_step_staged(950 + g, sync=False, next_slot=950 + g)
                     dev.event_record(1)
                     ms.append(dev.event_elapsed_ms(0, 1))
                 times.append(min(ms))
@@ -687,7 +687,8 @@ def cost_balancing(pk, mcfg, tc, G=8, B=48, steps=6):
 def time_rank_slices(pk, dev, pool, sched, G, B, tc, steps, slot0=970):
     """Per scheduled mini-batch, each of the G ranks' B-sample slices staged and
     timed as its own device step on this GPU (min of 3, CUDA events on the ctx
-    stream); returns [(rank atoms [G], rank ms [G])] per step."""
+    stream; the next step's batch preparation built during each step, as in the
+    headline loop); returns [(rank atoms [G], rank ms [G])] per step."""
     out = []
     per = G * B
     for s in range(min(steps, sched["n_batches"])):
@@ -696,11 +697,11 @@ def time_rank_slices(pk, dev, pool, sched, G, B, tc, steps, slot0=970):
         for g in range(G):
             sub = pk.select(pool, ids[g * B:(g + 1) * B])
             dev.stage(sub, tc, step=s, slot=slot0 + g, workers=G, rank=g)
-            dev.train_step_staged(slot0 + g, sync=True)
+            dev.train_step_staged(slot0 + g, sync=True, next_slot=slot0 + g)
             ms = []
-            for _ in range(3):
+            for _ in range(3):  # as in the headline loop: the next step's batch preparation overlaps
                 dev.event_record(0)
-                dev.train_step_staged(slot0 + g, sync=False)
+                dev.train_step_staged(slot0 + g, sync=False, next_slot=slot0 + g)
                 dev.event_record(1)
                 ms.append(dev.event_elapsed_ms(0, 1))
             atoms.append(int(sub["atom_ptr"][-1]))
