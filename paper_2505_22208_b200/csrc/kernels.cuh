@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) 
 // over the grid: the exact test of k_prep's sweep against the atoms of the 27
 // neighbour cells. The warp that counts a sample's last atom scans the sample's
 // row offsets; the one that finishes the last such sample runs finalize_csr_warp.
-__global__ void __launch_bounds__(256) k_cell_count(Dev d, int Q) {
+__global__ void __launch_bounds__(256, 3) k_cell_count(Dev d, int Q) {
     __shared__ uint32_t wbits[8][kMaskWords];
     pdl_enter();
     const StepHeader& hd = *d.hdr;
