@@ -207,9 +207,11 @@ void drain_pipe(Ctx& c) {
     if (c.side) CK(cudaStreamSynchronize(c.side));
     c.pipe_valid = false;
 }
-void require_no_chain(Ctx& c) {
+// keep_prefetch: the call touches only the parameter / optimizer / gradient state,
+// which the batch preparation neither reads nor writes — a prefetched batch stays valid.
+void require_no_chain(Ctx& c, bool keep_prefetch = false) {
     require(c.oldest_ticket == c.next_ticket, "call while pipelined steps are in flight (lamm_train_step_wait first)");
-    drain_pipe(c);
+    if (!keep_prefetch) drain_pipe(c);
 }
 
 Buf& buf(Ctx& c, const std::string& name) { return c.bufs[name]; }
@@ -1322,7 +1324,7 @@ LAMM_API int lamm_ctx_set_option(lamm_ctx* c, const char* name, int64_t value) {
 LAMM_API int lamm_params_set(lamm_ctx* c, const double* flat, size_t n) {
     return lamm_guard([&] {
         require(c && flat && static_cast<int64_t>(n) == c->NP, "params_set: size mismatch");
-        require_no_chain(*c);
+        require_no_chain(*c, true);
         CK(cudaSetDevice(c->device));
         CK(cudaMemcpyAsync(c->p64.p, flat, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
         Dev d = make_dev(*c);
@@ -1337,7 +1339,7 @@ LAMM_API int lamm_params_set(lamm_ctx* c, const double* flat, size_t n) {
 LAMM_API int lamm_params_get(lamm_ctx* c, double* flat, size_t n) {
     return lamm_guard([&] {
         require(c && flat && static_cast<int64_t>(n) == c->NP, "params_get: size mismatch");
-        require_no_chain(*c);
+        require_no_chain(*c, true);
         CK(cudaSetDevice(c->device));
         CK(cudaMemcpyAsync(flat, c->p64.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -1347,7 +1349,7 @@ LAMM_API int lamm_params_get(lamm_ctx* c, double* flat, size_t n) {
 LAMM_API int lamm_rms_state_set(lamm_ctx* c, const double* flat, size_t n) {
     return lamm_guard([&] {
         require(c && flat && static_cast<int64_t>(n) == c->NP, "rms_state_set: size mismatch");
-        require_no_chain(*c);
+        require_no_chain(*c, true);
         CK(cudaSetDevice(c->device));
         CK(cudaMemcpyAsync(c->v64.p, flat, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -1357,7 +1359,7 @@ LAMM_API int lamm_rms_state_set(lamm_ctx* c, const double* flat, size_t n) {
 LAMM_API int lamm_rms_state_get(lamm_ctx* c, double* flat, size_t n) {
     return lamm_guard([&] {
         require(c && flat && static_cast<int64_t>(n) == c->NP, "rms_state_get: size mismatch");
-        require_no_chain(*c);
+        require_no_chain(*c, true);
         CK(cudaSetDevice(c->device));
         CK(cudaMemcpyAsync(flat, c->v64.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -1641,7 +1643,7 @@ LAMM_API int lamm_backward(lamm_ctx* c, const double* up_energy, const double* u
 LAMM_API int lamm_grads_get(lamm_ctx* c, double* flat, size_t n) {
     return lamm_guard([&] {
         require(c && flat && static_cast<int64_t>(n) == c->NP, "grads_get: size mismatch");
-        require_no_chain(*c);
+        require_no_chain(*c, true);
         CK(cudaSetDevice(c->device));
         if (c->grads_in_acc) {  // simulated workers: the fp64 worker sum the optimizer consumed
             CK(cudaMemcpyAsync(flat, c->g64.p, sizeof(double) * c->NP, cudaMemcpyDeviceToHost, c->stream));

@@ -128,8 +128,10 @@ def test_cfg2_bench_slots_match_reference(pk, oracle_ref):
 
 
 def test_cfg2_consecutive_staged_steps_match_reference(pk, oracle_ref):
-    """Three consecutive headline steps (graph replay, parameters and RMS state
-    carried on the device, the default clip of 10) against three reference steps."""
+    """Three consecutive headline steps exactly as bench.py runs them (graph replay,
+    the next step's batch preparation built on the side stream during each step,
+    parameters and RMS state carried on the device, the default clip of 10) against
+    three reference steps."""
     sys.path.insert(0, ROOT)
     import bench
     pool, table, sched = bench.make_workload(pk, 1)
@@ -150,7 +152,7 @@ def test_cfg2_consecutive_staged_steps_match_reference(pk, oracle_ref):
         b = shard(pool, sched, s, 0, 1, bench.BATCH_PER_GPU)
         ref = oracle_ref.train_step(cfg, 1, 256, b, table, params, v, seed=tc.seed, step=s, clip=tc.clip_norm,
                                     threads=THREADS)
-        res = dev.train_step_staged(s, sync=True)
+        res = dev.train_step_staged(s, sync=True, next_slot=(s + 1) % 3)
         _check_step(res, dev.grads(), None, ref, cfg, f"cfg2 consecutive step {s}")
         params, v = ref["params"], ref["rms_v"]
         # continue both from the reference's state so fp32 drift does not compound
