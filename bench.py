@@ -374,6 +374,7 @@ def run_ours(args, dist):
         out["semisup_cfg3"] = semisup_cfg3(pk, mcfg, tc)
         out["semisup_cfg3_periodic"] = semisup_cfg3(pk, mcfg, tc, periodic=True)
         out["cost_balancing"] = cost_balancing(pk, mcfg, tc)
+        out["batch_sweep"] = batch_sweep(pk, mcfg, tc)
         out["supercells_cfg4"] = supercells_cfg4(pk, mcfg, tc)
     if dist.rank == 0 and dist.world == 1 and not args.no_large:
         out["roofline_large"] = roofline_large(pk, mcfg, tc)
@@ -863,6 +864,29 @@ def crystal_pool(pk, count, seed, task, mode, sigma=0.5, lo=8, hi=200, dataset_i
     return pk.concat(parts)
 
 
+def batch_sweep(pk, mcfg, tc, sizes=(1, 16, 64, 256, 1024, 4096), steps=10):
+    """Throughput against the device-batch size for cfg2's molecules (the same
+    generator; one slot per size, pipelined steps, L2 flushed between steps): where
+    the fixed per-step cost (~18 kernels' critical paths) stops dominating."""
+    dev = pk.Device(mcfg, seed=7)
+    out = []
+    for n in sizes:
+        b = pk.synth_generate(n, 77, threads=os.cpu_count() or 8, **GEN)
+        dev.set_reference_table(fit_table(b, CFG["heads"]) if n > 8 else None)
+        dev.stage(b, tc, step=0, slot=0)
+        for _ in range(3):
+            r = dev.train_step_staged(0, sync=True, next_slot=0)
+        dev.kernel_times_reset()
+        for _ in range(steps):
+            dev.flush_l2(L2_FLUSH)
+            dev.train_step_staged(0, sync=True, next_slot=0)
+        ms, k = dev.step_times()
+        out.append({"molecules": n, "atoms": r.n_atoms, "edges": r.n_edges, "ms_per_step": ms / k,
+                    "atoms_per_s": r.n_atoms / (ms / k) * 1e3})
+    dev.close()
+    return out
+
+
 def semisup_cfg3(pk, mcfg, tc, G=8, B=32, steps=6, periodic=False):
     """BASELINE configs[2] (non-periodic twin): three subsets of
     reference-generator structures clamped to 8-200 atoms — E+F labeled (mode 15),
@@ -957,6 +981,7 @@ def main():
     ap.add_argument("--no-large", action="store_true", help="skip the larger-than-L2 roofline section")
     ap.add_argument("--only-large", action="store_true", help="run only the larger-than-L2 roofline section")
     ap.add_argument("--only-cost", action="store_true", help="run only the cost-model balancing section")
+    ap.add_argument("--only-sweep", action="store_true", help="run only the batch-size sweep")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -968,6 +993,10 @@ def main():
         assert "paper_2505_22208_b200" not in sys.modules, "the reference arm imported the product"
         out["product_imported"] = False
         print(json.dumps(out), flush=True)
+        return
+    if args.only_sweep:
+        import paper_2505_22208_b200 as pk
+        print(json.dumps(batch_sweep(pk, pk.ModelConfig(**CFG), pk.TrainConfig(seed=11))), flush=True)
         return
     if args.only_cost:
         import paper_2505_22208_b200 as pk
