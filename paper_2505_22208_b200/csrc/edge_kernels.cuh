@@ -493,7 +493,8 @@ struct ForceBody {
     bool kv;  // lanes 0..K-1 of warp g % (H/32): the channel-independent sums (one warp per
               // group, a different SM sub-partition per group)
     int k;
-    float Y0, Y1, Y2, U0, U1, U2, V0, V1, V2;
+    uint64_t Y01;  // (Y0, Y1) as a packed fp32 pair: one FFMA2 per edge for x and y
+    float Y2, U0, U1, U2, V0, V1, V2;
     __device__ void load(const EdgeStage<K>&, int, int j, Reg& r) const {
         r.t = __ldg(T + static_cast<int64_t>(j) * H + a);  // t[L], L >= 1 (ctx creation)
     }
@@ -503,8 +504,9 @@ struct ForceBody {
         const float mk = on ? 1.f : 0.f;
         const float fw = gv.w * mk;
         const float tf = r.t * fw;
-        Y0 = fmaf(tf, gv.x, Y0);
-        Y1 = fmaf(tf, gv.y, Y1);
+        uint64_t gxy;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(gxy) : "f"(gv.x), "f"(gv.y));
+        Y01 = ffma2(f32x2_splat(tf), gxy, Y01);
         Y2 = fmaf(tf, gv.z, Y2);
         if (kv) {  // channel-independent sums
             U0 = fmaf(fw, gv.x, U0);
@@ -516,9 +518,14 @@ struct ForceBody {
             V2 = fmaf(fr, gv.z, V2);
         }
     }
-    __device__ void begin(int) { Y0 = Y1 = Y2 = U0 = U1 = U2 = V0 = V1 = V2 = 0.f; }
+    __device__ void begin(int) {
+        Y01 = 0ull;
+        Y2 = U0 = U1 = U2 = V0 = V1 = V2 = 0.f;
+    }
     __device__ void end(int i) {
         float* y = d.Yf + static_cast<int64_t>(i) * kYW;
+        float Y0, Y1;
+        f32x2_unpack(Y01, Y0, Y1);
         y[a] = Y0, y[H + a] = Y1, y[2 * H + a] = Y2;
         if (kv && k == 0) y[3 * H] = U0, y[3 * H + 1] = U1, y[3 * H + 2] = U2;
         if (kv) y[3 * H + 3 + k] = V0, y[3 * H + 3 + K + k] = V1, y[3 * H + 3 + 2 * K + k] = V2;
