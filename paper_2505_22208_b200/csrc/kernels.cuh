@@ -590,11 +590,15 @@ __global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) 
     if (threadIdx.x == 0) d.hdr->done_counter = 0;
 }
 
-// Pair counts of the atoms of cell-list samples (kSmallAtoms < n), warp per atom
-// over the grid: the exact test of k_prep's sweep against the atoms of the 27
-// neighbour cells. The warp that counts a sample's last atom scans the sample's
-// row offsets; the one that finishes the last such sample runs finalize_csr_warp.
-__global__ void __launch_bounds__(256, 3) k_cell_count(Dev d, int Q) {
+// Pair counts of the atoms of cell-list samples (kSmallAtoms < n) and periodic
+// samples: the exact test of k_prep's sweep against the atoms of the 27 neighbour
+// cells (or every j and its images). Each warp takes a contiguous run of atoms, so
+// its atoms share their sample (per-sample data loaded once, one completion
+// atomic per run instead of one fenced atomic per atom) and mostly their neighbour
+// cells (L1). The warp that completes a sample scans the sample's row offsets;
+// the one that finishes the last such sample runs finalize_csr_warp.
+__global__ void __launch_bounds__(256, 2) k_cell_count(Dev d, int Q) {
+    constexpr int kR = 4;  // candidate rounds (32 candidates each) whose loads are in flight together
     __shared__ uint32_t wbits[8][kMaskWords];
     pdl_enter();
     const StepHeader& hd = *d.hdr;
@@ -603,62 +607,85 @@ __global__ void __launch_bounds__(256, 3) k_cell_count(Dev d, int Q) {
     const int N = hd.N;
     const int lane = threadIdx.x & 31;
     const int nw = (gridDim.x * blockDim.x) >> 5;
+    const int per = (N + nw - 1) / nw;
+    const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int i1 = min(N, (wid + 1) * per);
     const Cut cut = make_cut(d.rc);
-    for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < N; i += nw) {
+    int i = min(N, wid * per);
+    while (i < i1) {
         const int s = d.sample_of[i];
         const int lo = static_cast<int>(d.atom_ptr[s]), hi = static_cast<int>(d.atom_ptr[s + 1]);
+        const int iend = min(i1, hi);  // this warp's run of sample s
         const double* cell = sample_cell(d, s);
-        if (counted_in_prep(cell, hi - lo)) continue;
-        const Images im = sample_images(cell);
-        const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
-        int cnt = 0;
-        if (im.multi) {  // image sample: lane per source atom j, its images in a loop
-            int own = 0;
-            for (int j = lo + lane; j < hi; j += 32)
-                for_images(im, cell, xi, yi, zi, d.x[j], d.y[j], d.z[j], j == i, cut,
-                           [&](double, double, double, double) { ++own; });
-            cnt = __reduce_add_sync(0xffffffffu, own);
-        } else if (!uses_cells(cell, hi - lo)) {  // small periodic sample: minimum image, lane per j
-            int own = 0;
-            for (int j = lo + lane; j < hi; j += 32) {
-                double dx, dy, dz;
-                own += (j != i && inside(pair_sq(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz, cell), cut)) ? 1 : 0;
-            }
-            cnt = __reduce_add_sync(0xffffffffu, own);
-        } else {
-        const CellGrid g = d.cgrid[s];
-        // samples of <= 1024 atoms (one window of k_nbr_fill): the hits as a bitmask over
-        // the sample's atoms, kept for the fill (no second pass of pair tests)
-        const bool keep = hi - lo <= kMaskAtoms;
-        uint32_t* bits = wbits[threadIdx.x >> 5];
-#pragma unroll
-        for (int q = 0; q < kMaskWords / 32; ++q) bits[32 * q + lane] = 0u;
-        __syncwarp();
-        const CellWalk w = cell_walk_setup(d, g, d.acell[i]);
-        for (int t0 = 0; t0 < w.total; t0 += 32) {
-            const int k = cell_walk_slot(w, t0 + lane);
-            bool in = false;
-            int j = 0;
-            if (t0 + lane < w.total) {
-                const double4 p = d.cpos[lo + k];
-                double dx, dy, dz;
-                j = static_cast<int>(__double_as_longlong(p.w));
-                in = j != i && inside(pair_sq(xi, yi, zi, p.x, p.y, p.z, dx, dy, dz, cell), cut);
-            }
-            if (keep && in) atomicOr(bits + ((j - lo) >> 5), 1u << ((j - lo) & 31));
-            cnt += __popc(__ballot_sync(0xffffffffu, in));
+        if (counted_in_prep(cell, hi - lo)) {
+            i = iend;
+            continue;
         }
-        __syncwarp();
-        if (keep)
+        const Images im = sample_images(cell);
+        const bool cells = !im.multi && uses_cells(cell, hi - lo);
+        // samples of <= kMaskAtoms atoms: the hits as a bitmask over the sample's
+        // atoms, kept for the fill (no second pass of pair tests)
+        const bool keep = cells && hi - lo <= kMaskAtoms;
+        uint32_t* bits = wbits[threadIdx.x >> 5];
+        const int nrun = iend - i;
+        for (; i < iend; ++i) {
+            const double xi = d.x[i], yi = d.y[i], zi = d.z[i];
+            int cnt = 0;
+            if (im.multi) {  // image sample: lane per source atom j, its images in a loop
+                int own = 0;
+                for (int j = lo + lane; j < hi; j += 32)
+                    for_images(im, cell, xi, yi, zi, d.x[j], d.y[j], d.z[j], j == i, cut,
+                               [&](double, double, double, double) { ++own; });
+                cnt = __reduce_add_sync(0xffffffffu, own);
+            } else if (!cells) {  // small periodic sample: minimum image, lane per j
+                int own = 0;
+                for (int j = lo + lane; j < hi; j += 32) {
+                    double dx, dy, dz;
+                    own += (j != i && inside(pair_sq(xi, yi, zi, d.x[j], d.y[j], d.z[j], dx, dy, dz, cell), cut)) ? 1 : 0;
+                }
+                cnt = __reduce_add_sync(0xffffffffu, own);
+            } else {
+                if (keep) {
 #pragma unroll
-            for (int q = 0; q < kMaskWords / 32; ++q)
-                d.cmask[static_cast<int64_t>(i) * kMaskWords + 32 * q + lane] = bits[32 * q + lane];
+                    for (int q = 0; q < kMaskWords / 32; ++q) bits[32 * q + lane] = 0u;
+                    __syncwarp();
+                }
+                const CellWalk w = cell_walk_setup(d, d.cgrid[s], d.acell[i]);
+                for (int t0 = 0; t0 < w.total; t0 += 32 * kR) {
+                    double4 p[kR];
+#pragma unroll
+                    for (int u = 0; u < kR; ++u) {  // every lane runs the slot search (shuffles)
+                        const int t = t0 + 32 * u + lane;
+                        const int k = cell_walk_slot(w, t);
+                        if (t < w.total) p[u] = d.cpos[lo + k];
+                    }
+#pragma unroll
+                    for (int u = 0; u < kR; ++u) {
+                        bool in = false;
+                        int j = 0;
+                        if (t0 + 32 * u + lane < w.total) {
+                            double dx, dy, dz;
+                            j = static_cast<int>(__double_as_longlong(p[u].w));
+                            in = j != i && inside(pair_sq(xi, yi, zi, p[u].x, p[u].y, p[u].z, dx, dy, dz, cell), cut);
+                        }
+                        if (keep && in) atomicOr(bits + ((j - lo) >> 5), 1u << ((j - lo) & 31));
+                        cnt += __popc(__ballot_sync(0xffffffffu, in));
+                    }
+                }
+                if (keep) {
+                    __syncwarp();
+#pragma unroll
+                    for (int q = 0; q < kMaskWords / 32; ++q)
+                        d.cmask[static_cast<int64_t>(i) * kMaskWords + 32 * q + lane] = bits[32 * q + lane];
+                    __syncwarp();
+                }
+            }
+            if (lane == 0) d.cnt[i] = cnt;
         }
         unsigned last = 0;
         if (lane == 0) {
-            d.cnt[i] = cnt;
-            __threadfence();
-            last = atomicAdd(d.sdone + s, 1u) == static_cast<unsigned>(hi - lo - 1);
+            __threadfence();  // the run's counts before its completion
+            last = atomicAdd(d.sdone + s, static_cast<unsigned>(nrun)) + nrun == static_cast<unsigned>(hi - lo);
         }
         if (!__shfl_sync(0xffffffffu, last, 0)) continue;
         __threadfence();
