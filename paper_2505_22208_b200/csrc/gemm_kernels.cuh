@@ -1,18 +1,23 @@
 // gemm_kernels.cuh - the per-atom dense contractions of the step on tcgen05
 // tensor cores (3xTF32, fp32-accurate), accumulators in TMEM.
 //
-//   k_node_gemm mode 0 (update, S/model.cpp:93-102):   Y = mu_l W_u^T   (M = 128 atoms, N = H, K = H)
-//               epilogue h_{l+1} = h_l + Y, t_{l+1} = tanh h_{l+1}
-//   k_node_gemm mode 1 (S/model.cpp:380-390):          gm = (gh W_u) (.) (1 - mu^2)
-//   k_dwu              (S/model.cpp:381-383):          dW_u = gh^T mu, split-K over atoms
-//                                                       (one per-CTA partial, summed by k_grad_reduce)
+//   k_message_update (train step, H = 128; S/model.cpp:78-102): the message walk of
+//               the CTA's edge partitions, then the update GEMM of the CTA's own atoms
+//               Y = mu_l W_u^T (M = 128 atom rows per tile, two 64-column W_u blocks
+//               by TMA, 48 MMAs each), epilogue h_{l+1} = h_l + Y, t_{l+1} = tanh
+//   k_bwd_gemm  (train step, H = 128; S/model.cpp:380-390): gm = (gh W_u) (.) (1 - mu^2)
+//               fused with dW_u = gh^T mu (per-CTA partial, summed by k_grad_reduce)
+//   k_node_gemm mode 0 / 1 and k_dwu: the same contractions as separate kernels
+//               (forward / backward entry points and H != 128)
 //
-// One 128-thread CTA per SM, persistent over 128-atom tiles. The weight matrix
-// stays resident in shared memory as tf32 hi/lo K-major tiles; activations are
-// staged K-chunk by K-chunk (32 wide, double buffered) into hi/lo tiles by the
-// threads, then thread 0 issues the tcgen05.mma chain (12 per chunk) and
-// commits to an mbarrier; the epilogue reads the accumulator with tcgen05.ld
-// (thread = TMEM lane = one atom row).
+// Geometry: one CTA per SM, 512 threads (256 for H = 32) = 4 threads per TMEM lane:
+// warps w, w + 4, w + 8, w + 12 share lanes 32 (w % 4) .. + 31 and split the output
+// columns. Activation tiles arrive by TMA (SWIZZLE_128B boxes, the raw fp32 values
+// as the tf32 hi operand, lo = x - trunc_tf32(x) split in place by the threads);
+// weight blocks are K-major canonical hi/lo tiles packed by k_pack_weights / k_opt
+// and fetched with one bulk copy, before the dependency wait where the weights are
+// at least two kernels old. Thread 0 issues the MMA chain (3 per k-step of 8) and
+// commits to an mbarrier; the epilogue reads the accumulator with tcgen05.ld.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -97,11 +102,12 @@ __global__ void __launch_bounds__(256) k_opt(Dev d, int G, double inv_g, double 
     });
 }
 
-// One tile = 128 atoms x NC output columns, K = H, 256 threads: the whole
-// activation tile is staged at once (16 independent float4 loads per thread),
-// the weight block arrives by TMA, 3*H/8 MMAs accumulate into TMEM, and the
+// One tile = 128 atoms x NC output columns, K = H, NT threads (512; 256 at H = 32):
+// the activation tile arrives by TMA in 32-column SWIZZLE_128B boxes (one barrier
+// each; the threads split box kb into hi/lo while the tensor core runs box kb - 1),
+// the weight block by one bulk copy, 3*H/8 MMAs accumulate into TMEM, and the
 // epilogue inputs (residual / mu) are prefetched while the tensor core runs.
-// Warps w and w+4 share TMEM lanes 32*(w%4).. and split the NC columns.
+// The NT/32 warps share TMEM lanes 32*(w%4).. in groups of four and split the NC columns.
 template <int H>
 __global__ void __launch_bounds__(NodeGemmCfg<H>::NT, 1) k_node_gemm(Dev d, int l, int mode, const __grid_constant__ CUtensorMap amap,
                                                       const __grid_constant__ CUtensorMap omap0,
