@@ -9,8 +9,9 @@
 //   * edge metadata (j, i, unit/fcut, fcut*rbf) arrives in shared memory in
 //     64-edge chunks by TMA bulk copies (cp.async.bulk + mbarrier, double
 //     buffered);
-//   * edges are consumed in 8-edge blocks: vector reads of j/i, 8 independent
-//     coalesced source-row gathers per thread issued up front (the CSR is padded
+//   * edges are consumed in blocks of 8 (16 in the message walk): vector reads of
+//     j/i, one coalesced source-row gather per edge and thread, the next block's
+//     issued before the current one is consumed (the CSR is padded
 //     so every staged j is a valid atom), a uniform validity mask, and the
 //     per-destination segmented sum as a register accumulation flushed when the
 //     destination changes;
@@ -18,8 +19,10 @@
 //     of the layer backward runs on the tensor core: the group leader issues
 //     D[a][e] = sum_k W_f[a][k] fcut rbf[e][k] (M = 128 channels = TMEM lanes,
 //     N = 64 edges, K = 16, 3xTF32 tcgen05.mma) for chunk c+1 while the group
-//     drains chunk c, and thread a reads its filter row 8 edges at a time with
-//     tcgen05.ld 32x32b.x8.
+//     drains chunk c, and thread a reads its filter row a block at a time with
+//     tcgen05.ld 32x32b.x8 / .x16.
+// The message walk of the train step is followed, in the same kernel, by the
+// update GEMM of the CTA's own atoms (k_message_update, gemm_kernels.cuh).
 // No atomics: parameter-gradient contributions accumulate in thread-owned
 // registers / shared memory and leave each kernel as one per-CTA partial,
 // summed across CTAs in index order by k_grad_reduce.

@@ -8,7 +8,9 @@
 //
 // Reference semantics (S = /root/reference/proj/core/src):
 //   k_prep .......... S/denoise.cpp:7-29 (centering) + S/loss.cpp:113-126 (normalize)
-//                     + the per-atom pair counts of S/core.cpp:30-48
+//                     + the per-atom pair counts of S/core.cpp:30-48 (small samples)
+//                     + the cell-list binning of large ones
+//   k_cell_count .... the pair counts of cell-list, periodic and image samples
 //   k_nbr_fill ...... S/core.cpp:30-48  (bit-exact fp64 pair test, i-major, j ascending)
 //   k_energy/k_loss . S/model.cpp:208-218 + S/loss.cpp:140-213 (Eq. 5, per-rank mask denominators)
 //   k_emb_grad ...... S/model.cpp:421-424
