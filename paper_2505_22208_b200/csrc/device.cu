@@ -677,7 +677,7 @@ struct Model {
     static void nlist(Ctx& c) {
         const Dev d = make_dev(c);
         if (!c.omit_cell_count)  // (k_prep finalizes the CSR itself when no sample needs k_cell_count)
-            launch(c, "cell_count", k_cell_count, c.grid_warp, 256, 0, d, c.grid_edge * kPartsPerCta);
+            launch(c, "cell_count", k_cell_count, 2 * c.nsm, 256, 0, d, c.grid_edge * kPartsPerCta);  // one wave
         launch(c, "nbr_fill", k_nbr_fill<K>, c.grid_warp, 256, 0, d, c.grid_edge * kPartsPerCta);
     }
 

@@ -407,7 +407,7 @@ __device__ void finalize_csr_warp(const Dev& d, int Q) {
 // P / the capacity-overflow flag / row_ptr[N] / the CSR padding, so the
 // neighbour fill can place every atom's row without a separate scan kernel.
 // Q: edge-kernel partitions (k_nbr_fill cuts them while writing row_ptr).
-__global__ void __launch_bounds__(128, 2) k_prep(Dev d, BatchArrays out, int Q) {
+__global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) {
     pdl_enter();
     const StepHeader& hd = *d.hdr;
     const char* base = reinterpret_cast<const char*>(d.hdr);
