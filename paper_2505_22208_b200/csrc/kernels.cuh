@@ -874,16 +874,6 @@ __global__ void __launch_bounds__(256, 4) k_nbr_fill(Dev d, int Q) {
     }
 }
 
-template <int K>
-__device__ __forceinline__ void load_rbf(const float* __restrict__ src, float (&rb)[K]) {
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-#pragma unroll
-    for (int k = 0; k < K / 4; ++k) {
-        const float4 q = __ldg(s4 + k);
-        rb[4 * k] = q.x, rb[4 * k + 1] = q.y, rb[4 * k + 2] = q.z, rb[4 * k + 3] = q.w;
-    }
-}
-
 // ---------------------------------------------------------------- energy ---
 // Per-sample energies for every head (S/model.cpp:208-218),
 // E_s^d = sum_{i in s} sum_a W_e[a,d] h^L_ia: thread a accumulates its channel
