@@ -136,3 +136,45 @@ def test_unlabeled_batch_is_a_zero_step(pk, oracle_ref):
     assert np.array_equal(dev.params(), params)
     assert np.array_equal(dev.rms_state(), ref["rms_v"])
     dev.close()
+
+
+def test_resume_from_checkpoint_is_bit_identical(pk, tmp_path):
+    """Checkpoint / resume: parameters (LAMMCKPT, S/model.cpp:445-497) and the RMS
+    state (LAMMRMS1) saved after step 1 and loaded into a new context reproduce the
+    uninterrupted run's steps 2 and 3 bit for bit (pipelined staged steps)."""
+    from paper_2505_22208_b200 import io
+    mcfg = _mcfg(pk)
+    batches = [cases.mixed_batch(pk, D=cases.CFG[4], seed=40 + s, count=12) for s in range(3)]
+    table = cases.random_table(cases.CFG[4], seed=3)
+    tc = pk.TrainConfig(seed=13)
+
+    def run(dev, steps):
+        for s in steps:
+            dev.stage(batches[s], tc, step=s, slot=s)
+        out = []
+        for k, s in enumerate(steps):
+            nxt = steps[k + 1] if k + 1 < len(steps) else None
+            out.append(dev.train_step_staged(s, sync=True, next_slot=nxt))
+        return out
+
+    a = pk.Device(mcfg, seed=4)
+    a.set_reference_table(table)
+    run(a, [0])
+    io.save_checkpoint(str(tmp_path / "p.ckpt"), mcfg, a.params())
+    io.save_rms_state(str(tmp_path / "v.rms"), mcfg, a.rms_state())
+    ra = run(a, [1, 2])
+    pa, va = a.params(), a.rms_state()
+    a.close()
+
+    c1, p = io.load_checkpoint(str(tmp_path / "p.ckpt"))
+    c2, v = io.load_rms_state(str(tmp_path / "v.rms"))
+    assert c1 == mcfg and c2 == mcfg
+    b = pk.Device(mcfg, seed=99)  # different init: everything comes from the files
+    b.set_params(p)
+    b.set_rms_state(v)
+    b.set_reference_table(table)
+    rb = run(b, [1, 2])
+    assert [r.loss for r in ra] == [r.loss for r in rb]
+    assert np.array_equal(pa.view(np.uint64), b.params().view(np.uint64))
+    assert np.array_equal(va.view(np.uint64), b.rms_state().view(np.uint64))
+    b.close()
