@@ -51,7 +51,7 @@ typedef enum {
 typedef struct lamm_ctx lamm_ctx;
 
 /* lamm::model::ModelConfig, H/model.hpp:34-40. The sm_100a kernels are
- * instantiated for (hidden, rbf) in {(128,16), (64,16), (32,8)}; layers <= 8,
+ * instantiated for (hidden, rbf) in {(128,16), (128,8), (64,16), (64,8), (32,8), (32,16)}; layers <= 8,
  * heads <= 16. */
 typedef struct {
     int32_t hidden;

@@ -761,8 +761,11 @@ struct Model {
 
 const Ops* select_ops(int H, int K) {
     if (H == 128 && K == 16) return &Model<128, 16>::ops;
+    if (H == 128 && K == 8) return &Model<128, 8>::ops;
     if (H == 64 && K == 16) return &Model<64, 16>::ops;
+    if (H == 64 && K == 8) return &Model<64, 8>::ops;
     if (H == 32 && K == 8) return &Model<32, 8>::ops;
+    if (H == 32 && K == 16) return &Model<32, 16>::ops;
     return nullptr;
 }
 
@@ -1221,7 +1224,7 @@ LAMM_API int lamm_ctx_create(int device, const lamm_model_config* cfg, lamm_ctx*
         require(cfg->layers >= 1 && cfg->layers <= kMaxLayers, "model: device path supports 1..8 layers");
         require(cfg->heads <= kMaxHeads, "model: device path supports at most 16 heads");
         const Ops* ops = select_ops(cfg->hidden, cfg->rbf);
-        require(ops != nullptr, "model: (hidden, rbf) must be one of (128,16), (64,16), (32,8)");
+        require(ops != nullptr, "model: (hidden, rbf) must be one of (128, 8|16), (64, 8|16), (32, 8|16)");
         int ndev = 0;
         CK(cudaGetDeviceCount(&ndev));
         require(device >= 0 && device < ndev, "ctx_create: no such CUDA device");

@@ -194,11 +194,14 @@ def test_train_step_matches_oracle(pk, oracle_ref):
     dev.close()
 
 
-@pytest.mark.parametrize("cfg", [(64, 2, 16, 5.0, 3), (32, 1, 8, 4.0, 3)])
+@pytest.mark.parametrize("cfg", [(64, 2, 16, 5.0, 3), (32, 1, 8, 4.0, 3), (64, 2, 8, 4.5, 2), (32, 2, 16, 5.0, 1),
+                                 (128, 2, 8, 5.0, 3)])
 def test_train_step_other_model_sizes(pk, oracle_ref, cfg):
-    """The other device instantiations (hidden 64 / rbf 16 and hidden 32 / rbf 8:
-    unfused update backward + split-K dW_u GEMM, FFMA filter) through a full step,
-    with samples above the cell-list threshold."""
+    """The other device instantiations through a full step, with samples above the
+    cell-list threshold: hidden 64 / 32 (unfused update backward + split-K dW_u GEMM,
+    FFMA filter) and hidden 128 with 8 Gaussians (the tensor-core filter with one
+    K-step, the fused layer and update-backward kernels); the reference's
+    own default is hidden 64 / rbf 16 / 2 layers / 1 head."""
     mcfg = pk.ModelConfig(*cfg[:3], cutoff=cfg[3], heads=cfg[4])
     dev = pk.Device(mcfg, seed=0)
     params = oracle_ref.init_params(cfg, 21)
