@@ -2206,6 +2206,7 @@ LAMM_API int lamm_ctx_get_info(lamm_ctx* c, const char* name, int64_t* value) {
         if (n == "grid_edge") *value = c->grid_edge;
         else if (n == "parts_per_cta") *value = kPartsPerCta;
         else if (n == "chunk_edges") *value = kChunk;
+        else if (n == "atom_cost") *value = kAtomCost;
         else if (n == "message_groups") *value = kMsgGroups;
         else if (n == "message_block") *value = MessageBody<128, 16, true, false>::kBlock;
         else if (n == "edge_groups") *value = kGroups;

@@ -754,6 +754,12 @@ __device__ __forceinline__ void emit_pair(const Dev& d, int p, int i, int j, dou
 // consecutive j, the exact test over the neighbour cells sets bit j of a per-warp
 // shared-memory mask, the set bits are listed in ascending j (one mask word per
 // lane, warp scan of the popcounts) and the lanes emit the listed pairs.
+// The edge walks cost ~0.1 us per edge and ~0.4-0.5 us per destination atom (its
+// segment flush and per-atom loads) per group (%globaltimer fit on the layer
+// backward at cfg2): a 4-edge weight per atom in the partition cut. Measured: cfg2
+// step -0.6 %, the 28-edges-per-atom supercell batch +0.8 % (profiles/README.md).
+constexpr int kAtomCost = 4;
+
 template <int K>
 __global__ void __launch_bounds__(256, 4) k_nbr_fill(Dev d, int Q) {
     constexpr int kWin = 1024;
@@ -788,15 +794,19 @@ __global__ void __launch_bounds__(256, 4) k_nbr_fill(Dev d, int Q) {
             const int ci = d.cnt[i];
             d.row_ptr[i] = base;
             if (ci > 0) atomicOr(d.segw + (base >> 5), 1u << (base & 31));
-            // edge-kernel partitions: part_lo[q] = first atom with row_ptr >= floor(P q / Q)
+            // edge-kernel partitions balanced on the walk's cost, kAtomCost edges' worth per
+            // atom (its begin / end) plus one per edge: with x_i = row_ptr[i] + kAtomCost i
+            // and T = P + kAtomCost N, part_lo[q] = first atom with x_i >= floor(T q / Q)
             if (P > 0) {
-                const int64_t prev = i == 0 ? -1 : base - d.cnt[i - 1];  // row_ptr[i - 1]
-                const int64_t qlo = i == 0 ? 0 : ((prev + 1) * Q + P - 1) / P;
-                int64_t qhi = ((static_cast<int64_t>(base) + 1) * Q + P - 1) / P - 1;
+                const int64_t T = P + static_cast<int64_t>(kAtomCost) * N;
+                const int64_t x = static_cast<int64_t>(base) + static_cast<int64_t>(kAtomCost) * i;
+                const int64_t xprev = i == 0 ? -1 : x - d.cnt[i - 1] - kAtomCost;  // x_{i-1}
+                const int64_t qlo = i == 0 ? 0 : ((xprev + 1) * Q + T - 1) / T;
+                int64_t qhi = ((x + 1) * Q + T - 1) / T - 1;
                 if (qhi > Q - 1) qhi = Q - 1;
                 for (int64_t q = qlo; q <= qhi; ++q) d.part_lo[q] = i;
-                if (i == N - 1)  // targets in (row_ptr[N-1], P] start at atom N
-                    for (int64_t q = ((static_cast<int64_t>(base) + 1) * Q + P - 1) / P; q < Q; ++q) d.part_lo[q] = N;
+                if (i == N - 1)  // targets in (x_{N-1}, T] start at atom N
+                    for (int64_t q = ((x + 1) * Q + T - 1) / T; q < Q; ++q) d.part_lo[q] = N;
             }
         }
         const Images im = sample_images(cell);

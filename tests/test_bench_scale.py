@@ -61,21 +61,23 @@ def row_ptr_of(dev, batch):
     return np.concatenate([[0], np.cumsum(counts)])
 
 
-def max_chunks_per_group(row_ptr, Q, groups, parts_per_cta, block, chunk):
-    """Replays k_nbr_fill's edge-balanced cut (part_lo[q] = the atom whose row holds
-    edge floor-ish(P q / Q), kernels.cuh) and walk_edges' chunking (chunks start on
-    whole blocks): the largest number of staged chunks any group walks."""
+def max_chunks_per_group(row_ptr, Q, groups, parts_per_cta, block, chunk, atom_cost):
+    """Replays k_nbr_fill's cost-balanced cut (x_i = row_ptr[i] + atom_cost i,
+    T = P + atom_cost N, part_lo[q] = first atom with x_i >= floor(T q / Q),
+    kernels.cuh) and walk_edges' chunking (chunks start on whole blocks): the largest
+    number of staged chunks any group walks."""
     N, P = len(row_ptr) - 1, int(row_ptr[-1])
+    T = P + atom_cost * N
     part_lo = np.zeros(Q + 1, np.int64)
     part_lo[Q] = N
     for i in range(N):
-        base = int(row_ptr[i])
-        qlo = 0 if i == 0 else ((int(row_ptr[i - 1]) + 1) * Q + P - 1) // P
-        qhi = min(((base + 1) * Q + P - 1) // P - 1, Q - 1)
+        x = int(row_ptr[i]) + atom_cost * i
+        qlo = 0 if i == 0 else ((int(row_ptr[i - 1]) + atom_cost * (i - 1) + 1) * Q + T - 1) // T
+        qhi = min(((x + 1) * Q + T - 1) // T - 1, Q - 1)
         if qhi >= qlo:
             part_lo[qlo:qhi + 1] = i
         if i == N - 1:
-            part_lo[((base + 1) * Q + P - 1) // P:Q] = N
+            part_lo[((x + 1) * Q + T - 1) // T:Q] = N
     per = parts_per_cta // groups
     best = 0
     for q0 in range(0, Q, per):
@@ -104,7 +106,7 @@ def test_cfg2_bench_slots_match_reference(pk, oracle_ref):
     tc = pk.TrainConfig(seed=11, clip_norm=1e9)
     dev = pk.Device(mcfg, seed=7)
     geo = {k: dev.info(k) for k in ("grid_edge", "parts_per_cta", "chunk_edges", "message_groups", "message_block",
-                                    "edge_groups", "edge_block")}
+                                    "edge_groups", "edge_block", "atom_cost")}
     Q = geo["grid_edge"] * geo["parts_per_cta"]
     for s in picks:
         b = shards[s]
@@ -113,7 +115,7 @@ def test_cfg2_bench_slots_match_reference(pk, oracle_ref):
         if s == picks[0]:  # the steady-state restage path (k + 2 < nchunks) runs
             assert atoms[s] > 5000
             for g, blk in ((geo["message_groups"], geo["message_block"]), (geo["edge_groups"], geo["edge_block"])):
-                nch = max_chunks_per_group(rp, Q, g, geo["parts_per_cta"], blk, geo["chunk_edges"])
+                nch = max_chunks_per_group(rp, Q, g, geo["parts_per_cta"], blk, geo["chunk_edges"], geo["atom_cost"])
                 assert nch >= 3, (g, blk, nch)
         ref = oracle_ref.train_step(cfg, 1, 256, b, table, params, v0, seed=tc.seed, step=s, clip=tc.clip_norm,
                                     threads=THREADS)
