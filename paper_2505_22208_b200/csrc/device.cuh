@@ -101,7 +101,7 @@ struct Dev {
     int32_t* colz;             // [P] Z_j - 1 of each edge's source (layer-0 message rows)
     int32_t *lptr, *stot, *soff;  // per-atom row offset inside its sample, per-sample edge totals / offsets
     uint32_t* segw;            // bit p set: edge p is the first of its destination atom
-    int32_t* part_lo;          // [Q+1] edge-balanced atom partitions (edge kernels)
+    int32_t* part_lo;          // [Q+1] atom partitions of the edge kernels, balanced on edges + kAtomCost per atom
     // cell lists of the large samples (k_prep bins, k_cell_count / k_nbr_fill walk)
     CellGrid* cgrid;           // [B]
     int32_t* acell;            // [N]  linear cell of the atom inside its sample's grid

@@ -2,7 +2,7 @@
 // message, force head, head backward, layer backward), sm_100a.
 //
 // Shape of every kernel: the CSR edge list (grouped by destination atom i, j
-// ascending) is cut by k_nbr_fill into Q = gridDim.x * 12 edge-balanced
+// ascending) is cut by k_nbr_fill into Q = gridDim.x * 12 cost-balanced (edges + 4 per atom)
 // partitions of whole atoms. A CTA runs kGroups independent "groups" of H
 // threads; thread a of a group owns feature channel a. A group walks its
 // partition's edges in order:
