@@ -33,6 +33,12 @@ namespace lamm_b200 {
 
 constexpr double kPiD = 3.14159265358979323846;
 
+// Release / acquire fence at GPU scope for the "last block" and grid-barrier
+// patterns (writes -> fence -> counter atomic; counter atomic -> fence -> reads):
+// acq_rel suffices there, and it is cheaper than __threadfence()'s sequentially
+// consistent MEMBAR.SC.GPU.
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // All kernels share one dynamic shared-memory symbol (extern __shared__ arrays
 // of different element types would otherwise collide).
 template <class T>
@@ -582,12 +588,12 @@ __global__ void __launch_bounds__(128, 4) k_prep(Dev d, BatchArrays out, int Q) 
     }
     // the last block: offsets of the samples, P, overflow, row_ptr[N], padding —
     // unless cell-list samples are still to be counted (k_cell_count does it then)
-    __threadfence();
+    fence_gpu();
     __syncthreads();
     if (threadIdx.x == 0) last = atomicAdd(&d.hdr->done_counter, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!last) return;
-    __threadfence();
+    fence_gpu();
     if (hd.n_large == 0 && threadIdx.x < 32) finalize_csr_warp(d, Q);
     if (threadIdx.x == 0) d.hdr->done_counter = 0;
 }
@@ -686,20 +692,20 @@ __global__ void __launch_bounds__(256, 2) k_cell_count(Dev d, int Q) {
         }
         unsigned last = 0;
         if (lane == 0) {
-            __threadfence();  // the run's counts before its completion
+            fence_gpu();  // the run's counts before its completion
             last = atomicAdd(d.sdone + s, static_cast<unsigned>(nrun)) + nrun == static_cast<unsigned>(hi - lo);
         }
         if (!__shfl_sync(0xffffffffu, last, 0)) continue;
-        __threadfence();
+        fence_gpu();
         const int run = warp_excl_scan8(d.cnt + lo, d.lptr + lo, hi - lo);  // the sample's row offsets
         unsigned glast = 0;
         if (lane == 0) {
             d.stot[s] = run;
-            __threadfence();
+            fence_gpu();
             glast = atomicAdd(&d.hdr->large_done, 1u) == static_cast<unsigned>(n_large - 1);
         }
         if (!__shfl_sync(0xffffffffu, glast, 0)) continue;
-        __threadfence();
+        fence_gpu();
         finalize_csr_warp(d, Q);
         if (lane == 0) d.hdr->large_done = 0;
     }
@@ -1075,12 +1081,12 @@ __global__ void __launch_bounds__(128) k_loss(Dev d, int with_energy, int full_g
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        __threadfence();
+        fence_gpu();
         last = atomicAdd(&d.hdr->done_counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!last) return;
-    __threadfence();
+    fence_gpu();
     double e = 0.0, f = 0.0;
     for (int s = threadIdx.x; s < B; s += 128) e += d.sample_terms[2 * s], f += d.sample_terms[2 * s + 1];
     red[threadIdx.x] = e, red2[threadIdx.x] = f;
@@ -1154,12 +1160,12 @@ __global__ void __launch_bounds__(128) k_eval(Dev d) {
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        __threadfence();
+        fence_gpu();
         last = atomicAdd(&d.hdr->done_counter, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!last) return;
-    __threadfence();
+    fence_gpu();
     double e = 0.0, f = 0.0;
     for (int s = threadIdx.x; s < B; s += blockDim.x) e += d.sample_terms[2 * s], f += d.sample_terms[2 * s + 1];
 #pragma unroll
@@ -1294,15 +1300,15 @@ __device__ __forceinline__ void grid_barrier(unsigned int* count, unsigned int* 
     if (threadIdx.x == 0) {
         volatile unsigned int* vgen = gen;
         const unsigned int g = *vgen;
-        __threadfence();
+        fence_gpu();
         if (atomicAdd(count, 1u) == gridDim.x - 1) {
             *count = 0;
-            __threadfence();
+            fence_gpu();
             atomicAdd(gen, 1u);
         } else {
             while (*vgen == g) __nanosleep(64);
         }
-        __threadfence();
+        fence_gpu();
     }
     __syncthreads();
 }
