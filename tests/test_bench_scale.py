@@ -291,3 +291,50 @@ def test_cfg3_periodic_crystals_g8_b32_vs_port(pk, oracle_port):
     res = dev.train_step_workers([pk.select(batch, np.arange(g * B, (g + 1) * B)) for g in range(G)], tc, step=2)
     _check_step(res, dev.grads() / G, dev.rms_state(), ref, cases.CFG, "cfg3 periodic G=8 B=32")
     dev.close()
+
+
+def test_long_pipelined_runs_stay_bit_identical(pk):
+    """Soak: 400 headline steps (side-stream prefetch of the next slot, batch-state
+    parity swaps) against 400 unpipelined steps, and 300 public pipelined
+    submit / wait steps against 300 synchronous train_step calls: every loss and the
+    final parameters bit-identical (the loss falls from 8.7 to 0.6 on the way)."""
+    import bench
+    from paper_2505_22208_b200.dist import shard
+    pool, table, sched = bench.make_workload(pk, 1)
+    n = sched["n_batches"]
+    shards = [shard(pool, sched, s, 0, 1, bench.BATCH_PER_GPU) for s in range(n)]
+    cfg = pk.ModelConfig(**bench.CFG)
+    tc = pk.TrainConfig(seed=11)
+
+    def staged(pipelined, K=400):
+        dev = pk.Device(cfg, seed=7)
+        dev.set_reference_table(table)
+        for s, b in enumerate(shards):
+            dev.stage(b, tc, step=s, slot=s)
+        losses = [dev.train_step_staged(k % n, sync=True, next_slot=((k + 1) % n) if pipelined else None).loss
+                  for k in range(K)]
+        p = dev.params()
+        dev.close()
+        return losses, p
+
+    def public(pipelined, K=300):
+        dev = pk.Device(cfg, seed=7)
+        dev.set_reference_table(table)
+        if pipelined:
+            losses, pending = [], None
+            for k in range(K):
+                t = dev.train_step_submit(shards[k % n], tc, step=k)
+                if pending is not None:
+                    losses.append(dev.train_step_wait(pending).loss)
+                pending = t
+            losses.append(dev.train_step_wait(pending).loss)
+        else:
+            losses = [dev.train_step(shards[k % n], tc, step=k).loss for k in range(K)]
+        p = dev.params()
+        dev.close()
+        return losses, p
+
+    for run in (staged, public):
+        (la, pa), (lb, pb) = run(True), run(False)
+        assert la == lb, run.__name__
+        assert np.array_equal(pa.view(np.uint64), pb.view(np.uint64)), run.__name__
