@@ -38,14 +38,19 @@ struct Slot {
 // Key = the atom count (the reference's balancer) or a predicted cost (double).
 template <class Key>
 void balance_minibatch(const Key* key, std::int64_t count, int G, int B, std::int32_t* worker) {
-    std::vector<std::int64_t> order(static_cast<std::size_t>(count));
-    std::iota(order.begin(), order.end(), 0);
-    std::sort(order.begin(), order.end(), [&](std::int64_t a, std::int64_t b) {
-        return key[a] != key[b] ? key[a] > key[b] : a < b;
+    // scratch reused across the epoch's mini-batches (plan() calls this ~n / (G B) times)
+    thread_local std::vector<std::pair<Key, std::int64_t>> order;
+    thread_local std::vector<Key> load;
+    thread_local std::vector<int> filled;
+    order.resize(static_cast<std::size_t>(count));
+    for (std::int64_t e = 0; e < count; ++e) order[static_cast<std::size_t>(e)] = {key[e], e};
+    std::sort(order.begin(), order.end(), [](const std::pair<Key, std::int64_t>& a, const std::pair<Key, std::int64_t>& b) {
+        return a.first != b.first ? a.first > b.first : a.second < b.second;
     });
-    std::vector<Key> load(static_cast<std::size_t>(G), Key(0));
-    std::vector<int> filled(static_cast<std::size_t>(G), 0);
-    for (const std::int64_t e : order) {
+    load.assign(static_cast<std::size_t>(G), Key(0));
+    filled.assign(static_cast<std::size_t>(G), 0);
+    for (const auto& oe : order) {
+        const std::int64_t e = oe.second;
         int pick = -1;
         for (int g = 0; g < G; ++g)
             if (filled[g] < B && (pick < 0 || load[g] < load[pick])) pick = g;
@@ -163,10 +168,18 @@ void plan_impl(const Key* key, const int64_t* atoms, int64_t n, int32_t G, int32
         for (int64_t s = 0; s < S; ++s) bounds[s + 1] = bounds[s] + n / S + (s < n % S ? 1 : 0);
         std::vector<std::int64_t> sorted = ids;
         int64_t ranks_max = 0;
+        std::vector<std::pair<Key, std::int64_t>> kv;  // (key, id) pairs: the sort touches contiguous memory
         for (int64_t s = 0; s < S; ++s) {
-            std::sort(sorted.begin() + bounds[s], sorted.begin() + bounds[s + 1], [&](std::int64_t a, std::int64_t b) {
-                return key[a] != key[b] ? key[a] > key[b] : a < b;
+            kv.resize(static_cast<std::size_t>(bounds[s + 1] - bounds[s]));
+            for (int64_t k = bounds[s]; k < bounds[s + 1]; ++k) {
+                const std::int64_t id = sorted[static_cast<std::size_t>(k)];
+                kv[static_cast<std::size_t>(k - bounds[s])] = {key[id], id};
+            }
+            std::sort(kv.begin(), kv.end(), [](const std::pair<Key, std::int64_t>& a, const std::pair<Key, std::int64_t>& b) {
+                return a.first != b.first ? a.first > b.first : a.second < b.second;
             });
+            for (int64_t k = bounds[s]; k < bounds[s + 1]; ++k)
+                sorted[static_cast<std::size_t>(k)] = kv[static_cast<std::size_t>(k - bounds[s])].second;
             const int64_t len = bounds[s + 1] - bounds[s];
             lost += len % G;
             ranks_max = std::max<int64_t>(ranks_max, len / G);
@@ -274,23 +287,34 @@ LAMM_API int lamm_schedule_metrics(int64_t nb, int32_t G, int32_t B, const int32
         } else {
             worst = acc = 1.0;
         }
-        // Chunk totals keyed by (split, chunk_rank), walked in key order.
-        struct Key {
-            int64_t split, rank, atoms;
+        // Chunk totals keyed by (split, chunk_rank), walked in key order: the entries
+        // ordered by (split, rank) with a two-pass LSD counting sort (stable by rank,
+        // then by split), O(n) instead of a comparison sort of the whole epoch.
+        const int64_t m = nb * per;
+        int64_t max_split = 0, max_rank = 0;
+        for (int64_t e = 0; e < m; ++e) {
+            require(split[e] >= 0 && chunk_rank[e] >= 0, "schedule_metrics: negative split / chunk rank");
+            max_split = std::max(max_split, split[e]);
+            max_rank = std::max(max_rank, chunk_rank[e]);
+        }
+        auto counting = [&](const std::vector<int64_t>& in, const int64_t* key, int64_t kmax) {
+            std::vector<int64_t> start(static_cast<std::size_t>(kmax) + 2, 0), out(in.size());
+            for (const int64_t e : in) ++start[static_cast<std::size_t>(key[e]) + 1];
+            for (int64_t k = 0; k <= kmax; ++k) start[k + 1] += start[k];
+            for (const int64_t e : in) out[static_cast<std::size_t>(start[static_cast<std::size_t>(key[e])]++)] = e;
+            return out;
         };
-        std::vector<Key> keys(static_cast<std::size_t>(nb * per));
-        for (int64_t e = 0; e < nb * per; ++e) keys[e] = {split[e], chunk_rank[e], atoms[e]};
-        std::sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
-            return a.split != b.split ? a.split < b.split : a.rank < b.rank;
-        });
+        std::vector<int64_t> order(static_cast<std::size_t>(m));
+        std::iota(order.begin(), order.end(), 0);
+        order = counting(counting(order, chunk_rank, max_rank), split, max_split);
         int64_t violations = 0, prev_split = -1, prev_total = 0;
-        for (std::size_t e = 0; e < keys.size();) {
+        for (std::size_t e = 0; e < order.size();) {
+            const int64_t s0 = split[order[e]], r0 = chunk_rank[order[e]];
             std::size_t f = e;
             int64_t total = 0;
-            while (f < keys.size() && keys[f].split == keys[e].split && keys[f].rank == keys[e].rank)
-                total += keys[f++].atoms;
-            if (keys[e].split == prev_split && total > prev_total) ++violations;
-            prev_split = keys[e].split;
+            while (f < order.size() && split[order[f]] == s0 && chunk_rank[order[f]] == r0) total += atoms[order[f++]];
+            if (s0 == prev_split && total > prev_total) ++violations;
+            prev_split = s0;
             prev_total = total;
             e = f;
         }
