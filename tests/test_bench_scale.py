@@ -338,3 +338,27 @@ def test_long_pipelined_runs_stay_bit_identical(pk):
         (la, pa), (lb, pb) = run(True), run(False)
         assert la == lb, run.__name__
         assert np.array_equal(pa.view(np.uint64), pb.view(np.uint64)), run.__name__
+
+
+def test_cfg2_evaluation_at_bench_scale(pk, oracle_ref):
+    """The validation path (lamm_evaluate, S/trainer.cpp:528-553) on the heaviest
+    cfg2 mini-batch of the bench's epoch (256 molecules, ~14 k atoms, ~300 k edges:
+    several TMA chunks per group): physical-unit energy and force MAEs vs the reference."""
+    import bench
+    from paper_2505_22208_b200.dist import shard
+    pool, table, sched = bench.make_workload(pk, 1)
+    shards = [shard(pool, sched, s, 0, 1, bench.BATCH_PER_GPU) for s in range(sched["n_batches"])]
+    b = max(shards, key=lambda x: int(x["atom_ptr"][-1]))
+    b = dict(b)
+    b["denoise"] = np.zeros_like(b["denoise"])
+    cfg = (bench.CFG["hidden"], bench.CFG["layers"], bench.CFG["rbf"], bench.CFG["cutoff"], bench.CFG["heads"])
+    params = oracle_ref.init_params(cfg, 17)
+    dev = pk.Device(pk.ModelConfig(**bench.CFG), seed=0)
+    dev.set_params(params)
+    dev.set_reference_table(table)
+    got = dev.evaluate(b)
+    dev.close()
+    want = oracle_ref.evaluate(cfg, params, b, table)
+    assert got["energy_count"] == want["energy_count"] and got["force_count"] == want["force_count"]
+    for k in ("energy_mae", "force_mae"):
+        assert abs(got[k] - want[k]) <= TOL * abs(want[k]), (k, got[k], want[k])
