@@ -362,3 +362,18 @@ def test_cfg2_evaluation_at_bench_scale(pk, oracle_ref):
     assert got["energy_count"] == want["energy_count"] and got["force_count"] == want["force_count"]
     for k in ("energy_mae", "force_mae"):
         assert abs(got[k] - want[k]) <= TOL * abs(want[k]), (k, got[k], want[k])
+
+
+def test_cfg2_neighbor_lists_bit_exact_at_bench_scale(pk, oracle_ref):
+    """Every mini-batch of the bench's cfg2 epoch (256 molecules each, 3-14 k atoms):
+    pair set, order, fp64 distances and unit vectors bit-identical to the reference's
+    build_neighbor_list (S/core.cpp:30-48), sample by sample."""
+    import bench
+    from paper_2505_22208_b200.dist import shard
+    from test_gpu_parity import check_nlist
+    pool, table, sched = bench.make_workload(pk, 1)
+    dev = pk.Device(pk.ModelConfig(**bench.CFG), seed=0)
+    dev.set_option("export_fp64", 1)
+    for s in range(sched["n_batches"]):
+        check_nlist(dev, oracle_ref, shard(pool, sched, s, 0, 1, bench.BATCH_PER_GPU))
+    dev.close()
